@@ -1,0 +1,252 @@
+/*
+ * vrod C-ABI — the drop-in boundary for the VIPER rod-solver substep hot path.
+ *
+ * The reference (`/root/reference/proj`) has no FFI: its boundary is the C++ header API in
+ * `proj/core/include/vrod/` headers. This header restates exactly that API as
+ * plain C (pointers + sizes, no C++/torch types) so one binding drives three libraries:
+ *
+ *   paper_1906_05260_b200/lib/libvrod_b200.so   the product: host C++ + sm_100a CUDA
+ *   oracle/lib/libvrod_oracle.so                CPU restatement (test infrastructure)
+ *   oracle/_ref/libvrod_ref.so                  the reference's own sources + adapter (tests)
+ *
+ * Every entry point names the reference interface it replaces. Conventions:
+ *   - return value: VROD_OK or an error code mirroring the reference exception type
+ *     (std::invalid_argument via require, types.h:67-69; std::out_of_range via
+ *     require_index, types.h:71-77; vrod::SimulationError, types.h:25-28); the message
+ *     (identical to the reference's what()) is available from vrod_last_error().
+ *   - vectors are packed doubles: Vec3 = 3 doubles (x,y,z); Quat = 4 doubles (w,x,y,z).
+ *   - "global slot" order is DofLayout's (layout.h:17-41): rods in order, vertices /
+ *     elements in order within a rod.
+ *   - a solver handle is single-caller; handles are independent.
+ */
+#ifndef VROD_CAPI_H
+#define VROD_CAPI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VROD_CAPI_VERSION 1
+
+enum vrod_status {
+  VROD_OK = 0,
+  VROD_INVALID_ARGUMENT = 1, /* std::invalid_argument (require, types.h:67-69) */
+  VROD_OUT_OF_RANGE = 2,     /* std::out_of_range (require_index, types.h:71-77) */
+  VROD_SIMULATION_ERROR = 3, /* vrod::SimulationError (types.h:25-28) */
+  VROD_RUNTIME_ERROR = 4,    /* any other std::exception */
+  VROD_DEVICE_ERROR = 5      /* CUDA failure (product only) */
+};
+
+/* Message of the last failing call on this thread (what() of the reference exception). */
+const char* vrod_last_error(void);
+/* "b200-cuda", "oracle-cpu" or "reference-cpu". */
+const char* vrod_backend_name(void);
+int32_t vrod_capi_version(void);
+
+/* ---- plain data (reference structs) -------------------------------------------------- */
+
+/* MaterialParams, rod.h:13-24 (defaults :14-21). */
+typedef struct vrod_material {
+  double stretch_x, stretch_y, stretch_z;
+  double bend_x, bend_y, bend_z;
+  double volume, density;
+} vrod_material;
+
+/* SolverSettings, scene.h:25-39 (scale_mode: 0 kSimulated, 1 kPostStepLengthRatio). */
+typedef struct vrod_settings {
+  double dt;
+  int32_t iterations;
+  int32_t substeps;
+  double beta;
+  double gravity[3];
+  int32_t dichotomous_iterations;
+  int32_t shape_match_period;
+  double contact_stiffness;
+  double velocity_damping;
+  int32_t deterministic;
+  int32_t scale_mode;
+} vrod_settings;
+
+/* Pill, collision.h:16-25. rod == -1 for kinematic pills. */
+typedef struct vrod_pill {
+  double c0[3];
+  double c1[3];
+  double r0, r1;
+  int32_t rod, element, group, self_collide;
+} vrod_pill;
+
+/* StepReport, solver.h:23-33 (+ PhaseTimings :14-21). residuals are indexed by
+ * ConstraintKind (constraints.h:14-26) for the 8 elastic kinds. */
+typedef struct vrod_step_report {
+  int32_t step;
+  int32_t contact_count;
+  int32_t broad_pairs;
+  int32_t skipped_singular;
+  int32_t dof_count;
+  int32_t pad_;
+  double time;
+  double residuals[8];
+  double max_penetration;
+  double predict_ms, broad_ms, narrow_ms, solve_ms, finalize_ms, total_ms;
+} vrod_step_report;
+
+/* One rod: RodRestPose (rod.h:30-46) + RodState (:50-60) + Rod (:64-74). n = vertex_count,
+ * m = n - 1. All rest/state arrays are required; pinned may be NULL (nothing pinned). */
+typedef struct vrod_rod_desc {
+  int32_t vertex_count;
+  int32_t material;
+  int32_t collision_group;
+  int32_t self_collide;
+  const double* rest_centers;     /* 3n */
+  const double* rest_scales;      /* n */
+  const double* radii;            /* n */
+  const double* lengths;          /* m  (strain targets) */
+  const double* initial_lengths;  /* m  (as-built) */
+  const double* rest_frames;      /* 4m */
+  const double* darboux;          /* 3(m-1) */
+  const double* tangent_dots;     /* m */
+  const double* scale_grads;      /* m */
+  const double* scale_laplacians; /* m-1 */
+  const double* centers;          /* 3n */
+  const double* scales;           /* n */
+  const double* frames;           /* 4m */
+  const double* center_vel;       /* 3n */
+  const double* scale_vel;        /* n */
+  const double* angular_vel;      /* 3m, body frame */
+  const uint8_t* pinned;          /* n, 0/1, or NULL */
+  int32_t bone_count;             /* optional two-bone rig (rod.h:71-73) */
+  int32_t pad_;
+  const int32_t* bones;           /* bone_count */
+  const double* bone_weights;     /* n * bone_count, row per vertex */
+} vrod_rod_desc;
+
+/* Output of make_rest_pose (caller-allocated, sizes as in vrod_rod_desc). */
+typedef struct vrod_rest_pose_out {
+  double* rest_scales;      /* n */
+  double* radii;            /* n */
+  double* lengths;          /* m */
+  double* initial_lengths;  /* m */
+  double* rest_frames;      /* 4m */
+  double* darboux;          /* 3(m-1) */
+  double* tangent_dots;     /* m */
+  double* scale_grads;      /* m */
+  double* scale_laplacians; /* m-1 */
+} vrod_rest_pose_out;
+
+void vrod_default_material(vrod_material* out); /* rod.h:14-21 */
+void vrod_default_settings(vrod_settings* out); /* scene.h:26-37 */
+
+/* make_rest_pose(centers, radii, scales), rod.h:88-90 / rod.cpp:60-112. radii_count is 1 or
+ * n; scales_count is 0 (unit), 1 or n. */
+int vrod_make_rest_pose(int32_t n, const double* centers, int32_t radii_count, const double* radii,
+                        int32_t scales_count, const double* scales, vrod_rest_pose_out* out);
+
+/* ---- scene builder (Scene, scene.h:109-126) ------------------------------------------- */
+
+typedef struct vrod_scene vrod_scene;
+int vrod_scene_create(vrod_scene** out);
+void vrod_scene_destroy(vrod_scene* scene);
+int vrod_scene_set_settings(vrod_scene* scene, const vrod_settings* settings);
+int vrod_scene_add_material(vrod_scene* scene, const vrod_material* material);
+int vrod_scene_add_rod(vrod_scene* scene, const vrod_rod_desc* rod);
+int vrod_scene_add_plane(vrod_scene* scene, const double normal[3], double offset);     /* HalfPlane */
+/* Bone (scene.h:49-53): key_count keyframes (t, position xyz, rotation wxyz). */
+int vrod_scene_add_bone(vrod_scene* scene, int32_t key_count, const double* times,
+                        const double* positions, const double* rotations);
+int vrod_scene_add_kinematic_pill(vrod_scene* scene, const vrod_pill* pill, int32_t bone); /* KinematicPill */
+int vrod_scene_add_bundle(vrod_scene* scene, int32_t member_count, const int32_t* rods,
+                          const int32_t* vertices);                                     /* BundleMember list */
+int vrod_scene_add_pin_motion(vrod_scene* scene, int32_t rod, int32_t vertex, const double start[3],
+                              const double target[3], double t0, double t1);            /* PinMotion */
+int vrod_scene_add_soft_pin(vrod_scene* scene, int32_t rod, int32_t vertex, const double target[3],
+                            double stiffness);                                          /* SoftPin */
+int vrod_scene_add_activation(vrod_scene* scene, int32_t rod, double factor, double t_start,
+                              double t_end, int32_t first_element, int32_t last_element); /* Activation */
+/* Scene::validate, scene.cpp:63-157 — same checks, same messages. */
+int vrod_scene_validate(const vrod_scene* scene);
+
+/* ---- solver (class Solver, solver.h:54-115) ------------------------------------------- */
+
+typedef struct vrod_solver vrod_solver;
+
+typedef struct vrod_solver_info {
+  int32_t rod_count;
+  int32_t total_vertices;
+  int32_t total_elements;
+  int32_t dof_count;     /* Solver::dof_count, 4V + 3E */
+  int32_t step_index;    /* Solver::step_index */
+  int32_t bundle_count;
+  int32_t elastic_blocks;
+  int32_t pad_;
+  double time;           /* Solver::time */
+} vrod_solver_info;
+
+/* Solver::Solver(Scene), solver.cpp:102-136. The scene is copied; it may be destroyed after. */
+int vrod_solver_create(const vrod_scene* scene, vrod_solver** out);
+void vrod_solver_destroy(vrod_solver* solver);
+/* Solver::step(), solver.cpp:363-388. */
+int vrod_solver_step(vrod_solver* solver, vrod_step_report* report);
+/* Solver::probe_convergence(iterations), solver.cpp:390-398: writes iterations x 8 residuals. */
+int vrod_solver_probe_convergence(vrod_solver* solver, int32_t iterations, double* residual_log);
+int vrod_solver_get_info(const vrod_solver* solver, vrod_solver_info* info);
+/* Per-rod vertex counts (rod_count entries). */
+int vrod_solver_get_rod_sizes(const vrod_solver* solver, int32_t* vertex_counts);
+
+/* Solver::scene() state access, global slot order; any pointer may be NULL. get = read the
+ * live state; set = the mutable scene() write-back between steps (SURVEY.md §7 hard part 5). */
+int vrod_solver_get_state(vrod_solver* solver, double* centers, double* scales, double* frames,
+                          double* center_vel, double* scale_vel, double* angular_vel);
+int vrod_solver_set_state(vrod_solver* solver, const double* centers, const double* scales,
+                          const double* frames, const double* center_vel, const double* scale_vel,
+                          const double* angular_vel);
+/* Live rest quantities (activation rewrites lengths & derived data, rod.cpp:164-176). */
+int vrod_solver_get_rest(vrod_solver* solver, double* lengths, double* darboux_per_element,
+                         double* scale_grads, double* scale_laplacians_per_element);
+/* ExternalLoads (solver.h:35-41) via Solver::loads(). Arrays are global-slot sized; the
+ * per-rod flag arrays say which rods carry that load (an empty vector in the reference).
+ * Passing NULL for an array clears that load. */
+int vrod_solver_set_loads(vrod_solver* solver, const double* force_density, const uint8_t* fd_rods,
+                          const double* torque, const uint8_t* torque_rods, const double* scale_load,
+                          const uint8_t* scale_load_rods);
+/* Solver::kinetic_energy / total_volume / total_rest_volume, solver.cpp:400-430. */
+int vrod_solver_energy(vrod_solver* solver, double* kinetic, double* volume, double* rest_volume);
+/* DofLayout weights (layout.h:25-34): per vertex center/scale inverse weights, per element
+ * theta inverse weights (3 each). Any may be NULL. */
+int vrod_solver_get_inverse_weights(vrod_solver* solver, double* inv_center, double* inv_scale,
+                                    double* inv_theta);
+/* Contacts of the last substep (contact blocks, solver.cpp:210-224): pill ids in the pill
+ * array of that substep, frozen alpha/beta. */
+int vrod_solver_get_contacts(vrod_solver* solver, int64_t capacity, int64_t* count,
+                             int32_t* pill_a, int32_t* pill_b, double* alpha, double* beta);
+/* Solver::current_pills(), solver.cpp:432-436 (rod pills then kinematic pills). */
+int vrod_solver_current_pills(vrod_solver* solver, int64_t capacity, int64_t* count, vrod_pill* pills);
+
+/* ---- fine-grained (kernel-level) boundary, on host arrays ------------------------------ */
+
+/* pill_project(x, pill), collision.h:64 / collision.cpp:15-49 — n independent queries. */
+int vrod_pill_project(int64_t n, const double* points, const vrod_pill* pills, double* t,
+                      double* distance, uint8_t* degenerate);
+/* deepest_penetration(a, b, iterations, warm_alpha), collision.h:74-75 / :78-135. warm may be
+ * NULL (= -1 for all). */
+int vrod_deepest_penetration(int64_t n, const vrod_pill* a, const vrod_pill* b, int32_t iterations,
+                             const double* warm_alpha, double* alpha, double* beta, double* distance);
+/* broad_phase(pills), collision.h:87 / collision.cpp:184-238. Pairs (i<j) ascending; writes at
+ * most `capacity` pairs but always reports the full count. */
+int vrod_broad_phase(int64_t n, const vrod_pill* pills, int64_t capacity, int64_t* pair_count,
+                     int32_t* pairs);
+/* find_contacts(pills, pairs, iterations, warm), collision.h:92-95 / collision.cpp:251-273.
+ * warm_keys/warm_alpha may be NULL (no warm list). */
+int vrod_find_contacts(int64_t n, const vrod_pill* pills, int64_t pair_count, const int32_t* pairs,
+                       int32_t iterations, int64_t warm_count, const uint64_t* warm_keys,
+                       const double* warm_alpha, int64_t capacity, int64_t* count, int32_t* pill_a,
+                       int32_t* pill_b, double* alpha, double* beta, double* distance);
+/* pair_key(a, b), collision.h:90 / collision.cpp:240-249. */
+uint64_t vrod_pair_key(const vrod_pill* a, const vrod_pill* b);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VROD_CAPI_H */

@@ -1,0 +1,280 @@
+"""Solver handle over any library exporting include/vrod_capi.h.
+
+`SolverHandle` is the Python face of `vrod::Solver` (solver.h:54-115): construct from a Scene,
+`step()`, state access in DofLayout global-slot order, loads, energy queries, contacts, pills,
+probe_convergence. The product's `paper_1906_05260_b200.Solver` is this class bound to the
+CUDA library; tests bind the same class to the CPU oracle libraries to compare.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import capi
+from .scene import Scene, check, marshal_scene
+
+KIND_NAMES = ("stretch_z", "cross_section", "surface_stretch", "bend_twist", "surface_bending",
+              "volume_stretch", "volume_bend_u", "volume_bend_v")
+
+
+@dataclass
+class StepReport:
+    """StepReport, solver.h:23-33 (+ PhaseTimings :14-21)."""
+    step: int
+    time: float
+    residuals: np.ndarray
+    max_penetration: float
+    contact_count: int
+    broad_pairs: int
+    skipped_singular: int
+    dof_count: int
+    timings: dict
+
+    @staticmethod
+    def from_c(r: capi.StepReport) -> "StepReport":
+        return StepReport(step=r.step, time=r.time, residuals=np.array(r.residuals[:], dtype=np.float64),
+                          max_penetration=r.max_penetration, contact_count=r.contact_count,
+                          broad_pairs=r.broad_pairs, skipped_singular=r.skipped_singular, dof_count=r.dof_count,
+                          timings=dict(predict_ms=r.predict_ms, broad_ms=r.broad_ms, narrow_ms=r.narrow_ms,
+                                       solve_ms=r.solve_ms, finalize_ms=r.finalize_ms, total_ms=r.total_ms))
+
+
+class SolverHandle:
+    def __init__(self, lib, scene: Scene):
+        self._lib = lib
+        self._h = C.c_void_p()
+        sh = marshal_scene(lib, scene)
+        try:
+            check(lib, lib.vrod_solver_create(sh, C.byref(self._h)))
+        finally:
+            lib.vrod_scene_destroy(sh)
+        info = self.info()
+        self.rod_count = info.rod_count
+        self.total_vertices = info.total_vertices
+        self.total_elements = info.total_elements
+        sizes = np.zeros(max(self.rod_count, 1), dtype=np.int32)
+        check(lib, lib.vrod_solver_get_rod_sizes(self._h, capi.ptr(sizes, C.c_int32)))
+        self.rod_sizes = sizes[: self.rod_count].astype(np.int64)
+        self.vertex_base = np.concatenate([[0], np.cumsum(self.rod_sizes)])[:-1] if self.rod_count else np.zeros(0)
+        self.element_base = self.vertex_base - np.arange(self.rod_count)
+
+    # -- lifetime -------------------------------------------------------------------------------
+    def close(self) -> None:
+        if self._h:
+            self._lib.vrod_solver_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def backend(self) -> str:
+        return self._lib.vrod_backend_name().decode()
+
+    # -- stepping -------------------------------------------------------------------------------
+    def step(self) -> StepReport:
+        """Solver::step(), solver.cpp:363-388."""
+        r = capi.StepReport()
+        check(self._lib, self._lib.vrod_solver_step(self._h, C.byref(r)))
+        return StepReport.from_c(r)
+
+    def probe_convergence(self, iterations: int) -> np.ndarray:
+        """Solver::probe_convergence, solver.cpp:390-398 -> (iterations, 8) residual log."""
+        out = np.zeros((max(iterations, 1), 8))
+        check(self._lib, self._lib.vrod_solver_probe_convergence(self._h, iterations, capi.ptr(out)))
+        return out[:iterations]
+
+    # -- queries --------------------------------------------------------------------------------
+    def info(self) -> capi.SolverInfo:
+        i = capi.SolverInfo()
+        check(self._lib, self._lib.vrod_solver_get_info(self._h, C.byref(i)))
+        return i
+
+    def time(self) -> float:
+        return self.info().time
+
+    def step_index(self) -> int:
+        return self.info().step_index
+
+    def dof_count(self) -> int:
+        return self.info().dof_count
+
+    def state(self) -> dict:
+        """Live state, global slot order: centers (V,3), scales (V,), frames (E,4) wxyz, velocities."""
+        V, E = self.total_vertices, self.total_elements
+        out = dict(centers=np.zeros((V, 3)), scales=np.zeros(V), frames=np.zeros((E, 4)),
+                   center_vel=np.zeros((V, 3)), scale_vel=np.zeros(V), angular_vel=np.zeros((E, 3)))
+        check(self._lib, self._lib.vrod_solver_get_state(
+            self._h, capi.ptr(out["centers"]), capi.ptr(out["scales"]), capi.ptr(out["frames"]),
+            capi.ptr(out["center_vel"]), capi.ptr(out["scale_vel"]), capi.ptr(out["angular_vel"])))
+        return out
+
+    def set_state(self, centers=None, scales=None, frames=None, center_vel=None, scale_vel=None,
+                  angular_vel=None) -> None:
+        """Write back into the live scene between steps (Solver::scene() mutation)."""
+        def p(a, shape):
+            if a is None:
+                return None
+            x = np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(shape))
+            keep.append(x)
+            return capi.ptr(x)
+
+        keep: list = []
+        V, E = self.total_vertices, self.total_elements
+        check(self._lib, self._lib.vrod_solver_set_state(
+            self._h, p(centers, (V, 3)), p(scales, (V,)), p(frames, (E, 4)), p(center_vel, (V, 3)),
+            p(scale_vel, (V,)), p(angular_vel, (E, 3))))
+
+    def rod_state(self, r: int) -> dict:
+        st = self.state()
+        v0, n = int(self.vertex_base[r]), int(self.rod_sizes[r])
+        e0 = int(self.element_base[r])
+        return dict(centers=st["centers"][v0:v0 + n], scales=st["scales"][v0:v0 + n],
+                    frames=st["frames"][e0:e0 + n - 1], center_vel=st["center_vel"][v0:v0 + n],
+                    scale_vel=st["scale_vel"][v0:v0 + n], angular_vel=st["angular_vel"][e0:e0 + n - 1])
+
+    def rest(self) -> dict:
+        """Live rest data per element slot (activation rewrites it): lengths, darboux, grads, laplacians."""
+        E = self.total_elements
+        out = dict(lengths=np.zeros(E), darboux=np.zeros((E, 3)), scale_grads=np.zeros(E),
+                   scale_laplacians=np.zeros(E))
+        check(self._lib, self._lib.vrod_solver_get_rest(self._h, capi.ptr(out["lengths"]), capi.ptr(out["darboux"]),
+                                                        capi.ptr(out["scale_grads"]),
+                                                        capi.ptr(out["scale_laplacians"])))
+        return out
+
+    def set_loads(self, force_density=None, torque=None, scale_load=None, force_rods=None, torque_rods=None,
+                  scale_load_rods=None) -> None:
+        """Solver::loads() (ExternalLoads, solver.h:35-41) as global arrays + optional per-rod masks."""
+        keep: list = []
+
+        def p(a, shape, ct=C.c_double, dt=np.float64):
+            if a is None:
+                return None
+            x = np.ascontiguousarray(np.asarray(a, dtype=dt).reshape(shape))
+            keep.append(x)
+            return capi.ptr(x, ct)
+
+        V, E, R = self.total_vertices, self.total_elements, self.rod_count
+        check(self._lib, self._lib.vrod_solver_set_loads(
+            self._h, p(force_density, (V, 3)), p(force_rods, (R,), C.c_uint8, np.uint8), p(torque, (E, 3)),
+            p(torque_rods, (R,), C.c_uint8, np.uint8), p(scale_load, (E,)),
+            p(scale_load_rods, (R,), C.c_uint8, np.uint8)))
+
+    def kinetic_energy(self) -> float:
+        x = C.c_double()
+        check(self._lib, self._lib.vrod_solver_energy(self._h, C.byref(x), None, None))
+        return x.value
+
+    def total_volume(self) -> float:
+        x = C.c_double()
+        check(self._lib, self._lib.vrod_solver_energy(self._h, None, C.byref(x), None))
+        return x.value
+
+    def total_rest_volume(self) -> float:
+        x = C.c_double()
+        check(self._lib, self._lib.vrod_solver_energy(self._h, None, None, C.byref(x)))
+        return x.value
+
+    def inverse_weights(self) -> dict:
+        V, E = self.total_vertices, self.total_elements
+        out = dict(inv_center=np.zeros(V), inv_scale=np.zeros(V), inv_theta=np.zeros((E, 3)))
+        check(self._lib, self._lib.vrod_solver_get_inverse_weights(
+            self._h, capi.ptr(out["inv_center"]), capi.ptr(out["inv_scale"]), capi.ptr(out["inv_theta"])))
+        return out
+
+    def contacts(self) -> dict:
+        n = C.c_int64()
+        check(self._lib, self._lib.vrod_solver_get_contacts(self._h, 0, C.byref(n), None, None, None, None))
+        k = n.value
+        out = dict(pill_a=np.zeros(k, dtype=np.int32), pill_b=np.zeros(k, dtype=np.int32), alpha=np.zeros(k),
+                   beta=np.zeros(k))
+        if k:
+            check(self._lib, self._lib.vrod_solver_get_contacts(
+                self._h, k, C.byref(n), capi.ptr(out["pill_a"], C.c_int32), capi.ptr(out["pill_b"], C.c_int32),
+                capi.ptr(out["alpha"]), capi.ptr(out["beta"])))
+        return out
+
+    def current_pills(self) -> np.ndarray:
+        n = C.c_int64()
+        check(self._lib, self._lib.vrod_solver_current_pills(self._h, 0, C.byref(n), None))
+        out = np.zeros(n.value, dtype=capi.PILL_DTYPE)
+        if n.value:
+            check(self._lib, self._lib.vrod_solver_current_pills(self._h, n.value, C.byref(n),
+                                                                 out.ctypes.data_as(C.c_void_p)))
+        return out
+
+
+# ---- fine-grained collision entry points (collision.h:64-95) -----------------------------------
+
+def _pills(p: np.ndarray) -> np.ndarray:
+    p = np.ascontiguousarray(p)
+    assert p.dtype == capi.PILL_DTYPE
+    return p
+
+
+def pill_project(lib, points: np.ndarray, pills: np.ndarray):
+    x = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    p = _pills(pills)
+    n = x.shape[0]
+    t, d, g = np.zeros(n), np.zeros(n), np.zeros(n, dtype=np.uint8)
+    check(lib, lib.vrod_pill_project(n, capi.ptr(x), p.ctypes.data_as(C.c_void_p), capi.ptr(t), capi.ptr(d),
+                                     capi.ptr(g, C.c_uint8)))
+    return t, d, g
+
+
+def deepest_penetration(lib, a: np.ndarray, b: np.ndarray, iterations: int = 10, warm_alpha=None):
+    a, b = _pills(a), _pills(b)
+    n = a.shape[0]
+    w = None if warm_alpha is None else np.ascontiguousarray(warm_alpha, dtype=np.float64)
+    al, be, d = np.zeros(n), np.zeros(n), np.zeros(n)
+    check(lib, lib.vrod_deepest_penetration(n, a.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
+                                            iterations, capi.ptr(w), capi.ptr(al), capi.ptr(be), capi.ptr(d)))
+    return al, be, d
+
+
+def broad_phase(lib, pills: np.ndarray) -> np.ndarray:
+    p = _pills(pills)
+    cnt = C.c_int64()
+    check(lib, lib.vrod_broad_phase(p.shape[0], p.ctypes.data_as(C.c_void_p), 0, C.byref(cnt), None))
+    out = np.zeros((cnt.value, 2), dtype=np.int32)
+    if cnt.value:
+        check(lib, lib.vrod_broad_phase(p.shape[0], p.ctypes.data_as(C.c_void_p), cnt.value, C.byref(cnt),
+                                        capi.ptr(out, C.c_int32)))
+    return out
+
+
+def find_contacts(lib, pills: np.ndarray, pairs: np.ndarray, iterations: int = 10, warm_keys=None,
+                  warm_alpha=None) -> dict:
+    p = _pills(pills)
+    pr = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+    wk = None if warm_keys is None else np.ascontiguousarray(warm_keys, dtype=np.uint64)
+    wa = None if warm_alpha is None else np.ascontiguousarray(warm_alpha, dtype=np.float64)
+    nw = 0 if wk is None else wk.size
+    cap = pr.shape[0]
+    out = dict(pill_a=np.zeros(cap, dtype=np.int32), pill_b=np.zeros(cap, dtype=np.int32), alpha=np.zeros(cap),
+               beta=np.zeros(cap), distance=np.zeros(cap))
+    cnt = C.c_int64()
+    check(lib, lib.vrod_find_contacts(p.shape[0], p.ctypes.data_as(C.c_void_p), pr.shape[0],
+                                      capi.ptr(pr, C.c_int32), iterations, nw, capi.ptr(wk, C.c_uint64),
+                                      capi.ptr(wa), cap, C.byref(cnt), capi.ptr(out["pill_a"], C.c_int32),
+                                      capi.ptr(out["pill_b"], C.c_int32), capi.ptr(out["alpha"]),
+                                      capi.ptr(out["beta"]), capi.ptr(out["distance"])))
+    return {k: v[: cnt.value] for k, v in out.items()}
+
+
+def pair_key(lib, a: np.ndarray, b: np.ndarray) -> int:
+    pa = capi.Pill.from_buffer_copy(np.ascontiguousarray(a).tobytes())
+    pb = capi.Pill.from_buffer_copy(np.ascontiguousarray(b).tobytes())
+    return int(lib.vrod_pair_key(C.byref(pa), C.byref(pb)))

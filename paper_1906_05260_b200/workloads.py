@@ -1,0 +1,176 @@
+"""Synthetic workloads C1-C5 of BASELINE.json (concrete definitions: SURVEY.md §8(d)).
+
+All generators are deterministic (numpy Generator seeded per config). They build plain
+`Scene`s; the rest pose comes from `make_rest_pose` of the library handed in (the product or,
+in tests, an oracle) — the same arrays then feed every backend.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .scene import (Activation, MaterialParams, PinMotion, Rod, RodRestPose, Scene, SolverSettings,
+                    make_rest_pose, make_rest_state)
+
+
+def _translated(rest: RodRestPose, offset) -> RodRestPose:
+    """Rest pose of a translated copy. Every derived quantity of make_rest_pose depends on center
+    differences only; for the axis-aligned templates used here those are bitwise unchanged."""
+    r = rest.copy()
+    r.centers = r.centers + np.asarray(offset, dtype=np.float64)
+    return r
+
+
+def _vertical_template(lib, n: int, element: float, radius: float) -> RodRestPose:
+    centers = np.zeros((n, 3))
+    centers[:, 2] = element * np.arange(n)
+    return make_rest_pose(lib, centers, [radius])
+
+
+def c1_single_rod(lib) -> Scene:
+    """C1: one 100-vertex rod along +x, pinned at vertex 0, gravity, I=10."""
+    n = 100
+    centers = np.zeros((n, 3))
+    centers[:, 0] = np.arange(n) / (n - 1)  # length 1.0
+    rest = make_rest_pose(lib, centers, [0.02])
+    rod = Rod(rest=rest, state=make_rest_state(rest))
+    rod.pinned[0] = 1
+    s = Scene(rods=[rod], materials=[MaterialParams()])
+    s.settings = SolverSettings(iterations=10)
+    return s
+
+
+def _volume_dominant() -> MaterialParams:  # scenarios.cpp:32-39
+    return MaterialParams(stretch_x=1e4, stretch_y=1e4, stretch_z=1e4, bend_x=1e3, bend_y=1e3, volume=1e8,
+                          density=1000.0)
+
+
+def c2_stretch_grid(lib, rods_per_side: int = 8, vertices: int = 256) -> Scene:
+    """C2: 64 rods x 256 vertices along +z on an 8x8 grid (1 m pitch), both ends pinned and pulled
+    apart to 2x over 1 s (scenario_stretch pattern, scenarios.cpp:71-88), collision group 0 for
+    all (no pairs), volume-dominant material, g = 0, damping 0.1, dt = 1/240, I = 20."""
+    element = 0.01
+    L = element * (vertices - 1)
+    tmpl = _vertical_template(lib, vertices, element, 0.01)
+    s = Scene(materials=[_volume_dominant()])
+    for i in range(rods_per_side):
+        for j in range(rods_per_side):
+            rest = _translated(tmpl, (float(i), float(j), 0.0))
+            rod = Rod(rest=rest, state=make_rest_state(rest), collision_group=0)
+            rod.pinned[0] = 1
+            rod.pinned[-1] = 1
+            r = len(s.rods)
+            s.rods.append(rod)
+            s.pin_motions.append(PinMotion(r, 0, tuple(rest.centers[0]), (float(i), float(j), -0.5 * L), 0.0, 1.0))
+            s.pin_motions.append(PinMotion(r, vertices - 1, tuple(rest.centers[-1]), (float(i), float(j), 1.5 * L),
+                                           0.0, 1.0))
+    s.settings = SolverSettings(dt=1.0 / 240.0, iterations=20, substeps=1, gravity=(0.0, 0.0, 0.0),
+                                velocity_damping=0.1)
+    return s
+
+
+def _hex_points(count: int, pitch: float) -> np.ndarray:
+    """The `count` triangular-lattice points nearest the origin, ties broken by angle."""
+    pts = []
+    k = int(math.ceil(math.sqrt(count))) + 3
+    for a in range(-k, k + 1):
+        for b in range(-k, k + 1):
+            x = pitch * (a + 0.5 * b)
+            y = pitch * (b * math.sqrt(3.0) / 2.0)
+            pts.append((round(x * x + y * y, 12), math.atan2(y, x) % (2 * math.pi), x, y))
+    pts.sort()
+    return np.array([(p[2], p[3]) for p in pts[:count]])
+
+
+def c3_muscle_bundle(lib, muscles: int = 4, rods_per_muscle: int = 32, vertices: int = 30,
+                     activate=(0, 2)) -> Scene:
+    """C3: paper-scale ~26k-DOF synthetic muscle bundle: 4 muscles x 32 rods x 30
+    vertices (element 0.01 m, r = 0.004 m); muscle axes at (+-d, +-d) with d set so the closest
+    rods of adjacent muscles overlap by 0.02*2r (contact at t = 0); collision_group = muscle id;
+    both rod ends pinned; per-muscle per-vertex shape-matching groups (scenarios.cpp:219-221);
+    band material (scenarios.cpp:198-202); gravity; damping 0.02; activation 0.2 over [0, 0.5] s
+    on muscles 0 and 2; default settings (dt 1/60, substeps 1, I = 20)."""
+    r = 0.004
+    element = 0.01
+    pitch = 0.0085
+    lattice = _hex_points(rods_per_muscle, pitch)
+    target = 2 * r - 0.02 * 2 * r  # center distance of the closest inter-muscle pair
+
+    def min_sep(d):
+        a = lattice + np.array([d, 0.0])
+        b = lattice + np.array([-d, 0.0])
+        dx = np.linalg.norm(a[:, None, :] - b[None, :, :], axis=-1).min()
+        a = lattice + np.array([0.0, d])
+        b = lattice + np.array([0.0, -d])
+        dy = np.linalg.norm(a[:, None, :] - b[None, :, :], axis=-1).min()
+        return min(dx, dy)
+
+    lo, hi = 0.0, 1.0
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if min_sep(mid) < target:
+            lo = mid
+        else:
+            hi = mid
+    d = hi
+    mat = MaterialParams(stretch_x=1e6, stretch_y=1e6, stretch_z=1e6, bend_x=1e5, bend_y=1e5, volume=1e8,
+                         density=1000.0)
+    tmpl = _vertical_template(lib, vertices, element, r)
+    s = Scene(materials=[mat])
+    axes = [(d, d), (-d, d), (-d, -d), (d, -d)][:muscles]
+    for mu, (ax, ay) in enumerate(axes):
+        first = len(s.rods)
+        for (px, py) in lattice:
+            rest = _translated(tmpl, (ax + px, ay + py, 0.0))
+            rod = Rod(rest=rest, state=make_rest_state(rest), collision_group=mu)
+            rod.pinned[0] = 1
+            rod.pinned[-1] = 1
+            s.rods.append(rod)
+        for v in range(vertices):
+            s.bundles.append([(first + k, v) for k in range(rods_per_muscle)])
+        if mu in activate:
+            for k in range(rods_per_muscle):
+                s.activations.append(Activation(rod=first + k, factor=0.2, t_start=0.0, t_end=0.5))
+    s.settings = SolverSettings(velocity_damping=0.02)
+    return s
+
+
+def c4_rod_forest(lib, nx: int = 125, ny: int = 250, vertices: int = 32, seed: int = 1234) -> Scene:
+    """C4: 1M-vertex synthetic rod forest: nx x ny vertical rods x 32 vertices
+    (element 0.05 m, r = 0.05 m) on a 0.098 m lattice (2% overlap -> dense pill contacts),
+    bottom vertex pinned, gravity, no groups, bench material (scenarios.cpp:246-251),
+    dt = 1/240, I = 10, initial lateral velocity U[-0.5, 0.5] per rod scaled by height."""
+    element, r, pitch = 0.05, 0.05, 0.098
+    tmpl = _vertical_template(lib, vertices, element, r)
+    rng = np.random.default_rng(seed)
+    vel = rng.uniform(-0.5, 0.5, size=(nx * ny, 2))
+    frac = np.arange(vertices) / (vertices - 1)
+    mat = MaterialParams(stretch_x=1e6, stretch_y=1e6, stretch_z=1e6, bend_x=1e4, bend_y=1e4, volume=1e7,
+                         density=100.0)
+    s = Scene(materials=[mat])
+    for i in range(nx):
+        for j in range(ny):
+            rest = _translated(tmpl, (pitch * i, pitch * j, 0.0))
+            st = make_rest_state(rest)
+            u = vel[i * ny + j]
+            st.center_vel[:, 0] = u[0] * frac
+            st.center_vel[:, 1] = u[1] * frac
+            rod = Rod(rest=rest, state=st)
+            rod.pinned[0] = 1
+            s.rods.append(rod)
+    s.settings = SolverSettings(dt=1.0 / 240.0, iterations=10, substeps=1)
+    return s
+
+
+CONFIGS = {
+    "C1": c1_single_rod,
+    "C2": c2_stretch_grid,
+    "C3": c3_muscle_bundle,
+    "C4": c4_rod_forest,
+}
+
+
+def algorithmic_bytes(V: int, E: int, I: int, coupled: bool, P: int, Nc: int) -> int:
+    """B_substep of SURVEY §8(d) / BASELINE.md §4 — the roofline numerator per substep."""
+    return int(160 * V + 176 * E + (64 * I * (V + E) if coupled else 0) + 24 * P + 24 * Nc * (1 + I))
