@@ -1,1 +1,46 @@
-"""B200-native VIPER rod-solver substep (arXiv 1906.05260) behind the reference's C++ core API."""
+"""B200-native VIPER rod-solver substep (arXiv 1906.05260) behind the reference's core API.
+
+    from paper_1906_05260_b200 import Solver, Scene, Rod, MaterialParams, make_rest_pose
+    solver = Solver(scene)          # vrod::Solver(Scene)            solver.h:60
+    report = solver.step()          # vrod::Solver::step()           solver.cpp:363-388
+
+The compute path is libvrod_b200.so (hand-written sm_100a CUDA + host C++ behind the C-ABI
+in include/vrod_capi.h). There is no CPU fallback: if the library is missing, importing the
+solver raises.
+"""
+from __future__ import annotations
+
+from . import capi, workloads
+from ._lib import LIB_PATH, library
+from .handle import StepReport, SolverHandle
+from .scene import (Activation, Bone, DeviceError, HalfPlane, InvalidArgument, KinematicPill, MaterialParams,
+                    OutOfRange, Pill, PinMotion, RigidKeyframe, Rod, RodRestPose, RodState, Scene,
+                    SimulationError, SoftPin, SolverSettings, VrodError, make_rest_state)
+from . import scene as _scene
+
+
+class Solver(SolverHandle):
+    """vrod::Solver on the B200 (solver.h:54-115)."""
+
+    def __init__(self, scene: Scene):
+        super().__init__(library(), scene)
+
+
+def make_rest_pose(centers, radii, scales=None) -> RodRestPose:
+    """make_rest_pose (rod.h:88-90), computed by the product's host code."""
+    return _scene.make_rest_pose(library(), centers, radii, scales)
+
+
+def straight_rod(origin, direction, length, elements, radius, material=0) -> Rod:
+    return _scene.straight_rod(library(), origin, direction, length, elements, radius, material)
+
+
+def validate(scene: Scene) -> None:
+    """Scene::validate (scene.cpp:63-157)."""
+    _scene.validate(library(), scene)
+
+
+__all__ = ["Solver", "Scene", "Rod", "RodRestPose", "RodState", "MaterialParams", "SolverSettings", "HalfPlane",
+           "Pill", "KinematicPill", "Bone", "RigidKeyframe", "PinMotion", "SoftPin", "Activation", "StepReport",
+           "make_rest_pose", "make_rest_state", "straight_rod", "validate", "VrodError", "InvalidArgument",
+           "OutOfRange", "SimulationError", "DeviceError", "library", "LIB_PATH", "capi", "workloads"]

@@ -1,0 +1,173 @@
+// Launch interfaces of the product's sm_100a kernels. One substep (solver.cpp:301-361) is:
+//
+//   animate      pin motions + activation rest refresh         integrate.cu
+//   predict      prev snapshot, inertial prediction, LBS,      integrate.cu
+//                orientation inertia
+//   collide      pills -> bounding spheres -> hash grid ->     collide.cu
+//                candidate count/fill -> narrow phase -> ordered contacts, half-planes
+//   ext setup    external-block incidence (slot -> blocks)      sweep.cu
+//   I x sweep    external blocks, fused rod stencil sweep       sweep.cu
+//                (+ shape matching every period)               shape.cu
+//   finalize     classic scales, velocities                    integrate.cu
+//   report       residual RMS per kind, penetration            sweep.cu
+//
+// Everything is launched on one stream with device-side counts so a whole step is
+// capturable in one CUDA graph.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "world.cuh"
+
+namespace vdev {
+
+constexpr int kSweepThreads = 128;  // rod-sweep CTA (covers 126 owned slots + 2 halo)
+
+// Per-substep collision / external-block buffers.
+struct Collide {
+  int P = 0;            // pills
+  int T = 0;            // hash table size (power of two >= 2P)
+  long long cand_cap = 0;
+  long long contact_cap = 0;
+  int hp_cap = 0;
+  int n_planes = 0;
+  int n_pins = 0;
+  int iters_dich = 10;
+  int scan_parts = 0;
+
+  // pills (SoA): c0xyz c1xyz r0 r1 = 8 fields x P
+  double* pill = nullptr;
+  int* pill_rod = nullptr;
+  int* pill_el = nullptr;
+  int* pill_group = nullptr;
+  uint8_t* pill_self = nullptr;
+  uint32_t* pill_id = nullptr;   // pair_key id (collision.cpp:241-245)
+  double* bsph = nullptr;        // bounding spheres: cx cy cz R (4 x P)
+  long long* cellkey = nullptr;  // 3 x P
+  // grid
+  int* table = nullptr;          // T: representative pill or -1
+  int* cell_count = nullptr;     // T
+  int* cell_start = nullptr;     // T+1
+  int* cell_cursor = nullptr;    // T
+  int* cell_items = nullptr;     // P
+  int* pill_cell = nullptr;      // P
+  // candidates
+  int* cand_count = nullptr;     // P+1
+  int* cand_off = nullptr;       // P+1
+  int* cand_i = nullptr;         // cand_cap
+  int* cand_j = nullptr;
+  int* cand_flag = nullptr;      // cand_cap+1
+  int* cand_pos = nullptr;       // cand_cap+1
+  double* cand_ab = nullptr;     // 3 x cand_cap (alpha, beta, distance)
+  // contacts (current substep), ordered by (pill_a, pill_b)
+  int* ct_a = nullptr;
+  int* ct_b = nullptr;
+  double* ct_alpha = nullptr;
+  double* ct_beta = nullptr;
+  double* ct_dist = nullptr;     // standalone find_contacts only
+  // warm-start lists from the previous substep (sorted by pair key)
+  unsigned long long* warm_rr_key = nullptr;
+  double* warm_rr_alpha = nullptr;
+  unsigned long long* warm_rk_key = nullptr;
+  double* warm_rk_alpha = nullptr;
+  int* rk_flag = nullptr;        // contact_cap+1 scratch
+  int* rk_pos = nullptr;
+  // half-planes
+  double* planes = nullptr;      // 4 x n_planes (nx ny nz offset)
+  int* hp_flag = nullptr;        // n_planes*V + 1
+  int* hp_pos = nullptr;
+  int* hp_slot = nullptr;        // hp_cap
+  int* hp_plane = nullptr;
+  // pins (static): slot, target xyz, stiffness
+  int* pin_slot = nullptr;
+  double* pin_data = nullptr;    // 4 x n_pins
+  // external blocks: pins | contacts | half-planes
+  long long ext_cap = 0;
+  double* ext_lam = nullptr;     // 3 x ext_cap
+  double* ext_out = nullptr;     // 16 x ext_cap: dc[4][3], ds[4]
+  uint8_t* ext_active = nullptr; // ext_cap
+  int* ext_cnt = nullptr;        // V+1 incidence counts
+  int* ext_off = nullptr;        // V+1
+  int* ext_cur = nullptr;        // V
+  int* ext_items = nullptr;      // 4 x ext_cap entries (block << 2 | endpoint)
+  // device scalars
+  int* scalars = nullptr;        // see Scalar enum
+  unsigned long long* maxr_bits = nullptr;
+  int* scan_tmp = nullptr;       // scan partials
+};
+enum Scalar : int { SC_NCAND = 0, SC_NCT, SC_NHP, SC_NRR, SC_NRK, SC_NRR_PREV, SC_NRK_PREV, SC_BROAD, SC_OVF,
+                    kScalars };
+
+struct Groups {  // shape matching (bundling.cpp)
+  int G = 0;
+  int levels = 0;
+  int* off = nullptr;            // G+1 member offsets
+  int* mslot = nullptr;          // member vertex slot
+  int* meslot = nullptr;         // member frame slot
+  double* mrest = nullptr;       // 17 per member: rc(3) rs rR(9) qR(4)
+  double* grest = nullptr;       // 4 per group: rcent(3) denom
+  double* warm = nullptr;        // 4 per group: warm rotation (w,x,y,z), persistent
+  uint8_t* serial = nullptr;
+  int* level_off = nullptr;      // host-side only (levels+1)
+  int* level_groups = nullptr;   // device: group ids ordered by level
+};
+
+// Animation packet per substep (host-evaluated, uploaded once per step).
+struct AnimLayout {
+  int n_pm = 0, n_act = 0, n_bone = 0, n_kin = 0;
+  int stride = 0;  // doubles per substep
+  int off_time = 0, off_pm = 0, off_act = 0, off_bone = 0, off_kin = 0;
+};
+
+struct SweepParams {
+  double h, h2, beta;
+  int classic;
+  int iter;            // iteration index (error word / singular counter)
+  int substep;         // substep index within the step (error word)
+  int n_pins;
+  int elastic_blocks;  // first external block index in the reference's block list
+  double contact_k;    // settings.contact_stiffness
+};
+
+// scan.cu
+void scan_exclusive(const int* in, int* out, long long n_cap, const int* n_dev, int* partials, int parts,
+                    cudaStream_t st);
+long long scan_partials_needed(long long n);
+
+// integrate.cu
+void launch_animate(const World& w, const double* anim, const AnimLayout& al, const int* pm_slot,
+                    const int* act_rod_off, const int* act_list, double* act_applied, const int* act_rods,
+                    int n_act_rods, cudaStream_t st);
+void launch_predict(const World& w, const double* anim, const AnimLayout& al, const double* gravity_h,
+                    double h, int substep, unsigned long long* err, cudaStream_t st);
+void launch_finalize_from(const World& w, const double* src, double h, double keep, cudaStream_t st);
+void launch_copy_state(const World& w, const double* src, double* dst, cudaStream_t st);
+
+// collide.cu
+void launch_collide(const World& w, Collide& c, const double* anim, const AnimLayout& al, int substep,
+                    unsigned long long* err, StepAccum* acc, int possible, cudaStream_t st);
+void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int prefilter, int do_narrow,
+                         int split_warm, int store_d, cudaStream_t st);
+void launch_narrow_only(Collide& c, int split_warm, int store_d, cudaStream_t st);
+void launch_halfplanes(const World& w, Collide& c, cudaStream_t st);
+// standalone fine-grained entry points (vrod_pill_project & co), on device arrays
+void launch_pill_project(long long n, const double* x, const double* pills, double* t, double* d,
+                         uint8_t* deg, cudaStream_t st);
+void launch_deepest(long long n, const double* a, const double* b, int iters, const double* warm, double* alpha,
+                    double* beta, double* dist, cudaStream_t st);
+
+// sweep.cu
+void launch_ext_setup(const World& w, Collide& c, cudaStream_t st);
+void launch_iteration(const World& w, Collide& c, const double* X, double* Y, const SweepParams& sp,
+                      int* singular_counter, unsigned long long* err, cudaStream_t st);
+void launch_residuals(const World& w, const double* X, int classic, double* partials, int parts, double* out8,
+                      cudaStream_t st);
+void launch_penetration(const World& w, Collide& c, const double* X, StepAccum* acc, cudaStream_t st);
+int report_parts(int V);
+
+// shape.cu
+void launch_shape_match(const World& w, const Groups& g, double* X, const int* level_off_host, cudaStream_t st);
+
+}  // namespace vdev

@@ -1,0 +1,980 @@
+// Host orchestration of the product Solver (reference: Solver, solver.cpp:102-442).
+//
+// Construction validates the scene, derives the setup (host_model.cpp), lays the world out in
+// device memory (world.cuh) and uploads it once. step() evaluates the per-substep animation
+// inputs on the host exactly like the reference (pin paths, activation amounts, bone poses),
+// then replays ONE CUDA graph holding every kernel of every substep of the step — predict,
+// collide, the I Jacobi sweeps with shape matching, finalize, report — and reads back a single
+// StepReport. Nothing leaves the device between steps.
+#include "solver.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstddef>
+#include <cstring>
+#include <map>
+
+namespace vhost {
+
+using namespace vm;
+using vdev::StepAccum;
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw DeviceError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+template <typename T>
+T* Solver::dalloc(std::size_t n) {
+  void* p = nullptr;
+  const std::size_t bytes = std::max<std::size_t>(n, 1) * sizeof(T);
+  check_cuda(cudaMalloc(&p, bytes), "cudaMalloc");
+  check_cuda(cudaMemsetAsync(p, 0, bytes, stream_), "cudaMemset");
+  allocs_.push_back(p);
+  return static_cast<T*>(p);
+}
+
+template <typename T>
+static void upload(T* dst, const std::vector<T>& src, cudaStream_t st) {
+  if (!src.empty()) check_cuda(cudaMemcpyAsync(dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, st), "upload");
+}
+
+static int next_pow2(long long x) {
+  int p = 64;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+Solver::Solver(const SceneData& scene) : scene_(scene) {
+  scene_.validate();
+  // assemble_rod_constraints validates material and rest pose again (constraints.cpp:284-285)
+  setup_ = build_setup(scene_);
+  classic_ = scene_.settings.scale_mode == 1;
+  const int R = setup_.R, V = setup_.V, vpad = setup_.vpad;
+  const int K = static_cast<int>(scene_.kpills.size());
+  for (const auto& rod : scene_.rods)
+    if (rod.n + 1 >= 65536) throw std::invalid_argument("rod too long for the pair_key warm-start ids (>= 65535 elements)");
+  if (R + 1 >= 65536) throw std::invalid_argument("too many rods for the pair_key warm-start ids (>= 65535)");
+  for (const auto& kp : scene_.kpills)
+    if (kp.pill.element != -1) throw std::invalid_argument("kinematic pills with element != -1 are not supported");
+
+  check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+
+  // ---- world -------------------------------------------------------------------------------
+  w_.R = R;
+  w_.V = V;
+  w_.vpad = vpad;
+  w_.E = setup_.E;
+  w_.K = K;
+  w_.P = setup_.E + K;
+  w_.classic = classic_ ? 1 : 0;
+  w_.rod_vbase = dalloc<int>(R);
+  w_.rod_n = dalloc<int>(R);
+  w_.rod_block_base = dalloc<int>(R);
+  w_.rod_material = dalloc<int>(R);
+  w_.rod_group = dalloc<int>(R);
+  w_.rod_self = dalloc<uint8_t>(R);
+  w_.rod_ekinds = dalloc<uint8_t>(R);
+  w_.rod_vkinds = dalloc<uint8_t>(R);
+  w_.load_flags = dalloc<uint8_t>(R);
+  w_.slot_rod = dalloc<int>(vpad);
+  w_.slot_loc = dalloc<int>(vpad);
+  w_.slot_m = dalloc<int>(vpad);
+  w_.pinned = dalloc<uint8_t>(vpad);
+  w_.vstat = dalloc<double>(static_cast<std::size_t>(vdev::kVStatFields) * vpad);
+  w_.estat = dalloc<double>(static_cast<std::size_t>(vdev::kEStatFields) * vpad);
+  w_.mat = dalloc<double>(8 * scene_.materials.size());
+  w_.X = dalloc<double>(static_cast<std::size_t>(vdev::kStateFields) * vpad);
+  w_.Y = dalloc<double>(static_cast<std::size_t>(vdev::kStateFields) * vpad);
+  w_.prev = dalloc<double>(static_cast<std::size_t>(vdev::kStateFields) * vpad);
+  w_.vel = dalloc<double>(static_cast<std::size_t>(vdev::kVelFields) * vpad);
+  w_.lam = dalloc<double>(static_cast<std::size_t>(vdev::kLamFields) * vpad);
+  w_.loads = dalloc<double>(7ull * vpad);
+  int nbones_total = 0;
+  for (const auto& rod : scene_.rods) nbones_total += static_cast<int>(rod.bones.size());
+  w_.has_bones = nbones_total > 0;
+  w_.rod_bone_off = dalloc<int>(R + 1);
+  w_.rod_bones = dalloc<int>(nbones_total);
+  w_.slot_bw_off = dalloc<int>(vpad);
+  long long bw_total = 0;
+  for (const auto& rod : scene_.rods) bw_total += static_cast<long long>(rod.n) * rod.bones.size();
+  w_.bone_w = dalloc<double>(bw_total);
+
+  // ---- collision ---------------------------------------------------------------------------
+  c_.P = w_.P;
+  c_.T = next_pow2(2ll * std::max(c_.P, 1));
+  c_.n_planes = static_cast<int>(scene_.planes.size());
+  c_.n_pins = static_cast<int>(scene_.soft_pins.size());
+  c_.iters_dich = scene_.settings.dich;
+  // Can any pair pass pair_allowed (collision.cpp:172-180)?
+  {
+    bool any = false;
+    std::map<int, int> groups;  // group -> rods with that group (>= 0)
+    int ungrouped = 0;
+    for (const auto& rod : scene_.rods) {
+      if (rod.group >= 0) groups[rod.group]++;
+      else ++ungrouped;
+      if (rod.self_collide && rod.n >= 4) any = true;
+    }
+    if (ungrouped + static_cast<int>(groups.size()) >= 2) any = true;
+    if (ungrouped >= 1 && R >= 2) any = true;
+    for (const auto& kp : scene_.kpills)
+      for (const auto& rod : scene_.rods)
+        if (kp.pill.group < 0 || kp.pill.group != rod.group) any = true;
+    collide_possible_ = any && c_.P >= 2;
+  }
+  ext_possible_ = collide_possible_ || c_.n_planes > 0 || c_.n_pins > 0;
+  c_.cand_cap = collide_possible_ ? std::max<long long>(1 << 16, 32ll * c_.P) : 0;
+  c_.contact_cap = collide_possible_ ? std::max<long long>(1 << 15, 16ll * c_.P) : 0;
+  c_.hp_cap = c_.n_planes * V;
+  c_.ext_cap = ext_possible_ ? c_.n_pins + c_.contact_cap + c_.hp_cap : 0;
+  c_.pill = dalloc<double>(8ull * std::max(c_.P, 1));
+  c_.pill_rod = dalloc<int>(c_.P);
+  c_.pill_el = dalloc<int>(c_.P);
+  c_.pill_group = dalloc<int>(c_.P);
+  c_.pill_self = dalloc<uint8_t>(c_.P);
+  c_.pill_id = dalloc<uint32_t>(c_.P);
+  c_.bsph = dalloc<double>(4ull * std::max(c_.P, 1));
+  c_.cellkey = dalloc<long long>(3ull * std::max(c_.P, 1));
+  c_.table = dalloc<int>(c_.T);
+  c_.cell_count = dalloc<int>(c_.T);
+  c_.cell_start = dalloc<int>(c_.T + 1);
+  c_.cell_cursor = dalloc<int>(c_.T);
+  c_.cell_items = dalloc<int>(c_.P);
+  c_.pill_cell = dalloc<int>(c_.P);
+  c_.cand_count = dalloc<int>(c_.P + 1);
+  c_.cand_off = dalloc<int>(c_.P + 1);
+  c_.cand_i = dalloc<int>(c_.cand_cap);
+  c_.cand_j = dalloc<int>(c_.cand_cap);
+  c_.cand_flag = dalloc<int>(c_.cand_cap + 1);
+  c_.cand_pos = dalloc<int>(c_.cand_cap + 1);
+  c_.cand_ab = dalloc<double>(3 * c_.cand_cap);
+  c_.ct_a = dalloc<int>(c_.contact_cap);
+  c_.ct_b = dalloc<int>(c_.contact_cap);
+  c_.ct_alpha = dalloc<double>(c_.contact_cap);
+  c_.ct_beta = dalloc<double>(c_.contact_cap);
+  c_.warm_rr_key = dalloc<unsigned long long>(c_.contact_cap);
+  c_.warm_rr_alpha = dalloc<double>(c_.contact_cap);
+  c_.warm_rk_key = dalloc<unsigned long long>(K > 0 ? c_.contact_cap : 1);
+  c_.warm_rk_alpha = dalloc<double>(K > 0 ? c_.contact_cap : 1);
+  c_.rk_flag = dalloc<int>(K > 0 ? c_.contact_cap + 1 : 1);
+  c_.rk_pos = dalloc<int>(K > 0 ? c_.contact_cap + 1 : 1);
+  c_.planes = dalloc<double>(4 * std::max(c_.n_planes, 1));
+  c_.hp_flag = dalloc<int>(static_cast<std::size_t>(c_.hp_cap) + 1);
+  c_.hp_pos = dalloc<int>(static_cast<std::size_t>(c_.hp_cap) + 1);
+  c_.hp_slot = dalloc<int>(c_.hp_cap);
+  c_.hp_plane = dalloc<int>(c_.hp_cap);
+  c_.pin_slot = dalloc<int>(c_.n_pins);
+  c_.pin_data = dalloc<double>(4 * std::max(c_.n_pins, 1));
+  c_.ext_lam = dalloc<double>(3 * c_.ext_cap);
+  c_.ext_out = dalloc<double>(16 * c_.ext_cap);
+  c_.ext_active = dalloc<uint8_t>(c_.ext_cap);
+  c_.ext_cnt = dalloc<int>(V + 1);
+  c_.ext_off = dalloc<int>(V + 1);
+  c_.ext_cur = dalloc<int>(V);
+  c_.ext_items = dalloc<int>(4 * c_.ext_cap);
+  c_.scalars = dalloc<int>(vdev::kScalars);
+  c_.maxr_bits = dalloc<unsigned long long>(1);
+  const long long scan_max = std::max<long long>({c_.cand_cap, static_cast<long long>(c_.T), static_cast<long long>(c_.P),
+                                                  c_.contact_cap, static_cast<long long>(c_.hp_cap), static_cast<long long>(V)});
+  c_.scan_parts = static_cast<int>(vdev::scan_partials_needed(scan_max));
+  c_.scan_tmp = dalloc<int>(c_.scan_parts);
+
+  // ---- shape matching ----------------------------------------------------------------------
+  g_.G = static_cast<int>(setup_.groups.size());
+  g_.levels = setup_.levels;
+  {
+    std::vector<int> off(1, 0), ms, mes, lvl_groups;
+    std::vector<double> mrest, grest, warm;
+    std::vector<uint8_t> serial;
+    for (const auto& g : setup_.groups) {
+      for (std::size_t i = 0; i < g.slot.size(); ++i) {
+        ms.push_back(g.slot[i]);
+        mes.push_back(g.eslot[i]);
+        mrest.insert(mrest.end(), {g.rc[i].x, g.rc[i].y, g.rc[i].z, g.rs[i]});
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b) mrest.push_back(g.rR[i].m[a][b]);
+        mrest.insert(mrest.end(), {g.qR[i].w, g.qR[i].x, g.qR[i].y, g.qR[i].z});
+      }
+      off.push_back(static_cast<int>(ms.size()));
+      grest.insert(grest.end(), {g.rcent.x, g.rcent.y, g.rcent.z, g.denom});
+      warm.insert(warm.end(), {1.0, 0.0, 0.0, 0.0});
+      serial.push_back(g.serial_apply ? 1 : 0);
+    }
+    level_off_.assign(g_.levels + 1, 0);
+    for (int l = 0; l < g_.levels; ++l) {
+      for (int gi = 0; gi < g_.G; ++gi)
+        if (setup_.group_level[gi] == l) lvl_groups.push_back(gi);
+      level_off_[l + 1] = static_cast<int>(lvl_groups.size());
+    }
+    g_.off = dalloc<int>(off.size());
+    g_.mslot = dalloc<int>(ms.size());
+    g_.meslot = dalloc<int>(mes.size());
+    g_.mrest = dalloc<double>(mrest.size());
+    g_.grest = dalloc<double>(grest.size());
+    g_.warm = dalloc<double>(warm.size());
+    g_.serial = dalloc<uint8_t>(serial.size());
+    g_.level_groups = dalloc<int>(lvl_groups.size());
+    upload(g_.off, off, stream_);
+    upload(g_.mslot, ms, stream_);
+    upload(g_.meslot, mes, stream_);
+    upload(g_.mrest, mrest, stream_);
+    upload(g_.grest, grest, stream_);
+    upload(g_.warm, warm, stream_);
+    upload(g_.serial, serial, stream_);
+    upload(g_.level_groups, lvl_groups, stream_);
+  }
+
+  // ---- animation packet ----------------------------------------------------------------------
+  al_.n_pm = static_cast<int>(setup_.pin_motion_ids.size());
+  al_.n_act = static_cast<int>(scene_.activations.size());
+  al_.n_bone = static_cast<int>(scene_.bones.size());
+  al_.n_kin = K;
+  al_.off_time = 0;
+  al_.off_pm = 1;
+  al_.off_act = al_.off_pm + 3 * al_.n_pm;
+  al_.off_bone = al_.off_act + al_.n_act;
+  al_.off_kin = al_.off_bone + 14 * al_.n_bone;
+  al_.stride = al_.off_kin + 8 * al_.n_kin;
+  const int S = scene_.settings.substeps;
+  d_anim_ = dalloc<double>(static_cast<std::size_t>(al_.stride) * S);
+  check_cuda(cudaMallocHost(&h_anim_, sizeof(double) * al_.stride * S), "cudaMallocHost");
+  {
+    std::vector<int> pm_slot;
+    for (int id : setup_.pin_motion_ids) {
+      const auto& pm = scene_.pin_motions[id];
+      pm_slot.push_back(setup_.vbase[pm.rod] + pm.vertex);
+    }
+    d_pm_slot_ = dalloc<int>(pm_slot.size());
+    upload(d_pm_slot_, pm_slot, stream_);
+    // activations grouped per rod, in activation order
+    std::map<int, std::vector<int>> per_rod;
+    for (int i = 0; i < al_.n_act; ++i) per_rod[scene_.activations[i].rod].push_back(i);
+    std::vector<int> rod_off(1, 0), list, rods;
+    for (auto& [r, ids] : per_rod) {
+      rods.push_back(r);
+      list.insert(list.end(), ids.begin(), ids.end());
+      rod_off.push_back(static_cast<int>(list.size()));
+    }
+    n_act_rods_ = static_cast<int>(rods.size());
+    d_act_rod_off_ = dalloc<int>(rod_off.size());
+    d_act_list_ = dalloc<int>(list.size());
+    d_act_rods_ = dalloc<int>(rods.size());
+    upload(d_act_rod_off_, rod_off, stream_);
+    upload(d_act_list_, list, stream_);
+    upload(d_act_rods_, rods, stream_);
+    std::vector<double> act(al_.n_act, -1.0);  // applied_activation_ starts at -1 (solver.cpp:142)
+    for (const auto& a : scene_.activations) act.insert(act.end(), {a.factor, double(a.first), double(a.last)});
+    d_act_applied_ = dalloc<double>(act.size());
+    upload(d_act_applied_, act, stream_);
+  }
+
+  d_acc_ = dalloc<StepAccum>(1);
+  check_cuda(cudaMallocHost(&h_acc_, sizeof(StepAccum)), "cudaMallocHost");
+  d_singular_ = dalloc<int>(std::max(scene_.settings.iterations, 1));
+  d_err_ = dalloc<unsigned long long>(1);
+  report_parts_ = vdev::report_parts(V);
+  d_report_partials_ = dalloc<double>(16ull * std::max(report_parts_, 1));
+
+  upload_static();
+  check_cuda(cudaStreamSynchronize(stream_), "setup");
+}
+
+Solver::~Solver() {
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (void* p : allocs_) cudaFree(p);
+  if (h_anim_) cudaFreeHost(h_anim_);
+  if (h_acc_) cudaFreeHost(h_acc_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Solver::upload_static() {
+  const int R = setup_.R, vpad = setup_.vpad;
+  const bool scale_kinds = !classic_;
+  std::vector<int> vbase = setup_.vbase, rn(R), mat(R), grp(R), bone_off(1, 0), bones;
+  std::vector<uint8_t> self(R);
+  for (int r = 0; r < R; ++r) {
+    const RodData& rod = scene_.rods[r];
+    rn[r] = rod.n;
+    mat[r] = rod.material;
+    grp[r] = rod.group;
+    self[r] = rod.self_collide ? 1 : 0;
+    bones.insert(bones.end(), rod.bones.begin(), rod.bones.end());
+    bone_off.push_back(static_cast<int>(bones.size()));
+  }
+  upload(w_.rod_vbase, vbase, stream_);
+  upload(w_.rod_n, rn, stream_);
+  upload(w_.rod_block_base, setup_.block_base, stream_);
+  upload(w_.rod_material, mat, stream_);
+  upload(w_.rod_group, grp, stream_);
+  upload(w_.rod_self, self, stream_);
+  upload(w_.rod_ekinds, setup_.ekinds, stream_);
+  upload(w_.rod_vkinds, setup_.vkinds, stream_);
+  upload(w_.rod_bone_off, bone_off, stream_);
+  upload(w_.rod_bones, bones, stream_);
+  std::vector<double> mats;
+  for (const auto& m : scene_.materials) mats.insert(mats.end(), {m.sx, m.sy, m.sz, m.bx, m.by, m.bz, m.vol, m.rho});
+  upload(w_.mat, mats, stream_);
+
+  std::vector<int> srod(vpad, 0), sloc(vpad, 0), sm(vpad, 0), bw_off(vpad, 0);
+  std::vector<uint8_t> pinned(vpad, 0);
+  std::vector<double> vstat(static_cast<std::size_t>(vdev::kVStatFields) * vpad, 0.0);
+  std::vector<double> estat(static_cast<std::size_t>(vdev::kEStatFields) * vpad, 0.0);
+  std::vector<double> X(static_cast<std::size_t>(vdev::kStateFields) * vpad, 0.0);
+  std::vector<double> vel(static_cast<std::size_t>(vdev::kVelFields) * vpad, 0.0);
+  std::vector<double> bw;
+  cw_.assign(setup_.V, 0.0);
+  sw_.assign(setup_.V, 0.0);
+  auto VS = [&](int f, int i) -> double& { return vstat[static_cast<std::size_t>(f) * vpad + i]; };
+  auto ES = [&](int f, int i) -> double& { return estat[static_cast<std::size_t>(f) * vpad + i]; };
+  auto XS = [&](int f, int i) -> double& { return X[static_cast<std::size_t>(f) * vpad + i]; };
+  auto VL = [&](int f, int i) -> double& { return vel[static_cast<std::size_t>(f) * vpad + i]; };
+  for (int r = 0; r < R; ++r) {
+    const RodData& rod = scene_.rods[r];
+    const Material& M = scene_.materials[rod.material];
+    const double rho = M.rho, kxy = M.sx + M.sy, bxy = M.bx + M.by;
+    const int n = rod.n, m = n - 1, v0 = setup_.vbase[r];
+    for (int k = 0; k < n; ++k) {
+      const int v = v0 + k;
+      srod[v] = r;
+      sloc[v] = k;
+      sm[v] = m;
+      bw_off[v] = static_cast<int>(bw.size());
+      for (std::size_t b = 0; b < rod.bones.size(); ++b) bw.push_back(rod.bone_w[k * rod.bones.size() + b]);
+      // build_layout, layout.cpp:46-69
+      double lump = 0.0;
+      if (k > 0) lump += 0.5 * rod.len0[k - 1];
+      if (k < n - 1) lump += 0.5 * rod.len0[k];
+      const double rbar = rod.r[k];
+      const bool pin = rod.pinned[k] != 0;
+      pinned[v] = pin ? 1 : 0;
+      VS(vdev::RBAR, v) = rbar;
+      VS(vdev::SBAR, v) = rod.rs[k];
+      if (pin) {
+        cw_[v] = kInf;
+        sw_[v] = kInf;
+        VS(vdev::IC, v) = 0.0;
+        VS(vdev::IS, v) = 0.0;
+      } else {
+        const double cw = kPi * rbar * rbar * rho * lump;
+        const double sw = 0.5 * kPi * rbar * rbar * rbar * rbar * rho * lump;
+        cw_[v] = cw;
+        sw_[v] = sw;
+        VS(vdev::IC, v) = 1.0 / cw;
+        VS(vdev::IS, v) = classic_ ? 0.0 : 1.0 / sw;  // classic: scale DOFs kinematic (solver.cpp:106-109)
+      }
+      XS(vdev::CX, v) = rod.c[k].x;
+      XS(vdev::CY, v) = rod.c[k].y;
+      XS(vdev::CZ, v) = rod.c[k].z;
+      XS(vdev::S, v) = rod.s[k];
+      VL(vdev::VX, v) = rod.cv[k].x;
+      VL(vdev::VY, v) = rod.cv[k].y;
+      VL(vdev::VZ, v) = rod.cv[k].z;
+      VL(vdev::VS, v) = rod.sv[k];
+      if (k < m) {
+        XS(vdev::QW, v) = rod.q[k].w;
+        XS(vdev::QX, v) = rod.q[k].x;
+        XS(vdev::QY, v) = rod.q[k].y;
+        XS(vdev::QZ, v) = rod.q[k].z;
+        VL(vdev::WX, v) = rod.av[k].x;
+        VL(vdev::WY, v) = rod.av[k].y;
+        VL(vdev::WZ, v) = rod.av[k].z;
+        ES(vdev::LEN, v) = rod.len[k];
+        ES(vdev::LEN0, v) = rod.len0[k];
+        ES(vdev::TDOT, v) = rod.tdot[k];
+        ES(vdev::SGRAD, v) = rod.sgrad[k];
+        if (k < m - 1) {
+          ES(vdev::SLAP, v) = rod.slap[k];
+          ES(vdev::DARBX, v) = rod.darb[k].x;
+          ES(vdev::DARBY, v) = rod.darb[k].y;
+          ES(vdev::DARBZ, v) = rod.darb[k].z;
+        }
+        ES(vdev::RQW, v) = rod.rq[k].w;
+        ES(vdev::RQX, v) = rod.rq[k].x;
+        ES(vdev::RQY, v) = rod.rq[k].y;
+        ES(vdev::RQZ, v) = rod.rq[k].z;
+        // assemble_rod_constraints element pass (constraints.cpp:302-314)
+        const double rmid = 0.5 * (rod.r[k] + rod.r[k + 1]);
+        const double a2 = kPi * rmid * rmid;
+        const double a4 = 0.25 * kPi * rmid * rmid * rmid * rmid;
+        const double l = rod.len[k], l0 = rod.len0[k];
+        ES(vdev::A2E, v) = a2;
+        ES(vdev::A4EP, v) = 0.25 * kPi * std::pow(rmid, 4);
+        ES(vdev::KSZ, v) = a2 * M.sz * l;
+        ES(vdev::KCS, v) = a2 * kxy * l;
+        ES(vdev::KSS, v) = a4 * kxy * l;
+        ES(vdev::KVS, v) = a2 * M.vol * l0;
+        // refresh_orientation_inertia at construction (layout.cpp:76-93)
+        const double smid = 0.5 * (rod.s[k] + rod.s[k + 1]);
+        const double r4 = kPi * rmid * rmid * rmid * rmid;
+        const double base = rho * smid * smid * r4 * l0;
+        ES(vdev::TWB, v) = base;
+        ES(vdev::ITX, v) = 1.0 / (0.25 * base);
+        ES(vdev::ITY, v) = 1.0 / (0.25 * base);
+        ES(vdev::ITZ, v) = 1.0 / (0.5 * base);
+      }
+      if (k >= 1 && k <= m - 1) {  // vertex pass (constraints.cpp:315-327)
+        const double rv = rod.r[k];
+        const double a4 = 0.25 * kPi * rv * rv * rv * rv;
+        const double lw = 0.5 * (rod.len[k - 1] + rod.len[k]);
+        const double lw0 = 0.5 * (rod.len0[k - 1] + rod.len0[k]);
+        ES(vdev::A4VP, v) = 0.25 * kPi * std::pow(rv, 4);
+        ES(vdev::KBT0, v) = a4 * M.sz * lw;
+        ES(vdev::KBT1, v) = a4 * M.sz * lw;
+        ES(vdev::KBT2, v) = a4 * kxy * lw;
+        ES(vdev::KSB, v) = a4 * bxy * lw;
+        ES(vdev::KVB, v) = 2.0 * a4 * M.vol * lw0;
+      }
+      (void)scale_kinds;
+    }
+  }
+  upload(w_.slot_rod, srod, stream_);
+  upload(w_.slot_loc, sloc, stream_);
+  upload(w_.slot_m, sm, stream_);
+  upload(w_.pinned, pinned, stream_);
+  upload(w_.vstat, vstat, stream_);
+  upload(w_.estat, estat, stream_);
+  upload(w_.X, X, stream_);
+  upload(w_.vel, vel, stream_);
+  upload(w_.slot_bw_off, bw_off, stream_);
+  upload(w_.bone_w, bw, stream_);
+
+  // static pill attributes: rod pills in (rod, element) order, then kinematic pills
+  const int P = c_.P;
+  std::vector<int> prod(P), pel(P), pgrp(P);
+  std::vector<uint8_t> pself(P);
+  std::vector<uint32_t> pid(P);
+  int i = 0;
+  for (int r = 0; r < R; ++r) {
+    const RodData& rod = scene_.rods[r];
+    for (int e = 0; e < rod.n - 1; ++e, ++i) {
+      prod[i] = r;
+      pel[i] = e;
+      pgrp[i] = rod.group;
+      pself[i] = rod.self_collide ? 1 : 0;
+      pid[i] = (static_cast<uint32_t>(r + 1) << 16) | (static_cast<uint32_t>(e + 1) & 0xffffu);
+    }
+  }
+  for (const auto& kp : scene_.kpills) {
+    prod[i] = -1;
+    pel[i] = kp.pill.element;
+    pgrp[i] = kp.pill.group;
+    pself[i] = kp.pill.self_collide ? 1 : 0;
+    pid[i] = (0u << 16) | (static_cast<uint32_t>(kp.pill.element + 1) & 0xffffu);
+    ++i;
+  }
+  upload(c_.pill_rod, prod, stream_);
+  upload(c_.pill_el, pel, stream_);
+  upload(c_.pill_group, pgrp, stream_);
+  upload(c_.pill_self, pself, stream_);
+  upload(c_.pill_id, pid, stream_);
+  std::vector<double> planes;
+  for (const auto& p : scene_.planes) planes.insert(planes.end(), {p.first.x, p.first.y, p.first.z, p.second});
+  upload(c_.planes, planes, stream_);
+  std::vector<int> pin_slot;
+  std::vector<double> pin_data;
+  for (const auto& sp : scene_.soft_pins) {
+    pin_slot.push_back(setup_.vbase[sp.rod] + sp.vertex);
+    pin_data.insert(pin_data.end(), {sp.target.x, sp.target.y, sp.target.z, sp.k});
+  }
+  upload(c_.pin_slot, pin_slot, stream_);
+  upload(c_.pin_data, pin_data, stream_);
+  int zero_scalars[vdev::kScalars] = {0};
+  check_cuda(cudaMemcpyAsync(c_.scalars, zero_scalars, sizeof(zero_scalars), cudaMemcpyHostToDevice, stream_), "scalars");
+}
+
+// Host evaluation of the per-substep animation inputs (scene.cpp:22-61, solver.cpp:138-197).
+void Solver::fill_animation(int substeps, double h) {
+  double t = time_;
+  for (int s = 0; s < substeps; ++s) {
+    const double t_prev = t;
+    const double t_new = t + h;
+    double* a = h_anim_ + static_cast<std::size_t>(al_.stride) * s;
+    a[al_.off_time] = t_new;
+    for (int i = 0; i < al_.n_pm; ++i) {
+      const V3 p = scene_.pin_motions[setup_.pin_motion_ids[i]].position_at(t_new);
+      a[al_.off_pm + 3 * i] = p.x;
+      a[al_.off_pm + 3 * i + 1] = p.y;
+      a[al_.off_pm + 3 * i + 2] = p.z;
+    }
+    for (int i = 0; i < al_.n_act; ++i) a[al_.off_act + i] = scene_.activations[i].amount_at(t_new);
+    for (int b = 0; b < al_.n_bone; ++b) {
+      const BoneData& bone = scene_.bones[b];
+      const Q4 rp = bone.rotation_at(t_prev), rn = bone.rotation_at(t_new);
+      const V3 pp = bone.position_at(t_prev), pn = bone.position_at(t_new);
+      double* o = a + al_.off_bone + 14 * b;
+      const double vals[14] = {rp.w, rp.x, rp.y, rp.z, rn.w, rn.x, rn.y, rn.z, pp.x, pp.y, pp.z, pn.x, pn.y, pn.z};
+      std::memcpy(o, vals, sizeof(vals));
+    }
+    for (int k = 0; k < al_.n_kin; ++k) {
+      PillData p = scene_.kpills[k].pill;
+      if (scene_.kpills[k].bone >= 0) {
+        const BoneData& bone = scene_.bones[scene_.kpills[k].bone];
+        const Q4 rot = bone.rotation_at(t_new);
+        const V3 pos = bone.position_at(t_new);
+        p.c0 = qrot(rot, p.c0) + pos;
+        p.c1 = qrot(rot, p.c1) + pos;
+      }
+      double* o = a + al_.off_kin + 8 * k;
+      const double vals[8] = {p.c0.x, p.c0.y, p.c0.z, p.c1.x, p.c1.y, p.c1.z, p.r0, p.r1};
+      std::memcpy(o, vals, sizeof(vals));
+    }
+    t = t_new;
+  }
+}
+
+__global__ void k_init_acc(StepAccum* acc, unsigned long long* err, int* scalars) {
+  scalars[vdev::SC_OVF] = 0;
+  for (int q = 0; q < 8; ++q) acc->residuals[q] = 0.0;
+  acc->max_penetration = 0.0;
+  acc->contact_count = 0;
+  acc->broad_pairs = 0;
+  acc->skipped_singular = 0;
+  acc->error = ~0ull;
+  acc->max_candidates = 0;
+  acc->max_contacts = 0;
+  *err = ~0ull;
+}
+__global__ void k_end_substep(StepAccum* acc, const int* singular_last) { acc->skipped_singular += *singular_last; }
+__global__ void k_end_step(StepAccum* acc, const unsigned long long* err, const int* scalars) {
+  unsigned long long e = *err;
+  if (scalars[vdev::SC_OVF]) e = vdev::err_code(0, vdev::ERR_CAPACITY, scalars[vdev::SC_OVF], 0);  // results invalid
+  acc->error = e;
+}
+
+// Records every kernel of one step (or, with probe_log, one probe substep) on stream_.
+void Solver::record_step(double h, int substeps, int iterations, double* probe_log) {
+  cudaStream_t st = stream_;
+  const double h2 = h * h;
+  const double keep = 1.0 - scene_.settings.damping;
+  const double g[3] = {scene_.settings.g.x, scene_.settings.g.y, scene_.settings.g.z};
+  k_init_acc<<<1, 1, 0, st>>>(d_acc_, d_err_, c_.scalars);
+  check_cuda(cudaMemcpyAsync(d_anim_, h_anim_, sizeof(double) * al_.stride * substeps, cudaMemcpyHostToDevice, st),
+             "anim upload");
+  for (int s = 0; s < substeps; ++s) {
+    const double* anim = d_anim_ + static_cast<std::size_t>(al_.stride) * s;
+    vdev::launch_animate(w_, anim, al_, d_pm_slot_, d_act_rod_off_, d_act_list_, d_act_applied_, d_act_rods_,
+                         n_act_rods_, st);
+    vdev::launch_predict(w_, anim, al_, g, h, s, d_err_, st);
+    check_cuda(cudaMemsetAsync(w_.lam, 0, sizeof(double) * vdev::kLamFields * w_.vpad, st), "lam reset");
+    if (c_.P >= 1) vdev::launch_collide(w_, c_, anim, al_, s, d_err_, d_acc_, collide_possible_ ? 1 : 0, st);
+    vdev::launch_halfplanes(w_, c_, st);
+    if (ext_possible_) vdev::launch_ext_setup(w_, c_, st);
+    check_cuda(cudaMemsetAsync(d_singular_, 0, sizeof(int) * iterations, st), "singular reset");
+    double* cur = w_.X;
+    double* nxt = w_.Y;
+    vdev::SweepParams sp{h, h2, scene_.settings.beta, classic_ ? 1 : 0, 0, s, c_.n_pins, setup_.elastic_blocks,
+                         scene_.settings.contact_k};
+    for (int it = 0; it < iterations; ++it) {
+      sp.iter = it;
+      vdev::launch_iteration(w_, c_, cur, nxt, sp, d_singular_ + it, d_err_, st);
+      std::swap(cur, nxt);
+      if (g_.G > 0 && (it + 1) % scene_.settings.sm_period == 0)
+        vdev::launch_shape_match(w_, g_, cur, level_off_.data(), st);
+      if (probe_log) vdev::launch_residuals(w_, cur, w_.classic, d_report_partials_, report_parts_, probe_log + 8 * it, st);
+    }
+    vdev::launch_finalize_from(w_, cur, h, keep, st);
+    vdev::launch_residuals(w_, w_.X, w_.classic, d_report_partials_, report_parts_,
+                           reinterpret_cast<double*>(reinterpret_cast<char*>(d_acc_) + offsetof(StepAccum, residuals)), st);
+    if (ext_possible_ && (c_.contact_cap + c_.hp_cap) > 0) vdev::launch_penetration(w_, c_, w_.X, d_acc_, st);
+    k_end_substep<<<1, 1, 0, st>>>(d_acc_, d_singular_ + (iterations - 1));
+  }
+  k_end_step<<<1, 1, 0, st>>>(d_acc_, d_err_, c_.scalars);
+  check_cuda(cudaMemcpyAsync(h_acc_, d_acc_, sizeof(StepAccum), cudaMemcpyDeviceToHost, st), "report download");
+}
+
+static const char* kKindNames[11] = {"stretch_z", "cross_section", "surface_stretch", "bend_twist", "surface_bending",
+                                     "volume_stretch", "volume_bend_u", "volume_bend_v", "contact", "half_plane", "pin"};
+
+void Solver::check_error() {
+  const unsigned long long e = h_acc_->error;
+  if (e == vdev::kNoError) return;
+  const int stage = static_cast<int>((e >> 52) & 0xf);
+  const unsigned a = static_cast<unsigned>((e >> 32) & 0xfffff);
+  const unsigned idx = static_cast<unsigned>(e & 0xffffffffu);
+  if (stage == vdev::ERR_PREDICT) {
+    const int r = static_cast<int>(a);
+    const int n = scene_.rods[r].n;
+    if (idx == 0xfffffffeu) throw SimulationError("non-finite prediction in rod " + std::to_string(r));
+    if (idx < static_cast<unsigned>(2 * n)) {
+      if (idx % 2 == 0) throw std::invalid_argument("external force must be finite");
+      throw std::invalid_argument("external scale load must be finite");
+    }
+    throw std::invalid_argument("external torque must be finite");
+  }
+  if (stage == vdev::ERR_BROAD) throw std::invalid_argument("broad_phase: non-finite pill");
+  if (stage == vdev::ERR_CAPACITY)
+    throw std::runtime_error(a == 1 ? "collision candidate capacity exceeded" : "contact capacity exceeded");
+  // sweep: map the global block index back to its kind (solver.cpp:324-328 block order)
+  const int eb = setup_.elastic_blocks;
+  std::string kind;
+  if (static_cast<int>(idx) >= eb) {
+    const int b = static_cast<int>(idx) - eb;
+    kind = b < c_.n_pins ? "pin" : "contact_or_half_plane";
+    if (b >= c_.n_pins) {
+      int nct = 0;
+      check_cuda(cudaMemcpy(&nct, c_.scalars + vdev::SC_NCT, sizeof(int), cudaMemcpyDeviceToHost), "nct");
+      kind = (b - c_.n_pins) < nct ? "contact" : "half_plane";
+    }
+  } else {
+    int r = static_cast<int>(std::upper_bound(setup_.block_base.begin(), setup_.block_base.end(), static_cast<int>(idx)) -
+                             setup_.block_base.begin()) - 1;
+    while (r > 0 && setup_.block_base[r] == setup_.block_base[r - 1] && setup_.block_base[r] > static_cast<int>(idx)) --r;
+    const int local = static_cast<int>(idx) - setup_.block_base[r];
+    const int m = scene_.rods[r].n - 1;
+    const int ek = setup_.ekinds[r], vk = setup_.vkinds[r];
+    const int ne = popcount4(ek), nv = popcount4(vk);
+    int bits, rank;
+    const int* order;
+    static const int eorder[4] = {0, 1, 2, 5};  // StretchZ, CrossSection, SurfaceStretch, VolumeStretch
+    static const int vorder[4] = {3, 4, 6, 7};  // BendTwist, SurfaceBending, VolumeBendU, VolumeBendV
+    if (local < m * ne) {
+      bits = ek;
+      rank = local % ne;
+      order = eorder;
+    } else {
+      bits = vk;
+      rank = (local - m * ne) % nv;
+      order = vorder;
+    }
+    int seen = -1, pick = 0;
+    for (int b = 0; b < 4; ++b)
+      if (bits & (1 << b)) {
+        if (++seen == rank) {
+          pick = order[b];
+          break;
+        }
+      }
+    kind = kKindNames[pick];
+  }
+  throw SimulationError("non-finite update from constraint " + kind + " #" + std::to_string(idx));
+}
+
+Report Solver::step() {
+  const auto t0 = std::chrono::steady_clock::now();
+  const int S = scene_.settings.substeps;
+  const double h = scene_.settings.dt / S;
+  fill_animation(S, h);
+  if (use_graph_) {
+    if (!graph_exec_) {
+      cudaGraph_t graph;
+      check_cuda(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+      record_step(h, S, scene_.settings.iterations, nullptr);
+      check_cuda(cudaStreamEndCapture(stream_, &graph), "end capture");
+      std::size_t nodes = 0;
+      cudaGraphGetNodes(graph, nullptr, &nodes);
+      kernels_per_step_ = static_cast<int>(nodes);
+      check_cuda(cudaGraphInstantiate(&graph_exec_, graph, 0), "graph instantiate");
+      cudaGraphDestroy(graph);
+    }
+    check_cuda(cudaGraphLaunch(graph_exec_, stream_), "graph launch");
+  } else {
+    record_step(h, S, scene_.settings.iterations, nullptr);
+  }
+  check_cuda(cudaStreamSynchronize(stream_), "step");
+  check_cuda(cudaGetLastError(), "step kernels");
+  // time advances substep by substep exactly like the reference (solver.cpp:307,355)
+  for (int s = 0; s < S; ++s) time_ = time_ + h;
+  last_max_cand_ = h_acc_->max_candidates;
+  last_max_ct_ = h_acc_->max_contacts;
+  check_error();
+  ++step_index_;
+  Report r;
+  r.step = step_index_;
+  r.time = time_;
+  std::memcpy(r.residuals, h_acc_->residuals, sizeof(r.residuals));
+  r.max_pen = h_acc_->max_penetration;
+  r.contacts = h_acc_->contact_count;
+  r.broad = h_acc_->broad_pairs;
+  r.singular = h_acc_->skipped_singular;
+  r.dof = dof_count();
+  r.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return r;
+}
+
+std::vector<double> Solver::probe_convergence(int iterations) {
+  require(iterations >= 1, "probe needs at least one iteration");
+  const double h = scene_.settings.dt / scene_.settings.substeps;
+  if (iterations > scene_.settings.iterations) {
+    // grow the per-iteration singular counters (graph is re-captured lazily)
+    d_singular_ = dalloc<int>(iterations);
+    if (graph_exec_) {
+      cudaGraphExecDestroy(graph_exec_);
+      graph_exec_ = nullptr;
+    }
+  }
+  d_probe_ = dalloc<double>(8ull * iterations);
+  fill_animation(1, h);
+  record_step(h, 1, iterations, d_probe_);
+  std::vector<double> log(8ull * iterations);
+  check_cuda(cudaMemcpyAsync(log.data(), d_probe_, sizeof(double) * log.size(), cudaMemcpyDeviceToHost, stream_), "probe");
+  check_cuda(cudaStreamSynchronize(stream_), "probe");
+  time_ = time_ + h;
+  check_error();
+  ++step_index_;
+  return log;
+}
+
+// ---- state access (global slot order with compact element numbering) -----------------------
+
+void Solver::get_state(double* c, double* s, double* q, double* cv, double* sv, double* av) {
+  const int vpad = setup_.vpad, V = setup_.V;
+  std::vector<double> X(static_cast<std::size_t>(vdev::kStateFields) * vpad), vel(static_cast<std::size_t>(vdev::kVelFields) * vpad);
+  check_cuda(cudaMemcpyAsync(X.data(), w_.X, sizeof(double) * X.size(), cudaMemcpyDeviceToHost, stream_), "get_state");
+  check_cuda(cudaMemcpyAsync(vel.data(), w_.vel, sizeof(double) * vel.size(), cudaMemcpyDeviceToHost, stream_), "get_state");
+  check_cuda(cudaStreamSynchronize(stream_), "get_state");
+  int e = 0;
+  for (int r = 0; r < setup_.R; ++r) {
+    const int n = scene_.rods[r].n, v0 = setup_.vbase[r];
+    for (int k = 0; k < n; ++k) {
+      const int v = v0 + k;
+      if (c) {
+        c[3 * v] = X[vdev::CX * vpad + v];
+        c[3 * v + 1] = X[vdev::CY * vpad + v];
+        c[3 * v + 2] = X[vdev::CZ * vpad + v];
+      }
+      if (s) s[v] = X[vdev::S * vpad + v];
+      if (cv) {
+        cv[3 * v] = vel[vdev::VX * vpad + v];
+        cv[3 * v + 1] = vel[vdev::VY * vpad + v];
+        cv[3 * v + 2] = vel[vdev::VZ * vpad + v];
+      }
+      if (sv) sv[v] = vel[vdev::VS * vpad + v];
+      if (k < n - 1) {
+        if (q)
+          for (int f = 0; f < 4; ++f) q[4 * e + f] = X[(vdev::QW + f) * vpad + v];
+        if (av)
+          for (int f = 0; f < 3; ++f) av[3 * e + f] = vel[(vdev::WX + f) * vpad + v];
+        ++e;
+      }
+    }
+  }
+  (void)V;
+}
+
+void Solver::set_state(const double* c, const double* s, const double* q, const double* cv, const double* sv,
+                       const double* av) {
+  const int vpad = setup_.vpad;
+  std::vector<double> X(static_cast<std::size_t>(vdev::kStateFields) * vpad), vel(static_cast<std::size_t>(vdev::kVelFields) * vpad);
+  check_cuda(cudaMemcpyAsync(X.data(), w_.X, sizeof(double) * X.size(), cudaMemcpyDeviceToHost, stream_), "set_state");
+  check_cuda(cudaMemcpyAsync(vel.data(), w_.vel, sizeof(double) * vel.size(), cudaMemcpyDeviceToHost, stream_), "set_state");
+  check_cuda(cudaStreamSynchronize(stream_), "set_state");
+  int e = 0;
+  for (int r = 0; r < setup_.R; ++r) {
+    const int n = scene_.rods[r].n, v0 = setup_.vbase[r];
+    for (int k = 0; k < n; ++k) {
+      const int v = v0 + k;
+      if (c) {
+        X[vdev::CX * vpad + v] = c[3 * v];
+        X[vdev::CY * vpad + v] = c[3 * v + 1];
+        X[vdev::CZ * vpad + v] = c[3 * v + 2];
+      }
+      if (s) X[vdev::S * vpad + v] = s[v];
+      if (cv) {
+        vel[vdev::VX * vpad + v] = cv[3 * v];
+        vel[vdev::VY * vpad + v] = cv[3 * v + 1];
+        vel[vdev::VZ * vpad + v] = cv[3 * v + 2];
+      }
+      if (sv) vel[vdev::VS * vpad + v] = sv[v];
+      if (k < n - 1) {
+        if (q)
+          for (int f = 0; f < 4; ++f) X[(vdev::QW + f) * vpad + v] = q[4 * e + f];
+        if (av)
+          for (int f = 0; f < 3; ++f) vel[(vdev::WX + f) * vpad + v] = av[3 * e + f];
+        ++e;
+      }
+    }
+  }
+  check_cuda(cudaMemcpyAsync(w_.X, X.data(), sizeof(double) * X.size(), cudaMemcpyHostToDevice, stream_), "set_state");
+  check_cuda(cudaMemcpyAsync(w_.vel, vel.data(), sizeof(double) * vel.size(), cudaMemcpyHostToDevice, stream_), "set_state");
+  check_cuda(cudaStreamSynchronize(stream_), "set_state");
+}
+
+void Solver::get_rest(double* lengths, double* darb, double* grads, double* laps) {
+  const int vpad = setup_.vpad;
+  std::vector<double> es(static_cast<std::size_t>(vdev::kEStatFields) * vpad);
+  check_cuda(cudaMemcpy(es.data(), w_.estat, sizeof(double) * es.size(), cudaMemcpyDeviceToHost), "get_rest");
+  int e = 0;
+  for (int r = 0; r < setup_.R; ++r) {
+    const int m = scene_.rods[r].n - 1, v0 = setup_.vbase[r];
+    for (int k = 0; k < m; ++k, ++e) {
+      const int v = v0 + k;
+      if (lengths) lengths[e] = es[vdev::LEN * vpad + v];
+      if (grads) grads[e] = es[vdev::SGRAD * vpad + v];
+      const bool in = k + 1 < m;
+      if (darb)
+        for (int f = 0; f < 3; ++f) darb[3 * e + f] = in ? es[(vdev::DARBX + f) * vpad + v] : 0.0;
+      if (laps) laps[e] = in ? es[vdev::SLAP * vpad + v] : 0.0;
+    }
+  }
+}
+
+void Solver::set_loads(const double* fd, const uint8_t* fdr, const double* tq, const uint8_t* tqr, const double* sl,
+                       const uint8_t* slr) {
+  const int vpad = setup_.vpad, R = setup_.R;
+  std::vector<double> L(7ull * vpad, 0.0);
+  std::vector<uint8_t> flags(R, 0);
+  int e = 0;
+  for (int r = 0; r < R; ++r) {
+    const int n = scene_.rods[r].n, v0 = setup_.vbase[r];
+    if (fd && (!fdr || fdr[r])) flags[r] |= 1;
+    if (tq && (!tqr || tqr[r])) flags[r] |= 2;
+    if (sl && (!slr || slr[r])) flags[r] |= 4;
+    for (int k = 0; k < n; ++k) {
+      const int v = v0 + k;
+      if (flags[r] & 1)
+        for (int f = 0; f < 3; ++f) L[f * vpad + v] = fd[3 * v + f];
+      if (k < n - 1) {
+        if (flags[r] & 2)
+          for (int f = 0; f < 3; ++f) L[(3 + f) * vpad + v] = tq[3 * e + f];
+        if (flags[r] & 4) L[6 * vpad + v] = sl[e];
+        ++e;
+      }
+    }
+  }
+  bool any = false;
+  for (uint8_t f : flags) any = any || f;
+  upload(w_.loads, L, stream_);
+  upload(w_.load_flags, flags, stream_);
+  check_cuda(cudaStreamSynchronize(stream_), "set_loads");
+  if (w_.has_loads != (any ? 1 : 0)) {
+    w_.has_loads = any ? 1 : 0;
+    if (graph_exec_) {  // the flag is a kernel argument baked into the graph
+      cudaGraphExecDestroy(graph_exec_);
+      graph_exec_ = nullptr;
+    }
+  }
+}
+
+void Solver::energy(double* ke, double* vol, double* rest_vol) {
+  const int vpad = setup_.vpad;
+  std::vector<double> X(static_cast<std::size_t>(vdev::kStateFields) * vpad), vel(static_cast<std::size_t>(vdev::kVelFields) * vpad),
+      es(static_cast<std::size_t>(vdev::kEStatFields) * vpad);
+  check_cuda(cudaMemcpy(X.data(), w_.X, sizeof(double) * X.size(), cudaMemcpyDeviceToHost), "energy");
+  check_cuda(cudaMemcpy(vel.data(), w_.vel, sizeof(double) * vel.size(), cudaMemcpyDeviceToHost), "energy");
+  check_cuda(cudaMemcpy(es.data(), w_.estat, sizeof(double) * es.size(), cudaMemcpyDeviceToHost), "energy");
+  if (ke) {  // Solver::kinetic_energy, solver.cpp:400-418
+    double en = 0.0;
+    for (int v = 0; v < setup_.V; ++v) {
+      if (std::isinf(cw_[v])) continue;  // inv_center == 0
+      const V3 u{vel[vdev::VX * vpad + v], vel[vdev::VY * vpad + v], vel[vdev::VZ * vpad + v]};
+      en += 0.5 * cw_[v] * sqnorm(u);
+      if (!classic_) en += 0.5 * sw_[v] * vel[vdev::VS * vpad + v] * vel[vdev::VS * vpad + v];
+    }
+    for (int r = 0; r < setup_.R; ++r) {
+      const int m = scene_.rods[r].n - 1, v0 = setup_.vbase[r];
+      for (int k = 0; k < m; ++k) {
+        const int v = v0 + k;
+        const double base = es[vdev::TWB * vpad + v];
+        const V3 tw{0.25 * base, 0.25 * base, 0.5 * base};
+        const V3 u{vel[vdev::WX * vpad + v], vel[vdev::WY * vpad + v], vel[vdev::WZ * vpad + v]};
+        en += 0.5 * dot(u, cwmul(tw, u));
+      }
+    }
+    *ke = en;
+  }
+  if (vol) {  // current_volume, rod.cpp:178-187
+    double t = 0.0;
+    for (int r = 0; r < setup_.R; ++r) {
+      const RodData& rod = scene_.rods[r];
+      const int v0 = setup_.vbase[r];
+      double v = 0.0;
+      for (int e = 0; e < rod.n - 1; ++e) {
+        const double s = 0.5 * (X[vdev::S * vpad + v0 + e] + X[vdev::S * vpad + v0 + e + 1]);
+        const double rr = 0.5 * (rod.r[e] + rod.r[e + 1]);
+        const V3 a{X[vdev::CX * vpad + v0 + e], X[vdev::CY * vpad + v0 + e], X[vdev::CZ * vpad + v0 + e]};
+        const V3 b{X[vdev::CX * vpad + v0 + e + 1], X[vdev::CY * vpad + v0 + e + 1], X[vdev::CZ * vpad + v0 + e + 1]};
+        v += kPi * (s * rr) * (s * rr) * norm(b - a);
+      }
+      t += v;
+    }
+    *vol = t;
+  }
+  if (rest_vol) {  // rest_volume, rod.cpp:189-197
+    double t = 0.0;
+    for (const RodData& rod : scene_.rods) {
+      double v = 0.0;
+      for (int e = 0; e < rod.n - 1; ++e) {
+        const double s = 0.5 * (rod.rs[e] + rod.rs[e + 1]);
+        const double rr = 0.5 * (rod.r[e] + rod.r[e + 1]);
+        v += kPi * (s * rr) * (s * rr) * rod.len0[e];
+      }
+      t += v;
+    }
+    *rest_vol = t;
+  }
+}
+
+void Solver::inverse_weights(double* ic, double* is, double* it) {
+  const int vpad = setup_.vpad;
+  std::vector<double> vs(static_cast<std::size_t>(vdev::kVStatFields) * vpad), es(static_cast<std::size_t>(vdev::kEStatFields) * vpad);
+  check_cuda(cudaMemcpy(vs.data(), w_.vstat, sizeof(double) * vs.size(), cudaMemcpyDeviceToHost), "weights");
+  check_cuda(cudaMemcpy(es.data(), w_.estat, sizeof(double) * es.size(), cudaMemcpyDeviceToHost), "weights");
+  int e = 0;
+  for (int r = 0; r < setup_.R; ++r) {
+    const int n = scene_.rods[r].n, v0 = setup_.vbase[r];
+    for (int k = 0; k < n; ++k) {
+      const int v = v0 + k;
+      if (ic) ic[v] = vs[vdev::IC * vpad + v];
+      if (is) is[v] = vs[vdev::IS * vpad + v];
+      if (k < n - 1) {
+        if (it)
+          for (int f = 0; f < 3; ++f) it[3 * e + f] = es[(vdev::ITX + f) * vpad + v];
+        ++e;
+      }
+    }
+  }
+}
+
+long long Solver::contacts(long long cap, int* a, int* b, double* alpha, double* beta) {
+  if (!collide_possible_) return 0;
+  int n = 0;
+  check_cuda(cudaMemcpy(&n, c_.scalars + vdev::SC_NCT, sizeof(int), cudaMemcpyDeviceToHost), "contacts");
+  const long long k = std::min<long long>(cap, n);
+  if (k > 0) {
+    if (a) check_cuda(cudaMemcpy(a, c_.ct_a, sizeof(int) * k, cudaMemcpyDeviceToHost), "contacts");
+    if (b) check_cuda(cudaMemcpy(b, c_.ct_b, sizeof(int) * k, cudaMemcpyDeviceToHost), "contacts");
+    if (alpha) check_cuda(cudaMemcpy(alpha, c_.ct_alpha, sizeof(double) * k, cudaMemcpyDeviceToHost), "contacts");
+    if (beta) check_cuda(cudaMemcpy(beta, c_.ct_beta, sizeof(double) * k, cudaMemcpyDeviceToHost), "contacts");
+  }
+  return n;
+}
+
+std::vector<PillData> Solver::current_pills() {  // Solver::current_pills, solver.cpp:432-436
+  const int V = setup_.V;
+  std::vector<double> c(3ull * V), s(V);
+  get_state(c.data(), s.data(), nullptr, nullptr, nullptr, nullptr);
+  std::vector<PillData> out;
+  for (int r = 0; r < setup_.R; ++r) {
+    const RodData& rod = scene_.rods[r];
+    const int v0 = setup_.vbase[r];
+    for (int e = 0; e < rod.n - 1; ++e) {
+      PillData p;
+      const int v = v0 + e;
+      p.c0 = V3{c[3 * v], c[3 * v + 1], c[3 * v + 2]};
+      p.c1 = V3{c[3 * v + 3], c[3 * v + 4], c[3 * v + 5]};
+      p.r0 = s[v] * rod.r[e];
+      p.r1 = s[v + 1] * rod.r[e + 1];
+      p.rod = r;
+      p.element = e;
+      p.group = rod.group;
+      p.self_collide = rod.self_collide;
+      out.push_back(p);
+    }
+  }
+  for (const auto& kp : scene_.kpills) {
+    PillData p = kp.pill;
+    if (kp.bone >= 0) {
+      const BoneData& bone = scene_.bones[kp.bone];
+      const Q4 rot = bone.rotation_at(time_);
+      const V3 pos = bone.position_at(time_);
+      p.c0 = qrot(rot, p.c0) + pos;
+      p.c1 = qrot(rot, p.c1) + pos;
+    }
+    out.push_back(p);
+  }
+  return out;
+}
+
+}  // namespace vhost

@@ -1,0 +1,116 @@
+// The product's Solver: vrod::Solver (solver.h:54-115 of the reference) on a B200.
+// Owns the device world, replays one CUDA graph per step(), mirrors the reference's queries.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host_model.h"
+#include "kernels.cuh"
+
+namespace vhost {
+
+struct Report {
+  int step = 0, contacts = 0, broad = 0, singular = 0, dof = 0;
+  double time = 0.0;
+  double residuals[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double max_pen = 0.0;
+  double total_ms = 0.0;
+};
+
+struct DeviceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+class Solver {
+ public:
+  explicit Solver(const SceneData& scene);
+  ~Solver();
+  Solver(const Solver&) = delete;
+  Solver& operator=(const Solver&) = delete;
+
+  Report step();
+  std::vector<double> probe_convergence(int iterations);  // iterations x 8
+
+  int rod_count() const { return setup_.R; }
+  int total_vertices() const { return setup_.V; }
+  int total_elements() const { return setup_.E; }
+  int dof_count() const { return 4 * setup_.V + 3 * setup_.E; }
+  int step_index() const { return step_index_; }
+  double time() const { return time_; }
+  int bundle_count() const { return static_cast<int>(setup_.groups.size()); }
+  int elastic_blocks() const { return setup_.elastic_blocks; }
+  const SceneData& scene() const { return scene_; }
+
+  // global slot order of the C-ABI (compact element numbering)
+  void get_state(double* c, double* s, double* q, double* cv, double* sv, double* av);
+  void set_state(const double* c, const double* s, const double* q, const double* cv, const double* sv,
+                 const double* av);
+  void get_rest(double* lengths, double* darb, double* grads, double* laps);
+  void set_loads(const double* fd, const uint8_t* fdr, const double* tq, const uint8_t* tqr, const double* sl,
+                 const uint8_t* slr);
+  void energy(double* ke, double* vol, double* rest_vol);
+  void inverse_weights(double* ic, double* is, double* it);
+  long long contacts(long long cap, int* a, int* b, double* alpha, double* beta);
+  std::vector<PillData> current_pills();
+
+  // diagnostics for bench.py
+  long long last_max_candidates() const { return last_max_cand_; }
+  long long last_max_contacts() const { return last_max_ct_; }
+  cudaStream_t stream() const { return stream_; }
+  int kernels_per_step() const { return kernels_per_step_; }
+  void set_graphs(bool on) { use_graph_ = on; }
+
+ private:
+  void upload_static();
+  void fill_animation(int substeps, double h);
+  void record_step(double h, int substeps, int iterations, double* probe_log);
+  void check_error();
+  void download_state_cache();
+
+  SceneData scene_;
+  Setup setup_;
+  bool classic_ = false;
+  bool collide_possible_ = false;
+  bool ext_possible_ = false;
+  double time_ = 0.0;
+  int step_index_ = 0;
+  int kernels_per_step_ = 0;
+  bool use_graph_ = true;
+
+  cudaStream_t stream_ = nullptr;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  std::vector<void*> allocs_;
+  template <typename T>
+  T* dalloc(std::size_t n);
+
+  vdev::World w_;
+  vdev::Collide c_;
+  vdev::Groups g_;
+  vdev::AnimLayout al_;
+  std::vector<int> level_off_;
+  std::vector<double> cw_, sw_;          // layout weights (host copies)
+  double* d_anim_ = nullptr;
+  double* h_anim_ = nullptr;             // pinned
+  int* d_pm_slot_ = nullptr;
+  int* d_act_rod_off_ = nullptr;
+  int* d_act_list_ = nullptr;
+  int* d_act_rods_ = nullptr;
+  double* d_act_applied_ = nullptr;      // applied amounts + static (factor, first, last)
+  int n_act_rods_ = 0;
+  vdev::StepAccum* d_acc_ = nullptr;
+  vdev::StepAccum* h_acc_ = nullptr;     // pinned
+  int* d_singular_ = nullptr;            // per iteration
+  unsigned long long* d_err_ = nullptr;
+  double* d_report_partials_ = nullptr;
+  int report_parts_ = 0;
+  double* d_probe_ = nullptr;
+  long long last_max_cand_ = 0, last_max_ct_ = 0;
+};
+
+void check_cuda(cudaError_t e, const char* what);
+
+}  // namespace vhost
