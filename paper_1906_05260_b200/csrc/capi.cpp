@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "../../include/vrod_bench.h"
 #include "../../include/vrod_capi.h"
 #include "host_model.h"
 #include "solver.h"
@@ -337,6 +338,26 @@ int vrod_find_contacts(int64_t n, const vrod_pill* pills, int64_t np, const int3
                        double* alpha, double* beta, double* dist) {
   return guarded([&] { *count = gpu_find_contacts(n, pills, np, pairs, iters, nw, wk, wa, cap, pa, pb, alpha, beta, dist); });
 }
+int vrod_bench_run(vrod_solver* h, int32_t steps, int64_t flush_bytes, double* device_ms, int64_t* kernels) {
+  return guarded([&] {
+    *device_ms = h->s->bench_run(steps, flush_bytes);
+    if (kernels) *kernels = h->s->kernel_nodes_per_step();
+  });
+}
+int vrod_bench_kernel_times(vrod_solver* h, int32_t steps, double* ms, int64_t* launches) {
+  return guarded([&] {
+    long long l[Solver::kCategories];
+    h->s->kernel_times(steps, ms, l);
+    for (int c = 0; c < Solver::kCategories; ++c) launches[c] = l[c];
+  });
+}
+int vrod_bench_last_counts(vrod_solver* h, int64_t* cand, int64_t* ct) {
+  return guarded([&] {
+    if (cand) *cand = h->s->last_max_candidates();
+    if (ct) *ct = h->s->last_max_contacts();
+  });
+}
+
 uint64_t vrod_pair_key(const vrod_pill* a, const vrod_pill* b) {  // collision.cpp:240-249
   auto id = [](const vrod_pill& p) {
     return (static_cast<uint32_t>(p.rod + 1) << 16) | (static_cast<uint32_t>(p.element + 1) & 0xffffu);

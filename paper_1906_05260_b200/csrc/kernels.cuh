@@ -162,6 +162,10 @@ void launch_deepest(long long n, const double* a, const double* b, int iters, co
 void launch_ext_setup(const World& w, Collide& c, cudaStream_t st);
 void launch_iteration(const World& w, Collide& c, const double* X, double* Y, const SweepParams& sp,
                       int* singular_counter, unsigned long long* err, cudaStream_t st);
+void launch_ext_solve(const World& w, Collide& c, const double* X, const SweepParams& sp, int* singular_counter,
+                      unsigned long long* err, cudaStream_t st);
+void launch_rod_sweep(const World& w, Collide& c, const double* X, double* Y, const SweepParams& sp,
+                      int* singular_counter, unsigned long long* err, cudaStream_t st);
 void launch_residuals(const World& w, const double* X, int classic, double* partials, int parts, double* out8,
                       cudaStream_t st);
 void launch_penetration(const World& w, Collide& c, const double* X, StepAccum* acc, cudaStream_t st);

@@ -283,6 +283,7 @@ Solver::Solver(const SceneData& scene) : scene_(scene) {
 Solver::~Solver() {
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (stream_) cudaStreamSynchronize(stream_);
+  if (flush_buf_) cudaFree(flush_buf_);
   for (void* p : allocs_) cudaFree(p);
   if (h_anim_) cudaFreeHost(h_anim_);
   if (h_acc_) cudaFreeHost(h_acc_);
@@ -544,41 +545,73 @@ __global__ void k_end_step(StepAccum* acc, const unsigned long long* err, const 
 }
 
 // Records every kernel of one step (or, with probe_log, one probe substep) on stream_.
-void Solver::record_step(double h, int substeps, int iterations, double* probe_log) {
+void Solver::record_step(double h, int substeps, int iterations, double* probe_log, Prof* prof) {
   cudaStream_t st = stream_;
   const double h2 = h * h;
   const double keep = 1.0 - scene_.settings.damping;
   const double g[3] = {scene_.settings.g.x, scene_.settings.g.y, scene_.settings.g.z};
+  // profiling brackets (direct launches only): an event pair per kernel category
+  auto begin = [&](int cat) {
+    if (!prof) return;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+    prof->cat.push_back(cat);
+    prof->ev.push_back(a);
+    prof->ev.push_back(b);
+  };
+  auto end = [&]() {
+    if (prof) cudaEventRecord(prof->ev.back(), st);
+  };
   k_init_acc<<<1, 1, 0, st>>>(d_acc_, d_err_, c_.scalars);
   check_cuda(cudaMemcpyAsync(d_anim_, h_anim_, sizeof(double) * al_.stride * substeps, cudaMemcpyHostToDevice, st),
              "anim upload");
   for (int s = 0; s < substeps; ++s) {
     const double* anim = d_anim_ + static_cast<std::size_t>(al_.stride) * s;
+    begin(CAT_PREDICT);
     vdev::launch_animate(w_, anim, al_, d_pm_slot_, d_act_rod_off_, d_act_list_, d_act_applied_, d_act_rods_,
                          n_act_rods_, st);
     vdev::launch_predict(w_, anim, al_, g, h, s, d_err_, st);
     check_cuda(cudaMemsetAsync(w_.lam, 0, sizeof(double) * vdev::kLamFields * w_.vpad, st), "lam reset");
+    end();
+    begin(CAT_COLLIDE);
     if (c_.P >= 1) vdev::launch_collide(w_, c_, anim, al_, s, d_err_, d_acc_, collide_possible_ ? 1 : 0, st);
     vdev::launch_halfplanes(w_, c_, st);
+    end();
+    begin(CAT_EXT_SETUP);
     if (ext_possible_) vdev::launch_ext_setup(w_, c_, st);
     check_cuda(cudaMemsetAsync(d_singular_, 0, sizeof(int) * iterations, st), "singular reset");
+    end();
     double* cur = w_.X;
     double* nxt = w_.Y;
     vdev::SweepParams sp{h, h2, scene_.settings.beta, classic_ ? 1 : 0, 0, s, c_.n_pins, setup_.elastic_blocks,
                          scene_.settings.contact_k};
     for (int it = 0; it < iterations; ++it) {
       sp.iter = it;
-      vdev::launch_iteration(w_, c_, cur, nxt, sp, d_singular_ + it, d_err_, st);
+      if (c_.ext_cap > 0) {
+        begin(CAT_EXT_SOLVE);
+        vdev::launch_ext_solve(w_, c_, cur, sp, d_singular_ + it, d_err_, st);
+        end();
+      }
+      begin(CAT_ROD_SWEEP);
+      vdev::launch_rod_sweep(w_, c_, cur, nxt, sp, d_singular_ + it, d_err_, st);
+      end();
       std::swap(cur, nxt);
-      if (g_.G > 0 && (it + 1) % scene_.settings.sm_period == 0)
+      if (g_.G > 0 && (it + 1) % scene_.settings.sm_period == 0) {
+        begin(CAT_SHAPE);
         vdev::launch_shape_match(w_, g_, cur, level_off_.data(), st);
+        end();
+      }
       if (probe_log) vdev::launch_residuals(w_, cur, w_.classic, d_report_partials_, report_parts_, probe_log + 8 * it, st);
     }
+    begin(CAT_REPORT);
     vdev::launch_finalize_from(w_, cur, h, keep, st);
     vdev::launch_residuals(w_, w_.X, w_.classic, d_report_partials_, report_parts_,
                            reinterpret_cast<double*>(reinterpret_cast<char*>(d_acc_) + offsetof(StepAccum, residuals)), st);
     if (ext_possible_ && (c_.contact_cap + c_.hp_cap) > 0) vdev::launch_penetration(w_, c_, w_.X, d_acc_, st);
     k_end_substep<<<1, 1, 0, st>>>(d_acc_, d_singular_ + (iterations - 1));
+    end();
   }
   k_end_step<<<1, 1, 0, st>>>(d_acc_, d_err_, c_.scalars);
   check_cuda(cudaMemcpyAsync(h_acc_, d_acc_, sizeof(StepAccum), cudaMemcpyDeviceToHost, st), "report download");
@@ -651,46 +684,123 @@ void Solver::check_error() {
   throw SimulationError("non-finite update from constraint " + kind + " #" + std::to_string(idx));
 }
 
+void Solver::ensure_graph() {
+  if (graph_exec_) return;
+  const int S = scene_.settings.substeps;
+  const double h = scene_.settings.dt / S;
+  cudaGraph_t graph;
+  check_cuda(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+  record_step(h, S, scene_.settings.iterations, nullptr);
+  check_cuda(cudaStreamEndCapture(stream_, &graph), "end capture");
+  std::size_t n = 0;
+  cudaGraphGetNodes(graph, nullptr, &n);
+  std::vector<cudaGraphNode_t> nodes(n);
+  cudaGraphGetNodes(graph, nodes.data(), &n);
+  int kernels = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    cudaGraphNodeGetType(nd, &t);
+    if (t == cudaGraphNodeTypeKernel) ++kernels;
+  }
+  kernels_per_step_ = kernels;
+  check_cuda(cudaGraphInstantiate(&graph_exec_, graph, 0), "graph instantiate");
+  cudaGraphDestroy(graph);
+}
+
+long long Solver::kernel_nodes_per_step() {
+  ensure_graph();
+  return kernels_per_step_;
+}
+
+int Solver::contact_count_last() { return h_acc_->contact_count; }
+
+double Solver::bench_run(int steps, long long flush_bytes) {
+  const int S = scene_.settings.substeps;
+  const double h = scene_.settings.dt / S;
+  ensure_graph();
+  if (flush_bytes > 0 && flush_bytes_ < flush_bytes) {
+    if (flush_buf_) cudaFree(flush_buf_);
+    check_cuda(cudaMalloc(&flush_buf_, flush_bytes), "flush buffer");
+    flush_bytes_ = flush_bytes;
+  }
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  double total = 0.0;
+  for (int k = 0; k < steps; ++k) {
+    fill_animation(S, h);
+    if (flush_bytes > 0) check_cuda(cudaMemsetAsync(flush_buf_, k & 0xff, flush_bytes, stream_), "L2 flush");
+    cudaEventRecord(a, stream_);
+    check_cuda(cudaGraphLaunch(graph_exec_, stream_), "graph launch");
+    cudaEventRecord(b, stream_);
+    Report r;
+    finish_step(h, S, &r);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    total += ms;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return total;
+}
+
+void Solver::kernel_times(int steps, double* ms, long long* launches) {
+  const int S = scene_.settings.substeps;
+  const double h = scene_.settings.dt / S;
+  for (int c = 0; c < kCategories; ++c) {
+    ms[c] = 0.0;
+    launches[c] = 0;
+  }
+  for (int k = 0; k < steps; ++k) {
+    Prof prof;
+    fill_animation(S, h);
+    record_step(h, S, scene_.settings.iterations, nullptr, &prof);
+    Report r;
+    finish_step(h, S, &r);
+    for (std::size_t i = 0; i < prof.cat.size(); ++i) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, prof.ev[2 * i], prof.ev[2 * i + 1]);
+      ms[prof.cat[i]] += t;
+      launches[prof.cat[i]] += 1;
+      cudaEventDestroy(prof.ev[2 * i]);
+      cudaEventDestroy(prof.ev[2 * i + 1]);
+    }
+  }
+}
+
+void Solver::finish_step(double h, int substeps, Report* out) {
+  check_cuda(cudaStreamSynchronize(stream_), "step");
+  check_cuda(cudaGetLastError(), "step kernels");
+  for (int s = 0; s < substeps; ++s) time_ = time_ + h;
+  last_max_cand_ = h_acc_->max_candidates;
+  last_max_ct_ = h_acc_->max_contacts;
+  check_error();
+  ++step_index_;
+  out->step = step_index_;
+  out->time = time_;
+  std::memcpy(out->residuals, h_acc_->residuals, sizeof(out->residuals));
+  out->max_pen = h_acc_->max_penetration;
+  out->contacts = h_acc_->contact_count;
+  out->broad = h_acc_->broad_pairs;
+  out->singular = h_acc_->skipped_singular;
+  out->dof = dof_count();
+}
+
 Report Solver::step() {
   const auto t0 = std::chrono::steady_clock::now();
   const int S = scene_.settings.substeps;
   const double h = scene_.settings.dt / S;
   fill_animation(S, h);
   if (use_graph_) {
-    if (!graph_exec_) {
-      cudaGraph_t graph;
-      check_cuda(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
-      record_step(h, S, scene_.settings.iterations, nullptr);
-      check_cuda(cudaStreamEndCapture(stream_, &graph), "end capture");
-      std::size_t nodes = 0;
-      cudaGraphGetNodes(graph, nullptr, &nodes);
-      kernels_per_step_ = static_cast<int>(nodes);
-      check_cuda(cudaGraphInstantiate(&graph_exec_, graph, 0), "graph instantiate");
-      cudaGraphDestroy(graph);
-    }
+    ensure_graph();
     check_cuda(cudaGraphLaunch(graph_exec_, stream_), "graph launch");
   } else {
     record_step(h, S, scene_.settings.iterations, nullptr);
   }
-  check_cuda(cudaStreamSynchronize(stream_), "step");
-  check_cuda(cudaGetLastError(), "step kernels");
-  // time advances substep by substep exactly like the reference (solver.cpp:307,355)
-  for (int s = 0; s < S; ++s) time_ = time_ + h;
-  last_max_cand_ = h_acc_->max_candidates;
-  last_max_ct_ = h_acc_->max_contacts;
-  check_error();
-  ++step_index_;
-  Report r;
-  r.step = step_index_;
-  r.time = time_;
-  std::memcpy(r.residuals, h_acc_->residuals, sizeof(r.residuals));
-  r.max_pen = h_acc_->max_penetration;
-  r.contacts = h_acc_->contact_count;
-  r.broad = h_acc_->broad_pairs;
-  r.singular = h_acc_->skipped_singular;
-  r.dof = dof_count();
-  r.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  return r;
+  Report rr;
+  finish_step(h, S, &rr);
+  rr.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return rr;
 }
 
 std::vector<double> Solver::probe_convergence(int iterations) {

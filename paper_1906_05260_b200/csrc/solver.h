@@ -57,6 +57,17 @@ class Solver {
   long long contacts(long long cap, int* a, int* b, double* alpha, double* beta);
   std::vector<PillData> current_pills();
 
+  // ---- bench / profiling (include/vrod_bench.h) ----
+  enum Category { CAT_PREDICT = 0, CAT_COLLIDE, CAT_EXT_SETUP, CAT_EXT_SOLVE, CAT_ROD_SWEEP, CAT_SHAPE, CAT_REPORT,
+                  kCategories };
+  // steps graph replays, each bracketed by CUDA events on the solver stream; an L2-flushing
+  // memset of flush_bytes runs (untimed) before every step. Returns summed device ms.
+  double bench_run(int steps, long long flush_bytes);
+  // steps direct-launched steps with event pairs around each kernel category.
+  void kernel_times(int steps, double* ms, long long* launches);
+  long long kernel_nodes_per_step();
+  int contact_count_last();
+
   // diagnostics for bench.py
   long long last_max_candidates() const { return last_max_cand_; }
   long long last_max_contacts() const { return last_max_ct_; }
@@ -65,9 +76,18 @@ class Solver {
   void set_graphs(bool on) { use_graph_ = on; }
 
  private:
+  struct Prof {
+    std::vector<int> cat;
+    std::vector<cudaEvent_t> ev;  // pairs
+    std::vector<int> launches;
+  };
   void upload_static();
   void fill_animation(int substeps, double h);
-  void record_step(double h, int substeps, int iterations, double* probe_log);
+  void record_step(double h, int substeps, int iterations, double* probe_log, Prof* prof = nullptr);
+  void ensure_graph();
+  void finish_step(double h, int substeps, Report* out);
+  void* flush_buf_ = nullptr;
+  long long flush_bytes_ = 0;
   void check_error();
   void download_state_cache();
 

@@ -1054,12 +1054,22 @@ void launch_ext_setup(const World& w, Collide& c, cudaStream_t st) {
   k_ext_sort<<<(w.V + kThreads - 1) / kThreads, kThreads, 0, st>>>(c, w.V);
 }
 
-void launch_iteration(const World& w, Collide& c, const double* X, double* Y, const SweepParams& sp,
+void launch_ext_solve(const World& w, Collide& c, const double* X, const SweepParams& sp, int* singular_counter,
+                      unsigned long long* err, cudaStream_t st) {
+  if (c.ext_cap > 0) k_ext_solve<<<grid_for(c.ext_cap), kThreads, 0, st>>>(w, c, X, sp, singular_counter, err);
+}
+
+void launch_rod_sweep(const World& w, Collide& c, const double* X, double* Y, const SweepParams& sp,
                       int* singular_counter, unsigned long long* err, cudaStream_t st) {
   const int has_ext = c.ext_cap > 0 ? 1 : 0;
-  if (has_ext) k_ext_solve<<<grid_for(c.ext_cap), kThreads, 0, st>>>(w, c, X, sp, singular_counter, err);
   const int blocks = (w.V + (kSweepThreads - 2) - 1) / (kSweepThreads - 2);
   k_rod_sweep<<<blocks, kSweepThreads, 0, st>>>(w, c, X, Y, sp, singular_counter, err, has_ext);
+}
+
+void launch_iteration(const World& w, Collide& c, const double* X, double* Y, const SweepParams& sp,
+                      int* singular_counter, unsigned long long* err, cudaStream_t st) {
+  launch_ext_solve(w, c, X, sp, singular_counter, err, st);
+  launch_rod_sweep(w, c, X, Y, sp, singular_counter, err, st);
 }
 
 void launch_residuals(const World& w, const double* X, int classic, double* partials, int parts, double* out8,
