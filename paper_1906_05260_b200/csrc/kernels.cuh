@@ -129,6 +129,8 @@ struct SweepParams {
   int n_pins;
   int elastic_blocks;  // first external block index in the reference's block list
   double contact_k;    // settings.contact_stiffness
+  const double* lam_in;  // elastic multipliers before this sweep (kLamFields x vpad)
+  double* lam_out;       // after this sweep (ping-pong partner)
 };
 
 // scan.cu

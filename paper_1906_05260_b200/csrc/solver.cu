@@ -88,7 +88,7 @@ Solver::Solver(const SceneData& scene) : scene_(scene) {
   w_.Y = dalloc<double>(static_cast<std::size_t>(vdev::kStateFields) * vpad);
   w_.prev = dalloc<double>(static_cast<std::size_t>(vdev::kStateFields) * vpad);
   w_.vel = dalloc<double>(static_cast<std::size_t>(vdev::kVelFields) * vpad);
-  w_.lam = dalloc<double>(static_cast<std::size_t>(vdev::kLamFields) * vpad);
+  w_.lam = dalloc<double>(2ull * vdev::kLamFields * vpad);  // ping-pong pair
   w_.loads = dalloc<double>(7ull * vpad);
   int nbones_total = 0;
   for (const auto& rod : scene_.rods) nbones_total += static_cast<int>(rod.bones.size());
@@ -586,9 +586,13 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
     double* cur = w_.X;
     double* nxt = w_.Y;
     vdev::SweepParams sp{h, h2, scene_.settings.beta, classic_ ? 1 : 0, 0, s, c_.n_pins, setup_.elastic_blocks,
-                         scene_.settings.contact_k};
+                         scene_.settings.contact_k, nullptr, nullptr};
+    double* lam_a = w_.lam;
+    double* lam_b = w_.lam + static_cast<std::size_t>(vdev::kLamFields) * w_.vpad;
     for (int it = 0; it < iterations; ++it) {
       sp.iter = it;
+      sp.lam_in = (it & 1) ? lam_b : lam_a;
+      sp.lam_out = (it & 1) ? lam_a : lam_b;
       if (c_.ext_cap > 0) {
         begin(CAT_EXT_SOLVE);
         vdev::launch_ext_solve(w_, c_, cur, sp, d_singular_ + it, d_err_, st);

@@ -420,6 +420,13 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
   unsigned long long bad = kNoError;
   const int ne = __popc(ek), nv = __popc(vk);
   const int bbase = valid ? w.rod_block_base[r] : 0;
+  // Multipliers are ping-ponged like the state: every CTA reads lam_in (its halo blocks
+  // included) and only the owner of a slot writes lam_out, so no CTA can observe another's
+  // update within the sweep. A singular block keeps its multiplier (constraints.cpp:511-514).
+  auto keep_lam = [&](int f0, int nf) {
+    if (!owned) return;
+    for (int f = f0; f < f0 + nf; ++f) sp.lam_out[f * (long long)vp + p] = sp.lam_in[f * (long long)vp + p];
+  };
 
   if (has_el) {
     const V3 c0{sc[0][li], sc[1][li], sc[2][li]}, c1{sc[0][li + 1], sc[1][li + 1], sc[2][li + 1]};
@@ -452,7 +459,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
       }
       const double kinv = inverse_stiffness(F(w.estat, KSZ, vp, p));
       double rhs[3], dl[3];
-      const double lam[3] = {F(w.lam, L_SZ0, vp, p), F(w.lam, L_SZ1, vp, p), F(w.lam, L_SZ2, vp, p)};
+      const double lam[3] = {F(sp.lam_in, L_SZ0, vp, p), F(sp.lam_in, L_SZ1, vp, p), F(sp.lam_in, L_SZ2, vp, p)};
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
         M[d][d] = M[d][d] + kinv;
@@ -472,7 +479,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
         own_flags |= 1;
         ff |= F_SZ;
         if (owned) {
-          double* L = w.lam;
+          double* L = sp.lam_out;
           L[L_SZ0 * (long long)vp + p] = lam[0] + dl[0];
           L[L_SZ1 * (long long)vp + p] = lam[1] + dl[1];
           L[L_SZ2 * (long long)vp + p] = lam[2] + dl[2];
@@ -482,6 +489,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
         }
       } else {
         ++nsing;
+        keep_lam(L_SZ0, 3);
       }
     }
     // --- CrossSection (:120-129) and SurfaceStretch (:130-138), dim 1
@@ -491,7 +499,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
       if (is0 != 0.0) M = M + (h2 * is0 * 0.5) * 0.5;
       if (is1 != 0.0) M = M + (h2 * is1 * 0.5) * 0.5;
       const double kinv = inverse_stiffness(F(w.estat, KCS, vp, p));
-      const double lam = F(w.lam, L_CS, vp, p);
+      const double lam = F(sp.lam_in, L_CS, vp, p);
       M = M + kinv;
       if (M > 1e-250) {
         const double dl = beta * (W - kinv * lam) / M;
@@ -500,12 +508,13 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
         own_flags |= 4;
         ff |= F_CS;
         if (owned) {
-          w.lam[L_CS * (long long)vp + p] = lam + dl;
+          sp.lam_out[L_CS * (long long)vp + p] = lam + dl;
           if (!(isfinite(dl) && isfinite(own_ds0_cs) && isfinite(f.cs_ds1)))
             bad = umin64(bad, err_code(sp.substep, ERR_SWEEP, sp.iter, lbase + rank_of(ek, EK_CS)));
         }
       } else {
         ++nsing;
+        keep_lam(L_CS, 1);
       }
     }
     if (ek & EK_SS) {
@@ -516,7 +525,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
       if (is0 != 0.0) M = M + (h2 * is0 * j0) * j0;
       if (is1 != 0.0) M = M + (h2 * is1 * j1) * j1;
       const double kinv = inverse_stiffness(F(w.estat, KSS, vp, p));
-      const double lam = F(w.lam, L_SS, vp, p);
+      const double lam = F(sp.lam_in, L_SS, vp, p);
       M = M + kinv;
       if (M > 1e-250) {
         const double dl = beta * (W - kinv * lam) / M;
@@ -525,12 +534,13 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
         own_flags |= 8;
         ff |= F_SS;
         if (owned) {
-          w.lam[L_SS * (long long)vp + p] = lam + dl;
+          sp.lam_out[L_SS * (long long)vp + p] = lam + dl;
           if (!(isfinite(dl) && isfinite(own_ds0_ss) && isfinite(f.ss_ds1)))
             bad = umin64(bad, err_code(sp.substep, ERR_SWEEP, sp.iter, lbase + rank_of(ek, EK_SS)));
         }
       } else {
         ++nsing;
+        keep_lam(L_SS, 1);
       }
     }
     // --- VolumeStretch (:169-188), dim 3
@@ -565,7 +575,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
       }
       const double kinv = inverse_stiffness(F(w.estat, KVS, vp, p));
       double rhs[3], dl[3];
-      const double lam[3] = {F(w.lam, L_VS0, vp, p), F(w.lam, L_VS1, vp, p), F(w.lam, L_VS2, vp, p)};
+      const double lam[3] = {F(sp.lam_in, L_VS0, vp, p), F(sp.lam_in, L_VS1, vp, p), F(sp.lam_in, L_VS2, vp, p)};
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
         M[d][d] = M[d][d] + kinv;
@@ -588,7 +598,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
         own_flags |= 2;
         ff |= F_VS;
         if (owned) {
-          double* L = w.lam;
+          double* L = sp.lam_out;
           L[L_VS0 * (long long)vp + p] = lam[0] + dl[0];
           L[L_VS1 * (long long)vp + p] = lam[1] + dl[1];
           L[L_VS2 * (long long)vp + p] = lam[2] + dl[2];
@@ -599,6 +609,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
         }
       } else {
         ++nsing;
+        keep_lam(L_VS0, 3);
       }
     }
   }
@@ -656,7 +667,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
       }
       const double kinv[3] = {inverse_stiffness(F(w.estat, KBT0, vp, p)), inverse_stiffness(F(w.estat, KBT1, vp, p)),
                               inverse_stiffness(F(w.estat, KBT2, vp, p))};
-      const double lam[3] = {F(w.lam, L_BT0, vp, p), F(w.lam, L_BT1, vp, p), F(w.lam, L_BT2, vp, p)};
+      const double lam[3] = {F(sp.lam_in, L_BT0, vp, p), F(sp.lam_in, L_BT1, vp, p), F(sp.lam_in, L_BT2, vp, p)};
       double rhs[3], dl[3];
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
@@ -684,7 +695,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
         th_sum = th_sum + tb;
         ++th_cnt;
         if (owned) {
-          double* L = w.lam;
+          double* L = sp.lam_out;
           L[L_BT0 * (long long)vp + p] = lam[0] + dl[0];
           L[L_BT1 * (long long)vp + p] = lam[1] + dl[1];
           L[L_BT2 * (long long)vp + p] = lam[2] + dl[2];
@@ -693,6 +704,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
         }
       } else {
         ++nsing;
+        keep_lam(L_BT0, 3);
       }
     }
     // --- SurfaceBending (:156-168), dim 1
@@ -706,7 +718,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
       if (is0 != 0.0) M = M + (h2 * is0 * j0) * j0;
       if (isp != 0.0) M = M + (h2 * isp * jp) * jp;
       const double kinv = inverse_stiffness(F(w.estat, KSB, vp, p));
-      const double lam = F(w.lam, L_SB, vp, p);
+      const double lam = F(sp.lam_in, L_SB, vp, p);
       M = M + kinv;
       if (M > 1e-250) {
         const double dl = beta * (W - kinv * lam) / M;
@@ -717,12 +729,13 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
         ff |= F_SB;
         own_flags |= 32;
         if (owned) {
-          w.lam[L_SB * (long long)vp + p] = lam + dl;
+          sp.lam_out[L_SB * (long long)vp + p] = lam + dl;
           if (!(isfinite(dl) && isfinite(bk.sb_dsm) && isfinite(own_ds_sb) && isfinite(f.sb_dsp)))
             bad = umin64(bad, err_code(sp.substep, ERR_SWEEP, sp.iter, lbase + rank_of(vk, VK_SB)));
         }
       } else {
         ++nsing;
+        keep_lam(L_SB, 1);
       }
     }
     // --- VolumeBendU / V (:189-214), dim 1
@@ -747,7 +760,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
       M = M + (((h2 * jb[0]) * itb.x * jb[0] + (h2 * jb[1]) * itb.y * jb[1]) + (h2 * jb[2]) * itb.z * jb[2]);
       const double kinv = inverse_stiffness(F(w.estat, KVB, vp, p));
       const int lf = cc == 0 ? L_VBU : L_VBV;
-      const double lam = F(w.lam, lf, vp, p);
+      const double lam = F(sp.lam_in, lf, vp, p);
       M = M + kinv;
       if (M > 1e-250) {
         const double dl = beta * (W - kinv * lam) / M;
@@ -772,12 +785,13 @@ __global__ void __launch_bounds__(kSweepThreads) k_rod_sweep(World w, Collide c,
         th_sum = th_sum + tb;
         ++th_cnt;
         if (owned) {
-          w.lam[lf * (long long)vp + p] = lam + dl;
+          sp.lam_out[lf * (long long)vp + p] = lam + dl;
           if (!(isfinite(dl) && isfinite(ds) && finite3(ta) && finite3(tb)))
             bad = umin64(bad, err_code(sp.substep, ERR_SWEEP, sp.iter, lbase + rank_of(vk, bit)));
         }
       } else {
         ++nsing;
+        keep_lam(lf, 1);
       }
     }
   }

@@ -172,3 +172,24 @@ SCENES = {
     "mini_forest": mini_forest,
     "C1": workloads.c1_single_rod,
 }
+
+
+def pile_noplane(lib) -> Scene:
+    s = pile(lib)
+    s.planes.clear()
+    return s
+
+
+def pile_nogravity(lib) -> Scene:
+    s = pile(lib)
+    s.settings.gravity = (0.0, 0.0, 0.0)
+    return s
+
+
+def pile_bottom_only(lib) -> Scene:
+    s = pile(lib)
+    s.rods = s.rods[:15]
+    return s
+
+
+DEBUG_SCENES = {"pile_noplane": pile_noplane, "pile_nogravity": pile_nogravity, "pile_bottom_only": pile_bottom_only}

@@ -15,13 +15,19 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 import paper_1906_05260_b200 as pb  # noqa: E402
 from paper_1906_05260_b200 import capi  # noqa: E402
 from paper_1906_05260_b200.handle import SolverHandle  # noqa: E402
-from scenes import SCENES  # noqa: E402
+from scenes import DEBUG_SCENES, SCENES  # noqa: E402
+SCENES = {**SCENES, **DEBUG_SCENES}
 
 
 def main():
     orc = capi.bind(C.CDLL(os.path.join(ROOT, "oracle", "lib", "libvrod_oracle.so")))
-    gpu = pb.library()
-    names = sys.argv[1:] or sorted(SCENES)
+    args = sys.argv[1:]
+    if args and args[0] == "--strict":
+        gpu = capi.bind(C.CDLL(os.path.join(ROOT, "paper_1906_05260_b200", "lib", "libvrod_b200_strict.so")))
+        args = args[1:]
+    else:
+        gpu = pb.library()
+    names = args or sorted(SCENES)
     for name in names:
         scene = SCENES[name](orc)
         try:
