@@ -8,7 +8,9 @@ import subprocess
 from . import capi
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libvrod_b200.so")
+# VROD_B200_VARIANT=fast selects the FMA-contracted build of the same kernels (experiments).
+LIB_PATH = os.path.join(PKG_DIR, "lib", "libvrod_b200_fast.so" if os.environ.get("VROD_B200_VARIANT") == "fast"
+                        else "libvrod_b200.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 
 _lib = None

@@ -22,8 +22,8 @@ SCENES = {**SCENES, **DEBUG_SCENES}
 def main():
     orc = capi.bind(C.CDLL(os.path.join(ROOT, "oracle", "lib", "libvrod_oracle.so")))
     args = sys.argv[1:]
-    if args and args[0] == "--strict":
-        gpu = capi.bind(C.CDLL(os.path.join(ROOT, "paper_1906_05260_b200", "lib", "libvrod_b200_strict.so")))
+    if args and args[0] == "--fast":
+        gpu = capi.bind(C.CDLL(os.path.join(ROOT, "paper_1906_05260_b200", "lib", "libvrod_b200_fast.so")))
         args = args[1:]
     else:
         gpu = pb.library()
