@@ -284,6 +284,38 @@ def settings_to_c(s: SolverSettings) -> capi.Settings:
                          s.velocity_damping, int(bool(s.deterministic)), int(s.scale_mode))
 
 
+def _check_sizes(rod: Rod, r: int) -> None:
+    """The array-size checks of RodRestPose::validate (rod.cpp:15-28) and Scene::validate
+    (scene.cpp:71-80) that a pointer-based C-ABI cannot see, with the reference's messages."""
+    rest, st = rod.rest, rod.state
+    n = rest.vertex_count()
+    m = int(np.asarray(rest.frames).reshape(-1, 4).shape[0])
+    sizes = lambda a: int(np.asarray(a).shape[0]) if np.ndim(a) else 1  # noqa: E731
+    if n < 2:
+        raise InvalidArgument("rest pose: need at least 2 vertices")
+    if m != n - 1:
+        raise InvalidArgument("rest pose: frame count must be vertex count - 1")
+    for a, what in ((rest.scales, "scales"), (rest.radii, "radii")):
+        if sizes(a) != n:
+            raise InvalidArgument(f"rest pose: {what} size mismatch")
+    for a, what in ((rest.lengths, "lengths"), (rest.initial_lengths, "initial lengths"),
+                    (rest.tangent_dots, "tangent dots"), (rest.scale_grads, "scale grads")):
+        if sizes(a) != m:
+            raise InvalidArgument(f"rest pose: {what} size mismatch")
+    if sizes(rest.darboux) != max(0, m - 1):
+        raise InvalidArgument("rest pose: darboux size mismatch")
+    if sizes(rest.scale_laplacians) != max(0, m - 1):
+        raise InvalidArgument("rest pose: scale laplacians size mismatch")
+    if sizes(rod.pinned) != n:
+        raise InvalidArgument(f"rod {r} pinned flags size")
+    if sizes(st.centers) != n or sizes(st.scales) != n or sizes(st.center_vel) != n or sizes(st.scale_vel) != n:
+        raise InvalidArgument(f"rod {r} state size")
+    if sizes(st.frames) != m or sizes(st.angular_vel) != m:
+        raise InvalidArgument(f"rod {r} frame count")
+    if len(rod.bones) and (rod.bone_weights is None or np.asarray(rod.bone_weights).size != n * len(rod.bones)):
+        raise InvalidArgument(f"rod {r} bone weights per vertex")
+
+
 def _rod_desc(rod: Rod, keep: list) -> capi.RodDesc:
     def arr(a, shape=None):
         x = _f64(a, shape)
@@ -327,7 +359,8 @@ def marshal_scene(lib, scene: Scene) -> C.c_void_p:
             cm = capi.Material(m.stretch_x, m.stretch_y, m.stretch_z, m.bend_x, m.bend_y, m.bend_z, m.volume,
                                m.density)
             check(lib, lib.vrod_scene_add_material(h, C.byref(cm)))
-        for rod in scene.rods:
+        for r, rod in enumerate(scene.rods):
+            _check_sizes(rod, r)
             keep: list = []
             d = _rod_desc(rod, keep)
             check(lib, lib.vrod_scene_add_rod(h, C.byref(d)))
