@@ -243,20 +243,28 @@ __global__ void k_build_pills(World w, Collide c, const double* __restrict__ ani
 // Bounding spheres, max radius, finiteness (broad_phase, collision.cpp:189-196).
 __global__ void k_bounds(Collide c, int substep, unsigned long long* err) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= c.P) return;
-  const PillV p = load_pill(c.pill, c.P, i);
-  V3 ctr;
-  double r;
-  bounding_sphere(p, ctr, r);
-  c.bsph[i] = ctr.x;
-  c.bsph[c.P + i] = ctr.y;
-  c.bsph[2 * c.P + i] = ctr.z;
-  c.bsph[3 * c.P + i] = r;
-  if (!(finite3(ctr) && isfinite(r))) {
-    if (c.P >= 2) atomicMin(err, err_code(substep, ERR_BROAD, 0, i));
-    return;
+  unsigned long long bits = 0;
+  if (i < c.P) {
+    const PillV p = load_pill(c.pill, c.P, i);
+    V3 ctr;
+    double r;
+    bounding_sphere(p, ctr, r);
+    c.bsph[i] = ctr.x;
+    c.bsph[c.P + i] = ctr.y;
+    c.bsph[2 * c.P + i] = ctr.z;
+    c.bsph[3 * c.P + i] = r;
+    if (!(finite3(ctr) && isfinite(r))) {
+      if (c.P >= 2) atomicMin(err, err_code(substep, ERR_BROAD, 0, i));
+    } else {
+      bits = static_cast<unsigned long long>(__double_as_longlong(r));  // r >= 0: bit order == value order
+    }
   }
-  atomicMax(c.maxr_bits, static_cast<unsigned long long>(__double_as_longlong(r)));  // r >= 0
+  // warp max, one atomic per warp (max is order independent)
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long v = __shfl_down_sync(0xffffffffu, bits, o);
+    bits = v > bits ? v : bits;
+  }
+  if ((threadIdx.x & 31) == 0 && bits) atomicMax(c.maxr_bits, bits);
 }
 
 __device__ __forceinline__ double cell_inv(const Collide& c) {
@@ -322,65 +330,6 @@ __device__ __forceinline__ bool spheres_touch(const Collide& c, int i, int j) {
   return dx * dx + dy * dy + dz * dz <= rr * rr;
 }
 
-template <bool kFill>
-__global__ void k_candidates(Collide c, int prefilter, int* broad_total) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  int broad = 0, cand = 0;
-  if (i < c.P) {
-    const long long kx = c.cellkey[i], ky = c.cellkey[c.P + i], kz = c.cellkey[2 * c.P + i];
-    const int ri = c.pill_rod[i], gi = c.pill_group[i], ei = c.pill_el[i];
-    const bool si = c.pill_self[i] != 0;
-    long long base = 0;
-    if (kFill) base = c.cand_off[i];
-    for (int dx = -1; dx <= 1; ++dx)
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dz = -1; dz <= 1; ++dz) {
-          const int h = find_cell(c, kx + dx, ky + dy, kz + dz);
-          if (h < 0) continue;
-          const int s0 = c.cell_start[h], s1 = c.cell_start[h + 1];
-          for (int q = s0; q < s1; ++q) {
-            const int j = c.cell_items[q];
-            if (j <= i) continue;
-            if (!pair_allowed(ri, gi, si, ei, c.pill_rod[j], c.pill_group[j], c.pill_el[j])) continue;
-            ++broad;
-            if (prefilter && !spheres_touch(c, i, j)) continue;
-            if (kFill) {
-              const long long pos = base + cand;
-              if (pos < c.cand_cap) {
-                c.cand_j[pos] = j;
-                c.cand_i[pos] = i;
-              }
-            }
-            ++cand;
-          }
-        }
-    if (!kFill) c.cand_count[i] = cand;
-    if (kFill) {  // insertion sort of this pill's segment by j (deterministic (i, j) order)
-      const long long end = min(base + cand, c.cand_cap);
-      for (long long a = base + 1; a < end; ++a) {
-        const int key = c.cand_j[a];
-        long long b = a - 1;
-        while (b >= base && c.cand_j[b] > key) {
-          c.cand_j[b + 1] = c.cand_j[b];
-          --b;
-        }
-        c.cand_j[b + 1] = key;
-      }
-    }
-  }
-  if (!kFill && broad_total) {
-    // warp-aggregate the broad-phase pair count
-    for (int o = 16; o > 0; o >>= 1) broad += __shfl_down_sync(0xffffffffu, broad, o);
-    if ((threadIdx.x & 31) == 0 && broad) atomicAdd(broad_total, broad);
-  }
-}
-
-__global__ void k_clamp_count(const int* total, long long cap, int* out, int* ovf) {
-  const int t = *total;
-  if (t > cap) atomicExch(ovf, 1);
-  *out = t > cap ? static_cast<int>(cap) : t;
-}
-
 __device__ __forceinline__ double warm_lookup(const unsigned long long* keys, const double* alpha, int n,
                                               unsigned long long key) {
   int lo = 0, hi = n;  // lower_bound: first inserted wins on duplicate keys
@@ -390,6 +339,324 @@ __device__ __forceinline__ double warm_lookup(const unsigned long long* keys, co
     else hi = mid;
   }
   return (lo < n && keys[lo] == key) ? alpha[lo] : -1.0;
+}
+
+// Squared distance between segments [p0,p1] and [q0,q1] (closest points of two segments,
+// clamped parametric solution).
+__device__ __forceinline__ double seg_seg_dist2(const V3& p0, const V3& p1, const V3& q0, const V3& q1) {
+  const V3 d1 = p1 - p0, d2 = q1 - q0, r = p0 - q0;
+  const double a = dot(d1, d1), e = dot(d2, d2), f = dot(d2, r);
+  double s = 0.0, t = 0.0;
+  if (a <= 1e-300 && e <= 1e-300) return sqnorm(r);
+  if (a <= 1e-300) {
+    t = fmin(fmax(f / e, 0.0), 1.0);
+  } else {
+    const double cc = dot(d1, r);
+    if (e <= 1e-300) {
+      s = fmin(fmax(-cc / a, 0.0), 1.0);
+    } else {
+      const double b = dot(d1, d2);
+      const double denom = a * e - b * b;
+      s = denom > 0.0 ? fmin(fmax((b * f - cc * e) / denom, 0.0), 1.0) : 0.0;
+      t = (b * s + f) / e;
+      if (t < 0.0) {
+        t = 0.0;
+        s = fmin(fmax(-cc / a, 0.0), 1.0);
+      } else if (t > 1.0) {
+        t = 1.0;
+        s = fmin(fmax((b - cc) / a, 0.0), 1.0);
+      }
+    }
+  }
+  const V3 x = (p0 + s * d1) - (q0 + t * d2);
+  return sqnorm(x);
+}
+
+// Conservative "can these pills penetrate" test. A pill lies inside its axis segment dilated by
+// max(r0, r1), and every value deepest_penetration evaluates is >= dist(segments) - rmax_a -
+// rmax_b (collision.cpp:9-61), so a pair whose segments are farther apart than the summed max
+// radii (with a 1e-9 relative + 1e-12 absolute margin for rounding) has a strictly positive
+// computed distance: dropping it cannot change the contact set. First the bounding spheres,
+// then the exact segment distance.
+__device__ __forceinline__ bool may_penetrate(const Collide& c, int i, int j) {
+  const int P = c.P;
+  const double dx = c.bsph[i] - c.bsph[j], dy = c.bsph[P + i] - c.bsph[P + j], dz = c.bsph[2 * P + i] - c.bsph[2 * P + j];
+  const double rs = (c.bsph[3 * P + i] + c.bsph[3 * P + j]) * (1.0 + 1e-9) + 1e-12;
+  if (dx * dx + dy * dy + dz * dz > rs * rs) return false;
+  const PillV a = load_pill(c.pill, P, i), b = load_pill(c.pill, P, j);
+  const double rr = (fmax(a.r0, a.r1) + fmax(b.r0, b.r1)) * (1.0 + 1e-9) + 1e-12;
+  return seg_seg_dist2(a.c0, a.c1, b.c0, b.c1) <= rr * rr;
+}
+
+// One WARP per pill i. Lanes 0..26 probe the 27 cells of i's 3x3x3 block in parallel; the warp
+// then strides over the flattened list of their items (uniform work per lane), counts every
+// allowed pair j > i (broad_phase, collision.cpp:213-226 — StepReport.broad_pairs) and keeps the
+// pairs that may penetrate. Each CTA (8 pills) counts first, reserves its slots in the global
+// candidate list with ONE atomic, then writes (the checks are recomputed: cheaper than
+// storing them). The list is unordered; contacts are put in (i, j) order after the narrow phase.
+constexpr int kPairWarps = 8;
+__global__ void __launch_bounds__(32 * kPairWarps) k_pairs_warp(Collide c, int prefilter, int* broad_total,
+                                                                int* cand_total) {
+  __shared__ int s_start[kPairWarps][27];
+  __shared__ int s_off[kPairWarps][28];
+  __shared__ int s_cnt[kPairWarps];
+  __shared__ int s_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kPairWarps + warp;
+  const bool live = i < c.P;
+  int size = 0;
+  if (live && lane < 27) {
+    const int h = find_cell(c, c.cellkey[i] + (lane / 9 - 1), c.cellkey[c.P + i] + ((lane / 3) % 3 - 1),
+                            c.cellkey[2 * c.P + i] + (lane % 3 - 1));
+    if (h >= 0) {
+      s_start[warp][lane] = c.cell_start[h];
+      size = c.cell_start[h + 1] - c.cell_start[h];
+    }
+  }
+  int incl = size;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane < 27) s_off[warp][lane + 1] = incl;
+  if (lane == 0) s_off[warp][0] = 0;
+  const int total = __shfl_sync(0xffffffffu, incl, 26);
+  __syncwarp();
+  int ri = 0, gi = 0, ei = 0;
+  bool si = false;
+  if (live) {
+    ri = c.pill_rod[i];
+    gi = c.pill_group[i];
+    ei = c.pill_el[i];
+    si = c.pill_self[i] != 0;
+  }
+  int cur_d = 0;            // a lane's k only grows, so its cell index only moves forward
+  auto item = [&](int k) {  // k-th item of the flattened neighbourhood
+    while (s_off[warp][cur_d + 1] <= k) ++cur_d;
+    return c.cell_items[s_start[warp][cur_d] + (k - s_off[warp][cur_d])];
+  };
+  auto accept = [&](int j, bool& is_cand) {
+    if (j <= i || !pair_allowed(ri, gi, si, ei, c.pill_rod[j], c.pill_group[j], c.pill_el[j])) return false;
+    is_cand = !prefilter || spheres_touch(c, i, j);  // the exact segment test runs once, in k_narrow_append
+    return true;
+  };
+  int broad = 0, ncand = 0;
+  if (live)
+    for (int k = lane; k < total; k += 32) {
+      bool cand = false;
+      if (accept(item(k), cand)) {
+        ++broad;
+        ncand += cand;
+      }
+    }
+  for (int o = 16; o > 0; o >>= 1) {
+    broad += __shfl_down_sync(0xffffffffu, broad, o);
+    ncand += __shfl_down_sync(0xffffffffu, ncand, o);
+  }
+  if (lane == 0) s_cnt[warp] = ncand;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int sum = 0;
+    for (int w = 0; w < kPairWarps; ++w) {
+      const int v = s_cnt[w];
+      s_cnt[w] = sum;
+      sum += v;
+    }
+    s_base = sum ? atomicAdd(cand_total, sum) : 0;
+  }
+  __syncthreads();
+  if (lane == 0 && broad) atomicAdd(broad_total, broad);
+  if (!live) return;
+  cur_d = 0;  // second pass restarts at k = lane
+  long long pos = static_cast<long long>(s_base) + s_cnt[warp];
+  for (int k0 = 0; k0 < total; k0 += 32) {
+    const int k = k0 + lane;
+    bool cand = false;
+    int j = -1;
+    if (k < total) {
+      j = item(k);
+      if (!accept(j, cand)) cand = false;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, cand);
+    if (cand) {
+      const long long p = pos + __popc(m & ((1u << lane) - 1));
+      if (p < c.cand_cap) {
+        c.cand_i[p] = i;
+        c.cand_j[p] = j;
+      }
+    }
+    pos += __popc(m);
+  }
+}
+
+// One thread per (pill i, neighbour cell d of its 3x3x3 block): counts the allowed pairs j > i
+// (broad_phase, collision.cpp:213-226 — every one, for StepReport.broad_pairs) and appends the
+// pairs that may penetrate to the candidate list. Appends are warp-aggregated (one atomic per
+// warp); the list is unordered — contacts are put in (i, j) order after the narrow phase.
+__global__ void k_pairs(Collide c, int prefilter, int* broad_total, int* cand_total) {
+  const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int broad = 0, ncand = 0, h = -1, i = 0;
+  if (t < 27ll * c.P) {
+    i = static_cast<int>(t / 27);
+    const int d = static_cast<int>(t - 27ll * i);
+    h = find_cell(c, c.cellkey[i] + (d / 9 - 1), c.cellkey[c.P + i] + ((d / 3) % 3 - 1),
+                  c.cellkey[2 * c.P + i] + (d % 3 - 1));
+  }
+  int s0 = 0, s1 = 0, ri = 0, gi = 0, ei = 0;
+  bool si = false;
+  if (h >= 0) {
+    s0 = c.cell_start[h];
+    s1 = c.cell_start[h + 1];
+    ri = c.pill_rod[i];
+    gi = c.pill_group[i];
+    ei = c.pill_el[i];
+    si = c.pill_self[i] != 0;
+    for (int q = s0; q < s1; ++q) {
+      const int j = c.cell_items[q];
+      if (j <= i || !pair_allowed(ri, gi, si, ei, c.pill_rod[j], c.pill_group[j], c.pill_el[j])) continue;
+      ++broad;
+      if (!prefilter || may_penetrate(c, i, j)) ++ncand;
+    }
+  }
+  // warp-aggregated reservation of ncand slots
+  int incl = ncand;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int warp_total = __shfl_sync(0xffffffffu, incl, 31);
+  int base = 0;
+  if (lane == 31 && warp_total) base = atomicAdd(cand_total, warp_total);
+  base = __shfl_sync(0xffffffffu, base, 31) + incl - ncand;
+  if (ncand) {
+    int k = 0;
+    for (int q = s0; q < s1; ++q) {
+      const int j = c.cell_items[q];
+      if (j <= i || !pair_allowed(ri, gi, si, ei, c.pill_rod[j], c.pill_group[j], c.pill_el[j])) continue;
+      if (prefilter && !may_penetrate(c, i, j)) continue;
+      const long long pos = static_cast<long long>(base) + k++;
+      if (pos < c.cand_cap) {
+        c.cand_i[pos] = i;
+        c.cand_j[pos] = j;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) broad += __shfl_down_sync(0xffffffffu, broad, o);
+  if (lane == 0 && broad) atomicAdd(broad_total, broad);
+}
+
+// Exact conservative segment test (see may_penetrate) over the sphere-filtered candidates;
+// survivors are compacted (warp-aggregated append) into cand2 so the expensive narrow phase
+// runs without divergence.
+__global__ void k_seg_filter(Collide c) {
+  const int n = c.scalars[SC_NCAND];
+  const int lane = threadIdx.x & 31;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long q0 = blockIdx.x * static_cast<long long>(blockDim.x); q0 < n; q0 += stride) {
+    const long long q = q0 + threadIdx.x;
+    int i = 0, j = 0;
+    bool keep = false;
+    if (q < n) {
+      i = c.cand_i[q];
+      j = c.cand_j[q];
+      const PillV A = load_pill(c.pill, c.P, i), B = load_pill(c.pill, c.P, j);
+      const double rr = (fmax(A.r0, A.r1) + fmax(B.r0, B.r1)) * (1.0 + 1e-9) + 1e-12;
+      keep = seg_seg_dist2(A.c0, A.c1, B.c0, B.c1) <= rr * rr;
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    int base = 0;
+    if (lane == 0 && mask) base = atomicAdd(&c.scalars[SC_NCAND2], __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) {
+      const long long k = base + __popc(mask & ((1u << lane) - 1));
+      c.cand2_i[k] = i;  // k < n <= cand_cap
+      c.cand2_j[k] = j;
+    }
+  }
+}
+
+// Narrow phase over the unordered candidates; penetrating pairs are appended (warp-aggregated)
+// to the raw contact list.
+__global__ void k_narrow_append(Collide c, int split_warm) {
+  const int n = c.scalars[SC_NCAND2];
+  const int nrr = c.scalars[SC_NRR_PREV], nrk = c.scalars[SC_NRK_PREV];
+  const int lane = threadIdx.x & 31;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long q0 = blockIdx.x * static_cast<long long>(blockDim.x); q0 < n; q0 += stride) {
+    const long long q = q0 + threadIdx.x;
+    int i = 0, j = 0;
+    double al = 0, be = 0, d = 1.0;
+    if (q < n) {
+      i = c.cand2_i[q];
+      j = c.cand2_j[q];
+      const unsigned long long key = pair_key(c.pill_id[i], c.pill_id[j]);
+      double warm;
+      if (!split_warm || (c.pill_rod[i] >= 0 && c.pill_rod[j] >= 0))
+        warm = warm_lookup(c.warm_rr_key, c.warm_rr_alpha, nrr, key);
+      else
+        warm = warm_lookup(c.warm_rk_key, c.warm_rk_alpha, nrk, key);
+      deepest(load_pill(c.pill, c.P, i), load_pill(c.pill, c.P, j), c.iters_dich, warm, al, be, d);
+    }
+    const bool hit = q < n && d < 0.0;
+    const unsigned mask = __ballot_sync(0xffffffffu, hit);
+    int base = 0;
+    if (lane == 0 && mask) base = atomicAdd(&c.scalars[SC_NCT_RAW], __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (hit) {
+      const long long k = base + __popc(mask & ((1u << lane) - 1));
+      if (k < c.contact_cap) {
+        c.raw_i[k] = i;
+        c.raw_j[k] = j;
+        c.raw_ab[k] = al;
+        c.raw_ab[c.contact_cap + k] = be;
+      }
+    }
+  }
+}
+
+// (i, j) ordering of the raw contacts: count per pill i -> scan -> scatter -> per-i sort by j.
+__global__ void k_ct_count(Collide c) {
+  const int n = c.scalars[SC_NCT];
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    atomicAdd(&c.ct_cnt[c.raw_i[k]], 1);
+}
+__global__ void k_ct_scatter(Collide c) {
+  const int n = c.scalars[SC_NCT];
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int i = c.raw_i[k];
+    const int pos = c.ct_off[i] + atomicAdd(&c.ct_cur[i], 1);
+    c.ct_a[pos] = i;
+    c.ct_b[pos] = c.raw_j[k];
+    c.ct_alpha[pos] = c.raw_ab[k];
+    c.ct_beta[pos] = c.raw_ab[c.contact_cap + k];
+  }
+}
+__global__ void k_ct_sort(Collide c) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= c.P) return;
+  const int s0 = c.ct_off[i], s1 = c.ct_off[i + 1];
+  for (int a = s0 + 1; a < s1; ++a) {
+    const int kj = c.ct_b[a];
+    const double ka = c.ct_alpha[a], kb = c.ct_beta[a];
+    int b = a - 1;
+    while (b >= s0 && c.ct_b[b] > kj) {
+      c.ct_b[b + 1] = c.ct_b[b];
+      c.ct_alpha[b + 1] = c.ct_alpha[b];
+      c.ct_beta[b + 1] = c.ct_beta[b];
+      --b;
+    }
+    c.ct_b[b + 1] = kj;
+    c.ct_alpha[b + 1] = ka;
+    c.ct_beta[b + 1] = kb;
+  }
+}
+__global__ void k_clamp_raw(int* scalars, int raw, int out, long long cap, int ovf_code) {
+  const int t = scalars[raw];
+  if (t > cap) atomicExch(&scalars[SC_OVF], ovf_code);
+  scalars[out] = t > cap ? static_cast<int>(cap) : t;
 }
 
 // Narrow phase over the candidate list (find_contacts, collision.cpp:261-271).
@@ -426,14 +693,21 @@ __global__ void k_compact_contacts(Collide c) {
 }
 
 __global__ void k_contact_count(Collide c, StepAccum* acc) {
-  const int n = c.cand_pos[c.scalars[SC_NCAND]];
-  if (n > c.contact_cap) atomicExch(&c.scalars[SC_OVF], 2);
-  const int nc = n > c.contact_cap ? static_cast<int>(c.contact_cap) : n;
-  c.scalars[SC_NCT] = nc;
-  atomicAdd(&acc->contact_count, nc);
+  atomicAdd(&acc->contact_count, c.scalars[SC_NCT]);
   atomicAdd(&acc->broad_pairs, c.scalars[SC_BROAD]);
-  if (n > acc->max_contacts) acc->max_contacts = n;
-  if (c.cand_off[c.P] > acc->max_candidates) acc->max_candidates = c.cand_off[c.P];
+  if (c.scalars[SC_NCT_RAW] > acc->max_contacts) acc->max_contacts = c.scalars[SC_NCT_RAW];
+  if (c.scalars[SC_NCAND_RAW] > acc->max_candidates) acc->max_candidates = c.scalars[SC_NCAND_RAW];
+}
+
+__global__ void k_cand_to_raw(Collide c) {
+  const int n = c.scalars[SC_NCAND];
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    c.raw_i[k] = c.cand_i[k];
+    c.raw_j[k] = c.cand_j[k];
+    c.raw_ab[k] = 0.0;
+    c.raw_ab[c.contact_cap + k] = 0.0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) c.scalars[SC_NCT] = n;
 }
 
 // Warm list for the next substep: (pair key, alpha) of the new contacts (solver.cpp:210-214).
@@ -548,8 +822,23 @@ void launch_narrow_only(Collide& c, int split_warm, int store_d, cudaStream_t st
   k_compact_contacts<<<g, kThreads, 0, st>>>(c);
 }
 
+// Puts the first scalars[SC_NCT] raw (i, j, alpha, beta) records into (i, j) order in ct_*.
+void launch_order_contacts(Collide& c, cudaStream_t st) {
+  const int g = grid_for(c.contact_cap);
+  cudaMemsetAsync(c.ct_cnt, 0, sizeof(int) * (c.P + 1), st);
+  cudaMemsetAsync(c.ct_cur, 0, sizeof(int) * (c.P + 1), st);
+  k_ct_count<<<g, kThreads, 0, st>>>(c);
+  scan_exclusive(c.ct_cnt, c.ct_off, c.P, nullptr, c.scan_tmp, c.scan_parts, st);
+  k_ct_scatter<<<g, kThreads, 0, st>>>(c);
+  k_ct_sort<<<(c.P + kThreads - 1) / kThreads, kThreads, 0, st>>>(c);
+}
+
+// Broad + narrow phase on the pill arrays already in `c` (pill, pill_rod/el/group/self/id).
+// prefilter=0 keeps every allowed pair (the standalone broad_phase contract); with do_narrow=0
+// the (unordered) candidates are left in cand_i/cand_j, scalars[SC_NCAND].
 void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int prefilter, int do_narrow,
                          int split_warm, int store_d, cudaStream_t st) {
+  (void)store_d;
   const int P = c.P;
   const int b = (P + kThreads - 1) / kThreads;
   cudaMemsetAsync(c.maxr_bits, 0, sizeof(unsigned long long), st);
@@ -557,6 +846,8 @@ void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
   cudaMemsetAsync(c.cell_count, 0, sizeof(int) * c.T, st);
   cudaMemsetAsync(c.cell_cursor, 0, sizeof(int) * c.T, st);
   cudaMemsetAsync(c.scalars + SC_BROAD, 0, sizeof(int), st);
+  cudaMemsetAsync(c.scalars + SC_NCAND_RAW, 0, sizeof(int), st);
+  cudaMemsetAsync(c.scalars + SC_NCT_RAW, 0, sizeof(int), st);
   if (P > 0) {
     k_bounds<<<b, kThreads, 0, st>>>(c, substep, err);
     k_insert<<<b, kThreads, 0, st>>>(c);
@@ -564,13 +855,23 @@ void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
   scan_exclusive(c.cell_count, c.cell_start, c.T, nullptr, c.scan_tmp, c.scan_parts, st);
   if (P > 0) {
     k_scatter<<<b, kThreads, 0, st>>>(c);
-    k_candidates<false><<<b, kThreads, 0, st>>>(c, prefilter, c.scalars + SC_BROAD);
+    k_pairs_warp<<<(P + kPairWarps - 1) / kPairWarps, 32 * kPairWarps, 0, st>>>(c, prefilter, c.scalars + SC_BROAD,
+                                                                              c.scalars + SC_NCAND_RAW);
   }
-  scan_exclusive(c.cand_count, c.cand_off, P, nullptr, c.scan_tmp, c.scan_parts, st);
-  if (P > 0) k_candidates<true><<<b, kThreads, 0, st>>>(c, prefilter, nullptr);
-  k_clamp_count<<<1, 1, 0, st>>>(c.cand_off + P, c.cand_cap, c.scalars + SC_NCAND, c.scalars + SC_OVF);
+  k_clamp_raw<<<1, 1, 0, st>>>(c.scalars, SC_NCAND_RAW, SC_NCAND, c.cand_cap, 1);
   if (!do_narrow) return;
-  launch_narrow_only(c, split_warm, store_d, st);
+  cudaMemsetAsync(c.scalars + SC_NCAND2, 0, sizeof(int), st);
+  k_seg_filter<<<grid_for(c.cand_cap), kThreads, 0, st>>>(c);
+  k_narrow_append<<<grid_for(c.cand_cap), kThreads, 0, st>>>(c, split_warm);
+  k_clamp_raw<<<1, 1, 0, st>>>(c.scalars, SC_NCT_RAW, SC_NCT, c.contact_cap, 2);
+  launch_order_contacts(c, st);
+}
+
+// Standalone broad_phase: every allowed pair, in the reference's (i, j) order.
+void launch_broad_ordered(Collide& c, unsigned long long* err, cudaStream_t st) {
+  launch_broad_narrow(c, 0, err, 0, 0, 0, 0, st);
+  k_cand_to_raw<<<grid_for(c.cand_cap), kThreads, 0, st>>>(c);
+  launch_order_contacts(c, st);
 }
 
 void launch_collide(const World& w, Collide& c, const double* anim, const AnimLayout& al, int substep,

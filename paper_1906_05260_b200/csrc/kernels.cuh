@@ -23,8 +23,6 @@
 
 namespace vdev {
 
-constexpr int kSweepThreads = 128;  // rod-sweep CTA (covers 126 owned slots + 2 halo)
-
 // Per-substep collision / external-block buffers.
 struct Collide {
   int P = 0;            // pills
@@ -58,6 +56,8 @@ struct Collide {
   int* cand_off = nullptr;       // P+1
   int* cand_i = nullptr;         // cand_cap
   int* cand_j = nullptr;
+  int* cand2_i = nullptr;        // cand_cap: survivors of the exact segment test
+  int* cand2_j = nullptr;
   int* cand_flag = nullptr;      // cand_cap+1
   int* cand_pos = nullptr;       // cand_cap+1
   double* cand_ab = nullptr;     // 3 x cand_cap (alpha, beta, distance)
@@ -67,6 +67,13 @@ struct Collide {
   double* ct_alpha = nullptr;
   double* ct_beta = nullptr;
   double* ct_dist = nullptr;     // standalone find_contacts only
+  // raw (unordered) narrow-phase hits and the (i, j) ordering scratch
+  int* raw_i = nullptr;          // contact_cap
+  int* raw_j = nullptr;
+  double* raw_ab = nullptr;      // 2 x contact_cap
+  int* ct_cnt = nullptr;         // P+1
+  int* ct_off = nullptr;         // P+1
+  int* ct_cur = nullptr;         // P+1
   // warm-start lists from the previous substep (sorted by pair key)
   unsigned long long* warm_rr_key = nullptr;
   double* warm_rr_alpha = nullptr;
@@ -86,8 +93,11 @@ struct Collide {
   // external blocks: pins | contacts | half-planes
   long long ext_cap = 0;
   double* ext_lam = nullptr;     // 3 x ext_cap
-  double* ext_out = nullptr;     // 16 x ext_cap: dc[4][3], ds[4]
-  uint8_t* ext_active = nullptr; // ext_cap
+  // Results are written per incidence entry q (slot-sorted), so the sweep's gather reads
+  // contiguous entries instead of chasing block ids.
+  double* ext_contrib = nullptr; // 4 x (4 x ext_cap): entry q -> dc xyz, ds
+  uint8_t* ext_flag = nullptr;   // 4 x ext_cap: entry q -> kExtCenter | kExtScale, 0 = no update
+  int* ext_pos = nullptr;        // 4 x ext_cap: (block << 2 | endpoint) -> entry q
   int* ext_cnt = nullptr;        // V+1 incidence counts
   int* ext_off = nullptr;        // V+1
   int* ext_cur = nullptr;        // V
@@ -97,8 +107,9 @@ struct Collide {
   unsigned long long* maxr_bits = nullptr;
   int* scan_tmp = nullptr;       // scan partials
 };
+enum : int { kExtCenter = 1, kExtScale = 2 };
 enum Scalar : int { SC_NCAND = 0, SC_NCT, SC_NHP, SC_NRR, SC_NRK, SC_NRR_PREV, SC_NRK_PREV, SC_BROAD, SC_OVF,
-                    kScalars };
+                    SC_NCAND_RAW, SC_NCT_RAW, SC_NCAND2, kScalars };
 
 struct Groups {  // shape matching (bundling.cpp)
   int G = 0;
@@ -153,6 +164,7 @@ void launch_collide(const World& w, Collide& c, const double* anim, const AnimLa
 void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int prefilter, int do_narrow,
                          int split_warm, int store_d, cudaStream_t st);
 void launch_narrow_only(Collide& c, int split_warm, int store_d, cudaStream_t st);
+void launch_broad_ordered(Collide& c, unsigned long long* err, cudaStream_t st);
 void launch_halfplanes(const World& w, Collide& c, cudaStream_t st);
 // standalone fine-grained entry points (vrod_pill_project & co), on device arrays
 void launch_pill_project(long long n, const double* x, const double* pills, double* t, double* d,

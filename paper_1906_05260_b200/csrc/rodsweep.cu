@@ -1,0 +1,658 @@
+// The rod stencil of one averaged-Jacobi sweep (jacobi_sweep, constraints.cpp:491-556): every
+// elastic block of every rod evaluated and solved against the snapshot X, all corrections
+// gathered per DOF in the reference's block order, averaged and applied into Y.
+//
+// CTA = 4 warps over a tile of 64 consecutive slots (62 owned + 1 halo slot each side). The
+// blocks of the tile are evaluated kind-major (eval_constraint :101-270 + solve_block
+// :400-487): work item = (kind present in the tile, position), so each warp runs one block
+// formula over 32 positions. Per-block results go to shared memory; then one thread per owned slot gathers —
+// element pass of element k-1 then k, vertex pass of vertex k-1, k, k+1, then the external
+// blocks (soft pins, contacts, half-planes) through the slot-sorted incidence list — divides
+// by the number of active touching blocks, clamps the scale and renormalizes the frame
+// (constraints.cpp:509-554). The shapes of all expressions follow the reference, so with
+// --fmad=false the result is the reference's arithmetic bit for bit; there are no atomics on
+// the data path (bitwise run-to-run determinism) and no colouring (Jacobi
+// snapshot semantics, test_sweep.cpp:132-142).
+#include "kernels.cuh"
+#include "vmath.cuh"
+
+namespace vdev {
+
+using namespace vm;
+
+namespace {
+
+// Tile of TP computed positions start-1 .. start+TP-2 (TP-2 owned), staged slots start-2 ..
+// start+TP-1. TP = 64 for large worlds; 32 when 64-wide tiles would leave SMs idle.
+constexpr int kWarps = 4;
+
+__device__ __forceinline__ unsigned long long umin64(unsigned long long a, unsigned long long b) { return a < b ? a : b; }
+
+// Per-position block results (written by the kind warps, read by the gather).
+struct PosRes {
+  double sz_dc0[3], sz_dc1[3], sz_dt[3];
+  double cs[2], ss[2];
+  double vs_dc0[3], vs_dc1[3], vs_ds[2], vs_dt[3];
+  double bt_ds, bt_dta[3], bt_dtb[3];
+  double sb[3];  // ds_{j-1}, ds_j, ds_{j+1}
+  double vb_ds[2], vb_dta[2][3], vb_dtb[2][3];
+  double pad;  // 49-double stride: lane-consecutive records fall in distinct banks
+};
+enum : int { A_SZ = 0, A_CS, A_SS, A_VS, A_BT, A_SB, A_VBU, A_VBV, kKinds };
+
+// Staged fields (rows of Tile::st), one column per slot start-2 .. start+63.
+enum StageRow : int {
+  T_CX = 0, T_CY, T_CZ, T_S, T_QW, T_QX, T_QY, T_QZ,  // snapshot X
+  T_SBAR, T_IC, T_IS,                                  // static vertex fields
+  T_ITX, T_ITY, T_ITZ,                                 // inverse theta weights
+  T_LEN, T_LEN0, T_TDOT, T_SGRAD, T_SLAP, T_DARBX, T_DARBY, T_DARBZ,
+  T_KSZ, T_KCS, T_KSS, T_KVS, T_KBT0, T_KBT1, T_KBT2, T_KSB, T_KVB,
+  T_LAM,                                               // + LamField: multipliers before the sweep
+  kStageRows = T_LAM + kLamFields
+};
+constexpr int kKindSZ = 1 << A_SZ, kKindCS = 1 << A_CS, kKindSS = 1 << A_SS, kKindVS = 1 << A_VS,
+              kKindBT = 1 << A_BT, kKindSB = 1 << A_SB, kKindVBU = 1 << A_VBU, kKindVBV = 1 << A_VBV;
+constexpr int kKindVB = kKindVBU | kKindVBV;
+constexpr int kAllKinds = 0xff;
+
+// Which kinds read a staged row (rows nobody in the tile needs are not loaded).
+__device__ __forceinline__ int row_need(int r) {
+  switch (r) {
+    case T_SBAR: return kKindCS | kKindVS | kKindBT | kKindSB | kKindVB;
+    case T_ITX: case T_ITY: return kKindSZ | kKindVS | kKindBT | kKindVB;
+    case T_ITZ: return kKindBT | kKindVB;
+    case T_LEN: return kKindSZ | kKindSS | kKindBT | kKindSB | kKindVB;
+    case T_LEN0: return kKindVS | kKindVB;
+    case T_TDOT: return kKindSZ | kKindVS;
+    case T_SGRAD: return kKindSS;
+    case T_SLAP: return kKindSB;
+    case T_DARBX: case T_DARBY: return kKindBT | kKindVB;
+    case T_DARBZ: return kKindBT;
+    case T_KSZ: return kKindSZ;
+    case T_KCS: return kKindCS;
+    case T_KSS: return kKindSS;
+    case T_KVS: return kKindVS;
+    case T_KBT0: case T_KBT1: case T_KBT2: return kKindBT;
+    case T_KSB: return kKindSB;
+    case T_KVB: return kKindVB;
+    case T_LAM + L_SZ0: case T_LAM + L_SZ1: case T_LAM + L_SZ2: return kKindSZ;
+    case T_LAM + L_CS: return kKindCS;
+    case T_LAM + L_SS: return kKindSS;
+    case T_LAM + L_VS0: case T_LAM + L_VS1: case T_LAM + L_VS2: return kKindVS;
+    case T_LAM + L_BT0: case T_LAM + L_BT1: case T_LAM + L_BT2: return kKindBT;
+    case T_LAM + L_SB: return kKindSB;
+    case T_LAM + L_VBU: return kKindVBU;
+    case T_LAM + L_VBV: return kKindVBV;
+    default: return kAllKinds;  // X, IC, IS: centers/scales/frames are always applied
+  }
+}
+__constant__ int kStagedEField[T_LAM - T_LEN] = {LEN, LEN0, TDOT, SGRAD, SLAP, DARBX, DARBY, DARBZ, KSZ,
+                                                 KCS, KSS, KVS, KBT0, KBT1, KBT2, KSB, KVB};
+__device__ __forceinline__ const double* row_src(int r, const World& w, const double* X, const double* lam) {
+  const long long vp = w.vpad;
+  if (r < T_SBAR) return X + (CX + r) * vp;
+  if (r < T_ITX) return w.vstat + (SBAR + (r - T_SBAR)) * vp;
+  if (r < T_LEN) return w.estat + (ITX + (r - T_ITX)) * vp;
+  if (r >= T_LAM) return lam + (r - T_LAM) * vp;
+  return w.estat + kStagedEField[r - T_LEN] * vp;
+}
+
+template <int TP>
+struct Tile {
+  static constexpr int kTilePos = TP, kTileStage = TP + 2;
+  double st[kStageRows][kTileStage];
+  PosRes res[kTilePos];
+  int loc[kTilePos], m[kTilePos], kinds[kTilePos], bbase[kTilePos];
+  unsigned wmask[kTilePos / 32];  // OR of the kinds present, per 32 positions
+  uint8_t act[kKinds][kTilePos];
+};
+
+template <int TP>
+__global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c, const double* __restrict__ X,
+                                                          double* __restrict__ Y, SweepParams sp, int* singular,
+                                                          unsigned long long* err, int has_ext) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int kTilePos = TP, kTileOwned = TP - 2, kTileStage = TP + 2;
+  Tile<TP>& t = *reinterpret_cast<Tile<TP>*>(smem_raw);
+  const int V = w.V, vp = w.vpad;
+  const int start = blockIdx.x * kTileOwned;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < kTilePos; i += 32 * kWarps) {
+    const int p = start - 1 + i;
+    int k = -1, m = 0, kinds = 0, bb = 0;
+    if (p >= 0 && p < V) {
+      const int r = w.slot_rod[p];
+      k = w.slot_loc[p];
+      m = w.slot_m[p];
+      kinds = w.rod_ekinds[r] | (w.rod_vkinds[r] << 4);
+      bb = w.rod_block_base[r];
+    }
+    const unsigned wm = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(kinds));
+    if (lane == 0) t.wmask[i >> 5] = wm;
+    t.loc[i] = k;
+    t.m[i] = m;
+    t.kinds[i] = kinds;
+    t.bbase[i] = bb;
+#pragma unroll
+    for (int a = 0; a < kKinds; ++a) t.act[a][i] = 0;
+  }
+  __syncthreads();
+  unsigned mask = 0;
+#pragma unroll
+  for (int i = 0; i < kTilePos / 32; ++i) mask |= t.wmask[i];
+  // Stage every row the tile's kinds read: 16-byte cp.async chunks (start-2 is even and rows
+  // are 256-byte aligned), all in flight at once; slots outside [0, V) are zero-filled.
+  constexpr int kChunks = kTileStage / 2;
+  for (int x = tid; x < kStageRows * kChunks; x += 32 * kWarps) {
+    const int r = x / kChunks, j = x - r * kChunks;
+    if (!(row_need(r) & mask)) continue;
+    const int v = start - 2 + 2 * j;
+    const int valid = v < 0 ? 0 : min(2, V - v);
+    const double* src = row_src(r, w, X, sp.lam_in) + (valid > 0 ? v : 0);
+    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&t.st[r][2 * j]));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(8 * max(valid, 0)));
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+
+  const double h2 = sp.h2, beta = sp.beta;
+  int nsing = 0;
+  unsigned long long bad = kNoError;
+  // Work items (kind, position), kind-major over the kinds present in the tile: 64 positions
+  // per kind, so every warp evaluates a single kind (no divergence between block formulas)
+  // and all four warps share the tile's work whatever its kind mix.
+  const int items = __popc(mask) * kTilePos;
+  for (int item = tid; item < items; item += 32 * kWarps) {
+    const int pi = item % kTilePos;
+    unsigned mm = mask;
+    for (int n = item / kTilePos; n > 0; --n) mm &= mm - 1;
+    const int kind = __ffs(mm) - 1;
+    const int k = t.loc[pi];
+    if (k < 0) continue;
+    const int p = start - 1 + pi;
+    const int m = t.m[pi];
+    const int ek = t.kinds[pi] & 15, vk = t.kinds[pi] >> 4;
+    const bool owned = pi >= 1 && pi <= kTileOwned;
+    const int si = pi + 1;  // staging index of p
+    PosRes& R = t.res[pi];
+    auto keep_lam = [&](int f0, int nf) {
+      if (!owned) return;
+      for (int f = f0; f < f0 + nf; ++f) sp.lam_out[f * (long long)vp + p] = t.st[T_LAM + f][si];
+    };
+    auto fail = [&](int local) { bad = umin64(bad, err_code(sp.substep, ERR_SWEEP, sp.iter, t.bbase[pi] + local)); };
+    const int ne = __popc(ek), nv = __popc(vk);
+
+    if (k < m && kind < A_BT) {  // element pass of element k (constraints.cpp:302-314)
+      const V3 c0{t.st[T_CX][si], t.st[T_CY][si], t.st[T_CZ][si]}, c1{t.st[T_CX][si + 1], t.st[T_CY][si + 1], t.st[T_CZ][si + 1]};
+      const double s0 = t.st[T_S][si], s1 = t.st[T_S][si + 1];
+      const double ic0 = t.st[T_IC][si], ic1 = t.st[T_IC][si + 1], is0 = t.st[T_IS][si], is1 = t.st[T_IS][si + 1];
+      const V3 it{t.st[T_ITX][si], t.st[T_ITY][si], t.st[T_ITZ][si]};
+      const int lbase = k * ne;
+      if (kind == A_SZ && (ek & EK_SZ)) {  // StretchZ (:106-119), dim 3
+        const M3 Rm = qmat(Q4{t.st[T_QW][si], t.st[T_QX][si], t.st[T_QY][si], t.st[T_QZ][si]});
+        const double tbar = t.st[T_TDOT][si];
+        const double l = t.st[T_LEN][si];
+        const double inv_l = 1.0 / l;
+        const V3 dzc = (c1 - c0) / l;
+        const V3 wv = col(Rm, 2);
+        const double W[3] = {dzc.x - tbar * wv.x, dzc.y - tbar * wv.y, dzc.z - tbar * wv.z};
+        const double J0[3] = {tbar * Rm.m[0][1], tbar * Rm.m[1][1], tbar * Rm.m[2][1]};
+        const double J1[3] = {-tbar * Rm.m[0][0], -tbar * Rm.m[1][0], -tbar * Rm.m[2][0]};
+        double M[3][3];
+        double cd = 0.0;
+        if (ic0 != 0.0) cd = cd + (h2 * ic0 * inv_l) * inv_l;
+        if (ic1 != 0.0) cd = cd + (h2 * ic1 * inv_l) * inv_l;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const double b0 = (h2 * J0[a]) * it.x, b1 = (h2 * J1[a]) * it.y;
+#pragma unroll
+          for (int b = 0; b < 3; ++b) M[a][b] = (a == b ? cd : 0.0) + (b0 * J0[b] + b1 * J1[b]);
+        }
+        const double kinv = inverse_stiffness(t.st[T_KSZ][si]);
+        double rhs[3], dl[3];
+        const double lam[3] = {t.st[T_LAM + L_SZ0][si], t.st[T_LAM + L_SZ1][si], t.st[T_LAM + L_SZ2][si]};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          M[d][d] = M[d][d] + kinv;
+          rhs[d] = W[d] - kinv * lam[d];
+        }
+        if (solve3(M, rhs, beta, dl)) {
+          const double f0 = -h2 * ic0, f1 = -h2 * ic1;
+          bool ok = true;
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            R.sz_dc0[d] = f0 * (-inv_l * dl[d]);
+            R.sz_dc1[d] = f1 * (inv_l * dl[d]);
+            ok = ok && isfinite(dl[d]) && isfinite(R.sz_dc0[d]) && isfinite(R.sz_dc1[d]);
+          }
+          const double jt0 = (J0[0] * dl[0] + J0[1] * dl[1]) + J0[2] * dl[2];
+          const double jt1 = (J1[0] * dl[0] + J1[1] * dl[1]) + J1[2] * dl[2];
+          R.sz_dt[0] = -h2 * (it.x * jt0);
+          R.sz_dt[1] = -h2 * (it.y * jt1);
+          R.sz_dt[2] = 0.0;
+          t.act[A_SZ][pi] = 1;
+          if (owned) {
+            sp.lam_out[L_SZ0 * (long long)vp + p] = lam[0] + dl[0];
+            sp.lam_out[L_SZ1 * (long long)vp + p] = lam[1] + dl[1];
+            sp.lam_out[L_SZ2 * (long long)vp + p] = lam[2] + dl[2];
+            if (!(ok && isfinite(R.sz_dt[0]) && isfinite(R.sz_dt[1]))) fail(lbase + __popc(ek & (EK_SZ - 1)));
+          }
+        } else {
+          nsing += owned;
+          keep_lam(L_SZ0, 3);
+        }
+      }
+      if (kind == A_CS && (ek & EK_CS)) {  // CrossSection (:120-129), dim 1
+        const double W = 0.5 * (s0 + s1) - 0.5 * (t.st[T_SBAR][si] + t.st[T_SBAR][si + 1]);
+        double M = 0.0;
+        if (is0 != 0.0) M = M + (h2 * is0 * 0.5) * 0.5;
+        if (is1 != 0.0) M = M + (h2 * is1 * 0.5) * 0.5;
+        const double kinv = inverse_stiffness(t.st[T_KCS][si]);
+        const double lam = t.st[T_LAM + L_CS][si];
+        M = M + kinv;
+        if (M > 1e-250) {
+          const double dl = beta * (W - kinv * lam) / M;
+          R.cs[0] = -h2 * is0 * (0.5 * dl);
+          R.cs[1] = -h2 * is1 * (0.5 * dl);
+          t.act[A_CS][pi] = 1;
+          if (owned) {
+            sp.lam_out[L_CS * (long long)vp + p] = lam + dl;
+            if (!(isfinite(dl) && isfinite(R.cs[0]) && isfinite(R.cs[1]))) fail(lbase + __popc(ek & (EK_CS - 1)));
+          }
+        } else {
+          nsing += owned;
+          keep_lam(L_CS, 1);
+        }
+      }
+      if (kind == A_SS && (ek & EK_SS)) {  // SurfaceStretch (:130-138), dim 1
+        const double l = t.st[T_LEN][si];
+        const double W = (s1 - s0) / l - t.st[T_SGRAD][si];
+        const double j0 = -1.0 / l, j1 = 1.0 / l;
+        double M = 0.0;
+        if (is0 != 0.0) M = M + (h2 * is0 * j0) * j0;
+        if (is1 != 0.0) M = M + (h2 * is1 * j1) * j1;
+        const double kinv = inverse_stiffness(t.st[T_KSS][si]);
+        const double lam = t.st[T_LAM + L_SS][si];
+        M = M + kinv;
+        if (M > 1e-250) {
+          const double dl = beta * (W - kinv * lam) / M;
+          R.ss[0] = -h2 * is0 * (j0 * dl);
+          R.ss[1] = -h2 * is1 * (j1 * dl);
+          t.act[A_SS][pi] = 1;
+          if (owned) {
+            sp.lam_out[L_SS * (long long)vp + p] = lam + dl;
+            if (!(isfinite(dl) && isfinite(R.ss[0]) && isfinite(R.ss[1]))) fail(lbase + __popc(ek & (EK_SS - 1)));
+          }
+        } else {
+          nsing += owned;
+          keep_lam(L_SS, 1);
+        }
+      }
+      if (kind == A_VS && (ek & EK_VS)) {  // VolumeStretch (:169-188), dim 3
+        const M3 Rm = qmat(Q4{t.st[T_QW][si], t.st[T_QX][si], t.st[T_QY][si], t.st[T_QZ][si]});
+        const double tbar = t.st[T_TDOT][si];
+        const double l0 = t.st[T_LEN0][si];
+        const double smid = 0.5 * (s0 + s1);
+        const double smr = 0.5 * (t.st[T_SBAR][si] + t.st[T_SBAR][si + 1]);
+        const V3 dzc = (c1 - c0) / l0;
+        const V3 wv = col(Rm, 2);
+        const double ka = smid * smid, kb = smr * smr * tbar;
+        const double W[3] = {ka * dzc.x - kb * wv.x, ka * dzc.y - kb * wv.y, ka * dzc.z - kb * wv.z};
+        const double jc = smid * smid / l0;
+        const double js[3] = {smid * dzc.x, smid * dzc.y, smid * dzc.z};
+        const double fac = -smr * smr * tbar;
+        const double J0[3] = {fac * -Rm.m[0][1], fac * -Rm.m[1][1], fac * -Rm.m[2][1]};
+        const double J1[3] = {fac * Rm.m[0][0], fac * Rm.m[1][0], fac * Rm.m[2][0]};
+        double M[3][3];
+        double cd = 0.0;
+        if (ic0 != 0.0) cd = cd + (h2 * ic0 * jc) * jc;
+        if (ic1 != 0.0) cd = cd + (h2 * ic1 * jc) * jc;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const double sa0 = h2 * is0 * js[a], sa1 = h2 * is1 * js[a];
+          const double b0 = (h2 * J0[a]) * it.x, b1 = (h2 * J1[a]) * it.y;
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            double v = a == b ? cd : 0.0;
+            if (is0 != 0.0) v = v + sa0 * js[b];
+            if (is1 != 0.0) v = v + sa1 * js[b];
+            M[a][b] = v + (b0 * J0[b] + b1 * J1[b]);
+          }
+        }
+        const double kinv = inverse_stiffness(t.st[T_KVS][si]);
+        double rhs[3], dl[3];
+        const double lam[3] = {t.st[T_LAM + L_VS0][si], t.st[T_LAM + L_VS1][si], t.st[T_LAM + L_VS2][si]};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          M[d][d] = M[d][d] + kinv;
+          rhs[d] = W[d] - kinv * lam[d];
+        }
+        if (solve3(M, rhs, beta, dl)) {
+          const double f0 = -h2 * ic0, f1 = -h2 * ic1;
+          bool ok = true;
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            R.vs_dc0[d] = f0 * (-jc * dl[d]);
+            R.vs_dc1[d] = f1 * (jc * dl[d]);
+            ok = ok && isfinite(dl[d]) && isfinite(R.vs_dc0[d]) && isfinite(R.vs_dc1[d]);
+          }
+          const double jd = (js[0] * dl[0] + js[1] * dl[1]) + js[2] * dl[2];
+          R.vs_ds[0] = -h2 * is0 * jd;
+          R.vs_ds[1] = -h2 * is1 * jd;
+          const double jt0 = (J0[0] * dl[0] + J0[1] * dl[1]) + J0[2] * dl[2];
+          const double jt1 = (J1[0] * dl[0] + J1[1] * dl[1]) + J1[2] * dl[2];
+          R.vs_dt[0] = -h2 * (it.x * jt0);
+          R.vs_dt[1] = -h2 * (it.y * jt1);
+          R.vs_dt[2] = 0.0;
+          t.act[A_VS][pi] = 1;
+          if (owned) {
+            sp.lam_out[L_VS0 * (long long)vp + p] = lam[0] + dl[0];
+            sp.lam_out[L_VS1 * (long long)vp + p] = lam[1] + dl[1];
+            sp.lam_out[L_VS2 * (long long)vp + p] = lam[2] + dl[2];
+            if (!(ok && isfinite(R.vs_ds[0]) && isfinite(R.vs_ds[1]) && isfinite(R.vs_dt[0]) && isfinite(R.vs_dt[1])))
+              fail(lbase + __popc(ek & (EK_VS - 1)));
+          }
+        } else {
+          nsing += owned;
+          keep_lam(L_VS0, 3);
+        }
+      }
+    }
+
+    if (k >= 1 && k <= m - 1 && kind >= A_BT) {  // vertex pass of vertex k (:315-327)
+      const Q4 qa{t.st[T_QW][si - 1], t.st[T_QX][si - 1], t.st[T_QY][si - 1], t.st[T_QZ][si - 1]};
+      const Q4 qb{t.st[T_QW][si], t.st[T_QX][si], t.st[T_QY][si], t.st[T_QZ][si]};
+      const double sm = t.st[T_S][si - 1], s0 = t.st[T_S][si], spp = t.st[T_S][si + 1];
+      const double is0 = t.st[T_IS][si];
+      const V3 ita{t.st[T_ITX][si - 1], t.st[T_ITY][si - 1], t.st[T_ITZ][si - 1]};
+      const V3 itb{t.st[T_ITX][si], t.st[T_ITY][si], t.st[T_ITZ][si]};
+      const double sbar = t.st[T_SBAR][si];
+      const double la = t.st[T_LEN][si - 1], lb = t.st[T_LEN][si];
+      const int lbase = m * ne + (k - 1) * nv;
+      Q4 pr{1, 0, 0, 0};
+      if (vk & (VK_BT | VK_VBU | VK_VBV)) pr = relative_rotation(qa, qb);
+      // 0.5*(-+p.w I + [p_v]x) (constraints.cpp:50-51)
+      const double Da[3][3] = {{0.5 * -pr.w, 0.5 * -pr.z, 0.5 * pr.y},
+                               {0.5 * pr.z, 0.5 * -pr.w, 0.5 * -pr.x},
+                               {0.5 * -pr.y, 0.5 * pr.x, 0.5 * -pr.w}};
+      const double Db[3][3] = {{0.5 * pr.w, 0.5 * -pr.z, 0.5 * pr.y},
+                               {0.5 * pr.z, 0.5 * pr.w, 0.5 * -pr.x},
+                               {0.5 * -pr.y, 0.5 * pr.x, 0.5 * pr.w}};
+      if (kind == A_BT && (vk & VK_BT)) {  // BendTwist (:139-155), dim 3
+        const double inv_len = 4.0 / (la + lb);
+        const V3 om = inv_len * qvec(pr);
+        const double s = sp.classic ? sbar : s0;
+        const V3 darb{t.st[T_DARBX][si - 1], t.st[T_DARBY][si - 1], t.st[T_DARBZ][si - 1]};
+        const double W[3] = {s * om.x - sbar * darb.x, s * om.y - sbar * darb.y, s * om.z - sbar * darb.z};
+        const double fs = s * inv_len;
+        double Ja[3][3], Jb[3][3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            Ja[a][b] = fs * Da[a][b];
+            Jb[a][b] = fs * Db[a][b];
+          }
+        const double omv[3] = {om.x, om.y, om.z};
+        const bool sc_on = !sp.classic && is0 != 0.0;
+        double M[3][3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const double sa = h2 * is0 * omv[a];
+          const double ba0 = (h2 * Ja[a][0]) * ita.x, ba1 = (h2 * Ja[a][1]) * ita.y, ba2 = (h2 * Ja[a][2]) * ita.z;
+          const double bb0 = (h2 * Jb[a][0]) * itb.x, bb1 = (h2 * Jb[a][1]) * itb.y, bb2 = (h2 * Jb[a][2]) * itb.z;
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            double v = sc_on ? sa * omv[b] : 0.0;
+            v = v + ((ba0 * Ja[b][0] + ba1 * Ja[b][1]) + ba2 * Ja[b][2]);
+            v = v + ((bb0 * Jb[b][0] + bb1 * Jb[b][1]) + bb2 * Jb[b][2]);
+            M[a][b] = v;
+          }
+        }
+        const double kinv[3] = {inverse_stiffness(t.st[T_KBT0][si]), inverse_stiffness(t.st[T_KBT1][si]),
+                                inverse_stiffness(t.st[T_KBT2][si])};
+        const double lam[3] = {t.st[T_LAM + L_BT0][si], t.st[T_LAM + L_BT1][si], t.st[T_LAM + L_BT2][si]};
+        double rhs[3], dl[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          M[d][d] = M[d][d] + kinv[d];
+          rhs[d] = W[d] - kinv[d] * lam[d];
+        }
+        if (solve3(M, rhs, beta, dl)) {
+          bool ok = isfinite(dl[0]) && isfinite(dl[1]) && isfinite(dl[2]);
+          R.bt_ds = 0.0;
+          if (!sp.classic) {
+            R.bt_ds = -h2 * is0 * ((omv[0] * dl[0] + omv[1] * dl[1]) + omv[2] * dl[2]);
+            ok = ok && isfinite(R.bt_ds);
+          }
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            R.bt_dta[b] = -h2 * (comp(ita, b) * ((Ja[0][b] * dl[0] + Ja[1][b] * dl[1]) + Ja[2][b] * dl[2]));
+            R.bt_dtb[b] = -h2 * (comp(itb, b) * ((Jb[0][b] * dl[0] + Jb[1][b] * dl[1]) + Jb[2][b] * dl[2]));
+            ok = ok && isfinite(R.bt_dta[b]) && isfinite(R.bt_dtb[b]);
+          }
+          t.act[A_BT][pi] = 1;
+          if (owned) {
+            sp.lam_out[L_BT0 * (long long)vp + p] = lam[0] + dl[0];
+            sp.lam_out[L_BT1 * (long long)vp + p] = lam[1] + dl[1];
+            sp.lam_out[L_BT2 * (long long)vp + p] = lam[2] + dl[2];
+            if (!ok) fail(lbase + __popc(vk & (VK_BT - 1)));
+          }
+        } else {
+          nsing += owned;
+          keep_lam(L_BT0, 3);
+        }
+      }
+      if (kind == A_SB && (vk & VK_SB)) {  // SurfaceBending (:156-168), dim 1
+        const double lap = (spp - s0) / lb - (s0 - sm) / la;
+        const double W = lap - t.st[T_SLAP][si - 1];
+        const double jm = 1.0 / la, j0 = -1.0 / la - 1.0 / lb, jp = 1.0 / lb;
+        const double ism = t.st[T_IS][si - 1], isp = t.st[T_IS][si + 1];
+        double M = 0.0;
+        if (ism != 0.0) M = M + (h2 * ism * jm) * jm;
+        if (is0 != 0.0) M = M + (h2 * is0 * j0) * j0;
+        if (isp != 0.0) M = M + (h2 * isp * jp) * jp;
+        const double kinv = inverse_stiffness(t.st[T_KSB][si]);
+        const double lam = t.st[T_LAM + L_SB][si];
+        M = M + kinv;
+        if (M > 1e-250) {
+          const double dl = beta * (W - kinv * lam) / M;
+          R.sb[0] = -h2 * ism * (jm * dl);
+          R.sb[1] = -h2 * is0 * (j0 * dl);
+          R.sb[2] = -h2 * isp * (jp * dl);
+          t.act[A_SB][pi] = 1;
+          if (owned) {
+            sp.lam_out[L_SB * (long long)vp + p] = lam + dl;
+            if (!(isfinite(dl) && isfinite(R.sb[0]) && isfinite(R.sb[1]) && isfinite(R.sb[2])))
+              fail(lbase + __popc(vk & (VK_SB - 1)));
+          }
+        } else {
+          nsing += owned;
+          keep_lam(L_SB, 1);
+        }
+      }
+      if (kind >= A_VBU) {  // VolumeBendU / V (:189-214), dim 1
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int bit = cc == 0 ? VK_VBU : VK_VBV;
+          if (kind != A_VBU + cc || !(vk & bit)) continue;
+          const double la0 = t.st[T_LEN0][si - 1], lb0 = t.st[T_LEN0][si];
+          const double inv_len0 = 4.0 / (la0 + lb0);
+          const double om = inv_len0 * (cc == 0 ? pr.x : pr.y);
+          const double darb = t.st[cc == 0 ? T_DARBX : T_DARBY][si - 1];
+          const double rest_om = darb * (la + lb) / (la0 + lb0);
+          const double s = s0;
+          const double W = s * s * s * om - sbar * sbar * sbar * rest_om;
+          const double js = 3.0 * s * s * om;
+          const double fs = s * s * s * inv_len0;
+          const double ja[3] = {fs * Da[cc][0], fs * Da[cc][1], fs * Da[cc][2]};
+          const double jb[3] = {fs * Db[cc][0], fs * Db[cc][1], fs * Db[cc][2]};
+          double M = 0.0;
+          if (is0 != 0.0) M = M + (h2 * is0 * js) * js;
+          M = M + (((h2 * ja[0]) * ita.x * ja[0] + (h2 * ja[1]) * ita.y * ja[1]) + (h2 * ja[2]) * ita.z * ja[2]);
+          M = M + (((h2 * jb[0]) * itb.x * jb[0] + (h2 * jb[1]) * itb.y * jb[1]) + (h2 * jb[2]) * itb.z * jb[2]);
+          const double kinv = inverse_stiffness(t.st[T_KVB][si]);
+          const int lf = cc == 0 ? L_VBU : L_VBV;
+          const double lam = t.st[T_LAM + lf][si];
+          M = M + kinv;
+          if (M > 1e-250) {
+            const double dl = beta * (W - kinv * lam) / M;
+            R.vb_ds[cc] = -h2 * is0 * (js * dl);
+            bool ok = isfinite(dl) && isfinite(R.vb_ds[cc]);
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+              R.vb_dta[cc][b] = -h2 * (comp(ita, b) * (ja[b] * dl));
+              R.vb_dtb[cc][b] = -h2 * (comp(itb, b) * (jb[b] * dl));
+              ok = ok && isfinite(R.vb_dta[cc][b]) && isfinite(R.vb_dtb[cc][b]);
+            }
+            t.act[cc == 0 ? A_VBU : A_VBV][pi] = 1;
+            if (owned) {
+              sp.lam_out[lf * (long long)vp + p] = lam + dl;
+              if (!ok) fail(lbase + __popc(vk & (bit - 1)));
+            }
+          } else {
+            nsing += owned;
+            keep_lam(lf, 1);
+          }
+        }
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    nsing += __shfl_down_sync(0xffffffffu, nsing, o);
+    const unsigned long long b2 = __shfl_down_sync(0xffffffffu, bad, o);
+    bad = umin64(bad, b2);
+  }
+  if (lane == 0) {
+    if (nsing) atomicAdd(singular, nsing);
+    if (bad != kNoError) atomicMin(err, bad);
+  }
+  __syncthreads();
+
+  // ---- gather in block order (constraints.cpp:509-534) and apply (:537-554)
+  for (int pi = 1 + tid; pi <= kTileOwned; pi += 32 * kWarps) {
+    const int k = t.loc[pi];
+    if (k < 0) continue;
+    const int p = start - 1 + pi;
+    const int m = t.m[pi];
+    const int si = pi + 1;
+    const bool prev_el = k >= 1, has_el = k < m, prev_vx = k - 1 >= 1, has_vx = k >= 1 && k <= m - 1,
+               next_vx = k + 1 <= m - 1;
+    const PosRes& A = t.res[pi - 1];  // element k-1 / vertex k-1
+    const PosRes& B = t.res[pi];      // element k / vertex k
+    const PosRes& N = t.res[pi + 1];  // vertex k+1
+    V3 csum{0, 0, 0};
+    int ccnt = 0;
+    double ssum = 0.0;
+    int scnt = 0;
+    V3 tsum{0, 0, 0};
+    int tcnt = 0;
+    auto addc = [&](const double* d) {
+      csum = csum + V3{d[0], d[1], d[2]};
+      ++ccnt;
+    };
+    auto adds = [&](double d) {
+      ssum += d;
+      ++scnt;
+    };
+    auto addt = [&](const double* d) {
+      tsum = tsum + V3{d[0], d[1], d[2]};
+      ++tcnt;
+    };
+    // element pass: element k-1 (this vertex is its c1/s1), then element k (c0/s0, theta)
+    if (prev_el) {
+      if (t.act[A_SZ][pi - 1]) addc(A.sz_dc1);
+      if (t.act[A_CS][pi - 1]) adds(A.cs[1]);
+      if (t.act[A_SS][pi - 1]) adds(A.ss[1]);
+      if (t.act[A_VS][pi - 1]) {
+        addc(A.vs_dc1);
+        adds(A.vs_ds[1]);
+      }
+    }
+    if (has_el) {
+      if (t.act[A_SZ][pi]) {
+        addc(B.sz_dc0);
+        addt(B.sz_dt);
+      }
+      if (t.act[A_CS][pi]) adds(B.cs[0]);
+      if (t.act[A_SS][pi]) adds(B.ss[0]);
+      if (t.act[A_VS][pi]) {
+        addc(B.vs_dc0);
+        adds(B.vs_ds[0]);
+        addt(B.vs_dt);
+      }
+    }
+    // vertex pass: vertex k-1 (SurfaceBending s_{j+1}), vertex k, vertex k+1
+    if (prev_vx && t.act[A_SB][pi - 1]) adds(A.sb[2]);
+    if (has_vx) {
+      if (t.act[A_BT][pi]) {
+        if (!sp.classic) adds(B.bt_ds);
+        addt(B.bt_dtb);
+      }
+      if (t.act[A_SB][pi]) adds(B.sb[1]);
+      if (t.act[A_VBU][pi]) {
+        adds(B.vb_ds[0]);
+        addt(B.vb_dtb[0]);
+      }
+      if (t.act[A_VBV][pi]) {
+        adds(B.vb_ds[1]);
+        addt(B.vb_dtb[1]);
+      }
+    }
+    if (next_vx) {
+      if (t.act[A_BT][pi + 1]) addt(N.bt_dta);
+      if (t.act[A_SB][pi + 1]) adds(N.sb[0]);
+      if (t.act[A_VBU][pi + 1]) addt(N.vb_dta[0]);
+      if (t.act[A_VBV][pi + 1]) addt(N.vb_dta[1]);
+    }
+    if (has_ext) {  // external blocks touching this vertex, in block order (entries slot-sorted)
+      const int e0 = c.ext_off[p], e1 = c.ext_off[p + 1];
+      for (int q = e0; q < e1; ++q) {
+        const int fl = c.ext_flag[q];
+        if (!fl) continue;
+        const double* o = c.ext_contrib + 4ll * q;
+        addc(o);
+        if (fl & kExtScale) adds(o[3]);
+      }
+    }
+    V3 cn{t.st[T_CX][si], t.st[T_CY][si], t.st[T_CZ][si]};
+    if (ccnt > 0) cn = cn + csum / static_cast<double>(ccnt);
+    double sn = t.st[T_S][si];
+    if (scnt > 0) sn = fmax(sn + ssum / static_cast<double>(scnt), kMinScale);
+    Q4 qn{t.st[T_QW][si], t.st[T_QX][si], t.st[T_QY][si], t.st[T_QZ][si]};
+    if (has_el && tcnt > 0) qn = apply_increment(qn, tsum / static_cast<double>(tcnt));
+    Y[CX * (long long)vp + p] = cn.x;
+    Y[CY * (long long)vp + p] = cn.y;
+    Y[CZ * (long long)vp + p] = cn.z;
+    Y[S * (long long)vp + p] = sn;
+    Y[QW * (long long)vp + p] = qn.w;
+    Y[QX * (long long)vp + p] = qn.x;
+    Y[QY * (long long)vp + p] = qn.y;
+    Y[QZ * (long long)vp + p] = qn.z;
+  }
+}
+
+
+template <int TP>
+void launch_tiles(const World& w, Collide& c, const double* X, double* Y, const SweepParams& sp, int* singular_counter,
+                  unsigned long long* err, cudaStream_t st) {
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_rod_sweep<TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(Tile<TP>));
+  (void)attr;  // a failure surfaces as a launch error
+  const int has_ext = c.ext_cap > 0 ? 1 : 0;
+  const int blocks = (w.V + TP - 3) / (TP - 2);
+  k_rod_sweep<TP><<<blocks, 32 * kWarps, sizeof(Tile<TP>), st>>>(w, c, X, Y, sp, singular_counter, err, has_ext);
+}
+
+}  // namespace
+
+void launch_rod_sweep(const World& w, Collide& c, const double* X, double* Y, const SweepParams& sp,
+                      int* singular_counter, unsigned long long* err, cudaStream_t st) {
+  // 64-wide tiles once they fill every SM twice over (148 SMs x 2 x 62 slots).
+  if (w.V >= 2 * 148 * 62)
+    launch_tiles<64>(w, c, X, Y, sp, singular_counter, err, st);
+  else
+    launch_tiles<32>(w, c, X, Y, sp, singular_counter, err, st);
+}
+
+}  // namespace vdev

@@ -124,8 +124,8 @@ Solver::Solver(const SceneData& scene) : scene_(scene) {
     collide_possible_ = any && c_.P >= 2;
   }
   ext_possible_ = collide_possible_ || c_.n_planes > 0 || c_.n_pins > 0;
-  c_.cand_cap = collide_possible_ ? std::max<long long>(1 << 16, 32ll * c_.P) : 0;
-  c_.contact_cap = collide_possible_ ? std::max<long long>(1 << 15, 16ll * c_.P) : 0;
+  c_.cand_cap = collide_possible_ ? std::max<long long>(1 << 16, 24ll * c_.P) : 0;
+  c_.contact_cap = collide_possible_ ? std::max<long long>(1 << 15, 12ll * c_.P) : 0;
   c_.hp_cap = c_.n_planes * V;
   c_.ext_cap = ext_possible_ ? c_.n_pins + c_.contact_cap + c_.hp_cap : 0;
   c_.pill = dalloc<double>(8ull * std::max(c_.P, 1));
@@ -142,13 +142,16 @@ Solver::Solver(const SceneData& scene) : scene_(scene) {
   c_.cell_cursor = dalloc<int>(c_.T);
   c_.cell_items = dalloc<int>(c_.P);
   c_.pill_cell = dalloc<int>(c_.P);
-  c_.cand_count = dalloc<int>(c_.P + 1);
-  c_.cand_off = dalloc<int>(c_.P + 1);
   c_.cand_i = dalloc<int>(c_.cand_cap);
   c_.cand_j = dalloc<int>(c_.cand_cap);
-  c_.cand_flag = dalloc<int>(c_.cand_cap + 1);
-  c_.cand_pos = dalloc<int>(c_.cand_cap + 1);
-  c_.cand_ab = dalloc<double>(3 * c_.cand_cap);
+  c_.cand2_i = dalloc<int>(c_.cand_cap);
+  c_.cand2_j = dalloc<int>(c_.cand_cap);
+  c_.raw_i = dalloc<int>(c_.contact_cap);
+  c_.raw_j = dalloc<int>(c_.contact_cap);
+  c_.raw_ab = dalloc<double>(2 * c_.contact_cap);
+  c_.ct_cnt = dalloc<int>(c_.P + 1);
+  c_.ct_off = dalloc<int>(c_.P + 1);
+  c_.ct_cur = dalloc<int>(c_.P + 1);
   c_.ct_a = dalloc<int>(c_.contact_cap);
   c_.ct_b = dalloc<int>(c_.contact_cap);
   c_.ct_alpha = dalloc<double>(c_.contact_cap);
@@ -167,8 +170,9 @@ Solver::Solver(const SceneData& scene) : scene_(scene) {
   c_.pin_slot = dalloc<int>(c_.n_pins);
   c_.pin_data = dalloc<double>(4 * std::max(c_.n_pins, 1));
   c_.ext_lam = dalloc<double>(3 * c_.ext_cap);
-  c_.ext_out = dalloc<double>(16 * c_.ext_cap);
-  c_.ext_active = dalloc<uint8_t>(c_.ext_cap);
+  c_.ext_contrib = dalloc<double>(16 * c_.ext_cap);
+  c_.ext_flag = dalloc<uint8_t>(4 * c_.ext_cap);
+  c_.ext_pos = dalloc<int>(4 * c_.ext_cap);
   c_.ext_cnt = dalloc<int>(V + 1);
   c_.ext_off = dalloc<int>(V + 1);
   c_.ext_cur = dalloc<int>(V);

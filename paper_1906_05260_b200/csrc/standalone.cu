@@ -84,8 +84,12 @@ void make_collide(Buf& b, vdev::Collide& c, const vrod_pill* pills, int P, long 
   c.cell_cursor = b.get<int>(c.T);
   c.cell_items = b.get<int>(P);
   c.pill_cell = b.get<int>(P);
-  c.cand_count = b.get<int>(P + 1);
-  c.cand_off = b.get<int>(P + 1);
+  c.raw_i = b.get<int>(cap);
+  c.raw_j = b.get<int>(cap);
+  c.raw_ab = b.get<double>(2 * cap);
+  c.ct_cnt = b.get<int>(P + 1);
+  c.ct_off = b.get<int>(P + 1);
+  c.ct_cur = b.get<int>(P + 1);
   c.cand_i = b.get<int>(cap);
   c.cand_j = b.get<int>(cap);
   c.cand_flag = b.get<int>(cap + 1);
@@ -146,13 +150,13 @@ long long gpu_broad_phase(long long n, const vrod_pill* pills, long long cap_out
     make_collide(b, c, pills, static_cast<int>(n), cap);
     unsigned long long* err = b.get<unsigned long long>(1);
     check_cuda(cudaMemset(err, 0xff, sizeof(unsigned long long)), "err");
-    vdev::launch_broad_narrow(c, 0, err, /*prefilter=*/0, /*do_narrow=*/0, 0, 0, nullptr);
+    vdev::launch_broad_ordered(c, err, nullptr);
     check_cuda(cudaDeviceSynchronize(), "broad_phase");
     unsigned long long e = 0;
     fetch(&e, err, 1);
     if (e != vdev::kNoError) throw std::invalid_argument("broad_phase: non-finite pill");
     int total = 0;
-    fetch(&total, c.cand_off + n, 1);
+    fetch(&total, c.scalars + vdev::SC_NCAND_RAW, 1);
     if (total > cap) {
       cap = total;
       continue;
@@ -160,8 +164,8 @@ long long gpu_broad_phase(long long n, const vrod_pill* pills, long long cap_out
     const long long k = std::min<long long>(total, cap_out);
     if (k > 0 && pairs) {
       std::vector<int> ci(k), cj(k);
-      fetch(ci.data(), c.cand_i, k);
-      fetch(cj.data(), c.cand_j, k);
+      fetch(ci.data(), c.ct_a, k);
+      fetch(cj.data(), c.ct_b, k);
       for (long long q = 0; q < k; ++q) {
         pairs[2 * q] = ci[q];
         pairs[2 * q + 1] = cj[q];

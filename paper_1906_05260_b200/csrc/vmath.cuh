@@ -191,4 +191,34 @@ VHD double inverse_stiffness(double k) {
   return fmin(1.0 / k, 1e30);
 }
 
+// 3x3 solve of solve_block's dim-3 branch (constraints.cpp:446-454): singular test on Eigen's
+// determinant, cofactor inverse, dlambda = beta * M^-1 * rhs.
+VHD bool solve3(const double (&M)[3][3], const double (&rhs)[3], double beta, double (&dl)[3]) {
+  double md = fabs(M[0][0]);
+  for (int j = 0; j < 3; ++j)
+    for (int i = 0; i < 3; ++i) md = fmax(md, fabs(M[i][j]));
+  md = fmax(md, 1e-300);
+  const double det = M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) -
+                     M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                     M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0]);
+  if (fabs(det) <= 1e-14 * md * md * md) return false;
+  const double c00 = M[1][1] * M[2][2] - M[1][2] * M[2][1];
+  const double c10 = M[2][1] * M[0][2] - M[2][2] * M[0][1];
+  const double c20 = M[0][1] * M[1][2] - M[0][2] * M[1][1];
+  const double c01 = M[1][2] * M[2][0] - M[1][0] * M[2][2];
+  const double c11 = M[2][2] * M[0][0] - M[2][0] * M[0][2];
+  const double c21 = M[0][2] * M[1][0] - M[0][0] * M[1][2];
+  const double c02 = M[1][0] * M[2][1] - M[1][1] * M[2][0];
+  const double c12 = M[2][0] * M[0][1] - M[2][1] * M[0][0];
+  const double c22 = M[0][0] * M[1][1] - M[0][1] * M[1][0];
+  const double d = (c00 * M[0][0] + c10 * M[1][0]) + c20 * M[2][0];
+  const double invdet = 1.0 / d;
+  const double inv[3][3] = {{c00 * invdet, c10 * invdet, c20 * invdet},
+                            {c01 * invdet, c11 * invdet, c21 * invdet},
+                            {c02 * invdet, c12 * invdet, c22 * invdet}};
+  for (int i = 0; i < 3; ++i)
+    dl[i] = ((beta * inv[i][0]) * rhs[0] + (beta * inv[i][1]) * rhs[1]) + (beta * inv[i][2]) * rhs[2];
+  return true;
+}
+
 }  // namespace vm

@@ -1,0 +1,23 @@
+"""Aggregate an ncu --metrics gpu__time_duration.sum --csv launch list by kernel."""
+import collections, csv, sys
+
+def main(path, top=25):
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[hi]
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0].replace("(anonymous namespace)::", "").replace("void ", "")
+        v = float(r[vi].replace(",", "")) * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(r[ui], 1.0)
+        agg[name][0] += 1
+        agg[name][1] += v
+    tot = sum(v[1] for v in agg.values())
+    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
+        print(f"{k[-42:]:42s} n={n:5d} total={t:10.1f} us avg={t / n:9.2f} us share={t / tot:6.1%}")
+    print(f"total {tot / 1e3:.3f} ms over {sum(v[0] for v in agg.values())} launches")
+
+if __name__ == "__main__":
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25)
