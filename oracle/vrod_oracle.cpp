@@ -5,7 +5,7 @@
 // bundling,scene,solver}.cpp`) function by function, each citing the file:line it follows,
 // and exports the same C-ABI as the product (include/vrod_capi.h). Its arithmetic order
 // mirrors the reference compiled against oracle/shim/Eigen (oracle/_ref), and
-// tests/test_oracle_vs_ref.py pins it there bit for bit. Only tests/, __graft_entry__.smoke()
+// tests/test_oracle_pinning.py pins it there bit for bit. Only tests/, __graft_entry__.smoke()
 // and bench.py's cpu_baseline leg load it — never the product path.
 
 #include <algorithm>
