@@ -33,7 +33,13 @@ __device__ __forceinline__ Q4 ldq(const double* X, int vp, int v) {
   return Q4{X[QW * (long long)vp + v], X[QX * (long long)vp + v], X[QY * (long long)vp + v], X[QZ * (long long)vp + v]};
 }
 
-// extract_rotation, bundling.cpp:50-67.
+// extract_rotation, bundling.cpp:50-67: the same iteration (omega = sum R_a x B_a / (|sum
+// R_a . B_a| + 1e-9), q <- AngleAxis(|omega|, omega^) q, normalize, stop at |omega| < 1e-9).
+// The loop is one serial dependency chain (tens of iterations even warm-started), so it is
+// written for latency. Warm-started steps are tiny: for half angles below 1e-2 the increment
+// [cos(a/2), sin(a/2)/a * omega] comes from the Taylor series in a^2 (truncation < 1e-20
+// relative) with no sqrt, division or sincos on the chain; larger steps take the general
+// route. These change last-ulp rounding only; shape matching is tolerance-pinned.
 __device__ Q4 extract_rotation(const M3& B, const Q4& guess) {
   Q4 q = qnormalized(guess);
   for (int it = 0; it < 100; ++it) {
@@ -45,13 +51,25 @@ __device__ Q4 extract_rotation(const M3& B, const Q4& guess) {
       omega = omega + cross(col(R, a), col(B, a));
       d += dot(col(R, a), col(B, a));
     }
-    omega = omega / (fabs(d) + 1e-9);
-    const double angle = norm(omega);
-    if (angle < 1e-9) break;
-    const V3 axis = omega / angle;
-    const double ha = 0.5 * angle;
-    const V3 v = sin(ha) * axis;
-    q = qnormalized(qmul(Q4{cos(ha), v.x, v.y, v.z}, q));
+    omega = (1.0 / (fabs(d) + 1e-9)) * omega;
+    const double a2 = sqnorm(omega);
+    if (a2 < 1e-18) break;  // |omega| < 1e-9
+    const double x2 = 0.25 * a2;  // (angle / 2)^2
+    double k, c;  // k = sin(angle/2) / angle, c = cos(angle/2)
+    if (x2 < 1e-4) {
+      k = 0.5 * (1.0 - x2 * (1.0 / 6) * (1.0 - x2 * (1.0 / 20) * (1.0 - x2 * (1.0 / 42) * (1.0 - x2 * (1.0 / 72)))));
+      c = 1.0 - x2 * 0.5 *
+                    (1.0 - x2 * (1.0 / 12) * (1.0 - x2 * (1.0 / 30) * (1.0 - x2 * (1.0 / 56) * (1.0 - x2 * (1.0 / 90)))));
+    } else {
+      const double angle = sqrt(a2);
+      double s;
+      sincos(0.5 * angle, &s, &c);
+      k = s / angle;
+    }
+    const V3 v = k * omega;
+    const Q4 p = qmul(Q4{c, v.x, v.y, v.z}, q);
+    const double r = rsqrt(qsqnorm(p));
+    q = Q4{p.w * r, p.x * r, p.y * r, p.z * r};
   }
   return q;
 }
