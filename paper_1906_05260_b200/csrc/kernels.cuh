@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <utility>
 
 #include "world.cuh"
 
@@ -140,9 +141,36 @@ struct SweepParams {
   int n_pins;
   int elastic_blocks;  // first external block index in the reference's block list
   double contact_k;    // settings.contact_stiffness
+  // Programmatic dependent launch inside the iteration loop: 0 off; 1 the kernel waits for its
+  // predecessor before touching any state; 2 (rod sweep right after an ext solve) it stages
+  // and solves its tile first and waits only before gathering the external contributions.
+  int pdl;
   const double* lam_in;  // elastic multipliers before this sweep (kLamFields x vpad)
   double* lam_out;       // after this sweep (ping-pong partner)
 };
+
+// Programmatic dependent launch (sm_90+): the next kernel in the stream may start while this
+// one finishes; griddepcontrol.wait blocks until the predecessor grid has completed and its
+// writes are visible. Each kernel triggers its dependents only after its own wait, so a
+// kernel's pre-wait prologue overlaps only the post-wait tail of its predecessor.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+template <typename... Exp, typename... Act>
+inline void launch_kernel(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                          Act&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...);
+}
 
 // scan.cu
 void scan_exclusive(const int* in, int* out, long long n_cap, const int* n_dev, int* partials, int parts,
@@ -186,6 +214,6 @@ void launch_penetration(const World& w, Collide& c, const double* X, StepAccum* 
 int report_parts(int V);
 
 // shape.cu
-void launch_shape_match(const World& w, const Groups& g, double* X, const int* level_off_host, cudaStream_t st);
+void launch_shape_match(const World& w, const Groups& g, double* X, const int* level_off_host, bool pdl, cudaStream_t st);
 
 }  // namespace vdev

@@ -114,6 +114,10 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int kTilePos = TP, kTileOwned = TP - 2, kTileStage = TP + 2;
   Tile<TP>& t = *reinterpret_cast<Tile<TP>*>(smem_raw);
+  if (sp.pdl == 1) {  // predecessor wrote X: wait before staging
+    pdl_wait();
+    pdl_trigger();
+  }
   const int V = w.V, vp = w.vpad;
   const int start = blockIdx.x * kTileOwned;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -528,6 +532,10 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
     if (bad != kNoError) atomicMin(err, bad);
   }
   __syncthreads();
+  if (sp.pdl == 2) {  // predecessor = the ext solve of this iteration: its entries are read below
+    pdl_wait();
+    pdl_trigger();
+  }
 
   // ---- gather in block order (constraints.cpp:509-534) and apply (:537-554)
   for (int pi = 1 + tid; pi <= kTileOwned; pi += 32 * kWarps) {
@@ -641,7 +649,8 @@ void launch_tiles(const World& w, Collide& c, const double* X, double* Y, const 
   (void)attr;  // a failure surfaces as a launch error
   const int has_ext = c.ext_cap > 0 ? 1 : 0;
   const int blocks = (w.V + TP - 3) / (TP - 2);
-  k_rod_sweep<TP><<<blocks, 32 * kWarps, sizeof(Tile<TP>), st>>>(w, c, X, Y, sp, singular_counter, err, has_ext);
+  launch_kernel(k_rod_sweep<TP>, blocks, 32 * kWarps, sizeof(Tile<TP>), st, sp.pdl != 0, w, c, X, Y, sp, singular_counter,
+                err, has_ext);
 }
 
 }  // namespace

@@ -74,7 +74,11 @@ __device__ Q4 extract_rotation(const M3& B, const Q4& guess) {
   return q;
 }
 
-__global__ void k_shape_level(World w, Groups g, double* __restrict__ X, int gbeg, int gend) {
+__global__ void k_shape_level(World w, Groups g, double* __restrict__ X, int gbeg, int gend, int pdl) {
+  if (pdl) {
+    pdl_wait();
+    pdl_trigger();
+  }
   const int lane = threadIdx.x & 31;
   const int gi = gbeg + (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   if (gi >= gend) return;
@@ -188,13 +192,13 @@ __global__ void k_shape_level(World w, Groups g, double* __restrict__ X, int gbe
 
 }  // namespace
 
-void launch_shape_match(const World& w, const Groups& g, double* X, const int* level_off_host, cudaStream_t st) {
+void launch_shape_match(const World& w, const Groups& g, double* X, const int* level_off_host, bool pdl, cudaStream_t st) {
   for (int l = 0; l < g.levels; ++l) {
     const int gb = level_off_host[l], ge = level_off_host[l + 1];
     const int ng = ge - gb;
     if (ng <= 0) continue;
     const int blocks = (ng + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    k_shape_level<<<blocks, 32 * kWarpsPerBlock, 0, st>>>(w, g, X, gb, ge);
+    launch_kernel(k_shape_level, blocks, 32 * kWarpsPerBlock, 0, st, pdl, w, g, X, gb, ge, pdl ? 1 : 0);
   }
 }
 

@@ -590,7 +590,9 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
     double* cur = w_.X;
     double* nxt = w_.Y;
     vdev::SweepParams sp{h, h2, scene_.settings.beta, classic_ ? 1 : 0, 0, s, c_.n_pins, setup_.elastic_blocks,
-                         scene_.settings.contact_k, nullptr, nullptr};
+                         scene_.settings.contact_k, 0, nullptr, nullptr};
+    // Programmatic dependent launch only between the loop's kernels (no event brackets there).
+    const bool pdl = pdl_ && !prof;
     double* lam_a = w_.lam;
     double* lam_b = w_.lam + static_cast<std::size_t>(vdev::kLamFields) * w_.vpad;
     for (int it = 0; it < iterations; ++it) {
@@ -599,16 +601,18 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
       sp.lam_out = (it & 1) ? lam_a : lam_b;
       if (c_.ext_cap > 0) {
         begin(CAT_EXT_SOLVE);
+        sp.pdl = pdl ? 1 : 0;
         vdev::launch_ext_solve(w_, c_, cur, sp, d_singular_ + it, d_err_, st);
         end();
       }
       begin(CAT_ROD_SWEEP);
+      sp.pdl = !pdl ? 0 : (c_.ext_cap > 0 ? 2 : 1);
       vdev::launch_rod_sweep(w_, c_, cur, nxt, sp, d_singular_ + it, d_err_, st);
       end();
       std::swap(cur, nxt);
       if (g_.G > 0 && (it + 1) % scene_.settings.sm_period == 0) {
         begin(CAT_SHAPE);
-        vdev::launch_shape_match(w_, g_, cur, level_off_.data(), st);
+        vdev::launch_shape_match(w_, g_, cur, level_off_.data(), pdl, st);
         end();
       }
       if (probe_log) vdev::launch_residuals(w_, cur, w_.classic, d_report_partials_, report_parts_, probe_log + 8 * it, st);

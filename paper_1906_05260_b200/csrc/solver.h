@@ -2,6 +2,8 @@
 // Owns the device world, replays one CUDA graph per step(), mirrors the reference's queries.
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include <memory>
@@ -100,6 +102,8 @@ class Solver {
   int step_index_ = 0;
   int kernels_per_step_ = 0;
   bool use_graph_ = true;
+  // programmatic dependent launch in the iteration loop (VROD_PDL=0 disables, for A/B runs)
+  bool pdl_ = !(std::getenv("VROD_PDL") && std::getenv("VROD_PDL")[0] == '0');
 
   cudaStream_t stream_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;

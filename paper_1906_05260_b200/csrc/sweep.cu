@@ -88,6 +88,10 @@ __device__ double ext_residual(const World& w, const Collide& c, const double* X
 
 __global__ void k_ext_solve(World w, Collide c, const double* __restrict__ X, SweepParams sp, int* singular,
                             unsigned long long* err) {
+  if (sp.pdl) {
+    pdl_wait();
+    pdl_trigger();
+  }
   const double contact_k = sp.contact_k;
   const int elastic_blocks = sp.elastic_blocks;
   const int npins = sp.n_pins;
@@ -473,7 +477,8 @@ void launch_ext_setup(const World& w, Collide& c, cudaStream_t st) {
 
 void launch_ext_solve(const World& w, Collide& c, const double* X, const SweepParams& sp, int* singular_counter,
                       unsigned long long* err, cudaStream_t st) {
-  if (c.ext_cap > 0) k_ext_solve<<<grid_for(c.ext_cap), kThreads, 0, st>>>(w, c, X, sp, singular_counter, err);
+  if (c.ext_cap > 0)
+    launch_kernel(k_ext_solve, grid_for(c.ext_cap), kThreads, 0, st, sp.pdl != 0, w, c, X, sp, singular_counter, err);
 }
 
 void launch_iteration(const World& w, Collide& c, const double* X, double* Y, const SweepParams& sp,
