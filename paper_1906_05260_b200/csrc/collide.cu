@@ -214,6 +214,8 @@ __device__ __forceinline__ bool pair_allowed(int ra, int ga, bool sa, int ea, in
 
 // rod_pills from the predicted state + the posed kinematic pills of this substep.
 __global__ void k_build_pills(World w, Collide c, const double* __restrict__ anim, AnimLayout al) {
+  pdl_wait();
+  pdl_trigger();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   const int P = c.P;
   if (v < w.V) {
@@ -242,6 +244,8 @@ __global__ void k_build_pills(World w, Collide c, const double* __restrict__ ani
 
 // Bounding spheres, max radius, finiteness (broad_phase, collision.cpp:189-196).
 __global__ void k_bounds(Collide c, int substep, unsigned long long* err) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long bits = 0;
   if (i < c.P) {
@@ -278,6 +282,8 @@ __device__ __forceinline__ long long key1(double x, double inv) {
 }
 
 __global__ void k_insert(Collide c) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= c.P) return;
   const double inv = cell_inv(c);
@@ -302,6 +308,8 @@ __global__ void k_insert(Collide c) {
 }
 
 __global__ void k_scatter(Collide c) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= c.P) return;
   const int h = c.pill_cell[i];
@@ -397,6 +405,8 @@ __device__ __forceinline__ bool may_penetrate(const Collide& c, int i, int j) {
 constexpr int kPairWarps = 8;
 __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_warp(Collide c, int prefilter, int* broad_total,
                                                                 int* cand_total) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int s_start[kPairWarps][27];
   __shared__ int s_off[kPairWarps][28];
   __shared__ int s_cnt[kPairWarps];
@@ -495,6 +505,8 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_warp(Collide c, int p
 // pairs that may penetrate to the candidate list. Appends are warp-aggregated (one atomic per
 // warp); the list is unordered — contacts are put in (i, j) order after the narrow phase.
 __global__ void k_pairs(Collide c, int prefilter, int* broad_total, int* cand_total) {
+  pdl_wait();
+  pdl_trigger();
   const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   const int lane = threadIdx.x & 31;
   int broad = 0, ncand = 0, h = -1, i = 0;
@@ -552,6 +564,8 @@ __global__ void k_pairs(Collide c, int prefilter, int* broad_total, int* cand_to
 // survivors are compacted (warp-aggregated append) into cand2 so the expensive narrow phase
 // runs without divergence.
 __global__ void k_seg_filter(Collide c) {
+  pdl_wait();
+  pdl_trigger();
   const int n = c.scalars[SC_NCAND];
   const int lane = threadIdx.x & 31;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
@@ -581,6 +595,8 @@ __global__ void k_seg_filter(Collide c) {
 // Narrow phase over the unordered candidates; penetrating pairs are appended (warp-aggregated)
 // to the raw contact list.
 __global__ void k_narrow_append(Collide c, int split_warm) {
+  pdl_wait();
+  pdl_trigger();
   const int n = c.scalars[SC_NCAND2];
   const int nrr = c.scalars[SC_NRR_PREV], nrk = c.scalars[SC_NRK_PREV];
   const int lane = threadIdx.x & 31;
@@ -619,11 +635,15 @@ __global__ void k_narrow_append(Collide c, int split_warm) {
 
 // (i, j) ordering of the raw contacts: count per pill i -> scan -> scatter -> per-i sort by j.
 __global__ void k_ct_count(Collide c) {
+  pdl_wait();
+  pdl_trigger();
   const int n = c.scalars[SC_NCT];
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
     atomicAdd(&c.ct_cnt[c.raw_i[k]], 1);
 }
 __global__ void k_ct_scatter(Collide c) {
+  pdl_wait();
+  pdl_trigger();
   const int n = c.scalars[SC_NCT];
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const int i = c.raw_i[k];
@@ -635,6 +655,8 @@ __global__ void k_ct_scatter(Collide c) {
   }
 }
 __global__ void k_ct_sort(Collide c) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= c.P) return;
   const int s0 = c.ct_off[i], s1 = c.ct_off[i + 1];
@@ -654,6 +676,8 @@ __global__ void k_ct_sort(Collide c) {
   }
 }
 __global__ void k_clamp_raw(int* scalars, int raw, int out, long long cap, int ovf_code) {
+  pdl_wait();
+  pdl_trigger();
   const int t = scalars[raw];
   if (t > cap) atomicExch(&scalars[SC_OVF], ovf_code);
   scalars[out] = t > cap ? static_cast<int>(cap) : t;
@@ -661,6 +685,8 @@ __global__ void k_clamp_raw(int* scalars, int raw, int out, long long cap, int o
 
 // Narrow phase over the candidate list (find_contacts, collision.cpp:261-271).
 __global__ void k_narrow(Collide c, int split_warm, int store_d) {
+  pdl_wait();
+  pdl_trigger();
   const int n = c.scalars[SC_NCAND];
   const int nrr = c.scalars[SC_NRR_PREV], nrk = c.scalars[SC_NRK_PREV];
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
@@ -679,6 +705,8 @@ __global__ void k_narrow(Collide c, int split_warm, int store_d) {
 }
 
 __global__ void k_compact_contacts(Collide c) {
+  pdl_wait();
+  pdl_trigger();
   const int n = c.scalars[SC_NCAND];
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
     if (!c.cand_flag[q]) continue;
@@ -693,6 +721,8 @@ __global__ void k_compact_contacts(Collide c) {
 }
 
 __global__ void k_contact_count(Collide c, StepAccum* acc) {
+  pdl_wait();
+  pdl_trigger();
   atomicAdd(&acc->contact_count, c.scalars[SC_NCT]);
   atomicAdd(&acc->broad_pairs, c.scalars[SC_BROAD]);
   if (c.scalars[SC_NCT_RAW] > acc->max_contacts) acc->max_contacts = c.scalars[SC_NCT_RAW];
@@ -700,6 +730,8 @@ __global__ void k_contact_count(Collide c, StepAccum* acc) {
 }
 
 __global__ void k_cand_to_raw(Collide c) {
+  pdl_wait();
+  pdl_trigger();
   const int n = c.scalars[SC_NCAND];
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     c.raw_i[k] = c.cand_i[k];
@@ -714,11 +746,15 @@ __global__ void k_cand_to_raw(Collide c) {
 // Rod-rod contacts in (i, j) order have increasing keys; contacts with a kinematic pill are
 // kept in a second list, also increasing in key, so both are searchable by lower_bound.
 __global__ void k_warm_flags(Collide c) {
+  pdl_wait();
+  pdl_trigger();
   const int n = c.scalars[SC_NCT];
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
     c.rk_flag[k] = (c.pill_rod[c.ct_a[k]] < 0 || c.pill_rod[c.ct_b[k]] < 0) ? 1 : 0;
 }
 __global__ void k_warm_build(Collide c, int split) {
+  pdl_wait();
+  pdl_trigger();
   const int n = c.scalars[SC_NCT];
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const unsigned long long key = pair_key(c.pill_id[c.ct_a[k]], c.pill_id[c.ct_b[k]]);
@@ -737,6 +773,8 @@ __global__ void k_warm_build(Collide c, int split) {
   }
 }
 __global__ void k_warm_counts(Collide c, int split) {
+  pdl_wait();
+  pdl_trigger();
   const int n = c.scalars[SC_NCT];
   const int nrk = split ? c.rk_pos[n] : 0;
   c.scalars[SC_NRK_PREV] = nrk;
@@ -745,6 +783,8 @@ __global__ void k_warm_counts(Collide c, int split) {
 
 // Half-plane blocks (solver.cpp:229-249): plane-major, then global vertex order.
 __global__ void k_hp_flags(World w, Collide c) {
+  pdl_wait();
+  pdl_trigger();
   const long long n = static_cast<long long>(c.n_planes) * w.V;
   for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < n;
        q += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -760,6 +800,8 @@ __global__ void k_hp_flags(World w, Collide c) {
   }
 }
 __global__ void k_hp_compact(World w, Collide c) {
+  pdl_wait();
+  pdl_trigger();
   const long long n = static_cast<long long>(c.n_planes) * w.V;
   for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < n;
        q += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -783,6 +825,8 @@ __device__ __forceinline__ PillV from_aos(const PillAoS& p) {
 }
 __global__ void k_pill_project(long long n, const double* __restrict__ x, const PillAoS* __restrict__ pills,
                                double* t, double* d, uint8_t* deg) {
+  pdl_wait();
+  pdl_trigger();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const PillPrep p = prep_pill(from_aos(pills[i]));
@@ -796,6 +840,8 @@ __global__ void k_pill_project(long long n, const double* __restrict__ x, const 
 }
 __global__ void k_deepest(long long n, const PillAoS* __restrict__ a, const PillAoS* __restrict__ b, int iters,
                           const double* __restrict__ warm, double* alpha, double* beta, double* dist) {
+  pdl_wait();
+  pdl_trigger();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     double al, be, d;
@@ -817,9 +863,9 @@ int grid_for(long long n) {
 // prefilter=0 keeps every allowed pair (the standalone broad_phase contract).
 void launch_narrow_only(Collide& c, int split_warm, int store_d, cudaStream_t st) {
   const int g = grid_for(c.cand_cap);
-  k_narrow<<<g, kThreads, 0, st>>>(c, split_warm, store_d);
+  launch_kernel(k_narrow, g, kThreads, 0, st, g_pdl, c, split_warm, store_d);
   scan_exclusive(c.cand_flag, c.cand_pos, c.cand_cap, c.scalars + SC_NCAND, c.scan_tmp, c.scan_parts, st);
-  k_compact_contacts<<<g, kThreads, 0, st>>>(c);
+  launch_kernel(k_compact_contacts, g, kThreads, 0, st, g_pdl, c);
 }
 
 // Puts the first scalars[SC_NCT] raw (i, j, alpha, beta) records into (i, j) order in ct_*.
@@ -827,10 +873,10 @@ void launch_order_contacts(Collide& c, cudaStream_t st) {
   const int g = grid_for(c.contact_cap);
   cudaMemsetAsync(c.ct_cnt, 0, sizeof(int) * (c.P + 1), st);
   cudaMemsetAsync(c.ct_cur, 0, sizeof(int) * (c.P + 1), st);
-  k_ct_count<<<g, kThreads, 0, st>>>(c);
+  launch_kernel(k_ct_count, g, kThreads, 0, st, g_pdl, c);
   scan_exclusive(c.ct_cnt, c.ct_off, c.P, nullptr, c.scan_tmp, c.scan_parts, st);
-  k_ct_scatter<<<g, kThreads, 0, st>>>(c);
-  k_ct_sort<<<(c.P + kThreads - 1) / kThreads, kThreads, 0, st>>>(c);
+  launch_kernel(k_ct_scatter, g, kThreads, 0, st, g_pdl, c);
+  launch_kernel(k_ct_sort, (c.P + kThreads - 1) / kThreads, kThreads, 0, st, g_pdl, c);
 }
 
 // Broad + narrow phase on the pill arrays already in `c` (pill, pill_rod/el/group/self/id).
@@ -849,71 +895,69 @@ void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
   cudaMemsetAsync(c.scalars + SC_NCAND_RAW, 0, sizeof(int), st);
   cudaMemsetAsync(c.scalars + SC_NCT_RAW, 0, sizeof(int), st);
   if (P > 0) {
-    k_bounds<<<b, kThreads, 0, st>>>(c, substep, err);
-    k_insert<<<b, kThreads, 0, st>>>(c);
+    launch_kernel(k_bounds, b, kThreads, 0, st, g_pdl, c, substep, err);
+    launch_kernel(k_insert, b, kThreads, 0, st, g_pdl, c);
   }
   scan_exclusive(c.cell_count, c.cell_start, c.T, nullptr, c.scan_tmp, c.scan_parts, st);
   if (P > 0) {
-    k_scatter<<<b, kThreads, 0, st>>>(c);
-    k_pairs_warp<<<(P + kPairWarps - 1) / kPairWarps, 32 * kPairWarps, 0, st>>>(c, prefilter, c.scalars + SC_BROAD,
-                                                                              c.scalars + SC_NCAND_RAW);
+    launch_kernel(k_scatter, b, kThreads, 0, st, g_pdl, c);
+    launch_kernel(k_pairs_warp, (P + kPairWarps - 1) / kPairWarps, 32 * kPairWarps, 0, st, g_pdl, c, prefilter, c.scalars + SC_BROAD, c.scalars + SC_NCAND_RAW);
   }
-  k_clamp_raw<<<1, 1, 0, st>>>(c.scalars, SC_NCAND_RAW, SC_NCAND, c.cand_cap, 1);
+  launch_kernel(k_clamp_raw, 1, 1, 0, st, g_pdl, c.scalars, SC_NCAND_RAW, SC_NCAND, c.cand_cap, 1);
   if (!do_narrow) return;
   cudaMemsetAsync(c.scalars + SC_NCAND2, 0, sizeof(int), st);
-  k_seg_filter<<<grid_for(c.cand_cap), kThreads, 0, st>>>(c);
-  k_narrow_append<<<grid_for(c.cand_cap), kThreads, 0, st>>>(c, split_warm);
-  k_clamp_raw<<<1, 1, 0, st>>>(c.scalars, SC_NCT_RAW, SC_NCT, c.contact_cap, 2);
+  launch_kernel(k_seg_filter, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c);
+  launch_kernel(k_narrow_append, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c, split_warm);
+  launch_kernel(k_clamp_raw, 1, 1, 0, st, g_pdl, c.scalars, SC_NCT_RAW, SC_NCT, c.contact_cap, 2);
   launch_order_contacts(c, st);
 }
 
 // Standalone broad_phase: every allowed pair, in the reference's (i, j) order.
 void launch_broad_ordered(Collide& c, unsigned long long* err, cudaStream_t st) {
   launch_broad_narrow(c, 0, err, 0, 0, 0, 0, st);
-  k_cand_to_raw<<<grid_for(c.cand_cap), kThreads, 0, st>>>(c);
+  launch_kernel(k_cand_to_raw, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c);
   launch_order_contacts(c, st);
 }
 
 void launch_collide(const World& w, Collide& c, const double* anim, const AnimLayout& al, int substep,
                     unsigned long long* err, StepAccum* acc, int possible, cudaStream_t st) {
   const int nb = (std::max(w.V, al.n_kin) + kThreads - 1) / kThreads;
-  k_build_pills<<<nb, kThreads, 0, st>>>(w, c, anim, al);
+  launch_kernel(k_build_pills, nb, kThreads, 0, st, g_pdl, w, c, anim, al);
   if (!possible) {  // no pair can pass pair_allowed: only broad_phase's finiteness check remains
-    if (c.P >= 2) k_bounds<<<(c.P + kThreads - 1) / kThreads, kThreads, 0, st>>>(c, substep, err);
+    if (c.P >= 2) launch_kernel(k_bounds, (c.P + kThreads - 1) / kThreads, kThreads, 0, st, g_pdl, c, substep, err);
     return;
   }
   const int split = w.K > 0 ? 1 : 0;
   launch_broad_narrow(c, substep, err, 1, 1, split, 0, st);
-  k_contact_count<<<1, 1, 0, st>>>(c, acc);
+  launch_kernel(k_contact_count, 1, 1, 0, st, g_pdl, c, acc);
   const int g = grid_for(c.contact_cap);
   if (split) {
-    k_warm_flags<<<g, kThreads, 0, st>>>(c);
+    launch_kernel(k_warm_flags, g, kThreads, 0, st, g_pdl, c);
     scan_exclusive(c.rk_flag, c.rk_pos, c.contact_cap, c.scalars + SC_NCT, c.scan_tmp, c.scan_parts, st);
   }
-  k_warm_build<<<g, kThreads, 0, st>>>(c, split);
-  k_warm_counts<<<1, 1, 0, st>>>(c, split);
+  launch_kernel(k_warm_build, g, kThreads, 0, st, g_pdl, c, split);
+  launch_kernel(k_warm_counts, 1, 1, 0, st, g_pdl, c, split);
 }
 
 void launch_halfplanes(const World& w, Collide& c, cudaStream_t st) {
   if (c.n_planes == 0) return;
   const long long n = static_cast<long long>(c.n_planes) * w.V;
   const int g = grid_for(n);
-  k_hp_flags<<<g, kThreads, 0, st>>>(w, c);
+  launch_kernel(k_hp_flags, g, kThreads, 0, st, g_pdl, w, c);
   scan_exclusive(c.hp_flag, c.hp_pos, n, nullptr, c.scan_tmp, c.scan_parts, st);
-  k_hp_compact<<<g, kThreads, 0, st>>>(w, c);
+  launch_kernel(k_hp_compact, g, kThreads, 0, st, g_pdl, w, c);
 }
 
 void launch_pill_project(long long n, const double* x, const double* pills, double* t, double* d, uint8_t* deg,
                          cudaStream_t st) {
   if (n <= 0) return;
-  k_pill_project<<<grid_for(n), kThreads, 0, st>>>(n, x, reinterpret_cast<const PillAoS*>(pills), t, d, deg);
+  launch_kernel(k_pill_project, grid_for(n), kThreads, 0, st, g_pdl, n, x, reinterpret_cast<const PillAoS*>(pills), t, d, deg);
 }
 
 void launch_deepest(long long n, const double* a, const double* b, int iters, const double* warm, double* alpha,
                     double* beta, double* dist, cudaStream_t st) {
   if (n <= 0) return;
-  k_deepest<<<grid_for(n), kThreads, 0, st>>>(n, reinterpret_cast<const PillAoS*>(a),
-                                              reinterpret_cast<const PillAoS*>(b), iters, warm, alpha, beta, dist);
+  launch_kernel(k_deepest, grid_for(n), kThreads, 0, st, g_pdl, n, reinterpret_cast<const PillAoS*>(a), reinterpret_cast<const PillAoS*>(b), iters, warm, alpha, beta, dist);
 }
 
 }  // namespace vdev

@@ -16,6 +16,8 @@ __device__ __forceinline__ double F(const double* a, int f, int vpad, int i) { r
 __device__ __forceinline__ double& Fr(double* a, int f, int vpad, int i) { return a[static_cast<long long>(f) * vpad + i]; }
 
 __global__ void k_pin_motions(World w, const double* __restrict__ anim, AnimLayout al, const int* __restrict__ pm_slot) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= al.n_pm) return;
   const int v = pm_slot[i];
@@ -31,6 +33,8 @@ __global__ void k_pin_motions(World w, const double* __restrict__ anim, AnimLayo
 __global__ void k_activation(World w, const double* __restrict__ anim, AnimLayout al, const int* __restrict__ rod_off,
                              const int* __restrict__ act_list, double* applied, const int* __restrict__ act_rods,
                              const double* __restrict__ act_static) {
+  pdl_wait();
+  pdl_trigger();
   const int r = act_rods[blockIdx.x];
   const int v0 = w.rod_vbase[r];
   const int n = w.rod_n[r];
@@ -97,6 +101,8 @@ __global__ void k_activation(World w, const double* __restrict__ anim, AnimLayou
 // prediction check (:179-181). Also takes the pre-predict snapshot (solver.cpp:311-316).
 __global__ void k_predict_vertices(World w, const double* __restrict__ anim, AnimLayout al, V3 g, double h,
                                    int substep, unsigned long long* err) {
+  pdl_wait();
+  pdl_trigger();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= w.V) return;
   const int vp = w.vpad;
@@ -166,6 +172,8 @@ __global__ void k_predict_vertices(World w, const double* __restrict__ anim, Ani
 // predict_rod element loop (solver.cpp:60-72) + refresh_orientation_inertia (layout.cpp:76-93)
 // from the predicted scales.
 __global__ void k_predict_elements(World w, double h, int substep, unsigned long long* err) {
+  pdl_wait();
+  pdl_trigger();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= w.V) return;
   const int k = w.slot_loc[v];
@@ -211,6 +219,8 @@ __global__ void k_predict_elements(World w, double h, int substep, unsigned long
 // post_step_scales (classic mode, solver.cpp:253-271) + finalize_velocities (:273-289).
 // Reads the final sweep buffer `src`, writes the canonical state X and the velocities.
 __global__ void k_finalize(World w, const double* __restrict__ src, double h, double keep) {
+  pdl_wait();
+  pdl_trigger();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= w.V) return;
   const int vp = w.vpad;
@@ -258,6 +268,8 @@ __global__ void k_finalize(World w, const double* __restrict__ src, double h, do
 }
 
 __global__ void k_copy_state(int V, int vpad, const double* __restrict__ src, double* __restrict__ dst) {
+  pdl_wait();
+  pdl_trigger();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= V) return;
 #pragma unroll
@@ -269,11 +281,11 @@ __global__ void k_copy_state(int V, int vpad, const double* __restrict__ src, do
 void launch_animate(const World& w, const double* anim, const AnimLayout& al, const int* pm_slot,
                     const int* act_rod_off, const int* act_list, double* act_applied, const int* act_rods,
                     int n_act_rods, cudaStream_t st) {
-  if (al.n_pm > 0) k_pin_motions<<<(al.n_pm + 127) / 128, 128, 0, st>>>(w, anim, al, pm_slot);
+  if (al.n_pm > 0) launch_kernel(k_pin_motions, (al.n_pm + 127) / 128, 128, 0, st, g_pdl, w, anim, al, pm_slot);
   if (n_act_rods > 0) {
     // act_static follows act_applied in the same allocation (see solver.cu)
     const double* act_static = act_applied + al.n_act;
-    k_activation<<<n_act_rods, 128, 0, st>>>(w, anim, al, act_rod_off, act_list, act_applied, act_rods, act_static);
+    launch_kernel(k_activation, n_act_rods, 128, 0, st, g_pdl, w, anim, al, act_rod_off, act_list, act_applied, act_rods, act_static);
   }
 }
 
@@ -281,16 +293,16 @@ void launch_predict(const World& w, const double* anim, const AnimLayout& al, co
                     int substep, unsigned long long* err, cudaStream_t st) {
   const V3 g{gravity_h[0], gravity_h[1], gravity_h[2]};
   const int b = (w.V + 127) / 128;
-  k_predict_vertices<<<b, 128, 0, st>>>(w, anim, al, g, h, substep, err);
-  k_predict_elements<<<b, 128, 0, st>>>(w, h, substep, err);
+  launch_kernel(k_predict_vertices, b, 128, 0, st, g_pdl, w, anim, al, g, h, substep, err);
+  launch_kernel(k_predict_elements, b, 128, 0, st, g_pdl, w, h, substep, err);
 }
 
 void launch_finalize_from(const World& w, const double* src, double h, double keep, cudaStream_t st) {
-  k_finalize<<<(w.V + 127) / 128, 128, 0, st>>>(w, src, h, keep);
+  launch_kernel(k_finalize, (w.V + 127) / 128, 128, 0, st, g_pdl, w, src, h, keep);
 }
 
 void launch_copy_state(const World& w, const double* src, double* dst, cudaStream_t st) {
-  k_copy_state<<<(w.V + 127) / 128, 128, 0, st>>>(w.V, w.vpad, src, dst);
+  launch_kernel(k_copy_state, (w.V + 127) / 128, 128, 0, st, g_pdl, w.V, w.vpad, src, dst);
 }
 
 }  // namespace vdev

@@ -156,6 +156,10 @@ struct SweepParams {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
+// Set by Solver::record_step while it records a step: every launch of the step then carries the
+// programmatic-serialization attribute, and every kernel opens with pdl_wait(); pdl_trigger().
+extern bool g_pdl;
+
 template <typename... Exp, typename... Act>
 inline void launch_kernel(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
                           Act&&... args) {

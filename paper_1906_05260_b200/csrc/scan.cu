@@ -6,6 +6,8 @@
 
 namespace vdev {
 
+bool g_pdl = false;
+
 namespace {
 
 constexpr int kThreads = 512;
@@ -42,6 +44,8 @@ __device__ int block_excl(int v, int* total) {
 
 __global__ void k_tile_scan(const int* __restrict__ in, int* __restrict__ out, long long n_cap,
                             const int* n_dev, int* partials) {
+  pdl_wait();
+  pdl_trigger();
   const long long n = n_dev ? static_cast<long long>(*n_dev) : n_cap;
   const long long base = static_cast<long long>(blockIdx.x) * kTile;
   if (base > n) return;
@@ -65,6 +69,8 @@ __global__ void k_tile_scan(const int* __restrict__ in, int* __restrict__ out, l
 }
 
 __global__ void k_partials_scan(int* partials, long long n_cap, const int* n_dev) {
+  pdl_wait();
+  pdl_trigger();
   const long long n = n_dev ? static_cast<long long>(*n_dev) : n_cap;
   const long long parts = n / kTile + 1;
   int carry = 0;
@@ -79,6 +85,8 @@ __global__ void k_partials_scan(int* partials, long long n_cap, const int* n_dev
 }
 
 __global__ void k_add(int* __restrict__ out, long long n_cap, const int* n_dev, const int* __restrict__ partials) {
+  pdl_wait();
+  pdl_trigger();
   const long long n = n_dev ? static_cast<long long>(*n_dev) : n_cap;
   const long long base = static_cast<long long>(blockIdx.x) * kTile;
   if (base > n || blockIdx.x == 0) return;
@@ -98,9 +106,9 @@ void scan_exclusive(const int* in, int* out, long long n_cap, const int* n_dev, 
                     cudaStream_t st) {
   (void)parts;
   const long long blocks = n_cap / kTile + 1;
-  k_tile_scan<<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(in, out, n_cap, n_dev, partials);
-  k_partials_scan<<<1, kThreads, 0, st>>>(partials, n_cap, n_dev);
-  k_add<<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(out, n_cap, n_dev, partials);
+  launch_kernel(k_tile_scan, static_cast<unsigned>(blocks), kThreads, 0, st, g_pdl, in, out, n_cap, n_dev, partials);
+  launch_kernel(k_partials_scan, 1, kThreads, 0, st, g_pdl, partials, n_cap, n_dev);
+  launch_kernel(k_add, static_cast<unsigned>(blocks), kThreads, 0, st, g_pdl, out, n_cap, n_dev, partials);
 }
 
 }  // namespace vdev

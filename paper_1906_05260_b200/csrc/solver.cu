@@ -530,6 +530,8 @@ void Solver::fill_animation(int substeps, double h) {
 }
 
 __global__ void k_init_acc(StepAccum* acc, unsigned long long* err, int* scalars) {
+  vdev::pdl_wait();
+  vdev::pdl_trigger();
   scalars[vdev::SC_OVF] = 0;
   for (int q = 0; q < 8; ++q) acc->residuals[q] = 0.0;
   acc->max_penetration = 0.0;
@@ -541,8 +543,14 @@ __global__ void k_init_acc(StepAccum* acc, unsigned long long* err, int* scalars
   acc->max_contacts = 0;
   *err = ~0ull;
 }
-__global__ void k_end_substep(StepAccum* acc, const int* singular_last) { acc->skipped_singular += *singular_last; }
+__global__ void k_end_substep(StepAccum* acc, const int* singular_last) {
+  vdev::pdl_wait();
+  vdev::pdl_trigger();
+  acc->skipped_singular += *singular_last;
+}
 __global__ void k_end_step(StepAccum* acc, const unsigned long long* err, const int* scalars) {
+  vdev::pdl_wait();
+  vdev::pdl_trigger();
   unsigned long long e = *err;
   if (scalars[vdev::SC_OVF]) e = vdev::err_code(0, vdev::ERR_CAPACITY, scalars[vdev::SC_OVF], 0);  // results invalid
   acc->error = e;
@@ -568,7 +576,10 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
   auto end = [&]() {
     if (prof) cudaEventRecord(prof->ev.back(), st);
   };
-  k_init_acc<<<1, 1, 0, st>>>(d_acc_, d_err_, c_.scalars);
+  // Programmatic dependent launch between the step's kernels (not when profiling: the event
+  // brackets between categories would serialize them anyway).
+  vdev::g_pdl = pdl_ && !prof;
+  vdev::launch_kernel(k_init_acc, 1, 1, 0, st, vdev::g_pdl, d_acc_, d_err_, c_.scalars);
   check_cuda(cudaMemcpyAsync(d_anim_, h_anim_, sizeof(double) * al_.stride * substeps, cudaMemcpyHostToDevice, st),
              "anim upload");
   for (int s = 0; s < substeps; ++s) {
@@ -591,8 +602,7 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
     double* nxt = w_.Y;
     vdev::SweepParams sp{h, h2, scene_.settings.beta, classic_ ? 1 : 0, 0, s, c_.n_pins, setup_.elastic_blocks,
                          scene_.settings.contact_k, 0, nullptr, nullptr};
-    // Programmatic dependent launch only between the loop's kernels (no event brackets there).
-    const bool pdl = pdl_ && !prof;
+    const bool pdl = vdev::g_pdl;
     double* lam_a = w_.lam;
     double* lam_b = w_.lam + static_cast<std::size_t>(vdev::kLamFields) * w_.vpad;
     for (int it = 0; it < iterations; ++it) {
@@ -622,10 +632,11 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
     vdev::launch_residuals(w_, w_.X, w_.classic, d_report_partials_, report_parts_,
                            reinterpret_cast<double*>(reinterpret_cast<char*>(d_acc_) + offsetof(StepAccum, residuals)), st);
     if (ext_possible_ && (c_.contact_cap + c_.hp_cap) > 0) vdev::launch_penetration(w_, c_, w_.X, d_acc_, st);
-    k_end_substep<<<1, 1, 0, st>>>(d_acc_, d_singular_ + (iterations - 1));
+    vdev::launch_kernel(k_end_substep, 1, 1, 0, st, vdev::g_pdl, d_acc_, d_singular_ + (iterations - 1));
     end();
   }
-  k_end_step<<<1, 1, 0, st>>>(d_acc_, d_err_, c_.scalars);
+  vdev::launch_kernel(k_end_step, 1, 1, 0, st, vdev::g_pdl, d_acc_, d_err_, c_.scalars);
+  vdev::g_pdl = false;
   check_cuda(cudaMemcpyAsync(h_acc_, d_acc_, sizeof(StepAccum), cudaMemcpyDeviceToHost, st), "report download");
 }
 

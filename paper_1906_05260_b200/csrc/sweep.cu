@@ -289,6 +289,8 @@ __device__ __forceinline__ int ext_endpoints(const Collide& c, int b, int npins,
 }
 
 __global__ void k_ext_count(Collide c, int npins) {
+  pdl_wait();
+  pdl_trigger();
   const int nct = c.scalars[SC_NCT];
   const int n = npins + nct + c.scalars[SC_NHP];
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) {
@@ -302,6 +304,8 @@ __global__ void k_ext_count(Collide c, int npins) {
   }
 }
 __global__ void k_ext_fill(Collide c, int npins) {
+  pdl_wait();
+  pdl_trigger();
   const int nct = c.scalars[SC_NCT];
   const int n = npins + nct + c.scalars[SC_NHP];
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) {
@@ -315,6 +319,8 @@ __global__ void k_ext_fill(Collide c, int npins) {
   }
 }
 __global__ void k_ext_sort(Collide c, int V) {
+  pdl_wait();
+  pdl_trigger();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= V) return;
   const int s0 = c.ext_off[v], s1 = c.ext_off[v + 1];
@@ -336,6 +342,8 @@ __global__ void k_ext_sort(Collide c, int V) {
 constexpr int kRepThreads = 256;
 
 __global__ void k_report_partial(World w, const double* __restrict__ X, int classic, double* partials) {
+  pdl_wait();
+  pdl_trigger();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   double acc[16];
 #pragma unroll
@@ -425,6 +433,8 @@ __global__ void k_report_partial(World w, const double* __restrict__ X, int clas
 // Sums the per-CTA partials: 16 quantities x `parts`, one CTA of 256 threads, each thread a
 // strided fixed subset, then a fixed tree — deterministic, no atomics.
 __global__ void k_report_final(const double* partials, int parts, double* out8) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double red[16][kRepThreads / 16];
   const int q = threadIdx.x & 15, lane = threadIdx.x >> 4;  // 16 threads per quantity
   double acc = 0.0;
@@ -442,6 +452,8 @@ __global__ void k_report_final(const double* partials, int parts, double* out8) 
 }
 
 __global__ void k_penetration(World w, Collide c, const double* __restrict__ X, StepAccum* acc) {
+  pdl_wait();
+  pdl_trigger();
   const int npins = c.n_pins;
   const int nct = c.scalars[SC_NCT];
   const int n = nct + c.scalars[SC_NHP];
@@ -469,10 +481,10 @@ void launch_ext_setup(const World& w, Collide& c, cudaStream_t st) {
   cudaMemsetAsync(c.ext_cnt, 0, sizeof(int) * (w.V + 1), st);
   cudaMemsetAsync(c.ext_cur, 0, sizeof(int) * w.V, st);
   const int g = grid_for(c.ext_cap);
-  k_ext_count<<<g, kThreads, 0, st>>>(c, c.n_pins);
+  launch_kernel(k_ext_count, g, kThreads, 0, st, g_pdl, c, c.n_pins);
   scan_exclusive(c.ext_cnt, c.ext_off, w.V, nullptr, c.scan_tmp, c.scan_parts, st);
-  k_ext_fill<<<g, kThreads, 0, st>>>(c, c.n_pins);
-  k_ext_sort<<<(w.V + kThreads - 1) / kThreads, kThreads, 0, st>>>(c, w.V);
+  launch_kernel(k_ext_fill, g, kThreads, 0, st, g_pdl, c, c.n_pins);
+  launch_kernel(k_ext_sort, (w.V + kThreads - 1) / kThreads, kThreads, 0, st, g_pdl, c, w.V);
 }
 
 void launch_ext_solve(const World& w, Collide& c, const double* X, const SweepParams& sp, int* singular_counter,
@@ -489,12 +501,12 @@ void launch_iteration(const World& w, Collide& c, const double* X, double* Y, co
 
 void launch_residuals(const World& w, const double* X, int classic, double* partials, int parts, double* out8,
                       cudaStream_t st) {
-  k_report_partial<<<parts, kRepThreads, 0, st>>>(w, X, classic, partials);
-  k_report_final<<<1, kRepThreads, 0, st>>>(partials, parts, out8);
+  launch_kernel(k_report_partial, parts, kRepThreads, 0, st, g_pdl, w, X, classic, partials);
+  launch_kernel(k_report_final, 1, kRepThreads, 0, st, g_pdl, partials, parts, out8);
 }
 
 void launch_penetration(const World& w, Collide& c, const double* X, StepAccum* acc, cudaStream_t st) {
-  k_penetration<<<grid_for(c.contact_cap + c.hp_cap), kThreads, 0, st>>>(w, c, X, acc);
+  launch_kernel(k_penetration, grid_for(c.contact_cap + c.hp_cap), kThreads, 0, st, g_pdl, w, c, X, acc);
 }
 
 }  // namespace vdev
