@@ -223,6 +223,22 @@ int vrod_solver_get_contacts(vrod_solver* solver, int64_t capacity, int64_t* cou
 /* Solver::current_pills(), solver.cpp:432-436 (rod pills then kinematic pills). */
 int vrod_solver_current_pills(vrod_solver* solver, int64_t capacity, int64_t* count, vrod_pill* pills);
 
+/* ---- batches of independent scenes (BASELINE config C5) --------------------------------
+ * The reference has no batch API: a batch is N independent vrod::Solver(Scene) objects
+ * stepped in lockstep (solver.h:54-115, once per scene). Here one solver handle steps them
+ * all in one device world: pairs never cross scenes, pair_key ids stay scene-local, every
+ * scene's results equal that scene solved alone. All scenes must share one SolverSettings
+ * (dt, substeps, iterations, ...). State / rod-size queries see the scenes concatenated in
+ * order (global slot order of scene 0, then scene 1, ...). vrod_solver_step on a batch
+ * returns the batch total: contact_count, broad_pairs, skipped_singular summed,
+ * max_penetration and each residual the maximum over scenes. */
+int vrod_batch_create(int32_t scene_count, const vrod_scene* const* scenes, vrod_solver** out);
+/* Number of scenes of a solver (1 for vrod_solver_create). */
+int vrod_solver_scene_count(const vrod_solver* solver, int32_t* count);
+/* Per-scene StepReports of the last step (the same report Solver::step() of that scene alone
+ * returns). capacity >= scene count. */
+int vrod_solver_scene_reports(const vrod_solver* solver, int32_t capacity, vrod_step_report* reports);
+
 /* ---- fine-grained (kernel-level) boundary, on host arrays ------------------------------ */
 
 /* pill_project(x, pill), collision.h:64 / collision.cpp:15-49 — n independent queries. */

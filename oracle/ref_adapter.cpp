@@ -94,9 +94,42 @@ vrod_pill from_pill(const Pill& p) {
 struct vrod_scene {
   Scene scene;
 };
+// A batch (vrod_batch_create) is N independent reference solvers stepped in lockstep — the
+// reference has no batch API of its own.
 struct vrod_solver {
   std::unique_ptr<Solver> solver;
+  std::vector<std::unique_ptr<Solver>> batch;
+  std::vector<StepReport> last;
 };
+namespace {
+Solver& one(const vrod_solver* h) {
+  if (!h->solver) throw std::invalid_argument("this query needs a single-scene solver (not a batch)");
+  return *h->solver;
+}
+std::vector<Solver*> all(const vrod_solver* h) {
+  std::vector<Solver*> v;
+  if (h->solver) v.push_back(h->solver.get());
+  for (const auto& b : h->batch) v.push_back(b.get());
+  return v;
+}
+void put_report(const StepReport& r, vrod_step_report* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->step = r.step;
+  out->time = r.time;
+  for (int k = 0; k < 8 && k < static_cast<int>(r.residuals.size()); ++k) out->residuals[k] = r.residuals[k];
+  out->max_penetration = r.max_penetration;
+  out->contact_count = r.contact_count;
+  out->broad_pairs = r.broad_pairs;
+  out->skipped_singular = r.skipped_singular;
+  out->dof_count = r.dof_count;
+  out->predict_ms = r.timings.predict_ms;
+  out->broad_ms = r.timings.broad_ms;
+  out->narrow_ms = r.timings.narrow_ms;
+  out->solve_ms = r.timings.solve_ms;
+  out->finalize_ms = r.timings.finalize_ms;
+  out->total_ms = r.timings.total_ms;
+}
+}  // namespace
 
 extern "C" {
 
@@ -298,30 +331,54 @@ int vrod_solver_create(const vrod_scene* s, vrod_solver** out) {
 }
 void vrod_solver_destroy(vrod_solver* s) { delete s; }
 
+int vrod_batch_create(int32_t n, const vrod_scene* const* scenes, vrod_solver** out) {
+  return guarded([&] {
+    if (n < 1 || !scenes) throw std::invalid_argument("batch needs at least one scene");
+    auto h = std::make_unique<vrod_solver>();
+    for (int i = 0; i < n; ++i) h->batch.push_back(std::make_unique<Solver>(scenes[i]->scene));
+    *out = h.release();
+  });
+}
+int vrod_solver_scene_count(const vrod_solver* s, int32_t* count) {
+  return guarded([&] { *count = static_cast<int32_t>(all(s).size()); });
+}
+int vrod_solver_scene_reports(const vrod_solver* s, int32_t capacity, vrod_step_report* reports) {
+  return guarded([&] {
+    if (capacity < static_cast<int32_t>(s->last.size())) throw std::invalid_argument("scene report capacity too small");
+    for (std::size_t i = 0; i < s->last.size(); ++i) put_report(s->last[i], reports + i);
+  });
+}
+
 int vrod_solver_step(vrod_solver* s, vrod_step_report* out) {
   return guarded([&] {
-    const StepReport r = s->solver->step();
-    std::memset(out, 0, sizeof(*out));
-    out->step = r.step;
-    out->time = r.time;
-    for (int k = 0; k < 8 && k < static_cast<int>(r.residuals.size()); ++k) out->residuals[k] = r.residuals[k];
-    out->max_penetration = r.max_penetration;
-    out->contact_count = r.contact_count;
-    out->broad_pairs = r.broad_pairs;
-    out->skipped_singular = r.skipped_singular;
-    out->dof_count = r.dof_count;
-    out->predict_ms = r.timings.predict_ms;
-    out->broad_ms = r.timings.broad_ms;
-    out->narrow_ms = r.timings.narrow_ms;
-    out->solve_ms = r.timings.solve_ms;
-    out->finalize_ms = r.timings.finalize_ms;
-    out->total_ms = r.timings.total_ms;
+    s->last.clear();
+    StepReport tot;
+    tot.residuals.assign(8, 0.0);
+    for (Solver* sv : all(s)) {
+      s->last.push_back(sv->step());
+      const StepReport& r = s->last.back();
+      if (s->solver) {
+        tot = r;
+        break;
+      }
+      tot.step = r.step;
+      tot.time = r.time;
+      for (int k = 0; k < 8 && k < static_cast<int>(r.residuals.size()); ++k)
+        tot.residuals[k] = std::max(tot.residuals[k], r.residuals[k]);
+      tot.max_penetration = std::max(tot.max_penetration, r.max_penetration);
+      tot.contact_count += r.contact_count;
+      tot.broad_pairs += r.broad_pairs;
+      tot.skipped_singular += r.skipped_singular;
+      tot.dof_count += r.dof_count;
+      tot.timings.total_ms += r.timings.total_ms;
+    }
+    put_report(tot, out);
   });
 }
 
 int vrod_solver_probe_convergence(vrod_solver* s, int32_t iterations, double* log) {
   return guarded([&] {
-    const auto rows = s->solver->probe_convergence(iterations);
+    const auto rows = one(s).probe_convergence(iterations);
     for (std::size_t i = 0; i < rows.size(); ++i)
       for (int k = 0; k < 8; ++k) log[i * 8 + k] = rows[i][k];
   });
@@ -329,23 +386,26 @@ int vrod_solver_probe_convergence(vrod_solver* s, int32_t iterations, double* lo
 
 int vrod_solver_get_info(const vrod_solver* s, vrod_solver_info* info) {
   return guarded([&] {
-    const Solver& sv = *s->solver;
     std::memset(info, 0, sizeof(*info));
-    info->rod_count = static_cast<int32_t>(sv.scene().rods.size());
-    info->total_vertices = sv.layout().total_vertices;
-    info->total_elements = sv.layout().total_elements;
-    info->dof_count = sv.dof_count();
-    info->step_index = sv.step_index();
-    info->bundle_count = static_cast<int32_t>(sv.bundles().size());
-    info->elastic_blocks = static_cast<int32_t>(sv.elastic_.size());
-    info->time = sv.time();
+    for (const Solver* p : all(s)) {
+      const Solver& sv = *p;
+      info->rod_count += static_cast<int32_t>(sv.scene().rods.size());
+      info->total_vertices += sv.layout().total_vertices;
+      info->total_elements += sv.layout().total_elements;
+      info->dof_count += sv.dof_count();
+      info->step_index = sv.step_index();
+      info->bundle_count += static_cast<int32_t>(sv.bundles().size());
+      info->elastic_blocks += static_cast<int32_t>(sv.elastic_.size());
+      info->time = sv.time();
+    }
   });
 }
 
 int vrod_solver_get_rod_sizes(const vrod_solver* s, int32_t* counts) {
   return guarded([&] {
-    const auto& rods = s->solver->scene().rods;
-    for (std::size_t r = 0; r < rods.size(); ++r) counts[r] = rods[r].rest.vertex_count();
+    int i = 0;
+    for (const Solver* p : all(s))
+      for (const Rod& rod : p->scene().rods) counts[i++] = rod.rest.vertex_count();
   });
 }
 
@@ -353,18 +413,19 @@ int vrod_solver_get_state(vrod_solver* s, double* c, double* sc, double* f, doub
                           double* av) {
   return guarded([&] {
     std::size_t vi = 0, ei = 0;
-    for (const Rod& rod : s->solver->scene().rods) {
-      for (int v = 0; v < rod.rest.vertex_count(); ++v, ++vi) {
-        if (c) put3(c + 3 * vi, rod.state.centers[v]);
-        if (sc) sc[vi] = rod.state.scales[v];
-        if (cv) put3(cv + 3 * vi, rod.state.center_vel[v]);
-        if (sv) sv[vi] = rod.state.scale_vel[v];
+    for (const Solver* p : all(s))
+      for (const Rod& rod : p->scene().rods) {
+        for (int v = 0; v < rod.rest.vertex_count(); ++v, ++vi) {
+          if (c) put3(c + 3 * vi, rod.state.centers[v]);
+          if (sc) sc[vi] = rod.state.scales[v];
+          if (cv) put3(cv + 3 * vi, rod.state.center_vel[v]);
+          if (sv) sv[vi] = rod.state.scale_vel[v];
+        }
+        for (int e = 0; e < rod.rest.element_count(); ++e, ++ei) {
+          if (f) put4(f + 4 * ei, rod.state.frames[e]);
+          if (av) put3(av + 3 * ei, rod.state.angular_vel[e]);
+        }
       }
-      for (int e = 0; e < rod.rest.element_count(); ++e, ++ei) {
-        if (f) put4(f + 4 * ei, rod.state.frames[e]);
-        if (av) put3(av + 3 * ei, rod.state.angular_vel[e]);
-      }
-    }
   });
 }
 
@@ -372,7 +433,7 @@ int vrod_solver_set_state(vrod_solver* s, const double* c, const double* sc, con
                           const double* cv, const double* sv, const double* av) {
   return guarded([&] {
     std::size_t vi = 0, ei = 0;
-    for (Rod& rod : s->solver->scene().rods) {
+    for (Rod& rod : one(s).scene().rods) {
       for (int v = 0; v < rod.rest.vertex_count(); ++v, ++vi) {
         if (c) rod.state.centers[v] = v3(c + 3 * vi);
         if (sc) rod.state.scales[v] = sc[vi];
@@ -390,7 +451,7 @@ int vrod_solver_set_state(vrod_solver* s, const double* c, const double* sc, con
 int vrod_solver_get_rest(vrod_solver* s, double* lengths, double* darboux, double* grads, double* laps) {
   return guarded([&] {
     std::size_t ei = 0;
-    for (const Rod& rod : s->solver->scene().rods) {
+    for (const Rod& rod : one(s).scene().rods) {
       const int m = rod.rest.element_count();
       for (int e = 0; e < m; ++e, ++ei) {
         if (lengths) lengths[ei] = rod.rest.lengths[e];
@@ -406,8 +467,8 @@ int vrod_solver_get_rest(vrod_solver* s, double* lengths, double* darboux, doubl
 int vrod_solver_set_loads(vrod_solver* s, const double* fd, const uint8_t* fd_rods, const double* tq,
                           const uint8_t* tq_rods, const double* sl, const uint8_t* sl_rods) {
   return guarded([&] {
-    ExternalLoads& L = s->solver->loads();
-    const auto& rods = s->solver->scene().rods;
+    ExternalLoads& L = one(s).loads();
+    const auto& rods = one(s).scene().rods;
     const std::size_t nr = rods.size();
     L.force_density.clear();
     L.torque.clear();
@@ -433,15 +494,15 @@ int vrod_solver_set_loads(vrod_solver* s, const double* fd, const uint8_t* fd_ro
 
 int vrod_solver_energy(vrod_solver* s, double* ke, double* vol, double* rest_vol) {
   return guarded([&] {
-    if (ke) *ke = s->solver->kinetic_energy();
-    if (vol) *vol = s->solver->total_volume();
-    if (rest_vol) *rest_vol = s->solver->total_rest_volume();
+    if (ke) *ke = one(s).kinetic_energy();
+    if (vol) *vol = one(s).total_volume();
+    if (rest_vol) *rest_vol = one(s).total_rest_volume();
   });
 }
 
 int vrod_solver_get_inverse_weights(vrod_solver* s, double* ic, double* is, double* it) {
   return guarded([&] {
-    const DofLayout& L = s->solver->layout();
+    const DofLayout& L = one(s).layout();
     for (int v = 0; v < L.total_vertices; ++v) {
       if (ic) ic[v] = L.inv_center[v];
       if (is) is[v] = L.inv_scale[v];
@@ -455,7 +516,7 @@ int vrod_solver_get_contacts(vrod_solver* s, int64_t cap, int64_t* count, int32_
                              double* alpha, double* beta) {
   return guarded([&] {
     int64_t k = 0;
-    for (const ConstraintBlock& blk : s->solver->contact_blocks_) {
+    for (const ConstraintBlock& blk : one(s).contact_blocks_) {
       if (blk.kind != ConstraintKind::kContact) continue;
       if (k < cap) {
         if (a) a[k] = blk.pill_a;
@@ -471,7 +532,7 @@ int vrod_solver_get_contacts(vrod_solver* s, int64_t cap, int64_t* count, int32_
 
 int vrod_solver_current_pills(vrod_solver* s, int64_t cap, int64_t* count, vrod_pill* out) {
   return guarded([&] {
-    const auto pills = s->solver->current_pills();
+    const auto pills = one(s).current_pills();
     for (std::size_t i = 0; i < pills.size() && static_cast<int64_t>(i) < cap; ++i) out[i] = from_pill(pills[i]);
     *count = static_cast<int64_t>(pills.size());
   });

@@ -1887,9 +1887,25 @@ vrod_pill from_pill(const Pill& p) {
 struct vrod_scene {
   Scene scene;
 };
+// A batch (vrod_batch_create) is N independent reference solvers stepped in lockstep.
 struct vrod_solver {
   std::unique_ptr<Solver> s;
+  std::vector<std::unique_ptr<Solver>> batch;
+  std::vector<Report> last;
 };
+namespace {
+Solver& one(vrod_solver* h) {
+  if (!h->s) throw std::invalid_argument("this query needs a single-scene solver (not a batch)");
+  return *h->s;
+}
+const Solver& one(const vrod_solver* h) { return one(const_cast<vrod_solver*>(h)); }
+std::vector<Solver*> all(const vrod_solver* h) {  // the scenes, in order
+  std::vector<Solver*> v;
+  if (h->s) v.push_back(h->s.get());
+  for (const auto& b : h->batch) v.push_back(b.get());
+  return v;
+}
+}  // namespace
 
 extern "C" {
 
@@ -2051,9 +2067,68 @@ int vrod_solver_create(const vrod_scene* s, vrod_solver** out) {
 }
 void vrod_solver_destroy(vrod_solver* s) { delete s; }
 
+static void put_report(const Report& r, vrod_step_report* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->step = r.step;
+  out->time = r.time;
+  for (int k = 0; k < 8; ++k) out->residuals[k] = r.residuals[k];
+  out->max_penetration = r.max_pen;
+  out->contact_count = r.contacts;
+  out->broad_pairs = r.broad;
+  out->skipped_singular = r.singular;
+  out->dof_count = r.dof;
+}
+
+int vrod_batch_create(int32_t n, const vrod_scene* const* scenes, vrod_solver** out) {
+  return guarded([&] {
+    require(n >= 1 && scenes != nullptr, "batch needs at least one scene");
+    auto h = std::make_unique<vrod_solver>();
+    for (int i = 0; i < n; ++i) {
+      if (i > 0) {
+        const Settings& a = scenes[0]->scene.settings;
+        const Settings& b = scenes[i]->scene.settings;
+        require(a.dt == b.dt && a.iterations == b.iterations && a.substeps == b.substeps && a.beta == b.beta &&
+                    a.g.x == b.g.x && a.g.y == b.g.y && a.g.z == b.g.z && a.dich == b.dich && a.sm_period == b.sm_period && a.contact_k == b.contact_k &&
+                    a.damping == b.damping && a.deterministic == b.deterministic && a.scale_mode == b.scale_mode,
+                "batch scene " + std::to_string(i) + ": all scenes of a batch must share one SolverSettings");
+      }
+      h->batch.push_back(std::make_unique<Solver>(scenes[i]->scene));
+    }
+    *out = h.release();
+  });
+}
+int vrod_solver_scene_count(const vrod_solver* h, int32_t* count) {
+  return guarded([&] { *count = h->s ? 1 : static_cast<int32_t>(h->batch.size()); });
+}
+int vrod_solver_scene_reports(const vrod_solver* h, int32_t capacity, vrod_step_report* reports) {
+  return guarded([&] {
+    require(capacity >= static_cast<int32_t>(h->last.size()), "scene report capacity too small");
+    for (std::size_t i = 0; i < h->last.size(); ++i) put_report(h->last[i], reports + i);
+  });
+}
+
 int vrod_solver_step(vrod_solver* h, vrod_step_report* out) {
   return guarded([&] {
-    const Report r = h->s->step();
+    if (!h->s) {  // batch: every scene alone, in order; the total as documented in vrod_capi.h
+      h->last.clear();
+      Report tot;
+      for (auto& sv : h->batch) {
+        h->last.push_back(sv->step());
+        const Report& r = h->last.back();
+        tot.step = r.step;
+        tot.time = r.time;
+        for (int k = 0; k < 8; ++k) tot.residuals[k] = std::max(tot.residuals[k], r.residuals[k]);
+        tot.max_pen = std::max(tot.max_pen, r.max_pen);
+        tot.contacts += r.contacts;
+        tot.broad += r.broad;
+        tot.singular += r.singular;
+        tot.dof += r.dof;
+      }
+      put_report(tot, out);
+      return;
+    }
+    const Report r = one(h).step();
+    h->last.assign(1, r);
     std::memset(out, 0, sizeof(*out));
     out->step = r.step;
     out->time = r.time;
@@ -2067,52 +2142,57 @@ int vrod_solver_step(vrod_solver* h, vrod_step_report* out) {
 }
 int vrod_solver_probe_convergence(vrod_solver* h, int32_t iterations, double* log) {
   return guarded([&] {
-    const auto rows = h->s->probe_convergence(iterations);
+    const auto rows = one(h).probe_convergence(iterations);
     for (std::size_t i = 0; i < rows.size(); ++i)
       for (int k = 0; k < 8; ++k) log[i * 8 + k] = rows[i][k];
   });
 }
 int vrod_solver_get_info(const vrod_solver* h, vrod_solver_info* info) {
   return guarded([&] {
-    const Solver& s = *h->s;
     std::memset(info, 0, sizeof(*info));
-    info->rod_count = static_cast<int32_t>(s.s_.rods.size());
-    info->total_vertices = s.L_.V;
-    info->total_elements = s.L_.E;
-    info->dof_count = s.L_.dof;
-    info->step_index = s.step_index_;
-    info->bundle_count = static_cast<int32_t>(s.groups_.size());
-    info->elastic_blocks = static_cast<int32_t>(s.elastic_.size());
-    info->time = s.time_;
+    for (const Solver* sp : all(h)) {
+      const Solver& s = *sp;
+      info->rod_count += static_cast<int32_t>(s.s_.rods.size());
+      info->total_vertices += s.L_.V;
+      info->total_elements += s.L_.E;
+      info->dof_count += s.L_.dof;
+      info->step_index = s.step_index_;
+      info->bundle_count += static_cast<int32_t>(s.groups_.size());
+      info->elastic_blocks += static_cast<int32_t>(s.elastic_.size());
+      info->time = s.time_;
+    }
   });
 }
 int vrod_solver_get_rod_sizes(const vrod_solver* h, int32_t* counts) {
   return guarded([&] {
-    for (std::size_t r = 0; r < h->s->s_.rods.size(); ++r) counts[r] = h->s->s_.rods[r].rest.n();
+    int i = 0;
+    for (const Solver* sp : all(h))
+      for (const Rod& rod : sp->s_.rods) counts[i++] = rod.rest.n();
   });
 }
 int vrod_solver_get_state(vrod_solver* h, double* c, double* sc, double* f, double* cv, double* sv, double* av) {
   return guarded([&] {
     std::size_t vi = 0, ei = 0;
-    for (const Rod& rod : h->s->s_.rods) {
-      for (int v = 0; v < rod.rest.n(); ++v, ++vi) {
-        if (c) put3(c + 3 * vi, rod.st.c[v]);
-        if (sc) sc[vi] = rod.st.s[v];
-        if (cv) put3(cv + 3 * vi, rod.st.cv[v]);
-        if (sv) sv[vi] = rod.st.sv[v];
+    for (const Solver* sp : all(h))
+      for (const Rod& rod : sp->s_.rods) {
+        for (int v = 0; v < rod.rest.n(); ++v, ++vi) {
+          if (c) put3(c + 3 * vi, rod.st.c[v]);
+          if (sc) sc[vi] = rod.st.s[v];
+          if (cv) put3(cv + 3 * vi, rod.st.cv[v]);
+          if (sv) sv[vi] = rod.st.sv[v];
+        }
+        for (int e = 0; e < rod.rest.m(); ++e, ++ei) {
+          if (f) put4(f + 4 * ei, rod.st.q[e]);
+          if (av) put3(av + 3 * ei, rod.st.av[e]);
+        }
       }
-      for (int e = 0; e < rod.rest.m(); ++e, ++ei) {
-        if (f) put4(f + 4 * ei, rod.st.q[e]);
-        if (av) put3(av + 3 * ei, rod.st.av[e]);
-      }
-    }
   });
 }
 int vrod_solver_set_state(vrod_solver* h, const double* c, const double* sc, const double* f, const double* cv,
                           const double* sv, const double* av) {
   return guarded([&] {
     std::size_t vi = 0, ei = 0;
-    for (Rod& rod : h->s->s_.rods) {
+    for (Rod& rod : one(h).s_.rods) {
       for (int v = 0; v < rod.rest.n(); ++v, ++vi) {
         if (c) rod.st.c[v] = v3(c + 3 * vi);
         if (sc) rod.st.s[v] = sc[vi];
@@ -2129,7 +2209,7 @@ int vrod_solver_set_state(vrod_solver* h, const double* c, const double* sc, con
 int vrod_solver_get_rest(vrod_solver* h, double* lengths, double* darb, double* grads, double* laps) {
   return guarded([&] {
     std::size_t ei = 0;
-    for (const Rod& rod : h->s->s_.rods) {
+    for (const Rod& rod : one(h).s_.rods) {
       const int m = rod.rest.m();
       for (int e = 0; e < m; ++e, ++ei) {
         if (lengths) lengths[ei] = rod.rest.len[e];
@@ -2144,8 +2224,8 @@ int vrod_solver_get_rest(vrod_solver* h, double* lengths, double* darb, double* 
 int vrod_solver_set_loads(vrod_solver* h, const double* fd, const uint8_t* fdr, const double* tq,
                           const uint8_t* tqr, const double* sl, const uint8_t* slr) {
   return guarded([&] {
-    Loads& L = h->s->loads_;
-    const auto& rods = h->s->s_.rods;
+    Loads& L = one(h).loads_;
+    const auto& rods = one(h).s_.rods;
     const std::size_t nr = rods.size();
     L = Loads{};
     if (fd) L.fd.resize(nr);
@@ -2167,14 +2247,14 @@ int vrod_solver_set_loads(vrod_solver* h, const double* fd, const uint8_t* fdr, 
 }
 int vrod_solver_energy(vrod_solver* h, double* ke, double* vol, double* rvol) {
   return guarded([&] {
-    if (ke) *ke = h->s->kinetic_energy();
-    if (vol) *vol = h->s->total_volume();
-    if (rvol) *rvol = h->s->total_rest_volume();
+    if (ke) *ke = one(h).kinetic_energy();
+    if (vol) *vol = one(h).total_volume();
+    if (rvol) *rvol = one(h).total_rest_volume();
   });
 }
 int vrod_solver_get_inverse_weights(vrod_solver* h, double* ic, double* is, double* it) {
   return guarded([&] {
-    const Layout& L = h->s->L_;
+    const Layout& L = one(h).L_;
     for (int v = 0; v < L.V; ++v) {
       if (ic) ic[v] = L.ic[v];
       if (is) is[v] = L.is[v];
@@ -2187,7 +2267,7 @@ int vrod_solver_get_contacts(vrod_solver* h, int64_t cap, int64_t* count, int32_
                              double* beta) {
   return guarded([&] {
     int64_t k = 0;
-    for (const Block& blk : h->s->contacts_) {
+    for (const Block& blk : one(h).contacts_) {
       if (blk.kind != kContact) continue;
       if (k < cap) {
         if (a) a[k] = blk.pill_a;
@@ -2202,7 +2282,7 @@ int vrod_solver_get_contacts(vrod_solver* h, int64_t cap, int64_t* count, int32_
 }
 int vrod_solver_current_pills(vrod_solver* h, int64_t cap, int64_t* count, vrod_pill* out) {
   return guarded([&] {
-    const auto p = h->s->current_pills();
+    const auto p = one(h).current_pills();
     for (std::size_t i = 0; i < p.size() && static_cast<int64_t>(i) < cap; ++i) out[i] = from_pill(p[i]);
     *count = static_cast<int64_t>(p.size());
   });

@@ -26,6 +26,14 @@ class Solver(SolverHandle):
         super().__init__(library(), scene)
 
 
+class BatchSolver(SolverHandle):
+    """Independent scenes stepped together in one device world (BASELINE C5): every scene's
+    results equal that scene alone; `scene_reports()` gives each scene's StepReport."""
+
+    def __init__(self, scenes: list[Scene]):
+        super().__init__(library(), None, _batch=list(scenes))
+
+
 def make_rest_pose(centers, radii, scales=None) -> RodRestPose:
     """make_rest_pose (rod.h:88-90), computed by the product's host code."""
     return _scene.make_rest_pose(library(), centers, radii, scales)
@@ -40,7 +48,7 @@ def validate(scene: Scene) -> None:
     _scene.validate(library(), scene)
 
 
-__all__ = ["Solver", "Scene", "Rod", "RodRestPose", "RodState", "MaterialParams", "SolverSettings", "HalfPlane",
+__all__ = ["Solver", "BatchSolver", "Scene", "Rod", "RodRestPose", "RodState", "MaterialParams", "SolverSettings", "HalfPlane",
            "Pill", "KinematicPill", "Bone", "RigidKeyframe", "PinMotion", "SoftPin", "Activation", "StepReport",
            "make_rest_pose", "make_rest_state", "straight_rod", "validate", "VrodError", "InvalidArgument",
            "OutOfRange", "SimulationError", "DeviceError", "library", "LIB_PATH", "capi", "workloads"]

@@ -112,6 +112,9 @@ _SIGNATURES = {
     "vrod_solver_get_inverse_weights": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
     "vrod_solver_get_contacts": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _ip, _ip, _dp, _dp]),
     "vrod_solver_current_pills": (C.c_int, [C.c_void_p, C.c_int64, _i64p, C.c_void_p]),
+    "vrod_batch_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "vrod_solver_scene_count": (C.c_int, [C.c_void_p, _ip]),
+    "vrod_solver_scene_reports": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "vrod_pill_project": (C.c_int, [C.c_int64, _dp, C.c_void_p, _dp, _dp, _u8p]),
     "vrod_deepest_penetration": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, _dp, _dp, _dp, _dp]),
     "vrod_broad_phase": (C.c_int, [C.c_int64, C.c_void_p, C.c_int64, _i64p, _ip]),

@@ -2,6 +2,7 @@
 // API. Scene building is plain host data; vrod_solver_* drive the CUDA Solver (solver.cu);
 // the fine-grained collision entry points run on the GPU (standalone.cu). Exceptions map to
 // status codes with the reference's messages (types.h:25-28, 67-77).
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -240,19 +241,54 @@ int vrod_solver_create(const vrod_scene* s, vrod_solver** out) {
 }
 void vrod_solver_destroy(vrod_solver* s) { delete s; }
 
+static void put_report(const Report& r, vrod_step_report* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->step = r.step;
+  out->time = r.time;
+  for (int k = 0; k < 8; ++k) out->residuals[k] = r.residuals[k];
+  out->max_penetration = r.max_pen;
+  out->contact_count = r.contacts;
+  out->broad_pairs = r.broad;
+  out->skipped_singular = r.singular;
+  out->dof_count = r.dof;
+  out->total_ms = r.total_ms;
+}
+
 int vrod_solver_step(vrod_solver* h, vrod_step_report* out) {
   return guarded([&] {
-    const Report r = h->s->step();
-    std::memset(out, 0, sizeof(*out));
-    out->step = r.step;
-    out->time = r.time;
-    for (int k = 0; k < 8; ++k) out->residuals[k] = r.residuals[k];
-    out->max_penetration = r.max_pen;
-    out->contact_count = r.contacts;
-    out->broad_pairs = r.broad;
-    out->skipped_singular = r.singular;
-    out->dof_count = r.dof;
-    out->total_ms = r.total_ms;
+    Report r = h->s->step();
+    if (h->s->scene_count() > 1) {  // batch total: residuals and penetration as the max over scenes
+      for (int k = 0; k < 8; ++k) r.residuals[k] = 0.0;
+      r.max_pen = 0.0;
+      for (const Report& sr : h->s->scene_reports()) {
+        for (int k = 0; k < 8; ++k) r.residuals[k] = std::max(r.residuals[k], sr.residuals[k]);
+        r.max_pen = std::max(r.max_pen, sr.max_pen);
+      }
+    }
+    put_report(r, out);
+  });
+}
+
+int vrod_batch_create(int32_t n, const vrod_scene* const* scenes, vrod_solver** out) {
+  return guarded([&] {
+    require(n >= 1 && scenes != nullptr, "batch needs at least one scene");
+    std::vector<const SceneData*> list;
+    for (int i = 0; i < n; ++i) list.push_back(&scenes[i]->scene);
+    BatchLayout layout;
+    const SceneData merged = merge_scenes(list, layout);
+    auto h = std::make_unique<vrod_solver>();
+    h->s = std::make_unique<Solver>(merged, &layout);
+    *out = h.release();
+  });
+}
+int vrod_solver_scene_count(const vrod_solver* h, int32_t* count) {
+  return guarded([&] { *count = h->s->scene_count(); });
+}
+int vrod_solver_scene_reports(const vrod_solver* h, int32_t capacity, vrod_step_report* reports) {
+  return guarded([&] {
+    const std::vector<Report> rs = h->s->scene_reports();
+    require(capacity >= static_cast<int32_t>(rs.size()), "scene report capacity too small");
+    for (std::size_t i = 0; i < rs.size(); ++i) put_report(rs[i], reports + i);
   });
 }
 int vrod_solver_probe_convergence(vrod_solver* h, int32_t iterations, double* log) {

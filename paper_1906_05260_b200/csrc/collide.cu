@@ -189,10 +189,11 @@ __device__ __forceinline__ uint32_t pill_id(int rod, int el) {
   return (static_cast<uint32_t>(rod + 1) << 16) | (static_cast<uint32_t>(el + 1) & 0xffffu);
 }
 
-__device__ __forceinline__ unsigned long long cell_hash(long long x, long long y, long long z) {
+__device__ __forceinline__ unsigned long long cell_hash(long long x, long long y, long long z, int scene) {
   unsigned long long h = static_cast<unsigned long long>(x) * 73856093ull ^
                          static_cast<unsigned long long>(y) * 19349663ull ^
-                         static_cast<unsigned long long>(z) * 83492791ull;
+                         static_cast<unsigned long long>(z) * 83492791ull ^
+                         static_cast<unsigned long long>(scene) * 0x9e3779b97f4a7c15ull;
   h ^= h >> 33;
   h *= 0xff51afd7ed558ccdull;
   h ^= h >> 33;
@@ -263,16 +264,23 @@ __global__ void k_bounds(Collide c, int substep, unsigned long long* err) {
       bits = static_cast<unsigned long long>(__double_as_longlong(r));  // r >= 0: bit order == value order
     }
   }
-  // warp max, one atomic per warp (max is order independent)
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long v = __shfl_down_sync(0xffffffffu, bits, o);
-    bits = v > bits ? v : bits;
+  // warp max, one atomic per warp (max is order independent); a batch keeps one max per scene
+  const int sc = c.pill_scene && i < c.P ? c.pill_scene[i] : 0;
+  const int sc0 = __shfl_sync(0xffffffffu, sc, 0);
+  if (__all_sync(0xffffffffu, sc == sc0 || i >= c.P)) {
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long v = __shfl_down_sync(0xffffffffu, bits, o);
+      bits = v > bits ? v : bits;
+    }
+    if ((threadIdx.x & 31) == 0 && bits) atomicMax(c.pill_scene ? &c.scene_maxr[sc0] : c.maxr_bits, bits);
+  } else if (bits) {
+    atomicMax(&c.scene_maxr[sc], bits);
   }
-  if ((threadIdx.x & 31) == 0 && bits) atomicMax(c.maxr_bits, bits);
 }
 
-__device__ __forceinline__ double cell_inv(const Collide& c) {
-  const double maxr = __longlong_as_double(static_cast<long long>(*c.maxr_bits));
+__device__ __forceinline__ double cell_inv(const Collide& c, int scene) {
+  const double maxr =
+      __longlong_as_double(static_cast<long long>(c.pill_scene ? c.scene_maxr[scene] : *c.maxr_bits));
   const double cell = fmax(2.0 * maxr, 1e-12);  // collision.cpp:197-198
   return 1.0 / cell;
 }
@@ -286,21 +294,22 @@ __global__ void k_insert(Collide c) {
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= c.P) return;
-  const double inv = cell_inv(c);
+  const int scene = c.pill_scene ? c.pill_scene[i] : 0;
+  const double inv = cell_inv(c, scene);
   const long long kx = key1(c.bsph[i], inv), ky = key1(c.bsph[c.P + i], inv), kz = key1(c.bsph[2 * c.P + i], inv);
   c.cellkey[i] = kx;
   c.cellkey[c.P + i] = ky;
   c.cellkey[2 * c.P + i] = kz;
   __threadfence();
   const unsigned mask = static_cast<unsigned>(c.T - 1);
-  unsigned h = static_cast<unsigned>(cell_hash(kx, ky, kz)) & mask;
+  unsigned h = static_cast<unsigned>(cell_hash(kx, ky, kz, scene)) & mask;
   while (true) {
     int e = atomicCAS(&c.table[h], -1, i);
     if (e == -1) break;  // new cell, i is its representative
     const long long ex = static_cast<volatile long long*>(c.cellkey)[e];
     const long long ey = static_cast<volatile long long*>(c.cellkey)[c.P + e];
     const long long ez = static_cast<volatile long long*>(c.cellkey)[2 * c.P + e];
-    if (ex == kx && ey == ky && ez == kz) break;
+    if (ex == kx && ey == ky && ez == kz && (!c.pill_scene || c.pill_scene[e] == scene)) break;
     h = (h + 1) & mask;
   }
   c.pill_cell[i] = static_cast<int>(h);
@@ -317,13 +326,15 @@ __global__ void k_scatter(Collide c) {
   c.cell_items[pos] = i;
 }
 
-__device__ __forceinline__ int find_cell(const Collide& c, long long kx, long long ky, long long kz) {
+__device__ __forceinline__ int find_cell(const Collide& c, long long kx, long long ky, long long kz, int scene) {
   const unsigned mask = static_cast<unsigned>(c.T - 1);
-  unsigned h = static_cast<unsigned>(cell_hash(kx, ky, kz)) & mask;
+  unsigned h = static_cast<unsigned>(cell_hash(kx, ky, kz, scene)) & mask;
   while (true) {
     const int e = c.table[h];
     if (e < 0) return -1;
-    if (c.cellkey[e] == kx && c.cellkey[c.P + e] == ky && c.cellkey[2 * c.P + e] == kz) return static_cast<int>(h);
+    if (c.cellkey[e] == kx && c.cellkey[c.P + e] == ky && c.cellkey[2 * c.P + e] == kz &&
+        (!c.pill_scene || c.pill_scene[e] == scene))
+      return static_cast<int>(h);
     h = (h + 1) & mask;
   }
 }
@@ -338,15 +349,18 @@ __device__ __forceinline__ bool spheres_touch(const Collide& c, int i, int j) {
   return dx * dx + dy * dy + dz * dz <= rr * rr;
 }
 
-__device__ __forceinline__ double warm_lookup(const unsigned long long* keys, const double* alpha, int n,
-                                              unsigned long long key) {
+// Warm alpha of `key` in a list increasing in (scene, key) — scene-major in a batch, where the
+// pair ids are scene-local (the same pair_key as the scene alone).
+__device__ __forceinline__ double warm_lookup(const unsigned long long* keys, const int* scenes, const double* alpha,
+                                              int n, int scene, unsigned long long key) {
   int lo = 0, hi = n;  // lower_bound: first inserted wins on duplicate keys
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (keys[mid] < key) lo = mid + 1;
+    const bool less = scenes ? (scenes[mid] < scene || (scenes[mid] == scene && keys[mid] < key)) : keys[mid] < key;
+    if (less) lo = mid + 1;
     else hi = mid;
   }
-  return (lo < n && keys[lo] == key) ? alpha[lo] : -1.0;
+  return (lo < n && keys[lo] == key && (!scenes || scenes[lo] == scene)) ? alpha[lo] : -1.0;
 }
 
 // Squared distance between segments [p0,p1] and [q0,q1] (closest points of two segments,
@@ -415,9 +429,10 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_warp(Collide c, int p
   const int i = blockIdx.x * kPairWarps + warp;
   const bool live = i < c.P;
   int size = 0;
+  const int scene = live && c.pill_scene ? c.pill_scene[i] : 0;
   if (live && lane < 27) {
     const int h = find_cell(c, c.cellkey[i] + (lane / 9 - 1), c.cellkey[c.P + i] + ((lane / 3) % 3 - 1),
-                            c.cellkey[2 * c.P + i] + (lane % 3 - 1));
+                            c.cellkey[2 * c.P + i] + (lane % 3 - 1), scene);
     if (h >= 0) {
       s_start[warp][lane] = c.cell_start[h];
       size = c.cell_start[h + 1] - c.cell_start[h];
@@ -476,7 +491,10 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_warp(Collide c, int p
     s_base = sum ? atomicAdd(cand_total, sum) : 0;
   }
   __syncthreads();
-  if (lane == 0 && broad) atomicAdd(broad_total, broad);
+  if (lane == 0 && broad) {
+    atomicAdd(broad_total, broad);
+    if (c.pill_scene) atomicAdd(&c.scene_acc[scene].broad_pairs, broad);
+  }
   if (!live) return;
   cur_d = 0;  // second pass restarts at k = lane
   long long pos = static_cast<long long>(s_base) + s_cnt[warp];
@@ -498,66 +516,6 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_warp(Collide c, int p
     }
     pos += __popc(m);
   }
-}
-
-// One thread per (pill i, neighbour cell d of its 3x3x3 block): counts the allowed pairs j > i
-// (broad_phase, collision.cpp:213-226 — every one, for StepReport.broad_pairs) and appends the
-// pairs that may penetrate to the candidate list. Appends are warp-aggregated (one atomic per
-// warp); the list is unordered — contacts are put in (i, j) order after the narrow phase.
-__global__ void k_pairs(Collide c, int prefilter, int* broad_total, int* cand_total) {
-  pdl_wait();
-  pdl_trigger();
-  const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  int broad = 0, ncand = 0, h = -1, i = 0;
-  if (t < 27ll * c.P) {
-    i = static_cast<int>(t / 27);
-    const int d = static_cast<int>(t - 27ll * i);
-    h = find_cell(c, c.cellkey[i] + (d / 9 - 1), c.cellkey[c.P + i] + ((d / 3) % 3 - 1),
-                  c.cellkey[2 * c.P + i] + (d % 3 - 1));
-  }
-  int s0 = 0, s1 = 0, ri = 0, gi = 0, ei = 0;
-  bool si = false;
-  if (h >= 0) {
-    s0 = c.cell_start[h];
-    s1 = c.cell_start[h + 1];
-    ri = c.pill_rod[i];
-    gi = c.pill_group[i];
-    ei = c.pill_el[i];
-    si = c.pill_self[i] != 0;
-    for (int q = s0; q < s1; ++q) {
-      const int j = c.cell_items[q];
-      if (j <= i || !pair_allowed(ri, gi, si, ei, c.pill_rod[j], c.pill_group[j], c.pill_el[j])) continue;
-      ++broad;
-      if (!prefilter || may_penetrate(c, i, j)) ++ncand;
-    }
-  }
-  // warp-aggregated reservation of ncand slots
-  int incl = ncand;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  const int warp_total = __shfl_sync(0xffffffffu, incl, 31);
-  int base = 0;
-  if (lane == 31 && warp_total) base = atomicAdd(cand_total, warp_total);
-  base = __shfl_sync(0xffffffffu, base, 31) + incl - ncand;
-  if (ncand) {
-    int k = 0;
-    for (int q = s0; q < s1; ++q) {
-      const int j = c.cell_items[q];
-      if (j <= i || !pair_allowed(ri, gi, si, ei, c.pill_rod[j], c.pill_group[j], c.pill_el[j])) continue;
-      if (prefilter && !may_penetrate(c, i, j)) continue;
-      const long long pos = static_cast<long long>(base) + k++;
-      if (pos < c.cand_cap) {
-        c.cand_i[pos] = i;
-        c.cand_j[pos] = j;
-      }
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) broad += __shfl_down_sync(0xffffffffu, broad, o);
-  if (lane == 0 && broad) atomicAdd(broad_total, broad);
 }
 
 // Exact conservative segment test (see may_penetrate) over the sphere-filtered candidates;
@@ -610,10 +568,11 @@ __global__ void k_narrow_append(Collide c, int split_warm) {
       j = c.cand2_j[q];
       const unsigned long long key = pair_key(c.pill_id[i], c.pill_id[j]);
       double warm;
+      const int scene = c.pill_scene ? c.pill_scene[i] : 0;
       if (!split_warm || (c.pill_rod[i] >= 0 && c.pill_rod[j] >= 0))
-        warm = warm_lookup(c.warm_rr_key, c.warm_rr_alpha, nrr, key);
+        warm = warm_lookup(c.warm_rr_key, c.warm_rr_scene, c.warm_rr_alpha, nrr, scene, key);
       else
-        warm = warm_lookup(c.warm_rk_key, c.warm_rk_alpha, nrk, key);
+        warm = warm_lookup(c.warm_rk_key, c.warm_rk_scene, c.warm_rk_alpha, nrk, scene, key);
       deepest(load_pill(c.pill, c.P, i), load_pill(c.pill, c.P, j), c.iters_dich, warm, al, be, d);
     }
     const bool hit = q < n && d < 0.0;
@@ -693,8 +652,10 @@ __global__ void k_narrow(Collide c, int split_warm, int store_d) {
     const int i = c.cand_i[q], j = c.cand_j[q];
     const unsigned long long key = pair_key(c.pill_id[i], c.pill_id[j]);
     double warm;
-    if (!split_warm || (c.pill_rod[i] >= 0 && c.pill_rod[j] >= 0)) warm = warm_lookup(c.warm_rr_key, c.warm_rr_alpha, nrr, key);
-    else warm = warm_lookup(c.warm_rk_key, c.warm_rk_alpha, nrk, key);
+    if (!split_warm || (c.pill_rod[i] >= 0 && c.pill_rod[j] >= 0))
+      warm = warm_lookup(c.warm_rr_key, nullptr, c.warm_rr_alpha, nrr, 0, key);
+    else
+      warm = warm_lookup(c.warm_rk_key, nullptr, c.warm_rk_alpha, nrk, 0, key);
     double al, be, d;
     deepest(load_pill(c.pill, c.P, i), load_pill(c.pill, c.P, j), c.iters_dich, warm, al, be, d);
     c.cand_flag[q] = d < 0.0 ? 1 : 0;
@@ -758,17 +719,22 @@ __global__ void k_warm_build(Collide c, int split) {
   const int n = c.scalars[SC_NCT];
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const unsigned long long key = pair_key(c.pill_id[c.ct_a[k]], c.pill_id[c.ct_b[k]]);
+    const int scene = c.pill_scene ? c.pill_scene[c.ct_a[k]] : 0;
+    if (c.pill_scene) atomicAdd(&c.scene_acc[scene].contact_count, 1);
     if (!split) {
       c.warm_rr_key[k] = key;
       c.warm_rr_alpha[k] = c.ct_alpha[k];
+      if (c.pill_scene) c.warm_rr_scene[k] = scene;
     } else if (c.rk_flag[k]) {
       const int p = c.rk_pos[k];
       c.warm_rk_key[p] = key;
       c.warm_rk_alpha[p] = c.ct_alpha[k];
+      if (c.pill_scene) c.warm_rk_scene[p] = scene;
     } else {
       const int p = k - c.rk_pos[k];
       c.warm_rr_key[p] = key;
       c.warm_rr_alpha[p] = c.ct_alpha[k];
+      if (c.pill_scene) c.warm_rr_scene[p] = scene;
     }
   }
 }
@@ -790,6 +756,10 @@ __global__ void k_hp_flags(World w, Collide c) {
        q += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int p = static_cast<int>(q / w.V);
     const int v = static_cast<int>(q - static_cast<long long>(p) * w.V);
+    if (c.plane_scene && c.plane_scene[p] != w.rod_scene[w.slot_rod[v]]) {  // batch: own scene's planes only
+      c.hp_flag[q] = 0;
+      continue;
+    }
     const int vp = w.vpad;
     const double* pl = c.planes + 4 * p;
     const V3 nrm{pl[0], pl[1], pl[2]};
@@ -888,6 +858,7 @@ void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
   const int P = c.P;
   const int b = (P + kThreads - 1) / kThreads;
   cudaMemsetAsync(c.maxr_bits, 0, sizeof(unsigned long long), st);
+  if (c.pill_scene) cudaMemsetAsync(c.scene_maxr, 0, sizeof(unsigned long long) * c.n_scenes, st);
   cudaMemsetAsync(c.table, 0xff, sizeof(int) * c.T, st);
   cudaMemsetAsync(c.cell_count, 0, sizeof(int) * c.T, st);
   cudaMemsetAsync(c.cell_cursor, 0, sizeof(int) * c.T, st);

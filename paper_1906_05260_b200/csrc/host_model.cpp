@@ -336,3 +336,66 @@ Setup build_setup(const SceneData& s) {
 }
 
 }  // namespace vhost
+
+namespace vhost {
+
+static bool same_settings(const Settings& a, const Settings& b) {
+  return a.dt == b.dt && a.iterations == b.iterations && a.substeps == b.substeps && a.beta == b.beta &&
+         a.g.x == b.g.x && a.g.y == b.g.y && a.g.z == b.g.z && a.dich == b.dich && a.sm_period == b.sm_period &&
+         a.contact_k == b.contact_k && a.damping == b.damping && a.deterministic == b.deterministic &&
+         a.scale_mode == b.scale_mode;
+}
+
+SceneData merge_scenes(const std::vector<const SceneData*>& scenes, BatchLayout& layout) {
+  require(!scenes.empty(), "batch needs at least one scene");
+  SceneData out;
+  out.settings = scenes[0]->settings;
+  layout = BatchLayout{};
+  layout.scenes = static_cast<int>(scenes.size());
+  layout.rod_base.push_back(0);
+  for (std::size_t si = 0; si < scenes.size(); ++si) {
+    const SceneData& s = *scenes[si];
+    s.validate();
+    require(same_settings(s.settings, out.settings), "batch scene " + std::to_string(si) +
+                                                         ": all scenes of a batch must share one SolverSettings");
+    const int rb = static_cast<int>(out.rods.size());
+    const int mb = static_cast<int>(out.materials.size());
+    const int bb = static_cast<int>(out.bones.size());
+    for (RodData rod : s.rods) {
+      rod.material += mb;
+      for (int& b : rod.bones) b += bb;
+      out.rods.push_back(std::move(rod));
+    }
+    out.materials.insert(out.materials.end(), s.materials.begin(), s.materials.end());
+    for (const auto& p : s.planes) {
+      out.planes.push_back(p);
+      layout.plane_scene.push_back(static_cast<int>(si));
+    }
+    for (KinPill kp : s.kpills) {
+      if (kp.bone >= 0) kp.bone += bb;
+      out.kpills.push_back(kp);
+      layout.kpill_scene.push_back(static_cast<int>(si));
+    }
+    out.bones.insert(out.bones.end(), s.bones.begin(), s.bones.end());
+    for (auto members : s.bundles) {
+      for (auto& m : members) m.first += rb;
+      out.bundles.push_back(std::move(members));
+    }
+    for (PinMotion pm : s.pin_motions) {
+      pm.rod += rb;
+      out.pin_motions.push_back(pm);
+    }
+    for (SoftPin sp : s.soft_pins) {
+      sp.rod += rb;
+      out.soft_pins.push_back(sp);
+    }
+    for (Activation a : s.activations) {
+      a.rod += rb;
+      out.activations.push_back(a);
+    }
+    layout.rod_base.push_back(static_cast<int>(out.rods.size()));
+  }
+  return out;
+}
+
+}  // namespace vhost

@@ -121,6 +121,19 @@ struct SceneData {
   void validate() const;  // Scene::validate, scene.cpp:63-157
 };
 
+// A batch of independent scenes merged into one world (BASELINE config C5): rods, materials,
+// planes, kinematic pills, bones, bundles, pins and activations concatenated scene by scene,
+// indices re-based. Each scene is validated on its own (same messages); all must share one
+// SolverSettings. Block order inside the merged world keeps every slot's reference order:
+// elastic (rods ascending), then pins, contacts and half-planes, each scene-major.
+struct BatchLayout {
+  int scenes = 1;
+  std::vector<int> rod_base;     // scenes + 1
+  std::vector<int> plane_scene;  // per plane
+  std::vector<int> kpill_scene;  // per kinematic pill
+};
+SceneData merge_scenes(const std::vector<const SceneData*>& scenes, BatchLayout& layout);
+
 // make_rest_pose, rod.cpp:60-112 (fills the rest fields of `rod`).
 void make_rest_pose(RodData& rod, const std::vector<V3>& centers, const std::vector<double>& radii,
                     const std::vector<double>& scales);

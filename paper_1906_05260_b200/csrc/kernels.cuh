@@ -27,6 +27,7 @@ namespace vdev {
 // Per-substep collision / external-block buffers.
 struct Collide {
   int P = 0;            // pills
+  int n_scenes = 1;     // batch: see World
   int T = 0;            // hash table size (power of two >= 2P)
   long long cand_cap = 0;
   long long contact_cap = 0;
@@ -103,6 +104,13 @@ struct Collide {
   int* ext_off = nullptr;        // V+1
   int* ext_cur = nullptr;        // V
   int* ext_items = nullptr;      // 4 x ext_cap entries (block << 2 | endpoint)
+  // batch of scenes (World::n_scenes > 1): pairs only within a scene, per-scene grid cell
+  int* pill_scene = nullptr;     // P
+  unsigned long long* scene_maxr = nullptr;  // per scene: max bounding radius bits
+  int* plane_scene = nullptr;    // n_planes
+  int* warm_rr_scene = nullptr;  // scene of each warm entry (lists are scene-major)
+  int* warm_rk_scene = nullptr;
+  SceneAcc* scene_acc = nullptr; // == World::scene_acc
   // device scalars
   int* scalars = nullptr;        // see Scalar enum
   unsigned long long* maxr_bits = nullptr;
@@ -145,6 +153,7 @@ struct SweepParams {
   // predecessor before touching any state; 2 (rod sweep right after an ext solve) it stages
   // and solves its tile first and waits only before gathering the external contributions.
   int pdl;
+  int* scene_singular;    // batch, last iteration only: per-scene singular-block counter
   const double* lam_in;  // elastic multipliers before this sweep (kLamFields x vpad)
   double* lam_out;       // after this sweep (ping-pong partner)
 };
@@ -215,6 +224,8 @@ void launch_rod_sweep(const World& w, Collide& c, const double* X, double* Y, co
 void launch_residuals(const World& w, const double* X, int classic, double* partials, int parts, double* out8,
                       cudaStream_t st);
 void launch_penetration(const World& w, Collide& c, const double* X, StepAccum* acc, cudaStream_t st);
+// batch: per-scene residual norms (one CTA per scene) and end-of-substep singular fold-in
+void launch_scene_report(const World& w, const double* X, int classic, int* scene_singular, cudaStream_t st);
 int report_parts(int V);
 
 // shape.cu

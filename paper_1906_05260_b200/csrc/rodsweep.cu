@@ -183,6 +183,11 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
       if (!owned) return;
       for (int f = f0; f < f0 + nf; ++f) sp.lam_out[f * (long long)vp + p] = t.st[T_LAM + f][si];
     };
+    auto sing = [&]() {  // singular block: counted by its owner (per scene in a batch's last sweep)
+      if (!owned) return;
+      ++nsing;
+      if (sp.scene_singular) atomicAdd(&sp.scene_singular[w.rod_scene[w.slot_rod[p]]], 1);
+    };
     auto fail = [&](int local) { bad = umin64(bad, err_code(sp.substep, ERR_SWEEP, sp.iter, t.bbase[pi] + local)); };
     const int ne = __popc(ek), nv = __popc(vk);
 
@@ -242,7 +247,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
             if (!(ok && isfinite(R.sz_dt[0]) && isfinite(R.sz_dt[1]))) fail(lbase + __popc(ek & (EK_SZ - 1)));
           }
         } else {
-          nsing += owned;
+          sing();
           keep_lam(L_SZ0, 3);
         }
       }
@@ -264,7 +269,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
             if (!(isfinite(dl) && isfinite(R.cs[0]) && isfinite(R.cs[1]))) fail(lbase + __popc(ek & (EK_CS - 1)));
           }
         } else {
-          nsing += owned;
+          sing();
           keep_lam(L_CS, 1);
         }
       }
@@ -288,7 +293,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
             if (!(isfinite(dl) && isfinite(R.ss[0]) && isfinite(R.ss[1]))) fail(lbase + __popc(ek & (EK_SS - 1)));
           }
         } else {
-          nsing += owned;
+          sing();
           keep_lam(L_SS, 1);
         }
       }
@@ -357,7 +362,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
               fail(lbase + __popc(ek & (EK_VS - 1)));
           }
         } else {
-          nsing += owned;
+          sing();
           keep_lam(L_VS0, 3);
         }
       }
@@ -443,7 +448,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
             if (!ok) fail(lbase + __popc(vk & (VK_BT - 1)));
           }
         } else {
-          nsing += owned;
+          sing();
           keep_lam(L_BT0, 3);
         }
       }
@@ -471,7 +476,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
               fail(lbase + __popc(vk & (VK_SB - 1)));
           }
         } else {
-          nsing += owned;
+          sing();
           keep_lam(L_SB, 1);
         }
       }
@@ -515,7 +520,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
               if (!ok) fail(lbase + __popc(vk & (bit - 1)));
             }
           } else {
-            nsing += owned;
+            sing();
             keep_lam(lf, 1);
           }
         }

@@ -45,7 +45,11 @@ static int next_pow2(long long x) {
   return p;
 }
 
-Solver::Solver(const SceneData& scene) : scene_(scene) {
+Solver::Solver(const SceneData& scene, const BatchLayout* batch) : scene_(scene) {
+  if (batch && batch->scenes > 1) {
+    batch_ = *batch;
+    n_scenes_ = batch->scenes;
+  }
   scene_.validate();
   // assemble_rod_constraints validates material and rest pose again (constraints.cpp:284-285)
   setup_ = build_setup(scene_);
@@ -54,7 +58,10 @@ Solver::Solver(const SceneData& scene) : scene_(scene) {
   const int K = static_cast<int>(scene_.kpills.size());
   for (const auto& rod : scene_.rods)
     if (rod.n + 1 >= 65536) throw std::invalid_argument("rod too long for the pair_key warm-start ids (>= 65535 elements)");
-  if (R + 1 >= 65536) throw std::invalid_argument("too many rods for the pair_key warm-start ids (>= 65535)");
+  for (int sc = 0; sc < n_scenes_; ++sc) {  // pair ids are scene-local
+    const int rods = n_scenes_ > 1 ? batch_.rod_base[sc + 1] - batch_.rod_base[sc] : R;
+    if (rods + 1 >= 65536) throw std::invalid_argument("too many rods for the pair_key warm-start ids (>= 65535)");
+  }
   for (const auto& kp : scene_.kpills)
     if (kp.pill.element != -1) throw std::invalid_argument("kinematic pills with element != -1 are not supported");
 
@@ -124,8 +131,11 @@ Solver::Solver(const SceneData& scene) : scene_(scene) {
     collide_possible_ = any && c_.P >= 2;
   }
   ext_possible_ = collide_possible_ || c_.n_planes > 0 || c_.n_pins > 0;
-  c_.cand_cap = collide_possible_ ? std::max<long long>(1 << 16, 24ll * c_.P) : 0;
-  c_.contact_cap = collide_possible_ ? std::max<long long>(1 << 15, 12ll * c_.P) : 0;
+  // Capacities (overflow raises a capacity error, never truncates). A batch of scenes gets a
+  // third of the single-scene headroom: its scenes are small and independent.
+  const long long cand_per_pill = n_scenes_ > 1 ? 8 : 24, ct_per_pill = n_scenes_ > 1 ? 4 : 12;
+  c_.cand_cap = collide_possible_ ? std::max<long long>(1 << 16, cand_per_pill * c_.P) : 0;
+  c_.contact_cap = collide_possible_ ? std::max<long long>(1 << 15, ct_per_pill * c_.P) : 0;
   c_.hp_cap = c_.n_planes * V;
   c_.ext_cap = ext_possible_ ? c_.n_pins + c_.contact_cap + c_.hp_cap : 0;
   c_.pill = dalloc<double>(8ull * std::max(c_.P, 1));
@@ -183,6 +193,39 @@ Solver::Solver(const SceneData& scene) : scene_(scene) {
                                                   c_.contact_cap, static_cast<long long>(c_.hp_cap), static_cast<long long>(V)});
   c_.scan_parts = static_cast<int>(vdev::scan_partials_needed(scan_max));
   c_.scan_tmp = dalloc<int>(c_.scan_parts);
+
+  // ---- batch of scenes ---------------------------------------------------------------------
+  if (n_scenes_ > 1) {
+    const int S = n_scenes_;
+    w_.n_scenes = S;
+    c_.n_scenes = S;
+    w_.rod_scene = dalloc<int>(R);
+    w_.scene_vbase = dalloc<int>(S + 1);
+    w_.scene_acc = dalloc<vdev::SceneAcc>(S);
+    c_.scene_acc = w_.scene_acc;
+    c_.pill_scene = dalloc<int>(c_.P);
+    c_.scene_maxr = dalloc<unsigned long long>(S);
+    c_.plane_scene = dalloc<int>(c_.n_planes);
+    c_.warm_rr_scene = dalloc<int>(c_.contact_cap);
+    c_.warm_rk_scene = dalloc<int>(K > 0 ? c_.contact_cap : 1);
+    d_scene_sing_ = dalloc<int>(S);
+    check_cuda(cudaMallocHost(&h_scene_acc_, sizeof(vdev::SceneAcc) * S), "cudaMallocHost");
+    std::vector<int> rod_scene(R), vb(S + 1), pill_scene;
+    for (int sc = 0; sc < S; ++sc) {
+      for (int r = batch_.rod_base[sc]; r < batch_.rod_base[sc + 1]; ++r) rod_scene[r] = sc;
+      vb[sc] = batch_.rod_base[sc] < R ? setup_.vbase[batch_.rod_base[sc]] : V;
+    }
+    vb[S] = V;
+    for (int sc = S - 1; sc >= 0; --sc)  // scenes without rods: empty range
+      if (batch_.rod_base[sc] == batch_.rod_base[sc + 1]) vb[sc] = vb[sc + 1];
+    for (int r = 0; r < R; ++r)
+      for (int e = 0; e < scene_.rods[r].n - 1; ++e) pill_scene.push_back(rod_scene[r]);
+    pill_scene.insert(pill_scene.end(), batch_.kpill_scene.begin(), batch_.kpill_scene.end());
+    upload(w_.rod_scene, rod_scene, stream_);
+    upload(w_.scene_vbase, vb, stream_);
+    upload(c_.pill_scene, pill_scene, stream_);
+    upload(c_.plane_scene, batch_.plane_scene, stream_);
+  }
 
   // ---- shape matching ----------------------------------------------------------------------
   g_.G = static_cast<int>(setup_.groups.size());
@@ -291,6 +334,7 @@ Solver::~Solver() {
   for (void* p : allocs_) cudaFree(p);
   if (h_anim_) cudaFreeHost(h_anim_);
   if (h_acc_) cudaFreeHost(h_acc_);
+  if (h_scene_acc_) cudaFreeHost(h_scene_acc_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -458,7 +502,10 @@ void Solver::upload_static() {
       pel[i] = e;
       pgrp[i] = rod.group;
       pself[i] = rod.self_collide ? 1 : 0;
-      pid[i] = (static_cast<uint32_t>(r + 1) << 16) | (static_cast<uint32_t>(e + 1) & 0xffffu);
+      const int local = n_scenes_ > 1 ? r - batch_.rod_base[std::upper_bound(batch_.rod_base.begin(), batch_.rod_base.end(), r) -
+                                                         batch_.rod_base.begin() - 1]
+                                      : r;  // pair ids are scene-local in a batch
+      pid[i] = (static_cast<uint32_t>(local + 1) << 16) | (static_cast<uint32_t>(e + 1) & 0xffffu);
     }
   }
   for (const auto& kp : scene_.kpills) {
@@ -579,6 +626,8 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
   // Programmatic dependent launch between the step's kernels (not when profiling: the event
   // brackets between categories would serialize them anyway).
   vdev::g_pdl = pdl_ && !prof;
+  if (n_scenes_ > 1)
+    check_cuda(cudaMemsetAsync(w_.scene_acc, 0, sizeof(vdev::SceneAcc) * n_scenes_, st), "scene report reset");
   vdev::launch_kernel(k_init_acc, 1, 1, 0, st, vdev::g_pdl, d_acc_, d_err_, c_.scalars);
   check_cuda(cudaMemcpyAsync(d_anim_, h_anim_, sizeof(double) * al_.stride * substeps, cudaMemcpyHostToDevice, st),
              "anim upload");
@@ -601,12 +650,13 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
     double* cur = w_.X;
     double* nxt = w_.Y;
     vdev::SweepParams sp{h, h2, scene_.settings.beta, classic_ ? 1 : 0, 0, s, c_.n_pins, setup_.elastic_blocks,
-                         scene_.settings.contact_k, 0, nullptr, nullptr};
+                         scene_.settings.contact_k, 0, nullptr, nullptr, nullptr};
     const bool pdl = vdev::g_pdl;
     double* lam_a = w_.lam;
     double* lam_b = w_.lam + static_cast<std::size_t>(vdev::kLamFields) * w_.vpad;
     for (int it = 0; it < iterations; ++it) {
       sp.iter = it;
+      sp.scene_singular = (n_scenes_ > 1 && it == iterations - 1) ? d_scene_sing_ : nullptr;
       sp.lam_in = (it & 1) ? lam_b : lam_a;
       sp.lam_out = (it & 1) ? lam_a : lam_b;
       if (c_.ext_cap > 0) {
@@ -632,12 +682,16 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
     vdev::launch_residuals(w_, w_.X, w_.classic, d_report_partials_, report_parts_,
                            reinterpret_cast<double*>(reinterpret_cast<char*>(d_acc_) + offsetof(StepAccum, residuals)), st);
     if (ext_possible_ && (c_.contact_cap + c_.hp_cap) > 0) vdev::launch_penetration(w_, c_, w_.X, d_acc_, st);
+    if (n_scenes_ > 1) vdev::launch_scene_report(w_, w_.X, w_.classic, d_scene_sing_, st);
     vdev::launch_kernel(k_end_substep, 1, 1, 0, st, vdev::g_pdl, d_acc_, d_singular_ + (iterations - 1));
     end();
   }
   vdev::launch_kernel(k_end_step, 1, 1, 0, st, vdev::g_pdl, d_acc_, d_err_, c_.scalars);
   vdev::g_pdl = false;
   check_cuda(cudaMemcpyAsync(h_acc_, d_acc_, sizeof(StepAccum), cudaMemcpyDeviceToHost, st), "report download");
+  if (n_scenes_ > 1)
+    check_cuda(cudaMemcpyAsync(h_scene_acc_, w_.scene_acc, sizeof(vdev::SceneAcc) * n_scenes_, cudaMemcpyDeviceToHost, st),
+               "scene report download");
 }
 
 static const char* kKindNames[11] = {"stretch_z", "cross_section", "surface_stretch", "bend_twist", "surface_bending",
@@ -823,6 +877,7 @@ Report Solver::step() {
   Report rr;
   finish_step(h, S, &rr);
   rr.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  last_report_ = rr;
   return rr;
 }
 
@@ -1106,6 +1161,32 @@ std::vector<PillData> Solver::current_pills() {  // Solver::current_pills, solve
       p.c1 = qrot(rot, p.c1) + pos;
     }
     out.push_back(p);
+  }
+  return out;
+}
+
+}  // namespace vhost
+
+namespace vhost {
+
+std::vector<Report> Solver::scene_reports() const {
+  if (n_scenes_ <= 1) return {last_report_};
+  std::vector<Report> out(n_scenes_);
+  for (int sc = 0; sc < n_scenes_; ++sc) {
+    const vdev::SceneAcc& a = h_scene_acc_[sc];
+    Report& r = out[sc];
+    r.step = last_report_.step;
+    r.time = last_report_.time;
+    r.total_ms = last_report_.total_ms;
+    r.contacts = a.contact_count;
+    r.broad = a.broad_pairs;
+    r.singular = a.skipped_singular;
+    r.max_pen = a.max_penetration;
+    for (int k = 0; k < 8; ++k) r.residuals[k] = a.residuals[k];
+    int dof = 0;
+    for (int rod = batch_.rod_base[sc]; rod < batch_.rod_base[sc + 1]; ++rod)
+      dof += 4 * scene_.rods[rod].n + 3 * (scene_.rods[rod].n - 1);
+    r.dof = dof;
   }
   return out;
 }

@@ -29,7 +29,8 @@ struct DeviceError : std::runtime_error {
 
 class Solver {
  public:
-  explicit Solver(const SceneData& scene);
+  // batch != nullptr with batch->scenes > 1: `scene` is merge_scenes() of independent scenes
+  explicit Solver(const SceneData& scene, const BatchLayout* batch = nullptr);
   ~Solver();
   Solver(const Solver&) = delete;
   Solver& operator=(const Solver&) = delete;
@@ -58,6 +59,9 @@ class Solver {
   void inverse_weights(double* ic, double* is, double* it);
   long long contacts(long long cap, int* a, int* b, double* alpha, double* beta);
   std::vector<PillData> current_pills();
+  // Per-scene reports of the last step (batch; a single scene returns one entry == step()).
+  int scene_count() const { return n_scenes_; }
+  std::vector<Report> scene_reports() const;
 
   // ---- bench / profiling (include/vrod_bench.h) ----
   enum Category { CAT_PREDICT = 0, CAT_COLLIDE, CAT_EXT_SETUP, CAT_EXT_SOLVE, CAT_ROD_SWEEP, CAT_SHAPE, CAT_REPORT,
@@ -133,6 +137,12 @@ class Solver {
   int report_parts_ = 0;
   double* d_probe_ = nullptr;
   long long last_max_cand_ = 0, last_max_ct_ = 0;
+  // batch of scenes
+  int n_scenes_ = 1;
+  BatchLayout batch_;
+  int* d_scene_sing_ = nullptr;
+  vdev::SceneAcc* h_scene_acc_ = nullptr;  // pinned, n_scenes_ (batch only)
+  Report last_report_;
 };
 
 void check_cuda(cudaError_t e, const char* what);

@@ -86,6 +86,13 @@ __device__ double ext_residual(const World& w, const Collide& c, const double* X
   return dot(V3{pl[0], pl[1], pl[2]}, ldc(X, vp, v)) - pl[3] - F(X, S, vp, v) * F(w.vstat, RBAR, vp, v);
 }
 
+// Scene of external block b (batch only).
+__device__ __forceinline__ int ext_scene(const World& w, const Collide& c, int b, int npins, int nct) {
+  if (b < npins) return w.rod_scene[w.slot_rod[c.pin_slot[b]]];
+  if (b < npins + nct) return c.pill_scene[c.ct_a[b - npins]];
+  return c.plane_scene[c.hp_plane[b - npins - nct]];
+}
+
 __global__ void k_ext_solve(World w, Collide c, const double* __restrict__ X, SweepParams sp, int* singular,
                             unsigned long long* err) {
   if (sp.pdl) {
@@ -102,6 +109,10 @@ __global__ void k_ext_solve(World w, Collide c, const double* __restrict__ X, Sw
   int nsing = 0;
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) {
     double* lam = c.ext_lam + 3ll * b;
+    auto sing = [&]() {  // singular block (counted; per scene in a batch's last sweep)
+      ++nsing;
+      if (sp.scene_singular) atomicAdd(&sp.scene_singular[ext_scene(w, c, b, npins, nct)], 1);
+    };
     // Writes endpoint e's update into its incidence entry (flag 0 = no update from this block).
     auto put = [&](int e, int flag, double x, double y, double z, double ds) {
       const int q = c.ext_pos[4 * b + e];
@@ -136,7 +147,7 @@ __global__ void k_ext_solve(World w, Collide c, const double* __restrict__ X, Sw
         rhs[d] = W[d] - kinv * lam[d];
       }
       if (!solve3(M, rhs, sp.beta, dl)) {
-        ++nsing;
+        sing();
         put(0, 0, 0, 0, 0, 0);
       } else {
         active = true;
@@ -195,7 +206,7 @@ __global__ void k_ext_solve(World w, Collide c, const double* __restrict__ X, Sw
         M = M + kinv;
         const double rhs = W - kinv * lam[0];
         if (M <= 1e-250) {
-          ++nsing;
+          sing();
         } else {
           double dl = sp.beta * rhs / M;
           if (lam[0] + dl > 0.0) dl = -lam[0];
@@ -237,7 +248,7 @@ __global__ void k_ext_solve(World w, Collide c, const double* __restrict__ X, Sw
         M = M + kinv;
         const double rhs = W - kinv * lam[0];
         if (M <= 1e-250) {
-          ++nsing;
+          sing();
         } else {
           double dl = sp.beta * rhs / M;
           if (lam[0] + dl > 0.0) dl = -lam[0];
@@ -258,6 +269,7 @@ __global__ void k_ext_solve(World w, Collide c, const double* __restrict__ X, Sw
   for (int o = 16; o > 0; o >>= 1) nsing += __shfl_down_sync(0xffffffffu, nsing, o);
   if ((threadIdx.x & 31) == 0 && nsing) atomicAdd(singular, nsing);
 }
+
 
 // ---- incidence list slot -> external blocks (built once per substep) ---------------------
 
@@ -341,14 +353,11 @@ __global__ void k_ext_sort(Collide c, int V) {
 
 constexpr int kRepThreads = 256;
 
-__global__ void k_report_partial(World w, const double* __restrict__ X, int classic, double* partials) {
-  pdl_wait();
-  pdl_trigger();
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  double acc[16];
-#pragma unroll
-  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
-  if (v < w.V) {
+// Residual terms of the elastic blocks owned by slot v (element v, interior vertex v):
+// acc[kind] += length weight * |W|^2, acc[8 + kind] += length weight.
+__device__ __forceinline__ void slot_residual_terms(const World& w, const double* __restrict__ X, int classic, int v,
+                                                    double (&acc)[16]) {
+  {
     const int vp = w.vpad;
     const int k = w.slot_loc[v], m = w.slot_m[v], r = w.slot_rod[v];
     const int ek = w.rod_ekinds[r], vk = w.rod_vkinds[r];
@@ -416,6 +425,16 @@ __global__ void k_report_partial(World w, const double* __restrict__ X, int clas
       }
     }
   }
+}
+
+__global__ void k_report_partial(World w, const double* __restrict__ X, int classic, double* partials) {
+  pdl_wait();
+  pdl_trigger();
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  double acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+  if (v < w.V) slot_residual_terms(w, X, classic, v, acc);
   // fixed-order block tree reduction
   __shared__ double red[kRepThreads];
   for (int q = 0; q < 16; ++q) {
@@ -461,11 +480,55 @@ __global__ void k_penetration(World w, Collide c, const double* __restrict__ X, 
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
     const double pen = -ext_residual(w, c, X, npins + q, npins, nct);
     if (pen > deepest) deepest = pen;
+    if (c.pill_scene && pen > 0.0) {  // batch: per-scene max as well
+      const int scene = q < nct ? c.pill_scene[c.ct_a[q]] : c.plane_scene[c.hp_plane[q - nct]];
+      atomicMax(reinterpret_cast<unsigned long long*>(&c.scene_acc[scene].max_penetration),
+                static_cast<unsigned long long>(__double_as_longlong(pen)));
+    }
   }
   for (int o = 16; o > 0; o >>= 1) deepest = fmax(deepest, __shfl_down_sync(0xffffffffu, deepest, o));
   if ((threadIdx.x & 31) == 0 && deepest > 0.0)
     atomicMax(reinterpret_cast<unsigned long long*>(&acc->max_penetration),
               static_cast<unsigned long long>(__double_as_longlong(deepest)));
+}
+
+// Batch: per-scene residual norms of the scene's slot range (one CTA per scene, fixed tree),
+// overwriting the previous substep's (Solver::step keeps the last substep's, solver.cpp:370).
+__global__ void k_report_scene(World w, const double* __restrict__ X, int classic) {
+  pdl_wait();
+  pdl_trigger();
+  const int sc = blockIdx.x;
+  double acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+  for (int v = w.scene_vbase[sc] + threadIdx.x; v < w.scene_vbase[sc + 1]; v += kRepThreads)
+    slot_residual_terms(w, X, classic, v, acc);
+  __shared__ double red[kRepThreads];
+  __shared__ double res[16];
+  for (int q = 0; q < 16; ++q) {
+    red[threadIdx.x] = acc[q];
+    __syncthreads();
+    for (int s = kRepThreads / 2; s > 0; s >>= 1) {
+      if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) res[q] = red[0];
+    __syncthreads();
+  }
+  if (threadIdx.x < 8) {
+    const double num = res[threadIdx.x], den = res[threadIdx.x + 8];
+    w.scene_acc[sc].residuals[threadIdx.x] = den > 0 ? sqrt(num / den) : 0.0;
+  }
+}
+
+// Batch: fold the last sweep's per-scene singular counts into the step totals.
+__global__ void k_scene_singular(World w, int* scene_singular) {
+  pdl_wait();
+  pdl_trigger();
+  for (int sc = blockIdx.x * blockDim.x + threadIdx.x; sc < w.n_scenes; sc += gridDim.x * blockDim.x) {
+    w.scene_acc[sc].skipped_singular += scene_singular[sc];
+    scene_singular[sc] = 0;
+  }
 }
 
 int grid_for(long long n) {
@@ -503,6 +566,11 @@ void launch_residuals(const World& w, const double* X, int classic, double* part
                       cudaStream_t st) {
   launch_kernel(k_report_partial, parts, kRepThreads, 0, st, g_pdl, w, X, classic, partials);
   launch_kernel(k_report_final, 1, kRepThreads, 0, st, g_pdl, partials, parts, out8);
+}
+
+void launch_scene_report(const World& w, const double* X, int classic, int* scene_singular, cudaStream_t st) {
+  launch_kernel(k_report_scene, w.n_scenes, kRepThreads, 0, st, g_pdl, w, X, classic);
+  launch_kernel(k_scene_singular, (w.n_scenes + kThreads - 1) / kThreads, kThreads, 0, st, g_pdl, w, scene_singular);
 }
 
 void launch_penetration(const World& w, Collide& c, const double* X, StepAccum* acc, cudaStream_t st) {

@@ -64,7 +64,24 @@ struct StepAccum {  // device-side StepReport accumulation (solver.cpp:363-388)
   long long max_contacts;
 };
 
+// Per-scene StepReport accumulation when the world is a batch of independent scenes
+// (BASELINE config C5). Same semantics as StepAccum, per scene.
+struct SceneAcc {
+  double residuals[8];
+  double max_penetration;
+  int contact_count;
+  int broad_pairs;
+  int skipped_singular;
+  int pad;
+};
+
 struct World {
+  // Batch of independent scenes: rods of scene s are [scene_rod_base[s], scene_rod_base[s+1]),
+  // their slots contiguous [scene_vbase[s], scene_vbase[s+1]). n_scenes == 1: arrays null.
+  int n_scenes = 1;
+  int* rod_scene = nullptr;
+  int* scene_vbase = nullptr;
+  SceneAcc* scene_acc = nullptr;
   int R = 0;          // rods
   int V = 0;          // slots (= total vertices)
   int vpad = 0;       // field stride

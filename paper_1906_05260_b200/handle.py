@@ -42,14 +42,30 @@ class StepReport:
 
 
 class SolverHandle:
-    def __init__(self, lib, scene: Scene):
+    def __init__(self, lib, scene: Scene | None, *, _batch: list[Scene] | None = None):
         self._lib = lib
         self._h = C.c_void_p()
-        sh = marshal_scene(lib, scene)
-        try:
-            check(lib, lib.vrod_solver_create(sh, C.byref(self._h)))
-        finally:
-            lib.vrod_scene_destroy(sh)
+        if _batch is None:
+            sh = marshal_scene(lib, scene)
+            try:
+                check(lib, lib.vrod_solver_create(sh, C.byref(self._h)))
+            finally:
+                lib.vrod_scene_destroy(sh)
+        else:
+            # a Scene object repeated in the batch is marshalled once and referenced again
+            unique: dict[int, C.c_void_p] = {}
+            try:
+                for s in _batch:
+                    if id(s) not in unique:
+                        unique[id(s)] = marshal_scene(lib, s)
+                arr = (C.c_void_p * len(_batch))(*[unique[id(s)].value for s in _batch])
+                check(lib, lib.vrod_batch_create(len(_batch), arr, C.byref(self._h)))
+            finally:
+                for h in unique.values():
+                    lib.vrod_scene_destroy(h)
+        n = C.c_int32()
+        check(lib, lib.vrod_solver_scene_count(self._h, C.byref(n)))
+        self.scene_count = n.value
         info = self.info()
         self.rod_count = info.rod_count
         self.total_vertices = info.total_vertices
@@ -59,6 +75,17 @@ class SolverHandle:
         self.rod_sizes = sizes[: self.rod_count].astype(np.int64)
         self.vertex_base = np.concatenate([[0], np.cumsum(self.rod_sizes)])[:-1] if self.rod_count else np.zeros(0)
         self.element_base = self.vertex_base - np.arange(self.rod_count)
+
+    @classmethod
+    def batch(cls, lib, scenes: list[Scene]) -> "SolverHandle":
+        """A batch of independent scenes stepped together (vrod_batch_create, BASELINE C5)."""
+        return cls(lib, None, _batch=list(scenes))
+
+    def scene_reports(self) -> list[StepReport]:
+        """Per-scene StepReports of the last step (vrod_solver_scene_reports)."""
+        arr = (capi.StepReport * self.scene_count)()
+        check(self._lib, self._lib.vrod_solver_scene_reports(self._h, self.scene_count, arr))
+        return [StepReport.from_c(r) for r in arr]
 
     # -- lifetime -------------------------------------------------------------------------------
     def close(self) -> None:

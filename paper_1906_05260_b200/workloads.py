@@ -142,6 +142,40 @@ def c3_muscle_bundle(lib, muscles: int = 4, rods_per_muscle: int = 32, vertices:
     return s
 
 
+def c5_scene(lib, index: int) -> Scene:
+    """Scene `index` of C5, the batch of independent C3 scenes: activation on
+    muscle (index mod 4) and an initial lateral velocity of amplitude 0.5 * (1 + (index mod 7)/7)
+    m/s (sine profile along each rod, zero at the pinned ends, per-rod direction from a seeded
+    generator). Scenes with equal (index mod 4, index mod 7) are identical: 28 distinct scenes."""
+    s = c3_muscle_bundle(lib, activate=(index % 4,))
+    amp = 0.5 * (1.0 + (index % 7) / 7.0)
+    rng = np.random.default_rng(1000 + (index % 28))
+    for rod in s.rods:
+        phi = rng.uniform(0.0, 2.0 * np.pi)
+        n = len(rod.state.scales)
+        prof = np.sin(np.pi * np.arange(n) / (n - 1))
+        rod.state.center_vel[:, 0] = amp * np.cos(phi) * prof
+        rod.state.center_vel[:, 1] = amp * np.sin(phi) * prof
+    return s
+
+
+def c5_batch(lib, count: int, first: int = 0) -> list[Scene]:
+    """Scenes first .. first+count-1 of C5 (the 28 distinct ones are built once and shared)."""
+    distinct: dict[int, Scene] = {}
+    out = []
+    for i in range(first, first + count):
+        key = i % 28
+        if key not in distinct:
+            distinct[key] = c5_scene(lib, i)
+        out.append(distinct[key])
+    return out
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous shard [rank*n/world, (rank+1)*n/world) of n independent scenes."""
+    return rank * n // world, (rank + 1) * n // world
+
+
 def c4_rod_forest(lib, nx: int = 125, ny: int = 250, vertices: int = 32, seed: int = 1234,
                   pitch: float = 0.100) -> Scene:
     """C4: 1M-vertex synthetic rod forest: nx x ny vertical rods x 32 vertices
