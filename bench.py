@@ -17,6 +17,10 @@ Multi-GPU: one process per GPU (torchrun); each rank steps its own independent C
 (replicas / weak scaling, no inter-GPU collective on the data path); the timed region is
 bracketed by barriers and the max over ranks is reported.
 
+Batch (`batch` key): C5, 8192 independent C3 scenes split into contiguous shards over the
+ranks (strong scaling), each shard stepped as one device world; per-scene stats are
+all-gathered to rank 0 over NCCL at the end — the only collective.
+
 `--impl reference` times the reference's own CPU implementation (oracle/_ref: the reference's
 sources compiled against the Eigen shim; else the oracle restatement) on all host threads.
 """
@@ -203,6 +207,9 @@ def main():
     ap.add_argument("--secondary-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=90.0, help="cap of the --impl reference timed sample")
+    ap.add_argument("--no-batch", action="store_true", help="skip the C5 sharded-batch measurement")
+    ap.add_argument("--batch-scenes", type=int, default=8192, help="C5 batch size, sharded over the ranks")
+    ap.add_argument("--batch-steps", type=int, default=3)
     args = ap.parse_args()
     rank, world, local = dist_info()
     if args.impl == "reference":
@@ -222,7 +229,8 @@ def main():
         import torch
         import torch.distributed as tdist
         # host-side barrier / max-over-ranks only: the replicas exchange no data
-        tdist.init_process_group("gloo")
+        from datetime import timedelta
+        tdist.init_process_group("gloo", timeout=timedelta(seconds=900))
         dist = (torch, tdist)
 
     lib = bind_bench(pb.library())
@@ -265,6 +273,14 @@ def main():
     vpad = max(32, (V + 31) // 32 * 32)
     h2d = 8 * S * (1 + 3 * 0 + len(scene.activations) + 14 * len(scene.bones) + 8 * len(scene.kinematic_pills))
     d2h = 8 * (8 + 7) * vpad + 160  # state + velocity fields of get_state, plus the StepReport
+
+    # ---- C5: the 8192-scene batch sharded over the ranks (every rank takes part) ----
+    batch = None
+    if not args.no_batch:
+        try:
+            batch = run_c5(lib, args, rank, world, dist, barrier)
+        except Exception as exc:  # report, do not lose the headline
+            batch = {"error": f"{type(exc).__name__}: {exc}"}
 
     if rank != 0:
         if dist:
@@ -309,6 +325,8 @@ def main():
             "gpu_launches": int(kern) * args.steps, "kernels_per_step": int(kern),
             "roofline": roofline, "breakdown": breakdown, "cpu_baseline": cpu, "clocks": clocks}
 
+    if batch is not None:
+        line["batch"] = batch
     if not args.no_secondary:
         try:
             line["secondary"] = run_c4(lib, args.secondary_steps, peak)
@@ -317,6 +335,51 @@ def main():
     print(json.dumps(line), flush=True)
     if dist:
         dist[1].destroy_process_group()
+
+
+def run_c5(lib, args, rank, world, dist, barrier):
+    """C5: `--batch-scenes` independent C3 scenes, contiguous shard per rank, each shard ONE device
+    world; timed with CUDA events (max over ranks); per-scene stats all-gathered to rank 0 at the
+    end (NCCL when N > 1) — the only inter-GPU traffic."""
+    import paper_1906_05260_b200 as pb
+    from paper_1906_05260_b200 import batch as pbatch
+    from paper_1906_05260_b200 import workloads
+    n_total = args.batch_scenes
+    lo, hi = workloads.shard_range(n_total, rank, world)
+    t0 = time.perf_counter()
+    solver = pb.BatchSolver(workloads.c5_batch(lib, hi - lo, first=lo))
+    setup_s = time.perf_counter() - t0
+    scene0 = workloads.c5_scene(lib, lo)
+    S, I = scene0.settings.substeps, scene0.settings.iterations
+    solver.step()  # warm-up (captures the graph)
+    barrier()
+    ms, kern = device_run(lib, solver, args.batch_steps, 0)  # >= 3.9M vertices per GPU: working set >> L2
+    barrier()
+    if dist:
+        t = dist[0].tensor([ms], dtype=dist[0].float64)
+        dist[1].all_reduce(t, op=dist[1].ReduceOp.MAX)
+        ms = float(t.item())
+    rows = pbatch.report_rows(solver.scene_reports())
+    if dist:
+        torch, tdist = dist
+        nccl = tdist.new_group(backend="nccl")
+        table = pbatch.gather_scene_stats(rows, n_total, device=torch.device("cuda", 0), group=nccl)
+    else:
+        table = rows
+    t_step = ms / 1e3 / args.batch_steps
+    V = solver.total_vertices
+    out = {"workload": f"C5 batch of {n_total} independent C3 scenes (28 distinct), contiguous shard per GPU, "
+                       f"one device world per shard",
+           "scenes": n_total, "scenes_per_gpu": hi - lo, "vertices_per_gpu": V, "steps": args.batch_steps,
+           "ms_per_step": t_step * 1e3, "scene_substeps_per_sec": n_total * S / t_step,
+           "vertex_iters_per_sec": V * world * I * S / t_step, "setup_s": setup_s, "kernels_per_step": int(kern),
+           "scaling": "strong (fixed 8192-scene batch split over the GPUs)",
+           "stats_gather": "NCCL all_gather of per-scene stats" if dist else "single GPU"}
+    if table is not None:
+        out["gathered"] = {"scenes": int(table.shape[0]), "contacts": int(table[:, 9].sum()),
+                           "broad_pairs": int(table[:, 10].sum()), "max_penetration": float(table[:, 8].max())}
+    del solver
+    return out
 
 
 def run_c4(lib, steps, peak):

@@ -230,8 +230,8 @@ int vrod_solver_current_pills(vrod_solver* solver, int64_t capacity, int64_t* co
  * scene's results equal that scene solved alone. All scenes must share one SolverSettings
  * (dt, substeps, iterations, ...). State / rod-size queries see the scenes concatenated in
  * order (global slot order of scene 0, then scene 1, ...). vrod_solver_step on a batch
- * returns the batch total: contact_count, broad_pairs, skipped_singular summed,
- * max_penetration and each residual the maximum over scenes. */
+ * returns the batch total: contact_count, broad_pairs, skipped_singular summed (saturating
+ * at INT32_MAX), max_penetration and each residual the maximum over scenes. */
 int vrod_batch_create(int32_t scene_count, const vrod_scene* const* scenes, vrod_solver** out);
 /* Number of scenes of a solver (1 for vrod_solver_create). */
 int vrod_solver_scene_count(const vrod_solver* solver, int32_t* count);

@@ -28,7 +28,7 @@ def report_rows(reports) -> np.ndarray:
     return out
 
 
-def gather_scene_stats(rows: np.ndarray, n_total: int, device=None) -> np.ndarray | None:
+def gather_scene_stats(rows: np.ndarray, n_total: int, device=None, group=None) -> np.ndarray | None:
     """All-gather every rank's shard rows; rank 0 gets the (n_total, 12) table in scene order.
 
     Shards are contiguous (`shard_range`), so concatenating rank by rank restores scene order.
@@ -36,12 +36,12 @@ def gather_scene_stats(rows: np.ndarray, n_total: int, device=None) -> np.ndarra
     import torch
     import torch.distributed as dist
 
-    world, rank = dist.get_world_size(), dist.get_rank()
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
     cap = max(hi - lo for lo, hi in (shard_range(n_total, r, world) for r in range(world)))
     buf = torch.zeros((cap, rows.shape[1]), dtype=torch.float64, device=device)
     buf[: rows.shape[0]] = torch.from_numpy(rows).to(device)
     parts = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(parts, buf)
+    dist.all_gather(parts, buf, group=group)
     if rank != 0:
         return None
     out = []

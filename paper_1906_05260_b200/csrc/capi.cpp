@@ -257,13 +257,21 @@ static void put_report(const Report& r, vrod_step_report* out) {
 int vrod_solver_step(vrod_solver* h, vrod_step_report* out) {
   return guarded([&] {
     Report r = h->s->step();
-    if (h->s->scene_count() > 1) {  // batch total: residuals and penetration as the max over scenes
+    if (h->s->scene_count() > 1) {  // batch total: maxima over scenes, counters summed (saturating)
       for (int k = 0; k < 8; ++k) r.residuals[k] = 0.0;
       r.max_pen = 0.0;
+      long long ct = 0, bp = 0, sg = 0;
       for (const Report& sr : h->s->scene_reports()) {
         for (int k = 0; k < 8; ++k) r.residuals[k] = std::max(r.residuals[k], sr.residuals[k]);
         r.max_pen = std::max(r.max_pen, sr.max_pen);
+        ct += sr.contacts;
+        bp += sr.broad;
+        sg += sr.singular;
       }
+      const auto sat = [](long long v) { return static_cast<int>(std::min<long long>(v, 2147483647ll)); };
+      r.contacts = sat(ct);
+      r.broad = sat(bp);
+      r.singular = sat(sg);
     }
     put_report(r, out);
   });

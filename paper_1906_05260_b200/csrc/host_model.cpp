@@ -206,13 +206,18 @@ void SceneData::validate() const {
     require(kp.bone < static_cast<int>(bones.size()), "kinematic pill bone out of range");
     if (kp.bone >= 0) require(!bones[kp.bone].keys.empty(), "kinematic pill bone has no keyframes");
   }
-  std::set<std::pair<int, int>> seen;
+  // one flag per (rod, vertex): linear in the member count (batches merge ~10^7 members)
+  std::vector<std::size_t> vbase(rc + 1, 0);
+  for (int r = 0; r < rc; ++r) vbase[r + 1] = vbase[r] + rods[r].rc.size();
+  std::vector<uint8_t> seen(bundles.empty() ? 0 : vbase[rc], 0);
   for (const auto& members : bundles) {
     require(members.size() >= 2, "bundle needs at least two members");
     for (const auto& [mr, mv] : members) {
       require_index(mr, rc, "bundle member rod");
       require_index(mv, static_cast<int>(rods[mr].rc.size()), "bundle member vertex");
-      require(seen.insert({mr, mv}).second, "bundle groups must not share a vertex");
+      uint8_t& f = seen[vbase[mr] + mv];
+      require(!f, "bundle groups must not share a vertex");
+      f = 1;
     }
   }
   for (const PinMotion& pm : pin_motions) {
@@ -284,8 +289,11 @@ Setup build_setup(const SceneData& s) {
   out.vpad = std::max(32, (out.V + 31) / 32 * 32);
 
   // Shape-matching groups (make_bundle_group, bundling.cpp:17-48) + level schedule.
-  std::map<int, int> last_level;  // frame slot -> highest level that wrote it so far
+  // frame slot -> highest level that wrote it so far; per-slot stamps find a group's distinct
+  // frames (flat arrays: batches merge ~10^6 groups)
+  std::vector<int> last_level(out.V, -1), stamp(out.V, -1);
   for (const auto& members : s.bundles) {
+    const int gid = static_cast<int>(out.groups.size());
     Setup::Group g;
     require(!members.empty(), "bundle group needs at least one member");
     const int n = static_cast<int>(members.size());
@@ -298,7 +306,7 @@ Setup build_setup(const SceneData& s) {
     cent = cent / static_cast<double>(n);
     g.rcent = cent;
     double denom = 0.0;
-    std::set<int> frames;
+    std::vector<int> frames;
     for (const auto& [mr, mv] : members) {
       const RodData& rod = s.rods[mr];
       const int e = std::min(mv, rod.n - 2);
@@ -312,15 +320,19 @@ Setup build_setup(const SceneData& s) {
       g.rR.push_back(R);
       g.qR.push_back(qfrom_mat(R));
       denom += sqnorm(c) + 3.0 * sc * sc;
-      if (!frames.insert(out.vbase[mr] + e).second) g.serial_apply = true;
+      const int f = out.vbase[mr] + e;
+      if (stamp[f] == gid) {
+        g.serial_apply = true;
+      } else {
+        stamp[f] = gid;
+        frames.push_back(f);
+      }
     }
     g.denom = denom;
     int level = 0;
-    for (int f : frames) {
-      auto it = last_level.find(f);
-      if (it != last_level.end()) level = std::max(level, it->second + 1);
-    }
-    for (int f : frames) last_level[f] = std::max(last_level.count(f) ? last_level[f] : -1, level);
+    for (int f : frames)
+      if (last_level[f] >= 0) level = std::max(level, last_level[f] + 1);
+    for (int f : frames) last_level[f] = std::max(last_level[f], level);
     out.group_level.push_back(level);
     out.levels = std::max(out.levels, level + 1);
     out.groups.push_back(std::move(g));
