@@ -69,6 +69,8 @@ struct Collide {
   double* ct_alpha = nullptr;
   double* ct_beta = nullptr;
   double* ct_dist = nullptr;     // standalone find_contacts only
+  int* ct_va = nullptr;          // first slot of each contact's pills (-1: kinematic), per substep
+  int* ct_vb = nullptr;
   // raw (unordered) narrow-phase hits and the (i, j) ordering scratch
   int* raw_i = nullptr;          // contact_cap
   int* raw_j = nullptr;
@@ -97,8 +99,7 @@ struct Collide {
   double* ext_lam = nullptr;     // 3 x ext_cap
   // Results are written per incidence entry q (slot-sorted), so the sweep's gather reads
   // contiguous entries instead of chasing block ids.
-  double* ext_contrib = nullptr; // 4 x (4 x ext_cap): entry q -> dc xyz, ds
-  uint8_t* ext_flag = nullptr;   // 4 x ext_cap: entry q -> kExtCenter | kExtScale, 0 = no update
+  double* ext_contrib = nullptr; // 4 x (4 x ext_cap): entry q -> dc xyz, ds (kExtNone markers)
   int* ext_pos = nullptr;        // 4 x ext_cap: (block << 2 | endpoint) -> entry q
   int* ext_cnt = nullptr;        // V+1 incidence counts
   int* ext_off = nullptr;        // V+1
@@ -117,6 +118,16 @@ struct Collide {
   int* scan_tmp = nullptr;       // scan partials
 };
 enum : int { kExtCenter = 1, kExtScale = 2 };
+// "No update" marker of an incidence entry: a NaN with a private payload in dc.x (the block
+// made no update) or in ds (no scale update: soft pins). A computed non-finite update can never
+// be applied silently — the ext solve flags it as the reference's SimulationError.
+constexpr unsigned long long kExtNoneBits = 0x7ff4e0de00000001ull;
+#ifdef __CUDACC__
+__device__ __forceinline__ double ext_none() { return __longlong_as_double(static_cast<long long>(kExtNoneBits)); }
+__device__ __forceinline__ bool is_ext_none(double v) {
+  return static_cast<unsigned long long>(__double_as_longlong(v)) == kExtNoneBits;
+}
+#endif
 enum Scalar : int { SC_NCAND = 0, SC_NCT, SC_NHP, SC_NRR, SC_NRK, SC_NRR_PREV, SC_NRK_PREV, SC_BROAD, SC_OVF,
                     SC_NCAND_RAW, SC_NCT_RAW, SC_NCAND2, kScalars };
 

@@ -619,26 +619,24 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
       if (t.act[A_VBV][pi + 1]) addt(N.vb_dta[1]);
     }
     if (has_ext) {  // external blocks touching this vertex, in block order (entries slot-sorted)
-      // Chunks of 4 entries: all loads of a chunk are issued before the first add (the flag only
-      // predicates the add), so the per-slot entry list costs one memory latency per chunk.
+      // Chunks of 4 entries: all loads of a chunk are issued before the first add (the entry's
+      // kExtNone markers only predicate the adds), so a slot's list costs one latency per chunk.
       const int e0 = c.ext_off[p], e1 = c.ext_off[p + 1];
       for (int q0 = e0; q0 < e1; q0 += 4) {
-        int fl[4];
         double2 o01[4], o23[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int q = q0 + u < e1 ? q0 + u : e0;
-          fl[u] = q0 + u < e1 ? c.ext_flag[q] : 0;
           const double2* o = reinterpret_cast<const double2*>(c.ext_contrib + 4ll * q);
           o01[u] = o[0];
           o23[u] = o[1];
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          if (!fl[u]) continue;
+          if (q0 + u >= e1 || is_ext_none(o01[u].x)) continue;
           const double d[3] = {o01[u].x, o01[u].y, o23[u].x};
           addc(d);
-          if (fl[u] & kExtScale) adds(o23[u].y);
+          if (!is_ext_none(o23[u].y)) adds(o23[u].y);
         }
       }
     }

@@ -166,6 +166,8 @@ Solver::Solver(const SceneData& scene, const BatchLayout* batch) : scene_(scene)
   c_.ct_b = dalloc<int>(c_.contact_cap);
   c_.ct_alpha = dalloc<double>(c_.contact_cap);
   c_.ct_beta = dalloc<double>(c_.contact_cap);
+  c_.ct_va = dalloc<int>(c_.contact_cap);
+  c_.ct_vb = dalloc<int>(c_.contact_cap);
   c_.warm_rr_key = dalloc<unsigned long long>(c_.contact_cap);
   c_.warm_rr_alpha = dalloc<double>(c_.contact_cap);
   c_.warm_rk_key = dalloc<unsigned long long>(K > 0 ? c_.contact_cap : 1);
@@ -181,7 +183,6 @@ Solver::Solver(const SceneData& scene, const BatchLayout* batch) : scene_(scene)
   c_.pin_data = dalloc<double>(4 * std::max(c_.n_pins, 1));
   c_.ext_lam = dalloc<double>(3 * c_.ext_cap);
   c_.ext_contrib = dalloc<double>(16 * c_.ext_cap);
-  c_.ext_flag = dalloc<uint8_t>(4 * c_.ext_cap);
   c_.ext_pos = dalloc<int>(4 * c_.ext_cap);
   c_.ext_cnt = dalloc<int>(V + 1);
   c_.ext_off = dalloc<int>(V + 1);

@@ -39,11 +39,10 @@ struct ExtGeom {  // resolve_pill, constraints.cpp:76-97
   double r0, r1, rb0, rb1;
   int v0;
 };
-__device__ __forceinline__ ExtGeom resolve(const World& w, const Collide& c, const double* X, int pill) {
+// resolve with the pill's first slot known (v = pill + rod, or -1 for a kinematic pill)
+__device__ __forceinline__ ExtGeom resolve_at(const World& w, const Collide& c, const double* X, int pill, int v) {
   ExtGeom g;
-  const int rod = c.pill_rod[pill];
-  if (rod >= 0) {
-    const int v = pill + rod;
+  if (v >= 0) {
     const int vp = w.vpad;
     g.c0 = ldc(X, vp, v);
     g.c1 = ldc(X, vp, v + 1);
@@ -62,6 +61,10 @@ __device__ __forceinline__ ExtGeom resolve(const World& w, const Collide& c, con
     g.v0 = -1;
   }
   return g;
+}
+__device__ __forceinline__ ExtGeom resolve(const World& w, const Collide& c, const double* X, int pill) {
+  const int rod = c.pill_rod[pill];
+  return resolve_at(w, c, X, pill, rod >= 0 ? pill + rod : -1);
 }
 
 // Residual of an external block (contact / half-plane only), for the end-of-step penetration.
@@ -93,8 +96,8 @@ __device__ __forceinline__ int ext_scene(const World& w, const Collide& c, int b
   return c.plane_scene[c.hp_plane[b - npins - nct]];
 }
 
-__global__ void k_ext_solve(World w, Collide c, const double* __restrict__ X, SweepParams sp, int* singular,
-                            unsigned long long* err) {
+__global__ void __launch_bounds__(256, 3) k_ext_solve(World w, Collide c, const double* __restrict__ X,
+                                                     SweepParams sp, int* singular, unsigned long long* err) {
   if (sp.pdl) {
     pdl_wait();
     pdl_trigger();
@@ -113,17 +116,19 @@ __global__ void k_ext_solve(World w, Collide c, const double* __restrict__ X, Sw
       ++nsing;
       if (sp.scene_singular) atomicAdd(&sp.scene_singular[ext_scene(w, c, b, npins, nct)], 1);
     };
-    // Writes endpoint e's update into its incidence entry (flag 0 = no update from this block).
-    auto put = [&](int e, int flag, double x, double y, double z, double ds) {
-      const int q = c.ext_pos[4 * b + e];
-      c.ext_flag[q] = static_cast<uint8_t>(flag);
+    // Writes an endpoint's update into its incidence entry q (flag 0 = no update from this block).
+    // The flag is folded into the entry: kExtNone in dc.x = no update, in ds = no scale update.
+    auto put_at = [&](int q, int flag, double x, double y, double z, double ds) {
+      double2* o = reinterpret_cast<double2*>(c.ext_contrib + 4ll * q);
       if (flag) {
-        double* o = c.ext_contrib + 4ll * q;
-        o[0] = x;
-        o[1] = y;
-        o[2] = z;
-        o[3] = ds;
+        o[0] = make_double2(x, y);
+        o[1] = make_double2(z, (flag & kExtScale) ? ds : ext_none());
+      } else {
+        o[0].x = ext_none();
       }
+    };
+    auto put = [&](int e, int flag, double x, double y, double z, double ds) {
+      put_at(c.ext_pos[4 * b + e], flag, x, y, z, ds);
     };
     bool active = false, finite = true;
     if (b < npins) {  // kPin (constraints.cpp:261-267), dim 3
@@ -163,8 +168,9 @@ __global__ void k_ext_solve(World w, Collide c, const double* __restrict__ X, Sw
       }
     } else if (b < npins + nct) {  // kContact (constraints.cpp:215-247), unilateral, dim 1
       const int k = b - npins;
-      const ExtGeom A = resolve(w, c, X, c.ct_a[k]);
-      const ExtGeom B = resolve(w, c, X, c.ct_b[k]);
+      // endpoint slots were stored by k_ext_count: X is one dependent load away
+      const ExtGeom A = resolve_at(w, c, X, c.ct_a[k], c.ct_va[k]);
+      const ExtGeom B = resolve_at(w, c, X, c.ct_b[k], c.ct_vb[k]);
       const double al = c.ct_alpha[k], be = c.ct_beta[k];
       const V3 ca = (1.0 - al) * A.c0 + al * A.c1;
       const V3 cb = (1.0 - be) * B.c0 + be * B.c1;
@@ -179,17 +185,27 @@ __global__ void k_ext_solve(World w, Collide c, const double* __restrict__ X, Sw
         W = dist - ra - rb;
       }
       const bool entry[4] = {A.v0 >= 0, A.v0 >= 0, B.v0 >= 0, B.v0 >= 0};
+      const int slot[4] = {A.v0, A.v0 + 1, B.v0, B.v0 + 1};
+      // every per-endpoint load issued up front (one latency, not a chain behind the branch)
+      double icv[4] = {0, 0, 0, 0}, isv[4] = {0, 0, 0, 0};
+      int qpos[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (entry[e]) {
+          icv[e] = F(w.vstat, IC, vp, slot[e]);
+          isv[e] = F(w.vstat, IS, vp, slot[e]);
+          qpos[e] = c.ext_pos[4 * b + e];
+        }
       bool wrote[4] = {false, false, false, false};
       if (!(W >= 0.0 && lam[0] == 0.0)) {
         const double coef[4] = {1.0 - al, al, -(1.0 - be), -be};
         const double sj[4] = {-(1.0 - al) * A.rb0, -al * A.rb1, -(1.0 - be) * B.rb0, -be * B.rb1};
-        const int slot[4] = {A.v0, A.v0 + 1, B.v0, B.v0 + 1};
         const bool has[4] = {live && A.v0 >= 0, live && A.v0 >= 0, live && B.v0 >= 0, live && B.v0 >= 0};
         double M = 0.0;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {  // centers
           if (!has[e]) continue;
-          const double ic = F(w.vstat, IC, vp, slot[e]);
+          const double ic = icv[e];
           if (ic == 0.0) continue;
           const double s = h2 * ic;
           const V3 j = coef[e] * nrm;
@@ -198,7 +214,7 @@ __global__ void k_ext_solve(World w, Collide c, const double* __restrict__ X, Sw
 #pragma unroll
         for (int e = 0; e < 4; ++e) {  // scales
           if (!has[e]) continue;
-          const double is = F(w.vstat, IS, vp, slot[e]);
+          const double is = isv[e];
           if (is == 0.0) continue;
           M = M + (h2 * is * sj[e]) * sj[e];
         }
@@ -217,18 +233,18 @@ __global__ void k_ext_solve(World w, Collide c, const double* __restrict__ X, Sw
           for (int e = 0; e < 4; ++e) {
             if (!has[e]) continue;
             const V3 j = coef[e] * nrm;
-            const double fc = -h2 * F(w.vstat, IC, vp, slot[e]);
+            const double fc = -h2 * icv[e];
             const double ox = fc * (j.x * dl), oy = fc * (j.y * dl), oz = fc * (j.z * dl);
-            const double os = -h2 * F(w.vstat, IS, vp, slot[e]) * (sj[e] * dl);
+            const double os = -h2 * isv[e] * (sj[e] * dl);
             finite = finite && isfinite(ox) && isfinite(oy) && isfinite(oz) && isfinite(os);
-            put(e, kExtCenter | kExtScale, ox, oy, oz, os);
+            put_at(qpos[e], kExtCenter | kExtScale, ox, oy, oz, os);
             wrote[e] = true;
           }
         }
       }
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (entry[e] && !wrote[e]) put(e, 0, 0, 0, 0, 0);
+        if (entry[e] && !wrote[e]) put_at(qpos[e], 0, 0, 0, 0, 0);
     } else {  // kHalfPlane (constraints.cpp:248-260), unilateral, dim 1
       const int k = b - npins - nct;
       const int v = c.hp_slot[k];
@@ -310,6 +326,10 @@ __global__ void k_ext_count(Collide c, int npins) {
     const int ne = ext_endpoints(c, b, npins, nct, slots);
     for (int e = 0; e < ne; ++e)
       if (slots[e] >= 0) atomicAdd(&c.ext_cnt[slots[e]], 1);
+    if (b >= npins && b < npins + nct) {
+      c.ct_va[b - npins] = slots[0];
+      c.ct_vb[b - npins] = slots[2];
+    }
     c.ext_lam[3ll * b] = 0.0;
     c.ext_lam[3ll * b + 1] = 0.0;
     c.ext_lam[3ll * b + 2] = 0.0;
