@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <cfloat>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "vmath.cuh"
 
@@ -303,9 +305,13 @@ __global__ void k_insert(Collide c) {
   __threadfence();
   const unsigned mask = static_cast<unsigned>(c.T - 1);
   unsigned h = static_cast<unsigned>(cell_hash(kx, ky, kz, scene)) & mask;
+  int rep = 0;
   while (true) {
     int e = atomicCAS(&c.table[h], -1, i);
-    if (e == -1) break;  // new cell, i is its representative
+    if (e == -1) {  // new cell, i is its representative
+      rep = 1;
+      break;
+    }
     const long long ex = static_cast<volatile long long*>(c.cellkey)[e];
     const long long ey = static_cast<volatile long long*>(c.cellkey)[c.P + e];
     const long long ez = static_cast<volatile long long*>(c.cellkey)[2 * c.P + e];
@@ -313,7 +319,16 @@ __global__ void k_insert(Collide c) {
     h = (h + 1) & mask;
   }
   c.pill_cell[i] = static_cast<int>(h);
+  c.rep_flag[i] = rep;
   atomicAdd(&c.cell_count[h], 1);
+}
+
+// Non-empty cells listed in representative-pill order (spatially coherent, deterministic).
+__global__ void k_cell_list(Collide c) {
+  pdl_wait();
+  pdl_trigger();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c.P; i += gridDim.x * blockDim.x)
+    if (c.rep_flag[i]) c.cell_list[c.rep_pos[i]] = c.pill_cell[i];
 }
 
 __global__ void k_scatter(Collide c) {
@@ -516,6 +531,139 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_warp(Collide c, int p
     }
     pos += __popc(m);
   }
+}
+
+// One WARP per non-empty grid cell (table slot). Lanes 0..26 probe the 27 cells of its 3x3x3
+// block; the cell's member pills are staged in shared memory, and the warp strides over the
+// flattened neighbourhood items j, loading each j once and testing it against every member i
+// (the neighbourhood is shared by all members of a cell). It counts every allowed pair j > i
+// (broad_phase, collision.cpp:213-226 — StepReport.broad_pairs, the reference has no overlap
+// test) and keeps the pairs whose bounding spheres touch (prefilter; all allowed pairs without
+// it). Kept pairs collect in a per-warp shared buffer flushed with one atomic per fill. The
+// list is unordered; contacts are put in (i, j) order after the narrow phase.
+constexpr int kCellWarps = 8;
+constexpr int kCellPathMinPills = 1 << 16;
+constexpr int kCellBuf = 128;
+__global__ void __launch_bounds__(32 * kCellWarps) k_pairs_cell(Collide c, int prefilter, int* broad_total,
+                                                                int* cand_total) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ int s_start[kCellWarps][27];
+  __shared__ int s_off[kCellWarps][28];
+  __shared__ int s_mi[kCellWarps][32], s_mrod[kCellWarps][32], s_mgrp[kCellWarps][32], s_mel[kCellWarps][32];
+  __shared__ uint8_t s_mself[kCellWarps][32];
+  __shared__ double s_mb[kCellWarps][4][32];
+  __shared__ int s_buf[kCellWarps][2][kCellBuf];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = c.P;
+  const int ncells = c.rep_pos[P];
+  int broad = 0, nbuf = 0, scene_broad_done = 0;
+  for (int ci = blockIdx.x * kCellWarps + warp; ci < ncells; ci += gridDim.x * kCellWarps) {
+  const int h = c.cell_list[ci];
+  const int n_c = c.cell_count[h];
+  const int rep = c.table[h];
+  const int scene = c.pill_scene ? c.pill_scene[rep] : 0;
+  int size = 0;
+  if (lane < 27) {
+    const int hn = find_cell(c, c.cellkey[rep] + (lane / 9 - 1), c.cellkey[P + rep] + ((lane / 3) % 3 - 1),
+                             c.cellkey[2 * P + rep] + (lane % 3 - 1), scene);
+    if (hn >= 0) {
+      s_start[warp][lane] = c.cell_start[hn];
+      size = c.cell_start[hn + 1] - c.cell_start[hn];
+    }
+  }
+  int incl = size;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane < 27) s_off[warp][lane + 1] = incl;
+  if (lane == 0) s_off[warp][0] = 0;
+  const int total = __shfl_sync(0xffffffffu, incl, 26);
+  const int mbase = c.cell_start[h];
+  auto flush = [&]() {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(cand_total, nbuf);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int q = lane; q < nbuf; q += 32) {
+      const long long p = static_cast<long long>(base) + q;
+      if (p < c.cand_cap) {
+        c.cand_i[p] = s_buf[warp][0][q];
+        c.cand_j[p] = s_buf[warp][1][q];
+      }
+    }
+    __syncwarp();
+    nbuf = 0;
+  };
+  for (int ib = 0; ib < n_c; ib += 32) {
+    const int nm = min(32, n_c - ib);
+    __syncwarp();
+    if (lane < nm) {
+      const int i = c.cell_items[mbase + ib + lane];
+      s_mi[warp][lane] = i;
+      s_mrod[warp][lane] = c.pill_rod[i];
+      s_mgrp[warp][lane] = c.pill_group[i];
+      s_mel[warp][lane] = c.pill_el[i];
+      s_mself[warp][lane] = c.pill_self[i];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) s_mb[warp][f][lane] = c.bsph[f * P + i];
+    }
+    __syncwarp();
+    int cur_d = 0;  // a lane's k only grows, so its cell index only moves forward
+    for (int k0 = 0; k0 < total; k0 += 32) {
+      const int k = k0 + lane;
+      int j = -1, rj = 0, gj = 0, ej = 0;
+      double jx = 0, jy = 0, jz = 0, jr = 0;
+      if (k < total) {
+        while (s_off[warp][cur_d + 1] <= k) ++cur_d;
+        j = c.cell_items[s_start[warp][cur_d] + (k - s_off[warp][cur_d])];
+        rj = c.pill_rod[j];
+        gj = c.pill_group[j];
+        ej = c.pill_el[j];
+        jx = c.bsph[j];
+        jy = c.bsph[P + j];
+        jz = c.bsph[2 * P + j];
+        jr = c.bsph[3 * P + j];
+      }
+      for (int m = 0; m < nm; ++m) {
+        const int i = s_mi[warp][m];
+        bool cand = false;
+        if (j > i && pair_allowed(s_mrod[warp][m], s_mgrp[warp][m], s_mself[warp][m] != 0, s_mel[warp][m], rj, gj, ej)) {
+          ++broad;
+          if (prefilter) {  // spheres_touch, same arithmetic
+            const double dx = s_mb[warp][0][m] - jx, dy = s_mb[warp][1][m] - jy, dz = s_mb[warp][2][m] - jz;
+            const double rr = (s_mb[warp][3][m] + jr) * (1.0 + 1e-9) + 1e-12;
+            cand = dx * dx + dy * dy + dz * dz <= rr * rr;
+          } else {
+            cand = true;
+          }
+        }
+        const unsigned msk = __ballot_sync(0xffffffffu, cand);
+        if (msk) {
+          if (nbuf + __popc(msk) > kCellBuf) flush();
+          if (cand) {
+            const int q = nbuf + __popc(msk & ((1u << lane) - 1));
+            s_buf[warp][0][q] = i;
+            s_buf[warp][1][q] = j;
+          }
+          nbuf += __popc(msk);
+        }
+      }
+    }
+  }
+  __syncwarp();
+  if (nbuf) flush();
+  if (c.pill_scene) {  // batch: per-scene count (a cell belongs to one scene)
+    int b = broad;
+    for (int o = 16; o > 0; o >>= 1) b += __shfl_down_sync(0xffffffffu, b, o);
+    if (lane == 0 && b) atomicAdd(&c.scene_acc[scene].broad_pairs, b);
+    broad = 0;
+    scene_broad_done += b;
+  }
+  }  // cells of this warp
+  for (int o = 16; o > 0; o >>= 1) broad += __shfl_down_sync(0xffffffffu, broad, o);
+  if (lane == 0 && (broad || scene_broad_done)) atomicAdd(broad_total, broad + scene_broad_done);
 }
 
 // Exact conservative segment test (see may_penetrate) over the sphere-filtered candidates;
@@ -872,7 +1020,18 @@ void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
   scan_exclusive(c.cell_count, c.cell_start, c.T, nullptr, c.scan_tmp, c.scan_parts, st);
   if (P > 0) {
     launch_kernel(k_scatter, b, kThreads, 0, st, g_pdl, c);
-    launch_kernel(k_pairs_warp, (P + kPairWarps - 1) / kPairWarps, 32 * kPairWarps, 0, st, g_pdl, c, prefilter, c.scalars + SC_BROAD, c.scalars + SC_NCAND_RAW);
+    // VROD_BROAD_CELL_MIN overrides the switch-over size (tests run small worlds down both paths)
+    const char* env = std::getenv("VROD_BROAD_CELL_MIN");
+    const int cell_min = env ? std::atoi(env) : kCellPathMinPills;
+    if (P < cell_min) {  // small worlds: one warp per pill, a single launch
+      launch_kernel(k_pairs_warp, (P + kPairWarps - 1) / kPairWarps, 32 * kPairWarps, 0, st, g_pdl, c, prefilter,
+                    c.scalars + SC_BROAD, c.scalars + SC_NCAND_RAW);
+    } else {  // large worlds: one warp per non-empty cell, neighbourhood loads shared by its pills
+      scan_exclusive(c.rep_flag, c.rep_pos, P, nullptr, c.scan_tmp, c.scan_parts, st);
+      launch_kernel(k_cell_list, b, kThreads, 0, st, g_pdl, c);
+      launch_kernel(k_pairs_cell, std::min((P + kCellWarps - 1) / kCellWarps, 148 * 16), 32 * kCellWarps, 0, st,
+                    g_pdl, c, prefilter, c.scalars + SC_BROAD, c.scalars + SC_NCAND_RAW);
+    }
   }
   launch_kernel(k_clamp_raw, 1, 1, 0, st, g_pdl, c.scalars, SC_NCAND_RAW, SC_NCAND, c.cand_cap, 1);
   if (!do_narrow) return;

@@ -53,6 +53,9 @@ struct Collide {
   int* cell_cursor = nullptr;    // T
   int* cell_items = nullptr;     // P
   int* pill_cell = nullptr;      // P
+  int* rep_flag = nullptr;       // P+1: pill is its cell's representative
+  int* rep_pos = nullptr;        // P+1: exclusive scan of rep_flag ([P] = cell count)
+  int* cell_list = nullptr;      // P: non-empty table slots, representative order
   // candidates
   int* cand_count = nullptr;     // P+1
   int* cand_off = nullptr;       // P+1

@@ -152,6 +152,9 @@ Solver::Solver(const SceneData& scene, const BatchLayout* batch) : scene_(scene)
   c_.cell_cursor = dalloc<int>(c_.T);
   c_.cell_items = dalloc<int>(c_.P);
   c_.pill_cell = dalloc<int>(c_.P);
+  c_.rep_flag = dalloc<int>(c_.P + 1);
+  c_.rep_pos = dalloc<int>(c_.P + 1);
+  c_.cell_list = dalloc<int>(c_.P);
   c_.cand_i = dalloc<int>(c_.cand_cap);
   c_.cand_j = dalloc<int>(c_.cand_cap);
   c_.cand2_i = dalloc<int>(c_.cand_cap);

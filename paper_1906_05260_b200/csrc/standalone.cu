@@ -84,6 +84,9 @@ void make_collide(Buf& b, vdev::Collide& c, const vrod_pill* pills, int P, long 
   c.cell_cursor = b.get<int>(c.T);
   c.cell_items = b.get<int>(P);
   c.pill_cell = b.get<int>(P);
+  c.rep_flag = b.get<int>(P + 1);
+  c.rep_pos = b.get<int>(P + 1);
+  c.cell_list = b.get<int>(P);
   c.raw_i = b.get<int>(cap);
   c.raw_j = b.get<int>(cap);
   c.raw_ab = b.get<double>(2 * cap);

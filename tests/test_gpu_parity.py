@@ -112,6 +112,30 @@ def test_identical_input_contacts_bit_exact(gpu, oracle):
     assert len(cg["pill_a"]) > 100
 
 
+@pytest.mark.parametrize("name", ["pile", "crossing", "mini_forest", "kitchen_sink"])
+def test_cell_broad_phase_path(gpu, oracle, name, monkeypatch):
+    """Worlds of >= 65536 pills take the cell-per-warp broad phase; force it on small scenes
+    (VROD_BROAD_CELL_MIN=0) and require the same pairs, counts and contacts as the oracle."""
+    monkeypatch.setenv("VROD_BROAD_CELL_MIN", "0")
+    rng = np.random.default_rng(31)
+    for n in (0, 1, 2, 50, 2000):
+        pills = random_pills(rng, n, spread=3.0 if n > 100 else 0.5, rmax=0.25)
+        np.testing.assert_array_equal(broad_phase(gpu, pills), broad_phase(oracle, pills))
+    pills = random_pills(rng, 300, spread=0.05, rmax=0.3)  # > 32 pills in one cell
+    np.testing.assert_array_equal(broad_phase(gpu, pills), broad_phase(oracle, pills))
+    scene = SCENES[name](oracle)
+    g, o = SolverHandle(gpu, scene), SolverHandle(oracle, scene)
+    for _ in range(3):
+        rg, ro = g.step(), o.step()
+        assert (rg.contact_count, rg.broad_pairs) == (ro.contact_count, ro.broad_pairs)
+        cg, co = g.contacts(), o.contacts()
+        np.testing.assert_array_equal(cg["pill_a"], co["pill_a"])
+        np.testing.assert_array_equal(cg["pill_b"], co["pill_b"])
+        if name not in BUNDLE_SCENES:
+            for k in cg:
+                np.testing.assert_array_equal(cg[k], co[k], err_msg=k)
+
+
 def test_broad_phase_edge_cases(gpu, oracle):
     rng = np.random.default_rng(9)
     for n in (0, 1, 2, 3, 50):
