@@ -55,47 +55,27 @@ constexpr int kKindSZ = 1 << A_SZ, kKindCS = 1 << A_CS, kKindSS = 1 << A_SS, kKi
 constexpr int kKindVB = kKindVBU | kKindVBV;
 constexpr int kAllKinds = 0xff;
 
-// Which kinds read a staged row (rows nobody in the tile needs are not loaded).
-__device__ __forceinline__ int row_need(int r) {
-  switch (r) {
-    case T_SBAR: return kKindCS | kKindVS | kKindBT | kKindSB | kKindVB;
-    case T_ITX: case T_ITY: return kKindSZ | kKindVS | kKindBT | kKindVB;
-    case T_ITZ: return kKindBT | kKindVB;
-    case T_LEN: return kKindSZ | kKindSS | kKindBT | kKindSB | kKindVB;
-    case T_LEN0: return kKindVS | kKindVB;
-    case T_TDOT: return kKindSZ | kKindVS;
-    case T_SGRAD: return kKindSS;
-    case T_SLAP: return kKindSB;
-    case T_DARBX: case T_DARBY: return kKindBT | kKindVB;
-    case T_DARBZ: return kKindBT;
-    case T_KSZ: return kKindSZ;
-    case T_KCS: return kKindCS;
-    case T_KSS: return kKindSS;
-    case T_KVS: return kKindVS;
-    case T_KBT0: case T_KBT1: case T_KBT2: return kKindBT;
-    case T_KSB: return kKindSB;
-    case T_KVB: return kKindVB;
-    case T_LAM + L_SZ0: case T_LAM + L_SZ1: case T_LAM + L_SZ2: return kKindSZ;
-    case T_LAM + L_CS: return kKindCS;
-    case T_LAM + L_SS: return kKindSS;
-    case T_LAM + L_VS0: case T_LAM + L_VS1: case T_LAM + L_VS2: return kKindVS;
-    case T_LAM + L_BT0: case T_LAM + L_BT1: case T_LAM + L_BT2: return kKindBT;
-    case T_LAM + L_SB: return kKindSB;
-    case T_LAM + L_VBU: return kKindVBU;
-    case T_LAM + L_VBV: return kKindVBV;
-    default: return kAllKinds;  // X, IC, IS: centers/scales/frames are always applied
-  }
-}
-__constant__ int kStagedEField[T_LAM - T_LEN] = {LEN, LEN0, TDOT, SGRAD, SLAP, DARBX, DARBY, DARBZ, KSZ,
-                                                 KCS, KSS, KVS, KBT0, KBT1, KBT2, KSB, KVB};
-__device__ __forceinline__ const double* row_src(int r, const World& w, const double* X, const double* lam) {
-  const long long vp = w.vpad;
-  if (r < T_SBAR) return X + (CX + r) * vp;
-  if (r < T_ITX) return w.vstat + (SBAR + (r - T_SBAR)) * vp;
-  if (r < T_LEN) return w.estat + (ITX + (r - T_ITX)) * vp;
-  if (r >= T_LAM) return lam + (r - T_LAM) * vp;
-  return w.estat + kStagedEField[r - T_LEN] * vp;
-}
+// Per staged row: which kinds read it (rows nobody in the tile needs are not loaded), and where
+// it comes from (array: 0 X, 1 vertex statics, 2 element statics, 3 lambda_in; field index).
+constexpr int kNeedSBAR = kKindCS | kKindVS | kKindBT | kKindSB | kKindVB;
+constexpr int kNeedITXY = kKindSZ | kKindVS | kKindBT | kKindVB;
+constexpr int kNeedLEN = kKindSZ | kKindSS | kKindBT | kKindSB | kKindVB;
+__constant__ uint8_t kRowNeed[kStageRows] = {
+    kAllKinds, kAllKinds, kAllKinds, kAllKinds, kAllKinds, kAllKinds, kAllKinds, kAllKinds,  // X
+    kNeedSBAR, kAllKinds, kAllKinds,                                                      // SBAR IC IS
+    kNeedITXY, kNeedITXY, kKindBT | kKindVB,                                              // IT xyz
+    kNeedLEN, kKindVS | kKindVB, kKindSZ | kKindVS, kKindSS, kKindSB,                       // LEN LEN0 TDOT SGRAD SLAP
+    kKindBT | kKindVB, kKindBT | kKindVB, kKindBT,                                         // DARB xyz
+    kKindSZ, kKindCS, kKindSS, kKindVS, kKindBT, kKindBT, kKindBT, kKindSB, kKindVB,        // stiffnesses
+    kKindSZ, kKindSZ, kKindSZ, kKindCS, kKindSS, kKindVS, kKindVS, kKindVS,                 // lambda element pass
+    kKindBT, kKindBT, kKindBT, kKindSB, kKindVBU, kKindVBV};                                // lambda vertex pass
+__constant__ uint8_t kRowArr[kStageRows] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2,
+                                            2, 2, 2, 2, 2, 2, 2, 2, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3};
+__constant__ uint8_t kRowField[kStageRows] = {
+    CX, CY, CZ, S, QW, QX, QY, QZ, SBAR, IC, IS, ITX, ITY, ITZ, LEN, LEN0, TDOT, SGRAD, SLAP, DARBX, DARBY, DARBZ,
+    KSZ, KCS, KSS, KVS, KBT0, KBT1, KBT2, KSB, KVB,
+    L_SZ0, L_SZ1, L_SZ2, L_CS, L_SS, L_VS0, L_VS1, L_VS2, L_BT0, L_BT1, L_BT2, L_SB, L_VBU, L_VBV};
+static_assert(kStageRows == 45, "row tables");
 
 template <int TP>
 struct Tile {
@@ -104,6 +84,7 @@ struct Tile {
   PosRes res[kTilePos];
   int loc[kTilePos], m[kTilePos], kinds[kTilePos], bbase[kTilePos];
   unsigned wmask[kTilePos / 32];  // OR of the kinds present, per 32 positions
+  int klist[kKinds];              // the kinds present, ascending
   uint8_t act[kKinds][kTilePos];
 };
 
@@ -144,17 +125,22 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
   unsigned mask = 0;
 #pragma unroll
   for (int i = 0; i < kTilePos / 32; ++i) mask |= t.wmask[i];
+  if (tid < kKinds && (mask & (1u << tid))) t.klist[__popc(mask & ((1u << tid) - 1))] = tid;  // n-th kind present
   // Stage every row the tile's kinds read: 16-byte cp.async chunks (start-2 is even and rows
   // are 256-byte aligned), all in flight at once; slots outside [0, V) are zero-filled.
   constexpr int kChunks = kTileStage / 2;
-  for (int x = tid; x < kStageRows * kChunks; x += 32 * kWarps) {
-    const int r = x / kChunks, j = x - r * kChunks;
-    if (!(row_need(r) & mask)) continue;
-    const int v = start - 2 + 2 * j;
-    const int valid = v < 0 ? 0 : min(2, V - v);
-    const double* src = row_src(r, w, X, sp.lam_in) + (valid > 0 ? v : 0);
-    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&t.st[r][2 * j]));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(8 * max(valid, 0)));
+  for (int r = tid >> 5; r < kStageRows; r += kWarps) {  // one warp per row, lanes over its chunks
+    if (!(kRowNeed[r] & mask)) continue;
+    const int arr = kRowArr[r];
+    const double* row = (arr == 0 ? X : arr == 1 ? w.vstat : arr == 2 ? w.estat : sp.lam_in) +
+                        static_cast<long long>(kRowField[r]) * vp;
+    for (int j = lane; j < kChunks; j += 32) {
+      const int v = start - 2 + 2 * j;
+      const int valid = v < 0 ? 0 : min(2, V - v);
+      const double* src = row + (valid > 0 ? v : 0);
+      const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&t.st[r][2 * j]));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(8 * max(valid, 0)));
+    }
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
@@ -168,9 +154,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
   const int items = __popc(mask) * kTilePos;
   for (int item = tid; item < items; item += 32 * kWarps) {
     const int pi = item % kTilePos;
-    unsigned mm = mask;
-    for (int n = item / kTilePos; n > 0; --n) mm &= mm - 1;
-    const int kind = __ffs(mm) - 1;
+    const int kind = t.klist[item / kTilePos];
     const int k = t.loc[pi];
     if (k < 0) continue;
     const int p = start - 1 + pi;
@@ -527,14 +511,16 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
       }
     }
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    nsing += __shfl_down_sync(0xffffffffu, nsing, o);
-    const unsigned long long b2 = __shfl_down_sync(0xffffffffu, bad, o);
-    bad = umin64(bad, b2);
-  }
-  if (lane == 0) {
-    if (nsing) atomicAdd(singular, nsing);
-    if (bad != kNoError) atomicMin(err, bad);
+  if (__any_sync(0xffffffffu, nsing != 0 || bad != kNoError)) {  // rare: singular blocks / errors
+    for (int o = 16; o > 0; o >>= 1) {
+      nsing += __shfl_down_sync(0xffffffffu, nsing, o);
+      const unsigned long long b2 = __shfl_down_sync(0xffffffffu, bad, o);
+      bad = umin64(bad, b2);
+    }
+    if (lane == 0) {
+      if (nsing) atomicAdd(singular, nsing);
+      if (bad != kNoError) atomicMin(err, bad);
+    }
   }
   __syncthreads();
   if (sp.pdl == 2) {  // predecessor = the ext solve of this iteration: its entries are read below
