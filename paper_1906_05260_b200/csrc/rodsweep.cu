@@ -142,6 +142,20 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(8 * max(valid, 0)));
     }
   }
+  // The ext solve of this iteration (the predecessor) writes the tile's incidence entries:
+  // wait for it here, then prefetch the tile's whole entry range into L2 so the gather after
+  // the block solves finds it on chip.
+  if (sp.pdl == 2) {
+    pdl_wait();
+    pdl_trigger();
+  }
+  if (has_ext) {
+    const int e0 = c.ext_off[max(start, 0)], e1 = c.ext_off[min(start + kTileOwned, V)];
+    const char* lo = reinterpret_cast<const char*>(c.ext_contrib + 4ll * e0);
+    const char* hi = reinterpret_cast<const char*>(c.ext_contrib + 4ll * e1);
+    for (const char* a = lo + 128ll * tid; a < hi; a += 128ll * 32 * kWarps)
+      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a));
+  }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
 
@@ -523,10 +537,6 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
     }
   }
   __syncthreads();
-  if (sp.pdl == 2) {  // predecessor = the ext solve of this iteration: its entries are read below
-    pdl_wait();
-    pdl_trigger();
-  }
 
   // ---- gather in block order (constraints.cpp:509-534) and apply (:537-554)
   for (int pi = 1 + tid; pi <= kTileOwned; pi += 32 * kWarps) {
