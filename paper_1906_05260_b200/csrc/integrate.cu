@@ -167,6 +167,9 @@ __global__ void k_predict_vertices(World w, const double* __restrict__ anim, Ani
   Fr(w.X, CY, vp, v) = c.y;
   Fr(w.X, CZ, vp, v) = c.z;
   Fr(w.X, S, vp, v) = s;
+  double2* xr = reinterpret_cast<double2*>(w.xrec + 8ll * v);
+  xr[0] = make_double2(c.x, c.y);
+  xr[1] = make_double2(c.z, s);
 }
 
 // predict_rod element loop (solver.cpp:60-72) + refresh_orientation_inertia (layout.cpp:76-93)

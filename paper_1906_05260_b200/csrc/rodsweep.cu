@@ -646,6 +646,11 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
     Y[CY * (long long)vp + p] = cn.y;
     Y[CZ * (long long)vp + p] = cn.z;
     Y[S * (long long)vp + p] = sn;
+    if (has_ext) {
+      double2* xr = reinterpret_cast<double2*>(w.xrec + 8ll * p);
+      xr[0] = make_double2(cn.x, cn.y);
+      xr[1] = make_double2(cn.z, sn);
+    }
     Y[QW * (long long)vp + p] = qn.w;
     Y[QX * (long long)vp + p] = qn.x;
     Y[QY * (long long)vp + p] = qn.y;

@@ -165,7 +165,11 @@ __global__ void k_shape_level(World w, Groups g, double* __restrict__ X, int gbe
       X[CX * (long long)vp + v] = x.x;
       X[CY * (long long)vp + v] = x.y;
       X[CZ * (long long)vp + v] = x.z;
-      X[S * (long long)vp + v] = fmax(scale * mr[3], kMinScale);
+      const double sn = fmax(scale * mr[3], kMinScale);
+      X[S * (long long)vp + v] = sn;
+      double2* xr = reinterpret_cast<double2*>(w.xrec + 8ll * v);
+      xr[0] = make_double2(x.x, x.y);
+      xr[1] = make_double2(x.z, sn);
     }
     const Q4 fr = qnormalized(qmul(qf, Q4{mr[13], mr[14], mr[15], mr[16]}));
     const int e = g.meslot[i];

@@ -97,6 +97,7 @@ Solver::Solver(const SceneData& scene, const BatchLayout* batch) : scene_(scene)
   w_.vel = dalloc<double>(static_cast<std::size_t>(vdev::kVelFields) * vpad);
   w_.lam = dalloc<double>(2ull * vdev::kLamFields * vpad);  // ping-pong pair
   w_.loads = dalloc<double>(7ull * vpad);
+  w_.xrec = dalloc<double>(8ull * vpad);
   int nbones_total = 0;
   for (const auto& rod : scene_.rods) nbones_total += static_cast<int>(rod.bones.size());
   w_.has_bones = nbones_total > 0;
@@ -491,6 +492,20 @@ void Solver::upload_static() {
   upload(w_.X, X, stream_);
   upload(w_.vel, vel, stream_);
   upload(w_.slot_bw_off, bw_off, stream_);
+  {  // slot records for the external blocks: current c, s + static rbar, 1/w_c, 1/w_s
+    std::vector<double> rec(8ull * vpad, 0.0);
+    for (int p = 0; p < setup_.V; ++p) {
+      double* o = rec.data() + 8ll * p;
+      o[0] = XS(vdev::CX, p);
+      o[1] = XS(vdev::CY, p);
+      o[2] = XS(vdev::CZ, p);
+      o[3] = XS(vdev::S, p);
+      o[4] = VS(vdev::RBAR, p);
+      o[5] = VS(vdev::IC, p);
+      o[6] = VS(vdev::IS, p);
+    }
+    upload(w_.xrec, rec, stream_);
+  }
   upload(w_.bone_w, bw, stream_);
 
   // static pill attributes: rod pills in (rod, element) order, then kinematic pills

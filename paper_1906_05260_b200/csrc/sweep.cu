@@ -39,6 +39,37 @@ struct ExtGeom {  // resolve_pill, constraints.cpp:76-97
   double r0, r1, rb0, rb1;
   int v0;
 };
+// resolve from the slot records (World::xrec): two 64-byte records per rod pill
+__device__ __forceinline__ ExtGeom resolve_rec(const World& w, const Collide& c, int pill, int v, double (&ic)[2],
+                                               double (&is)[2]) {
+  ExtGeom g;
+  if (v >= 0) {
+    const double4* r0 = reinterpret_cast<const double4*>(w.xrec + 8ll * v);
+    const double4 a = r0[0], b = r0[1], d = r0[2], e = r0[3];
+    g.c0 = V3{a.x, a.y, a.z};
+    g.c1 = V3{d.x, d.y, d.z};
+    g.rb0 = b.x;
+    g.rb1 = e.x;
+    g.r0 = a.w * g.rb0;
+    g.r1 = d.w * g.rb1;
+    g.v0 = v;
+    ic[0] = b.y;
+    ic[1] = e.y;
+    is[0] = b.z;
+    is[1] = e.z;
+  } else {
+    const int P = c.P;
+    g.c0 = V3{c.pill[pill], c.pill[P + pill], c.pill[2 * P + pill]};
+    g.c1 = V3{c.pill[3 * P + pill], c.pill[4 * P + pill], c.pill[5 * P + pill]};
+    g.r0 = c.pill[6 * P + pill];
+    g.r1 = c.pill[7 * P + pill];
+    g.rb0 = g.rb1 = 0.0;
+    g.v0 = -1;
+    ic[0] = ic[1] = is[0] = is[1] = 0.0;
+  }
+  return g;
+}
+
 // resolve with the pill's first slot known (v = pill + rod, or -1 for a kinematic pill)
 __device__ __forceinline__ ExtGeom resolve_at(const World& w, const Collide& c, const double* X, int pill, int v) {
   ExtGeom g;
@@ -168,9 +199,10 @@ __global__ void __launch_bounds__(256, 3) k_ext_solve(World w, Collide c, const 
       }
     } else if (b < npins + nct) {  // kContact (constraints.cpp:215-247), unilateral, dim 1
       const int k = b - npins;
-      // endpoint slots were stored by k_ext_count: X is one dependent load away
-      const ExtGeom A = resolve_at(w, c, X, c.ct_a[k], c.ct_va[k]);
-      const ExtGeom B = resolve_at(w, c, X, c.ct_b[k], c.ct_vb[k]);
+      // endpoint slots were stored by k_ext_count: the slot records are one dependent load away
+      double icA[2], isA[2], icB[2], isB[2];
+      const ExtGeom A = resolve_rec(w, c, c.ct_a[k], c.ct_va[k], icA, isA);
+      const ExtGeom B = resolve_rec(w, c, c.ct_b[k], c.ct_vb[k], icB, isB);
       const double al = c.ct_alpha[k], be = c.ct_beta[k];
       const V3 ca = (1.0 - al) * A.c0 + al * A.c1;
       const V3 cb = (1.0 - be) * B.c0 + be * B.c1;
@@ -186,16 +218,11 @@ __global__ void __launch_bounds__(256, 3) k_ext_solve(World w, Collide c, const 
       }
       const bool entry[4] = {A.v0 >= 0, A.v0 >= 0, B.v0 >= 0, B.v0 >= 0};
       const int slot[4] = {A.v0, A.v0 + 1, B.v0, B.v0 + 1};
-      // every per-endpoint load issued up front (one latency, not a chain behind the branch)
-      double icv[4] = {0, 0, 0, 0}, isv[4] = {0, 0, 0, 0};
+      const double icv[4] = {icA[0], icA[1], icB[0], icB[1]}, isv[4] = {isA[0], isA[1], isB[0], isB[1]};
       int qpos[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (entry[e]) {
-          icv[e] = F(w.vstat, IC, vp, slot[e]);
-          isv[e] = F(w.vstat, IS, vp, slot[e]);
-          qpos[e] = c.ext_pos[4 * b + e];
-        }
+        if (entry[e]) qpos[e] = c.ext_pos[4 * b + e];
       bool wrote[4] = {false, false, false, false};
       if (!(W >= 0.0 && lam[0] == 0.0)) {
         const double coef[4] = {1.0 - al, al, -(1.0 - be), -be};

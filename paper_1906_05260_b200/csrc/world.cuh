@@ -123,6 +123,10 @@ struct World {
   double* vel = nullptr;         // kVelFields x vpad
   double* lam = nullptr;         // kLamFields x vpad
   double* loads = nullptr;       // 3 force + 3 torque + 1 scale load per slot (7 x vpad)
+  // AoS mirror of what the external blocks read per slot, 64 B records: c xyz, s (current
+  // iterate; written by predict, the rod sweep and shape matching), rbar, 1/w_c, 1/w_s (static).
+  // One record = two 32-byte sectors, instead of seven scattered SoA sectors per endpoint.
+  double* xrec = nullptr;
 };
 
 }  // namespace vdev
