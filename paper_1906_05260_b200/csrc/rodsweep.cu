@@ -24,7 +24,10 @@ namespace {
 
 // Tile of TP computed positions start-1 .. start+TP-2 (TP-2 owned), staged slots start-2 ..
 // start+TP-1. TP = 64 for large worlds; 32 when 64-wide tiles would leave SMs idle.
-constexpr int kWarps = 4;
+// Warps per CTA: 4 for 64-wide tiles; 8 for 32-wide tiles (small worlds are latency-bound:
+// one item round per thread instead of two).
+template <int TP>
+constexpr int warps_for() { return TP == 64 ? 4 : 8; }
 
 __device__ __forceinline__ unsigned long long umin64(unsigned long long a, unsigned long long b) { return a < b ? a : b; }
 
@@ -89,9 +92,10 @@ struct Tile {
 };
 
 template <int TP>
-__global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c, const double* __restrict__ X,
+__global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_sweep(World w, Collide c, const double* __restrict__ X,
                                                           double* __restrict__ Y, SweepParams sp, int* singular,
                                                           unsigned long long* err, int has_ext) {
+  constexpr int kWarps = warps_for<TP>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int kTilePos = TP, kTileOwned = TP - 2, kTileStage = TP + 2;
   Tile<TP>& t = *reinterpret_cast<Tile<TP>*>(smem_raw);
@@ -142,14 +146,17 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(8 * max(valid, 0)));
     }
   }
-  // The ext solve of this iteration (the predecessor) writes the tile's incidence entries:
-  // wait for it here, then prefetch the tile's whole entry range into L2 so the gather after
-  // the block solves finds it on chip.
-  if (sp.pdl == 2) {
+  // The ext solve of this iteration (the predecessor) writes the tile's incidence entries.
+  // Large worlds (64-wide tiles, bandwidth-bound): wait for it here and prefetch the tile's
+  // entry range into L2 so the gather after the block solves finds it on chip. Small worlds
+  // (latency-bound): solve the tile's blocks first, overlapping the ext solve's tail, and wait
+  // just before the gather.
+  constexpr bool kEarlyWait = TP == 64;
+  if (kEarlyWait && sp.pdl == 2) {
     pdl_wait();
     pdl_trigger();
   }
-  if (has_ext) {
+  if (kEarlyWait && has_ext) {
     const int e0 = c.ext_off[max(start, 0)], e1 = c.ext_off[min(start + kTileOwned, V)];
     const char* lo = reinterpret_cast<const char*>(c.ext_contrib + 4ll * e0);
     const char* hi = reinterpret_cast<const char*>(c.ext_contrib + 4ll * e1);
@@ -538,6 +545,11 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_rod_sweep(World w, Collide c
   }
   __syncthreads();
 
+  if (!kEarlyWait && sp.pdl == 2) {
+    pdl_wait();
+    pdl_trigger();
+  }
+
   // ---- gather in block order (constraints.cpp:509-534) and apply (:537-554)
   for (int pi = 1 + tid; pi <= kTileOwned; pi += 32 * kWarps) {
     const int k = t.loc[pi];
@@ -667,7 +679,7 @@ void launch_tiles(const World& w, Collide& c, const double* X, double* Y, const 
   (void)attr;  // a failure surfaces as a launch error
   const int has_ext = c.ext_cap > 0 ? 1 : 0;
   const int blocks = (w.V + TP - 3) / (TP - 2);
-  launch_kernel(k_rod_sweep<TP>, blocks, 32 * kWarps, sizeof(Tile<TP>), st, sp.pdl != 0, w, c, X, Y, sp, singular_counter,
+  launch_kernel(k_rod_sweep<TP>, blocks, 32 * warps_for<TP>(), sizeof(Tile<TP>), st, sp.pdl != 0, w, c, X, Y, sp, singular_counter,
                 err, has_ext);
 }
 
