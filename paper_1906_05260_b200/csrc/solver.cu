@@ -340,6 +340,7 @@ Solver::~Solver() {
   if (h_anim_) cudaFreeHost(h_anim_);
   if (h_acc_) cudaFreeHost(h_acc_);
   if (h_scene_acc_) cudaFreeHost(h_scene_acc_);
+  if (h_state_) cudaFreeHost(h_state_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -927,9 +928,14 @@ std::vector<double> Solver::probe_convergence(int iterations) {
 
 void Solver::get_state(double* c, double* s, double* q, double* cv, double* sv, double* av) {
   const int vpad = setup_.vpad, V = setup_.V;
-  std::vector<double> X(static_cast<std::size_t>(vdev::kStateFields) * vpad), vel(static_cast<std::size_t>(vdev::kVelFields) * vpad);
-  check_cuda(cudaMemcpyAsync(X.data(), w_.X, sizeof(double) * X.size(), cudaMemcpyDeviceToHost, stream_), "get_state");
-  check_cuda(cudaMemcpyAsync(vel.data(), w_.vel, sizeof(double) * vel.size(), cudaMemcpyDeviceToHost, stream_), "get_state");
+  const std::size_t nx = static_cast<std::size_t>(vdev::kStateFields) * vpad;
+  const std::size_t nv = static_cast<std::size_t>(vdev::kVelFields) * vpad;
+  if (!h_state_) check_cuda(cudaMallocHost(&h_state_, sizeof(double) * (nx + nv)), "cudaMallocHost");  // pinned mirror
+  const double* X = h_state_;
+  const double* vel = h_state_ + nx;
+  check_cuda(cudaMemcpyAsync(h_state_, w_.X, sizeof(double) * nx, cudaMemcpyDeviceToHost, stream_), "get_state");
+  if (cv || sv || av)
+    check_cuda(cudaMemcpyAsync(h_state_ + nx, w_.vel, sizeof(double) * nv, cudaMemcpyDeviceToHost, stream_), "get_state");
   check_cuda(cudaStreamSynchronize(stream_), "get_state");
   int e = 0;
   for (int r = 0; r < setup_.R; ++r) {

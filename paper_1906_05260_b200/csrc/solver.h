@@ -143,6 +143,7 @@ class Solver {
   int* d_scene_sing_ = nullptr;
   vdev::SceneAcc* h_scene_acc_ = nullptr;  // pinned, n_scenes_ (batch only)
   Report last_report_;
+  double* h_state_ = nullptr;  // pinned mirror of X and the velocities for get_state
 };
 
 void check_cuda(cudaError_t e, const char* what);
