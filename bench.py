@@ -118,7 +118,7 @@ def bind_bench(lib):
     return lib
 
 
-CATS = ["predict", "collide", "ext_setup", "ext_solve", "rod_sweep", "shape", "report"]
+CATS = ["predict", "collide", "ext_setup", "ext_solve", "rod_sweep", "shape", "report", "iterate"]
 
 
 def device_run(lib, solver, steps, flush):
@@ -131,10 +131,10 @@ def device_run(lib, solver, steps, flush):
 
 def kernel_times(lib, solver, steps):
     from paper_1906_05260_b200.scene import check
-    ms = (C.c_double * 7)()
-    ln = (C.c_int64 * 7)()
+    ms = (C.c_double * len(CATS))()
+    ln = (C.c_int64 * len(CATS))()
     check(lib, lib.vrod_bench_kernel_times(solver._h, steps, ms, ln))
-    return {CATS[i]: (ms[i], ln[i]) for i in range(7)}
+    return {CATS[i]: (ms[i], ln[i]) for i in range(len(CATS))}
 
 
 def cpu_sample(lib_path, build_scene, target_s, threads, max_steps=200):
@@ -287,19 +287,23 @@ def main():
             dist[1].destroy_process_group()
         return
 
-    # ---- per-kernel attribution and roofline (dominant kernel: the fused rod sweep) ----
+    # ---- per-kernel attribution and roofline. Dominant kernel: the persistent iteration kernel
+    # k_iterate (all I sweeps + external blocks + shape matching of a substep in one launch) when
+    # the world fits on chip (C3), else the per-sweep fused rod sweep k_rod_sweep ----
     kt = kernel_times(lib, solver, 5)
     peak, peak_kind = load_peaks()
-    sweep_ms, sweep_n = kt["rod_sweep"]
+    persistent = kt["iterate"][1] > 0
+    sweep_ms, sweep_n = kt["iterate"] if persistent else kt["rod_sweep"]
     sweep_avg_s = sweep_ms / max(sweep_n, 1) / 1e3
-    sweep_bytes = 64 * (V + E)  # read+write c,s (vertex) / q (element) per iteration
+    # read+write c,s (vertex) / q (element) per sweep; the persistent kernel runs I
+    sweep_bytes = 64 * (V + E) * (I if persistent else 1)
     achieved = sweep_bytes / sweep_avg_s / 1e9
     total_dev_ms = sum(v[0] for v in kt.values())
     nc = rep.contact_count
     b_sub = workloads.algorithmic_bytes(V, E, I, True, E, nc)
     t_sub = ms_total / 1e3 / args.steps / S
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "k_rod_sweep", "bytes_per_launch": sweep_bytes,
+                "traffic": None, "kernel": "k_iterate" if persistent else "k_rod_sweep", "bytes_per_launch": sweep_bytes,
                 "avg_launch_us": sweep_avg_s * 1e6, "share_of_step": sweep_ms / total_dev_ms,
                 "peak_source": peak_kind,
                 "substep": {"algorithmic_bytes": b_sub, "seconds": t_sub, "achieved_gbs": b_sub / t_sub / 1e9,

@@ -22,7 +22,8 @@ enum vrod_kernel_category {
   VROD_CAT_ROD_SWEEP = 4, /* fused elastic stencil + gather + apply, per sweep */
   VROD_CAT_SHAPE = 5,     /* shape matching levels */
   VROD_CAT_REPORT = 6,    /* finalize + residual norms + penetration */
-  VROD_CAT_COUNT = 7
+  VROD_CAT_ITERATE = 7,   /* persistent kernel: the whole iteration loop (ext + rod sweeps + shape) */
+  VROD_CAT_COUNT = 8
 };
 
 /* Replays `steps` steps of the captured graph, each bracketed by CUDA events on the solver's
@@ -33,6 +34,9 @@ int vrod_bench_run(vrod_solver* solver, int32_t steps, int64_t flush_bytes, doub
 /* Runs `steps` steps with direct launches and event pairs around each kernel category;
  * ms[VROD_CAT_COUNT] = summed device ms, launches[VROD_CAT_COUNT] = bracket counts. */
 int vrod_bench_kernel_times(vrod_solver* solver, int32_t steps, double* ms, int64_t* launches);
+/* Debug: phase timestamps (globaltimer ns) of CTA 0 in the last persistent iteration kernel,
+ * when the solver was created with VROD_TRACE=1 (else count = 0). */
+int vrod_bench_trace(vrod_solver* solver, int32_t capacity, int64_t* out, int32_t* count);
 /* Contacts and candidates of the last step (capacity diagnostics). */
 int vrod_bench_last_counts(vrod_solver* solver, int64_t* max_candidates, int64_t* max_contacts);
 

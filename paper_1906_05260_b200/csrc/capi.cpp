@@ -395,6 +395,13 @@ int vrod_bench_kernel_times(vrod_solver* h, int32_t steps, double* ms, int64_t* 
     for (int c = 0; c < Solver::kCategories; ++c) launches[c] = l[c];
   });
 }
+int vrod_bench_trace(vrod_solver* h, int32_t cap, int64_t* out, int32_t* count) {
+  return guarded([&] {
+    std::vector<long long> t(cap > 0 ? cap : -cap);
+    *count = h->s->trace(t.data(), cap);
+    for (int i = 0; i < *count; ++i) out[i] = t[i];
+  });
+}
 int vrod_bench_last_counts(vrod_solver* h, int64_t* cand, int64_t* ct) {
   return guarded([&] {
     if (cand) *cand = h->s->last_max_candidates();

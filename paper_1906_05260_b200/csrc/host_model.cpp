@@ -291,7 +291,10 @@ Setup build_setup(const SceneData& s) {
   // Shape-matching groups (make_bundle_group, bundling.cpp:17-48) + level schedule.
   // frame slot -> highest level that wrote it so far; per-slot stamps find a group's distinct
   // frames (flat arrays: batches merge ~10^6 groups)
-  std::vector<int> last_level(out.V, -1), stamp(out.V, -1);
+  std::vector<int> last_level(out.V, -1), stamp(out.V, -1), last_writer(out.V, -1);
+  // chain schedule: a group's predecessor is the last earlier group that wrote one of its frames
+  std::vector<int> pred, nsucc;
+  bool chains_ok = true;
   for (const auto& members : s.bundles) {
     const int gid = static_cast<int>(out.groups.size());
     Setup::Group g;
@@ -333,9 +336,35 @@ Setup build_setup(const SceneData& s) {
     for (int f : frames)
       if (last_level[f] >= 0) level = std::max(level, last_level[f] + 1);
     for (int f : frames) last_level[f] = std::max(last_level[f], level);
+    int p = -1;
+    for (int f : frames) {
+      const int lw = last_writer[f];
+      if (lw < 0) continue;
+      if (p >= 0 && lw != p) chains_ok = false;  // two predecessors: not a chain
+      p = lw;
+    }
+    for (int f : frames) last_writer[f] = gid;
+    pred.push_back(p);
+    nsucc.push_back(0);
+    if (p >= 0 && ++nsucc[p] > 1) chains_ok = false;  // a fork: not a chain
     out.group_level.push_back(level);
     out.levels = std::max(out.levels, level + 1);
     out.groups.push_back(std::move(g));
+  }
+
+  // Chains: each group has <= 1 predecessor and <= 1 successor, so the dependency graph is a set
+  // of chains; one warp runs a chain's groups in order and chains run concurrently.
+  if (chains_ok && !out.groups.empty()) {
+    const int G = static_cast<int>(out.groups.size());
+    std::vector<int> next(G, -1);
+    for (int gi = 0; gi < G; ++gi)
+      if (pred[gi] >= 0) next[pred[gi]] = gi;
+    out.chain_off.push_back(0);
+    for (int gi = 0; gi < G; ++gi) {
+      if (pred[gi] >= 0) continue;  // not a chain head
+      for (int k = gi; k >= 0; k = next[k]) out.chain_groups.push_back(k);
+      out.chain_off.push_back(static_cast<int>(out.chain_groups.size()));
+    }
   }
 
   // Pin motions: sequential writes in the reference, so the last motion per vertex wins.

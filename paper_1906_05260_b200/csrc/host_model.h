@@ -160,6 +160,9 @@ struct Setup {
   std::vector<Group> groups;
   std::vector<int> group_level;
   int levels = 0;
+  // Chain schedule of the groups (empty when the frame dependencies are not chains):
+  // chain c = chain_groups[chain_off[c] .. chain_off[c+1]), in the reference's group order.
+  std::vector<int> chain_off, chain_groups;
   // pin motions after dedupe (last one per vertex wins, like the reference's sequential writes)
   std::vector<int> pin_motion_ids;
 };

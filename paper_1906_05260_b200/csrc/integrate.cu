@@ -70,10 +70,10 @@ __global__ void k_activation(World w, const double* __restrict__ anim, AnimLayou
     const int s = v0 + e;
     const double len = F(w.estat, LEN, vp, s);
     Fr(w.estat, SGRAD, vp, s) = (F(w.vstat, SBAR, vp, s + 1) - F(w.vstat, SBAR, vp, s)) / len;
-    // element-pass stiffness (StretchZ, CrossSection, SurfaceStretch)
-    Fr(w.estat, KSZ, vp, s) = F(w.estat, A2E, vp, s) * mat[2] * len;
-    Fr(w.estat, KCS, vp, s) = F(w.estat, A2E, vp, s) * kxy * len;
-    Fr(w.estat, KSS, vp, s) = F(w.estat, A4EP, vp, s) * kxy * len;
+    // element-pass stiffness (StretchZ, CrossSection, SurfaceStretch), stored inverted (K rows)
+    Fr(w.estat, KSZ, vp, s) = inverse_stiffness(F(w.estat, A2E, vp, s) * mat[2] * len);
+    Fr(w.estat, KCS, vp, s) = inverse_stiffness(F(w.estat, A2E, vp, s) * kxy * len);
+    Fr(w.estat, KSS, vp, s) = inverse_stiffness(F(w.estat, A4EP, vp, s) * kxy * len);
     if (e >= 1) {  // interior vertex j = e: Darboux, laplacian, BendTwist / SurfaceBending stiffness
       const int j = s;
       const double la = F(w.estat, LEN, vp, j - 1);
@@ -89,10 +89,10 @@ __global__ void k_activation(World w, const double* __restrict__ anim, AnimLayou
       Fr(w.estat, SLAP, vp, j - 1) = (sp - s0) / lb - (s0 - sm) / la;
       const double a4 = F(w.estat, A4VP, vp, j);
       const double lw = 0.5 * (la + lb);
-      Fr(w.estat, KBT0, vp, j) = a4 * mat[2] * lw;
-      Fr(w.estat, KBT1, vp, j) = a4 * mat[2] * lw;
-      Fr(w.estat, KBT2, vp, j) = a4 * kxy * lw;
-      Fr(w.estat, KSB, vp, j) = a4 * (mat[3] + mat[4]) * lw;
+      Fr(w.estat, KBT0, vp, j) = inverse_stiffness(a4 * mat[2] * lw);
+      Fr(w.estat, KBT1, vp, j) = inverse_stiffness(a4 * mat[2] * lw);
+      Fr(w.estat, KBT2, vp, j) = inverse_stiffness(a4 * kxy * lw);
+      Fr(w.estat, KSB, vp, j) = inverse_stiffness(a4 * (mat[3] + mat[4]) * lw);
     }
   }
 }

@@ -146,6 +146,10 @@ struct Groups {  // shape matching (bundling.cpp)
   uint8_t* serial = nullptr;
   int* level_off = nullptr;      // host-side only (levels+1)
   int* level_groups = nullptr;   // device: group ids ordered by level
+  // chain schedule (host_model.cpp), 0 chains when the frame dependencies are not chains
+  int nchains = 0;
+  int* chain_off = nullptr;      // nchains+1
+  int* chain_groups = nullptr;
 };
 
 // Animation packet per substep (host-evaluated, uploaded once per step).
@@ -170,7 +174,26 @@ struct SweepParams {
   int* scene_singular;    // batch, last iteration only: per-scene singular-block counter
   const double* lam_in;  // elastic multipliers before this sweep (kLamFields x vpad)
   double* lam_out;       // after this sweep (ping-pong partner)
+  unsigned long long* dbg = nullptr;  // debug trace (persistent kernel, VROD_TRACE=1)
 };
+
+// The persistent small-world iteration kernel (rodsweep.cu k_iterate): the whole iteration
+// loop of one substep in one launch.
+constexpr int kMaxPersistLevels = 8;
+struct PersistParams {
+  double* X;               // state at the start of the loop (w.X) and its ping-pong partner
+  double* Y;
+  double* xrec[2];         // slot records: [0] = w.xrec (written by predict), [1] its partner
+  double* lam_ext[2];      // external-block multipliers: [0] = c.ext_lam (zeroed by ext setup)
+  unsigned* bar;           // grid-barrier counter (zeroed before each launch)
+  int iterations;
+  int sm_period;
+  int levels;              // shape-matching levels (<= kMaxPersistLevels)
+  int has_ext;
+  int level_off[kMaxPersistLevels + 1];
+  unsigned long long* trace;  // optional phase timestamps of CTA 0 (globaltimer ns), see k_iterate
+};
+constexpr int kTraceCap = 1024;
 
 // Programmatic dependent launch (sm_90+): the next kernel in the stream may start while this
 // one finishes; griddepcontrol.wait blocks until the predecessor grid has completed and its
@@ -241,6 +264,12 @@ void launch_penetration(const World& w, Collide& c, const double* X, StepAccum* 
 // batch: per-scene residual norms (one CTA per scene) and end-of-substep singular fold-in
 void launch_scene_report(const World& w, const double* X, int classic, int* scene_singular, cudaStream_t st);
 int report_parts(int V);
+
+// rodsweep.cu: persistent iteration loop for small single-scene worlds. persistent_tiles()
+// returns the number of co-resident tiles the world needs, or 0 when it does not fit.
+int persistent_tiles(const World& w);
+void launch_iterate_persistent(const World& w, Collide& c, const Groups& g, const PersistParams& pp, const SweepParams& sp,
+                               int* singular_counters, unsigned long long* err, cudaStream_t st);
 
 // shape.cu
 void launch_shape_match(const World& w, const Groups& g, double* X, const int* level_off_host, bool pdl, cudaStream_t st);

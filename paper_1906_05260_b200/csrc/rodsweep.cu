@@ -13,7 +13,9 @@
 // --fmad=false the result is the reference's arithmetic bit for bit; there are no atomics on
 // the data path (bitwise run-to-run determinism) and no colouring (Jacobi
 // snapshot semantics, test_sweep.cpp:132-142).
+#include "ext.cuh"
 #include "kernels.cuh"
+#include "shape.cuh"
 #include "vmath.cuh"
 
 namespace vdev {
@@ -69,7 +71,7 @@ __constant__ uint8_t kRowNeed[kStageRows] = {
     kNeedITXY, kNeedITXY, kKindBT | kKindVB,                                              // IT xyz
     kNeedLEN, kKindVS | kKindVB, kKindSZ | kKindVS, kKindSS, kKindSB,                       // LEN LEN0 TDOT SGRAD SLAP
     kKindBT | kKindVB, kKindBT | kKindVB, kKindBT,                                         // DARB xyz
-    kKindSZ, kKindCS, kKindSS, kKindVS, kKindBT, kKindBT, kKindBT, kKindSB, kKindVB,        // stiffnesses
+    kKindSZ, kKindCS, kKindSS, kKindVS, kKindBT, 0, kKindBT, kKindSB, kKindVB,  // inverse stiffnesses (KBT1 == KBT0)
     kKindSZ, kKindSZ, kKindSZ, kKindCS, kKindSS, kKindVS, kKindVS, kKindVS,                 // lambda element pass
     kKindBT, kKindBT, kKindBT, kKindSB, kKindVBU, kKindVBV};                                // lambda vertex pass
 __constant__ uint8_t kRowArr[kStageRows] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2,
@@ -89,22 +91,17 @@ struct Tile {
   unsigned wmask[kTilePos / 32];  // OR of the kinds present, per 32 positions
   int klist[kKinds];              // the kinds present, ascending
   uint8_t act[kKinds][kTilePos];
+  int eoff[kTilePos];             // persistent kernel: incidence offsets of slots start .. start+TP-2
 };
 
+// Phase 0: per-position metadata of the tile (rod-local index, element count, kinds, block base),
+// the OR of the kinds present and their ascending list. Ends with __syncthreads(); returns the
+// kind mask.
 template <int TP>
-__global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_sweep(World w, Collide c, const double* __restrict__ X,
-                                                          double* __restrict__ Y, SweepParams sp, int* singular,
-                                                          unsigned long long* err, int has_ext) {
+__device__ __forceinline__ unsigned tile_meta(Tile<TP>& t, const World& w, int start) {
   constexpr int kWarps = warps_for<TP>();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int kTilePos = TP, kTileOwned = TP - 2, kTileStage = TP + 2;
-  Tile<TP>& t = *reinterpret_cast<Tile<TP>*>(smem_raw);
-  if (sp.pdl == 1) {  // predecessor wrote X: wait before staging
-    pdl_wait();
-    pdl_trigger();
-  }
-  const int V = w.V, vp = w.vpad;
-  const int start = blockIdx.x * kTileOwned;
+  constexpr int kTilePos = TP;
+  const int V = w.V;
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kTilePos; i += 32 * kWarps) {
     const int p = start - 1 + i;
@@ -130,13 +127,23 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
 #pragma unroll
   for (int i = 0; i < kTilePos / 32; ++i) mask |= t.wmask[i];
   if (tid < kKinds && (mask & (1u << tid))) t.klist[__popc(mask & ((1u << tid) - 1))] = tid;  // n-th kind present
-  // Stage every row the tile's kinds read: 16-byte cp.async chunks (start-2 is even and rows
-  // are 256-byte aligned), all in flight at once; slots outside [0, V) are zero-filled.
-  constexpr int kChunks = kTileStage / 2;
-  for (int r = tid >> 5; r < kStageRows; r += kWarps) {  // one warp per row, lanes over its chunks
+  return mask;
+}
+
+// Phase 1: stage rows [r0, r1) that the tile's kinds read: 16-byte cp.async chunks (start-2 is
+// even and rows are 256-byte aligned), all in flight at once; slots outside [0, V) are
+// zero-filled. The caller waits (cp.async.wait_all + __syncthreads).
+template <int TP>
+__device__ __forceinline__ void stage_rows(Tile<TP>& t, const World& w, const double* X, const double* lam_in, int start,
+                                           unsigned mask, int r0, int r1) {
+  constexpr int kWarps = warps_for<TP>();
+  constexpr int kChunks = (TP + 2) / 2;
+  const int V = w.V, vp = w.vpad;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int r = r0 + (tid >> 5); r < r1; r += kWarps) {  // one warp per row, lanes over its chunks
     if (!(kRowNeed[r] & mask)) continue;
     const int arr = kRowArr[r];
-    const double* row = (arr == 0 ? X : arr == 1 ? w.vstat : arr == 2 ? w.estat : sp.lam_in) +
+    const double* row = (arr == 0 ? X : arr == 1 ? w.vstat : arr == 2 ? w.estat : lam_in) +
                         static_cast<long long>(kRowField[r]) * vp;
     for (int j = lane; j < kChunks; j += 32) {
       const int v = start - 2 + 2 * j;
@@ -146,26 +153,22 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(8 * max(valid, 0)));
     }
   }
-  // The ext solve of this iteration (the predecessor) writes the tile's incidence entries.
-  // Large worlds (64-wide tiles, bandwidth-bound): wait for it here and prefetch the tile's
-  // entry range into L2 so the gather after the block solves finds it on chip. Small worlds
-  // (latency-bound): solve the tile's blocks first, overlapping the ext solve's tail, and wait
-  // just before the gather.
-  constexpr bool kEarlyWait = TP == 64;
-  if (kEarlyWait && sp.pdl == 2) {
-    pdl_wait();
-    pdl_trigger();
-  }
-  if (kEarlyWait && has_ext) {
-    const int e0 = c.ext_off[max(start, 0)], e1 = c.ext_off[min(start + kTileOwned, V)];
-    const char* lo = reinterpret_cast<const char*>(c.ext_contrib + 4ll * e0);
-    const char* hi = reinterpret_cast<const char*>(c.ext_contrib + 4ll * e1);
-    for (const char* a = lo + 128ll * tid; a < hi; a += 128ll * 32 * kWarps)
-      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a));
-  }
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-  __syncthreads();
+}
 
+// Phase 2: every elastic block of the tile evaluated and solved against the staged snapshot
+// (eval_constraint :101-270 + solve_block :400-487), results to t.res, activity to t.act.
+struct NoPost {
+  __device__ void operator()(int&, unsigned long long&) const {}
+};
+
+// post(nsing, bad): extra per-thread work after the items, counted in the same reduction.
+template <int TP, bool kLamSmem, class Post = NoPost>
+__device__ __forceinline__ void solve_items(Tile<TP>& t, const World& w, const SweepParams& sp, int start, unsigned mask,
+                                            int* singular, unsigned long long* err, Post&& post = Post()) {
+  constexpr int kWarps = warps_for<TP>();
+  constexpr int kTilePos = TP, kTileOwned = TP - 2;
+  const int vp = w.vpad;
+  const int tid = threadIdx.x, lane = tid & 31;
   const double h2 = sp.h2, beta = sp.beta;
   int nsing = 0;
   unsigned long long bad = kNoError;
@@ -184,8 +187,17 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
     const bool owned = pi >= 1 && pi <= kTileOwned;
     const int si = pi + 1;  // staging index of p
     PosRes& R = t.res[pi];
+    // Multipliers: per slot, ping-ponged in HBM (only the owner writes lam_out), or kept in the
+    // tile's shared rows (persistent kernel: halo positions are updated identically by both
+    // neighbouring tiles, so every copy stays equal to the owner's).
+    auto put_lam = [&](int f, double v) {
+      if (kLamSmem)
+        t.st[T_LAM + f][si] = v;
+      else if (owned)
+        sp.lam_out[f * (long long)vp + p] = v;
+    };
     auto keep_lam = [&](int f0, int nf) {
-      if (!owned) return;
+      if (kLamSmem || !owned) return;
       for (int f = f0; f < f0 + nf; ++f) sp.lam_out[f * (long long)vp + p] = t.st[T_LAM + f][si];
     };
     auto sing = [&]() {  // singular block: counted by its owner (per scene in a batch's last sweep)
@@ -222,7 +234,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
 #pragma unroll
           for (int b = 0; b < 3; ++b) M[a][b] = (a == b ? cd : 0.0) + (b0 * J0[b] + b1 * J1[b]);
         }
-        const double kinv = inverse_stiffness(t.st[T_KSZ][si]);
+        const double kinv = t.st[T_KSZ][si];
         double rhs[3], dl[3];
         const double lam[3] = {t.st[T_LAM + L_SZ0][si], t.st[T_LAM + L_SZ1][si], t.st[T_LAM + L_SZ2][si]};
 #pragma unroll
@@ -245,10 +257,10 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
           R.sz_dt[1] = -h2 * (it.y * jt1);
           R.sz_dt[2] = 0.0;
           t.act[A_SZ][pi] = 1;
+          put_lam(L_SZ0, lam[0] + dl[0]);
+          put_lam(L_SZ1, lam[1] + dl[1]);
+          put_lam(L_SZ2, lam[2] + dl[2]);
           if (owned) {
-            sp.lam_out[L_SZ0 * (long long)vp + p] = lam[0] + dl[0];
-            sp.lam_out[L_SZ1 * (long long)vp + p] = lam[1] + dl[1];
-            sp.lam_out[L_SZ2 * (long long)vp + p] = lam[2] + dl[2];
             if (!(ok && isfinite(R.sz_dt[0]) && isfinite(R.sz_dt[1]))) fail(lbase + __popc(ek & (EK_SZ - 1)));
           }
         } else {
@@ -261,7 +273,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
         double M = 0.0;
         if (is0 != 0.0) M = M + (h2 * is0 * 0.5) * 0.5;
         if (is1 != 0.0) M = M + (h2 * is1 * 0.5) * 0.5;
-        const double kinv = inverse_stiffness(t.st[T_KCS][si]);
+        const double kinv = t.st[T_KCS][si];
         const double lam = t.st[T_LAM + L_CS][si];
         M = M + kinv;
         if (M > 1e-250) {
@@ -269,8 +281,8 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
           R.cs[0] = -h2 * is0 * (0.5 * dl);
           R.cs[1] = -h2 * is1 * (0.5 * dl);
           t.act[A_CS][pi] = 1;
+          put_lam(L_CS, lam + dl);
           if (owned) {
-            sp.lam_out[L_CS * (long long)vp + p] = lam + dl;
             if (!(isfinite(dl) && isfinite(R.cs[0]) && isfinite(R.cs[1]))) fail(lbase + __popc(ek & (EK_CS - 1)));
           }
         } else {
@@ -285,7 +297,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
         double M = 0.0;
         if (is0 != 0.0) M = M + (h2 * is0 * j0) * j0;
         if (is1 != 0.0) M = M + (h2 * is1 * j1) * j1;
-        const double kinv = inverse_stiffness(t.st[T_KSS][si]);
+        const double kinv = t.st[T_KSS][si];
         const double lam = t.st[T_LAM + L_SS][si];
         M = M + kinv;
         if (M > 1e-250) {
@@ -293,8 +305,8 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
           R.ss[0] = -h2 * is0 * (j0 * dl);
           R.ss[1] = -h2 * is1 * (j1 * dl);
           t.act[A_SS][pi] = 1;
+          put_lam(L_SS, lam + dl);
           if (owned) {
-            sp.lam_out[L_SS * (long long)vp + p] = lam + dl;
             if (!(isfinite(dl) && isfinite(R.ss[0]) && isfinite(R.ss[1]))) fail(lbase + __popc(ek & (EK_SS - 1)));
           }
         } else {
@@ -333,7 +345,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
             M[a][b] = v + (b0 * J0[b] + b1 * J1[b]);
           }
         }
-        const double kinv = inverse_stiffness(t.st[T_KVS][si]);
+        const double kinv = t.st[T_KVS][si];
         double rhs[3], dl[3];
         const double lam[3] = {t.st[T_LAM + L_VS0][si], t.st[T_LAM + L_VS1][si], t.st[T_LAM + L_VS2][si]};
 #pragma unroll
@@ -359,10 +371,10 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
           R.vs_dt[1] = -h2 * (it.y * jt1);
           R.vs_dt[2] = 0.0;
           t.act[A_VS][pi] = 1;
+          put_lam(L_VS0, lam[0] + dl[0]);
+          put_lam(L_VS1, lam[1] + dl[1]);
+          put_lam(L_VS2, lam[2] + dl[2]);
           if (owned) {
-            sp.lam_out[L_VS0 * (long long)vp + p] = lam[0] + dl[0];
-            sp.lam_out[L_VS1 * (long long)vp + p] = lam[1] + dl[1];
-            sp.lam_out[L_VS2 * (long long)vp + p] = lam[2] + dl[2];
             if (!(ok && isfinite(R.vs_ds[0]) && isfinite(R.vs_ds[1]) && isfinite(R.vs_dt[0]) && isfinite(R.vs_dt[1])))
               fail(lbase + __popc(ek & (EK_VS - 1)));
           }
@@ -423,8 +435,8 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
             M[a][b] = v;
           }
         }
-        const double kinv[3] = {inverse_stiffness(t.st[T_KBT0][si]), inverse_stiffness(t.st[T_KBT1][si]),
-                                inverse_stiffness(t.st[T_KBT2][si])};
+        const double kinv[3] = {t.st[T_KBT0][si], t.st[T_KBT0][si],
+                                t.st[T_KBT2][si]};
         const double lam[3] = {t.st[T_LAM + L_BT0][si], t.st[T_LAM + L_BT1][si], t.st[T_LAM + L_BT2][si]};
         double rhs[3], dl[3];
 #pragma unroll
@@ -446,10 +458,10 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
             ok = ok && isfinite(R.bt_dta[b]) && isfinite(R.bt_dtb[b]);
           }
           t.act[A_BT][pi] = 1;
+          put_lam(L_BT0, lam[0] + dl[0]);
+          put_lam(L_BT1, lam[1] + dl[1]);
+          put_lam(L_BT2, lam[2] + dl[2]);
           if (owned) {
-            sp.lam_out[L_BT0 * (long long)vp + p] = lam[0] + dl[0];
-            sp.lam_out[L_BT1 * (long long)vp + p] = lam[1] + dl[1];
-            sp.lam_out[L_BT2 * (long long)vp + p] = lam[2] + dl[2];
             if (!ok) fail(lbase + __popc(vk & (VK_BT - 1)));
           }
         } else {
@@ -466,7 +478,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
         if (ism != 0.0) M = M + (h2 * ism * jm) * jm;
         if (is0 != 0.0) M = M + (h2 * is0 * j0) * j0;
         if (isp != 0.0) M = M + (h2 * isp * jp) * jp;
-        const double kinv = inverse_stiffness(t.st[T_KSB][si]);
+        const double kinv = t.st[T_KSB][si];
         const double lam = t.st[T_LAM + L_SB][si];
         M = M + kinv;
         if (M > 1e-250) {
@@ -475,8 +487,8 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
           R.sb[1] = -h2 * is0 * (j0 * dl);
           R.sb[2] = -h2 * isp * (jp * dl);
           t.act[A_SB][pi] = 1;
+          put_lam(L_SB, lam + dl);
           if (owned) {
-            sp.lam_out[L_SB * (long long)vp + p] = lam + dl;
             if (!(isfinite(dl) && isfinite(R.sb[0]) && isfinite(R.sb[1]) && isfinite(R.sb[2])))
               fail(lbase + __popc(vk & (VK_SB - 1)));
           }
@@ -505,7 +517,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
           if (is0 != 0.0) M = M + (h2 * is0 * js) * js;
           M = M + (((h2 * ja[0]) * ita.x * ja[0] + (h2 * ja[1]) * ita.y * ja[1]) + (h2 * ja[2]) * ita.z * ja[2]);
           M = M + (((h2 * jb[0]) * itb.x * jb[0] + (h2 * jb[1]) * itb.y * jb[1]) + (h2 * jb[2]) * itb.z * jb[2]);
-          const double kinv = inverse_stiffness(t.st[T_KVB][si]);
+          const double kinv = t.st[T_KVB][si];
           const int lf = cc == 0 ? L_VBU : L_VBV;
           const double lam = t.st[T_LAM + lf][si];
           M = M + kinv;
@@ -520,8 +532,8 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
               ok = ok && isfinite(R.vb_dta[cc][b]) && isfinite(R.vb_dtb[cc][b]);
             }
             t.act[cc == 0 ? A_VBU : A_VBV][pi] = 1;
+            put_lam(lf, lam + dl);
             if (owned) {
-              sp.lam_out[lf * (long long)vp + p] = lam + dl;
               if (!ok) fail(lbase + __popc(vk & (bit - 1)));
             }
           } else {
@@ -532,6 +544,8 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
       }
     }
   }
+  post(nsing, bad);
+  if (sp.dbg && blockIdx.x == 0 && (threadIdx.x & 31) == 0) sp.dbg[threadIdx.x >> 5] = gtimer();
   if (__any_sync(0xffffffffu, nsing != 0 || bad != kNoError)) {  // rare: singular blocks / errors
     for (int o = 16; o > 0; o >>= 1) {
       nsing += __shfl_down_sync(0xffffffffu, nsing, o);
@@ -545,13 +559,24 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
   }
   __syncthreads();
 
-  if (!kEarlyWait && sp.pdl == 2) {
-    pdl_wait();
-    pdl_trigger();
-  }
+}
 
-  // ---- gather in block order (constraints.cpp:509-534) and apply (:537-554)
-  for (int pi = 1 + tid; pi <= kTileOwned; pi += 32 * kWarps) {
+// Phase 3: one thread per owned slot gathers the corrections of every block touching it in the
+// reference's block order (constraints.cpp:509-534) — element pass of element k-1 then k,
+// vertex pass of vertex k-1, k, k+1, then the external blocks through `ext` — divides by the
+// number of active touching blocks and applies (:537-554) into Y (and the slot record).
+template <int TP, class ExtGather>
+__device__ __forceinline__ void gather_apply(const Tile<TP>& t, const World& w, const SweepParams& sp, int start, double* Y,
+                                             double* xrec_out, ExtGather&& ext) {
+  constexpr int kWarps = warps_for<TP>();
+  constexpr int kTileOwned = TP - 2;
+  const int vp = w.vpad;
+  const int tid = threadIdx.x, lane = tid & 31;
+  // Two threads per slot (adjacent warps): role 0 gathers and applies the center and scale
+  // (elastic + external blocks), role 1 the frame (elastic blocks only; external blocks have no
+  // theta slots) — two shorter dependency chains instead of one.
+  const int role = (tid >> 5) & 1;
+  for (int pi = 1 + lane + 32 * (tid >> 6); pi <= kTileOwned; pi += 16 * kWarps) {
     const int k = t.loc[pi];
     if (k < 0) continue;
     const int p = start - 1 + pi;
@@ -569,14 +594,17 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
     V3 tsum{0, 0, 0};
     int tcnt = 0;
     auto addc = [&](const double* d) {
+      if (role != 0) return;
       csum = csum + V3{d[0], d[1], d[2]};
       ++ccnt;
     };
     auto adds = [&](double d) {
+      if (role != 0) return;
       ssum += d;
       ++scnt;
     };
     auto addt = [&](const double* d) {
+      if (role != 1) return;
       tsum = tsum + V3{d[0], d[1], d[2]};
       ++tcnt;
     };
@@ -626,50 +654,256 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
       if (t.act[A_VBU][pi + 1]) addt(N.vb_dta[0]);
       if (t.act[A_VBV][pi + 1]) addt(N.vb_dta[1]);
     }
-    if (has_ext) {  // external blocks touching this vertex, in block order (entries slot-sorted)
-      // Chunks of 4 entries: all loads of a chunk are issued before the first add (the entry's
-      // kExtNone markers only predicate the adds), so a slot's list costs one latency per chunk.
-      const int e0 = c.ext_off[p], e1 = c.ext_off[p + 1];
-      for (int q0 = e0; q0 < e1; q0 += 4) {
-        double2 o01[4], o23[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int q = q0 + u < e1 ? q0 + u : e0;
-          const double2* o = reinterpret_cast<const double2*>(c.ext_contrib + 4ll * q);
-          o01[u] = o[0];
-          o23[u] = o[1];
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (q0 + u >= e1 || is_ext_none(o01[u].x)) continue;
-          const double d[3] = {o01[u].x, o01[u].y, o23[u].x};
-          addc(d);
-          if (!is_ext_none(o23[u].y)) adds(o23[u].y);
-        }
+    if (role == 0) {
+      ext(p, addc, adds);
+      V3 cn{t.st[T_CX][si], t.st[T_CY][si], t.st[T_CZ][si]};
+      if (ccnt > 0) cn = cn + csum / static_cast<double>(ccnt);
+      double sn = t.st[T_S][si];
+      if (scnt > 0) sn = fmax(sn + ssum / static_cast<double>(scnt), kMinScale);
+      Y[CX * (long long)vp + p] = cn.x;
+      Y[CY * (long long)vp + p] = cn.y;
+      Y[CZ * (long long)vp + p] = cn.z;
+      Y[S * (long long)vp + p] = sn;
+      if (xrec_out) {
+        double2* xr = reinterpret_cast<double2*>(xrec_out + 8ll * p);
+        xr[0] = make_double2(cn.x, cn.y);
+        xr[1] = make_double2(cn.z, sn);
       }
+    } else {
+      Q4 qn{t.st[T_QW][si], t.st[T_QX][si], t.st[T_QY][si], t.st[T_QZ][si]};
+      if (has_el && tcnt > 0) qn = apply_increment(qn, tsum / static_cast<double>(tcnt));
+      Y[QW * (long long)vp + p] = qn.w;
+      Y[QX * (long long)vp + p] = qn.x;
+      Y[QY * (long long)vp + p] = qn.y;
+      Y[QZ * (long long)vp + p] = qn.z;
     }
-    V3 cn{t.st[T_CX][si], t.st[T_CY][si], t.st[T_CZ][si]};
-    if (ccnt > 0) cn = cn + csum / static_cast<double>(ccnt);
-    double sn = t.st[T_S][si];
-    if (scnt > 0) sn = fmax(sn + ssum / static_cast<double>(scnt), kMinScale);
-    Q4 qn{t.st[T_QW][si], t.st[T_QX][si], t.st[T_QY][si], t.st[T_QZ][si]};
-    if (has_el && tcnt > 0) qn = apply_increment(qn, tsum / static_cast<double>(tcnt));
-    Y[CX * (long long)vp + p] = cn.x;
-    Y[CY * (long long)vp + p] = cn.y;
-    Y[CZ * (long long)vp + p] = cn.z;
-    Y[S * (long long)vp + p] = sn;
-    if (has_ext) {
-      double2* xr = reinterpret_cast<double2*>(w.xrec + 8ll * p);
-      xr[0] = make_double2(cn.x, cn.y);
-      xr[1] = make_double2(cn.z, sn);
-    }
-    Y[QW * (long long)vp + p] = qn.w;
-    Y[QX * (long long)vp + p] = qn.x;
-    Y[QY * (long long)vp + p] = qn.y;
-    Y[QZ * (long long)vp + p] = qn.z;
   }
 }
 
+
+
+// The external blocks touching a slot (entries [e0, e1)), in block order (incidence entries are slot-sorted, then
+// block-sorted): each entry holds the block's correction of this endpoint (ext_contrib, kExtNone
+// markers for "no update" / "no scale update"). Chunks of 4 entries: all loads of a chunk are
+// issued before the first add (the markers only predicate the adds), so a slot's list costs one
+// latency per chunk.
+template <class AddC, class AddS>
+__device__ __forceinline__ void gather_entries(const Collide& c, int e0, int e1, AddC& addc, AddS& adds) {
+  for (int q0 = e0; q0 < e1; q0 += 4) {
+    double2 o01[4], o23[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + u < e1 ? q0 + u : e0;
+      const double2* o = reinterpret_cast<const double2*>(c.ext_contrib + 4ll * q);
+      o01[u] = o[0];
+      o23[u] = o[1];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (q0 + u >= e1 || is_ext_none(o01[u].x)) continue;
+      const double d[3] = {o01[u].x, o01[u].y, o23[u].x};
+      addc(d);
+      if (!is_ext_none(o23[u].y)) adds(o23[u].y);
+    }
+  }
+}
+
+// Writes an endpoint's correction into its incidence entry q (flag 0 = no update from the block;
+// kExtNone in ds = no scale update).
+__device__ __forceinline__ void put_entry(const Collide& c, int q, int flag, double x, double y, double z, double ds) {
+  double2* o = reinterpret_cast<double2*>(c.ext_contrib + 4ll * q);
+  if (flag) {
+    o[0] = make_double2(x, y);
+    o[1] = make_double2(z, (flag & kExtScale) ? ds : ext_none());
+  } else {
+    o[0].x = ext_none();
+  }
+}
+
+// One sweep per launch (large worlds; every world when the persistent kernel does not apply).
+template <int TP>
+__global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_sweep(World w, Collide c, const double* __restrict__ X,
+                                                          double* __restrict__ Y, SweepParams sp, int* singular,
+                                                          unsigned long long* err, int has_ext) {
+  constexpr int kWarps = warps_for<TP>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int kTileOwned = TP - 2;
+  Tile<TP>& t = *reinterpret_cast<Tile<TP>*>(smem_raw);
+  if (sp.pdl == 1) {  // predecessor wrote X: wait before staging
+    pdl_wait();
+    pdl_trigger();
+  }
+  const int V = w.V;
+  const int start = blockIdx.x * kTileOwned;
+  const int tid = threadIdx.x;
+  const unsigned mask = tile_meta(t, w, start);
+  stage_rows(t, w, X, sp.lam_in, start, mask, 0, kStageRows);
+  // The ext solve of this iteration (the predecessor) writes the tile's incidence entries.
+  // Large worlds (64-wide tiles, bandwidth-bound): wait for it here and prefetch the tile's
+  // entry range into L2 so the gather after the block solves finds it on chip. Small worlds
+  // (latency-bound): solve the tile's blocks first, overlapping the ext solve's tail, and wait
+  // just before the gather.
+  constexpr bool kEarlyWait = TP == 64;
+  if (kEarlyWait && sp.pdl == 2) {
+    pdl_wait();
+    pdl_trigger();
+  }
+  if (kEarlyWait && has_ext) {
+    const int e0 = c.ext_off[max(start, 0)], e1 = c.ext_off[min(start + kTileOwned, V)];
+    const char* lo = reinterpret_cast<const char*>(c.ext_contrib + 4ll * e0);
+    const char* hi = reinterpret_cast<const char*>(c.ext_contrib + 4ll * e1);
+    for (const char* a = lo + 128ll * tid; a < hi; a += 128ll * 32 * kWarps)
+      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a));
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+
+  solve_items<TP, false>(t, w, sp, start, mask, singular, err);
+
+  if (!kEarlyWait && sp.pdl == 2) {
+    pdl_wait();
+    pdl_trigger();
+  }
+  gather_apply(t, w, sp, start, Y, has_ext ? w.xrec : nullptr, [&](int p, auto& addc, auto& adds) {
+    if (has_ext) gather_entries(c, c.ext_off[p], c.ext_off[p + 1], addc, adds);
+  });
+}
+
+// Grid-wide barrier of the persistent kernel (all CTAs co-resident: cooperative launch). The
+// counter is zeroed before each launch; `target` advances by gridDim.x per barrier.
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+// The whole iteration loop of one substep (solver.cpp:330-339) for small single-scene worlds,
+// in ONE launch: one CTA per tile, all tiles co-resident, a grid barrier after each sweep and
+// after each shape-matching level. What the per-launch path moves through HBM every sweep
+// stays on chip: the tile's static rows are staged once, the elastic multipliers live in the
+// tile's shared rows (never written back; they are reset every substep anyway), and the
+// external blocks are not solved by a separate kernel: every incidence entry re-solves its block
+// in the gather (ext_block, ext.cuh — the same arithmetic as k_ext_solve, so the same bits)
+// and only the block's owner entry commits its multiplier (ping-pong lam_ext[2]) and counts
+// singular / non-finite outcomes. The slot records are ping-ponged too (xrec[2]), so blocks
+// solved by other tiles during a sweep always see the snapshot.
+template <int TP>
+__global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Collide c, Groups g, PersistParams pp,
+                                                                      SweepParams sp, int* singular,
+                                                                      unsigned long long* err) {
+  constexpr int kWarps = warps_for<TP>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int kTileOwned = TP - 2, kTileStage = TP + 2;
+  Tile<TP>& t = *reinterpret_cast<Tile<TP>*>(smem_raw);
+  const int start = blockIdx.x * kTileOwned;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned mask = tile_meta(t, w, start);
+  stage_rows(t, w, nullptr, nullptr, start, mask, T_SBAR, T_LAM);  // statics: once per substep
+  if (pp.has_ext)
+    for (int i = tid; i <= kTileOwned; i += 32 * kWarps) t.eoff[i] = c.ext_off[min(start + i, w.V)];
+  for (int i = tid; i < kLamFields * kTileStage; i += 32 * kWarps) t.st[T_LAM + i / kTileStage][i % kTileStage] = 0.0;
+  const int has_ext = pp.has_ext;
+  double* cur = pp.X;
+  double* nxt = pp.Y;
+  double* xr_cur = pp.xrec[0];
+  double* xr_nxt = pp.xrec[1];
+  double* el_cur = pp.lam_ext[0];
+  double* el_nxt = pp.lam_ext[1];
+  unsigned target = 0;
+  int ntr = 0;
+  auto mark = [&]() {  // debug phase trace (VROD_TRACE=1): CTA 0, one timestamp per phase
+    if (pp.trace && blockIdx.x == 0 && tid == 0 && ntr < kTraceCap - 1) {
+      unsigned long long ns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+      pp.trace[1 + ntr++] = ns;
+      pp.trace[0] = ntr;
+    }
+  };
+  mark();
+  if (pp.trace && blockIdx.x == 0 && tid == 0) pp.trace[598] = g.nchains > 0 ? 1 : pp.levels;
+  for (int it = 0; it < pp.iterations; ++it) {
+    sp.iter = it;
+    if (it > 0) {
+      for (int i = tid; i < kKinds * TP; i += 32 * kWarps) t.act[i / TP][i % TP] = 0;
+    }
+    stage_rows(t, w, cur, nullptr, start, mask, 0, T_SBAR);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    mark();
+    // External blocks: every incidence entry of the tile's owned slots (a contiguous range)
+    // re-solves its block on the snapshot, one thread per entry, after that thread's elastic
+    // items — entries go to the warps of the cheapest kinds first — and writes its endpoint's
+    // correction into the entry; the block's owner entry commits the multiplier and counts.
+    auto ext_entries = [&](int& nsing, unsigned long long& bad) {
+      if (!has_ext) return;
+      constexpr int kOrder[8] = {7, 0, 1, 5, 6, 2, 3, 4};  // rank of warp w (CS, SS, SB, VB.. first)
+      const int r = (kWarps == 8 ? kOrder[warp] : warp) * 32 + lane;
+      const int q0 = t.eoff[0], q1 = t.eoff[kTileOwned];
+      for (int q = q0 + r; q < q1; q += 32 * kWarps) {
+        const int item = c.ext_items[q];
+        const int b = item >> 2, e = item & 3;
+        const ExtResult res = ext_block(w, c, cur, xr_cur, el_cur + 3ll * b, b, sp,
+                                        [&](int e2, int flag, double x, double y, double z, double ds) {
+                                          if (e2 == e) put_entry(c, q, flag, x, y, z, ds);
+                                        });
+        if (e == res.owner) {  // the block's owner entry commits it
+          for (int d = 0; d < res.nlam; ++d) el_nxt[3ll * b + d] = res.lam[d];
+          if (res.singular) ++nsing;
+          if (res.bad)
+            bad = umin64(bad, err_code(sp.substep, ERR_SWEEP, it, static_cast<unsigned long long>(sp.elastic_blocks) + b));
+        }
+      }
+    };
+    solve_items<TP, true>(t, w, sp, start, mask, singular + it, err, ext_entries);  // ends with __syncthreads()
+    mark();
+    gather_apply(t, w, sp, start, nxt, has_ext ? xr_nxt : nullptr, [&](int p, auto& addc, auto& adds) {
+      if (has_ext) gather_entries(c, t.eoff[p - start], t.eoff[p - start + 1], addc, adds);
+    });
+    mark();
+    if (pp.trace && it == 1 && tid == 0) pp.trace[700 + blockIdx.x] = gtimer();
+    grid_sync(pp.bar, target);
+    mark();
+    double* tmp = cur;
+    cur = nxt;
+    nxt = tmp;
+    tmp = xr_cur;
+    xr_cur = xr_nxt;
+    xr_nxt = tmp;
+    tmp = el_cur;
+    el_cur = el_nxt;
+    el_nxt = tmp;
+    if (g.G > 0 && (it + 1) % pp.sm_period == 0) {  // shape matching (shape.cuh)
+      // One warp per work unit: a dependency chain of groups (one barrier in all), or one group
+      // of the current level (a barrier per level). A single call site keeps one copy of the
+      // group code in the kernel.
+      const int gw = warp * gridDim.x + blockIdx.x, nw = kWarps * gridDim.x;
+      const bool chains = g.nchains > 0;
+      const int phases = chains ? 1 : pp.levels;
+      for (int l = 0; l < phases; ++l) {
+        const int u0 = chains ? 0 : pp.level_off[l], u1 = chains ? g.nchains : pp.level_off[l + 1];
+        for (int u = u0 + gw; u < u1; u += nw) {
+          const int k0 = chains ? g.chain_off[u] : u, k1 = chains ? g.chain_off[u + 1] : u + 1;
+          for (int k = k0; k < k1; ++k) {
+            const bool tr = pp.trace && it == 1 && (chains ? u == 28 : u == u0);
+            shape_group(w, g, cur, xr_cur, chains ? g.chain_groups[k] : g.level_groups[k], lane,
+                        tr ? pp.trace + 600 + 8 * (chains ? k - k0 : l) : nullptr);
+            __syncwarp();
+          }
+        }
+        grid_sync(pp.bar, target);
+        mark();
+      }
+    }
+  }
+}
 
 template <int TP>
 void launch_tiles(const World& w, Collide& c, const double* X, double* Y, const SweepParams& sp, int* singular_counter,
@@ -683,6 +917,8 @@ void launch_tiles(const World& w, Collide& c, const double* X, double* Y, const 
                 err, has_ext);
 }
 
+constexpr int kPersistTP = 32;
+
 }  // namespace
 
 void launch_rod_sweep(const World& w, Collide& c, const double* X, double* Y, const SweepParams& sp,
@@ -692,6 +928,37 @@ void launch_rod_sweep(const World& w, Collide& c, const double* X, double* Y, co
     launch_tiles<64>(w, c, X, Y, sp, singular_counter, err, st);
   else
     launch_tiles<32>(w, c, X, Y, sp, singular_counter, err, st);
+}
+
+int persistent_tiles(const World& w) {
+  if (w.n_scenes != 1 || w.V <= 0) return 0;
+  const int tiles = (w.V + kPersistTP - 3) / (kPersistTP - 2);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = sizeof(Tile<kPersistTP>);
+  if (cudaFuncSetAttribute(k_iterate<kPersistTP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iterate<kPersistTP>, 32 * warps_for<kPersistTP>(), smem) !=
+      cudaSuccess)
+    return 0;
+  return tiles <= per_sm * sms ? tiles : 0;
+}
+
+void launch_iterate_persistent(const World& w, Collide& c, const Groups& g, const PersistParams& pp, const SweepParams& sp,
+                               int* singular_counters, unsigned long long* err, cudaStream_t st) {
+  const int tiles = (w.V + kPersistTP - 3) / (kPersistTP - 2);
+  cudaMemsetAsync(pp.bar, 0, sizeof(unsigned), st);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles);
+  cfg.blockDim = dim3(32 * warps_for<kPersistTP>());
+  cfg.dynamicSmemBytes = sizeof(Tile<kPersistTP>);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barriers)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_iterate<kPersistTP>, w, c, g, pp, sp, singular_counters, err);
 }
 
 }  // namespace vdev

@@ -1,0 +1,254 @@
+// Bundle shape matching of one group (apply_shape_match / fit_similarity / extract_rotation,
+// bundling.cpp:50-133) by one warp. Shared by the per-level kernel k_shape_level (shape.cu) and
+// the persistent small-world iteration kernel (rodsweep.cu), so both paths give the same bits.
+//
+// Member loads are strided over lanes; the centroid, the 3x3 covariance B and the scale numerator
+// are warp tree reductions (fixed order, deterministic); the Müller rotation extraction
+// (warm-started from the group's persistent rotation) runs redundantly in every lane, and lanes
+// write their members back. Shape matching is tolerance-pinned: the rotation
+// chain uses explicit FMAs (both translation units compile with --fmad=false).
+#pragma once
+
+#include "kernels.cuh"
+#include "vmath.cuh"
+
+namespace vdev {
+
+__device__ __forceinline__ double shape_wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// General route of the rotation increment (half angle >= 1e-2: rare once warm-started); kept out
+// of line so sincos's range reduction does not bloat the hot loop's code.
+static __device__ __noinline__ void rotation_increment_general(double a2, double& k, double& c) {
+  const double angle = sqrt(a2);
+  double s;
+  sincos(0.5 * angle, &s, &c);
+  k = s / angle;
+}
+
+// Reciprocal for the rotation chain: MUFU seed + two Newton steps (relative error ~1 ulp).
+__device__ __forceinline__ double rcp_fast(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+// extract_rotation, bundling.cpp:50-67: the same iteration (omega = sum R_a x B_a / (|sum
+// R_a . B_a| + 1e-9), q <- AngleAxis(|omega|, omega^) q, normalize, stop at |omega| < 1e-9).
+// The loop is one serial dependency chain (~10 iterations warm-started at C3, up to ~20), so it
+// is written for latency (shape matching is tolerance-pinned): FMA trees, a Newton
+// reciprocal, and for half angles below 1e-2 the increment [cos(a/2), sin(a/2)/a * omega] from
+// its Taylor series in a^2 (truncation < 1e-20 relative); larger steps take the general route.
+// The product of two unit quaternions has |p|^2 = 1 + O(1e-15), so the renormalisation uses
+// 1/sqrt(n) = 1 - (n-1)/2 + 3/8 (n-1)^2 (exact to 1e-30 there; rsqrt otherwise).
+__device__ __forceinline__ vm::Q4 extract_rotation(const vm::M3& B, const vm::Q4& guess, int* iters = nullptr) {
+  using namespace vm;
+  Q4 q = qnormalized(guess);
+  int it = 0;
+#pragma unroll 1
+  for (; it < 100; ++it) {
+    // R = toRotationMatrix(q)
+    const double tx = 2.0 * q.x, ty = 2.0 * q.y, tz = 2.0 * q.z;
+    const double twx = tx * q.w, twy = ty * q.w, twz = tz * q.w;
+    const double txx = tx * q.x, txy = ty * q.x, txz = tz * q.x;
+    const double tyy = ty * q.y, tyz = tz * q.y, tzz = tz * q.z;
+    const double R[3][3] = {{1.0 - (tyy + tzz), txy - twz, txz + twy},
+                            {txy + twz, 1.0 - (txx + tzz), tyz - twx},
+                            {txz - twy, tyz + twx, 1.0 - (txx + tyy)}};
+    // w = sum_a col(R, a) x col(B, a); d = sum_a col(R, a) . col(B, a)
+    double wx[3], wy[3], wz[3], dd[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double r0 = R[0][a], r1 = R[1][a], r2 = R[2][a];
+      const double b0 = B.m[0][a], b1 = B.m[1][a], b2 = B.m[2][a];
+      wx[a] = fma(r1, b2, -r2 * b1);
+      wy[a] = fma(r2, b0, -r0 * b2);
+      wz[a] = fma(r0, b1, -r1 * b0);
+      dd[a] = fma(r0, b0, fma(r1, b1, r2 * b2));
+    }
+    const double ox = (wx[0] + wx[1]) + wx[2], oy = (wy[0] + wy[1]) + wy[2], oz = (wz[0] + wz[1]) + wz[2];
+    const double inv = rcp_fast(fabs((dd[0] + dd[1]) + dd[2]) + 1e-9);
+    const double w2 = fma(ox, ox, fma(oy, oy, oz * oz));
+    const double a2 = (w2 * inv) * inv;  // |omega|^2
+    if (a2 < 1e-18) break;  // |omega| < 1e-9
+    const double x2 = 0.25 * a2;  // (angle / 2)^2
+    double k, c;  // k = sin(angle/2) / angle, c = cos(angle/2)
+    if (x2 < 1e-4) {
+      k = 0.5 * fma(-x2 * (1.0 / 6), fma(-x2 * (1.0 / 20), fma(-x2 * (1.0 / 42), fma(-x2, 1.0 / 72, 1.0), 1.0), 1.0), 1.0);
+      c = fma(-x2 * 0.5,
+              fma(-x2 * (1.0 / 12), fma(-x2 * (1.0 / 30), fma(-x2 * (1.0 / 56), fma(-x2, 1.0 / 90, 1.0), 1.0), 1.0), 1.0),
+              1.0);
+    } else {
+      rotation_increment_general(a2, k, c);
+    }
+    const double ki = k * inv;
+    const double vx = ki * ox, vy = ki * oy, vz = ki * oz;
+    // p = [c, v] * q (Hamilton product)
+    const double pw = fma(c, q.w, -fma(vx, q.x, fma(vy, q.y, vz * q.z)));
+    const double px = fma(c, q.x, fma(vx, q.w, fma(vy, q.z, -vz * q.y)));
+    const double py = fma(c, q.y, fma(vy, q.w, fma(vz, q.x, -vx * q.z)));
+    const double pz = fma(c, q.z, fma(vz, q.w, fma(vx, q.y, -vy * q.x)));
+    const double e = fma(pw, pw, fma(px, px, fma(py, py, pz * pz))) - 1.0;
+    const double r = fabs(e) < 1e-6 ? fma(e, fma(e, 0.375, -0.5), 1.0) : rsqrt(e + 1.0);
+    q = Q4{pw * r, px * r, py * r, pz * r};
+  }
+  if (iters) *iters = it;
+  return q;
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long ns;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+  return ns;
+}
+
+// Fit and apply group `grp` (apply_shape_match, bundling.cpp:116-133) on the state rows X and
+// the slot records xrec. Called by all 32 lanes of a warp. tr: optional phase timestamps.
+__device__ __forceinline__ void shape_group(const World& w, const Groups& g, double* X, double* xrec, int grp,
+                                            int lane, unsigned long long* tr = nullptr) {
+  using namespace vm;
+  if (tr && lane == 0) tr[0] = gtimer();
+  const int m0 = g.off[grp], m1 = g.off[grp + 1];
+  const int n = m1 - m0;
+  const long long vp = w.vpad;
+  auto ldc = [&](int v) { return V3{X[CX * vp + v], X[CY * vp + v], X[CZ * vp + v]}; };
+  auto ldq = [&](int v) { return Q4{X[QW * vp + v], X[QX * vp + v], X[QY * vp + v], X[QZ * vp + v]}; };
+  // The lane's first member's state is loaded once, all loads in flight together, and reused by
+  // the three passes (members beyond 32 per group are reloaded).
+  const int i0 = m0 + lane;
+  const bool has0 = i0 < m1;
+  V3 c0{0, 0, 0};
+  double s0 = 0.0;
+  Q4 q0{1, 0, 0, 0};
+  if (has0) {
+    const int v = g.mslot[i0], e = g.meslot[i0];
+    c0 = ldc(v);
+    s0 = X[S * vp + v];
+    q0 = ldq(e);
+  }
+  // centroid of the current member centers
+  V3 sum = c0;
+  for (int i = i0 + 32; i < m1; i += 32) sum = sum + ldc(g.mslot[i]);
+  const V3 cent = V3{shape_wsum(sum.x), shape_wsum(sum.y), shape_wsum(sum.z)} / static_cast<double>(n);
+  if (tr && lane == 0) tr[1] = gtimer();
+  // B = sum (s * sbar) R Rbar^T + (c - mu) cbar^T
+  double Bp[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = i0; i < m1; i += 32) {
+    const double* mr = g.mrest + 17ll * i;
+    const bool first = i == i0;
+    const int v = first ? 0 : g.mslot[i];
+    const V3 c = (first ? c0 : ldc(v)) - cent;
+    const double s = first ? s0 : X[S * vp + v];
+    const M3 R = qmat(first ? q0 : ldq(g.meslot[i]));
+    M3 rR;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) rR.m[a][b] = mr[4 + 3 * a + b];
+    const double ss = s * mr[3];
+    M3 A;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) A.m[a][b] = ss * R.m[a][b];
+    const M3 P = mmul_bt(A, rR);
+    const double cv[3] = {c.x, c.y, c.z};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) Bp[3 * a + b] += P.m[a][b] + cv[a] * mr[b];
+  }
+  M3 B;
+  double sq[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      B.m[a][b] = shape_wsum(Bp[3 * a + b]);
+      sq[a + 3 * b] = B.m[a][b] * B.m[a][b];
+    }
+  if (tr && lane == 0) tr[2] = gtimer();
+  const double* gr = g.grest + 4ll * grp;
+  const double denom = gr[3];
+  if (sqrt(sum9(sq)) < 1e-12 || denom < 1e-300) return;  // degenerate: no write (bundling.cpp:86-90)
+  const double* wq = g.warm + 4ll * grp;
+  int nit = 0;
+  const Q4 q = extract_rotation(B, Q4{wq[0], wq[1], wq[2], wq[3]}, &nit);
+  if (tr && lane == 0) {
+    tr[3] = gtimer();
+    tr[6] = nit;
+  }
+  const M3 Rf = qmat(q);
+  const V3 rcent{gr[0], gr[1], gr[2]};
+  double numer = 0.0;
+  for (int i = i0; i < m1; i += 32) {
+    const double* mr = g.mrest + 17ll * i;
+    const bool first = i == i0;
+    const int v = first ? 0 : g.mslot[i];
+    const V3 c = (first ? c0 : ldc(v)) - cent;
+    const double s = first ? s0 : X[S * vp + v];
+    const M3 R = qmat(first ? q0 : ldq(g.meslot[i]));
+    M3 rR;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) rR.m[a][b] = mr[4 + 3 * a + b];
+    const M3 RR = mmul(Rf, rR);
+    double e[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) e[a + 3 * b] = RR.m[a][b] * R.m[a][b];
+    numer += (s * mr[3]) * sum9(e);
+    numer += dot(c, mvmul(Rf, V3{mr[0], mr[1], mr[2]}));
+  }
+  numer = shape_wsum(numer);
+  if (tr && lane == 0) tr[4] = gtimer();
+  const double scale = fmax(numer / denom, kMinScale);
+  const V3 t = cent - scale * mvmul(Rf, rcent);
+  const Q4 qf = qfrom_mat(Rf);
+  auto apply = [&](int i) {
+    const double* mr = g.mrest + 17ll * i;
+    const int v = g.mslot[i];
+    if (!w.pinned[v]) {
+      const V3 x = scale * mvmul(Rf, V3{mr[0], mr[1], mr[2]} + rcent) + t;
+      X[CX * vp + v] = x.x;
+      X[CY * vp + v] = x.y;
+      X[CZ * vp + v] = x.z;
+      const double sn = fmax(scale * mr[3], kMinScale);
+      X[S * vp + v] = sn;
+      double2* xr = reinterpret_cast<double2*>(xrec + 8ll * v);
+      xr[0] = make_double2(x.x, x.y);
+      xr[1] = make_double2(x.z, sn);
+    }
+    const Q4 fr = qnormalized(qmul(qf, Q4{mr[13], mr[14], mr[15], mr[16]}));
+    const int e = g.meslot[i];
+    X[QW * vp + e] = fr.w;
+    X[QX * vp + e] = fr.x;
+    X[QY * vp + e] = fr.y;
+    X[QZ * vp + e] = fr.z;
+  };
+  __syncwarp();
+  if (g.serial[grp]) {
+    if (lane == 0)
+      for (int i = m0; i < m1; ++i) apply(i);
+  } else {
+    for (int i = m0 + lane; i < m1; i += 32) apply(i);
+  }
+  if (tr && lane == 0) tr[5] = gtimer();
+  if (lane == 0) {
+    double* wo = g.warm + 4ll * grp;
+    wo[0] = q.w;
+    wo[1] = q.x;
+    wo[2] = q.y;
+    wo[3] = q.z;
+  }
+}
+
+}  // namespace vdev

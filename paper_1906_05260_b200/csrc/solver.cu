@@ -275,6 +275,13 @@ Solver::Solver(const SceneData& scene, const BatchLayout* batch) : scene_(scene)
     upload(g_.warm, warm, stream_);
     upload(g_.serial, serial, stream_);
     upload(g_.level_groups, lvl_groups, stream_);
+    if (!setup_.chain_groups.empty()) {
+      g_.nchains = static_cast<int>(setup_.chain_off.size()) - 1;
+      g_.chain_off = dalloc<int>(setup_.chain_off.size());
+      g_.chain_groups = dalloc<int>(setup_.chain_groups.size());
+      upload(g_.chain_off, setup_.chain_off, stream_);
+      upload(g_.chain_groups, setup_.chain_groups, stream_);
+    }
   }
 
   // ---- animation packet ----------------------------------------------------------------------
@@ -325,6 +332,16 @@ Solver::Solver(const SceneData& scene, const BatchLayout* batch) : scene_(scene)
   check_cuda(cudaMallocHost(&h_acc_, sizeof(StepAccum)), "cudaMallocHost");
   d_singular_ = dalloc<int>(std::max(scene_.settings.iterations, 1));
   d_err_ = dalloc<unsigned long long>(1);
+  if (persist_ok_ && n_scenes_ == 1 && g_.levels <= vdev::kMaxPersistLevels) persist_tiles_ = vdev::persistent_tiles(w_);
+  if (persist_tiles_ > 0) {
+    xrec2_ = dalloc<double>(8ull * w_.vpad);
+    ext_lam2_ = dalloc<double>(3 * std::max(c_.ext_cap, 1ll));
+    d_bar_ = dalloc<unsigned>(1);
+    if (std::getenv("VROD_TRACE") && std::getenv("VROD_TRACE")[0] == '1') {
+      d_trace_ = dalloc<unsigned long long>(vdev::kTraceCap);
+      check_cuda(cudaMemset(d_trace_, 0, sizeof(unsigned long long) * vdev::kTraceCap), "trace");
+    }
+  }
   report_parts_ = vdev::report_parts(V);
   d_report_partials_ = dalloc<double>(16ull * std::max(report_parts_, 1));
 
@@ -456,10 +473,10 @@ void Solver::upload_static() {
         const double l = rod.len[k], l0 = rod.len0[k];
         ES(vdev::A2E, v) = a2;
         ES(vdev::A4EP, v) = 0.25 * kPi * std::pow(rmid, 4);
-        ES(vdev::KSZ, v) = a2 * M.sz * l;
-        ES(vdev::KCS, v) = a2 * kxy * l;
-        ES(vdev::KSS, v) = a4 * kxy * l;
-        ES(vdev::KVS, v) = a2 * M.vol * l0;
+        ES(vdev::KSZ, v) = inverse_stiffness(a2 * M.sz * l);
+        ES(vdev::KCS, v) = inverse_stiffness(a2 * kxy * l);
+        ES(vdev::KSS, v) = inverse_stiffness(a4 * kxy * l);
+        ES(vdev::KVS, v) = inverse_stiffness(a2 * M.vol * l0);
         // refresh_orientation_inertia at construction (layout.cpp:76-93)
         const double smid = 0.5 * (rod.s[k] + rod.s[k + 1]);
         const double r4 = kPi * rmid * rmid * rmid * rmid;
@@ -475,11 +492,11 @@ void Solver::upload_static() {
         const double lw = 0.5 * (rod.len[k - 1] + rod.len[k]);
         const double lw0 = 0.5 * (rod.len0[k - 1] + rod.len0[k]);
         ES(vdev::A4VP, v) = 0.25 * kPi * std::pow(rv, 4);
-        ES(vdev::KBT0, v) = a4 * M.sz * lw;
-        ES(vdev::KBT1, v) = a4 * M.sz * lw;
-        ES(vdev::KBT2, v) = a4 * kxy * lw;
-        ES(vdev::KSB, v) = a4 * bxy * lw;
-        ES(vdev::KVB, v) = 2.0 * a4 * M.vol * lw0;
+        ES(vdev::KBT0, v) = inverse_stiffness(a4 * M.sz * lw);
+        ES(vdev::KBT1, v) = inverse_stiffness(a4 * M.sz * lw);
+        ES(vdev::KBT2, v) = inverse_stiffness(a4 * kxy * lw);
+        ES(vdev::KSB, v) = inverse_stiffness(a4 * bxy * lw);
+        ES(vdev::KVB, v) = inverse_stiffness(2.0 * a4 * M.vol * lw0);
       }
       (void)scale_kinds;
     }
@@ -506,6 +523,7 @@ void Solver::upload_static() {
       o[6] = VS(vdev::IS, p);
     }
     upload(w_.xrec, rec, stream_);
+    if (xrec2_) upload(xrec2_, rec, stream_);  // statics of the persistent kernel's partner records
   }
   upload(w_.bone_w, bw, stream_);
 
@@ -674,7 +692,27 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
     const bool pdl = vdev::g_pdl;
     double* lam_a = w_.lam;
     double* lam_b = w_.lam + static_cast<std::size_t>(vdev::kLamFields) * w_.vpad;
-    for (int it = 0; it < iterations; ++it) {
+    if (persist_tiles_ > 0 && !probe_log) {  // the whole iteration loop in one launch
+      vdev::PersistParams pp{};
+      pp.X = cur;
+      pp.Y = nxt;
+      pp.xrec[0] = w_.xrec;
+      pp.xrec[1] = xrec2_;
+      pp.lam_ext[0] = c_.ext_lam;
+      pp.lam_ext[1] = ext_lam2_;
+      pp.bar = d_bar_;
+      pp.trace = d_trace_;
+      pp.iterations = iterations;
+      pp.sm_period = scene_.settings.sm_period;
+      pp.levels = g_.levels;
+      pp.has_ext = c_.ext_cap > 0 ? 1 : 0;
+      for (int l = 0; l <= g_.levels && g_.G > 0; ++l) pp.level_off[l] = level_off_[l];
+      begin(CAT_ITERATE);
+      vdev::launch_iterate_persistent(w_, c_, g_, pp, sp, d_singular_, d_err_, st);
+      end();
+      if (iterations & 1) std::swap(cur, nxt);
+    }
+    for (int it = 0; it < iterations && !(persist_tiles_ > 0 && !probe_log); ++it) {
       sp.iter = it;
       sp.scene_singular = (n_scenes_ > 1 && it == iterations - 1) ? d_scene_sing_ : nullptr;
       sp.lam_in = (it & 1) ? lam_b : lam_a;
@@ -809,6 +847,19 @@ long long Solver::kernel_nodes_per_step() {
   return kernels_per_step_;
 }
 
+int Solver::trace(long long* out, int cap) {
+  if (!d_trace_) return 0;
+  std::vector<unsigned long long> h(vdev::kTraceCap);
+  check_cuda(cudaMemcpy(h.data(), d_trace_, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost), "trace");
+  if (cap < 0) {  // raw buffer
+    const int n = std::min(-cap, vdev::kTraceCap);
+    for (int i = 0; i < n; ++i) out[i] = static_cast<long long>(h[i]);
+    return n;
+  }
+  const int n = static_cast<int>(std::min<unsigned long long>(h[0], static_cast<unsigned long long>(cap)));
+  for (int i = 0; i < n; ++i) out[i] = static_cast<long long>(h[1 + i]);
+  return n;
+}
 int Solver::contact_count_last() { return h_acc_->contact_count; }
 
 double Solver::bench_run(int steps, long long flush_bytes) {

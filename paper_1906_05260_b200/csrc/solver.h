@@ -65,7 +65,7 @@ class Solver {
 
   // ---- bench / profiling (include/vrod_bench.h) ----
   enum Category { CAT_PREDICT = 0, CAT_COLLIDE, CAT_EXT_SETUP, CAT_EXT_SOLVE, CAT_ROD_SWEEP, CAT_SHAPE, CAT_REPORT,
-                  kCategories };
+                  CAT_ITERATE, kCategories };
   // steps graph replays, each bracketed by CUDA events on the solver stream; an L2-flushing
   // memset of flush_bytes runs (untimed) before every step. Returns summed device ms.
   double bench_run(int steps, long long flush_bytes);
@@ -108,6 +108,16 @@ class Solver {
   bool use_graph_ = true;
   // programmatic dependent launch in the iteration loop (VROD_PDL=0 disables, for A/B runs)
   bool pdl_ = !(std::getenv("VROD_PDL") && std::getenv("VROD_PDL")[0] == '0');
+  // Persistent iteration kernel for small single-scene worlds (VROD_PERSIST=0 disables it).
+  bool persist_ok_ = !(std::getenv("VROD_PERSIST") && std::getenv("VROD_PERSIST")[0] == '0');
+  int persist_tiles_ = 0;
+  double* xrec2_ = nullptr;          // ping-pong partner of w_.xrec (persistent kernel)
+  double* ext_lam2_ = nullptr;       // ping-pong partner of c_.ext_lam
+  unsigned* d_bar_ = nullptr;        // grid-barrier counter
+  unsigned long long* d_trace_ = nullptr;  // VROD_TRACE=1: persistent-kernel phase timestamps
+ public:
+  int trace(long long* out, int cap);
+ private:
 
   cudaStream_t stream_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;

@@ -15,6 +15,7 @@
 // No atomics on the data path: the reduction order is fixed, the result is bitwise
 // deterministic run to run. There is no colouring — Jacobi snapshot semantics
 // exactly as the reference (test_sweep.cpp:132-142).
+#include "ext.cuh"
 #include "kernels.cuh"
 #include "vmath.cuh"
 
@@ -33,42 +34,6 @@ __device__ __forceinline__ double F(const double* a, int f, int vpad, int i) {
 __device__ __forceinline__ V3 ldc(const double* X, int vp, int v) { return V3{F(X, CX, vp, v), F(X, CY, vp, v), F(X, CZ, vp, v)}; }
 
 // ---- external blocks ----------------------------------------------------------------------
-
-struct ExtGeom {  // resolve_pill, constraints.cpp:76-97
-  V3 c0, c1;
-  double r0, r1, rb0, rb1;
-  int v0;
-};
-// resolve from the slot records (World::xrec): two 64-byte records per rod pill
-__device__ __forceinline__ ExtGeom resolve_rec(const World& w, const Collide& c, int pill, int v, double (&ic)[2],
-                                               double (&is)[2]) {
-  ExtGeom g;
-  if (v >= 0) {
-    const double4* r0 = reinterpret_cast<const double4*>(w.xrec + 8ll * v);
-    const double4 a = r0[0], b = r0[1], d = r0[2], e = r0[3];
-    g.c0 = V3{a.x, a.y, a.z};
-    g.c1 = V3{d.x, d.y, d.z};
-    g.rb0 = b.x;
-    g.rb1 = e.x;
-    g.r0 = a.w * g.rb0;
-    g.r1 = d.w * g.rb1;
-    g.v0 = v;
-    ic[0] = b.y;
-    ic[1] = e.y;
-    is[0] = b.z;
-    is[1] = e.z;
-  } else {
-    const int P = c.P;
-    g.c0 = V3{c.pill[pill], c.pill[P + pill], c.pill[2 * P + pill]};
-    g.c1 = V3{c.pill[3 * P + pill], c.pill[4 * P + pill], c.pill[5 * P + pill]};
-    g.r0 = c.pill[6 * P + pill];
-    g.r1 = c.pill[7 * P + pill];
-    g.rb0 = g.rb1 = 0.0;
-    g.v0 = -1;
-    ic[0] = ic[1] = is[0] = is[1] = 0.0;
-  }
-  return g;
-}
 
 // resolve with the pill's first slot known (v = pill + rod, or -1 for a kinematic pill)
 __device__ __forceinline__ ExtGeom resolve_at(const World& w, const Collide& c, const double* X, int pill, int v) {
@@ -120,26 +85,16 @@ __device__ double ext_residual(const World& w, const Collide& c, const double* X
   return dot(V3{pl[0], pl[1], pl[2]}, ldc(X, vp, v)) - pl[3] - F(X, S, vp, v) * F(w.vstat, RBAR, vp, v);
 }
 
-// Scene of external block b (batch only).
-__device__ __forceinline__ int ext_scene(const World& w, const Collide& c, int b, int npins, int nct) {
-  if (b < npins) return w.rod_scene[w.slot_rod[c.pin_slot[b]]];
-  if (b < npins + nct) return c.pill_scene[c.ct_a[b - npins]];
-  return c.plane_scene[c.hp_plane[b - npins - nct]];
-}
-
 __global__ void __launch_bounds__(256, 3) k_ext_solve(World w, Collide c, const double* __restrict__ X,
                                                      SweepParams sp, int* singular, unsigned long long* err) {
   if (sp.pdl) {
     pdl_wait();
     pdl_trigger();
   }
-  const double contact_k = sp.contact_k;
   const int elastic_blocks = sp.elastic_blocks;
   const int npins = sp.n_pins;
   const int nct = c.scalars[SC_NCT];
   const int n = npins + nct + c.scalars[SC_NHP];
-  const int vp = w.vpad;
-  const double h2 = sp.h2;
   int nsing = 0;
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) {
     double* lam = c.ext_lam + 3ll * b;
@@ -158,155 +113,12 @@ __global__ void __launch_bounds__(256, 3) k_ext_solve(World w, Collide c, const 
         o[0].x = ext_none();
       }
     };
-    auto put = [&](int e, int flag, double x, double y, double z, double ds) {
+    const ExtResult r = ext_block(w, c, X, w.xrec, lam, b, sp, [&](int e, int flag, double x, double y, double z, double ds) {
       put_at(c.ext_pos[4 * b + e], flag, x, y, z, ds);
-    };
-    bool active = false, finite = true;
-    if (b < npins) {  // kPin (constraints.cpp:261-267), dim 3
-      const int v = c.pin_slot[b];
-      const double* pd = c.pin_data + 4 * b;
-      const V3 x = ldc(X, vp, v);
-      const double W[3] = {x.x - pd[0], x.y - pd[1], x.z - pd[2]};
-      const double ic = F(w.vstat, IC, vp, v);
-      double M[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-      if (ic != 0.0) {
-        const double s = h2 * ic;
-        M[0][0] = s;
-        M[1][1] = s;
-        M[2][2] = s;
-      }
-      const double kinv = inverse_stiffness(pd[3]);
-      double rhs[3], dl[3];
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        M[d][d] = M[d][d] + kinv;
-        rhs[d] = W[d] - kinv * lam[d];
-      }
-      if (!solve3(M, rhs, sp.beta, dl)) {
-        sing();
-        put(0, 0, 0, 0, 0, 0);
-      } else {
-        active = true;
-        const double f = -h2 * ic;
-        double o[3];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          lam[d] = lam[d] + dl[d];
-          o[d] = f * dl[d];
-          finite = finite && isfinite(dl[d]) && isfinite(o[d]);
-        }
-        put(0, kExtCenter, o[0], o[1], o[2], 0.0);
-      }
-    } else if (b < npins + nct) {  // kContact (constraints.cpp:215-247), unilateral, dim 1
-      const int k = b - npins;
-      // endpoint slots were stored by k_ext_count: the slot records are one dependent load away
-      double icA[2], isA[2], icB[2], isB[2];
-      const ExtGeom A = resolve_rec(w, c, c.ct_a[k], c.ct_va[k], icA, isA);
-      const ExtGeom B = resolve_rec(w, c, c.ct_b[k], c.ct_vb[k], icB, isB);
-      const double al = c.ct_alpha[k], be = c.ct_beta[k];
-      const V3 ca = (1.0 - al) * A.c0 + al * A.c1;
-      const V3 cb = (1.0 - be) * B.c0 + be * B.c1;
-      const double ra = (1.0 - al) * A.r0 + al * A.r1;
-      const double rb = (1.0 - be) * B.r0 + be * B.r1;
-      V3 nrm = ca - cb;
-      const double dist = norm(nrm);
-      const bool live = dist >= 1e-12;
-      double W = 0.0;
-      if (live) {
-        nrm = nrm / dist;
-        W = dist - ra - rb;
-      }
-      const bool entry[4] = {A.v0 >= 0, A.v0 >= 0, B.v0 >= 0, B.v0 >= 0};
-      const int slot[4] = {A.v0, A.v0 + 1, B.v0, B.v0 + 1};
-      const double icv[4] = {icA[0], icA[1], icB[0], icB[1]}, isv[4] = {isA[0], isA[1], isB[0], isB[1]};
-      int qpos[4] = {0, 0, 0, 0};
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (entry[e]) qpos[e] = c.ext_pos[4 * b + e];
-      bool wrote[4] = {false, false, false, false};
-      if (!(W >= 0.0 && lam[0] == 0.0)) {
-        const double coef[4] = {1.0 - al, al, -(1.0 - be), -be};
-        const double sj[4] = {-(1.0 - al) * A.rb0, -al * A.rb1, -(1.0 - be) * B.rb0, -be * B.rb1};
-        const bool has[4] = {live && A.v0 >= 0, live && A.v0 >= 0, live && B.v0 >= 0, live && B.v0 >= 0};
-        double M = 0.0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {  // centers
-          if (!has[e]) continue;
-          const double ic = icv[e];
-          if (ic == 0.0) continue;
-          const double s = h2 * ic;
-          const V3 j = coef[e] * nrm;
-          M = M + (((s * j.x) * j.x + (s * j.y) * j.y) + (s * j.z) * j.z);
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {  // scales
-          if (!has[e]) continue;
-          const double is = isv[e];
-          if (is == 0.0) continue;
-          M = M + (h2 * is * sj[e]) * sj[e];
-        }
-        const double kinv = inverse_stiffness(contact_k);
-        M = M + kinv;
-        const double rhs = W - kinv * lam[0];
-        if (M <= 1e-250) {
-          sing();
-        } else {
-          double dl = sp.beta * rhs / M;
-          if (lam[0] + dl > 0.0) dl = -lam[0];
-          active = true;
-          lam[0] = lam[0] + dl;
-          finite = isfinite(dl);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            if (!has[e]) continue;
-            const V3 j = coef[e] * nrm;
-            const double fc = -h2 * icv[e];
-            const double ox = fc * (j.x * dl), oy = fc * (j.y * dl), oz = fc * (j.z * dl);
-            const double os = -h2 * isv[e] * (sj[e] * dl);
-            finite = finite && isfinite(ox) && isfinite(oy) && isfinite(oz) && isfinite(os);
-            put_at(qpos[e], kExtCenter | kExtScale, ox, oy, oz, os);
-            wrote[e] = true;
-          }
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (entry[e] && !wrote[e]) put_at(qpos[e], 0, 0, 0, 0, 0);
-    } else {  // kHalfPlane (constraints.cpp:248-260), unilateral, dim 1
-      const int k = b - npins - nct;
-      const int v = c.hp_slot[k];
-      const double* pl = c.planes + 4 * c.hp_plane[k];
-      const V3 n3{pl[0], pl[1], pl[2]};
-      const double rbar = F(w.vstat, RBAR, vp, v);
-      const double W = dot(n3, ldc(X, vp, v)) - pl[3] - F(X, S, vp, v) * rbar;
-      if (!(W >= 0.0 && lam[0] == 0.0)) {
-        const double ic = F(w.vstat, IC, vp, v), is = F(w.vstat, IS, vp, v);
-        double M = 0.0;
-        if (ic != 0.0) {
-          const double s = h2 * ic;
-          M = M + (((s * n3.x) * n3.x + (s * n3.y) * n3.y) + (s * n3.z) * n3.z);
-        }
-        if (is != 0.0) M = M + (h2 * is * -rbar) * -rbar;
-        const double kinv = inverse_stiffness(contact_k);
-        M = M + kinv;
-        const double rhs = W - kinv * lam[0];
-        if (M <= 1e-250) {
-          sing();
-        } else {
-          double dl = sp.beta * rhs / M;
-          if (lam[0] + dl > 0.0) dl = -lam[0];
-          active = true;
-          lam[0] = lam[0] + dl;
-          const double fc = -h2 * ic;
-          const double ox = fc * (n3.x * dl), oy = fc * (n3.y * dl), oz = fc * (n3.z * dl);
-          const double os = -h2 * is * (-rbar * dl);
-          finite = isfinite(dl) && isfinite(ox) && isfinite(oy) && isfinite(oz) && isfinite(os);
-          put(0, kExtCenter | kExtScale, ox, oy, oz, os);
-        }
-      }
-      if (!active) put(0, 0, 0, 0, 0, 0);
-    }
-    if (active && !finite)
+    });
+    for (int d = 0; d < r.nlam; ++d) lam[d] = r.lam[d];
+    if (r.singular) sing();
+    if (r.bad)
       atomicMin(err, err_code(sp.substep, ERR_SWEEP, sp.iter, static_cast<unsigned long long>(elastic_blocks) + b));
   }
   for (int o = 16; o > 0; o >>= 1) nsing += __shfl_down_sync(0xffffffffu, nsing, o);

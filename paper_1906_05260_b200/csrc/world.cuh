@@ -29,8 +29,10 @@ enum EStatField : int {
   A2E,      // pi * rmid^2
   A4EP,     // 0.25 * pi * pow(rmid, 4)   (refresh_stiffness form, constraints.cpp:352)
   A4VP,     // 0.25 * pi * pow(r_k, 4) of vertex k (constraints.cpp:357,363)
-  KSZ, KCS, KSS, KVS,     // element-pass stiffness (StretchZ/VolumeStretch are Constant)
-  KBT0, KBT1, KBT2, KSB, KVB,  // vertex-pass stiffness of vertex k (VolumeBendU == V)
+  // Stiffness rows hold the INVERSE stiffness inverse_stiffness(k) (constraints.cpp:274-278),
+  // computed once at setup / on activation refresh instead of once per block per sweep.
+  KSZ, KCS, KSS, KVS,     // element-pass (StretchZ/VolumeStretch are Constant)
+  KBT0, KBT1, KBT2, KSB, KVB,  // vertex-pass of vertex k (VolumeBendU == V; KBT1 == KBT0 always)
   ITX, ITY, ITZ,          // inverse theta weights (refreshed every substep)
   TWB,                    // theta weight base rho*s_mid^2*pi*r^4*l0 (weights = 0.25,0.25,0.5 x base)
   kEStatFields

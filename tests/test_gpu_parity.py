@@ -244,3 +244,36 @@ def test_probe_convergence_matches(gpu, oracle):
     lo = SolverHandle(oracle, scene).probe_convergence(25)
     np.testing.assert_allclose(lg, lo, rtol=1e-12, atol=0)
     assert lg.shape == (25, 8)
+
+
+def _iterate_launches(lib, handle) -> int:
+    """Launch brackets of the persistent iteration kernel (VROD_CAT_ITERATE) over one step."""
+    import ctypes as C
+    lib.vrod_bench_kernel_times.restype = C.c_int
+    lib.vrod_bench_kernel_times.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    ms, ln = (C.c_double * 8)(), (C.c_int64 * 8)()
+    assert lib.vrod_bench_kernel_times(handle._h, 1, ms, ln) == 0
+    return int(ln[7])
+
+
+@pytest.mark.parametrize("name", sorted(SCENES))
+def test_persistent_kernel_matches_per_launch_path(gpu, oracle, name, monkeypatch):
+    """Small single-scene worlds run the whole iteration loop as one persistent kernel
+    (rodsweep.cu k_iterate); VROD_PERSIST=0 forces the per-sweep launches. Both paths share
+    every block formula, so they must agree BIT FOR BIT — shape-matching scenes included —
+    on states, reports and contacts, step after step."""
+    scene = SCENES[name](oracle)
+    a = SolverHandle(gpu, scene)
+    monkeypatch.setenv("VROD_PERSIST", "0")
+    b = SolverHandle(gpu, scene)
+    monkeypatch.delenv("VROD_PERSIST")
+    for _ in range(3):
+        ra, rb = a.step(), b.step()
+        assert (ra.contact_count, ra.broad_pairs, ra.skipped_singular) == (rb.contact_count, rb.broad_pairs, rb.skipped_singular)
+        assert ra.max_penetration == rb.max_penetration
+        np.testing.assert_array_equal(ra.residuals, rb.residuals)
+        sa, sb = a.state(), b.state()
+        for k in sa:
+            np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
+    assert _iterate_launches(gpu, b) == 0
+    assert _iterate_launches(gpu, a) > 0  # the persistent path really ran
