@@ -572,11 +572,13 @@ __device__ __forceinline__ void gather_apply(const Tile<TP>& t, const World& w, 
   constexpr int kTileOwned = TP - 2;
   const int vp = w.vpad;
   const int tid = threadIdx.x, lane = tid & 31;
-  // Two threads per slot (adjacent warps): role 0 gathers and applies the center and scale
-  // (elastic + external blocks), role 1 the frame (elastic blocks only; external blocks have no
-  // theta slots) — two shorter dependency chains instead of one.
-  const int role = (tid >> 5) & 1;
-  for (int pi = 1 + lane + 32 * (tid >> 6); pi <= kTileOwned; pi += 16 * kWarps) {
+  // Small (latency-bound) tiles: two threads per slot (adjacent warps), role 0 gathers and
+  // applies the center and scale (elastic + external blocks), role 1 the frame (elastic blocks
+  // only; external blocks have no theta slots) — two shorter dependency chains instead of one.
+  // Large (issue-bound) tiles: one thread per slot does all three (role 2).
+  constexpr bool kSplit = TP == 32;
+  const int role = kSplit ? (tid >> 5) & 1 : 2;
+  for (int pi = kSplit ? 1 + lane + 32 * (tid >> 6) : 1 + tid; pi <= kTileOwned; pi += kSplit ? 16 * kWarps : 32 * kWarps) {
     const int k = t.loc[pi];
     if (k < 0) continue;
     const int p = start - 1 + pi;
@@ -594,17 +596,17 @@ __device__ __forceinline__ void gather_apply(const Tile<TP>& t, const World& w, 
     V3 tsum{0, 0, 0};
     int tcnt = 0;
     auto addc = [&](const double* d) {
-      if (role != 0) return;
+      if (role == 1) return;
       csum = csum + V3{d[0], d[1], d[2]};
       ++ccnt;
     };
     auto adds = [&](double d) {
-      if (role != 0) return;
+      if (role == 1) return;
       ssum += d;
       ++scnt;
     };
     auto addt = [&](const double* d) {
-      if (role != 1) return;
+      if (role == 0) return;
       tsum = tsum + V3{d[0], d[1], d[2]};
       ++tcnt;
     };
@@ -654,7 +656,7 @@ __device__ __forceinline__ void gather_apply(const Tile<TP>& t, const World& w, 
       if (t.act[A_VBU][pi + 1]) addt(N.vb_dta[0]);
       if (t.act[A_VBV][pi + 1]) addt(N.vb_dta[1]);
     }
-    if (role == 0) {
+    if (role != 1) {
       ext(p, addc, adds);
       V3 cn{t.st[T_CX][si], t.st[T_CY][si], t.st[T_CZ][si]};
       if (ccnt > 0) cn = cn + csum / static_cast<double>(ccnt);
@@ -669,7 +671,8 @@ __device__ __forceinline__ void gather_apply(const Tile<TP>& t, const World& w, 
         xr[0] = make_double2(cn.x, cn.y);
         xr[1] = make_double2(cn.z, sn);
       }
-    } else {
+    }
+    if (role != 0) {
       Q4 qn{t.st[T_QW][si], t.st[T_QX][si], t.st[T_QY][si], t.st[T_QZ][si]};
       if (has_el && tcnt > 0) qn = apply_increment(qn, tsum / static_cast<double>(tcnt));
       Y[QW * (long long)vp + p] = qn.w;

@@ -189,22 +189,38 @@ __global__ void k_ext_fill(Collide c, int npins) {
     }
   }
 }
+// Orders each slot's incidence entries by (block, endpoint): one warp per slot; up to 32 entries
+// are ranked in registers (keys are distinct), longer lists fall back to an insertion sort.
 __global__ void k_ext_sort(Collide c, int V) {
   pdl_wait();
   pdl_trigger();
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= V) return;
-  const int s0 = c.ext_off[v], s1 = c.ext_off[v + 1];
-  for (int a = s0 + 1; a < s1; ++a) {  // insertion sort: block order, then endpoint
-    const int key = c.ext_items[a];
-    int b = a - 1;
-    while (b >= s0 && c.ext_items[b] > key) {
-      c.ext_items[b + 1] = c.ext_items[b];
-      --b;
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < V; v += warps) {
+    const int s0 = c.ext_off[v], s1 = c.ext_off[v + 1], n = s1 - s0;
+    if (n <= 0) continue;
+    if (n <= 32) {
+      const int key = lane < n ? c.ext_items[s0 + lane] : 0x7fffffff;
+      int rank = 0;
+      for (int j = 0; j < n; ++j) rank += __shfl_sync(0xffffffffu, key, j) < key ? 1 : 0;
+      __syncwarp();
+      if (lane < n) {
+        c.ext_items[s0 + rank] = key;
+        c.ext_pos[key] = s0 + rank;
+      }
+    } else if (lane == 0) {
+      for (int a = s0 + 1; a < s1; ++a) {  // insertion sort: block order, then endpoint
+        const int key = c.ext_items[a];
+        int b = a - 1;
+        while (b >= s0 && c.ext_items[b] > key) {
+          c.ext_items[b + 1] = c.ext_items[b];
+          --b;
+        }
+        c.ext_items[b + 1] = key;
+      }
+      for (int a = s0; a < s1; ++a) c.ext_pos[c.ext_items[a]] = a;
     }
-    c.ext_items[b + 1] = key;
   }
-  for (int a = s0; a < s1; ++a) c.ext_pos[c.ext_items[a]] = a;
 }
 
 // ---- end-of-substep report (elastic_residual_norms, constraints.cpp:558-596, and
@@ -406,7 +422,7 @@ void launch_ext_setup(const World& w, Collide& c, cudaStream_t st) {
   launch_kernel(k_ext_count, g, kThreads, 0, st, g_pdl, c, c.n_pins);
   scan_exclusive(c.ext_cnt, c.ext_off, w.V, nullptr, c.scan_tmp, c.scan_parts, st);
   launch_kernel(k_ext_fill, g, kThreads, 0, st, g_pdl, c, c.n_pins);
-  launch_kernel(k_ext_sort, (w.V + kThreads - 1) / kThreads, kThreads, 0, st, g_pdl, c, w.V);
+  launch_kernel(k_ext_sort, grid_for(32ll * w.V), kThreads, 0, st, g_pdl, c, w.V);
 }
 
 void launch_ext_solve(const World& w, Collide& c, const double* X, const SweepParams& sp, int* singular_counter,
