@@ -239,6 +239,50 @@ int vrod_solver_scene_count(const vrod_solver* solver, int32_t* count);
  * returns). capacity >= scene count. */
 int vrod_solver_scene_reports(const vrod_solver* solver, int32_t capacity, vrod_step_report* reports);
 
+/* ---- skinning (skinning.h / skinning.cpp): the consumer of the step's output, SURVEY.md §8(f)
+ * rows 2-3. The CLI flow (vrod_main.cpp:52-73) is: rest pills + rest transforms of the rods ->
+ * bind_skin -> smooth_binding, then every frame deform_mesh(binding, solver.pill_transforms()). */
+
+/* PillTransform (skinning.h:19-25): element midpoint center, midpoint scale, element frame. */
+typedef struct vrod_pill_transform {
+  double center[3];
+  double scale;
+  double rotation[4]; /* w, x, y, z */
+} vrod_pill_transform;
+
+/* Solver::pill_transforms() = rod_pill_transforms(rods) of the live state (solver.cpp:438-440,
+ * skinning.cpp:9-22): rod pills in rod-major, element-major order. */
+int vrod_solver_pill_transforms(vrod_solver* solver, int64_t capacity, int64_t* count,
+                                vrod_pill_transform* out);
+/* rod_rest_pill_transforms / rod_rest_pills of the solver's rods (skinning.cpp:24-57): the
+ * bind-time inputs (rest centers, rest scales x radii). */
+int vrod_solver_rest_pill_transforms(vrod_solver* solver, int64_t capacity, int64_t* count,
+                                     vrod_pill_transform* out);
+int vrod_solver_rest_pills(vrod_solver* solver, int64_t capacity, int64_t* count, vrod_pill* out);
+
+/* SkinBinding (skinning.h:31-40) together with the TriMesh it was bound to. */
+typedef struct vrod_skin vrod_skin;
+/* bind_skin(mesh, rest_pills, rest_transforms, max_influences, epsilon), skinning.cpp:59-105:
+ * inverse-square surface-distance weights (pill_project), top max_influences per vertex with
+ * ties by pill index, renormalized, listed by pill index. vertices: 3 per vertex; triangles:
+ * 3 vertex ids each (used by smoothing; may be 0 triangles). */
+int vrod_skin_bind(int32_t vertex_count, const double* vertices, int32_t triangle_count, const int32_t* triangles,
+                   int32_t pill_count, const vrod_pill* rest_pills, const vrod_pill_transform* rest_transforms,
+                   int32_t max_influences, double epsilon, vrod_skin** out);
+void vrod_skin_destroy(vrod_skin* skin);
+/* smooth_binding(binding, mesh, iterations), skinning.cpp:107-163. */
+int vrod_skin_smooth(vrod_skin* skin, int32_t iterations);
+/* The binding's CSR: offsets (vertex_count + 1), pills and weights (nnz each); any pointer may
+ * be NULL; *nnz and *clamped_vertices always written. */
+int vrod_skin_get_binding(const vrod_skin* skin, int32_t* offsets, int32_t* pills, double* weights, int32_t* nnz,
+                          int32_t* clamped_vertices);
+/* deform_mesh(binding, current, rest_mesh, out), skinning.cpp:165-185: out = 3 per vertex. */
+int vrod_skin_deform(vrod_skin* skin, int32_t pill_count, const vrod_pill_transform* current, double* out_vertices);
+/* The per-frame path on one device: pill transforms of the solver's live state, then the
+ * deformation, without a host round trip of the transforms. out_vertices may be NULL (result
+ * stays on the device, for timing). */
+int vrod_skin_deform_solver(vrod_skin* skin, vrod_solver* solver, double* out_vertices);
+
 /* ---- fine-grained (kernel-level) boundary, on host arrays ------------------------------ */
 
 /* pill_project(x, pill), collision.h:64 / collision.cpp:15-49 — n independent queries. */

@@ -6,6 +6,7 @@
 // C++ API directly (vrod::Scene, vrod::Solver, broad_phase, ...), so tests and bench.py can
 // drive the reference exactly like the product. Never shipped, never on the product path.
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -22,6 +23,7 @@
 #include "vrod/layout.h"
 #include "vrod/rod.h"
 #include "vrod/scene.h"
+#include "vrod/skinning.h"
 #include "vrod_capi.h"
 
 using namespace vrod;
@@ -94,6 +96,10 @@ vrod_pill from_pill(const Pill& p) {
 struct vrod_scene {
   Scene scene;
 };
+struct vrod_skin {
+  TriMesh mesh;
+  SkinBinding binding;
+};
 // A batch (vrod_batch_create) is N independent reference solvers stepped in lockstep — the
 // reference has no batch API of its own.
 struct vrod_solver {
@@ -128,6 +134,23 @@ void put_report(const StepReport& r, vrod_step_report* out) {
   out->solve_ms = r.timings.solve_ms;
   out->finalize_ms = r.timings.finalize_ms;
   out->total_ms = r.timings.total_ms;
+}
+void put_transform(const PillTransform& t, vrod_pill_transform* o) {
+  put3(o->center, t.center);
+  o->scale = t.scale;
+  put4(o->rotation, t.rotation);
+}
+PillTransform to_transform(const vrod_pill_transform& t) {
+  PillTransform o;
+  o.center = v3(t.center);
+  o.scale = t.scale;
+  o.rotation = q4(t.rotation);
+  return o;
+}
+template <class T, class Put>
+void put_list(const std::vector<T>& v, int64_t cap, int64_t* count, Put&& put) {
+  for (std::size_t i = 0; i < v.size() && static_cast<int64_t>(i) < cap; ++i) put(v[i], i);
+  *count = static_cast<int64_t>(v.size());
 }
 }  // namespace
 
@@ -596,6 +619,71 @@ int vrod_find_contacts(int64_t n, const vrod_pill* pills, int64_t npairs, const 
       dist[k] = out[k].distance;
     }
     *count = static_cast<int64_t>(out.size());
+  });
+}
+
+int vrod_solver_pill_transforms(vrod_solver* s, int64_t cap, int64_t* count, vrod_pill_transform* out) {
+  return guarded([&] {
+    put_list(one(s).pill_transforms(), cap, count, [&](const PillTransform& t, std::size_t i) { put_transform(t, out + i); });
+  });
+}
+int vrod_solver_rest_pill_transforms(vrod_solver* s, int64_t cap, int64_t* count, vrod_pill_transform* out) {
+  return guarded([&] {
+    put_list(rod_rest_pill_transforms(one(s).scene().rods), cap, count,
+             [&](const PillTransform& t, std::size_t i) { put_transform(t, out + i); });
+  });
+}
+int vrod_solver_rest_pills(vrod_solver* s, int64_t cap, int64_t* count, vrod_pill* out) {
+  return guarded([&] {
+    put_list(rod_rest_pills(one(s).scene().rods), cap, count, [&](const Pill& p, std::size_t i) { out[i] = from_pill(p); });
+  });
+}
+int vrod_skin_bind(int32_t nv, const double* verts, int32_t nt, const int32_t* tris, int32_t np, const vrod_pill* pills,
+                   const vrod_pill_transform* rest, int32_t max_influences, double epsilon, vrod_skin** out) {
+  return guarded([&] {
+    auto sk = std::make_unique<vrod_skin>();
+    for (int32_t v = 0; v < nv; ++v) sk->mesh.vertices.push_back(v3(verts + 3 * v));
+    for (int32_t t = 0; t < nt; ++t) sk->mesh.triangles.push_back({tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]});
+    std::vector<Pill> p;
+    std::vector<PillTransform> tr;
+    for (int32_t i = 0; i < np; ++i) {
+      p.push_back(to_pill(pills[i]));
+      tr.push_back(to_transform(rest[i]));
+    }
+    sk->binding = bind_skin(sk->mesh, p, tr, max_influences, epsilon);
+    *out = sk.release();
+  });
+}
+void vrod_skin_destroy(vrod_skin* sk) { delete sk; }
+int vrod_skin_smooth(vrod_skin* sk, int32_t iterations) {
+  return guarded([&] { smooth_binding(sk->binding, sk->mesh, iterations); });
+}
+int vrod_skin_get_binding(const vrod_skin* sk, int32_t* offsets, int32_t* pills, double* weights, int32_t* nnz,
+                          int32_t* clamped) {
+  return guarded([&] {
+    const SkinBinding& b = sk->binding;
+    if (offsets) std::copy(b.offsets.begin(), b.offsets.end(), offsets);
+    if (pills) std::copy(b.pills.begin(), b.pills.end(), pills);
+    if (weights) std::copy(b.weights.begin(), b.weights.end(), weights);
+    *nnz = static_cast<int32_t>(b.pills.size());
+    *clamped = b.clamped_vertices;
+  });
+}
+int vrod_skin_deform(vrod_skin* sk, int32_t np, const vrod_pill_transform* cur, double* out) {
+  return guarded([&] {
+    std::vector<PillTransform> tr;
+    for (int32_t i = 0; i < np; ++i) tr.push_back(to_transform(cur[i]));
+    std::vector<Vec3> o;
+    deform_mesh(sk->binding, tr, sk->mesh, o);
+    for (std::size_t v = 0; v < o.size(); ++v) put3(out + 3 * v, o[v]);
+  });
+}
+int vrod_skin_deform_solver(vrod_skin* sk, vrod_solver* s, double* out) {
+  return guarded([&] {
+    std::vector<Vec3> o;
+    deform_mesh(sk->binding, one(s).pill_transforms(), sk->mesh, o);
+    if (out)
+      for (std::size_t v = 0; v < o.size(); ++v) put3(out + 3 * v, o[v]);
   });
 }
 

@@ -9,6 +9,7 @@
 // and bench.py's cpu_baseline leg load it — never the product path.
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -1844,6 +1845,158 @@ int guarded(Fn&& fn) {
     return VROD_RUNTIME_ERROR;
   }
 }
+// ---- skinning (skinning.cpp) ------------------------------------------------------------
+
+struct PillTransform {  // skinning.h:19-25
+  V3 center{0, 0, 0};
+  double scale = 1.0;
+  Q rotation{1, 0, 0, 0};
+};
+// rod_pill_transforms, skinning.cpp:9-22.
+std::vector<PillTransform> rod_pill_transforms(const std::vector<Rod>& rods) {
+  std::vector<PillTransform> out;
+  for (const Rod& rod : rods)
+    for (int e = 0; e < rod.rest.m(); ++e)
+      out.push_back({mul(0.5, add(rod.st.c[e], rod.st.c[e + 1])), 0.5 * (rod.st.s[e] + rod.st.s[e + 1]), rod.st.q[e]});
+  return out;
+}
+// rod_rest_pill_transforms, skinning.cpp:24-37.
+std::vector<PillTransform> rod_rest_pill_transforms(const std::vector<Rod>& rods) {
+  std::vector<PillTransform> out;
+  for (const Rod& rod : rods)
+    for (int e = 0; e < rod.rest.m(); ++e)
+      out.push_back({mul(0.5, add(rod.rest.c[e], rod.rest.c[e + 1])), 0.5 * (rod.rest.s[e] + rod.rest.s[e + 1]),
+                     rod.rest.q[e]});
+  return out;
+}
+// rod_rest_pills, skinning.cpp:39-57.
+std::vector<Pill> rod_rest_pills(const std::vector<Rod>& rods) {
+  std::vector<Pill> out;
+  for (int r = 0; r < static_cast<int>(rods.size()); ++r) {
+    const Rod& rod = rods[r];
+    for (int e = 0; e < rod.rest.m(); ++e) {
+      Pill p;
+      p.c0 = rod.rest.c[e];
+      p.c1 = rod.rest.c[e + 1];
+      p.r0 = rod.rest.s[e] * rod.rest.r[e];
+      p.r1 = rod.rest.s[e + 1] * rod.rest.r[e + 1];
+      p.rod = r;
+      p.element = e;
+      out.push_back(p);
+    }
+  }
+  return out;
+}
+struct SkinBinding {  // skinning.h:31-40
+  std::vector<int> offsets, pills;
+  std::vector<double> weights;
+  std::vector<PillTransform> rest;
+  int max_influences = 8;
+  int clamped_vertices = 0;
+};
+struct TriMesh {
+  std::vector<V3> vertices;
+  std::vector<std::array<int, 3>> triangles;
+};
+// Top-`keep` selection of partial_sort (score descending, pill ascending), renormalized over the
+// kept scores in that order, then listed by pill (skinning.cpp:80-93, 145-157).
+void keep_top(std::vector<std::pair<double, int>>& scored, int max_influences, SkinBinding& b) {
+  const int keep = std::min<int>(max_influences, static_cast<int>(scored.size()));
+  std::partial_sort(scored.begin(), scored.begin() + keep, scored.end(), [](const auto& x, const auto& y) {
+    return x.first != y.first ? x.first > y.first : x.second < y.second;
+  });
+  double total = 0.0;
+  for (int k = 0; k < keep; ++k) total += scored[k].first;
+  std::sort(scored.begin(), scored.begin() + keep, [](const auto& x, const auto& y) { return x.second < y.second; });
+  for (int k = 0; k < keep; ++k) {
+    b.pills.push_back(scored[k].second);
+    b.weights.push_back(scored[k].first / total);
+  }
+}
+// bind_skin, skinning.cpp:59-105.
+SkinBinding bind_skin(const TriMesh& mesh, const std::vector<Pill>& pills, const std::vector<PillTransform>& rest,
+                      int max_influences, double epsilon) {
+  require(!pills.empty(), "skin binding needs at least one pill");
+  require(pills.size() == rest.size(), "pill list and transform list must match");
+  require(max_influences >= 1, "max_influences must be at least 1");
+  require(epsilon > 0.0, "epsilon must be positive");
+  SkinBinding b;
+  b.max_influences = max_influences;
+  b.rest = rest;
+  const int nv = static_cast<int>(mesh.vertices.size()), np = static_cast<int>(pills.size());
+  b.offsets.assign(nv + 1, 0);
+  std::vector<std::pair<double, int>> scored(np);
+  for (int v = 0; v < nv; ++v) {
+    bool clamped = false;
+    for (int p = 0; p < np; ++p) {
+      const double d = pill_project(mesh.vertices[v], pills[p]).d;
+      if (d < epsilon) clamped = clamped || d < 0.0;
+      const double dc = std::max(d, epsilon);
+      scored[p] = {1.0 / (dc * dc), p};
+    }
+    if (clamped) ++b.clamped_vertices;
+    keep_top(scored, max_influences, b);
+    b.offsets[v + 1] = static_cast<int>(b.pills.size());
+  }
+  return b;
+}
+// smooth_binding, skinning.cpp:107-163.
+void smooth_binding(SkinBinding& b, const TriMesh& mesh, int iterations) {
+  if (iterations <= 0) return;
+  const int nv = static_cast<int>(mesh.vertices.size());
+  std::vector<std::vector<int>> nb(nv);
+  for (const auto& tri : mesh.triangles)
+    for (int k = 0; k < 3; ++k) {
+      const int a = tri[k], c = tri[(k + 1) % 3];
+      nb[a].push_back(c);
+      nb[c].push_back(a);
+    }
+  for (auto& l : nb) {
+    std::sort(l.begin(), l.end());
+    l.erase(std::unique(l.begin(), l.end()), l.end());
+  }
+  for (int it = 0; it < iterations; ++it) {
+    SkinBinding n;
+    n.offsets.push_back(0);
+    for (int v = 0; v < nv; ++v) {
+      std::map<int, double> blended;
+      for (int k = b.offsets[v]; k < b.offsets[v + 1]; ++k) blended[b.pills[k]] += 0.5 * b.weights[k];
+      if (!nb[v].empty()) {
+        const double share = 0.5 / nb[v].size();
+        for (int u : nb[v])
+          for (int k = b.offsets[u]; k < b.offsets[u + 1]; ++k) blended[b.pills[k]] += share * b.weights[k];
+      } else {
+        for (int k = b.offsets[v]; k < b.offsets[v + 1]; ++k) blended[b.pills[k]] += 0.5 * b.weights[k];
+      }
+      std::vector<std::pair<double, int>> scored;
+      for (const auto& [p, w] : blended) scored.push_back({w, p});
+      keep_top(scored, b.max_influences, n);
+      n.offsets.push_back(static_cast<int>(n.pills.size()));
+    }
+    b.offsets = std::move(n.offsets);
+    b.pills = std::move(n.pills);
+    b.weights = std::move(n.weights);
+  }
+}
+// deform_mesh, skinning.cpp:165-185 (Eigen: conj(q) * v is _transformVector of the conjugate).
+void deform_mesh(const SkinBinding& b, const std::vector<PillTransform>& cur, const TriMesh& mesh, std::vector<V3>& out) {
+  require(cur.size() == b.rest.size(), "transform count changed since binding");
+  const int nv = static_cast<int>(mesh.vertices.size());
+  require(static_cast<int>(b.offsets.size()) == nv + 1, "binding does not match mesh");
+  out.assign(nv, V3{0, 0, 0});
+  for (int v = 0; v < nv; ++v) {
+    const V3& rest = mesh.vertices[v];
+    V3 blended{0, 0, 0};
+    for (int k = b.offsets[v]; k < b.offsets[v + 1]; ++k) {
+      const PillTransform& c = cur[b.pills[k]];
+      const PillTransform& r = b.rest[b.pills[k]];
+      const V3 local = qrot(qconj(r.rotation), sub(rest, r.center));
+      blended = add(blended, mul(b.weights[k], add(c.center, mul(c.scale / r.scale, qrot(c.rotation, local)))));
+    }
+    out[v] = blended;
+  }
+}
+
 V3 v3(const double* p) { return V3{p[0], p[1], p[2]}; }
 Q q4(const double* p) { return Q{p[0], p[1], p[2], p[3]}; }
 void put3(double* p, const V3& v) {
@@ -1886,6 +2039,10 @@ vrod_pill from_pill(const Pill& p) {
 
 struct vrod_scene {
   Scene scene;
+};
+struct vrod_skin {
+  TriMesh mesh;
+  SkinBinding binding;
 };
 // A batch (vrod_batch_create) is N independent reference solvers stepped in lockstep.
 struct vrod_solver {
@@ -2342,5 +2499,89 @@ int vrod_find_contacts(int64_t n, const vrod_pill* pills, int64_t np, const int3
   });
 }
 uint64_t vrod_pair_key(const vrod_pill* a, const vrod_pill* b) { return pair_key(to_pill(*a), to_pill(*b)); }
+
+}  // extern "C"
+
+namespace {
+
+void put_transform(const PillTransform& t, vrod_pill_transform* o) {
+  put3(o->center, t.center);
+  o->scale = t.scale;
+  put4(o->rotation, t.rotation);
+}
+PillTransform to_transform(const vrod_pill_transform& t) { return {v3(t.center), t.scale, q4(t.rotation)}; }
+}  // namespace
+
+extern "C" {
+
+int vrod_solver_pill_transforms(vrod_solver* s, int64_t cap, int64_t* count, vrod_pill_transform* out) {
+  return guarded([&] {
+    const auto v = rod_pill_transforms(one(s).s_.rods);
+    for (std::size_t i = 0; i < v.size() && static_cast<int64_t>(i) < cap; ++i) put_transform(v[i], out + i);
+    *count = static_cast<int64_t>(v.size());
+  });
+}
+int vrod_solver_rest_pill_transforms(vrod_solver* s, int64_t cap, int64_t* count, vrod_pill_transform* out) {
+  return guarded([&] {
+    const auto v = rod_rest_pill_transforms(one(s).s_.rods);
+    for (std::size_t i = 0; i < v.size() && static_cast<int64_t>(i) < cap; ++i) put_transform(v[i], out + i);
+    *count = static_cast<int64_t>(v.size());
+  });
+}
+int vrod_solver_rest_pills(vrod_solver* s, int64_t cap, int64_t* count, vrod_pill* out) {
+  return guarded([&] {
+    const auto v = rod_rest_pills(one(s).s_.rods);
+    for (std::size_t i = 0; i < v.size() && static_cast<int64_t>(i) < cap; ++i) out[i] = from_pill(v[i]);
+    *count = static_cast<int64_t>(v.size());
+  });
+}
+int vrod_skin_bind(int32_t nv, const double* verts, int32_t nt, const int32_t* tris, int32_t np, const vrod_pill* pills,
+                   const vrod_pill_transform* rest, int32_t max_influences, double epsilon, vrod_skin** out) {
+  return guarded([&] {
+    auto sk = std::make_unique<vrod_skin>();
+    for (int32_t v = 0; v < nv; ++v) sk->mesh.vertices.push_back(v3(verts + 3 * v));
+    for (int32_t t = 0; t < nt; ++t) sk->mesh.triangles.push_back({tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]});
+    std::vector<Pill> p;
+    std::vector<PillTransform> tr;
+    for (int32_t i = 0; i < np; ++i) {
+      p.push_back(to_pill(pills[i]));
+      tr.push_back(to_transform(rest[i]));
+    }
+    sk->binding = bind_skin(sk->mesh, p, tr, max_influences, epsilon);
+    *out = sk.release();
+  });
+}
+void vrod_skin_destroy(vrod_skin* sk) { delete sk; }
+int vrod_skin_smooth(vrod_skin* sk, int32_t iterations) {
+  return guarded([&] { smooth_binding(sk->binding, sk->mesh, iterations); });
+}
+int vrod_skin_get_binding(const vrod_skin* sk, int32_t* offsets, int32_t* pills, double* weights, int32_t* nnz,
+                          int32_t* clamped) {
+  return guarded([&] {
+    const SkinBinding& b = sk->binding;
+    if (offsets) std::copy(b.offsets.begin(), b.offsets.end(), offsets);
+    if (pills) std::copy(b.pills.begin(), b.pills.end(), pills);
+    if (weights) std::copy(b.weights.begin(), b.weights.end(), weights);
+    *nnz = static_cast<int32_t>(b.pills.size());
+    *clamped = b.clamped_vertices;
+  });
+}
+int vrod_skin_deform(vrod_skin* sk, int32_t np, const vrod_pill_transform* cur, double* out) {
+  return guarded([&] {
+    std::vector<PillTransform> tr;
+    for (int32_t i = 0; i < np; ++i) tr.push_back(to_transform(cur[i]));
+    std::vector<V3> o;
+    deform_mesh(sk->binding, tr, sk->mesh, o);
+    for (std::size_t v = 0; v < o.size(); ++v) put3(out + 3 * v, o[v]);
+  });
+}
+int vrod_skin_deform_solver(vrod_skin* sk, vrod_solver* s, double* out) {
+  return guarded([&] {
+    std::vector<V3> o;
+    deform_mesh(sk->binding, rod_pill_transforms(one(s).s_.rods), sk->mesh, o);
+    if (out)
+      for (std::size_t v = 0; v < o.size(); ++v) put3(out + 3 * v, o[v]);
+  });
+}
 
 }  // extern "C"

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 from . import capi, workloads
 from ._lib import LIB_PATH, library
+from .handle import Skin as _SkinHandle
 from .handle import StepReport, SolverHandle
 from .scene import (Activation, Bone, DeviceError, HalfPlane, InvalidArgument, KinematicPill, MaterialParams,
                     OutOfRange, Pill, PinMotion, RigidKeyframe, Rod, RodRestPose, RodState, Scene,
@@ -34,6 +35,25 @@ class BatchSolver(SolverHandle):
         super().__init__(library(), None, _batch=list(scenes))
 
 
+class Skin(_SkinHandle):
+    """bind_skin / smooth_binding / deform_mesh (skinning.h) on the B200. Bind a mesh to a
+    solver's rest pills with `Skin.for_solver(solver, vertices, triangles)`, then every frame
+    `deform_solver(solver)` deforms it from the live state on the device."""
+
+    def __init__(self, vertices, triangles, rest_pills, rest_transforms, max_influences: int = 8,
+                 epsilon: float = 1e-4):
+        super().__init__(library(), vertices, triangles, rest_pills, rest_transforms, max_influences, epsilon)
+
+    @classmethod
+    def for_solver(cls, solver: SolverHandle, vertices, triangles=None, max_influences: int = 8,
+                   epsilon: float = 1e-4, smooth_iterations: int = 0) -> "Skin":
+        """The CLI's binding flow (vrod_main.cpp:52-63)."""
+        sk = cls(vertices, triangles, solver.rest_pills(), solver.rest_pill_transforms(), max_influences, epsilon)
+        if smooth_iterations:
+            sk.smooth(smooth_iterations)
+        return sk
+
+
 def make_rest_pose(centers, radii, scales=None) -> RodRestPose:
     """make_rest_pose (rod.h:88-90), computed by the product's host code."""
     return _scene.make_rest_pose(library(), centers, radii, scales)
@@ -48,7 +68,7 @@ def validate(scene: Scene) -> None:
     _scene.validate(library(), scene)
 
 
-__all__ = ["Solver", "BatchSolver", "Scene", "Rod", "RodRestPose", "RodState", "MaterialParams", "SolverSettings", "HalfPlane",
+__all__ = ["Solver", "BatchSolver", "Skin", "Scene", "Rod", "RodRestPose", "RodState", "MaterialParams", "SolverSettings", "HalfPlane",
            "Pill", "KinematicPill", "Bone", "RigidKeyframe", "PinMotion", "SoftPin", "Activation", "StepReport",
            "make_rest_pose", "make_rest_state", "straight_rod", "validate", "VrodError", "InvalidArgument",
            "OutOfRange", "SimulationError", "DeviceError", "library", "LIB_PATH", "capi", "workloads"]

@@ -47,6 +47,10 @@ PILL_DTYPE = np.dtype([("c0", "<f8", 3), ("c1", "<f8", 3), ("r0", "<f8"), ("r1",
 assert PILL_DTYPE.itemsize == C.sizeof(Pill)
 
 
+# PillTransform (skinning.h:19-25): center xyz, scale, rotation wxyz — 8 doubles.
+TRANSFORM_DTYPE = np.dtype([("center", "<f8", 3), ("scale", "<f8"), ("rotation", "<f8", 4)])
+
+
 class StepReport(C.Structure):
     _fields_ = [("step", C.c_int32), ("contact_count", C.c_int32), ("broad_pairs", C.c_int32),
                 ("skipped_singular", C.c_int32), ("dof_count", C.c_int32), ("pad_", C.c_int32),
@@ -121,6 +125,16 @@ _SIGNATURES = {
     "vrod_find_contacts": (C.c_int, [C.c_int64, C.c_void_p, C.c_int64, _ip, C.c_int32, C.c_int64, _u64p, _dp,
                                      C.c_int64, _i64p, _ip, _ip, _dp, _dp, _dp]),
     "vrod_pair_key": (C.c_uint64, [C.POINTER(Pill), C.POINTER(Pill)]),
+    "vrod_solver_pill_transforms": (C.c_int, [C.c_void_p, C.c_int64, _i64p, C.c_void_p]),
+    "vrod_solver_rest_pill_transforms": (C.c_int, [C.c_void_p, C.c_int64, _i64p, C.c_void_p]),
+    "vrod_solver_rest_pills": (C.c_int, [C.c_void_p, C.c_int64, _i64p, C.c_void_p]),
+    "vrod_skin_bind": (C.c_int, [C.c_int32, _dp, C.c_int32, _ip, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
+                                 C.c_double, C.POINTER(C.c_void_p)]),
+    "vrod_skin_destroy": (None, [C.c_void_p]),
+    "vrod_skin_smooth": (C.c_int, [C.c_void_p, C.c_int32]),
+    "vrod_skin_get_binding": (C.c_int, [C.c_void_p, _ip, _ip, _dp, _ip, _ip]),
+    "vrod_skin_deform": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, _dp]),
+    "vrod_skin_deform_solver": (C.c_int, [C.c_void_p, C.c_void_p, _dp]),
 }
 
 # Optional entry points (product-only extensions; absent from the oracle libraries).

@@ -12,6 +12,7 @@
 #include "../../include/vrod_bench.h"
 #include "../../include/vrod_capi.h"
 #include "host_model.h"
+#include "skin.h"
 #include "solver.h"
 #include "standalone.h"
 
@@ -80,6 +81,60 @@ struct vrod_scene {
 struct vrod_solver {
   std::unique_ptr<Solver> s;
 };
+struct vrod_skin {
+  std::unique_ptr<Skin> k;
+};
+namespace {
+void put_transform(const double* t, vrod_pill_transform* o) {  // device layout: center, scale, wxyz
+  std::copy(t, t + 3, o->center);
+  o->scale = t[3];
+  std::copy(t + 4, t + 8, o->rotation);
+}
+void get_transform(const vrod_pill_transform& t, double* o) {
+  std::copy(t.center, t.center + 3, o);
+  o[3] = t.scale;
+  std::copy(t.rotation, t.rotation + 4, o + 4);
+}
+// rod_rest_pill_transforms, skinning.cpp:24-37 (setup-time, host)
+std::vector<double> rest_transforms(const SceneData& sc) {
+  std::vector<double> out;
+  for (const RodData& r : sc.rods)
+    for (int e = 0; e + 1 < r.n; ++e) {
+      const V3 c = 0.5 * (r.rc[e] + r.rc[e + 1]);
+      const Q4& q = r.rq[e];
+      out.insert(out.end(), {c.x, c.y, c.z, 0.5 * (r.rs[e] + r.rs[e + 1]), q.w, q.x, q.y, q.z});
+    }
+  return out;
+}
+// rod_rest_pills, skinning.cpp:39-57 (setup-time, host)
+std::vector<PillData> rest_pills(const SceneData& sc) {
+  std::vector<PillData> out;
+  for (int ri = 0; ri < static_cast<int>(sc.rods.size()); ++ri) {
+    const RodData& r = sc.rods[ri];
+    for (int e = 0; e + 1 < r.n; ++e) {
+      PillData p;
+      p.c0 = r.rc[e];
+      p.c1 = r.rc[e + 1];
+      p.r0 = r.rs[e] * r.r[e];
+      p.r1 = r.rs[e + 1] * r.r[e + 1];
+      p.rod = ri;
+      p.element = e;
+      out.push_back(p);
+    }
+  }
+  return out;
+}
+void put_pill(const PillData& p, vrod_pill* o) {
+  put3(o->c0, p.c0);
+  put3(o->c1, p.c1);
+  o->r0 = p.r0;
+  o->r1 = p.r1;
+  o->rod = p.rod;
+  o->element = p.element;
+  o->group = p.group;
+  o->self_collide = p.self_collide ? 1 : 0;
+}
+}  // namespace
 
 extern "C" {
 
@@ -349,6 +404,66 @@ int vrod_solver_get_contacts(vrod_solver* h, int64_t cap, int64_t* count, int32_
                              double* beta) {
   return guarded([&] { *count = h->s->contacts(cap, a, b, alpha, beta); });
 }
+int vrod_solver_pill_transforms(vrod_solver* h, int64_t cap, int64_t* count, vrod_pill_transform* out) {
+  return guarded([&] {
+    const std::vector<double> t = h->s->pill_transforms();
+    const int64_t n = static_cast<int64_t>(t.size() / 8);
+    for (int64_t i = 0; i < n && i < cap; ++i) put_transform(t.data() + 8 * i, out + i);
+    *count = n;
+  });
+}
+int vrod_solver_rest_pill_transforms(vrod_solver* h, int64_t cap, int64_t* count, vrod_pill_transform* out) {
+  return guarded([&] {
+    const std::vector<double> t = rest_transforms(h->s->scene());
+    const int64_t n = static_cast<int64_t>(t.size() / 8);
+    for (int64_t i = 0; i < n && i < cap; ++i) put_transform(t.data() + 8 * i, out + i);
+    *count = n;
+  });
+}
+int vrod_solver_rest_pills(vrod_solver* h, int64_t cap, int64_t* count, vrod_pill* out) {
+  return guarded([&] {
+    const auto p = rest_pills(h->s->scene());
+    for (std::size_t i = 0; i < p.size() && static_cast<int64_t>(i) < cap; ++i) put_pill(p[i], out + i);
+    *count = static_cast<int64_t>(p.size());
+  });
+}
+int vrod_skin_bind(int32_t nv, const double* verts, int32_t nt, const int32_t* tris, int32_t np, const vrod_pill* pills,
+                   const vrod_pill_transform* rest, int32_t max_influences, double epsilon, vrod_skin** out) {
+  return guarded([&] {
+    std::vector<V3> v(nv > 0 ? nv : 0);
+    for (int32_t i = 0; i < nv; ++i) v[i] = v3(verts + 3 * i);
+    std::vector<std::array<int, 3>> t(nt > 0 ? nt : 0);
+    for (int32_t i = 0; i < nt; ++i) t[i] = {tris[3 * i], tris[3 * i + 1], tris[3 * i + 2]};
+    std::vector<PillData> p(np > 0 ? np : 0);
+    std::vector<double> tr(8ull * p.size());
+    for (int32_t i = 0; i < np; ++i) {
+      p[i] = to_pill(pills[i]);
+      get_transform(rest[i], tr.data() + 8ll * i);
+    }
+    auto sk = std::make_unique<vrod_skin>();
+    sk->k = std::make_unique<Skin>(v, t, p, tr, max_influences, epsilon);
+    *out = sk.release();
+  });
+}
+void vrod_skin_destroy(vrod_skin* sk) { delete sk; }
+int vrod_skin_smooth(vrod_skin* sk, int32_t iterations) {
+  return guarded([&] { sk->k->smooth(iterations); });
+}
+int vrod_skin_get_binding(const vrod_skin* sk, int32_t* offsets, int32_t* pills, double* weights, int32_t* nnz,
+                          int32_t* clamped) {
+  return guarded([&] { sk->k->get_binding(offsets, pills, weights, nnz, clamped); });
+}
+int vrod_skin_deform(vrod_skin* sk, int32_t np, const vrod_pill_transform* cur, double* out) {
+  return guarded([&] {
+    std::vector<double> t(8ull * (np > 0 ? np : 0));
+    for (int32_t i = 0; i < np; ++i) get_transform(cur[i], t.data() + 8ll * i);
+    sk->k->deform(np, t.data(), out);
+  });
+}
+int vrod_skin_deform_solver(vrod_skin* sk, vrod_solver* h, double* out) {
+  return guarded([&] { sk->k->deform_solver(*h->s, out); });
+}
+
 int vrod_solver_current_pills(vrod_solver* h, int64_t cap, int64_t* count, vrod_pill* out) {
   return guarded([&] {
     const auto pills = h->s->current_pills();

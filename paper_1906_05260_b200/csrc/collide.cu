@@ -16,6 +16,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "pill.cuh"
 #include "vmath.cuh"
 
 namespace vdev {
@@ -26,69 +27,6 @@ namespace {
 
 constexpr int kThreads = 256;
 
-struct PillV {
-  V3 c0, c1;
-  double r0, r1;
-};
-
-__device__ __forceinline__ PillV load_pill(const double* __restrict__ pill, int P, int i) {
-  return PillV{V3{pill[i], pill[P + i], pill[2 * P + i]}, V3{pill[3 * P + i], pill[4 * P + i], pill[5 * P + i]},
-               pill[6 * P + i], pill[7 * P + i]};
-}
-
-// pill_project (collision.cpp:15-49) with the per-pill constants (axis, length, unit axis,
-// cone slope) computed once per query pill: same operations on the same inputs, so the
-// results are identical to evaluating them inside every call.
-struct PillPrep {
-  V3 c0, c1;
-  double r0, r1;
-  bool degenerate;
-  double l;
-  V3 j;
-  double tan_t;
-};
-__device__ __forceinline__ PillPrep prep_pill(const PillV& p) {
-  PillPrep q;
-  q.c0 = p.c0;
-  q.c1 = p.c1;
-  q.r0 = p.r0;
-  q.r1 = p.r1;
-  const V3 axis = p.c1 - p.c0;
-  q.l = norm(axis);
-  q.degenerate = q.l <= fabs(p.r0 - p.r1) || q.l < 1e-14;
-  if (!q.degenerate) {
-    q.j = axis / q.l;
-    const double sin_t = (p.r1 - p.r0) / q.l;
-    q.tan_t = sin_t / sqrt(fmax(1e-16, 1.0 - sin_t * sin_t));
-  } else {
-    q.j = V3{0, 0, 0};
-    q.tan_t = 0;
-  }
-  return q;
-}
-__device__ __forceinline__ double project(const V3& x, const PillPrep& p, double& t_out, bool& deg) {
-  if (p.degenerate) {
-    const double d0 = norm(x - p.c0) - p.r0;
-    const double d1 = norm(x - p.c1) - p.r1;
-    deg = true;
-    if (d0 <= d1) {
-      t_out = 0.0;
-      return d0;
-    }
-    t_out = 1.0;
-    return d1;
-  }
-  deg = false;
-  const V3 y = x - p.c0;
-  const double a = dot(y, p.j);
-  const double b = norm(y - a * p.j);
-  double t = (a + b * p.tan_t) / p.l;
-  t = fmin(fmax(t, 0.0), 1.0);
-  t_out = t;
-  const V3 c = (1.0 - t) * p.c0 + t * p.c1;  // pill_distance_at, collision.cpp:9-13
-  const double r = (1.0 - t) * p.r0 + t * p.r1;
-  return norm(x - c) - r;
-}
 __device__ __forceinline__ double pair_distance(const PillV& a, const PillPrep& b, double alpha, double& beta) {
   const V3 ca = (1.0 - alpha) * a.c0 + alpha * a.c1;
   const double ra = (1.0 - alpha) * a.r0 + alpha * a.r1;

@@ -271,6 +271,9 @@ int persistent_tiles(const World& w);
 void launch_iterate_persistent(const World& w, Collide& c, const Groups& g, const PersistParams& pp, const SweepParams& sp,
                                int* singular_counters, unsigned long long* err, cudaStream_t st);
 
+// skin.cu: rod_pill_transforms of the state X (8 doubles per rod pill: center, scale, wxyz)
+void launch_pill_transforms(const World& w, const double* X, double* out, cudaStream_t st);
+
 // shape.cu
 void launch_shape_match(const World& w, const Groups& g, double* X, const int* level_off_host, bool pdl, cudaStream_t st);
 

@@ -847,6 +847,19 @@ long long Solver::kernel_nodes_per_step() {
   return kernels_per_step_;
 }
 
+void Solver::pill_transforms_device(double* d_out) { vdev::launch_pill_transforms(w_, w_.X, d_out, stream_); }
+
+std::vector<double> Solver::pill_transforms() {
+  std::vector<double> out(8ull * setup_.E);
+  if (setup_.E == 0) return out;
+  if (!d_ptrans_) d_ptrans_ = dalloc<double>(out.size());
+  pill_transforms_device(d_ptrans_);
+  check_cuda(cudaMemcpyAsync(out.data(), d_ptrans_, out.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_),
+             "pill transforms");
+  check_cuda(cudaStreamSynchronize(stream_), "pill transforms");
+  return out;
+}
+
 int Solver::trace(long long* out, int cap) {
   if (!d_trace_) return 0;
   std::vector<unsigned long long> h(vdev::kTraceCap);

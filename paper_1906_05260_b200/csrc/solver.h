@@ -59,6 +59,10 @@ class Solver {
   void inverse_weights(double* ic, double* is, double* it);
   long long contacts(long long cap, int* a, int* b, double* alpha, double* beta);
   std::vector<PillData> current_pills();
+  // Solver::pill_transforms() (solver.cpp:438-440): rod pills, 8 doubles each (center, scale,
+  // frame wxyz); the device variant writes into a device buffer on the solver's stream.
+  std::vector<double> pill_transforms();
+  void pill_transforms_device(double* d_out);
   // Per-scene reports of the last step (batch; a single scene returns one entry == step()).
   int scene_count() const { return n_scenes_; }
   std::vector<Report> scene_reports() const;
@@ -114,6 +118,7 @@ class Solver {
   double* xrec2_ = nullptr;          // ping-pong partner of w_.xrec (persistent kernel)
   double* ext_lam2_ = nullptr;       // ping-pong partner of c_.ext_lam
   unsigned* d_bar_ = nullptr;        // grid-barrier counter
+  double* d_ptrans_ = nullptr;       // pill transforms download buffer (lazy)
   unsigned long long* d_trace_ = nullptr;  // VROD_TRACE=1: persistent-kernel phase timestamps
  public:
   int trace(long long* out, int cap);

@@ -13,7 +13,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import capi
-from .scene import Scene, check, marshal_scene
+from .scene import InvalidArgument, Scene, check, marshal_scene
 
 KIND_NAMES = ("stretch_z", "cross_section", "surface_stretch", "bend_twist", "surface_bending",
               "volume_stretch", "volume_bend_u", "volume_bend_v")
@@ -240,6 +240,89 @@ class SolverHandle:
         if n.value:
             check(self._lib, self._lib.vrod_solver_current_pills(self._h, n.value, C.byref(n),
                                                                  out.ctypes.data_as(C.c_void_p)))
+        return out
+
+
+    def _transforms(self, fn) -> np.ndarray:
+        n = C.c_int64()
+        check(self._lib, fn(self._h, 0, C.byref(n), None))
+        out = np.zeros(n.value, dtype=capi.TRANSFORM_DTYPE)
+        if n.value:
+            check(self._lib, fn(self._h, n.value, C.byref(n), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def pill_transforms(self) -> np.ndarray:
+        """Solver::pill_transforms() (solver.cpp:438-440): rod pills, TRANSFORM_DTYPE records."""
+        return self._transforms(self._lib.vrod_solver_pill_transforms)
+
+    def rest_pill_transforms(self) -> np.ndarray:
+        """rod_rest_pill_transforms(scene().rods) (skinning.cpp:24-37)."""
+        return self._transforms(self._lib.vrod_solver_rest_pill_transforms)
+
+    def rest_pills(self) -> np.ndarray:
+        """rod_rest_pills(scene().rods) (skinning.cpp:39-57)."""
+        n = C.c_int64()
+        check(self._lib, self._lib.vrod_solver_rest_pills(self._h, 0, C.byref(n), None))
+        out = np.zeros(n.value, dtype=capi.PILL_DTYPE)
+        if n.value:
+            check(self._lib, self._lib.vrod_solver_rest_pills(self._h, n.value, C.byref(n),
+                                                              out.ctypes.data_as(C.c_void_p)))
+        return out
+
+
+class Skin:
+    """SkinBinding + TriMesh (skinning.h:14-63) over any library exporting include/vrod_capi.h:
+    bind_skin at construction, smooth_binding, deform_mesh (host transforms) and the fused
+    per-frame deform of a solver's live state."""
+
+    def __init__(self, lib, vertices, triangles, rest_pills: np.ndarray, rest_transforms: np.ndarray,
+                 max_influences: int = 8, epsilon: float = 1e-4):
+        self._lib = lib
+        self._h = C.c_void_p()
+        v = np.ascontiguousarray(vertices, dtype=np.float64).reshape(-1, 3)
+        t = np.ascontiguousarray(triangles if triangles is not None else np.zeros((0, 3)), dtype=np.int32).reshape(-1, 3)
+        p = _pills(rest_pills)
+        tr = np.ascontiguousarray(rest_transforms, dtype=capi.TRANSFORM_DTYPE)
+        if len(tr) != len(p):  # the C-ABI takes one count for both lists (skinning.cpp:63-64)
+            raise InvalidArgument("pill list and transform list must match")
+        self.vertex_count = v.shape[0]
+        check(lib, lib.vrod_skin_bind(v.shape[0], capi.ptr(v), t.shape[0], capi.ptr(t, C.c_int32), len(p),
+                                      p.ctypes.data_as(C.c_void_p), tr.ctypes.data_as(C.c_void_p), max_influences,
+                                      epsilon, C.byref(self._h)))
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.vrod_skin_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def smooth(self, iterations: int) -> None:
+        check(self._lib, self._lib.vrod_skin_smooth(self._h, iterations))
+
+    def binding(self) -> dict:
+        nnz, cl = C.c_int32(), C.c_int32()
+        check(self._lib, self._lib.vrod_skin_get_binding(self._h, None, None, None, C.byref(nnz), C.byref(cl)))
+        off = np.zeros(self.vertex_count + 1, dtype=np.int32)
+        pills = np.zeros(nnz.value, dtype=np.int32)
+        w = np.zeros(nnz.value)
+        check(self._lib, self._lib.vrod_skin_get_binding(self._h, capi.ptr(off, C.c_int32), capi.ptr(pills, C.c_int32),
+                                                         capi.ptr(w), C.byref(nnz), C.byref(cl)))
+        return dict(offsets=off, pills=pills, weights=w, clamped_vertices=cl.value)
+
+    def deform(self, transforms: np.ndarray) -> np.ndarray:
+        tr = np.ascontiguousarray(transforms, dtype=capi.TRANSFORM_DTYPE)
+        out = np.zeros((self.vertex_count, 3))
+        check(self._lib, self._lib.vrod_skin_deform(self._h, len(tr), tr.ctypes.data_as(C.c_void_p), capi.ptr(out)))
+        return out
+
+    def deform_solver(self, solver: "SolverHandle") -> np.ndarray:
+        out = np.zeros((self.vertex_count, 3))
+        check(self._lib, self._lib.vrod_skin_deform_solver(self._h, solver._h, capi.ptr(out)))
         return out
 
 

@@ -221,3 +221,38 @@ CONFIGS = {
 def algorithmic_bytes(V: int, E: int, I: int, coupled: bool, P: int, Nc: int) -> int:
     """B_substep of SURVEY §8(d) / BASELINE.md §4 — the roofline numerator per substep."""
     return int(160 * V + 176 * E + (64 * I * (V + E) if coupled else 0) + 24 * P + 24 * Nc * (1 + I))
+
+
+# ---- skinning (SURVEY.md §8(f) rows 2-3) ---------------------------------------------------------
+
+def sleeve_mesh(rest_pills: np.ndarray, rings: int, segments: int, margin: float = 0.3, inner: int = 0, seed: int = 7):
+    """A closed-sided tube mesh (quad grid split into triangles) wrapped around the rest pills'
+    bounding box along its longest axis, `margin` beyond the bounding radius, plus `inner`
+    vertices placed inside random pills (they clamp to epsilon, skinning.cpp:79-81). Returns
+    (vertices (n, 3), triangles (t, 3) int32)."""
+    c0, c1 = np.asarray(rest_pills["c0"]), np.asarray(rest_pills["c1"])
+    pts = np.concatenate([c0, c1])
+    lo, hi = pts.min(0), pts.max(0)
+    axis = int(np.argmax(hi - lo))
+    a, b = [k for k in range(3) if k != axis]
+    center = 0.5 * (lo + hi)
+    radius = 0.5 * float(np.hypot(hi[a] - lo[a], hi[b] - lo[b])) + margin * max(float((hi - lo).max()), 1e-3) * 0.1 + 1e-3
+    t = np.linspace(lo[axis], hi[axis], rings)
+    phi = np.linspace(0.0, 2 * np.pi, segments, endpoint=False)
+    V = np.zeros((rings * segments, 3))
+    V[:, axis] = np.repeat(t, segments)
+    V[:, a] = center[a] + radius * np.tile(np.cos(phi), rings)
+    V[:, b] = center[b] + radius * np.tile(np.sin(phi), rings)
+    tris = []
+    for r in range(rings - 1):
+        for s in range(segments):
+            i0, i1 = r * segments + s, r * segments + (s + 1) % segments
+            j0, j1 = i0 + segments, i1 + segments
+            tris.append((i0, i1, j1))
+            tris.append((i0, j1, j0))
+    if inner:
+        rng = np.random.default_rng(seed)
+        k = rng.integers(0, len(c0), inner)
+        u = rng.uniform(0.2, 0.8, inner)[:, None]
+        V = np.concatenate([V, (1 - u) * c0[k] + u * c1[k]])
+    return V, np.asarray(tris, dtype=np.int32).reshape(-1, 3)

@@ -68,6 +68,10 @@ def main():
         out[f"fc/{k}"] = v
     np.savez_compressed(os.path.join(HERE, "reference_golden.npz"), **out)
     print("wrote", len(out), "arrays")
+    from test_skinning import make_skin_golden  # skinning.cpp flow on the same scenes
+    skin = make_skin_golden(lib)
+    np.savez_compressed(os.path.join(HERE, "skin_golden.npz"), **skin)
+    print("wrote", len(skin), "skin arrays")
 
 
 if __name__ == "__main__":
