@@ -208,6 +208,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=90.0, help="cap of the --impl reference timed sample")
     ap.add_argument("--no-batch", action="store_true", help="skip the C5 sharded-batch measurement")
+    ap.add_argument("--no-skin", action="store_true", help="skip the skinning (deform_mesh) measurement")
+    ap.add_argument("--skin-rings", type=int, default=1000, help="skin mesh: rings x segments vertices")
     ap.add_argument("--batch-scenes", type=int, default=8192, help="C5 batch size, sharded over the ranks")
     ap.add_argument("--batch-steps", type=int, default=3)
     args = ap.parse_args()
@@ -336,6 +338,11 @@ def main():
             line["secondary"] = run_c4(lib, args.secondary_steps, peak)
         except Exception as exc:  # report, do not lose the headline
             line["secondary"] = {"error": f"{type(exc).__name__}: {exc}"}
+    if not args.no_skin:
+        try:
+            line["skin"] = run_skin(lib, solver, peak, args.cpu_seconds)
+        except Exception as exc:  # report, do not lose the headline
+            line["skin"] = {"error": f"{type(exc).__name__}: {exc}"}
     print(json.dumps(line), flush=True)
     if dist:
         dist[1].destroy_process_group()
@@ -384,6 +391,67 @@ def run_c5(lib, args, rank, world, dist, barrier):
                            "broad_pairs": int(table[:, 10].sum()), "max_penetration": float(table[:, 8].max())}
     del solver
     return out
+
+
+def run_skin(lib, solver, peak, cpu_seconds, rings=1000, segments=1000, k=8, iters=50):
+    """Skinning, the consumer of every frame: a rings x segments sleeve
+    mesh (1M vertices) bound to the C3 solver's 3,712 rest pills (top-8 inverse-square weights,
+    one smoothing pass), then per frame the solver's pill transforms + deform_mesh on the device.
+    Algorithmic bytes per vertex: rest 24 + CSR offset 4 + k x (pill 4 + weight 8) + out 24; the
+    3,712 x 128 B pill transform tables stay in L2."""
+    import paper_1906_05260_b200 as pb
+    from paper_1906_05260_b200 import workloads
+    from paper_1906_05260_b200.handle import Skin as SkinHandle
+    lib.vrod_bench_skin_deform.restype = C.c_int
+    lib.vrod_bench_skin_deform.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(C.c_double),
+                                           C.POINTER(C.c_double)]
+    pills, rest = solver.rest_pills(), solver.rest_pill_transforms()
+    V, T = workloads.sleeve_mesh(pills, rings, segments)
+    t0 = time.perf_counter()
+    sk = pb.Skin(V, T, pills, rest, max_influences=k)
+    bind_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    sk.smooth(1)
+    smooth_s = time.perf_counter() - t0
+    nnz = len(sk.binding()["pills"])
+    nv = V.shape[0]
+    tot, dfm = C.c_double(), C.c_double()
+    lib.vrod_bench_skin_deform(sk._h, solver._h, 3, C.byref(tot), C.byref(dfm))  # warm-up
+    from paper_1906_05260_b200.scene import check
+    check(lib, lib.vrod_bench_skin_deform(sk._h, solver._h, iters, C.byref(tot), C.byref(dfm)))
+    frame_s = tot.value / 1e3 / iters
+    deform_s = dfm.value / 1e3
+    bytes_v = (24 + 4 + 24) * nv + 12 * nnz
+    t0 = time.perf_counter()
+    for _ in range(10):
+        sk.deform_solver(solver)
+    e2e_s = (time.perf_counter() - t0) / 10
+    # CPU baseline: the oracle restatement's deform_mesh (1 thread) on a 250x250 sleeve
+    orc = capi_bind_oracle()
+    hv, ht = workloads.sleeve_mesh(pills, 250, 250)
+    osk = SkinHandle(orc, hv, ht, pills, rest, k)
+    cur = solver.pill_transforms()
+    n_cpu, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < min(cpu_seconds, 5.0):
+        osk.deform(cur)
+        n_cpu += 1
+    cpu_vps = n_cpu * hv.shape[0] / (time.perf_counter() - t0)
+    return {"workload": f"sleeve mesh {rings}x{segments} ({nv:,} vertices, {len(T):,} triangles) bound to the C3 "
+                        f"rest pills ({len(pills):,}), top-{k} weights, 1 smoothing pass; per frame: pill transforms "
+                        "+ deform_mesh",
+            "vertices_per_sec": nv / frame_s, "ms_per_frame": frame_s * 1e3, "bind_s": bind_s, "smooth_s": smooth_s,
+            "influences": nnz,
+            "roofline": {"bound": "hbm", "kernel": "k_skin_deform", "bytes_per_launch": bytes_v,
+                         "avg_launch_us": deform_s * 1e6, "achieved": bytes_v / deform_s / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": bytes_v / deform_s / 1e9 / peak},
+            "e2e": {"value": nv / e2e_s, "unit": "vertices/s", "d2h_bytes_per_frame": 24 * nv},
+            "cpu_baseline": {"value": cpu_vps, "unit": "vertices/s", "cores": 1, "kind": "port",
+                             "sample": f"{n_cpu} deform_mesh calls of a 250x250 sleeve (oracle restatement)"}}
+
+
+def capi_bind_oracle():
+    from paper_1906_05260_b200 import capi
+    return capi.bind(C.CDLL(ORACLE_LIB))
 
 
 def run_c4(lib, steps, peak):

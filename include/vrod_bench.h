@@ -37,6 +37,12 @@ int vrod_bench_kernel_times(vrod_solver* solver, int32_t steps, double* ms, int6
 /* Debug: phase timestamps (globaltimer ns) of CTA 0 in the last persistent iteration kernel,
  * when the solver was created with VROD_TRACE=1 (else count = 0). */
 int vrod_bench_trace(vrod_solver* solver, int32_t capacity, int64_t* out, int32_t* count);
+/* Skinning throughput: `iterations` per-frame deformations (pill transforms of the solver's live
+ * state + deform_mesh, all on the solver's stream, result left on the device), bracketed by CUDA
+ * events. Writes the summed device milliseconds and, if non-NULL, the milliseconds of the deform
+ * kernel alone (events around it). */
+int vrod_bench_skin_deform(vrod_skin* skin, vrod_solver* solver, int32_t iterations, double* device_ms,
+                           double* deform_ms);
 /* Contacts and candidates of the last step (capacity diagnostics). */
 int vrod_bench_last_counts(vrod_solver* solver, int64_t* max_candidates, int64_t* max_contacts);
 

@@ -517,6 +517,9 @@ int vrod_bench_trace(vrod_solver* h, int32_t cap, int64_t* out, int32_t* count) 
     for (int i = 0; i < *count; ++i) out[i] = t[i];
   });
 }
+int vrod_bench_skin_deform(vrod_skin* sk, vrod_solver* h, int32_t iterations, double* ms, double* deform_ms) {
+  return guarded([&] { sk->k->bench(*h->s, iterations, ms, deform_ms); });
+}
 int vrod_bench_last_counts(vrod_solver* h, int64_t* cand, int64_t* ct) {
   return guarded([&] {
     if (cand) *cand = h->s->last_max_candidates();

@@ -216,21 +216,53 @@ __global__ void k_compact_csr(int nv, int stride, const int* __restrict__ off, c
     }
 }
 
+// Per frame, per pill: cur.scale / ref.scale (the one division of deform_mesh's inner term,
+// the same IEEE quotient for every vertex the pill influences) into the scale slot of the
+// frame table, so the per-influence work is division-free.
+__global__ void k_skin_frame(int np, const double* __restrict__ rest, const double* __restrict__ cur,
+                             double* __restrict__ frame) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 8 * np; i += gridDim.x * blockDim.x) {
+    const int p = i >> 3, f = i & 7;
+    frame[i] = f == 3 ? cur[8ll * p + 3] / rest[8ll * p + 3] : cur[i];
+  }
+}
+
 // deform_mesh, skinning.cpp:165-185: local = conj(ref.rotation) * (rest - ref.center);
-// blended += w * (cur.center + (cur.scale / ref.scale) * (cur.rotation * local)).
-__global__ void k_skin_deform(int nv, const double* __restrict__ verts, const int* __restrict__ off,
-                              const int* __restrict__ pills, const double* __restrict__ w,
-                              const double* __restrict__ rest, const double* __restrict__ cur, double* __restrict__ out) {
+// blended += w * (cur.center + (cur.scale / ref.scale) * (cur.rotation * local)); the frame
+// table carries cur.scale / ref.scale in its scale slot (k_skin_frame).
+constexpr int kDeformThreads = 128;
+
+__device__ __forceinline__ void ld8(const double* __restrict__ p, double (&o)[8]) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double2 v = __ldg(q + i);
+    o[2 * i] = v.x;
+    o[2 * i + 1] = v.y;
+  }
+}
+
+// One thread per vertex; the pill records (64 B, L2/L1-resident) are read as 16-byte vectors.
+// FP64-pipe bound: ~75 dependent-free FP64 operations per influence (two quaternion rotations),
+// --fmad=false keeps the reference's rounding.
+__global__ void __launch_bounds__(kDeformThreads) k_skin_deform(int nv, const double* __restrict__ verts,
+                                                                const int* __restrict__ off,
+                                                                const int* __restrict__ pills,
+                                                                const double* __restrict__ w,
+                                                                const double* __restrict__ rest,
+                                                                const double* __restrict__ cur,
+                                                                double* __restrict__ out) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
     const V3 x{verts[3ll * v], verts[3ll * v + 1], verts[3ll * v + 2]};
     V3 blended{0, 0, 0};
     const int k1 = off[v + 1];
     for (int k = off[v]; k < k1; ++k) {
       const int p = pills[k];
-      const double* r = rest + 8ll * p;
-      const double* c = cur + 8ll * p;
+      double r[8], c[8];
+      ld8(rest + 8ll * p, r);
+      ld8(cur + 8ll * p, c);
       const V3 local = qrot(qconj(Q4{r[4], r[5], r[6], r[7]}), x - V3{r[0], r[1], r[2]});
-      const V3 moved = V3{c[0], c[1], c[2]} + (c[3] / r[3]) * qrot(Q4{c[4], c[5], c[6], c[7]}, local);
+      const V3 moved = V3{c[0], c[1], c[2]} + c[3] * qrot(Q4{c[4], c[5], c[6], c[7]}, local);
       blended = blended + w[k] * moved;
     }
     out[3ll * v] = blended.x;
@@ -306,6 +338,7 @@ Skin::Skin(const std::vector<V3>& vertices, const std::vector<std::array<int, 3>
   d_verts_ = dmalloc<double>(vx.size());
   d_rest_ = dmalloc<double>(rest_transforms.size());
   d_cur_ = dmalloc<double>(rest_transforms.size());
+  d_frame_ = dmalloc<double>(rest_transforms.size());
   d_off_ = dmalloc<int>(nv_ + 1ull);
   nnz_ = static_cast<long long>(nv_) * keep_;
   d_pills_ = dmalloc<int>(nnz_);
@@ -342,7 +375,7 @@ Skin::Skin(const std::vector<V3>& vertices, const std::vector<std::array<int, 3>
 
 Skin::~Skin() {
   if (stream_) cudaStreamSynchronize(stream_);
-  for (void* p : {static_cast<void*>(d_verts_), static_cast<void*>(d_rest_), static_cast<void*>(d_cur_),
+  for (void* p : {static_cast<void*>(d_verts_), static_cast<void*>(d_rest_), static_cast<void*>(d_cur_), static_cast<void*>(d_frame_),
                   static_cast<void*>(d_off_), static_cast<void*>(d_pills_), static_cast<void*>(d_weights_),
                   static_cast<void*>(d_cnt_), static_cast<void*>(d_out_), static_cast<void*>(d_nb_off_),
                   static_cast<void*>(d_nb_), static_cast<void*>(d_scr_pill_), static_cast<void*>(d_scr_w_),
@@ -401,8 +434,9 @@ void Skin::get_binding(int* offsets, int* pills, double* weights, int* nnz, int*
 }
 
 void Skin::deform_device(const double* d_transforms, cudaStream_t st) {
-  vdev::k_skin_deform<<<vdev::grid_of(nv_, 128), 128, 0, st>>>(nv_, d_verts_, d_off_, d_pills_, d_weights_, d_rest_,
-                                                                d_transforms, d_out_);
+  vdev::k_skin_frame<<<vdev::grid_of(8ll * np_, 256), 256, 0, st>>>(np_, d_rest_, d_transforms, d_frame_);
+  vdev::k_skin_deform<<<vdev::grid_of(nv_, vdev::kDeformThreads), vdev::kDeformThreads, 0, st>>>(
+      nv_, d_verts_, d_off_, d_pills_, d_weights_, d_rest_, d_frame_, d_out_);
 }
 
 void Skin::deform(int pill_count, const double* transforms, double* out) {
@@ -424,6 +458,29 @@ void Skin::deform_solver(Solver& solver, double* out) {
   ck(cudaGetLastError(), "deform launch");
   if (out) ck(cudaMemcpyAsync(out, d_out_, sizeof(double) * 3ull * nv_, cudaMemcpyDeviceToHost, st), "download");
   ck(cudaStreamSynchronize(st), "deform");
+}
+
+void Skin::bench(Solver& solver, int iterations, double* total_ms, double* deform_ms) {
+  require(solver.total_elements() == np_, "transform count changed since binding");
+  cudaStream_t st = solver.stream();
+  cudaEvent_t e[4];
+  for (auto& x : e) ck(cudaEventCreate(&x), "event");
+  float t_all = 0.f, t_def = 0.f;
+  ck(cudaEventRecord(e[0], st), "event");
+  for (int i = 0; i < iterations; ++i) {
+    solver.pill_transforms_device(d_cur_);
+    if (i == iterations - 1) ck(cudaEventRecord(e[2], st), "event");
+    deform_device(d_cur_, st);
+    if (i == iterations - 1) ck(cudaEventRecord(e[3], st), "event");
+  }
+  ck(cudaEventRecord(e[1], st), "event");
+  ck(cudaEventSynchronize(e[1]), "bench");
+  ck(cudaGetLastError(), "bench launch");
+  cudaEventElapsedTime(&t_all, e[0], e[1]);
+  cudaEventElapsedTime(&t_def, e[2], e[3]);
+  for (auto& x : e) cudaEventDestroy(x);
+  if (total_ms) *total_ms = t_all;
+  if (deform_ms) *deform_ms = t_def;
 }
 
 }  // namespace vhost

@@ -40,9 +40,10 @@ class Skin {
   // device output of the last deformation (3 doubles per vertex) and the bench helpers
   const double* device_out() const { return d_out_; }
   void deform_device(const double* d_transforms, cudaStream_t st);  // no host copies
+  // bench: iterations x (pill transforms + deform) on the solver's stream, device-timed
+  void bench(Solver& solver, int iterations, double* total_ms, double* deform_ms);
 
  private:
-  void upload_csr_from_counts(cudaStream_t st);
   int nv_ = 0, np_ = 0, keep_ = 0, max_influences_ = 8, clamped_ = 0;
   long long nnz_ = 0;
   std::vector<int> nb_off_, nb_list_;  // one-ring neighbours (sorted, unique), host CSR
@@ -50,6 +51,7 @@ class Skin {
   double* d_verts_ = nullptr;       // 3 per vertex
   double* d_rest_ = nullptr;        // 8 per pill
   double* d_cur_ = nullptr;         // 8 per pill (host transforms upload)
+  double* d_frame_ = nullptr;       // 8 per pill: cur transform with cur.scale / ref.scale
   int* d_off_ = nullptr;            // nv+1
   int* d_pills_ = nullptr;          // nv * keep (CSR packed in front)
   double* d_weights_ = nullptr;
