@@ -927,8 +927,10 @@ void launch_narrow_only(Collide& c, int split_warm, int store_d, cudaStream_t st
 // Puts the first scalars[SC_NCT] raw (i, j, alpha, beta) records into (i, j) order in ct_*.
 void launch_order_contacts(Collide& c, cudaStream_t st) {
   const int g = grid_for(c.contact_cap);
-  cudaMemsetAsync(c.ct_cnt, 0, sizeof(int) * (c.P + 1), st);
-  cudaMemsetAsync(c.ct_cur, 0, sizeof(int) * (c.P + 1), st);
+  FillList f;
+  f.add(c.ct_cnt, c.P + 1, 0);
+  f.add(c.ct_cur, c.P + 1, 0);
+  launch_fill(f, st);
   launch_kernel(k_ct_count, g, kThreads, 0, st, g_pdl, c);
   scan_exclusive(c.ct_cnt, c.ct_off, c.P, nullptr, c.scan_tmp, c.scan_parts, st);
   launch_kernel(k_ct_scatter, g, kThreads, 0, st, g_pdl, c);
@@ -943,14 +945,17 @@ void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
   (void)store_d;
   const int P = c.P;
   const int b = (P + kThreads - 1) / kThreads;
-  cudaMemsetAsync(c.maxr_bits, 0, sizeof(unsigned long long), st);
-  if (c.pill_scene) cudaMemsetAsync(c.scene_maxr, 0, sizeof(unsigned long long) * c.n_scenes, st);
-  cudaMemsetAsync(c.table, 0xff, sizeof(int) * c.T, st);
-  cudaMemsetAsync(c.cell_count, 0, sizeof(int) * c.T, st);
-  cudaMemsetAsync(c.cell_cursor, 0, sizeof(int) * c.T, st);
-  cudaMemsetAsync(c.scalars + SC_BROAD, 0, sizeof(int), st);
-  cudaMemsetAsync(c.scalars + SC_NCAND_RAW, 0, sizeof(int), st);
-  cudaMemsetAsync(c.scalars + SC_NCT_RAW, 0, sizeof(int), st);
+  FillList f;  // per-call resets, one launch
+  f.add(c.maxr_bits, 2, 0);
+  if (c.pill_scene) f.add(c.scene_maxr, 2ll * c.n_scenes, 0);
+  f.add(c.table, c.T, -1);
+  f.add(c.cell_count, c.T, 0);
+  f.add(c.cell_cursor, c.T, 0);
+  f.add(c.scalars + SC_BROAD, 1, 0);
+  f.add(c.scalars + SC_NCAND_RAW, 1, 0);
+  f.add(c.scalars + SC_NCT_RAW, 1, 0);
+  if (do_narrow) f.add(c.scalars + SC_NCAND2, 1, 0);  // k_seg_filter's counter
+  launch_fill(f, st);
   if (P > 0) {
     launch_kernel(k_bounds, b, kThreads, 0, st, g_pdl, c, substep, err);
     launch_kernel(k_insert, b, kThreads, 0, st, g_pdl, c);
@@ -973,7 +978,6 @@ void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
   }
   launch_kernel(k_clamp_raw, 1, 1, 0, st, g_pdl, c.scalars, SC_NCAND_RAW, SC_NCAND, c.cand_cap, 1);
   if (!do_narrow) return;
-  cudaMemsetAsync(c.scalars + SC_NCAND2, 0, sizeof(int), st);
   launch_kernel(k_seg_filter, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c);
   launch_kernel(k_narrow_append, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c, split_warm);
   launch_kernel(k_clamp_raw, 1, 1, 0, st, g_pdl, c.scalars, SC_NCT_RAW, SC_NCT, c.contact_cap, 2);

@@ -223,6 +223,24 @@ inline void launch_kernel(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t 
 }
 
 // scan.cu
+// Several int-array fills in ONE kernel launch (instead of a memset node each, which would also
+// break the programmatic-dependent-launch chain of the step graph). Byte-zero fills of other
+// types pass their size in ints.
+constexpr int kMaxFills = 12;
+struct FillList {
+  int n = 0;
+  int* ptr[kMaxFills];
+  long long count[kMaxFills];
+  int value[kMaxFills];
+  void add(void* p, long long ints, int v) {
+    if (!p || ints <= 0) return;
+    ptr[n] = static_cast<int*>(p);
+    count[n] = ints;
+    value[n] = v;
+    ++n;
+  }
+};
+void launch_fill(const FillList& f, cudaStream_t st);
 void scan_exclusive(const int* in, int* out, long long n_cap, const int* n_dev, int* partials, int parts,
                     cudaStream_t st);
 long long scan_partials_needed(long long n);

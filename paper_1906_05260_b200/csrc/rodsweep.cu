@@ -949,8 +949,7 @@ int persistent_tiles(const World& w) {
 
 void launch_iterate_persistent(const World& w, Collide& c, const Groups& g, const PersistParams& pp, const SweepParams& sp,
                                int* singular_counters, unsigned long long* err, cudaStream_t st) {
-  const int tiles = (w.V + kPersistTP - 3) / (kPersistTP - 2);
-  cudaMemsetAsync(pp.bar, 0, sizeof(unsigned), st);
+  const int tiles = (w.V + kPersistTP - 3) / (kPersistTP - 2);  // pp.bar must be zero (Solver's fill)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles);
   cfg.blockDim = dim3(32 * warps_for<kPersistTP>());

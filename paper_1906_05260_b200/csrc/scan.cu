@@ -97,7 +97,45 @@ __global__ void k_add(int* __restrict__ out, long long n_cap, const int* n_dev, 
   }
 }
 
+// Small scans (n_cap <= kSmallScan): one CTA does it all — a chunk of consecutive elements per
+// thread, a block scan of the chunk totals — one launch instead of three.
+constexpr long long kSmallScan = 8 * kTile;  // 32768
+__global__ void k_scan_small(const int* __restrict__ in, int* __restrict__ out, long long n_cap, const int* n_dev) {
+  pdl_wait();
+  pdl_trigger();
+  const long long n = n_dev ? static_cast<long long>(*n_dev) : n_cap;
+  const long long chunk = (n + kThreads - 1) / kThreads;
+  const long long b = threadIdx.x * chunk, e = b + chunk < n ? b + chunk : n;
+  int sum = 0;
+  for (long long i = b; i < e; ++i) sum += in[i];
+  int total;
+  int run = block_excl(sum, &total);
+  for (long long i = b; i < e; ++i) {
+    const int v = in[i];
+    out[i] = run;
+    run += v;
+  }
+  if (threadIdx.x == 0) out[n] = total;
+}
+
+__global__ void k_fill(FillList f) {
+  pdl_wait();
+  pdl_trigger();
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (int a = 0; a < f.n; ++a)
+    for (long long i = t; i < f.count[a]; i += stride) f.ptr[a][i] = f.value[a];
+}
+
 }  // namespace
+
+void launch_fill(const FillList& f, cudaStream_t st) {
+  if (f.n == 0) return;
+  long long mx = 0;
+  for (int a = 0; a < f.n; ++a) mx = f.count[a] > mx ? f.count[a] : mx;
+  const long long b = (mx + kThreads - 1) / kThreads;
+  launch_kernel(k_fill, static_cast<unsigned>(b < 1 ? 1 : (b > 148 * 8 ? 148 * 8 : b)), kThreads, 0, st, g_pdl, f);
+}
 
 long long scan_partials_needed(long long n) { return n / kTile + 2; }
 
@@ -105,6 +143,10 @@ long long scan_partials_needed(long long n) { return n / kTile + 2; }
 void scan_exclusive(const int* in, int* out, long long n_cap, const int* n_dev, int* partials, int parts,
                     cudaStream_t st) {
   (void)parts;
+  if (n_cap <= kSmallScan) {
+    launch_kernel(k_scan_small, 1, kThreads, 0, st, g_pdl, in, out, n_cap, n_dev);
+    return;
+  }
   const long long blocks = n_cap / kTile + 1;
   launch_kernel(k_tile_scan, static_cast<unsigned>(blocks), kThreads, 0, st, g_pdl, in, out, n_cap, n_dev, partials);
   launch_kernel(k_partials_scan, 1, kThreads, 0, st, g_pdl, partials, n_cap, n_dev);

@@ -675,7 +675,6 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
     vdev::launch_animate(w_, anim, al_, d_pm_slot_, d_act_rod_off_, d_act_list_, d_act_applied_, d_act_rods_,
                          n_act_rods_, st);
     vdev::launch_predict(w_, anim, al_, g, h, s, d_err_, st);
-    check_cuda(cudaMemsetAsync(w_.lam, 0, sizeof(double) * vdev::kLamFields * w_.vpad, st), "lam reset");
     end();
     begin(CAT_COLLIDE);
     if (c_.P >= 1) vdev::launch_collide(w_, c_, anim, al_, s, d_err_, d_acc_, collide_possible_ ? 1 : 0, st);
@@ -683,7 +682,15 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
     end();
     begin(CAT_EXT_SETUP);
     if (ext_possible_) vdev::launch_ext_setup(w_, c_, st);
-    check_cuda(cudaMemsetAsync(d_singular_, 0, sizeof(int) * iterations, st), "singular reset");
+    const bool persistent = persist_tiles_ > 0 && !probe_log;
+    {  // per-substep resets, one launch: multipliers (per-launch path; the persistent kernel keeps
+       // them on chip), singular counters, grid-barrier counter
+      vdev::FillList f;
+      if (!persistent) f.add(w_.lam, 2ll * vdev::kLamFields * w_.vpad, 0);
+      f.add(d_singular_, iterations, 0);
+      if (persistent) f.add(d_bar_, 1, 0);
+      vdev::launch_fill(f, st);
+    }
     end();
     double* cur = w_.X;
     double* nxt = w_.Y;
@@ -692,7 +699,7 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
     const bool pdl = vdev::g_pdl;
     double* lam_a = w_.lam;
     double* lam_b = w_.lam + static_cast<std::size_t>(vdev::kLamFields) * w_.vpad;
-    if (persist_tiles_ > 0 && !probe_log) {  // the whole iteration loop in one launch
+    if (persistent) {  // the whole iteration loop in one launch
       vdev::PersistParams pp{};
       pp.X = cur;
       pp.Y = nxt;
@@ -712,7 +719,7 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
       end();
       if (iterations & 1) std::swap(cur, nxt);
     }
-    for (int it = 0; it < iterations && !(persist_tiles_ > 0 && !probe_log); ++it) {
+    for (int it = 0; it < iterations && !persistent; ++it) {
       sp.iter = it;
       sp.scene_singular = (n_scenes_ > 1 && it == iterations - 1) ? d_scene_sing_ : nullptr;
       sp.lam_in = (it & 1) ? lam_b : lam_a;

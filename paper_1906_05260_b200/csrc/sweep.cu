@@ -416,8 +416,10 @@ int grid_for(long long n) {
 int report_parts(int V) { return (V + kRepThreads - 1) / kRepThreads; }
 
 void launch_ext_setup(const World& w, Collide& c, cudaStream_t st) {
-  cudaMemsetAsync(c.ext_cnt, 0, sizeof(int) * (w.V + 1), st);
-  cudaMemsetAsync(c.ext_cur, 0, sizeof(int) * w.V, st);
+  FillList f;
+  f.add(c.ext_cnt, w.V + 1, 0);
+  f.add(c.ext_cur, w.V, 0);
+  launch_fill(f, st);
   const int g = grid_for(c.ext_cap);
   launch_kernel(k_ext_count, g, kThreads, 0, st, g_pdl, c, c.n_pins);
   scan_exclusive(c.ext_cnt, c.ext_off, w.V, nullptr, c.scan_tmp, c.scan_parts, st);
