@@ -52,6 +52,15 @@ def dist_info():
     return rank, world, local
 
 
+def load_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture (profiles/r01_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            return json.load(f)[kernel]["bytes"]
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -305,7 +314,8 @@ def main():
     b_sub = workloads.algorithmic_bytes(V, E, I, True, E, nc)
     t_sub = ms_total / 1e3 / args.steps / S
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "k_iterate" if persistent else "k_rod_sweep", "bytes_per_launch": sweep_bytes,
+                "traffic": load_traffic("k_iterate" if persistent else "k_rod_sweep"),
+                "kernel": "k_iterate" if persistent else "k_rod_sweep", "bytes_per_launch": sweep_bytes,
                 "avg_launch_us": sweep_avg_s * 1e6, "share_of_step": sweep_ms / total_dev_ms,
                 "peak_source": peak_kind,
                 "substep": {"algorithmic_bytes": b_sub, "seconds": t_sub, "achieved_gbs": b_sub / t_sub / 1e9,
@@ -443,7 +453,8 @@ def run_skin(lib, solver, peak, cpu_seconds, rings=1000, segments=1000, k=8, ite
             "influences": nnz,
             "roofline": {"bound": "hbm", "kernel": "k_skin_deform", "bytes_per_launch": bytes_v,
                          "avg_launch_us": deform_s * 1e6, "achieved": bytes_v / deform_s / 1e9, "peak": peak,
-                         "unit": "GB/s", "frac": bytes_v / deform_s / 1e9 / peak},
+                         "unit": "GB/s", "frac": bytes_v / deform_s / 1e9 / peak,
+                         "traffic": load_traffic("k_skin_deform")},
             "e2e": {"value": nv / e2e_s, "unit": "vertices/s", "d2h_bytes_per_frame": 24 * nv},
             "cpu_baseline": {"value": cpu_vps, "unit": "vertices/s", "cores": 1, "kind": "port",
                              "sample": f"{n_cpu} deform_mesh calls of a 250x250 sleeve (oracle restatement)"}}
@@ -479,7 +490,8 @@ def run_c4(lib, steps, peak):
             "roofline_substep": {"algorithmic_bytes": b_sub, "achieved_gbs": b_sub / t_sub / 1e9, "peak": peak,
                                  "frac": b_sub / t_sub / 1e9 / peak},
             "rod_sweep": {"avg_launch_us": sweep_avg * 1e6, "bytes_per_launch": 64 * (V + E),
-                          "achieved_gbs": 64 * (V + E) / sweep_avg / 1e9},
+                          "achieved_gbs": 64 * (V + E) / sweep_avg / 1e9, "traffic": load_traffic("k_rod_sweep"),
+                          "traffic_gbs": (load_traffic("k_rod_sweep") or 0) / sweep_avg / 1e9},
             "breakdown_ms_per_step": {k: v[0] for k, v in kt.items()}, "kernels_per_step": int(kern)}
 
 

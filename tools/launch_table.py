@@ -11,7 +11,7 @@ def main(path, top=25):
         if len(r) <= vi:
             continue
         name = r[ki].split("(")[0].replace("(anonymous namespace)::", "").replace("void ", "")
-        v = float(r[vi].replace(",", "")) * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(r[ui], 1.0)
+        v = float(r[vi].replace(",", "")) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(r[ui], 1.0)
         agg[name][0] += 1
         agg[name][1] += v
     tot = sum(v[1] for v in agg.values())

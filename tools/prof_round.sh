@@ -1,9 +1,13 @@
+# Round profiling recipe (run on the GPU box from the repo root; each ncu command only after the
+# same workload exited 0 without ncu). Outputs go to gpurun_out/prof/.
 set -x
-cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out/p1
-timeout 300 python tools/profile_step.py C4 2 > gpurun_out/p1/plain.log 2>&1 || exit 1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/p1/c4_launches.csv python tools/profile_step.py C4 2 > gpurun_out/p1/ncu_l.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_rod_sweep|k_ext_solve|k_pairs|k_narrow|k_seg_filter|k_ext_sort" -s 60 -c 8 -o gpurun_out/p1/c4_full python tools/profile_step.py C4 2 > gpurun_out/p1/ncu_f.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/p1/c3_launches.csv python tools/profile_step.py C3 3 > gpurun_out/p1/ncu_l3.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_rod_sweep|k_ext_solve|k_shape" -s 200 -c 6 -o gpurun_out/p1/c3_full python tools/profile_step.py C3 3 > gpurun_out/p1/ncu_f3.log 2>&1
-ls -la gpurun_out/p1
+mkdir -p gpurun_out/prof
+timeout 300 python tools/profile_step.py C3 3 > gpurun_out/prof/c3_plain.log 2>&1 || exit 1
+timeout 300 python tools/profile_step.py C4 2 > gpurun_out/prof/c4_plain.log 2>&1 || exit 1
+timeout 300 python tools/profile_skin.py 2 > gpurun_out/prof/skin_plain.log 2>&1 || exit 1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/prof/c3_launches.csv python tools/profile_step.py C3 3 > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/prof/c4_launches.csv python tools/profile_step.py C4 2 > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_iterate -s 3 -c 1 -o gpurun_out/prof/c3_iterate python tools/profile_step.py C3 3 > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_rod_sweep|k_ext_solve|k_pairs_cell|k_narrow_append" -s 30 -c 4 -o gpurun_out/prof/c4_full python tools/profile_step.py C4 2 > /dev/null 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_skin_deform -c 1 -o gpurun_out/prof/skin_deform python tools/profile_skin.py 2 > /dev/null 2>&1
+ls -la gpurun_out/prof
