@@ -63,10 +63,12 @@ struct ExtResult {
 
 __device__ __forceinline__ double xget(const double* X, int f, int vp, int v) { return X[static_cast<long long>(f) * vp + v]; }
 
-// X: snapshot state rows (pins / half-planes); xrec: the matching slot records (contacts).
+// X: snapshot state rows (pins / half-planes); xrec: the matching slot records (contacts);
+// lam: the multipliers before the sweep, SoA (component d of block b at lam[d * ls + b]).
 template <class Emit>
 __device__ __forceinline__ ExtResult ext_block(const World& w, const Collide& c, const double* X, const double* xrec,
-                                               const double* lam_in, int b, const SweepParams& sp, Emit&& emit) {
+                                               const double* lam, long long ls, int b, const SweepParams& sp,
+                                               Emit&& emit) {
   using namespace vm;
   ExtResult r;
   r.singular = r.bad = false;
@@ -95,7 +97,7 @@ __device__ __forceinline__ ExtResult ext_block(const World& w, const Collide& c,
     double rhs[3], dl[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      r.lam[d] = lam_in[d];
+      r.lam[d] = lam[d * ls + b];
       M[d][d] = M[d][d] + kinv;
       rhs[d] = W[d] - kinv * r.lam[d];
     }
@@ -137,7 +139,7 @@ __device__ __forceinline__ ExtResult ext_block(const World& w, const Collide& c,
     bool wrote[4] = {false, false, false, false};
     r.owner = A.v0 >= 0 ? 0 : 2;
     const double icv[4] = {icA[0], icA[1], icB[0], icB[1]}, isv[4] = {isA[0], isA[1], isB[0], isB[1]};
-    r.lam[0] = lam_in[0];
+    r.lam[0] = lam[b];
     if (!(W >= 0.0 && r.lam[0] == 0.0)) {
       const double coef[4] = {1.0 - al, al, -(1.0 - be), -be};
       const double sj[4] = {-(1.0 - al) * A.rb0, -al * A.rb1, -(1.0 - be) * B.rb0, -be * B.rb1};
@@ -196,7 +198,7 @@ __device__ __forceinline__ ExtResult ext_block(const World& w, const Collide& c,
     const double rbar = xget(w.vstat, RBAR, vp, v);
     const V3 x{xget(X, CX, vp, v), xget(X, CY, vp, v), xget(X, CZ, vp, v)};
     const double W = dot(n3, x) - pl[3] - xget(X, S, vp, v) * rbar;
-    r.lam[0] = lam_in[0];
+    r.lam[0] = lam[b];
     if (!(W >= 0.0 && r.lam[0] == 0.0)) {
       const double ic = xget(w.vstat, IC, vp, v), is = xget(w.vstat, IS, vp, v);
       double M = 0.0;

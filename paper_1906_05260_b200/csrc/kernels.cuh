@@ -99,7 +99,7 @@ struct Collide {
   double* pin_data = nullptr;    // 4 x n_pins
   // external blocks: pins | contacts | half-planes
   long long ext_cap = 0;
-  double* ext_lam = nullptr;     // 3 x ext_cap
+  double* ext_lam = nullptr;     // 3 x ext_cap, SoA: component d of block b at [d * ext_cap + b]
   // Results are written per incidence entry q (slot-sorted), so the sweep's gather reads
   // contiguous entries instead of chasing block ids.
   double* ext_contrib = nullptr; // 4 x (4 x ext_cap): entry q -> dc xyz, ds (kExtNone markers)

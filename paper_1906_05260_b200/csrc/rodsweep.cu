@@ -853,12 +853,12 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
       for (int q = q0 + r; q < q1; q += 32 * kWarps) {
         const int item = c.ext_items[q];
         const int b = item >> 2, e = item & 3;
-        const ExtResult res = ext_block(w, c, cur, xr_cur, el_cur + 3ll * b, b, sp,
+        const ExtResult res = ext_block(w, c, cur, xr_cur, el_cur, c.ext_cap, b, sp,
                                         [&](int e2, int flag, double x, double y, double z, double ds) {
                                           if (e2 == e) put_entry(c, q, flag, x, y, z, ds);
                                         });
         if (e == res.owner) {  // the block's owner entry commits it
-          for (int d = 0; d < res.nlam; ++d) el_nxt[3ll * b + d] = res.lam[d];
+          for (int d = 0; d < res.nlam; ++d) el_nxt[d * c.ext_cap + b] = res.lam[d];
           if (res.singular) ++nsing;
           if (res.bad)
             bad = umin64(bad, err_code(sp.substep, ERR_SWEEP, it, static_cast<unsigned long long>(sp.elastic_blocks) + b));

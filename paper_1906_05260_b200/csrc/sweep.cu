@@ -85,7 +85,7 @@ __device__ double ext_residual(const World& w, const Collide& c, const double* X
   return dot(V3{pl[0], pl[1], pl[2]}, ldc(X, vp, v)) - pl[3] - F(X, S, vp, v) * F(w.vstat, RBAR, vp, v);
 }
 
-__global__ void __launch_bounds__(256, 3) k_ext_solve(World w, Collide c, const double* __restrict__ X,
+__global__ void __launch_bounds__(256, 4) k_ext_solve(World w, Collide c, const double* __restrict__ X,
                                                      SweepParams sp, int* singular, unsigned long long* err) {
   if (sp.pdl) {
     pdl_wait();
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(256, 3) k_ext_solve(World w, Collide c, const 
   const int n = npins + nct + c.scalars[SC_NHP];
   int nsing = 0;
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) {
-    double* lam = c.ext_lam + 3ll * b;
+    const long long ls = c.ext_cap;
     auto sing = [&]() {  // singular block (counted; per scene in a batch's last sweep)
       ++nsing;
       if (sp.scene_singular) atomicAdd(&sp.scene_singular[ext_scene(w, c, b, npins, nct)], 1);
@@ -113,10 +113,10 @@ __global__ void __launch_bounds__(256, 3) k_ext_solve(World w, Collide c, const 
         o[0].x = ext_none();
       }
     };
-    const ExtResult r = ext_block(w, c, X, w.xrec, lam, b, sp, [&](int e, int flag, double x, double y, double z, double ds) {
+    const ExtResult r = ext_block(w, c, X, w.xrec, c.ext_lam, ls, b, sp, [&](int e, int flag, double x, double y, double z, double ds) {
       put_at(c.ext_pos[4 * b + e], flag, x, y, z, ds);
     });
-    for (int d = 0; d < r.nlam; ++d) lam[d] = r.lam[d];
+    for (int d = 0; d < r.nlam; ++d) c.ext_lam[d * ls + b] = r.lam[d];
     if (r.singular) sing();
     if (r.bad)
       atomicMin(err, err_code(sp.substep, ERR_SWEEP, sp.iter, static_cast<unsigned long long>(elastic_blocks) + b));
@@ -169,9 +169,9 @@ __global__ void k_ext_count(Collide c, int npins) {
       c.ct_va[b - npins] = slots[0];
       c.ct_vb[b - npins] = slots[2];
     }
-    c.ext_lam[3ll * b] = 0.0;
-    c.ext_lam[3ll * b + 1] = 0.0;
-    c.ext_lam[3ll * b + 2] = 0.0;
+    c.ext_lam[b] = 0.0;  // SoA, stride ext_cap
+    c.ext_lam[c.ext_cap + b] = 0.0;
+    c.ext_lam[2 * c.ext_cap + b] = 0.0;
   }
 }
 __global__ void k_ext_fill(Collide c, int npins) {
