@@ -61,14 +61,25 @@ struct ExtResult {
   bool singular, bad;
 };
 
+// The per-substep constants of a contact block (solver.cpp:210-224): its pills, their first
+// slots (-1: kinematic), the frozen alpha / beta.
+struct ContactRef {
+  int a, b, va, vb;
+  double al, be;
+};
+__device__ __forceinline__ ContactRef contact_ref(const Collide& c, int k) {
+  return ContactRef{c.ct_a[k], c.ct_b[k], c.ct_va[k], c.ct_vb[k], c.ct_alpha[k], c.ct_beta[k]};
+}
+
 __device__ __forceinline__ double xget(const double* X, int f, int vp, int v) { return X[static_cast<long long>(f) * vp + v]; }
 
 // X: snapshot state rows (pins / half-planes); xrec: the matching slot records (contacts);
-// lam: the multipliers before the sweep, SoA (component d of block b at lam[d * ls + b]).
+// lam: the multipliers before the sweep, SoA (component d of block b at lam[d * ls + b]);
+// pre: the contact's constants if the caller has them at hand (else read from `c`).
 template <class Emit>
 __device__ __forceinline__ ExtResult ext_block(const World& w, const Collide& c, const double* X, const double* xrec,
                                                const double* lam, long long ls, int b, const SweepParams& sp,
-                                               Emit&& emit) {
+                                               Emit&& emit, const ContactRef* pre = nullptr) {
   using namespace vm;
   ExtResult r;
   r.singular = r.bad = false;
@@ -121,9 +132,10 @@ __device__ __forceinline__ ExtResult ext_block(const World& w, const Collide& c,
     const int k = b - npins;
     // endpoint slots were stored by k_ext_count: the slot records are one dependent load away
     double icA[2], isA[2], icB[2], isB[2];
-    const ExtGeom A = resolve_rec(xrec, c, c.ct_a[k], c.ct_va[k], icA, isA);
-    const ExtGeom B = resolve_rec(xrec, c, c.ct_b[k], c.ct_vb[k], icB, isB);
-    const double al = c.ct_alpha[k], be = c.ct_beta[k];
+    const ContactRef cr = pre ? *pre : contact_ref(c, k);
+    const ExtGeom A = resolve_rec(xrec, c, cr.a, cr.va, icA, isA);
+    const ExtGeom B = resolve_rec(xrec, c, cr.b, cr.vb, icB, isB);
+    const double al = cr.al, be = cr.be;
     const V3 ca = (1.0 - al) * A.c0 + al * A.c1;
     const V3 cb = (1.0 - be) * B.c0 + be * B.c1;
     const double ra = (1.0 - al) * A.r0 + al * A.r1;

@@ -82,6 +82,8 @@ __constant__ uint8_t kRowField[kStageRows] = {
     L_SZ0, L_SZ1, L_SZ2, L_CS, L_SS, L_VS0, L_VS1, L_VS2, L_BT0, L_BT1, L_BT2, L_SB, L_VBU, L_VBV};
 static_assert(kStageRows == 45, "row tables");
 
+constexpr int kTileEntries = 160;
+
 template <int TP>
 struct Tile {
   static constexpr int kTilePos = TP, kTileStage = TP + 2;
@@ -91,7 +93,17 @@ struct Tile {
   unsigned wmask[kTilePos / 32];  // OR of the kinds present, per 32 positions
   int klist[kKinds];              // the kinds present, ascending
   uint8_t act[kKinds][kTilePos];
-  int eoff[kTilePos];             // persistent kernel: incidence offsets of slots start .. start+TP-2
+};
+
+// The persistent kernel's tile: incidence offsets of the owned slots and the first kTileEntries
+// incidence entries, staged once per substep (item, contact constants), with their per-sweep
+// corrections.
+template <int TP>
+struct PTile : Tile<TP> {
+  int eoff[TP];
+  int e_item[kTileEntries];
+  ContactRef e_ref[kTileEntries];
+  alignas(16) double e_out[kTileEntries][4];  // read and written as double2
 };
 
 // Phase 0: per-position metadata of the tile (rod-local index, element count, kinds, block base),
@@ -691,13 +703,15 @@ __device__ __forceinline__ void gather_apply(const Tile<TP>& t, const World& w, 
 // issued before the first add (the markers only predicate the adds), so a slot's list costs one
 // latency per chunk.
 template <class AddC, class AddS>
-__device__ __forceinline__ void gather_entries(const Collide& c, int e0, int e1, AddC& addc, AddS& adds) {
+__device__ __forceinline__ void gather_entries(const Collide& c, int e0, int e1, AddC& addc, AddS& adds,
+                                               const double* local = nullptr, int local_q0 = 0, int local_n = 0) {
   for (int q0 = e0; q0 < e1; q0 += 4) {
     double2 o01[4], o23[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int q = q0 + u < e1 ? q0 + u : e0;
-      const double2* o = reinterpret_cast<const double2*>(c.ext_contrib + 4ll * q);
+      const int i = q - local_q0;  // entries staged in shared memory (persistent kernel)
+      const double2* o = reinterpret_cast<const double2*>(i >= 0 && i < local_n ? local + 4ll * i : c.ext_contrib + 4ll * q);
       o01[u] = o[0];
       o23[u] = o[1];
     }
@@ -711,10 +725,10 @@ __device__ __forceinline__ void gather_entries(const Collide& c, int e0, int e1,
   }
 }
 
-// Writes an endpoint's correction into its incidence entry q (flag 0 = no update from the block;
-// kExtNone in ds = no scale update).
-__device__ __forceinline__ void put_entry(const Collide& c, int q, int flag, double x, double y, double z, double ds) {
-  double2* o = reinterpret_cast<double2*>(c.ext_contrib + 4ll * q);
+// Writes an endpoint's correction into its incidence entry o (4 doubles; flag 0 = no update from
+// the block; kExtNone in ds = no scale update).
+__device__ __forceinline__ void put_entry(double* out, int flag, double x, double y, double z, double ds) {
+  double2* o = reinterpret_cast<double2*>(out);
   if (flag) {
     o[0] = make_double2(x, y);
     o[1] = make_double2(z, (flag & kExtScale) ? ds : ext_none());
@@ -805,13 +819,25 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
   constexpr int kWarps = warps_for<TP>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int kTileOwned = TP - 2, kTileStage = TP + 2;
-  Tile<TP>& t = *reinterpret_cast<Tile<TP>*>(smem_raw);
+  PTile<TP>& t = *reinterpret_cast<PTile<TP>*>(smem_raw);
   const int start = blockIdx.x * kTileOwned;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned mask = tile_meta(t, w, start);
   stage_rows(t, w, nullptr, nullptr, start, mask, T_SBAR, T_LAM);  // statics: once per substep
-  if (pp.has_ext)
+  int ent_q0 = 0, ent_n = 0;  // staged entries: [ent_q0, ent_q0 + ent_n)
+  if (pp.has_ext) {
+    const int q0 = c.ext_off[start], q1 = c.ext_off[min(start + kTileOwned, w.V)];
+    ent_q0 = q0;
+    ent_n = min(q1 - q0, kTileEntries);
+    const int npins = sp.n_pins, nct = c.scalars[SC_NCT];
     for (int i = tid; i <= kTileOwned; i += 32 * kWarps) t.eoff[i] = c.ext_off[min(start + i, w.V)];
+    for (int i = tid; i < ent_n; i += 32 * kWarps) {
+      const int item = c.ext_items[q0 + i];
+      t.e_item[i] = item;
+      const int b = item >> 2;
+      if (b >= npins && b < npins + nct) t.e_ref[i] = contact_ref(c, b - npins);
+    }
+  }
   for (int i = tid; i < kLamFields * kTileStage; i += 32 * kWarps) t.st[T_LAM + i / kTileStage][i % kTileStage] = 0.0;
   const int has_ext = pp.has_ext;
   double* cur = pp.X;
@@ -851,12 +877,17 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
       const int r = (kWarps == 8 ? kOrder[warp] : warp) * 32 + lane;
       const int q0 = t.eoff[0], q1 = t.eoff[kTileOwned];
       for (int q = q0 + r; q < q1; q += 32 * kWarps) {
-        const int item = c.ext_items[q];
+        const int i = q - ent_q0;
+        const bool staged = i < ent_n;
+        const int item = staged ? t.e_item[i] : c.ext_items[q];
         const int b = item >> 2, e = item & 3;
-        const ExtResult res = ext_block(w, c, cur, xr_cur, el_cur, c.ext_cap, b, sp,
-                                        [&](int e2, int flag, double x, double y, double z, double ds) {
-                                          if (e2 == e) put_entry(c, q, flag, x, y, z, ds);
-                                        });
+        double* out = staged ? t.e_out[i] : c.ext_contrib + 4ll * q;
+        const ExtResult res = ext_block(
+            w, c, cur, xr_cur, el_cur, c.ext_cap, b, sp,
+            [&](int e2, int flag, double x, double y, double z, double ds) {
+              if (e2 == e) put_entry(out, flag, x, y, z, ds);
+            },
+            staged && b >= sp.n_pins && b < sp.n_pins + c.scalars[SC_NCT] ? &t.e_ref[i] : nullptr);
         if (e == res.owner) {  // the block's owner entry commits it
           for (int d = 0; d < res.nlam; ++d) el_nxt[d * c.ext_cap + b] = res.lam[d];
           if (res.singular) ++nsing;
@@ -868,7 +899,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
     solve_items<TP, true>(t, w, sp, start, mask, singular + it, err, ext_entries);  // ends with __syncthreads()
     mark();
     gather_apply(t, w, sp, start, nxt, has_ext ? xr_nxt : nullptr, [&](int p, auto& addc, auto& adds) {
-      if (has_ext) gather_entries(c, t.eoff[p - start], t.eoff[p - start + 1], addc, adds);
+      if (has_ext) gather_entries(c, t.eoff[p - start], t.eoff[p - start + 1], addc, adds, &t.e_out[0][0], ent_q0, ent_n);
     });
     mark();
     if (pp.trace && it == 1 && tid == 0) pp.trace[700 + blockIdx.x] = gtimer();
@@ -939,7 +970,7 @@ int persistent_tiles(const World& w) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem = sizeof(Tile<kPersistTP>);
+  const size_t smem = sizeof(PTile<kPersistTP>);
   if (cudaFuncSetAttribute(k_iterate<kPersistTP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iterate<kPersistTP>, 32 * warps_for<kPersistTP>(), smem) !=
       cudaSuccess)
@@ -953,7 +984,7 @@ void launch_iterate_persistent(const World& w, Collide& c, const Groups& g, cons
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles);
   cfg.blockDim = dim3(32 * warps_for<kPersistTP>());
-  cfg.dynamicSmemBytes = sizeof(Tile<kPersistTP>);
+  cfg.dynamicSmemBytes = sizeof(PTile<kPersistTP>);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barriers)
