@@ -93,6 +93,7 @@ struct Tile {
   unsigned wmask[kTilePos / 32];  // OR of the kinds present, per 32 positions
   int klist[kKinds];              // the kinds present, ascending
   uint8_t act[kKinds][kTilePos];
+  alignas(8) unsigned long long bar;  // mbarrier of the bulk (TMA) staging
 };
 
 // The persistent kernel's tile: incidence offsets of the owned slots and the first kTileEntries
@@ -174,6 +175,53 @@ struct NoPost {
 };
 
 // post(nsing, bad): extra per-thread work after the items, counted in the same reduction.
+// ---- 1D bulk copies (TMA engine) global -> shared, completion on an mbarrier ----------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// Interior tiles of the per-sweep kernel: every needed row segment (TP + 2 doubles, 16-byte
+// aligned, a multiple of 16 bytes) is ONE bulk copy issued by the lanes of warp 0, all
+// completing on the tile's mbarrier (initialised by tile_meta's caller). A handful of
+// instructions per row instead of a cp.async loop per thread.
+template <int TP>
+__device__ __forceinline__ void stage_rows_bulk(Tile<TP>& t, const World& w, const double* X, const double* lam_in,
+                                                int start, unsigned mask) {
+  constexpr unsigned kBytes = (TP + 2) * sizeof(double);
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    unsigned total = 0;
+    for (int r = 0; r < kStageRows; ++r) total += (kRowNeed[r] & mask) ? kBytes : 0u;
+    if (lane == 0) mbar_arrive_expect(&t.bar, total);
+    __syncwarp();
+    for (int r = lane; r < kStageRows; r += 32) {
+      if (!(kRowNeed[r] & mask)) continue;
+      const int arr = kRowArr[r];
+      const double* row = (arr == 0 ? X : arr == 1 ? w.vstat : arr == 2 ? w.estat : lam_in) +
+                          static_cast<long long>(kRowField[r]) * w.vpad;
+      bulk_g2s(&t.st[r][0], row + (start - 2), kBytes, &t.bar);
+    }
+  }
+}
+
 template <int TP, bool kLamSmem, class Post = NoPost>
 __device__ __forceinline__ void solve_items(Tile<TP>& t, const World& w, const SweepParams& sp, int start, unsigned mask,
                                             int* singular, unsigned long long* err, Post&& post = Post()) {
@@ -556,8 +604,11 @@ __device__ __forceinline__ void solve_items(Tile<TP>& t, const World& w, const S
       }
     }
   }
+  if (sp.dbg && (blockIdx.x == 0 || blockIdx.x == 27) && (threadIdx.x & 31) == 0)
+    sp.dbg[(blockIdx.x ? 32 : 0) + (threadIdx.x >> 5)] = gtimer();
   post(nsing, bad);
-  if (sp.dbg && blockIdx.x == 0 && (threadIdx.x & 31) == 0) sp.dbg[threadIdx.x >> 5] = gtimer();
+  if (sp.dbg && (blockIdx.x == 0 || blockIdx.x == 27) && (threadIdx.x & 31) == 0)
+    sp.dbg[(blockIdx.x ? 48 : 16) + (threadIdx.x >> 5)] = gtimer();
   if (__any_sync(0xffffffffu, nsing != 0 || bad != kNoError)) {  // rare: singular blocks / errors
     for (int o = 16; o > 0; o >>= 1) {
       nsing += __shfl_down_sync(0xffffffffu, nsing, o);
@@ -753,8 +804,15 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
   const int V = w.V;
   const int start = blockIdx.x * kTileOwned;
   const int tid = threadIdx.x;
+  // interior tiles stage with bulk copies: the whole window [start-2, start+TP) lies inside
+  // every row's allocation (rows are vpad doubles)
+  const bool bulk = start >= 2 && start + TP <= w.vpad;
+  if (bulk && tid == 0) mbar_init(&t.bar);  // made visible by tile_meta's __syncthreads
   const unsigned mask = tile_meta(t, w, start);
-  stage_rows(t, w, X, sp.lam_in, start, mask, 0, kStageRows);
+  if (bulk)
+    stage_rows_bulk(t, w, X, sp.lam_in, start, mask);
+  else
+    stage_rows(t, w, X, sp.lam_in, start, mask, 0, kStageRows);
   // The ext solve of this iteration (the predecessor) writes the tile's incidence entries.
   // Large worlds (64-wide tiles, bandwidth-bound): wait for it here and prefetch the tile's
   // entry range into L2 so the gather after the block solves finds it on chip. Small worlds
@@ -772,7 +830,10 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
     for (const char* a = lo + 128ll * tid; a < hi; a += 128ll * 32 * kWarps)
       asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a));
   }
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  if (bulk)
+    mbar_wait(&t.bar, 0);
+  else
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
 
   solve_items<TP, false>(t, w, sp, start, mask, singular, err);
@@ -896,6 +957,8 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
         }
       }
     };
+    sp.dbg = pp.trace && it == 1 ? pp.trace + 900 : nullptr;  // debug trace (VROD_TRACE=1)
+    if (sp.dbg && (blockIdx.x == 0 || blockIdx.x == 27) && tid == 0) pp.trace[blockIdx.x ? 898 : 899] = gtimer();
     solve_items<TP, true>(t, w, sp, start, mask, singular + it, err, ext_entries);  // ends with __syncthreads()
     mark();
     gather_apply(t, w, sp, start, nxt, has_ext ? xr_nxt : nullptr, [&](int p, auto& addc, auto& adds) {

@@ -54,12 +54,8 @@ for l in range(2):
     if ph[0] > 0:
         print(f"shape level/chain pos {l} group phases us: centroid {(ph[1]-ph[0])/1e3:.2f} covariance {(ph[2]-ph[1])/1e3:.2f} "
               f"rotation {(ph[3]-ph[2])/1e3:.2f} ({int(raw[606 + 8 * l])} it) scale {(ph[4]-ph[3])/1e3:.2f} apply {(ph[5]-ph[4])/1e3:.2f}")
-t0 = raw[899]
-if t0 > 0:
-    print("iteration 1, CTA 0: per-warp end of block solves (us after staging):",
-          [round((raw[900 + k] - t0) / 1e3, 2) for k in range(8)])
-if raw[908] > 0:
-    a = [(raw[908 + k] - t0) / 1e3 for k in range(8)]
-    b = [(raw[916 + k] - raw[908 + k]) / 1e3 for k in range(8)]
-    c = [(raw[924 + k] - raw[916 + k]) / 1e3 for k in range(8)]
-    print("pass 1/2/3 per warp us:", [round(x, 2) for x in a], [round(x, 2) for x in b], [round(x, 2) for x in c])
+for cta, base, t0i in ((0, 900, 899), (27, 932, 898)):
+    t0 = raw[t0i]
+    if t0 > 0:
+        print(f"iteration 1, CTA {cta}: per-warp end of items / of ext entries (us after staging):",
+              [round((raw[base + k] - t0) / 1e3, 2) for k in range(8)], [round((raw[base + 16 + k] - t0) / 1e3, 2) for k in range(8)])
