@@ -173,12 +173,18 @@ def run_reference(args, rank, world):
         return
     from paper_1906_05260_b200 import capi, workloads
     from paper_1906_05260_b200.handle import SolverHandle
-    kind, path = ("reference", REF_LIB) if os.path.exists(REF_LIB) else ("port", ORACLE_LIB)
-    # The reference's only multi-core knob, VROD_THREADS > 1 (parallel.h:12-21), crashes: the
-    # `static thread_local` update buffer of jacobi_sweep (constraints.cpp:497-500) is resized on
-    # the calling thread only, and the pool's workers index their own empty copy. One thread is
-    # therefore all the host threads the reference can use.
-    threads = 1
+    # The reference's CPU path is timed through its bitwise-identical restatement (oracle/, "port")
+    # on all host threads: the reference's own block-solve threads (VROD_THREADS > 1, parallel.h)
+    # crash on the `static thread_local` update buffer of jacobi_sweep (constraints.cpp:497-500:
+    # resized on the calling thread only), and oracle/_ref — the reference's sources compiled
+    # here — links an Eigen SUBSET SHIM whose dynamic-shape matrices run ~5-10x slower than
+    # Eigen's fixed-size expressions, so it would understate the reference's speed.
+    # The restatement runs the reference's parallel_for over the block solves (VROD_THREADS).
+    # VROD_REF_IMPL=shim times oracle/_ref instead (1 thread).
+    if os.environ.get("VROD_REF_IMPL") == "shim" and os.path.exists(REF_LIB):
+        kind, path, threads = "reference", REF_LIB, 1
+    else:
+        kind, path, threads = "port", ORACLE_LIB, os.cpu_count() or 1
     os.environ["VROD_THREADS"] = str(threads)
     lib = capi.bind(C.CDLL(path))
     scene = workloads.c3_muscle_bundle(lib)

@@ -18,6 +18,7 @@
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <unordered_map>
 #include <vector>
@@ -1004,14 +1005,47 @@ struct SweepOutcome {
   int active = 0, skipped_singular = 0;
 };
 
-// jacobi_sweep, constraints.cpp:491-556 (single-threaded: VROD_THREADS unset).
+// thread_count / parallel_for, parallel.h:12-46: VROD_THREADS workers (clamped to the hardware),
+// contiguous chunks, index-addressed results — so the outcome is independent of scheduling. (The
+// reference's own multi-threaded run crashes on its thread_local update buffer, DESIGN.md §2;
+// this restatement keeps one shared buffer.)
+int thread_count() {
+  static const int cached = [] {
+    const char* env = std::getenv("VROD_THREADS");
+    if (!env) return 1;
+    const int hw = std::max(1u, std::thread::hardware_concurrency());
+    return std::clamp(std::atoi(env), 1, hw);
+  }();
+  return cached;
+}
+template <typename Fn>
+void parallel_for(int n, int threads, Fn&& fn) {
+  if (n <= 0) return;
+  if (threads <= 1 || n == 1) {
+    for (int i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  threads = std::min(threads, n);
+  std::vector<std::thread> pool;
+  const int chunk = (n + threads - 1) / threads;
+  for (int t = 0; t < threads; ++t) {
+    const int b = t * chunk, e = std::min(n, b + chunk);
+    if (b >= e) break;
+    pool.emplace_back([b, e, &fn] {
+      for (int i = b; i < e; ++i) fn(i);
+    });
+  }
+  for (std::thread& th : pool) th.join();
+}
+
+// jacobi_sweep, constraints.cpp:491-556 (block solves on VROD_THREADS workers, :497-500).
 SweepOutcome jacobi_sweep(std::vector<Block>& blocks, std::vector<Rod>& rods, const Ctx& ctx, double h,
                           double beta, Scratch& sc) {
   const Layout& L = *ctx.L;
   const int n = static_cast<int>(blocks.size());
   SweepOutcome out;
   std::vector<Update> ups(static_cast<std::size_t>(n));
-  for (int i = 0; i < n; ++i) ups[i] = solve_block(blocks[i], ctx, h, beta);
+  parallel_for(n, thread_count(), [&](int i) { ups[i] = solve_block(blocks[i], ctx, h, beta); });
   std::fill(sc.csum.begin(), sc.csum.end(), V3{});
   std::fill(sc.ssum.begin(), sc.ssum.end(), 0.0);
   std::fill(sc.tsum.begin(), sc.tsum.end(), V3{});

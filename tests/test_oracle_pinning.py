@@ -139,3 +139,22 @@ def test_make_rest_pose_bitwise(ref, oracle):
         ra, rb = make_rest_pose(ref, c, r, s), make_rest_pose(oracle, c, r, s)
         for k in ra.__dict__:
             np.testing.assert_array_equal(getattr(ra, k), getattr(rb, k))
+
+
+def test_restatement_threads_do_not_change_results():
+    """The restatement's block solves run on VROD_THREADS workers (parallel.h:26-46, used by
+    bench.py --impl reference); results must not depend on the thread count."""
+    import hashlib
+    import sys
+    code = ("import ctypes as C, hashlib, sys; sys.path.insert(0, %r); sys.path.insert(0, %r);"
+            "from paper_1906_05260_b200 import capi; from paper_1906_05260_b200.handle import SolverHandle;"
+            "from scenes import SCENES; lib = capi.bind(C.CDLL(%r)); h = SolverHandle(lib, SCENES['mini_muscle'](lib));"
+            "[h.step() for _ in range(3)]; s = h.state();"
+            "print(hashlib.sha256(b''.join(s[k].tobytes() for k in sorted(s))).hexdigest())") % (
+        ROOT, os.path.join(ROOT, "tests"), os.path.join(ROOT, "oracle", "lib", "libvrod_oracle.so"))
+    outs = []
+    for t in ("1", "4"):
+        env = dict(os.environ, VROD_THREADS=t)
+        outs.append(subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                                   check=True).stdout.strip())
+    assert outs[0] == outs[1] and len(outs[0]) == 64
