@@ -194,9 +194,10 @@ VHD double inverse_stiffness(double k) {
 // 3x3 solve of solve_block's dim-3 branch (constraints.cpp:446-454): singular test on Eigen's
 // determinant, cofactor inverse, dlambda = beta * M^-1 * rhs.
 VHD bool solve3(const double (&M)[3][3], const double (&rhs)[3], double beta, double (&dl)[3]) {
-  double md = fabs(M[0][0]);
-  for (int j = 0; j < 3; ++j)
-    for (int i = 0; i < 3; ++i) md = fmax(md, fabs(M[i][j]));
+  // max |M_ij| as a tree (max is order-independent; fmax ignores NaN either way)
+  const double m01 = fmax(fabs(M[0][0]), fabs(M[0][1])), m23 = fmax(fabs(M[0][2]), fabs(M[1][0]));
+  const double m45 = fmax(fabs(M[1][1]), fabs(M[1][2])), m67 = fmax(fabs(M[2][0]), fabs(M[2][1]));
+  double md = fmax(fmax(fmax(m01, m23), fmax(m45, m67)), fabs(M[2][2]));
   md = fmax(md, 1e-300);
   const double det = M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) -
                      M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
