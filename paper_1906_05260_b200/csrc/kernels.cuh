@@ -186,6 +186,9 @@ struct PersistParams {
   double* xrec[2];         // slot records: [0] = w.xrec (written by predict), [1] its partner
   double* lam_ext[2];      // external-block multipliers: [0] = c.ext_lam (zeroed by ext setup)
   unsigned* bar;           // grid-barrier counter (zeroed before each launch)
+  unsigned* ext_done;      // aux CTAs' external-block releases (zeroed before each launch)
+  int tiles;               // tile CTAs; CTAs tiles .. tiles+n_aux-1 are aux CTAs
+  int n_aux;
   int iterations;
   int sm_period;
   int levels;              // shape-matching levels (<= kMaxPersistLevels)
@@ -286,6 +289,7 @@ int report_parts(int V);
 // rodsweep.cu: persistent iteration loop for small single-scene worlds. persistent_tiles()
 // returns the number of co-resident tiles the world needs, or 0 when it does not fit.
 int persistent_tiles(const World& w);
+int persistent_aux_ctas(const World& w);
 void launch_iterate_persistent(const World& w, Collide& c, const Groups& g, const PersistParams& pp, const SweepParams& sp,
                                int* singular_counters, unsigned long long* err, cudaStream_t st);
 

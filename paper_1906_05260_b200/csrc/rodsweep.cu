@@ -873,6 +873,60 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& target) {
 // and only the block's owner entry commits its multiplier (ping-pong lam_ext[2]) and counts
 // singular / non-finite outcomes. The slot records are ping-ponged too (xrec[2]), so blocks
 // solved by other tiles during a sweep always see the snapshot.
+// Aux CTAs (the SMs the tiles leave idle): all external blocks of the sweep, one thread per
+// block (ext_block, the k_ext_solve code), corrections into the slot-sorted incidence entries;
+// then a release of `ext_done` for the tiles' gathers.
+template <int TP>
+__device__ __forceinline__ void aux_ext_phase(const World& w, const Collide& c, const PersistParams& pp,
+                                              const SweepParams& sp, const double* cur, const double* xr_cur,
+                                              const double* el_cur, double* el_nxt, int it, int* singular,
+                                              unsigned long long* err) {
+  constexpr int kThreadsPerCta = 32 * warps_for<TP>();
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int npins = sp.n_pins, nct = c.scalars[SC_NCT];
+  const int n = npins + nct + c.scalars[SC_NHP];
+  int nsing = 0;
+  unsigned long long bad = kNoError;
+  for (int b = (blockIdx.x - pp.tiles) * kThreadsPerCta + tid; b < n; b += pp.n_aux * kThreadsPerCta) {
+    const ExtResult r = ext_block(w, c, cur, xr_cur, el_cur, c.ext_cap, b, sp,
+                                  [&](int e, int flag, double x, double y, double z, double ds) {
+                                    put_entry(c.ext_contrib + 4ll * c.ext_pos[4 * b + e], flag, x, y, z, ds);
+                                  });
+    for (int d = 0; d < r.nlam; ++d) el_nxt[d * c.ext_cap + b] = r.lam[d];
+    if (r.singular) ++nsing;
+    if (r.bad) bad = umin64(bad, err_code(sp.substep, ERR_SWEEP, it, static_cast<unsigned long long>(sp.elastic_blocks) + b));
+  }
+  if (__any_sync(0xffffffffu, nsing != 0 || bad != kNoError)) {
+    for (int o = 16; o > 0; o >>= 1) {
+      nsing += __shfl_down_sync(0xffffffffu, nsing, o);
+      bad = umin64(bad, __shfl_down_sync(0xffffffffu, bad, o));
+    }
+    if (lane == 0) {
+      if (nsing) atomicAdd(singular, nsing);
+      if (bad != kNoError) atomicMin(err, bad);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    atomicAdd(pp.ext_done, 1u);
+  }
+}
+
+// The whole iteration loop of one substep (solver.cpp:330-339) for small single-scene worlds,
+// in ONE launch: one CTA per tile, all CTAs co-resident, a grid barrier after each sweep and
+// after each shape-matching phase. What the per-launch path moves through HBM every sweep
+// stays on chip: the tile's static rows are staged once, the elastic multipliers live in the
+// tile's shared rows (never written back; they are reset every substep anyway).
+//
+// When SMs are left over (pp.n_aux > 0, e.g. C3: 128 tiles + 20 aux CTAs on 148 SMs), the aux
+// CTAs solve the external blocks during each sweep (released to the tiles through ext_done, so
+// the tiles with contacts no longer finish late) and run the shape matching; their small code
+// stays hot in their instruction caches. Otherwise (n_aux = 0) every incidence entry of a
+// tile's owned slots re-solves its block in the tile (ext_block — the same arithmetic as
+// k_ext_solve, so the same bits) and only the block's owner entry commits its multiplier
+// (ping-pong lam_ext[2]) and counts; all CTAs share the shape work. The slot records are
+// ping-ponged (xrec[2]), so blocks solved elsewhere during a sweep always see the snapshot.
 template <int TP>
 __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Collide c, Groups g, PersistParams pp,
                                                                       SweepParams sp, int* singular,
@@ -881,26 +935,33 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int kTileOwned = TP - 2, kTileStage = TP + 2;
   PTile<TP>& t = *reinterpret_cast<PTile<TP>*>(smem_raw);
-  const int start = blockIdx.x * kTileOwned;
+  const bool is_aux = blockIdx.x >= pp.tiles;
+  const bool inline_ext = pp.n_aux == 0;
+  const int start = is_aux ? 0 : blockIdx.x * kTileOwned;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned mask = tile_meta(t, w, start);
-  stage_rows(t, w, nullptr, nullptr, start, mask, T_SBAR, T_LAM);  // statics: once per substep
-  int ent_q0 = 0, ent_n = 0;  // staged entries: [ent_q0, ent_q0 + ent_n)
-  if (pp.has_ext) {
-    const int q0 = c.ext_off[start], q1 = c.ext_off[min(start + kTileOwned, w.V)];
-    ent_q0 = q0;
-    ent_n = min(q1 - q0, kTileEntries);
-    const int npins = sp.n_pins, nct = c.scalars[SC_NCT];
-    for (int i = tid; i <= kTileOwned; i += 32 * kWarps) t.eoff[i] = c.ext_off[min(start + i, w.V)];
-    for (int i = tid; i < ent_n; i += 32 * kWarps) {
-      const int item = c.ext_items[q0 + i];
-      t.e_item[i] = item;
-      const int b = item >> 2;
-      if (b >= npins && b < npins + nct) t.e_ref[i] = contact_ref(c, b - npins);
-    }
-  }
-  for (int i = tid; i < kLamFields * kTileStage; i += 32 * kWarps) t.st[T_LAM + i / kTileStage][i % kTileStage] = 0.0;
   const int has_ext = pp.has_ext;
+  unsigned mask = 0;
+  int ent_q0 = 0, ent_n = 0;  // staged entries: [ent_q0, ent_q0 + ent_n)
+  if (!is_aux) {
+    mask = tile_meta(t, w, start);
+    stage_rows(t, w, nullptr, nullptr, start, mask, T_SBAR, T_LAM);  // statics: once per substep
+    if (has_ext) {
+      for (int i = tid; i <= kTileOwned; i += 32 * kWarps) t.eoff[i] = c.ext_off[min(start + i, w.V)];
+      const int q0 = c.ext_off[start], q1 = c.ext_off[min(start + kTileOwned, w.V)];
+      ent_q0 = q0;
+      ent_n = min(q1 - q0, kTileEntries);
+      if (inline_ext) {
+        const int npins = sp.n_pins, nct = c.scalars[SC_NCT];
+        for (int i = tid; i < ent_n; i += 32 * kWarps) {
+          const int item = c.ext_items[q0 + i];
+          t.e_item[i] = item;
+          const int b = item >> 2;
+          if (b >= npins && b < npins + nct) t.e_ref[i] = contact_ref(c, b - npins);
+        }
+      }
+    }
+    for (int i = tid; i < kLamFields * kTileStage; i += 32 * kWarps) t.st[T_LAM + i / kTileStage][i % kTileStage] = 0.0;
+  }
   double* cur = pp.X;
   double* nxt = pp.Y;
   double* xr_cur = pp.xrec[0];
@@ -921,51 +982,72 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
   if (pp.trace && blockIdx.x == 0 && tid == 0) pp.trace[598] = g.nchains > 0 ? 1 : pp.levels;
   for (int it = 0; it < pp.iterations; ++it) {
     sp.iter = it;
-    if (it > 0) {
-      for (int i = tid; i < kKinds * TP; i += 32 * kWarps) t.act[i / TP][i % TP] = 0;
-    }
-    stage_rows(t, w, cur, nullptr, start, mask, 0, T_SBAR);
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncthreads();
-    mark();
-    // External blocks: every incidence entry of the tile's owned slots (a contiguous range)
-    // re-solves its block on the snapshot, one thread per entry, after that thread's elastic
-    // items — entries go to the warps of the cheapest kinds first — and writes its endpoint's
-    // correction into the entry; the block's owner entry commits the multiplier and counts.
-    auto ext_entries = [&](int& nsing, unsigned long long& bad) {
-      if (!has_ext) return;
-      constexpr int kOrder[8] = {7, 0, 1, 5, 6, 2, 3, 4};  // rank of warp w (CS, SS, SB, VB.. first)
-      const int r = (kWarps == 8 ? kOrder[warp] : warp) * 32 + lane;
-      const int q0 = t.eoff[0], q1 = t.eoff[kTileOwned];
-      for (int q = q0 + r; q < q1; q += 32 * kWarps) {
-        const int i = q - ent_q0;
-        const bool staged = i < ent_n;
-        const int item = staged ? t.e_item[i] : c.ext_items[q];
-        const int b = item >> 2, e = item & 3;
-        double* out = staged ? t.e_out[i] : c.ext_contrib + 4ll * q;
-        const ExtResult res = ext_block(
-            w, c, cur, xr_cur, el_cur, c.ext_cap, b, sp,
-            [&](int e2, int flag, double x, double y, double z, double ds) {
-              if (e2 == e) put_entry(out, flag, x, y, z, ds);
-            },
-            staged && b >= sp.n_pins && b < sp.n_pins + c.scalars[SC_NCT] ? &t.e_ref[i] : nullptr);
-        if (e == res.owner) {  // the block's owner entry commits it
-          for (int d = 0; d < res.nlam; ++d) el_nxt[d * c.ext_cap + b] = res.lam[d];
-          if (res.singular) ++nsing;
-          if (res.bad)
-            bad = umin64(bad, err_code(sp.substep, ERR_SWEEP, it, static_cast<unsigned long long>(sp.elastic_blocks) + b));
-        }
+    if (is_aux) {
+      if (has_ext) aux_ext_phase<TP>(w, c, pp, sp, cur, xr_cur, el_cur, el_nxt, it, singular + it, err);
+    } else {
+      if (it > 0) {
+        for (int i = tid; i < kKinds * TP; i += 32 * kWarps) t.act[i / TP][i % TP] = 0;
       }
-    };
-    sp.dbg = pp.trace && it == 1 ? pp.trace + 900 : nullptr;  // debug trace (VROD_TRACE=1)
-    if (sp.dbg && (blockIdx.x == 0 || blockIdx.x == 27) && tid == 0) pp.trace[blockIdx.x ? 898 : 899] = gtimer();
-    solve_items<TP, true>(t, w, sp, start, mask, singular + it, err, ext_entries);  // ends with __syncthreads()
-    mark();
-    gather_apply(t, w, sp, start, nxt, has_ext ? xr_nxt : nullptr, [&](int p, auto& addc, auto& adds) {
-      if (has_ext) gather_entries(c, t.eoff[p - start], t.eoff[p - start + 1], addc, adds, &t.e_out[0][0], ent_q0, ent_n);
-    });
-    mark();
-    if (pp.trace && it == 1 && tid == 0) pp.trace[700 + blockIdx.x] = gtimer();
+      stage_rows(t, w, cur, nullptr, start, mask, 0, T_SBAR);
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      __syncthreads();
+      mark();
+      // Inline external blocks: every incidence entry of the tile's owned slots (a contiguous
+      // range) re-solves its block on the snapshot, one thread per entry, after that thread's
+      // elastic items — entries go to the warps of the cheapest kinds first — and writes its
+      // endpoint's correction into the entry; the block's owner entry commits the multiplier.
+      auto ext_entries = [&](int& nsing, unsigned long long& bad) {
+        if (!has_ext || !inline_ext) return;
+        constexpr int kOrder[8] = {7, 0, 1, 5, 6, 2, 3, 4};  // rank of warp w (CS, SS, SB, VB.. first)
+        const int r = (kWarps == 8 ? kOrder[warp] : warp) * 32 + lane;
+        const int q0 = t.eoff[0], q1 = t.eoff[kTileOwned];
+        for (int q = q0 + r; q < q1; q += 32 * kWarps) {
+          const int i = q - ent_q0;
+          const bool staged = i < ent_n;
+          const int item = staged ? t.e_item[i] : c.ext_items[q];
+          const int b = item >> 2, e = item & 3;
+          double* out = staged ? t.e_out[i] : c.ext_contrib + 4ll * q;
+          const ExtResult res = ext_block(
+              w, c, cur, xr_cur, el_cur, c.ext_cap, b, sp,
+              [&](int e2, int flag, double x, double y, double z, double ds) {
+                if (e2 == e) put_entry(out, flag, x, y, z, ds);
+              },
+              staged && b >= sp.n_pins && b < sp.n_pins + c.scalars[SC_NCT] ? &t.e_ref[i] : nullptr);
+          if (e == res.owner) {  // the block's owner entry commits it
+            for (int d = 0; d < res.nlam; ++d) el_nxt[d * c.ext_cap + b] = res.lam[d];
+            if (res.singular) ++nsing;
+            if (res.bad)
+              bad = umin64(bad, err_code(sp.substep, ERR_SWEEP, it, static_cast<unsigned long long>(sp.elastic_blocks) + b));
+          }
+        }
+      };
+      sp.dbg = pp.trace && it == 1 ? pp.trace + 900 : nullptr;  // debug trace (VROD_TRACE=1)
+      if (sp.dbg && (blockIdx.x == 0 || blockIdx.x == 27) && tid == 0) pp.trace[blockIdx.x ? 898 : 899] = gtimer();
+      solve_items<TP, true>(t, w, sp, start, mask, singular + it, err, ext_entries);  // ends with __syncthreads()
+      mark();
+      if (has_ext && !inline_ext) {  // the aux CTAs' external blocks of this sweep
+        if (tid == 0) {
+          const unsigned want = (it + 1u) * static_cast<unsigned>(pp.n_aux);
+          unsigned v;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(pp.ext_done) : "memory");
+          } while (v < want);
+        }
+        __syncthreads();
+        // the tile's entries in one coalesced copy (all loads in flight), then the gather reads
+        // them from shared memory
+        const double2* src = reinterpret_cast<const double2*>(c.ext_contrib + 4ll * ent_q0);
+        double2* dst = reinterpret_cast<double2*>(&t.e_out[0][0]);
+        for (int i = tid; i < 2 * ent_n; i += 32 * kWarps) dst[i] = __ldcg(src + i);
+        __syncthreads();
+      }
+      gather_apply(t, w, sp, start, nxt, has_ext ? xr_nxt : nullptr, [&](int p, auto& addc, auto& adds) {
+        if (has_ext)
+          gather_entries(c, t.eoff[p - start], t.eoff[p - start + 1], addc, adds, &t.e_out[0][0], ent_q0, ent_n);
+      });
+      mark();
+      if (pp.trace && it == 1 && tid == 0) pp.trace[700 + blockIdx.x] = gtimer();
+    }
     grid_sync(pp.bar, target);
     mark();
     double* tmp = cur;
@@ -979,14 +1061,16 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
     el_nxt = tmp;
     if (g.G > 0 && (it + 1) % pp.sm_period == 0) {  // shape matching (shape.cuh)
       // One warp per work unit: a dependency chain of groups (one barrier in all), or one group
-      // of the current level (a barrier per level). A single call site keeps one copy of the
-      // group code in the kernel.
-      const int gw = warp * gridDim.x + blockIdx.x, nw = kWarps * gridDim.x;
+      // of the current level (a barrier per level); the aux CTAs' warps when there are any. A
+      // single call site keeps one copy of the group code in the kernel.
+      const bool workers = inline_ext || is_aux;
+      const int ncta = inline_ext ? gridDim.x : pp.n_aux, cta = inline_ext ? blockIdx.x : blockIdx.x - pp.tiles;
+      const int gw = warp * ncta + cta, nw = kWarps * ncta;
       const bool chains = g.nchains > 0;
       const int phases = chains ? 1 : pp.levels;
       for (int l = 0; l < phases; ++l) {
         const int u0 = chains ? 0 : pp.level_off[l], u1 = chains ? g.nchains : pp.level_off[l + 1];
-        for (int u = u0 + gw; u < u1; u += nw) {
+        for (int u = u0 + gw; workers && u < u1; u += nw) {
           const int k0 = chains ? g.chain_off[u] : u, k1 = chains ? g.chain_off[u + 1] : u + 1;
           for (int k = k0; k < k1; ++k) {
             const bool tr = pp.trace && it == 1 && (chains ? u == 28 : u == u0);
@@ -1027,6 +1111,16 @@ void launch_rod_sweep(const World& w, Collide& c, const double* X, double* Y, co
     launch_tiles<32>(w, c, X, Y, sp, singular_counter, err, st);
 }
 
+int persistent_aux_ctas(const World& w) {
+  // the SMs the tiles leave idle (one CTA per SM), at least 2 to be worth it, at most 32
+  const int tiles = (w.V + kPersistTP - 3) / (kPersistTP - 2);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int spare = sms - tiles;
+  return spare >= 2 ? (spare > 32 ? 32 : spare) : 0;
+}
+
 int persistent_tiles(const World& w) {
   if (w.n_scenes != 1 || w.V <= 0) return 0;
   const int tiles = (w.V + kPersistTP - 3) / (kPersistTP - 2);
@@ -1043,9 +1137,9 @@ int persistent_tiles(const World& w) {
 
 void launch_iterate_persistent(const World& w, Collide& c, const Groups& g, const PersistParams& pp, const SweepParams& sp,
                                int* singular_counters, unsigned long long* err, cudaStream_t st) {
-  const int tiles = (w.V + kPersistTP - 3) / (kPersistTP - 2);  // pp.bar must be zero (Solver's fill)
+  // pp.bar and pp.ext_done must be zero (Solver's fill)
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(tiles);
+  cfg.gridDim = dim3(pp.tiles + pp.n_aux);
   cfg.blockDim = dim3(32 * warps_for<kPersistTP>());
   cfg.dynamicSmemBytes = sizeof(PTile<kPersistTP>);
   cfg.stream = st;

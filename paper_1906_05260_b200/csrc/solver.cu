@@ -336,7 +336,12 @@ Solver::Solver(const SceneData& scene, const BatchLayout* batch) : scene_(scene)
   if (persist_tiles_ > 0) {
     xrec2_ = dalloc<double>(8ull * w_.vpad);
     ext_lam2_ = dalloc<double>(3 * std::max(c_.ext_cap, 1ll));
-    d_bar_ = dalloc<unsigned>(1);
+    d_bar_ = dalloc<unsigned>(2);  // grid barrier, aux ext releases
+    // aux CTAs (external blocks + shape matching on the SMs the tiles leave idle) are opt-in:
+    // measured at C3 they do not beat the inline scheme (586 vs 566 us/step), VROD_PERSIST_AUX=1
+    persist_aux_ = (std::getenv("VROD_PERSIST_AUX") && std::getenv("VROD_PERSIST_AUX")[0] == '1')
+                       ? vdev::persistent_aux_ctas(w_)
+                       : 0;
     if (std::getenv("VROD_TRACE") && std::getenv("VROD_TRACE")[0] == '1') {
       d_trace_ = dalloc<unsigned long long>(vdev::kTraceCap);
       check_cuda(cudaMemset(d_trace_, 0, sizeof(unsigned long long) * vdev::kTraceCap), "trace");
@@ -688,7 +693,7 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
       vdev::FillList f;
       if (!persistent) f.add(w_.lam, 2ll * vdev::kLamFields * w_.vpad, 0);
       f.add(d_singular_, iterations, 0);
-      if (persistent) f.add(d_bar_, 1, 0);
+      if (persistent) f.add(d_bar_, 2, 0);
       vdev::launch_fill(f, st);
     }
     end();
@@ -708,6 +713,9 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
       pp.lam_ext[0] = c_.ext_lam;
       pp.lam_ext[1] = ext_lam2_;
       pp.bar = d_bar_;
+      pp.ext_done = d_bar_ + 1;
+      pp.tiles = persist_tiles_;
+      pp.n_aux = persist_aux_;
       pp.trace = d_trace_;
       pp.iterations = iterations;
       pp.sm_period = scene_.settings.sm_period;

@@ -115,6 +115,7 @@ class Solver {
   // Persistent iteration kernel for small single-scene worlds (VROD_PERSIST=0 disables it).
   bool persist_ok_ = !(std::getenv("VROD_PERSIST") && std::getenv("VROD_PERSIST")[0] == '0');
   int persist_tiles_ = 0;
+  int persist_aux_ = 0;              // aux CTAs of the persistent kernel (VROD_PERSIST_AUX=1)
   double* xrec2_ = nullptr;          // ping-pong partner of w_.xrec (persistent kernel)
   double* ext_lam2_ = nullptr;       // ping-pong partner of c_.ext_lam
   unsigned* d_bar_ = nullptr;        // grid-barrier counter

@@ -263,17 +263,24 @@ def test_persistent_kernel_matches_per_launch_path(gpu, oracle, name, monkeypatc
     every block formula, so they must agree BIT FOR BIT — shape-matching scenes included —
     on states, reports and contacts, step after step."""
     scene = SCENES[name](oracle)
-    a = SolverHandle(gpu, scene)
+    c = SolverHandle(gpu, scene)  # persistent, external blocks re-solved inside the tiles (default)
+    monkeypatch.setenv("VROD_PERSIST_AUX", "1")
+    a = SolverHandle(gpu, scene)  # persistent, external blocks and shape matching on aux CTAs
     monkeypatch.setenv("VROD_PERSIST", "0")
-    b = SolverHandle(gpu, scene)
+    b = SolverHandle(gpu, scene)  # per-sweep launches
     monkeypatch.delenv("VROD_PERSIST")
+    monkeypatch.delenv("VROD_PERSIST_AUX")
     for _ in range(3):
-        ra, rb = a.step(), b.step()
-        assert (ra.contact_count, ra.broad_pairs, ra.skipped_singular) == (rb.contact_count, rb.broad_pairs, rb.skipped_singular)
-        assert ra.max_penetration == rb.max_penetration
-        np.testing.assert_array_equal(ra.residuals, rb.residuals)
-        sa, sb = a.state(), b.state()
-        for k in sa:
-            np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
+        rb = b.step()
+        sb = b.state()
+        for h in (a, c):
+            ra = h.step()
+            assert (ra.contact_count, ra.broad_pairs, ra.skipped_singular) == \
+                   (rb.contact_count, rb.broad_pairs, rb.skipped_singular)
+            assert ra.max_penetration == rb.max_penetration
+            np.testing.assert_array_equal(ra.residuals, rb.residuals)
+            sa = h.state()
+            for k in sa:
+                np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
     assert _iterate_launches(gpu, b) == 0
-    assert _iterate_launches(gpu, a) > 0  # the persistent path really ran
+    assert _iterate_launches(gpu, a) > 0 and _iterate_launches(gpu, c) > 0  # the persistent paths really ran
