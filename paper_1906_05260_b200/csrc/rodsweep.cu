@@ -105,6 +105,7 @@ struct PTile : Tile<TP> {
   int e_item[kTileEntries];
   ContactRef e_ref[kTileEntries];
   alignas(16) double e_out[kTileEntries][4];  // read and written as double2
+  ShapeCache shape;                            // static data of this CTA's shape-matching chain
 };
 
 // Phase 0: per-position metadata of the tile (rod-local index, element count, kinds, block base),
@@ -962,6 +963,10 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
     }
     for (int i = tid; i < kLamFields * kTileStage; i += 32 * kWarps) t.st[T_LAM + i / kTileStage][i % kTileStage] = 0.0;
   }
+  // the groups of the chain this CTA's warp 0 runs (chain u = CTA index, see the shape pass)
+  const int my_chain = inline_ext ? blockIdx.x : blockIdx.x - pp.tiles;
+  const bool cache_shape = g.G > 0 && g.nchains > 0 && my_chain >= 0 && my_chain < g.nchains;
+  if (cache_shape) shape_cache_fill(t.shape, w, g, g.chain_groups, g.chain_off[my_chain], g.chain_off[my_chain + 1]);
   double* cur = pp.X;
   double* nxt = pp.Y;
   double* xr_cur = pp.xrec[0];
@@ -1075,7 +1080,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
           for (int k = k0; k < k1; ++k) {
             const bool tr = pp.trace && it == 1 && (chains ? u == 28 : u == u0);
             shape_group(w, g, cur, xr_cur, chains ? g.chain_groups[k] : g.level_groups[k], lane,
-                        tr ? pp.trace + 600 + 8 * (chains ? k - k0 : l) : nullptr);
+                        tr ? pp.trace + 600 + 8 * (chains ? k - k0 : l) : nullptr, cache_shape ? &t.shape : nullptr);
             __syncwarp();
           }
         }

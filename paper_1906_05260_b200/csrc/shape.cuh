@@ -108,13 +108,66 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return ns;
 }
 
+// Shared-memory copy of the static data of a few groups (the persistent kernel caches the groups
+// of the chain its CTA runs, so a shape-matching pass loads only the members' state).
+constexpr int kShapeCacheMembers = 64, kShapeCacheGroups = 4;
+struct ShapeCache {
+  int ng;
+  int gid[kShapeCacheGroups], m0[kShapeCacheGroups], m1[kShapeCacheGroups], base[kShapeCacheGroups];
+  int serial[kShapeCacheGroups];
+  double grest[kShapeCacheGroups][4];
+  int slot[kShapeCacheMembers], eslot[kShapeCacheMembers];
+  uint8_t pinned[kShapeCacheMembers];
+  double rest[kShapeCacheMembers][17];
+};
+
+// Fills `sc` with the groups k0 .. k1-1 of `list` while they fit (all threads of the CTA).
+__device__ __forceinline__ void shape_cache_fill(ShapeCache& sc, const World& w, const Groups& g, const int* list, int k0,
+                                                 int k1) {
+  if (threadIdx.x == 0) {
+    int ng = 0, nm = 0;
+    for (int k = k0; k < k1 && ng < kShapeCacheGroups; ++k) {
+      const int grp = list[k], m0 = g.off[grp], m1 = g.off[grp + 1];
+      if (nm + (m1 - m0) > kShapeCacheMembers) break;
+      sc.gid[ng] = grp;
+      sc.m0[ng] = m0;
+      sc.m1[ng] = m1;
+      sc.base[ng] = nm;
+      sc.serial[ng] = g.serial[grp];
+      for (int a = 0; a < 4; ++a) sc.grest[ng][a] = g.grest[4ll * grp + a];
+      nm += m1 - m0;
+      ++ng;
+    }
+    sc.ng = ng;
+  }
+  __syncthreads();
+  for (int c = 0; c < sc.ng; ++c)
+    for (int i = threadIdx.x; i < sc.m1[c] - sc.m0[c]; i += blockDim.x) {
+      const int m = sc.m0[c] + i, l = sc.base[c] + i;
+      sc.slot[l] = g.mslot[m];
+      sc.eslot[l] = g.meslot[m];
+      sc.pinned[l] = w.pinned[g.mslot[m]];
+      for (int a = 0; a < 17; ++a) sc.rest[l][a] = g.mrest[17ll * m + a];
+    }
+  __syncthreads();
+}
+
 // Fit and apply group `grp` (apply_shape_match, bundling.cpp:116-133) on the state rows X and
-// the slot records xrec. Called by all 32 lanes of a warp. tr: optional phase timestamps.
+// the slot records xrec. Called by all 32 lanes of a warp. tr: optional phase timestamps; sc:
+// optional shared-memory copy of the group's static data.
 __device__ __forceinline__ void shape_group(const World& w, const Groups& g, double* X, double* xrec, int grp,
-                                            int lane, unsigned long long* tr = nullptr) {
+                                            int lane, unsigned long long* tr = nullptr, const ShapeCache* sc = nullptr) {
   using namespace vm;
   if (tr && lane == 0) tr[0] = gtimer();
-  const int m0 = g.off[grp], m1 = g.off[grp + 1];
+  int ci = -1;
+  if (sc)
+    for (int k = 0; k < sc->ng; ++k)
+      if (sc->gid[k] == grp) ci = k;
+  const int m0 = ci >= 0 ? sc->m0[ci] : g.off[grp], m1 = ci >= 0 ? sc->m1[ci] : g.off[grp + 1];
+  const int lb = ci >= 0 ? sc->base[ci] - m0 : 0;  // member m -> cache line m + lb
+  auto MS = [&](int i) { return ci >= 0 ? sc->slot[i + lb] : g.mslot[i]; };
+  auto ME = [&](int i) { return ci >= 0 ? sc->eslot[i + lb] : g.meslot[i]; };
+  auto MR = [&](int i) -> const double* { return ci >= 0 ? &sc->rest[i + lb][0] : g.mrest + 17ll * i; };
   const int n = m1 - m0;
   const long long vp = w.vpad;
   auto ldc = [&](int v) { return V3{X[CX * vp + v], X[CY * vp + v], X[CZ * vp + v]}; };
@@ -127,25 +180,25 @@ __device__ __forceinline__ void shape_group(const World& w, const Groups& g, dou
   double s0 = 0.0;
   Q4 q0{1, 0, 0, 0};
   if (has0) {
-    const int v = g.mslot[i0], e = g.meslot[i0];
+    const int v = MS(i0), e = ME(i0);
     c0 = ldc(v);
     s0 = X[S * vp + v];
     q0 = ldq(e);
   }
   // centroid of the current member centers
   V3 sum = c0;
-  for (int i = i0 + 32; i < m1; i += 32) sum = sum + ldc(g.mslot[i]);
+  for (int i = i0 + 32; i < m1; i += 32) sum = sum + ldc(MS(i));
   const V3 cent = V3{shape_wsum(sum.x), shape_wsum(sum.y), shape_wsum(sum.z)} / static_cast<double>(n);
   if (tr && lane == 0) tr[1] = gtimer();
   // B = sum (s * sbar) R Rbar^T + (c - mu) cbar^T
   double Bp[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int i = i0; i < m1; i += 32) {
-    const double* mr = g.mrest + 17ll * i;
+    const double* mr = MR(i);
     const bool first = i == i0;
-    const int v = first ? 0 : g.mslot[i];
+    const int v = first ? 0 : MS(i);
     const V3 c = (first ? c0 : ldc(v)) - cent;
     const double s = first ? s0 : X[S * vp + v];
-    const M3 R = qmat(first ? q0 : ldq(g.meslot[i]));
+    const M3 R = qmat(first ? q0 : ldq(ME(i)));
     M3 rR;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
@@ -174,7 +227,7 @@ __device__ __forceinline__ void shape_group(const World& w, const Groups& g, dou
       sq[a + 3 * b] = B.m[a][b] * B.m[a][b];
     }
   if (tr && lane == 0) tr[2] = gtimer();
-  const double* gr = g.grest + 4ll * grp;
+  const double* gr = ci >= 0 ? sc->grest[ci] : g.grest + 4ll * grp;
   const double denom = gr[3];
   if (sqrt(sum9(sq)) < 1e-12 || denom < 1e-300) return;  // degenerate: no write (bundling.cpp:86-90)
   const double* wq = g.warm + 4ll * grp;
@@ -188,12 +241,12 @@ __device__ __forceinline__ void shape_group(const World& w, const Groups& g, dou
   const V3 rcent{gr[0], gr[1], gr[2]};
   double numer = 0.0;
   for (int i = i0; i < m1; i += 32) {
-    const double* mr = g.mrest + 17ll * i;
+    const double* mr = MR(i);
     const bool first = i == i0;
-    const int v = first ? 0 : g.mslot[i];
+    const int v = first ? 0 : MS(i);
     const V3 c = (first ? c0 : ldc(v)) - cent;
     const double s = first ? s0 : X[S * vp + v];
-    const M3 R = qmat(first ? q0 : ldq(g.meslot[i]));
+    const M3 R = qmat(first ? q0 : ldq(ME(i)));
     M3 rR;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
@@ -214,9 +267,9 @@ __device__ __forceinline__ void shape_group(const World& w, const Groups& g, dou
   const V3 t = cent - scale * mvmul(Rf, rcent);
   const Q4 qf = qfrom_mat(Rf);
   auto apply = [&](int i) {
-    const double* mr = g.mrest + 17ll * i;
-    const int v = g.mslot[i];
-    if (!w.pinned[v]) {
+    const double* mr = MR(i);
+    const int v = MS(i);
+    if (!(ci >= 0 ? sc->pinned[i + lb] : w.pinned[v])) {
       const V3 x = scale * mvmul(Rf, V3{mr[0], mr[1], mr[2]} + rcent) + t;
       X[CX * vp + v] = x.x;
       X[CY * vp + v] = x.y;
@@ -228,14 +281,14 @@ __device__ __forceinline__ void shape_group(const World& w, const Groups& g, dou
       xr[1] = make_double2(x.z, sn);
     }
     const Q4 fr = qnormalized(qmul(qf, Q4{mr[13], mr[14], mr[15], mr[16]}));
-    const int e = g.meslot[i];
+    const int e = ME(i);
     X[QW * vp + e] = fr.w;
     X[QX * vp + e] = fr.x;
     X[QY * vp + e] = fr.y;
     X[QZ * vp + e] = fr.z;
   };
   __syncwarp();
-  if (g.serial[grp]) {
+  if (ci >= 0 ? sc->serial[ci] : g.serial[grp]) {
     if (lane == 0)
       for (int i = m0; i < m1; ++i) apply(i);
   } else {
