@@ -767,14 +767,6 @@ __global__ void k_compact_contacts(Collide c) {
   }
 }
 
-__global__ void k_contact_count(Collide c, StepAccum* acc) {
-  pdl_wait();
-  pdl_trigger();
-  atomicAdd(&acc->contact_count, c.scalars[SC_NCT]);
-  atomicAdd(&acc->broad_pairs, c.scalars[SC_BROAD]);
-  if (c.scalars[SC_NCT_RAW] > acc->max_contacts) acc->max_contacts = c.scalars[SC_NCT_RAW];
-  if (c.scalars[SC_NCAND_RAW] > acc->max_candidates) acc->max_candidates = c.scalars[SC_NCAND_RAW];
-}
 
 __global__ void k_cand_to_raw(Collide c) {
   pdl_wait();
@@ -824,9 +816,15 @@ __global__ void k_warm_build(Collide c, int split) {
     }
   }
 }
-__global__ void k_warm_counts(Collide c, int split) {
+// The step report's collision counters (solver.cpp:203-225) and the sizes of the warm lists the
+// next substep looks up.
+__global__ void k_warm_counts(Collide c, int split, StepAccum* acc) {
   pdl_wait();
   pdl_trigger();
+  atomicAdd(&acc->contact_count, c.scalars[SC_NCT]);
+  atomicAdd(&acc->broad_pairs, c.scalars[SC_BROAD]);
+  if (c.scalars[SC_NCT_RAW] > acc->max_contacts) acc->max_contacts = c.scalars[SC_NCT_RAW];
+  if (c.scalars[SC_NCAND_RAW] > acc->max_candidates) acc->max_candidates = c.scalars[SC_NCAND_RAW];
   const int n = c.scalars[SC_NCT];
   const int nrk = split ? c.rk_pos[n] : 0;
   c.scalars[SC_NRK_PREV] = nrk;
@@ -1001,14 +999,13 @@ void launch_collide(const World& w, Collide& c, const double* anim, const AnimLa
   }
   const int split = w.K > 0 ? 1 : 0;
   launch_broad_narrow(c, substep, err, 1, 1, split, 0, st);
-  launch_kernel(k_contact_count, 1, 1, 0, st, g_pdl, c, acc);
   const int g = grid_for(c.contact_cap);
   if (split) {
     launch_kernel(k_warm_flags, g, kThreads, 0, st, g_pdl, c);
     scan_exclusive(c.rk_flag, c.rk_pos, c.contact_cap, c.scalars + SC_NCT, c.scan_tmp, c.scan_parts, st);
   }
   launch_kernel(k_warm_build, g, kThreads, 0, st, g_pdl, c, split);
-  launch_kernel(k_warm_counts, 1, 1, 0, st, g_pdl, c, split);
+  launch_kernel(k_warm_counts, 1, 1, 0, st, g_pdl, c, split, acc);
 }
 
 void launch_halfplanes(const World& w, Collide& c, cudaStream_t st) {

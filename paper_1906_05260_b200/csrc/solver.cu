@@ -633,14 +633,14 @@ __global__ void k_init_acc(StepAccum* acc, unsigned long long* err, int* scalars
   acc->max_contacts = 0;
   *err = ~0ull;
 }
-__global__ void k_end_substep(StepAccum* acc, const int* singular_last) {
+// End of a substep: the last sweep's singular count (solver.cpp:335, 375); after the step's last
+// substep also the error word (capacity overflow invalidates the results).
+__global__ void k_end_substep(StepAccum* acc, const int* singular_last, int last, const unsigned long long* err,
+                              const int* scalars) {
   vdev::pdl_wait();
   vdev::pdl_trigger();
   acc->skipped_singular += *singular_last;
-}
-__global__ void k_end_step(StepAccum* acc, const unsigned long long* err, const int* scalars) {
-  vdev::pdl_wait();
-  vdev::pdl_trigger();
+  if (!last) return;
   unsigned long long e = *err;
   if (scalars[vdev::SC_OVF]) e = vdev::err_code(0, vdev::ERR_CAPACITY, scalars[vdev::SC_OVF], 0);  // results invalid
   acc->error = e;
@@ -756,10 +756,10 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
                            reinterpret_cast<double*>(reinterpret_cast<char*>(d_acc_) + offsetof(StepAccum, residuals)), st);
     if (ext_possible_ && (c_.contact_cap + c_.hp_cap) > 0) vdev::launch_penetration(w_, c_, w_.X, d_acc_, st);
     if (n_scenes_ > 1) vdev::launch_scene_report(w_, w_.X, w_.classic, d_scene_sing_, st);
-    vdev::launch_kernel(k_end_substep, 1, 1, 0, st, vdev::g_pdl, d_acc_, d_singular_ + (iterations - 1));
+    vdev::launch_kernel(k_end_substep, 1, 1, 0, st, vdev::g_pdl, d_acc_, d_singular_ + (iterations - 1),
+                        s == substeps - 1 ? 1 : 0, d_err_, c_.scalars);
     end();
   }
-  vdev::launch_kernel(k_end_step, 1, 1, 0, st, vdev::g_pdl, d_acc_, d_err_, c_.scalars);
   vdev::g_pdl = false;
   check_cuda(cudaMemcpyAsync(h_acc_, d_acc_, sizeof(StepAccum), cudaMemcpyDeviceToHost, st), "report download");
   if (n_scenes_ > 1)
