@@ -223,6 +223,13 @@ int vrod_solver_get_contacts(vrod_solver* solver, int64_t capacity, int64_t* cou
 /* Solver::current_pills(), solver.cpp:432-436 (rod pills then kinematic pills). */
 int vrod_solver_current_pills(vrod_solver* solver, int64_t capacity, int64_t* count, vrod_pill* pills);
 
+/* One apply_shape_match pass over the solver's bundle groups in group order (bundling.cpp:116-133
+ * — the pass Solver::substep runs every shape_match_period sweeps, solver.cpp:336-338) on the live
+ * state, warm rotations updated. fits: 14 doubles per group (SimilarityFit, bundling.h:18-23:
+ * scale, translation xyz, rotation row-major 3x3, degenerate 0/1); at most `capacity` groups
+ * written, *count = the group count. */
+int vrod_solver_shape_match(vrod_solver* solver, int32_t capacity, int32_t* count, double* fits);
+
 /* ---- batches of independent scenes (BASELINE config C5) --------------------------------
  * The reference has no batch API: a batch is N independent vrod::Solver(Scene) objects
  * stepped in lockstep (solver.h:54-115, once per scene). Here one solver handle steps them
@@ -302,6 +309,11 @@ int vrod_find_contacts(int64_t n, const vrod_pill* pills, int64_t pair_count, co
                        int32_t iterations, int64_t warm_count, const uint64_t* warm_keys,
                        const double* warm_alpha, int64_t capacity, int64_t* count, int32_t* pill_a,
                        int32_t* pill_b, double* alpha, double* beta, double* distance);
+/* extract_rotation(covariance, guess, max_iterations, tolerance), bundling.h:42-43 /
+ * bundling.cpp:50-67: n independent problems; covariance row-major (9 each), guess and out
+ * quaternions (w, x, y, z). */
+int vrod_extract_rotation(int64_t n, const double* covariance, const double* guess, int32_t max_iterations,
+                          double tolerance, double* out);
 /* pair_key(a, b), collision.h:90 / collision.cpp:240-249. */
 uint64_t vrod_pair_key(const vrod_pill* a, const vrod_pill* b);
 

@@ -18,6 +18,7 @@
 #define private public
 #include "vrod/solver.h"
 #undef private
+#include "vrod/bundling.h"
 #include "vrod/collision.h"
 #include "vrod/constraints.h"
 #include "vrod/layout.h"
@@ -676,6 +677,36 @@ int vrod_skin_deform(vrod_skin* sk, int32_t np, const vrod_pill_transform* cur, 
     std::vector<Vec3> o;
     deform_mesh(sk->binding, tr, sk->mesh, o);
     for (std::size_t v = 0; v < o.size(); ++v) put3(out + 3 * v, o[v]);
+  });
+}
+int vrod_solver_shape_match(vrod_solver* s, int32_t cap, int32_t* count, double* fits) {
+  return guarded([&] {
+    int32_t k = 0;
+    for (Solver* sv : all(s))
+      for (BundleGroup& g : sv->groups_) {
+        const SimilarityFit f = apply_shape_match(g, sv->scene().rods);
+        if (fits && k < cap) {
+          double* o = fits + 14ll * k;
+          o[0] = f.scale;
+          put3(o + 1, f.translation);
+          for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) o[4 + 3 * a + b] = f.rotation(a, b);
+          o[13] = f.degenerate ? 1.0 : 0.0;
+        }
+        ++k;
+      }
+    *count = k;
+  });
+}
+int vrod_extract_rotation(int64_t n, const double* B, const double* guess, int32_t max_iterations, double tolerance,
+                          double* out) {
+  return guarded([&] {
+    for (int64_t i = 0; i < n; ++i) {
+      Mat3 m;
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) m(a, b) = B[9 * i + 3 * a + b];
+      put4(out + 4 * i, extract_rotation(m, q4(guess + 4 * i), max_iterations, tolerance));
+    }
   });
 }
 int vrod_skin_deform_solver(vrod_skin* sk, vrod_solver* s, double* out) {

@@ -1466,9 +1466,9 @@ Fit fit_similarity(Group& g, const std::vector<Rod>& rods) {
   return fit;
 }
 // apply_shape_match, bundling.cpp:116-133.
-void apply_shape_match(Group& g, std::vector<Rod>& rods) {
+Fit apply_shape_match(Group& g, std::vector<Rod>& rods) {
   const Fit fit = fit_similarity(g, rods);
-  if (fit.degenerate) return;
+  if (fit.degenerate) return fit;
   const int n = static_cast<int>(g.members.size());
   for (int i = 0; i < n; ++i) {
     const auto [mr, mv] = g.members[i];
@@ -1480,6 +1480,7 @@ void apply_shape_match(Group& g, std::vector<Rod>& rods) {
     }
     rod.st.q[e] = qnormalized(qmul(qfrom_mat(fit.R), qfrom_mat(g.rR[i])));
   }
+  return fit;
 }
 
 // ---- solver (solver.cpp) --------------------------------------------------------------------
@@ -2607,6 +2608,39 @@ int vrod_skin_deform(vrod_skin* sk, int32_t np, const vrod_pill_transform* cur, 
     std::vector<V3> o;
     deform_mesh(sk->binding, tr, sk->mesh, o);
     for (std::size_t v = 0; v < o.size(); ++v) put3(out + 3 * v, o[v]);
+  });
+}
+int vrod_solver_shape_match(vrod_solver* s, int32_t cap, int32_t* count, double* fits) {
+  return guarded([&] {
+    int32_t k = 0;
+    for (Solver* sv : all(s))
+      for (Group& g : sv->groups_) {
+        const Fit f = apply_shape_match(g, sv->s_.rods);
+        if (fits && k < cap) {
+          double* o = fits + 14ll * k;
+          o[0] = f.scale;
+          o[1] = f.t.x;
+          o[2] = f.t.y;
+          o[3] = f.t.z;
+          for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) o[4 + 3 * a + b] = f.R(a, b);
+          o[13] = f.degenerate ? 1.0 : 0.0;
+        }
+        ++k;
+      }
+    *count = k;
+  });
+}
+int vrod_extract_rotation(int64_t n, const double* B, const double* guess, int32_t max_iterations, double tolerance,
+                          double* out) {
+  return guarded([&] {
+    for (int64_t i = 0; i < n; ++i) {
+      M3 m;
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) m(a, b) = B[9 * i + 3 * a + b];
+      const Q q = extract_rotation(m, q4(guess + 4 * i), max_iterations, tolerance);
+      put4(out + 4 * i, q);
+    }
   });
 }
 int vrod_skin_deform_solver(vrod_skin* sk, vrod_solver* s, double* out) {

@@ -464,6 +464,19 @@ int vrod_skin_deform_solver(vrod_skin* sk, vrod_solver* h, double* out) {
   return guarded([&] { sk->k->deform_solver(*h->s, out); });
 }
 
+int vrod_solver_shape_match(vrod_solver* h, int32_t cap, int32_t* count, double* fits) {
+  return guarded([&] {
+    const std::vector<double> f = h->s->shape_match();
+    const int32_t n = static_cast<int32_t>(f.size() / 14);
+    if (fits) std::copy(f.begin(), f.begin() + 14ll * std::min(n, std::max(cap, 0)), fits);
+    *count = n;
+  });
+}
+int vrod_extract_rotation(int64_t n, const double* B, const double* guess, int32_t max_iterations, double tolerance,
+                          double* out) {
+  return guarded([&] { gpu_extract_rotation(n, B, guess, max_iterations, tolerance, out); });
+}
+
 int vrod_solver_current_pills(vrod_solver* h, int64_t cap, int64_t* count, vrod_pill* out) {
   return guarded([&] {
     const auto pills = h->s->current_pills();

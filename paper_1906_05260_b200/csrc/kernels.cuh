@@ -297,6 +297,9 @@ void launch_iterate_persistent(const World& w, Collide& c, const Groups& g, cons
 void launch_pill_transforms(const World& w, const double* X, double* out, cudaStream_t st);
 
 // shape.cu
-void launch_shape_match(const World& w, const Groups& g, double* X, const int* level_off_host, bool pdl, cudaStream_t st);
+void launch_shape_match(const World& w, const Groups& g, double* X, const int* level_off_host, bool pdl, cudaStream_t st,
+                        double* fits = nullptr);  // fits: 14 doubles per group (SimilarityFit), or null
+void launch_extract_rotation(long long n, const double* B, const double* guess, int max_iterations, double tolerance,
+                             double* out, cudaStream_t st);
 
 }  // namespace vdev

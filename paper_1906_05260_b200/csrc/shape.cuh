@@ -47,12 +47,13 @@ __device__ __forceinline__ double rcp_fast(double x) {
 // its Taylor series in a^2 (truncation < 1e-20 relative); larger steps take the general route.
 // The product of two unit quaternions has |p|^2 = 1 + O(1e-15), so the renormalisation uses
 // 1/sqrt(n) = 1 - (n-1)/2 + 3/8 (n-1)^2 (exact to 1e-30 there; rsqrt otherwise).
-__device__ __forceinline__ vm::Q4 extract_rotation(const vm::M3& B, const vm::Q4& guess, int* iters = nullptr) {
+__device__ __forceinline__ vm::Q4 extract_rotation(const vm::M3& B, const vm::Q4& guess, int* iters = nullptr,
+                                                   int max_iterations = 100, double tol2 = 1e-18) {
   using namespace vm;
   Q4 q = qnormalized(guess);
   int it = 0;
 #pragma unroll 1
-  for (; it < 100; ++it) {
+  for (; it < max_iterations; ++it) {
     // R = toRotationMatrix(q)
     const double tx = 2.0 * q.x, ty = 2.0 * q.y, tz = 2.0 * q.z;
     const double twx = tx * q.w, twy = ty * q.w, twz = tz * q.w;
@@ -76,7 +77,7 @@ __device__ __forceinline__ vm::Q4 extract_rotation(const vm::M3& B, const vm::Q4
     const double inv = rcp_fast(fabs((dd[0] + dd[1]) + dd[2]) + 1e-9);
     const double w2 = fma(ox, ox, fma(oy, oy, oz * oz));
     const double a2 = (w2 * inv) * inv;  // |omega|^2
-    if (a2 < 1e-18) break;  // |omega| < 1e-9
+    if (a2 < tol2) break;  // |omega| < tolerance (1e-9)
     const double x2 = 0.25 * a2;  // (angle / 2)^2
     double k, c;  // k = sin(angle/2) / angle, c = cos(angle/2)
     if (x2 < 1e-4) {
@@ -155,8 +156,11 @@ __device__ __forceinline__ void shape_cache_fill(ShapeCache& sc, const World& w,
 // Fit and apply group `grp` (apply_shape_match, bundling.cpp:116-133) on the state rows X and
 // the slot records xrec. Called by all 32 lanes of a warp. tr: optional phase timestamps; sc:
 // optional shared-memory copy of the group's static data.
+// fit: optional SimilarityFit record (bundling.h:18-23), 14 doubles: scale, translation xyz,
+// rotation (row-major 3x3), degenerate flag.
 __device__ __forceinline__ void shape_group(const World& w, const Groups& g, double* X, double* xrec, int grp,
-                                            int lane, unsigned long long* tr = nullptr, const ShapeCache* sc = nullptr) {
+                                            int lane, unsigned long long* tr = nullptr, const ShapeCache* sc = nullptr,
+                                            double* fit = nullptr) {
   using namespace vm;
   if (tr && lane == 0) tr[0] = gtimer();
   int ci = -1;
@@ -229,7 +233,14 @@ __device__ __forceinline__ void shape_group(const World& w, const Groups& g, dou
   if (tr && lane == 0) tr[2] = gtimer();
   const double* gr = ci >= 0 ? sc->grest[ci] : g.grest + 4ll * grp;
   const double denom = gr[3];
-  if (sqrt(sum9(sq)) < 1e-12 || denom < 1e-300) return;  // degenerate: no write (bundling.cpp:86-90)
+  if (sqrt(sum9(sq)) < 1e-12 || denom < 1e-300) {  // degenerate: no write (bundling.cpp:86-90)
+    if (fit && lane == 0) {
+      const V3 t = cent - V3{gr[0], gr[1], gr[2]};
+      const double rec[14] = {1.0, t.x, t.y, t.z, 1, 0, 0, 0, 1, 0, 0, 0, 1, 1.0};
+      for (int k = 0; k < 14; ++k) fit[k] = rec[k];
+    }
+    return;
+  }
   const double* wq = g.warm + 4ll * grp;
   int nit = 0;
   const Q4 q = extract_rotation(B, Q4{wq[0], wq[1], wq[2], wq[3]}, &nit);
@@ -295,6 +306,11 @@ __device__ __forceinline__ void shape_group(const World& w, const Groups& g, dou
     for (int i = m0 + lane; i < m1; i += 32) apply(i);
   }
   if (tr && lane == 0) tr[5] = gtimer();
+  if (fit && lane == 0) {
+    const double rec[14] = {scale, t.x, t.y, t.z, Rf.m[0][0], Rf.m[0][1], Rf.m[0][2], Rf.m[1][0], Rf.m[1][1],
+                            Rf.m[1][2], Rf.m[2][0], Rf.m[2][1], Rf.m[2][2], 0.0};
+    for (int k = 0; k < 14; ++k) fit[k] = rec[k];
+  }
   if (lane == 0) {
     double* wo = g.warm + 4ll * grp;
     wo[0] = q.w;

@@ -864,6 +864,18 @@ long long Solver::kernel_nodes_per_step() {
 
 void Solver::pill_transforms_device(double* d_out) { vdev::launch_pill_transforms(w_, w_.X, d_out, stream_); }
 
+std::vector<double> Solver::shape_match() {
+  std::vector<double> out(14ull * g_.G);
+  if (g_.G == 0) return out;
+  if (!d_fits_) d_fits_ = dalloc<double>(out.size());
+  vdev::launch_shape_match(w_, g_, w_.X, level_off_.data(), false, stream_, d_fits_);
+  check_cuda(cudaGetLastError(), "shape match launch");
+  check_cuda(cudaMemcpyAsync(out.data(), d_fits_, out.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_),
+             "shape match");
+  check_cuda(cudaStreamSynchronize(stream_), "shape match");
+  return out;
+}
+
 std::vector<double> Solver::pill_transforms() {
   std::vector<double> out(8ull * setup_.E);
   if (setup_.E == 0) return out;

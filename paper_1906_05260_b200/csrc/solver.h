@@ -62,6 +62,9 @@ class Solver {
   // Solver::pill_transforms() (solver.cpp:438-440): rod pills, 8 doubles each (center, scale,
   // frame wxyz); the device variant writes into a device buffer on the solver's stream.
   std::vector<double> pill_transforms();
+  // One apply_shape_match pass over every bundle group in group order (bundling.cpp:116-133) on
+  // the live state; 14 doubles per group (SimilarityFit: scale, translation, rotation, degenerate).
+  std::vector<double> shape_match();
   void pill_transforms_device(double* d_out);
   // Per-scene reports of the last step (batch; a single scene returns one entry == step()).
   int scene_count() const { return n_scenes_; }
@@ -120,6 +123,7 @@ class Solver {
   double* ext_lam2_ = nullptr;       // ping-pong partner of c_.ext_lam
   unsigned* d_bar_ = nullptr;        // grid-barrier counter
   double* d_ptrans_ = nullptr;       // pill transforms download buffer (lazy)
+  double* d_fits_ = nullptr;         // shape_match() fit records (lazy)
   unsigned long long* d_trace_ = nullptr;  // VROD_TRACE=1: persistent-kernel phase timestamps
  public:
   int trace(long long* out, int cap);

@@ -228,4 +228,16 @@ long long gpu_find_contacts(long long n, const vrod_pill* pills, long long npair
   return count;
 }
 
+void gpu_extract_rotation(long long n, const double* B, const double* guess, int max_iterations, double tolerance,
+                          double* out) {
+  if (n <= 0) return;
+  Buf b;
+  const double* dB = b.put(B, 9ull * n);
+  const double* dg = b.put(guess, 4ull * n);
+  double* dq = b.get<double>(4ull * n);
+  vdev::launch_extract_rotation(n, dB, dg, max_iterations, tolerance, dq, nullptr);
+  check_cuda(cudaGetLastError(), "extract_rotation launch");
+  fetch(out, dq, 4ull * n);
+}
+
 }  // namespace vhost

@@ -15,4 +15,8 @@ long long gpu_find_contacts(long long n, const vrod_pill* pills, long long npair
                             long long nwarm, const uint64_t* wkeys, const double* walpha, long long cap, int32_t* pa,
                             int32_t* pb, double* alpha, double* beta, double* dist);
 
+// extract_rotation (bundling.h:42-43) on the GPU: n problems, covariance row-major 9 each.
+void gpu_extract_rotation(long long n, const double* B, const double* guess, int max_iterations, double tolerance,
+                          double* out);
+
 }  // namespace vhost

@@ -243,6 +243,16 @@ class SolverHandle:
         return out
 
 
+    def shape_match(self) -> np.ndarray:
+        """One apply_shape_match pass over the bundle groups in group order (bundling.cpp:116-133)
+        on the live state (warm rotations updated); returns the SimilarityFit of every group as
+        rows (scale, translation xyz, rotation row-major 3x3, degenerate 0/1)."""
+        G = self.info().bundle_count
+        out = np.zeros((max(G, 1), 14))
+        n = C.c_int32()
+        check(self._lib, self._lib.vrod_solver_shape_match(self._h, G, C.byref(n), capi.ptr(out)))
+        return out[:n.value]
+
     def _transforms(self, fn) -> np.ndarray:
         n = C.c_int64()
         check(self._lib, fn(self._h, 0, C.byref(n), None))
@@ -382,6 +392,16 @@ def find_contacts(lib, pills: np.ndarray, pairs: np.ndarray, iterations: int = 1
                                       capi.ptr(out["pill_b"], C.c_int32), capi.ptr(out["alpha"]),
                                       capi.ptr(out["beta"]), capi.ptr(out["distance"])))
     return {k: v[: cnt.value] for k, v in out.items()}
+
+
+def extract_rotation(lib, covariance: np.ndarray, guess: np.ndarray, max_iterations: int = 100,
+                     tolerance: float = 1e-9) -> np.ndarray:
+    """extract_rotation (bundling.h:42-43) for n problems: covariance (n, 3, 3), guess (n, 4) wxyz."""
+    B = np.ascontiguousarray(covariance, dtype=np.float64).reshape(-1, 9)
+    g = np.ascontiguousarray(guess, dtype=np.float64).reshape(-1, 4)
+    out = np.zeros_like(g)
+    check(lib, lib.vrod_extract_rotation(len(B), capi.ptr(B), capi.ptr(g), max_iterations, tolerance, capi.ptr(out)))
+    return out
 
 
 def pair_key(lib, a: np.ndarray, b: np.ndarray) -> int:
