@@ -230,6 +230,18 @@ int vrod_solver_current_pills(vrod_solver* solver, int64_t capacity, int64_t* co
  * written, *count = the group count. */
 int vrod_solver_shape_match(vrod_solver* solver, int32_t capacity, int32_t* count, double* fits);
 
+/* jacobi_sweep (constraints.h:124-126 / constraints.cpp:491-556) of the solver's elastic blocks
+ * and soft pins — in the order of Solver::substep's block list (solver.cpp:324-328), multipliers
+ * zero — on the live state, with step h and relaxation beta; contacts and half-planes are not part
+ * of it (and the last substep's contact list is consumed). State updated in place. active /
+ * skipped_singular: the SweepOutcome (either may be NULL). VROD_SIMULATION_ERROR on a non-finite
+ * update, naming the constraint like the reference. */
+int vrod_solver_jacobi_sweep(vrod_solver* solver, double h, double beta, int32_t* active, int32_t* skipped_singular);
+/* eval_constraint(block, ctx).W (constraints.h:82 / constraints.cpp:101-214) of every elastic block
+ * in block order on the live state: 3 doubles per block (unused components 0); at most
+ * `capacity` blocks written, *count = the elastic block count. */
+int vrod_solver_elastic_residuals(vrod_solver* solver, int64_t capacity, int64_t* count, double* W);
+
 /* ---- batches of independent scenes (BASELINE config C5) --------------------------------
  * The reference has no batch API: a batch is N independent vrod::Solver(Scene) objects
  * stepped in lockstep (solver.h:54-115, once per scene). Here one solver handle steps them

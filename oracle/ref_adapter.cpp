@@ -698,6 +698,30 @@ int vrod_solver_shape_match(vrod_solver* s, int32_t cap, int32_t* count, double*
     *count = k;
   });
 }
+int vrod_solver_jacobi_sweep(vrod_solver* s, double h, double beta, int32_t* active, int32_t* singular) {
+  return guarded([&] {
+    Solver& sv = one(s);
+    std::vector<ConstraintBlock> blocks = sv.elastic_;
+    blocks.insert(blocks.end(), sv.pin_blocks_.begin(), sv.pin_blocks_.end());
+    for (ConstraintBlock& b : blocks) b.lambda = Vec3::Zero();
+    const EvalContext ctx{sv.scene_.rods, &sv.layout_, sv.pills_, sv.scene_.planes, sv.pin_targets_, sv.classic_};
+    const SweepOutcome o = jacobi_sweep(blocks, sv.scene_.rods, ctx, h, beta, sv.scratch_);
+    if (active) *active = o.active;
+    if (singular) *singular = o.skipped_singular;
+  });
+}
+int vrod_solver_elastic_residuals(vrod_solver* s, int64_t cap, int64_t* count, double* W) {
+  return guarded([&] {
+    Solver& sv = one(s);
+    const EvalContext ctx{sv.scene_.rods, &sv.layout_, sv.pills_, sv.scene_.planes, sv.pin_targets_, sv.classic_};
+    const int64_t n = static_cast<int64_t>(sv.elastic_.size());
+    for (int64_t i = 0; i < n && i < cap && W; ++i) {
+      const ResidualEval ev = eval_constraint(sv.elastic_[i], ctx);
+      for (int d = 0; d < 3; ++d) W[3 * i + d] = ev.W[d];
+    }
+    *count = n;
+  });
+}
 int vrod_extract_rotation(int64_t n, const double* B, const double* guess, int32_t max_iterations, double tolerance,
                           double* out) {
   return guarded([&] {

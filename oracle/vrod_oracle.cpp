@@ -1680,8 +1680,9 @@ class Solver {  // solver.h:54-115 / solver.cpp:102-442
   int step_index_ = 0;
   bool classic_ = false;
 
- private:
   Ctx ctx() const { return Ctx{&s_.rods, &L_, &pills_, &s_.planes, &pin_targets_, classic_}; }
+
+ private:
 
   void animate(double t_new) {  // solver.cpp:138-154
     for (const PinMotion& pm : s_.pin_motions) s_.rods[pm.rod].st.c[pm.vertex] = pm.position_at(t_new);
@@ -2629,6 +2630,29 @@ int vrod_solver_shape_match(vrod_solver* s, int32_t cap, int32_t* count, double*
         ++k;
       }
     *count = k;
+  });
+}
+int vrod_solver_jacobi_sweep(vrod_solver* s, double h, double beta, int32_t* active, int32_t* singular) {
+  return guarded([&] {
+    Solver& sv = one(s);
+    std::vector<Block> blocks = sv.elastic_;
+    blocks.insert(blocks.end(), sv.pins_.begin(), sv.pins_.end());
+    for (Block& b : blocks) b.lambda = V3{0, 0, 0};
+    const SweepOutcome o = jacobi_sweep(blocks, sv.s_.rods, sv.ctx(), h, beta, sv.scratch_);
+    if (active) *active = o.active;
+    if (singular) *singular = o.skipped_singular;
+  });
+}
+int vrod_solver_elastic_residuals(vrod_solver* s, int64_t cap, int64_t* count, double* W) {
+  return guarded([&] {
+    Solver& sv = one(s);
+    const Ctx c = sv.ctx();
+    const int64_t n = static_cast<int64_t>(sv.elastic_.size());
+    for (int64_t i = 0; i < n && i < cap && W; ++i) {
+      const Eval ev = eval_constraint(sv.elastic_[i], c);
+      for (int d = 0; d < 3; ++d) W[3 * i + d] = ev.W[d];
+    }
+    *count = n;
   });
 }
 int vrod_extract_rotation(int64_t n, const double* B, const double* guess, int32_t max_iterations, double tolerance,

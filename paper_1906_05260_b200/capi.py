@@ -137,6 +137,8 @@ _SIGNATURES = {
     "vrod_skin_deform_solver": (C.c_int, [C.c_void_p, C.c_void_p, _dp]),
     "vrod_solver_shape_match": (C.c_int, [C.c_void_p, C.c_int32, _ip, _dp]),
     "vrod_extract_rotation": (C.c_int, [C.c_int64, _dp, _dp, C.c_int32, C.c_double, _dp]),
+    "vrod_solver_jacobi_sweep": (C.c_int, [C.c_void_p, C.c_double, C.c_double, _ip, _ip]),
+    "vrod_solver_elastic_residuals": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _dp]),
 }
 
 # Optional entry points (product-only extensions; absent from the oracle libraries).

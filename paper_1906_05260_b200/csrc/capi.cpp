@@ -472,6 +472,21 @@ int vrod_solver_shape_match(vrod_solver* h, int32_t cap, int32_t* count, double*
     *count = n;
   });
 }
+int vrod_solver_jacobi_sweep(vrod_solver* h, double step, double beta, int32_t* active, int32_t* singular) {
+  return guarded([&] {
+    const auto o = h->s->jacobi_sweep(step, beta);
+    if (active) *active = o.first;
+    if (singular) *singular = o.second;
+  });
+}
+int vrod_solver_elastic_residuals(vrod_solver* h, int64_t cap, int64_t* count, double* W) {
+  return guarded([&] {
+    const std::vector<double> r = h->s->elastic_residuals();
+    const int64_t n = static_cast<int64_t>(r.size() / 3);
+    if (W) std::copy(r.begin(), r.begin() + 3 * std::min(n, std::max<int64_t>(cap, 0)), W);
+    *count = n;
+  });
+}
 int vrod_extract_rotation(int64_t n, const double* B, const double* guess, int32_t max_iterations, double tolerance,
                           double* out) {
   return guarded([&] { gpu_extract_rotation(n, B, guess, max_iterations, tolerance, out); });

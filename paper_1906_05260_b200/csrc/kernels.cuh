@@ -285,6 +285,8 @@ void launch_penetration(const World& w, Collide& c, const double* X, StepAccum* 
 // batch: per-scene residual norms (one CTA per scene) and end-of-substep singular fold-in
 void launch_scene_report(const World& w, const double* X, int classic, int* scene_singular, cudaStream_t st);
 int report_parts(int V);
+// eval_constraint(...).W of every elastic block, 3 doubles each, in block order
+void launch_block_residuals(const World& w, const double* X, int classic, double* out, cudaStream_t st);
 
 // rodsweep.cu: persistent iteration loop for small single-scene worlds. persistent_tiles()
 // returns the number of co-resident tiles the world needs, or 0 when it does not fit.

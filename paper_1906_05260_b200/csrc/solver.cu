@@ -876,6 +876,48 @@ std::vector<double> Solver::shape_match() {
   return out;
 }
 
+std::pair<int, int> Solver::jacobi_sweep(double h, double beta) {
+  cudaStream_t st = stream_;
+  if (ext_possible_) {  // external blocks of this sweep: the soft pins only
+    check_cuda(cudaMemsetAsync(c_.scalars + vdev::SC_NCT, 0, 2 * sizeof(int), st), "sweep reset");  // SC_NCT, SC_NHP
+    vdev::launch_ext_setup(w_, c_, st);
+  }
+  {
+    vdev::FillList f;
+    f.add(w_.lam, 2ll * vdev::kLamFields * w_.vpad, 0);
+    f.add(d_singular_, 1, 0);
+    f.add(d_err_, 2, -1);
+    vdev::launch_fill(f, st);
+  }
+  double* lam_a = w_.lam;
+  double* lam_b = w_.lam + static_cast<std::size_t>(vdev::kLamFields) * w_.vpad;
+  vdev::SweepParams sp{h, h * h, beta, classic_ ? 1 : 0, 0, 0, c_.n_pins, setup_.elastic_blocks,
+                       scene_.settings.contact_k, 0, nullptr, lam_a, lam_b};
+  vdev::launch_iteration(w_, c_, w_.X, w_.Y, sp, d_singular_, d_err_, st);
+  vdev::launch_copy_state(w_, w_.Y, w_.X, st);
+  check_cuda(cudaGetLastError(), "sweep launch");
+  int singular = 0;
+  unsigned long long err = 0;
+  check_cuda(cudaMemcpyAsync(&singular, d_singular_, sizeof(int), cudaMemcpyDeviceToHost, st), "sweep");
+  check_cuda(cudaMemcpyAsync(&err, d_err_, sizeof(err), cudaMemcpyDeviceToHost, st), "sweep");
+  check_cuda(cudaStreamSynchronize(st), "sweep");
+  h_acc_->error = err;
+  check_error();
+  return {setup_.elastic_blocks + c_.n_pins - singular, singular};
+}
+
+std::vector<double> Solver::elastic_residuals() {
+  std::vector<double> out(3ull * setup_.elastic_blocks);
+  if (out.empty()) return out;
+  if (!d_blockw_) d_blockw_ = dalloc<double>(out.size());
+  vdev::launch_block_residuals(w_, w_.X, w_.classic, d_blockw_, stream_);
+  check_cuda(cudaGetLastError(), "residuals launch");
+  check_cuda(cudaMemcpyAsync(out.data(), d_blockw_, out.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_),
+             "residuals");
+  check_cuda(cudaStreamSynchronize(stream_), "residuals");
+  return out;
+}
+
 std::vector<double> Solver::pill_transforms() {
   std::vector<double> out(8ull * setup_.E);
   if (setup_.E == 0) return out;

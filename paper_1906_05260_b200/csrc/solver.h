@@ -65,6 +65,11 @@ class Solver {
   // One apply_shape_match pass over every bundle group in group order (bundling.cpp:116-133) on
   // the live state; 14 doubles per group (SimilarityFit: scale, translation, rotation, degenerate).
   std::vector<double> shape_match();
+  // jacobi_sweep (constraints.cpp:491-556) of the elastic blocks and soft pins, multipliers zero,
+  // on the live state (contacts / half-planes excluded); returns {active, skipped_singular}.
+  std::pair<int, int> jacobi_sweep(double h, double beta);
+  // eval_constraint(...).W of every elastic block in block order, 3 doubles each.
+  std::vector<double> elastic_residuals();
   void pill_transforms_device(double* d_out);
   // Per-scene reports of the last step (batch; a single scene returns one entry == step()).
   int scene_count() const { return n_scenes_; }
@@ -124,6 +129,7 @@ class Solver {
   unsigned* d_bar_ = nullptr;        // grid-barrier counter
   double* d_ptrans_ = nullptr;       // pill transforms download buffer (lazy)
   double* d_fits_ = nullptr;         // shape_match() fit records (lazy)
+  double* d_blockw_ = nullptr;       // elastic_residuals() output (lazy)
   unsigned long long* d_trace_ = nullptr;  // VROD_TRACE=1: persistent-kernel phase timestamps
  public:
   int trace(long long* out, int cap);

@@ -302,6 +302,72 @@ __device__ __forceinline__ void slot_residual_terms(const World& w, const double
   }
 }
 
+// eval_constraint(...).W of every elastic block (constraints.cpp:106-214), written at the block's
+// index in the reference's order: rod block base + element pass (k * ne + rank) or vertex pass
+// (m * ne + (k - 1) * nv + rank). Same formulas as slot_residual_terms.
+__global__ void k_block_residuals(World w, const double* __restrict__ X, int classic, double* __restrict__ out) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < w.V; v += gridDim.x * blockDim.x) {
+    const int vp = w.vpad;
+    const int k = w.slot_loc[v], m = w.slot_m[v], r = w.slot_rod[v];
+    const int ek = w.rod_ekinds[r], vk = w.rod_vkinds[r];
+    const int ne = __popc(ek), nv = __popc(vk);
+    const long long base = w.rod_block_base[r];
+    auto put = [&](long long b, double x, double y, double z) {
+      out[3 * b] = x;
+      out[3 * b + 1] = y;
+      out[3 * b + 2] = z;
+    };
+    if (k < m) {
+      const V3 c0 = ldc(X, vp, v), c1 = ldc(X, vp, v + 1);
+      const double s0 = F(X, S, vp, v), s1 = F(X, S, vp, v + 1);
+      const double sb0 = F(w.vstat, SBAR, vp, v), sb1 = F(w.vstat, SBAR, vp, v + 1);
+      const double l = F(w.estat, LEN, vp, v), l0 = F(w.estat, LEN0, vp, v), tbar = F(w.estat, TDOT, vp, v);
+      const M3 R = qmat(Q4{F(X, QW, vp, v), F(X, QX, vp, v), F(X, QY, vp, v), F(X, QZ, vp, v)});
+      const V3 wv = col(R, 2);
+      const long long b0 = base + static_cast<long long>(k) * ne;
+      if (ek & EK_SZ) {
+        const V3 W = (c1 - c0) / l - tbar * wv;
+        put(b0 + __popc(ek & (EK_SZ - 1)), W.x, W.y, W.z);
+      }
+      if (ek & EK_CS) put(b0 + __popc(ek & (EK_CS - 1)), 0.5 * (s0 + s1) - 0.5 * (sb0 + sb1), 0, 0);
+      if (ek & EK_SS) put(b0 + __popc(ek & (EK_SS - 1)), (s1 - s0) / l - F(w.estat, SGRAD, vp, v), 0, 0);
+      if (ek & EK_VS) {
+        const double smid = 0.5 * (s0 + s1), smr = 0.5 * (sb0 + sb1);
+        const V3 W = (smid * smid) * ((c1 - c0) / l0) - (smr * smr * tbar) * wv;
+        put(b0 + __popc(ek & (EK_VS - 1)), W.x, W.y, W.z);
+      }
+    }
+    if (k >= 1 && k <= m - 1) {
+      const double la = F(w.estat, LEN, vp, v - 1), lb = F(w.estat, LEN, vp, v);
+      const double la0 = F(w.estat, LEN0, vp, v - 1), lb0 = F(w.estat, LEN0, vp, v);
+      const Q4 qa{F(X, QW, vp, v - 1), F(X, QX, vp, v - 1), F(X, QY, vp, v - 1), F(X, QZ, vp, v - 1)};
+      const Q4 qb{F(X, QW, vp, v), F(X, QX, vp, v), F(X, QY, vp, v), F(X, QZ, vp, v)};
+      const Q4 pr = relative_rotation(qa, qb);
+      const double s0 = F(X, S, vp, v), sbar = F(w.vstat, SBAR, vp, v);
+      const V3 darb{F(w.estat, DARBX, vp, v - 1), F(w.estat, DARBY, vp, v - 1), F(w.estat, DARBZ, vp, v - 1)};
+      const long long b0 = base + static_cast<long long>(m) * ne + static_cast<long long>(k - 1) * nv;
+      if (vk & VK_BT) {
+        const V3 om = (4.0 / (la + lb)) * qvec(pr);
+        const double s = classic ? sbar : s0;
+        const V3 W = s * om - sbar * darb;
+        put(b0 + __popc(vk & (VK_BT - 1)), W.x, W.y, W.z);
+      }
+      if (vk & VK_SB) {
+        const double sm = F(X, S, vp, v - 1), spp = F(X, S, vp, v + 1);
+        put(b0 + __popc(vk & (VK_SB - 1)), ((spp - s0) / lb - (s0 - sm) / la) - F(w.estat, SLAP, vp, v - 1), 0, 0);
+      }
+      const double inv_len0 = 4.0 / (la0 + lb0);
+      for (int cc = 0; cc < 2; ++cc) {
+        const int bit = cc == 0 ? VK_VBU : VK_VBV;
+        if (!(vk & bit)) continue;
+        const double om = inv_len0 * (cc == 0 ? pr.x : pr.y);
+        const double rest_om = (cc == 0 ? darb.x : darb.y) * (la + lb) / (la0 + lb0);
+        put(b0 + __popc(vk & (bit - 1)), s0 * s0 * s0 * om - sbar * sbar * sbar * rest_om, 0, 0);
+      }
+    }
+  }
+}
+
 __global__ void k_report_partial(World w, const double* __restrict__ X, int classic, double* partials) {
   pdl_wait();
   pdl_trigger();
@@ -443,6 +509,10 @@ void launch_residuals(const World& w, const double* X, int classic, double* part
                       cudaStream_t st) {
   launch_kernel(k_report_partial, parts, kRepThreads, 0, st, g_pdl, w, X, classic, partials);
   launch_kernel(k_report_final, 1, kRepThreads, 0, st, g_pdl, partials, parts, out8);
+}
+
+void launch_block_residuals(const World& w, const double* X, int classic, double* out, cudaStream_t st) {
+  launch_kernel(k_block_residuals, grid_for(w.V), kThreads, 0, st, false, w, X, classic, out);
 }
 
 void launch_scene_report(const World& w, const double* X, int classic, int* scene_singular, cudaStream_t st) {

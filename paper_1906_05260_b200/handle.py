@@ -253,6 +253,22 @@ class SolverHandle:
         check(self._lib, self._lib.vrod_solver_shape_match(self._h, G, C.byref(n), capi.ptr(out)))
         return out[:n.value]
 
+    def jacobi_sweep(self, h: float, beta: float) -> tuple[int, int]:
+        """jacobi_sweep (constraints.cpp:491-556) of the elastic blocks and soft pins with zero
+        multipliers on the live state; returns the SweepOutcome (active, skipped_singular)."""
+        a, s = C.c_int32(), C.c_int32()
+        check(self._lib, self._lib.vrod_solver_jacobi_sweep(self._h, h, beta, C.byref(a), C.byref(s)))
+        return a.value, s.value
+
+    def elastic_residuals(self) -> np.ndarray:
+        """eval_constraint(...).W of every elastic block in block order, (n, 3)."""
+        n = C.c_int64()
+        check(self._lib, self._lib.vrod_solver_elastic_residuals(self._h, 0, C.byref(n), None))
+        out = np.zeros((n.value, 3))
+        if n.value:
+            check(self._lib, self._lib.vrod_solver_elastic_residuals(self._h, n.value, C.byref(n), capi.ptr(out)))
+        return out
+
     def _transforms(self, fn) -> np.ndarray:
         n = C.c_int64()
         check(self._lib, fn(self._h, 0, C.byref(n), None))
