@@ -153,25 +153,44 @@ __device__ __forceinline__ void shape_cache_fill(ShapeCache& sc, const World& w,
   __syncthreads();
 }
 
-// Fit and apply group `grp` (apply_shape_match, bundling.cpp:116-133) on the state rows X and
-// the slot records xrec. Called by all 32 lanes of a warp. tr: optional phase timestamps; sc:
-// optional shared-memory copy of the group's static data.
-// fit: optional SimilarityFit record (bundling.h:18-23), 14 doubles: scale, translation xyz,
-// rotation (row-major 3x3), degenerate flag.
-__device__ __forceinline__ void shape_group(const World& w, const Groups& g, double* X, double* xrec, int grp,
-                                            int lane, unsigned long long* tr = nullptr, const ShapeCache* sc = nullptr,
-                                            double* fit = nullptr) {
+// Per-warp state of one group fit between its phases: member range / cache mapping, the lane's
+// first member (loaded once, reused), the centroid and the covariance.
+struct ShapeState {
+  int grp, m0, m1, ci, lb;
+  vm::V3 cent, c0;
+  double s0;
+  vm::Q4 q0;
+  vm::M3 B;
+  bool degenerate;
+};
+
+// Member accessors of a group: the shared-memory cache when it holds the group, else global.
+struct ShapeMembers {
+  const Groups& g;
+  const ShapeCache* sc;
+  int ci, lb;
+  __device__ __forceinline__ int slot(int i) const { return ci >= 0 ? sc->slot[i + lb] : g.mslot[i]; }
+  __device__ __forceinline__ int eslot(int i) const { return ci >= 0 ? sc->eslot[i + lb] : g.meslot[i]; }
+  __device__ __forceinline__ const double* rest(int i) const { return ci >= 0 ? &sc->rest[i + lb][0] : g.mrest + 17ll * i; }
+};
+
+// Phase 1 of fit_similarity (bundling.cpp:69-92): centroid and covariance
+// B = sum (s * sbar) R Rbar^T + (c - mu) cbar^T (warp tree reductions), degenerate test.
+__device__ __forceinline__ ShapeState shape_begin(const World& w, const Groups& g, const double* X, int grp, int lane,
+                                                  const ShapeCache* sc, unsigned long long* tr) {
   using namespace vm;
-  if (tr && lane == 0) tr[0] = gtimer();
-  int ci = -1;
+  ShapeState st;
+  st.grp = grp;
+  st.ci = -1;
   if (sc)
     for (int k = 0; k < sc->ng; ++k)
-      if (sc->gid[k] == grp) ci = k;
-  const int m0 = ci >= 0 ? sc->m0[ci] : g.off[grp], m1 = ci >= 0 ? sc->m1[ci] : g.off[grp + 1];
-  const int lb = ci >= 0 ? sc->base[ci] - m0 : 0;  // member m -> cache line m + lb
-  auto MS = [&](int i) { return ci >= 0 ? sc->slot[i + lb] : g.mslot[i]; };
-  auto ME = [&](int i) { return ci >= 0 ? sc->eslot[i + lb] : g.meslot[i]; };
-  auto MR = [&](int i) -> const double* { return ci >= 0 ? &sc->rest[i + lb][0] : g.mrest + 17ll * i; };
+      if (sc->gid[k] == grp) st.ci = k;
+  const int ci = st.ci;
+  st.m0 = ci >= 0 ? sc->m0[ci] : g.off[grp];
+  st.m1 = ci >= 0 ? sc->m1[ci] : g.off[grp + 1];
+  st.lb = ci >= 0 ? sc->base[ci] - st.m0 : 0;  // member m -> cache line m + lb
+  const ShapeMembers M{g, sc, ci, st.lb};
+  const int m0 = st.m0, m1 = st.m1;
   const int n = m1 - m0;
   const long long vp = w.vpad;
   auto ldc = [&](int v) { return V3{X[CX * vp + v], X[CY * vp + v], X[CZ * vp + v]}; };
@@ -179,30 +198,28 @@ __device__ __forceinline__ void shape_group(const World& w, const Groups& g, dou
   // The lane's first member's state is loaded once, all loads in flight together, and reused by
   // the three passes (members beyond 32 per group are reloaded).
   const int i0 = m0 + lane;
-  const bool has0 = i0 < m1;
-  V3 c0{0, 0, 0};
-  double s0 = 0.0;
-  Q4 q0{1, 0, 0, 0};
-  if (has0) {
-    const int v = MS(i0), e = ME(i0);
-    c0 = ldc(v);
-    s0 = X[S * vp + v];
-    q0 = ldq(e);
+  st.c0 = V3{0, 0, 0};
+  st.s0 = 0.0;
+  st.q0 = Q4{1, 0, 0, 0};
+  if (i0 < m1) {
+    const int v = M.slot(i0), e = M.eslot(i0);
+    st.c0 = ldc(v);
+    st.s0 = X[S * vp + v];
+    st.q0 = ldq(e);
   }
   // centroid of the current member centers
-  V3 sum = c0;
-  for (int i = i0 + 32; i < m1; i += 32) sum = sum + ldc(MS(i));
-  const V3 cent = V3{shape_wsum(sum.x), shape_wsum(sum.y), shape_wsum(sum.z)} / static_cast<double>(n);
+  V3 sum = st.c0;
+  for (int i = i0 + 32; i < m1; i += 32) sum = sum + ldc(M.slot(i));
+  st.cent = V3{shape_wsum(sum.x), shape_wsum(sum.y), shape_wsum(sum.z)} / static_cast<double>(n);
   if (tr && lane == 0) tr[1] = gtimer();
-  // B = sum (s * sbar) R Rbar^T + (c - mu) cbar^T
   double Bp[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int i = i0; i < m1; i += 32) {
-    const double* mr = MR(i);
+    const double* mr = M.rest(i);
     const bool first = i == i0;
-    const int v = first ? 0 : MS(i);
-    const V3 c = (first ? c0 : ldc(v)) - cent;
-    const double s = first ? s0 : X[S * vp + v];
-    const M3 R = qmat(first ? q0 : ldq(ME(i)));
+    const int v = first ? 0 : M.slot(i);
+    const V3 c = (first ? st.c0 : ldc(v)) - st.cent;
+    const double s = first ? st.s0 : X[S * vp + v];
+    const M3 R = qmat(first ? st.q0 : ldq(M.eslot(i)));
     M3 rR;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
@@ -221,43 +238,43 @@ __device__ __forceinline__ void shape_group(const World& w, const Groups& g, dou
 #pragma unroll
       for (int b = 0; b < 3; ++b) Bp[3 * a + b] += P.m[a][b] + cv[a] * mr[b];
   }
-  M3 B;
   double sq[9];
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      B.m[a][b] = shape_wsum(Bp[3 * a + b]);
-      sq[a + 3 * b] = B.m[a][b] * B.m[a][b];
+      st.B.m[a][b] = shape_wsum(Bp[3 * a + b]);
+      sq[a + 3 * b] = st.B.m[a][b] * st.B.m[a][b];
     }
   if (tr && lane == 0) tr[2] = gtimer();
-  const double* gr = ci >= 0 ? sc->grest[ci] : g.grest + 4ll * grp;
+  const double denom = ci >= 0 ? sc->grest[ci][3] : g.grest[4ll * grp + 3];
+  st.degenerate = sqrt(sum9(sq)) < 1e-12 || denom < 1e-300;  // bundling.cpp:86-90
+  return st;
+}
+
+// Phase 3 (bundling.cpp:94-133): scale numerator with the extracted rotation q, translation,
+// projection of the members, warm rotation, optional fit record.
+__device__ __forceinline__ void shape_end(const World& w, const Groups& g, double* X, double* xrec, const ShapeState& st,
+                                          const vm::Q4& q, int lane, const ShapeCache* sc, unsigned long long* tr,
+                                          double* fit) {
+  using namespace vm;
+  const ShapeMembers M{g, sc, st.ci, st.lb};
+  const int m0 = st.m0, m1 = st.m1, grp = st.grp, i0 = m0 + lane;
+  const long long vp = w.vpad;
+  auto ldc = [&](int v) { return V3{X[CX * vp + v], X[CY * vp + v], X[CZ * vp + v]}; };
+  auto ldq = [&](int v) { return Q4{X[QW * vp + v], X[QX * vp + v], X[QY * vp + v], X[QZ * vp + v]}; };
+  const double* gr = st.ci >= 0 ? sc->grest[st.ci] : g.grest + 4ll * grp;
   const double denom = gr[3];
-  if (sqrt(sum9(sq)) < 1e-12 || denom < 1e-300) {  // degenerate: no write (bundling.cpp:86-90)
-    if (fit && lane == 0) {
-      const V3 t = cent - V3{gr[0], gr[1], gr[2]};
-      const double rec[14] = {1.0, t.x, t.y, t.z, 1, 0, 0, 0, 1, 0, 0, 0, 1, 1.0};
-      for (int k = 0; k < 14; ++k) fit[k] = rec[k];
-    }
-    return;
-  }
-  const double* wq = g.warm + 4ll * grp;
-  int nit = 0;
-  const Q4 q = extract_rotation(B, Q4{wq[0], wq[1], wq[2], wq[3]}, &nit);
-  if (tr && lane == 0) {
-    tr[3] = gtimer();
-    tr[6] = nit;
-  }
   const M3 Rf = qmat(q);
   const V3 rcent{gr[0], gr[1], gr[2]};
   double numer = 0.0;
   for (int i = i0; i < m1; i += 32) {
-    const double* mr = MR(i);
+    const double* mr = M.rest(i);
     const bool first = i == i0;
-    const int v = first ? 0 : MS(i);
-    const V3 c = (first ? c0 : ldc(v)) - cent;
-    const double s = first ? s0 : X[S * vp + v];
-    const M3 R = qmat(first ? q0 : ldq(ME(i)));
+    const int v = first ? 0 : M.slot(i);
+    const V3 c = (first ? st.c0 : ldc(v)) - st.cent;
+    const double s = first ? st.s0 : X[S * vp + v];
+    const M3 R = qmat(first ? st.q0 : ldq(M.eslot(i)));
     M3 rR;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
@@ -275,12 +292,12 @@ __device__ __forceinline__ void shape_group(const World& w, const Groups& g, dou
   numer = shape_wsum(numer);
   if (tr && lane == 0) tr[4] = gtimer();
   const double scale = fmax(numer / denom, kMinScale);
-  const V3 t = cent - scale * mvmul(Rf, rcent);
+  const V3 t = st.cent - scale * mvmul(Rf, rcent);
   const Q4 qf = qfrom_mat(Rf);
   auto apply = [&](int i) {
-    const double* mr = MR(i);
-    const int v = MS(i);
-    if (!(ci >= 0 ? sc->pinned[i + lb] : w.pinned[v])) {
+    const double* mr = M.rest(i);
+    const int v = M.slot(i);
+    if (!(st.ci >= 0 ? sc->pinned[i + st.lb] : w.pinned[v])) {
       const V3 x = scale * mvmul(Rf, V3{mr[0], mr[1], mr[2]} + rcent) + t;
       X[CX * vp + v] = x.x;
       X[CY * vp + v] = x.y;
@@ -292,14 +309,14 @@ __device__ __forceinline__ void shape_group(const World& w, const Groups& g, dou
       xr[1] = make_double2(x.z, sn);
     }
     const Q4 fr = qnormalized(qmul(qf, Q4{mr[13], mr[14], mr[15], mr[16]}));
-    const int e = ME(i);
+    const int e = M.eslot(i);
     X[QW * vp + e] = fr.w;
     X[QX * vp + e] = fr.x;
     X[QY * vp + e] = fr.y;
     X[QZ * vp + e] = fr.z;
   };
   __syncwarp();
-  if (ci >= 0 ? sc->serial[ci] : g.serial[grp]) {
+  if (st.ci >= 0 ? sc->serial[st.ci] : g.serial[grp]) {
     if (lane == 0)
       for (int i = m0; i < m1; ++i) apply(i);
   } else {
@@ -318,6 +335,40 @@ __device__ __forceinline__ void shape_group(const World& w, const Groups& g, dou
     wo[2] = q.y;
     wo[3] = q.z;
   }
+}
+
+// The degenerate group's fit record (scale 1, identity, t = mu - mubar; bundling.cpp:86-90).
+__device__ __forceinline__ void shape_degenerate_fit(const Groups& g, const ShapeCache* sc, const ShapeState& st,
+                                                     int lane, double* fit) {
+  if (!fit || lane != 0) return;
+  const double* gr = st.ci >= 0 ? sc->grest[st.ci] : g.grest + 4ll * st.grp;
+  const vm::V3 t = st.cent - vm::V3{gr[0], gr[1], gr[2]};
+  const double rec[14] = {1.0, t.x, t.y, t.z, 1, 0, 0, 0, 1, 0, 0, 0, 1, 1.0};
+  for (int k = 0; k < 14; ++k) fit[k] = rec[k];
+}
+
+// Fit and apply group `grp` (apply_shape_match, bundling.cpp:116-133) on the state rows X and
+// the slot records xrec, all phases in one warp (the rotation extraction redundantly in every
+// lane). tr: optional phase timestamps; sc: optional shared-memory copy of the group's statics;
+// fit: optional SimilarityFit record (bundling.h:18-23), 14 doubles: scale, translation xyz,
+// rotation (row-major 3x3), degenerate flag.
+__device__ __forceinline__ void shape_group(const World& w, const Groups& g, double* X, double* xrec, int grp,
+                                            int lane, unsigned long long* tr = nullptr, const ShapeCache* sc = nullptr,
+                                            double* fit = nullptr) {
+  if (tr && lane == 0) tr[0] = gtimer();
+  const ShapeState st = shape_begin(w, g, X, grp, lane, sc, tr);
+  if (st.degenerate) {
+    shape_degenerate_fit(g, sc, st, lane, fit);
+    return;
+  }
+  const double* wq = g.warm + 4ll * grp;
+  int nit = 0;
+  const vm::Q4 q = extract_rotation(st.B, vm::Q4{wq[0], wq[1], wq[2], wq[3]}, &nit);
+  if (tr && lane == 0) {
+    tr[3] = gtimer();
+    tr[6] = nit;
+  }
+  shape_end(w, g, X, xrec, st, q, lane, sc, tr, fit);
 }
 
 }  // namespace vdev

@@ -115,3 +115,4 @@ def test_gpu_similarity_recovery(oracle):
     fb, *_ = similarity_recovery(oracle)
     np.testing.assert_array_equal(fa[:, 13], fb[:, 13])
     np.testing.assert_allclose(fa, fb, rtol=1e-10, atol=1e-10)
+
