@@ -75,17 +75,17 @@ __device__ __forceinline__ double xget(const double* X, int f, int vp, int v) { 
 
 // X: snapshot state rows (pins / half-planes); xrec: the matching slot records (contacts);
 // lam: the multipliers before the sweep, SoA (component d of block b at lam[d * ls + b]);
-// pre: the contact's constants if the caller has them at hand (else read from `c`).
+// pre: the contact's constants if the caller has them at hand (else read from `c`); nct: the
+// substep's contact count (c.scalars[SC_NCT], read once by the caller: a dependent load less).
 template <class Emit>
 __device__ __forceinline__ ExtResult ext_block(const World& w, const Collide& c, const double* X, const double* xrec,
                                                const double* lam, long long ls, int b, const SweepParams& sp,
-                                               Emit&& emit, const ContactRef* pre = nullptr) {
+                                               Emit&& emit, const ContactRef* pre, int nct) {
   using namespace vm;
   ExtResult r;
   r.singular = r.bad = false;
   r.owner = 0;
   const int npins = sp.n_pins;
-  const int nct = c.scalars[SC_NCT];
   const int vp = w.vpad;
   const double h2 = sp.h2;
   const double contact_k = sp.contact_k;

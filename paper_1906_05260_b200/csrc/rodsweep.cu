@@ -102,6 +102,7 @@ struct Tile {
 template <int TP>
 struct PTile : Tile<TP> {
   int eoff[TP];
+  int ent_next;                   // dynamic entry distribution of the current sweep
   int e_item[kTileEntries];
   ContactRef e_ref[kTileEntries];
   alignas(16) double e_out[kTileEntries][4];  // read and written as double2
@@ -154,6 +155,7 @@ __device__ __forceinline__ void stage_rows(Tile<TP>& t, const World& w, const do
   constexpr int kChunks = (TP + 2) / 2;
   const int V = w.V, vp = w.vpad;
   const int tid = threadIdx.x, lane = tid & 31;
+  if (tid >= 32 * kWarps) return;  // the persistent kernel's external-block warp stages nothing
   for (int r = r0 + (tid >> 5); r < r1; r += kWarps) {  // one warp per row, lanes over its chunks
     if (!(kRowNeed[r] & mask)) continue;
     const int arr = kRowArr[r];
@@ -882,17 +884,19 @@ __device__ __forceinline__ void aux_ext_phase(const World& w, const Collide& c, 
                                               const SweepParams& sp, const double* cur, const double* xr_cur,
                                               const double* el_cur, double* el_nxt, int it, int* singular,
                                               unsigned long long* err) {
-  constexpr int kThreadsPerCta = 32 * warps_for<TP>();
+  const int kThreadsPerCta = blockDim.x;
   const int tid = threadIdx.x, lane = tid & 31;
   const int npins = sp.n_pins, nct = c.scalars[SC_NCT];
   const int n = npins + nct + c.scalars[SC_NHP];
   int nsing = 0;
   unsigned long long bad = kNoError;
   for (int b = (blockIdx.x - pp.tiles) * kThreadsPerCta + tid; b < n; b += pp.n_aux * kThreadsPerCta) {
-    const ExtResult r = ext_block(w, c, cur, xr_cur, el_cur, c.ext_cap, b, sp,
-                                  [&](int e, int flag, double x, double y, double z, double ds) {
-                                    put_entry(c.ext_contrib + 4ll * c.ext_pos[4 * b + e], flag, x, y, z, ds);
-                                  });
+    const ExtResult r = ext_block(
+        w, c, cur, xr_cur, el_cur, c.ext_cap, b, sp,
+        [&](int e, int flag, double x, double y, double z, double ds) {
+          put_entry(c.ext_contrib + 4ll * c.ext_pos[4 * b + e], flag, x, y, z, ds);
+        },
+        nullptr, nct);
     for (int d = 0; d < r.nlam; ++d) el_nxt[d * c.ext_cap + b] = r.lam[d];
     if (r.singular) ++nsing;
     if (r.bad) bad = umin64(bad, err_code(sp.substep, ERR_SWEEP, it, static_cast<unsigned long long>(sp.elastic_blocks) + b));
@@ -929,7 +933,7 @@ __device__ __forceinline__ void aux_ext_phase(const World& w, const Collide& c, 
 // (ping-pong lam_ext[2]) and counts; all CTAs share the shape work. The slot records are
 // ping-ponged (xrec[2]), so blocks solved elsewhere during a sweep always see the snapshot.
 template <int TP>
-__global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Collide c, Groups g, PersistParams pp,
+__global__ void __launch_bounds__(32 * (warps_for<TP>() + 1), 1) k_iterate(World w, Collide c, Groups g, PersistParams pp,
                                                                       SweepParams sp, int* singular,
                                                                       unsigned long long* err) {
   constexpr int kWarps = warps_for<TP>();
@@ -938,6 +942,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
   PTile<TP>& t = *reinterpret_cast<PTile<TP>*>(smem_raw);
   const bool is_aux = blockIdx.x >= pp.tiles;
   const bool inline_ext = pp.n_aux == 0;
+  const int nct = pp.has_ext ? c.scalars[SC_NCT] : 0;  // the substep's contact count
   const int start = is_aux ? 0 : blockIdx.x * kTileOwned;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int has_ext = pp.has_ext;
@@ -952,7 +957,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
       ent_q0 = q0;
       ent_n = min(q1 - q0, kTileEntries);
       if (inline_ext) {
-        const int npins = sp.n_pins, nct = c.scalars[SC_NCT];
+        const int npins = sp.n_pins;
         for (int i = tid; i < ent_n; i += 32 * kWarps) {
           const int item = c.ext_items[q0 + i];
           t.e_item[i] = item;
@@ -993,6 +998,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
       if (it > 0) {
         for (int i = tid; i < kKinds * TP; i += 32 * kWarps) t.act[i / TP][i % TP] = 0;
       }
+      if (tid == 0) t.ent_next = 0;  // published by the __syncthreads below
       stage_rows(t, w, cur, nullptr, start, mask, 0, T_SBAR);
       asm volatile("cp.async.wait_all;\n" ::: "memory");
       __syncthreads();
@@ -1003,10 +1009,18 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
       // endpoint's correction into the entry; the block's owner entry commits the multiplier.
       auto ext_entries = [&](int& nsing, unsigned long long& bad) {
         if (!has_ext || !inline_ext) return;
-        constexpr int kOrder[8] = {7, 0, 1, 5, 6, 2, 3, 4};  // rank of warp w (CS, SS, SB, VB.. first)
-        const int r = (kWarps == 8 ? kOrder[warp] : warp) * 32 + lane;
+        // Dynamic distribution: every warp takes the next 32 entries from a shared counter once
+        // it is done with its elastic items — the CTA's extra warp (no items) at once, the warps
+        // of the cheap kinds early, the heavy ones rarely. Each entry's result is independent of
+        // which warp computes it.
         const int q0 = t.eoff[0], q1 = t.eoff[kTileOwned];
-        for (int q = q0 + r; q < q1; q += 32 * kWarps) {
+        for (;;) {
+          int b0 = 0;
+          if (lane == 0) b0 = atomicAdd(&t.ent_next, 32);
+          b0 = __shfl_sync(0xffffffffu, b0, 0);
+          if (b0 >= q1 - q0) break;
+          const int q = q0 + b0 + lane;
+          if (q >= q1) continue;
           const int i = q - ent_q0;
           const bool staged = i < ent_n;
           const int item = staged ? t.e_item[i] : c.ext_items[q];
@@ -1017,7 +1031,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
               [&](int e2, int flag, double x, double y, double z, double ds) {
                 if (e2 == e) put_entry(out, flag, x, y, z, ds);
               },
-              staged && b >= sp.n_pins && b < sp.n_pins + c.scalars[SC_NCT] ? &t.e_ref[i] : nullptr);
+              staged && b >= sp.n_pins && b < sp.n_pins + nct ? &t.e_ref[i] : nullptr, nct);
           if (e == res.owner) {  // the block's owner entry commits it
             for (int d = 0; d < res.nlam; ++d) el_nxt[d * c.ext_cap + b] = res.lam[d];
             if (res.singular) ++nsing;
@@ -1070,7 +1084,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), 2) k_iterate(World w, Co
       // single call site keeps one copy of the group code in the kernel.
       const bool workers = inline_ext || is_aux;
       const int ncta = inline_ext ? gridDim.x : pp.n_aux, cta = inline_ext ? blockIdx.x : blockIdx.x - pp.tiles;
-      const int gw = warp * ncta + cta, nw = kWarps * ncta;
+      const int gw = warp * ncta + cta, nw = static_cast<int>(blockDim.x >> 5) * ncta;
       const bool chains = g.nchains > 0;
       const int phases = chains ? 1 : pp.levels;
       for (int l = 0; l < phases; ++l) {
@@ -1134,7 +1148,7 @@ int persistent_tiles(const World& w) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = sizeof(PTile<kPersistTP>);
   if (cudaFuncSetAttribute(k_iterate<kPersistTP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iterate<kPersistTP>, 32 * warps_for<kPersistTP>(), smem) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iterate<kPersistTP>, 32 * (warps_for<kPersistTP>() + 1), smem) !=
       cudaSuccess)
     return 0;
   return tiles <= per_sm * sms ? tiles : 0;
@@ -1145,7 +1159,7 @@ void launch_iterate_persistent(const World& w, Collide& c, const Groups& g, cons
   // pp.bar and pp.ext_done must be zero (Solver's fill)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pp.tiles + pp.n_aux);
-  cfg.blockDim = dim3(32 * warps_for<kPersistTP>());
+  cfg.blockDim = dim3(32 * (warps_for<kPersistTP>() + 1));  // + the external-block warp
   cfg.dynamicSmemBytes = sizeof(PTile<kPersistTP>);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

@@ -113,9 +113,10 @@ __global__ void __launch_bounds__(256, 4) k_ext_solve(World w, Collide c, const 
         o[0].x = ext_none();
       }
     };  // (rodsweep.cu put_entry is the same record format)
-    const ExtResult r = ext_block(w, c, X, w.xrec, c.ext_lam, ls, b, sp, [&](int e, int flag, double x, double y, double z, double ds) {
-      put_at(c.ext_pos[4 * b + e], flag, x, y, z, ds);
-    });
+    const ExtResult r = ext_block(
+        w, c, X, w.xrec, c.ext_lam, ls, b, sp,
+        [&](int e, int flag, double x, double y, double z, double ds) { put_at(c.ext_pos[4 * b + e], flag, x, y, z, ds); },
+        nullptr, nct);
     for (int d = 0; d < r.nlam; ++d) c.ext_lam[d * ls + b] = r.lam[d];
     if (r.singular) sing();
     if (r.bad)

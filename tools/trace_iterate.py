@@ -58,4 +58,4 @@ for cta, base, t0i in ((0, 900, 899), (27, 932, 898)):
     t0 = raw[t0i]
     if t0 > 0:
         print(f"iteration 1, CTA {cta}: per-warp end of items / of ext entries (us after staging):",
-              [round((raw[base + k] - t0) / 1e3, 2) for k in range(8)], [round((raw[base + 16 + k] - t0) / 1e3, 2) for k in range(8)])
+              [round((raw[base + k] - t0) / 1e3, 2) for k in range(9)], [round((raw[base + 16 + k] - t0) / 1e3, 2) for k in range(9)])
