@@ -104,17 +104,22 @@ __global__ void k_scan_small(const int* __restrict__ in, int* __restrict__ out, 
   pdl_wait();
   pdl_trigger();
   const long long n = n_dev ? static_cast<long long>(*n_dev) : n_cap;
-  const long long chunk = (n + kThreads - 1) / kThreads;
-  const long long b = threadIdx.x * chunk, e = b + chunk < n ? b + chunk : n;
+  constexpr int kChunk = kSmallScan / kThreads;  // 64 consecutive elements per thread
+  const long long b = static_cast<long long>(threadIdx.x) * kChunk;
+  int vals[kChunk];
+#pragma unroll
+  for (int k = 0; k < kChunk; ++k) vals[k] = b + k < n ? in[b + k] : 0;  // all loads in flight
   int sum = 0;
-  for (long long i = b; i < e; ++i) sum += in[i];
+#pragma unroll
+  for (int k = 0; k < kChunk; ++k) sum += vals[k];
   int total;
   int run = block_excl(sum, &total);
-  for (long long i = b; i < e; ++i) {
-    const int v = in[i];
-    out[i] = run;
-    run += v;
-  }
+#pragma unroll
+  for (int k = 0; k < kChunk; ++k)
+    if (b + k < n) {
+      out[b + k] = run;
+      run += vals[k];
+    }
   if (threadIdx.x == 0) out[n] = total;
 }
 

@@ -377,17 +377,21 @@ __global__ void k_report_partial(World w, const double* __restrict__ X, int clas
 #pragma unroll
   for (int q = 0; q < 16; ++q) acc[q] = 0.0;
   if (v < w.V) slot_residual_terms(w, X, classic, v, acc);
-  // fixed-order block tree reduction
-  __shared__ double red[kRepThreads];
+  // fixed-order reduction: a shuffle tree per warp, then the warps' sums in warp order
+  __shared__ double red[16][kRepThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
   for (int q = 0; q < 16; ++q) {
-    red[threadIdx.x] = acc[q];
-    __syncthreads();
-    for (int s = kRepThreads / 2; s > 0; s >>= 1) {
-      if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) partials[16ll * blockIdx.x + q] = red[0];
-    __syncthreads();
+    double x = acc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) red[q][warp] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < 16) {
+    double x = red[threadIdx.x][0];
+    for (int k = 1; k < kRepThreads / 32; ++k) x += red[threadIdx.x][k];
+    partials[16ll * blockIdx.x + threadIdx.x] = x;
   }
 }
 
