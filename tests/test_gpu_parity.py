@@ -284,3 +284,24 @@ def test_persistent_kernel_matches_per_launch_path(gpu, oracle, name, monkeypatc
                 np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
     assert _iterate_launches(gpu, b) == 0
     assert _iterate_launches(gpu, a) > 0 and _iterate_launches(gpu, c) > 0  # the persistent paths really ran
+
+
+def test_large_world_tiles_bitwise(gpu, oracle):
+    """Worlds of >= 2 x 148 x 62 slots run the 64-wide per-sweep kernel (bulk TMA staging of
+    interior tiles, cp.async at the world's edges, early ext wait + L2 prefetch) — the C4 / C5
+    configuration. A 40 x 20 forest of 24-vertex rods (19,200 slots, live contacts) must stay
+    bit-identical to the oracle."""
+    from paper_1906_05260_b200 import workloads
+    scene = workloads.c4_rod_forest(oracle, nx=40, ny=20, vertices=24)
+    g, o = SolverHandle(gpu, scene), SolverHandle(oracle, scene)
+    assert g.total_vertices >= 2 * 148 * 62
+    for _ in range(2):
+        rg, ro = g.step(), o.step()
+        assert_reports_equal(rg, ro)
+        sg, so = g.state(), o.state()
+        for k in sg:
+            np.testing.assert_array_equal(sg[k], so[k], err_msg=k)
+    assert rg.contact_count > 0
+    cg, co = g.contacts(), o.contacts()
+    for k in cg:
+        np.testing.assert_array_equal(cg[k], co[k], err_msg=k)
