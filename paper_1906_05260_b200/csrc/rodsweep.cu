@@ -13,6 +13,8 @@
 // --fmad=false the result is the reference's arithmetic bit for bit; there are no atomics on
 // the data path (bitwise run-to-run determinism) and no colouring (Jacobi
 // snapshot semantics, test_sweep.cpp:132-142).
+#include <cstdlib>
+
 #include "ext.cuh"
 #include "kernels.cuh"
 #include "shape.cuh"
@@ -29,7 +31,7 @@ namespace {
 // Warps per CTA: 4 for 64-wide tiles; 8 for 32-wide tiles (small worlds are latency-bound:
 // one item round per thread instead of two).
 template <int TP>
-constexpr int warps_for() { return TP == 64 ? 4 : 8; }
+constexpr int warps_for() { return TP == 32 ? 8 : 4; }
 
 __device__ __forceinline__ unsigned long long umin64(unsigned long long a, unsigned long long b) { return a < b ? a : b; }
 
@@ -90,7 +92,7 @@ struct Tile {
   double st[kStageRows][kTileStage];
   PosRes res[kTilePos];
   int loc[kTilePos], m[kTilePos], kinds[kTilePos], bbase[kTilePos];
-  unsigned wmask[kTilePos / 32];  // OR of the kinds present, per 32 positions
+  unsigned wmask[(kTilePos + 31) / 32];  // OR of the kinds present, per 32 positions
   int klist[kKinds];              // the kinds present, ascending
   uint8_t act[kKinds][kTilePos];
   alignas(8) unsigned long long bar;  // mbarrier of the bulk (TMA) staging
@@ -118,10 +120,12 @@ __device__ __forceinline__ unsigned tile_meta(Tile<TP>& t, const World& w, int s
   constexpr int kTilePos = TP;
   const int V = w.V;
   const int tid = threadIdx.x, lane = tid & 31;
-  for (int i = tid; i < kTilePos; i += 32 * kWarps) {
+  // every lane of every warp takes part in the kind reduction (tiles need not be multiples of 32)
+  for (int i0 = tid & ~31; i0 < kTilePos; i0 += 32 * kWarps) {
+    const int i = i0 + lane;
     const int p = start - 1 + i;
     int k = -1, m = 0, kinds = 0, bb = 0;
-    if (p >= 0 && p < V) {
+    if (i < kTilePos && p >= 0 && p < V) {
       const int r = w.slot_rod[p];
       k = w.slot_loc[p];
       m = w.slot_m[p];
@@ -129,18 +133,20 @@ __device__ __forceinline__ unsigned tile_meta(Tile<TP>& t, const World& w, int s
       bb = w.rod_block_base[r];
     }
     const unsigned wm = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(kinds));
-    if (lane == 0) t.wmask[i >> 5] = wm;
-    t.loc[i] = k;
-    t.m[i] = m;
-    t.kinds[i] = kinds;
-    t.bbase[i] = bb;
+    if (lane == 0) t.wmask[i0 >> 5] = wm;
+    if (i < kTilePos) {
+      t.loc[i] = k;
+      t.m[i] = m;
+      t.kinds[i] = kinds;
+      t.bbase[i] = bb;
 #pragma unroll
-    for (int a = 0; a < kKinds; ++a) t.act[a][i] = 0;
+      for (int a = 0; a < kKinds; ++a) t.act[a][i] = 0;
+    }
   }
   __syncthreads();
   unsigned mask = 0;
 #pragma unroll
-  for (int i = 0; i < kTilePos / 32; ++i) mask |= t.wmask[i];
+  for (int i = 0; i < (kTilePos + 31) / 32; ++i) mask |= t.wmask[i];
   if (tid < kKinds && (mask & (1u << tid))) t.klist[__popc(mask & ((1u << tid) - 1))] = tid;  // n-th kind present
   return mask;
 }
@@ -793,7 +799,7 @@ __device__ __forceinline__ void put_entry(double* out, int flag, double x, doubl
 
 // One sweep per launch (large worlds; every world when the persistent kernel does not apply).
 template <int TP>
-__global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_sweep(World w, Collide c, const double* __restrict__ X,
+__global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 32 ? 2 : 4) k_rod_sweep(World w, Collide c, const double* __restrict__ X,
                                                           double* __restrict__ Y, SweepParams sp, int* singular,
                                                           unsigned long long* err, int has_ext) {
   constexpr int kWarps = warps_for<TP>();
@@ -821,7 +827,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 64 ? 4 : 2) k_rod_
   // entry range into L2 so the gather after the block solves finds it on chip. Small worlds
   // (latency-bound): solve the tile's blocks first, overlapping the ext solve's tail, and wait
   // just before the gather.
-  constexpr bool kEarlyWait = TP == 64;
+  constexpr bool kEarlyWait = TP != 32;
   if (kEarlyWait && sp.pdl == 2) {
     pdl_wait();
     pdl_trigger();
