@@ -194,7 +194,8 @@ struct PersistParams {
   int levels;              // shape-matching levels (<= kMaxPersistLevels)
   int has_ext;
   int level_off[kMaxPersistLevels + 1];
-  unsigned long long* trace;  // optional phase timestamps of CTA 0 (globaltimer ns), see k_iterate
+  unsigned long long* trace;  // optional phase timestamps (globaltimer ns), see k_iterate
+  int trace_cta;              // CTA whose per-warp phases are traced
 };
 constexpr int kTraceCap = 1024;
 

@@ -613,11 +613,9 @@ __device__ __forceinline__ void solve_items(Tile<TP>& t, const World& w, const S
       }
     }
   }
-  if (sp.dbg && (blockIdx.x == 0 || blockIdx.x == 27) && (threadIdx.x & 31) == 0)
-    sp.dbg[(blockIdx.x ? 32 : 0) + (threadIdx.x >> 5)] = gtimer();
+  if (sp.dbg && (threadIdx.x & 31) == 0) sp.dbg[threadIdx.x >> 5] = gtimer();  // VROD_TRACE: items done
   post(nsing, bad);
-  if (sp.dbg && (blockIdx.x == 0 || blockIdx.x == 27) && (threadIdx.x & 31) == 0)
-    sp.dbg[(blockIdx.x ? 48 : 16) + (threadIdx.x >> 5)] = gtimer();
+  if (sp.dbg && (threadIdx.x & 31) == 0) sp.dbg[16 + (threadIdx.x >> 5)] = gtimer();  // + external entries
   if (__any_sync(0xffffffffu, nsing != 0 || bad != kNoError)) {  // rare: singular blocks / errors
     for (int o = 16; o > 0; o >>= 1) {
       nsing += __shfl_down_sync(0xffffffffu, nsing, o);
@@ -1046,8 +1044,9 @@ __global__ void __launch_bounds__(32 * (warps_for<TP>() + 1), 1) k_iterate(World
           }
         }
       };
-      sp.dbg = pp.trace && it == 1 ? pp.trace + 900 : nullptr;  // debug trace (VROD_TRACE=1)
-      if (sp.dbg && (blockIdx.x == 0 || blockIdx.x == 27) && tid == 0) pp.trace[blockIdx.x ? 898 : 899] = gtimer();
+      // VROD_TRACE: per-warp phase ends of one CTA (pp.trace_cta, default 0) in iteration 1
+      sp.dbg = pp.trace && it == 1 && blockIdx.x == pp.trace_cta ? pp.trace + 900 : nullptr;
+      if (sp.dbg && tid == 0) pp.trace[899] = gtimer();
       solve_items<TP, true>(t, w, sp, start, mask, singular + it, err, ext_entries);  // ends with __syncthreads()
       mark();
       if (has_ext && !inline_ext) {  // the aux CTAs' external blocks of this sweep

@@ -717,6 +717,7 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
       pp.tiles = persist_tiles_;
       pp.n_aux = persist_aux_;
       pp.trace = d_trace_;
+      pp.trace_cta = std::getenv("VROD_TRACE_CTA") ? std::atoi(std::getenv("VROD_TRACE_CTA")) : 0;
       pp.iterations = iterations;
       pp.sm_period = scene_.settings.sm_period;
       pp.levels = g_.levels;

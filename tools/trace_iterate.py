@@ -1,5 +1,6 @@
 """Phase timeline of the persistent iteration kernel (CTA 0), VROD_TRACE=1: per iteration
-stage X / solve blocks / gather / barrier, then shape-matching levels. Usage: trace_iterate.py [C3]"""
+stage X / solve blocks / gather / barrier, then shape-matching levels; per-warp phases of CTA
+$VROD_TRACE_CTA in iteration 1. Usage: trace_iterate.py [C3]"""
 import ctypes as C, os, sys
 os.environ["VROD_TRACE"] = "1"
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -54,8 +55,8 @@ for l in range(2):
     if ph[0] > 0:
         print(f"shape level/chain pos {l} group phases us: centroid {(ph[1]-ph[0])/1e3:.2f} covariance {(ph[2]-ph[1])/1e3:.2f} "
               f"rotation {(ph[3]-ph[2])/1e3:.2f} ({int(raw[606 + 8 * l])} it) scale {(ph[4]-ph[3])/1e3:.2f} apply {(ph[5]-ph[4])/1e3:.2f}")
-for cta, base, t0i in ((0, 900, 899), (27, 932, 898)):
-    t0 = raw[t0i]
-    if t0 > 0:
-        print(f"iteration 1, CTA {cta}: per-warp end of items / of ext entries (us after staging):",
-              [round((raw[base + k] - t0) / 1e3, 2) for k in range(9)], [round((raw[base + 16 + k] - t0) / 1e3, 2) for k in range(9)])
+cta = int(os.environ.get("VROD_TRACE_CTA", "0"))
+t0 = raw[899]
+if t0 > 0:
+    print(f"iteration 1, CTA {cta}: per-warp end of items / of external entries (us after staging):",
+          [round((raw[900 + k] - t0) / 1e3, 2) for k in range(9)], [round((raw[916 + k] - t0) / 1e3, 2) for k in range(9)])
