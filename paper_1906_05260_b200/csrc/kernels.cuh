@@ -286,6 +286,10 @@ void launch_penetration(const World& w, Collide& c, const double* X, StepAccum* 
 // batch: per-scene residual norms (one CTA per scene) and end-of-substep singular fold-in
 void launch_scene_report(const World& w, const double* X, int classic, int* scene_singular, cudaStream_t st);
 int report_parts(int V);
+// kinetic energy and total volume (out[0], out[1]) in the reference's summation order;
+// terms: 4 x V scratch, rod_vol: R scratch; cw / sw: the layout's center / scale weights
+void launch_energy(const World& w, const double* X, const double* cw, const double* sw, int classic, double* terms,
+                   double* rod_vol, double* out, cudaStream_t st);
 // eval_constraint(...).W of every elastic block, 3 doubles each, in block order
 void launch_block_residuals(const World& w, const double* X, int classic, double* out, cudaStream_t st);
 

@@ -1195,48 +1195,24 @@ void Solver::set_loads(const double* fd, const uint8_t* fdr, const double* tq, c
 }
 
 void Solver::energy(double* ke, double* vol, double* rest_vol) {
-  const int vpad = setup_.vpad;
-  std::vector<double> X(static_cast<std::size_t>(vdev::kStateFields) * vpad), vel(static_cast<std::size_t>(vdev::kVelFields) * vpad),
-      es(static_cast<std::size_t>(vdev::kEStatFields) * vpad);
-  check_cuda(cudaMemcpy(X.data(), w_.X, sizeof(double) * X.size(), cudaMemcpyDeviceToHost), "energy");
-  check_cuda(cudaMemcpy(vel.data(), w_.vel, sizeof(double) * vel.size(), cudaMemcpyDeviceToHost), "energy");
-  check_cuda(cudaMemcpy(es.data(), w_.estat, sizeof(double) * es.size(), cudaMemcpyDeviceToHost), "energy");
-  if (ke) {  // Solver::kinetic_energy, solver.cpp:400-418
-    double en = 0.0;
-    for (int v = 0; v < setup_.V; ++v) {
-      if (std::isinf(cw_[v])) continue;  // inv_center == 0
-      const V3 u{vel[vdev::VX * vpad + v], vel[vdev::VY * vpad + v], vel[vdev::VZ * vpad + v]};
-      en += 0.5 * cw_[v] * sqnorm(u);
-      if (!classic_) en += 0.5 * sw_[v] * vel[vdev::VS * vpad + v] * vel[vdev::VS * vpad + v];
+  // Solver::kinetic_energy (solver.cpp:400-418) and current_volume (rod.cpp:178-187) on the
+  // device: terms in parallel, sums in the reference's sequential order (launch_energy).
+  if (ke || vol) {
+    const std::size_t V = static_cast<std::size_t>(setup_.V), R = static_cast<std::size_t>(setup_.R);
+    if (!d_energy_) {
+      d_energy_ = dalloc<double>(6 * V + R + 2);
+      check_cuda(cudaMemcpyAsync(d_energy_ + 4 * V, cw_.data(), sizeof(double) * V, cudaMemcpyHostToDevice, stream_), "energy");
+      check_cuda(cudaMemcpyAsync(d_energy_ + 5 * V, sw_.data(), sizeof(double) * V, cudaMemcpyHostToDevice, stream_), "energy");
     }
-    for (int r = 0; r < setup_.R; ++r) {
-      const int m = scene_.rods[r].n - 1, v0 = setup_.vbase[r];
-      for (int k = 0; k < m; ++k) {
-        const int v = v0 + k;
-        const double base = es[vdev::TWB * vpad + v];
-        const V3 tw{0.25 * base, 0.25 * base, 0.5 * base};
-        const V3 u{vel[vdev::WX * vpad + v], vel[vdev::WY * vpad + v], vel[vdev::WZ * vpad + v]};
-        en += 0.5 * dot(u, cwmul(tw, u));
-      }
-    }
-    *ke = en;
-  }
-  if (vol) {  // current_volume, rod.cpp:178-187
-    double t = 0.0;
-    for (int r = 0; r < setup_.R; ++r) {
-      const RodData& rod = scene_.rods[r];
-      const int v0 = setup_.vbase[r];
-      double v = 0.0;
-      for (int e = 0; e < rod.n - 1; ++e) {
-        const double s = 0.5 * (X[vdev::S * vpad + v0 + e] + X[vdev::S * vpad + v0 + e + 1]);
-        const double rr = 0.5 * (rod.r[e] + rod.r[e + 1]);
-        const V3 a{X[vdev::CX * vpad + v0 + e], X[vdev::CY * vpad + v0 + e], X[vdev::CZ * vpad + v0 + e]};
-        const V3 b{X[vdev::CX * vpad + v0 + e + 1], X[vdev::CY * vpad + v0 + e + 1], X[vdev::CZ * vpad + v0 + e + 1]};
-        v += kPi * (s * rr) * (s * rr) * norm(b - a);
-      }
-      t += v;
-    }
-    *vol = t;
+    double* terms = d_energy_;
+    double* out = d_energy_ + 6 * V + R;
+    vdev::launch_energy(w_, w_.X, d_energy_ + 4 * V, d_energy_ + 5 * V, classic_ ? 1 : 0, terms, d_energy_ + 6 * V, out,
+                        stream_);
+    double res[2];
+    check_cuda(cudaMemcpyAsync(res, out, sizeof(res), cudaMemcpyDeviceToHost, stream_), "energy");
+    check_cuda(cudaStreamSynchronize(stream_), "energy");
+    if (ke) *ke = res[0];
+    if (vol) *vol = res[1];
   }
   if (rest_vol) {  // rest_volume, rod.cpp:189-197
     double t = 0.0;

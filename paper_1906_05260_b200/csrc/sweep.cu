@@ -369,6 +369,56 @@ __global__ void k_block_residuals(World w, const double* __restrict__ X, int cla
   }
 }
 
+// ---- Solver::kinetic_energy / total_volume (solver.cpp:400-430, rod.cpp:178-187) on the device.
+// The terms are computed in parallel; the sums run in the reference's sequential order (one
+// thread, or one thread per rod for the per-rod volumes), so the results are the same bits.
+// terms: 4 per slot — vertex kinetic, scale kinetic, element kinetic, element volume.
+__global__ void k_energy_terms(World w, const double* __restrict__ X, const double* __restrict__ cw,
+                               const double* __restrict__ sw, double* __restrict__ terms) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < w.V; v += gridDim.x * blockDim.x) {
+    const int vp = w.vpad;
+    const V3 u{F(w.vel, VX, vp, v), F(w.vel, VY, vp, v), F(w.vel, VZ, vp, v)};
+    const double svel = F(w.vel, VS, vp, v);
+    terms[4ll * v] = 0.5 * cw[v] * sqnorm(u);
+    terms[4ll * v + 1] = 0.5 * sw[v] * svel * svel;
+    if (w.slot_loc[v] < w.slot_m[v]) {
+      const double base = F(w.estat, TWB, vp, v);
+      const V3 tw{0.25 * base, 0.25 * base, 0.5 * base};
+      const V3 om{F(w.vel, WX, vp, v), F(w.vel, WY, vp, v), F(w.vel, WZ, vp, v)};
+      terms[4ll * v + 2] = 0.5 * dot(om, cwmul(tw, om));
+      const double s = 0.5 * (F(X, S, vp, v) + F(X, S, vp, v + 1));
+      const double rr = 0.5 * (F(w.vstat, RBAR, vp, v) + F(w.vstat, RBAR, vp, v + 1));
+      terms[4ll * v + 3] = kPi * (s * rr) * (s * rr) * norm(ldc(X, vp, v + 1) - ldc(X, vp, v));
+    }
+  }
+}
+// per rod: its elements' volume terms in order (rod.cpp:178-187)
+__global__ void k_rod_volumes(World w, const double* __restrict__ terms, double* __restrict__ rod_vol) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < w.R; r += gridDim.x * blockDim.x) {
+    const int v0 = w.rod_vbase[r], m = w.rod_n[r] - 1;
+    double v = 0.0;
+    for (int e = 0; e < m; ++e) v += terms[4ll * (v0 + e) + 3];
+    rod_vol[r] = v;
+  }
+}
+// one thread: kinetic energy in the reference's order (vertices, then elements), volume over rods
+__global__ void k_energy_sum(World w, const double* __restrict__ terms, const double* __restrict__ cw,
+                             const double* __restrict__ rod_vol, int classic, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double en = 0.0;
+  for (int v = 0; v < w.V; ++v) {
+    if (isinf(cw[v])) continue;  // inv_center == 0
+    en += terms[4ll * v];
+    if (!classic) en += terms[4ll * v + 1];
+  }
+  for (int v = 0; v < w.V; ++v)
+    if (w.slot_loc[v] < w.slot_m[v]) en += terms[4ll * v + 2];
+  double vol = 0.0;
+  for (int r = 0; r < w.R; ++r) vol += rod_vol[r];
+  out[0] = en;
+  out[1] = vol;
+}
+
 __global__ void k_report_partial(World w, const double* __restrict__ X, int classic, double* partials) {
   pdl_wait();
   pdl_trigger();
@@ -514,6 +564,13 @@ void launch_residuals(const World& w, const double* X, int classic, double* part
                       cudaStream_t st) {
   launch_kernel(k_report_partial, parts, kRepThreads, 0, st, g_pdl, w, X, classic, partials);
   launch_kernel(k_report_final, 1, kRepThreads, 0, st, g_pdl, partials, parts, out8);
+}
+
+void launch_energy(const World& w, const double* X, const double* cw, const double* sw, int classic, double* terms,
+                   double* rod_vol, double* out, cudaStream_t st) {
+  launch_kernel(k_energy_terms, grid_for(w.V), kThreads, 0, st, false, w, X, cw, sw, terms);
+  launch_kernel(k_rod_volumes, grid_for(w.R), kThreads, 0, st, false, w, terms, rod_vol);
+  launch_kernel(k_energy_sum, 1, 32, 0, st, false, w, terms, cw, rod_vol, classic, out);
 }
 
 void launch_block_residuals(const World& w, const double* X, int classic, double* out, cudaStream_t st) {

@@ -73,6 +73,9 @@ def test_bitwise_equal_to_oracle(gpu, oracle, name):
     sg, so = g.state(), o.state()
     for k in sg:
         np.testing.assert_array_equal(sg[k], so[k], err_msg=f"{name}: {k}")
+    # device-side energy / volume sums follow the reference's sequential order: same bits
+    assert g.kinetic_energy() == o.kinetic_energy()
+    assert g.total_volume() == o.total_volume()
 
 
 @pytest.mark.parametrize("name", sorted(BUNDLE_SCENES))
@@ -302,6 +305,8 @@ def test_large_world_tiles_bitwise(gpu, oracle):
         for k in sg:
             np.testing.assert_array_equal(sg[k], so[k], err_msg=k)
     assert rg.contact_count > 0
+    assert g.kinetic_energy() == o.kinetic_energy()
+    assert g.total_volume() == o.total_volume()
     cg, co = g.contacts(), o.contacts()
     for k in cg:
         np.testing.assert_array_equal(cg[k], co[k], err_msg=k)
