@@ -5,11 +5,12 @@
 //
 // Broad phase on the GPU: the grid is an open-addressing hash table of cell keys built with
 // atomicCAS (one representative pill per cell), a count -> exclusive scan -> scatter counting
-// sort of pill ids into cells, then per pill a 27-cell scan that (1) counts every allowed pair
-// j > i (StepReport.broad_pairs, exactly the reference's candidate count) and (2) keeps the
-// pairs whose bounding spheres overlap — the only pairs that can penetrate — sorted by j.
-// Candidates are therefore in (i, j) order like the reference's pair list, and so are the
-// contacts after the stream compaction of the narrow-phase hits.
+// sort of pill ids into cells (with cell-sorted copies of the per-pill data the pair scan
+// reads), then a 27-cell scan per pill (small worlds) or per cell (large worlds) that (1) counts
+// every allowed pair j > i (StepReport.broad_pairs, exactly the reference's candidate count)
+// and (2) keeps the pairs that can penetrate (bounding spheres, then segment distance). The
+// candidate list is unordered; the narrow-phase hits are put in the reference's (i, j) order
+// afterwards (k_ct_order in one CTA, or count -> scan -> scatter -> per-i sort).
 #include <algorithm>
 #include <cfloat>
 
@@ -46,23 +47,29 @@ __device__ __forceinline__ bool pill_less(const PillV& a, const PillV& b) {  // 
   if (a.r0 != b.r0) return a.r0 < b.r0;
   return a.r1 < b.r1;
 }
-// deepest_penetration, collision.cpp:78-135.
-__device__ void deepest(const PillV& A, const PillV& B, int iterations, double warm, double& alpha_out,
-                        double& beta_out, double& dist_out) {
-  const bool swapped = pill_less(B, A);
-  const PillV& pa = swapped ? B : A;
-  const PillPrep pb = prep_pill(swapped ? A : B);
-  if (swapped && warm >= 0.0) warm = -1.0;
+// deepest_penetration, collision.cpp:78-135, in two parts: the dichotomous search (which does not
+// depend on the warm start) and the final evaluations of lo, hi and the warm alpha. Split so the
+// narrow phase can look the warm start up on another lane while the search runs.
+struct DeepState {
+  PillV pa;
+  PillPrep pb;
+  bool swapped;
+  double lo, hi, best, best_a, best_b;
+};
+__device__ __forceinline__ void deepest_search(const PillV& A, const PillV& B, int iterations, DeepState& s) {
+  s.swapped = pill_less(B, A);
+  s.pa = s.swapped ? B : A;
+  s.pb = prep_pill(s.swapped ? A : B);
   double lo = 0.0, hi = 1.0;
   double best_a = 0.5, best_b = 0.0;
-  double best = pair_distance(pa, pb, 0.5, best_b);
+  double best = pair_distance(s.pa, s.pb, 0.5, best_b);
   const double delta = 1e-6;
   for (int it = 0; it < iterations; ++it) {
     const double mid = 0.5 * (lo + hi);
     const double x1 = mid - delta, x2 = mid + delta;
     double b1 = 0.0, b2 = 0.0;
-    const double f1 = pair_distance(pa, pb, x1, b1);
-    const double f2 = pair_distance(pa, pb, x2, b2);
+    const double f1 = pair_distance(s.pa, s.pb, x1, b1);
+    const double f2 = pair_distance(s.pa, s.pb, x2, b2);
     if (f1 < best) {
       best = f1;
       best_a = x1;
@@ -76,13 +83,23 @@ __device__ void deepest(const PillV& A, const PillV& B, int iterations, double w
     if (f1 <= f2) hi = x2;
     else lo = x1;
   }
-  const double cands[3] = {lo, hi, warm};
+  s.lo = lo;
+  s.hi = hi;
+  s.best = best;
+  s.best_a = best_a;
+  s.best_b = best_b;
+}
+__device__ __forceinline__ void deepest_finish(const DeepState& s, double warm, double& alpha_out, double& beta_out,
+                                               double& dist_out) {
+  if (s.swapped && warm >= 0.0) warm = -1.0;
+  double best = s.best, best_a = s.best_a, best_b = s.best_b;
+  const double cands[3] = {s.lo, s.hi, warm};
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     const double cand = cands[k];
     if (cand < 0.0 || cand > 1.0) continue;
     double bc = 0.0;
-    const double fc = pair_distance(pa, pb, cand, bc);
+    const double fc = pair_distance(s.pa, s.pb, cand, bc);
     if (fc < best) {
       best = fc;
       best_a = cand;
@@ -90,13 +107,19 @@ __device__ void deepest(const PillV& A, const PillV& B, int iterations, double w
     }
   }
   dist_out = best;
-  if (swapped) {
+  if (s.swapped) {
     alpha_out = best_b;
     beta_out = best_a;
   } else {
     alpha_out = best_a;
     beta_out = best_b;
   }
+}
+__device__ void deepest(const PillV& A, const PillV& B, int iterations, double warm, double& alpha_out,
+                        double& beta_out, double& dist_out) {
+  DeepState s;
+  deepest_search(A, B, iterations, s);
+  deepest_finish(s, warm, alpha_out, beta_out, dist_out);
 }
 // bounding_sphere, collision.cpp:137-153.
 __device__ __forceinline__ void bounding_sphere(const PillV& p, V3& c, double& r) {
@@ -277,6 +300,12 @@ __global__ void k_scatter(Collide c) {
   const int h = c.pill_cell[i];
   const int pos = c.cell_start[h] + atomicAdd(&c.cell_cursor[h], 1);
   c.cell_items[pos] = i;
+  // cell-sorted copies of what the pair scan reads per neighbour: contiguous per cell, so the
+  // scan's loads are coalesced and need no second indirection
+  c.cell_attr[pos] = make_int4(i, c.pill_rod[i], c.pill_group[i], 2 * c.pill_el[i] + (c.pill_self[i] ? 1 : 0));
+  double2* sp = reinterpret_cast<double2*>(c.cell_sph) + 2 * pos;
+  sp[0] = make_double2(c.bsph[i], c.bsph[c.P + i]);
+  sp[1] = make_double2(c.bsph[2 * c.P + i], c.bsph[3 * c.P + i]);
 }
 
 __device__ __forceinline__ int find_cell(const Collide& c, long long kx, long long ky, long long kz, int scene) {
@@ -364,28 +393,40 @@ __device__ __forceinline__ bool may_penetrate(const Collide& c, int i, int j) {
 }
 
 // One WARP per pill i. Lanes 0..26 probe the 27 cells of i's 3x3x3 block in parallel; the warp
-// then strides over the flattened list of their items (uniform work per lane), counts every
-// allowed pair j > i (broad_phase, collision.cpp:213-226 — StepReport.broad_pairs) and keeps the
-// pairs that may penetrate. Each CTA (8 pills) counts first, reserves its slots in the global
-// candidate list with ONE atomic, then writes (the checks are recomputed: cheaper than
-// storing them). The list is unordered; contacts are put in (i, j) order after the narrow phase.
+// then strides over the flattened list of their items (uniform work per lane, kPairUnroll items
+// per lane in flight), reading the cell-sorted copies (cell_attr, cell_sph) written by k_scatter.
+// It counts every allowed pair j > i (broad_phase, collision.cpp:213-226 — StepReport.broad_pairs)
+// and keeps the pairs whose bounding spheres touch (prefilter; all allowed pairs without it). Kept pairs
+// collect in a per-warp shared buffer; the CTA reserves its slots with one atomic at the end
+// (a full buffer flushes early with its own). The list is unordered; contacts are put in (i, j)
+// order after the narrow phase.
+// may_penetrate's exact segment test (out of line: keeps the pair scan's registers low)
+__device__ __noinline__ bool segments_close(const double* __restrict__ pill, int P, int i, int j) {
+  const PillV a = load_pill(pill, P, i), b = load_pill(pill, P, j);
+  const double rr = (fmax(a.r0, a.r1) + fmax(b.r0, b.r1)) * (1.0 + 1e-9) + 1e-12;
+  return seg_seg_dist2(a.c0, a.c1, b.c0, b.c1) <= rr * rr;
+}
 constexpr int kPairWarps = 8;
-__global__ void __launch_bounds__(32 * kPairWarps) k_pairs_warp(Collide c, int prefilter, int* broad_total,
-                                                                int* cand_total) {
+constexpr int kPairUnroll = 4;
+constexpr int kPairBuf = 64;
+__global__ void __launch_bounds__(32 * kPairWarps, 3) k_pairs_warp(Collide c, int prefilter, int* broad_total,
+                                                                int* cand_total, int* out_i, int* out_j) {
   pdl_wait();
   pdl_trigger();
   __shared__ int s_start[kPairWarps][27];
   __shared__ int s_off[kPairWarps][28];
-  __shared__ int s_cnt[kPairWarps];
+  __shared__ int s_buf[kPairWarps][kPairBuf];
+  __shared__ int s_cnt[kPairWarps], s_broad[kPairWarps];
   __shared__ int s_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = c.P;
   const int i = blockIdx.x * kPairWarps + warp;
-  const bool live = i < c.P;
+  const bool live = i < P;
   int size = 0;
   const int scene = live && c.pill_scene ? c.pill_scene[i] : 0;
   if (live && lane < 27) {
-    const int h = find_cell(c, c.cellkey[i] + (lane / 9 - 1), c.cellkey[c.P + i] + ((lane / 3) % 3 - 1),
-                            c.cellkey[2 * c.P + i] + (lane % 3 - 1), scene);
+    const int h = find_cell(c, c.cellkey[i] + (lane / 9 - 1), c.cellkey[P + i] + ((lane / 3) % 3 - 1),
+                            c.cellkey[2 * P + i] + (lane % 3 - 1), scene);
     if (h >= 0) {
       s_start[warp][lane] = c.cell_start[h];
       size = c.cell_start[h + 1] - c.cell_start[h];
@@ -403,72 +444,98 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pairs_warp(Collide c, int p
   __syncwarp();
   int ri = 0, gi = 0, ei = 0;
   bool si = false;
+  double xi = 0, yi = 0, zi = 0, Ri = 0;
   if (live) {
     ri = c.pill_rod[i];
     gi = c.pill_group[i];
     ei = c.pill_el[i];
     si = c.pill_self[i] != 0;
+    xi = c.bsph[i];
+    yi = c.bsph[P + i];
+    zi = c.bsph[2 * P + i];
+    Ri = c.bsph[3 * P + i];
   }
-  int cur_d = 0;            // a lane's k only grows, so its cell index only moves forward
-  auto item = [&](int k) {  // k-th item of the flattened neighbourhood
-    while (s_off[warp][cur_d + 1] <= k) ++cur_d;
-    return c.cell_items[s_start[warp][cur_d] + (k - s_off[warp][cur_d])];
+  const int4* __restrict__ attr = c.cell_attr;
+  const double2* __restrict__ sph = reinterpret_cast<const double2*>(c.cell_sph);
+  const long long cap = c.cand_cap;
+  int broad = 0, nbuf = 0, cur_d = 0;  // a lane's k only grows: its cell index only moves forward
+  auto flush = [&]() {  // rare: the survivor buffer is full — reserve its slots with its own atomic
+    int base = 0;
+    if (lane == 0) base = atomicAdd(cand_total, nbuf);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int q = lane; q < nbuf; q += 32)
+      if (base + q < cap) {
+        out_i[base + q] = i;
+        out_j[base + q] = s_buf[warp][q];
+      }
+    __syncwarp();
+    nbuf = 0;
   };
-  auto accept = [&](int j, bool& is_cand) {
-    if (j <= i || !pair_allowed(ri, gi, si, ei, c.pill_rod[j], c.pill_group[j], c.pill_el[j])) return false;
-    is_cand = !prefilter || spheres_touch(c, i, j);  // the exact segment test runs once, in k_narrow_append
-    return true;
+  auto push = [&](bool keep, int j) {  // warp-uniform call: append the lanes' kept j
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (!m) return;
+    if (nbuf + __popc(m) > kPairBuf) flush();
+    if (keep) s_buf[warp][nbuf + __popc(m & ((1u << lane) - 1))] = j;
+    nbuf += __popc(m);
+    __syncwarp();
   };
-  int broad = 0, ncand = 0;
   if (live)
-    for (int k = lane; k < total; k += 32) {
-      bool cand = false;
-      if (accept(item(k), cand)) {
-        ++broad;
-        ncand += cand;
+    for (int k0 = 0; k0 < total; k0 += 32 * kPairUnroll) {
+      int4 at[kPairUnroll];
+      double2 s01[kPairUnroll], s23[kPairUnroll];
+#pragma unroll
+      for (int u = 0; u < kPairUnroll; ++u) {
+        const int k = k0 + u * 32 + lane;
+        at[u].x = -1;
+        if (k < total) {
+          while (s_off[warp][cur_d + 1] <= k) ++cur_d;
+          const int pos = s_start[warp][cur_d] + (k - s_off[warp][cur_d]);
+          at[u] = attr[pos];
+          s01[u] = sph[2 * pos];
+          s23[u] = sph[2 * pos + 1];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kPairUnroll; ++u) {
+        const int j = at[u].x;
+        bool cand = false;
+        if (j > i && pair_allowed(ri, gi, si, ei, at[u].y, at[u].z, at[u].w >> 1)) {
+          ++broad;
+          cand = true;
+          if (prefilter) {  // spheres_touch on the cell-sorted copies
+            const double dx = xi - s01[u].x, dy = yi - s01[u].y, dz = zi - s23[u].x;
+            const double rs = (Ri + s23[u].y) * (1.0 + 1e-9) + 1e-12;
+            cand = dx * dx + dy * dy + dz * dz <= rs * rs;
+          }
+        }
+        push(cand, j);
       }
     }
-  for (int o = 16; o > 0; o >>= 1) {
-    broad += __shfl_down_sync(0xffffffffu, broad, o);
-    ncand += __shfl_down_sync(0xffffffffu, ncand, o);
+  for (int o = 16; o > 0; o >>= 1) broad += __shfl_down_sync(0xffffffffu, broad, o);
+  if (lane == 0) {
+    s_cnt[warp] = nbuf;
+    s_broad[warp] = broad;
+    if (broad && c.pill_scene) atomicAdd(&c.scene_acc[scene].broad_pairs, broad);
   }
-  if (lane == 0) s_cnt[warp] = ncand;
   __syncthreads();
   if (threadIdx.x == 0) {
-    int sum = 0;
+    int sum = 0, bsum = 0;
     for (int w = 0; w < kPairWarps; ++w) {
       const int v = s_cnt[w];
       s_cnt[w] = sum;
       sum += v;
+      bsum += s_broad[w];
     }
     s_base = sum ? atomicAdd(cand_total, sum) : 0;
+    if (bsum) atomicAdd(broad_total, bsum);
   }
   __syncthreads();
-  if (lane == 0 && broad) {
-    atomicAdd(broad_total, broad);
-    if (c.pill_scene) atomicAdd(&c.scene_acc[scene].broad_pairs, broad);
-  }
-  if (!live) return;
-  cur_d = 0;  // second pass restarts at k = lane
-  long long pos = static_cast<long long>(s_base) + s_cnt[warp];
-  for (int k0 = 0; k0 < total; k0 += 32) {
-    const int k = k0 + lane;
-    bool cand = false;
-    int j = -1;
-    if (k < total) {
-      j = item(k);
-      if (!accept(j, cand)) cand = false;
+  const long long base = static_cast<long long>(s_base) + s_cnt[warp];
+  for (int q = lane; q < nbuf; q += 32)
+    if (base + q < cap) {
+      out_i[base + q] = i;
+      out_j[base + q] = s_buf[warp][q];
     }
-    const unsigned m = __ballot_sync(0xffffffffu, cand);
-    if (cand) {
-      const long long p = pos + __popc(m & ((1u << lane) - 1));
-      if (p < c.cand_cap) {
-        c.cand_i[p] = i;
-        c.cand_j[p] = j;
-      }
-    }
-    pos += __popc(m);
-  }
 }
 
 // One WARP per non-empty grid cell (table slot). Lanes 0..26 probe the 27 cells of its 3x3x3
@@ -637,31 +704,118 @@ __global__ void k_seg_filter(Collide c) {
 }
 
 // Narrow phase over the unordered candidates; penetrating pairs are appended (warp-aggregated)
-// to the raw contact list.
-__global__ void k_narrow_append(Collide c, int split_warm) {
+// to the raw contact list. Four lanes per candidate: each step of the dichotomous search
+// evaluates x1 and x2 on two lanes at once (a pair_distance is a ~1k-cycle dependent FP64 chain
+// of two square roots and a division), the start value and the final lo / hi / warm candidates
+// run side by side, and the fourth lane does the exact segment test and the warm-start binary
+// search while the first step runs. Every evaluation is the reference's, on the same inputs,
+// and the comparisons happen in the reference's order: the result is bit-identical to deepest().
+// raw_idx >= 0 (k_pairs_warp's path): the candidates are the first scalars[raw_idx] (unclamped)
+// sphere-touching pairs in cand_i/cand_j; the count is clamped here (k_clamp_raw's job on the
+// other path) and each pair first passes k_seg_filter's exact segment test.
+__global__ void k_narrow_append(Collide c, int split_warm, int raw_idx) {
   pdl_wait();
   pdl_trigger();
-  const int n = c.scalars[SC_NCAND2];
+  int n = c.scalars[SC_NCAND2];
+  const int* ci = c.cand2_i;
+  const int* cj = c.cand2_j;
+  if (raw_idx >= 0) {
+    const int t = c.scalars[raw_idx];
+    n = t > c.cand_cap ? static_cast<int>(c.cand_cap) : t;
+    if (t > c.cand_cap && blockIdx.x == 0 && threadIdx.x == 0) atomicExch(&c.scalars[SC_OVF], 1);
+    ci = c.cand_i;
+    cj = c.cand_j;
+  }
   const int nrr = c.scalars[SC_NRR_PREV], nrk = c.scalars[SC_NRK_PREV];
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, r = lane & 3, gb = lane & ~3;
+  const double delta = 1e-6;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-  for (long long q0 = blockIdx.x * static_cast<long long>(blockDim.x); q0 < n; q0 += stride) {
-    const long long q = q0 + threadIdx.x;
+  for (long long t0 = blockIdx.x * static_cast<long long>(blockDim.x); (t0 >> 2) < n; t0 += stride) {
+    const long long q = (t0 + threadIdx.x) >> 2;  // t0 is CTA-uniform: whole warps iterate together
+    const bool live = q < n;
     int i = 0, j = 0;
-    double al = 0, be = 0, d = 1.0;
-    if (q < n) {
-      i = c.cand2_i[q];
-      j = c.cand2_j[q];
-      const unsigned long long key = pair_key(c.pill_id[i], c.pill_id[j]);
-      double warm;
-      const int scene = c.pill_scene ? c.pill_scene[i] : 0;
-      if (!split_warm || (c.pill_rod[i] >= 0 && c.pill_rod[j] >= 0))
-        warm = warm_lookup(c.warm_rr_key, c.warm_rr_scene, c.warm_rr_alpha, nrr, scene, key);
-      else
-        warm = warm_lookup(c.warm_rk_key, c.warm_rk_scene, c.warm_rk_alpha, nrk, scene, key);
-      deepest(load_pill(c.pill, c.P, i), load_pill(c.pill, c.P, j), c.iters_dich, warm, al, be, d);
+    if (live) {
+      i = ci[q];
+      j = cj[q];
     }
-    const bool hit = q < n && d < 0.0;
+    // phase A: lanes 0 / 1 evaluate the first iteration's x1 / x2, lane 2 the start value at 0.5
+    // (none depends on another); lane 3 runs the exact segment test and the warm-start lookup
+    bool keep = false, swapped = false;
+    double warm = -1.0, f = 0.0, b = 0.0;
+    PillV pa{};
+    PillPrep pb{};
+    if (live) {
+      if (r == 3) {
+        keep = raw_idx < 0 || segments_close(c.pill, c.P, i, j);
+        if (keep) {
+          const unsigned long long key = pair_key(c.pill_id[i], c.pill_id[j]);
+          const int scene = c.pill_scene ? c.pill_scene[i] : 0;
+          if (!split_warm || (c.pill_rod[i] >= 0 && c.pill_rod[j] >= 0))
+            warm = warm_lookup(c.warm_rr_key, c.warm_rr_scene, c.warm_rr_alpha, nrr, scene, key);
+          else
+            warm = warm_lookup(c.warm_rk_key, c.warm_rk_scene, c.warm_rk_alpha, nrk, scene, key);
+        }
+      } else {
+        const PillV A = load_pill(c.pill, c.P, i), B = load_pill(c.pill, c.P, j);
+        swapped = pill_less(B, A);
+        pa = swapped ? B : A;
+        pb = prep_pill(swapped ? A : B);
+        const double mid = 0.5 * (0.0 + 1.0);
+        f = pair_distance(pa, pb, r == 2 ? 0.5 : (r == 0 ? mid - delta : mid + delta), b);
+      }
+    }
+    keep = __shfl_sync(0xffffffffu, static_cast<int>(keep), gb + 3) != 0;
+    warm = __shfl_sync(0xffffffffu, warm, gb + 3);
+    // the dichotomous search (deepest_penetration, collision.cpp:78-135): every lane of the group
+    // keeps the same state from the shuffled evaluations; lanes 0 / 1 evaluate x1 / x2
+    double best = __shfl_sync(0xffffffffu, f, gb + 2), best_b = __shfl_sync(0xffffffffu, b, gb + 2);
+    double best_a = 0.5, lo = 0.0, hi = 1.0;
+    for (int it = 0; it < c.iters_dich; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      const double x1 = mid - delta, x2 = mid + delta;
+      if (it > 0 && live && r < 2) f = pair_distance(pa, pb, r == 0 ? x1 : x2, b);
+      const double f1 = __shfl_sync(0xffffffffu, f, gb), b1 = __shfl_sync(0xffffffffu, b, gb);
+      const double f2 = __shfl_sync(0xffffffffu, f, gb + 1), b2 = __shfl_sync(0xffffffffu, b, gb + 1);
+      if (f1 < best) {
+        best = f1;
+        best_a = x1;
+        best_b = b1;
+      }
+      if (f2 < best) {
+        best = f2;
+        best_a = x2;
+        best_b = b2;
+      }
+      if (f1 <= f2) hi = x2;
+      else lo = x1;
+    }
+    // final candidates lo, hi, warm on lanes 0, 1, 2; compared in that order on lane 0
+    if (swapped && warm >= 0.0) warm = -1.0;
+    const double cand = r == 0 ? lo : (r == 1 ? hi : warm);
+    bool valid = false;
+    double fc = 0.0, bc = 0.0;
+    if (live && keep && r < 3 && !(cand < 0.0 || cand > 1.0)) {
+      valid = true;
+      fc = pair_distance(pa, pb, cand, bc);
+    }
+    double al = 0, be = 0, d = 1.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const bool vk = __shfl_sync(0xffffffffu, static_cast<int>(valid), gb + k) != 0;
+      const double ck = __shfl_sync(0xffffffffu, cand, gb + k);
+      const double fk = __shfl_sync(0xffffffffu, fc, gb + k), bk = __shfl_sync(0xffffffffu, bc, gb + k);
+      if (vk && fk < best) {
+        best = fk;
+        best_a = ck;
+        best_b = bk;
+      }
+    }
+    if (keep) {
+      d = best;
+      al = swapped ? best_b : best_a;
+      be = swapped ? best_a : best_b;
+    }
+    const bool hit = live && r == 0 && d < 0.0;
     const unsigned mask = __ballot_sync(0xffffffffu, hit);
     int base = 0;
     if (lane == 0 && mask) base = atomicAdd(&c.scalars[SC_NCT_RAW], __popc(mask));
@@ -699,11 +853,15 @@ __global__ void k_ct_scatter(Collide c) {
     c.ct_beta[pos] = c.raw_ab[c.contact_cap + k];
   }
 }
+__device__ void sort_pill_contacts(const Collide& c, int i);
 __global__ void k_ct_sort(Collide c) {
   pdl_wait();
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= c.P) return;
+  if (i < c.P) sort_pill_contacts(c, i);
+}
+// insertion sort of pill i's contacts by j (they are few)
+__device__ void sort_pill_contacts(const Collide& c, int i) {
   const int s0 = c.ct_off[i], s1 = c.ct_off[i + 1];
   for (int a = s0 + 1; a < s1; ++a) {
     const int kj = c.ct_b[a];
@@ -726,6 +884,128 @@ __global__ void k_clamp_raw(int* scalars, int raw, int out, long long cap, int o
   const int t = scalars[raw];
   if (t > cap) atomicExch(&scalars[SC_OVF], ovf_code);
   scalars[out] = t > cap ? static_cast<int>(cap) : t;
+}
+
+// (i, j) ordering of the raw contacts in ONE CTA (small worlds: one launch instead of five).
+// Up to `smem_cap` contacts the unique keys (i, j) + raw index, packed in 64 bits, go to shared
+// memory: up to 1024 each key's rank is counted directly (one thread per key), beyond that a
+// bitonic sort (padded to the next power of two) runs over just the warps it needs. More contacts: the counting sort of
+// the multi-launch path (count per i, scan, scatter, per-i insertion sort) run by this CTA in
+// global memory — slow but correct; the host then switches the next recording to the
+// multi-launch path. Either way the output is the same total (i, j) order.
+constexpr int kOrderThreads = 1024;
+__device__ __forceinline__ int block_excl_1024(int v, int* total, int* ws) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  if (lane == 31) ws[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int y = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += t;
+    }
+    ws[lane] = y;
+  }
+  __syncthreads();
+  const int r = (wid ? ws[wid - 1] : 0) + x - v;
+  *total = ws[31];
+  __syncthreads();
+  return r;
+}
+__global__ void __launch_bounds__(kOrderThreads) k_ct_order(Collide c, int smem_cap) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ unsigned long long okey[];  // smem_cap packed keys
+  __shared__ int ws[32];
+  const int n = c.scalars[SC_NCT];
+  const int tid = threadIdx.x;
+  if (n == 0) return;
+  if (n <= smem_cap && c.P <= 65536) {
+    // packed key (i << 48 | j << 32 | raw index): pill ids < 2^16 here, so sorting the packed
+    // words sorts by (i, j) and carries the raw index along
+    const bool rank = n <= kOrderThreads;
+    int m = 2;
+    while (m < n) m <<= 1;
+    // only the warps the sort needs take part (named barrier over `act` threads)
+    const int act = rank ? (n + 31) & ~31 : min(kOrderThreads, m >> 1);
+    if (tid >= act) return;
+    auto bar = [act]() { asm volatile("bar.sync 1, %0;" ::"r"(act) : "memory"); };
+    const int fill = rank ? (n + 1) & ~1 : m;
+    for (int k = tid; k < fill; k += act)
+      okey[k] = k < n ? (static_cast<unsigned long long>(c.raw_i[k]) << 48) |
+                            (static_cast<unsigned long long>(c.raw_j[k]) << 32) | static_cast<unsigned>(k)
+                      : ~0ull;
+    bar();
+    auto emit = [&](int r, unsigned long long key) {
+      const int q = static_cast<int>(key & 0xffffffffu);
+      c.ct_a[r] = static_cast<int>(key >> 48);
+      c.ct_b[r] = static_cast<int>((key >> 32) & 0xffffu);
+      c.ct_alpha[r] = c.raw_ab[q];
+      c.ct_beta[r] = c.raw_ab[c.contact_cap + q];
+    };
+    if (rank) {  // one key per thread: its rank among the (unique) keys, broadcast pair reads
+      if (tid >= n) return;
+      const unsigned long long key = okey[tid];
+      const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(okey);
+      int r = 0;
+#pragma unroll 4
+      for (int q = 0; q < fill / 2; ++q) {
+        const ulonglong2 v = k2[q];
+        r += (v.x < key) + (v.y < key);
+      }
+      emit(r, key);
+      return;
+    }
+    for (int size = 2; size <= m; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int t = tid; t < (m >> 1); t += act) {
+          const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+          const unsigned long long x = okey[lo], y = okey[hi];
+          if ((x > y) == ((lo & size) == 0)) {
+            okey[lo] = y;
+            okey[hi] = x;
+          }
+        }
+        bar();
+      }
+    for (int k = tid; k < n; k += act) emit(k, okey[k]);
+    return;
+  }
+  const int P = c.P;
+  for (int k = tid; k <= P; k += kOrderThreads) {
+    c.ct_cnt[k] = 0;
+    c.ct_cur[k] = 0;
+  }
+  __syncthreads();
+  for (int k = tid; k < n; k += kOrderThreads) atomicAdd(&c.ct_cnt[c.raw_i[k]], 1);
+  __syncthreads();
+  int carry = 0;
+  for (int b = 0; b < P; b += kOrderThreads) {
+    const int v = b + tid < P ? c.ct_cnt[b + tid] : 0;
+    int total;
+    const int ex = block_excl_1024(v, &total, ws);
+    if (b + tid < P) c.ct_off[b + tid] = carry + ex;
+    carry += total;
+  }
+  if (tid == 0) c.ct_off[P] = carry;
+  __syncthreads();
+  for (int k = tid; k < n; k += kOrderThreads) {
+    const int i = c.raw_i[k];
+    const int pos = c.ct_off[i] + atomicAdd(&c.ct_cur[i], 1);
+    c.ct_a[pos] = i;
+    c.ct_b[pos] = c.raw_j[k];
+    c.ct_alpha[pos] = c.raw_ab[k];
+    c.ct_beta[pos] = c.raw_ab[c.contact_cap + k];
+  }
+  __syncthreads();
+  for (int i = tid; i < P; i += kOrderThreads) sort_pill_contacts(c, i);
 }
 
 // Narrow phase over the candidate list (find_contacts, collision.cpp:261-271).
@@ -910,6 +1190,14 @@ int grid_for(long long n) {
   const long long b = (n + kThreads - 1) / kThreads;
   return static_cast<int>(b < 1 ? 1 : (b > 148 * 16 ? 148 * 16 : b));
 }
+// The narrow phase is FP64-issue-bound per SM (≈ 6k FP64-heavy instructions per candidate
+// warp): two-warp CTAs, so the live candidates (a prefix of the grid) spread over all SMs
+// instead of queueing on the few SMs that 256-thread CTAs would put them on.
+constexpr int kNarrowThreads = 64;
+int narrow_grid(long long cand_cap) {
+  const long long b = (4 * cand_cap + kNarrowThreads - 1) / kNarrowThreads;
+  return static_cast<int>(b < 1 ? 1 : (b > 148 * 32 ? 148 * 32 : b));
+}
 
 }  // namespace
 
@@ -923,7 +1211,19 @@ void launch_narrow_only(Collide& c, int split_warm, int store_d, cudaStream_t st
 }
 
 // Puts the first scalars[SC_NCT] raw (i, j, alpha, beta) records into (i, j) order in ct_*.
+int order_cap_for(int P) {
+  const char* env = std::getenv("VROD_CT_ORDER_CAP");  // tests: 0 forces the single-CTA fallback, -1 the multi-launch path
+  if (env) return std::atoi(env);
+  return P < kCellPathMinPills ? 4096 : -1;
+}
+
 void launch_order_contacts(Collide& c, cudaStream_t st) {
+  if (c.order_smem_cap >= 0) {  // one CTA (small worlds)
+    const std::size_t smem = 8ull * (c.order_smem_cap + 2);
+    cudaFuncSetAttribute(k_ct_order, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    launch_kernel(k_ct_order, 1, kOrderThreads, smem, st, g_pdl, c, c.order_smem_cap);
+    return;
+  }
   const int g = grid_for(c.contact_cap);
   FillList f;
   f.add(c.ct_cnt, c.P + 1, 0);
@@ -954,6 +1254,7 @@ void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
   f.add(c.scalars + SC_NCT_RAW, 1, 0);
   if (do_narrow) f.add(c.scalars + SC_NCAND2, 1, 0);  // k_seg_filter's counter
   launch_fill(f, st);
+  bool fused_seg = false;
   if (P > 0) {
     launch_kernel(k_bounds, b, kThreads, 0, st, g_pdl, c, substep, err);
     launch_kernel(k_insert, b, kThreads, 0, st, g_pdl, c);
@@ -965,8 +1266,9 @@ void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
     const char* env = std::getenv("VROD_BROAD_CELL_MIN");
     const int cell_min = env ? std::atoi(env) : kCellPathMinPills;
     if (P < cell_min) {  // small worlds: one warp per pill, a single launch
+      fused_seg = do_narrow && prefilter;
       launch_kernel(k_pairs_warp, (P + kPairWarps - 1) / kPairWarps, 32 * kPairWarps, 0, st, g_pdl, c, prefilter,
-                    c.scalars + SC_BROAD, c.scalars + SC_NCAND_RAW);
+                    c.scalars + SC_BROAD, c.scalars + SC_NCAND_RAW, c.cand_i, c.cand_j);
     } else {  // large worlds: one warp per non-empty cell, neighbourhood loads shared by its pills
       scan_exclusive(c.rep_flag, c.rep_pos, P, nullptr, c.scan_tmp, c.scan_parts, st);
       launch_kernel(k_cell_list, b, kThreads, 0, st, g_pdl, c);
@@ -974,10 +1276,15 @@ void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
                     g_pdl, c, prefilter, c.scalars + SC_BROAD, c.scalars + SC_NCAND_RAW);
     }
   }
-  launch_kernel(k_clamp_raw, 1, 1, 0, st, g_pdl, c.scalars, SC_NCAND_RAW, SC_NCAND, c.cand_cap, 1);
-  if (!do_narrow) return;
-  launch_kernel(k_seg_filter, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c);
-  launch_kernel(k_narrow_append, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c, split_warm);
+  if (fused_seg) {  // k_narrow_append clamps the count and runs the exact segment test itself
+    launch_kernel(k_narrow_append, narrow_grid(c.cand_cap), kNarrowThreads, 0, st, g_pdl, c, split_warm,
+                  int(SC_NCAND_RAW));
+  } else {
+    launch_kernel(k_clamp_raw, 1, 1, 0, st, g_pdl, c.scalars, SC_NCAND_RAW, SC_NCAND, c.cand_cap, 1);
+    if (!do_narrow) return;
+    launch_kernel(k_seg_filter, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c);
+    launch_kernel(k_narrow_append, narrow_grid(c.cand_cap), kNarrowThreads, 0, st, g_pdl, c, split_warm, -1);
+  }
   launch_kernel(k_clamp_raw, 1, 1, 0, st, g_pdl, c.scalars, SC_NCT_RAW, SC_NCT, c.contact_cap, 2);
   launch_order_contacts(c, st);
 }

@@ -35,6 +35,9 @@ struct Collide {
   int n_planes = 0;
   int n_pins = 0;
   int iters_dich = 10;
+  // contact ordering: >= 0 runs k_ct_order (one CTA; bitonic sort in shared memory of up to this
+  // many contacts, a single-CTA counting sort beyond); -1 the multi-launch counting sort
+  int order_smem_cap = -1;
   int scan_parts = 0;
 
   // pills (SoA): c0xyz c1xyz r0 r1 = 8 fields x P
@@ -52,6 +55,8 @@ struct Collide {
   int* cell_start = nullptr;     // T+1
   int* cell_cursor = nullptr;    // T
   int* cell_items = nullptr;     // P
+  int4* cell_attr = nullptr;     // P, cell-sorted: (pill, rod, group, 2 * element + self)
+  double* cell_sph = nullptr;    // 4 x P, cell-sorted AoS bounding spheres (cx cy cz R)
   int* pill_cell = nullptr;      // P
   int* rep_flag = nullptr;       // P+1: pill is its cell's representative
   int* rep_pos = nullptr;        // P+1: exclusive scan of rep_flag ([P] = cell count)
@@ -264,6 +269,7 @@ void launch_collide(const World& w, Collide& c, const double* anim, const AnimLa
 void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int prefilter, int do_narrow,
                          int split_warm, int store_d, cudaStream_t st);
 void launch_narrow_only(Collide& c, int split_warm, int store_d, cudaStream_t st);
+int order_cap_for(int P);  // Collide::order_smem_cap for a world of P pills
 void launch_broad_ordered(Collide& c, unsigned long long* err, cudaStream_t st);
 void launch_halfplanes(const World& w, Collide& c, cudaStream_t st);
 // standalone fine-grained entry points (vrod_pill_project & co), on device arrays

@@ -97,29 +97,32 @@ __global__ void k_add(int* __restrict__ out, long long n_cap, const int* n_dev, 
   }
 }
 
-// Small scans (n_cap <= kSmallScan): one CTA does it all — a chunk of consecutive elements per
-// thread, a block scan of the chunk totals — one launch instead of three.
+// Small scans (n_cap <= kSmallScan): one CTA does it all, one launch instead of three. The live
+// length n is staged through shared memory with coalesced loads (one pad word per 32 keeps the
+// per-thread chunk walks conflict-free), each thread scans a contiguous chunk of ceil(n / 512),
+// a block scan of the chunk totals gives the offsets, and the result leaves coalesced.
 constexpr long long kSmallScan = 8 * kTile;  // 32768
+__host__ __device__ constexpr long long small_pad(long long i) { return i + (i >> 5); }
 __global__ void k_scan_small(const int* __restrict__ in, int* __restrict__ out, long long n_cap, const int* n_dev) {
   pdl_wait();
   pdl_trigger();
-  const long long n = n_dev ? static_cast<long long>(*n_dev) : n_cap;
-  constexpr int kChunk = kSmallScan / kThreads;  // 64 consecutive elements per thread
-  const long long b = static_cast<long long>(threadIdx.x) * kChunk;
-  int vals[kChunk];
-#pragma unroll
-  for (int k = 0; k < kChunk; ++k) vals[k] = b + k < n ? in[b + k] : 0;  // all loads in flight
+  extern __shared__ int sm[];
+  const int n = static_cast<int>(n_dev ? static_cast<long long>(*n_dev) : n_cap);
+  for (int i = threadIdx.x; i < n; i += kThreads) sm[small_pad(i)] = in[i];
+  __syncthreads();
+  const int ch = (n + kThreads - 1) / kThreads;
+  const int b = threadIdx.x * ch, e = min(b + ch, n);
   int sum = 0;
-#pragma unroll
-  for (int k = 0; k < kChunk; ++k) sum += vals[k];
+  for (int k = b; k < e; ++k) sum += sm[small_pad(k)];
   int total;
   int run = block_excl(sum, &total);
-#pragma unroll
-  for (int k = 0; k < kChunk; ++k)
-    if (b + k < n) {
-      out[b + k] = run;
-      run += vals[k];
-    }
+  for (int k = b; k < e; ++k) {
+    const int v = sm[small_pad(k)];
+    sm[small_pad(k)] = run;
+    run += v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += kThreads) out[i] = sm[small_pad(i)];
   if (threadIdx.x == 0) out[n] = total;
 }
 
@@ -149,7 +152,11 @@ void scan_exclusive(const int* in, int* out, long long n_cap, const int* n_dev, 
                     cudaStream_t st) {
   (void)parts;
   if (n_cap <= kSmallScan) {
-    launch_kernel(k_scan_small, 1, kThreads, 0, st, g_pdl, in, out, n_cap, n_dev);
+    // (host-side, at graph-record time; per device, so set on every call)
+    cudaFuncSetAttribute(k_scan_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(int) * (small_pad(kSmallScan) + 1)));
+    const std::size_t smem = sizeof(int) * static_cast<std::size_t>(small_pad(n_cap) + 1);
+    launch_kernel(k_scan_small, 1, kThreads, smem, st, g_pdl, in, out, n_cap, n_dev);
     return;
   }
   const long long blocks = n_cap / kTile + 1;

@@ -152,6 +152,9 @@ Solver::Solver(const SceneData& scene, const BatchLayout* batch) : scene_(scene)
   c_.cell_start = dalloc<int>(c_.T + 1);
   c_.cell_cursor = dalloc<int>(c_.T);
   c_.cell_items = dalloc<int>(c_.P);
+  c_.order_smem_cap = vdev::order_cap_for(c_.P);
+  c_.cell_attr = dalloc<int4>(std::max(c_.P, 1));
+  c_.cell_sph = dalloc<double>(4ull * std::max(c_.P, 1));
   c_.pill_cell = dalloc<int>(c_.P);
   c_.rep_flag = dalloc<int>(c_.P + 1);
   c_.rep_pos = dalloc<int>(c_.P + 1);
@@ -1005,6 +1008,12 @@ void Solver::finish_step(double h, int substeps, Report* out) {
   for (int s = 0; s < substeps; ++s) time_ = time_ + h;
   last_max_cand_ = h_acc_->max_candidates;
   last_max_ct_ = h_acc_->max_contacts;
+  if (c_.order_smem_cap >= 0 && last_max_ct_ > c_.order_smem_cap && !std::getenv("VROD_CT_ORDER_CAP") && graph_exec_) {
+    // more contacts than the one-CTA sort holds: record the multi-launch ordering from now on
+    c_.order_smem_cap = -1;
+    cudaGraphExecDestroy(graph_exec_);
+    graph_exec_ = nullptr;
+  }
   check_error();
   ++step_index_;
   out->step = step_index_;

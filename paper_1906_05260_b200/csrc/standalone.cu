@@ -2,6 +2,7 @@
 // find_contacts (collision.h:64-95) over host pill arrays. They run the same device functions
 // as the solver's collision stage, so bit-exactness against the oracle on identical pill
 // arrays is tested directly (tests/test_gpu_collision.py).
+#include <cstdlib>
 #include <algorithm>
 #include <stdexcept>
 #include <vector>
@@ -83,6 +84,11 @@ void make_collide(Buf& b, vdev::Collide& c, const vrod_pill* pills, int P, long 
   c.cell_start = b.get<int>(c.T + 1);
   c.cell_cursor = b.get<int>(c.T);
   c.cell_items = b.get<int>(P);
+  // broad_phase lists every allowed pair (often far more than one CTA sorts well): multi-launch
+  // ordering unless a test forces a path
+  c.order_smem_cap = std::getenv("VROD_CT_ORDER_CAP") ? vdev::order_cap_for(P) : -1;
+  c.cell_attr = b.get<int4>(std::max(P, 1));
+  c.cell_sph = b.get<double>(4ull * std::max(P, 1));
   c.pill_cell = b.get<int>(P);
   c.rep_flag = b.get<int>(P + 1);
   c.rep_pos = b.get<int>(P + 1);

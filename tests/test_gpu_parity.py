@@ -139,6 +139,35 @@ def test_cell_broad_phase_path(gpu, oracle, name, monkeypatch):
                 np.testing.assert_array_equal(cg[k], co[k], err_msg=k)
 
 
+@pytest.mark.parametrize("cap", ["-1", "0", "64", "16384"])
+def test_contact_ordering_paths(gpu, oracle, cap, monkeypatch):
+    """Contacts are put in (i, j) order by one CTA in small worlds (bitonic sort in shared memory
+    up to VROD_CT_ORDER_CAP contacts, a single-CTA counting sort beyond it) and by the
+    multi-launch counting sort otherwise (-1). Every path must give the oracle's order."""
+    monkeypatch.setenv("VROD_CT_ORDER_CAP", cap)
+    rng = np.random.default_rng(77)
+    pills = random_pills(rng, 2000, spread=3.0, rmax=0.25)
+    pg = broad_phase(gpu, pills)
+    np.testing.assert_array_equal(pg, broad_phase(oracle, pills))
+    assert len(pg) > 64
+    keys = rng.integers(0, 2**40, 100).astype(np.uint64)
+    wa = rng.uniform(0, 1, 100)
+    cg, co = find_contacts(gpu, pills, pg, 10, keys, wa), find_contacts(oracle, pills, pg, 10, keys, wa)
+    for k in cg:
+        np.testing.assert_array_equal(cg[k], co[k], err_msg=k)
+    for name in ("pile", "mini_forest"):
+        scene = SCENES[name](oracle)
+        g, o = SolverHandle(gpu, scene), SolverHandle(oracle, scene)
+        for _ in range(3):
+            assert_reports_equal(g.step(), o.step())
+            cg, co = g.contacts(), o.contacts()
+            for k in cg:
+                np.testing.assert_array_equal(cg[k], co[k], err_msg=f"{name}: {k}")
+        sg, so = g.state(), o.state()
+        for k in sg:
+            np.testing.assert_array_equal(sg[k], so[k], err_msg=f"{name}: {k}")
+
+
 def test_broad_phase_edge_cases(gpu, oracle):
     rng = np.random.default_rng(9)
     for n in (0, 1, 2, 3, 50):
