@@ -22,47 +22,48 @@ __device__ __forceinline__ double shape_wsum(double v) {
 
 // General route of the rotation increment (half angle >= 1e-2: rare once warm-started); kept out
 // of line so sincos's range reduction does not bloat the hot loop's code.
-static __device__ __noinline__ void rotation_increment_general(double a2, double& k, double& c) {
+static __device__ __noinline__ double2 rotation_increment_general(double a2) {
   const double angle = sqrt(a2);
-  double s;
-  sincos(0.5 * angle, &s, &c);
-  k = s / angle;
+  double sn, cs;
+  sincos(0.5 * angle, &sn, &cs);
+  return make_double2(sn / angle, cs);  // (k, c), returned in registers
 }
 
-// Reciprocal for the rotation chain: MUFU seed + two Newton steps (relative error ~1 ulp).
-__device__ __forceinline__ double rcp_fast(double x) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  return fma(y, e, y);
+// 1 / |q| for a quaternion that is unit up to rounding: 1/sqrt(1+e) = 1 - e/2 + 3/8 e^2 (exact to
+// 1e-30 for |e| < 1e-6; rsqrt otherwise).
+__device__ __forceinline__ vm::Q4 qnormalized_fast(const vm::Q4& p) {
+  const double e = fma(p.w, p.w, p.x * p.x) + fma(p.y, p.y, p.z * p.z) - 1.0;
+  double r = fma(e, fma(e, 0.375, -0.5), 1.0);
+  if (!(fabs(e) < 1e-6)) r = e > -1.0 ? rsqrt(e + 1.0) : 1.0;
+  return vm::Q4{p.w * r, p.x * r, p.y * r, p.z * r};
 }
 
 // extract_rotation, bundling.cpp:50-67: the same iteration (omega = sum R_a x B_a / (|sum
 // R_a . B_a| + 1e-9), q <- AngleAxis(|omega|, omega^) q, normalize, stop at |omega| < 1e-9).
 // The loop is one serial dependency chain (~10 iterations warm-started at C3, up to ~20), so it
-// is written for latency (shape matching is tolerance-pinned): FMA trees, a Newton
-// reciprocal, and for half angles below 1e-2 the increment [cos(a/2), sin(a/2)/a * omega] from
-// its Taylor series in a^2 (truncation < 1e-20 relative); larger steps take the general route.
-// The product of two unit quaternions has |p|^2 = 1 + O(1e-15), so the renormalisation uses
-// 1/sqrt(n) = 1 - (n-1)/2 + 3/8 (n-1)^2 (exact to 1e-30 there; rsqrt otherwise).
+// is written for latency (shape matching is tolerance-pinned); per iteration the
+// critical path is ~18 dependent FP64 operations + one MUFU (tools/ubench/rotbench.cu):
+//  - R from q with FMA trees (depth 3); omega and the trace with FMA trees;
+//  - a Newton reciprocal with one cubic step;
+//  - the increment [cos(a/2), sin(a/2)/a * omega] from its Taylor series in x = (a/2)^2,
+//    Estrin-evaluated (truncation < 1e-21 relative for x < 1e-4; larger steps take sincos);
+//  - [c, k/d * omega] q = c q + (k/d) ([0, omega] q), the second product formed off the path;
+//  - the stop test and the rare branches issued after the update, so nothing waits on them;
+//  - the product of unit quaternions is unit to O(1e-16), so q is renormalised once at the end
+//    (the 13-odd iterations drift |q| by ~1e-15, far below the 1e-9 stopping tolerance).
 __device__ __forceinline__ vm::Q4 extract_rotation(const vm::M3& B, const vm::Q4& guess, int* iters = nullptr,
                                                    int max_iterations = 100, double tol2 = 1e-18) {
   using namespace vm;
-  Q4 q = qnormalized(guess);
+  Q4 q = qnormalized_fast(guess);
   int it = 0;
 #pragma unroll 1
   for (; it < max_iterations; ++it) {
     // R = toRotationMatrix(q)
     const double tx = 2.0 * q.x, ty = 2.0 * q.y, tz = 2.0 * q.z;
-    const double twx = tx * q.w, twy = ty * q.w, twz = tz * q.w;
-    const double txx = tx * q.x, txy = ty * q.x, txz = tz * q.x;
-    const double tyy = ty * q.y, tyz = tz * q.y, tzz = tz * q.z;
-    const double R[3][3] = {{1.0 - (tyy + tzz), txy - twz, txz + twy},
-                            {txy + twz, 1.0 - (txx + tzz), tyz - twx},
-                            {txz - twy, tyz + twx, 1.0 - (txx + tyy)}};
-    // w = sum_a col(R, a) x col(B, a); d = sum_a col(R, a) . col(B, a)
+    const double R[3][3] = {{fma(-ty, q.y, fma(-tz, q.z, 1.0)), fma(tx, q.y, -tz * q.w), fma(tx, q.z, ty * q.w)},
+                            {fma(tx, q.y, tz * q.w), fma(-tx, q.x, fma(-tz, q.z, 1.0)), fma(ty, q.z, -tx * q.w)},
+                            {fma(tx, q.z, -ty * q.w), fma(ty, q.z, tx * q.w), fma(-tx, q.x, fma(-ty, q.y, 1.0))}};
+    // omega = sum_a col(R, a) x col(B, a); d = sum_a col(R, a) . col(B, a)
     double wx[3], wy[3], wz[3], dd[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -74,33 +75,39 @@ __device__ __forceinline__ vm::Q4 extract_rotation(const vm::M3& B, const vm::Q4
       dd[a] = fma(r0, b0, fma(r1, b1, r2 * b2));
     }
     const double ox = (wx[0] + wx[1]) + wx[2], oy = (wy[0] + wy[1]) + wy[2], oz = (wz[0] + wz[1]) + wz[2];
-    const double inv = rcp_fast(fabs((dd[0] + dd[1]) + dd[2]) + 1e-9);
+    const double den = fabs((dd[0] + dd[1]) + dd[2]) + 1e-9;
+    // u = [0, omega] q: off the critical path (needs omega and q only)
+    const double uw = -fma(ox, q.x, fma(oy, q.y, oz * q.z));
+    const double ux = fma(ox, q.w, fma(oy, q.z, -oz * q.y));
+    const double uy = fma(oy, q.w, fma(oz, q.x, -ox * q.z));
+    const double uz = fma(oz, q.w, fma(ox, q.y, -oy * q.x));
     const double w2 = fma(ox, ox, fma(oy, oy, oz * oz));
-    const double a2 = (w2 * inv) * inv;  // |omega|^2
-    if (a2 < tol2) break;  // |omega| < tolerance (1e-9)
-    const double x2 = 0.25 * a2;  // (angle / 2)^2
-    double k, c;  // k = sin(angle/2) / angle, c = cos(angle/2)
-    if (x2 < 1e-4) {
-      k = 0.5 * fma(-x2 * (1.0 / 6), fma(-x2 * (1.0 / 20), fma(-x2 * (1.0 / 42), fma(-x2, 1.0 / 72, 1.0), 1.0), 1.0), 1.0);
-      c = fma(-x2 * 0.5,
-              fma(-x2 * (1.0 / 12), fma(-x2 * (1.0 / 30), fma(-x2 * (1.0 / 56), fma(-x2, 1.0 / 90, 1.0), 1.0), 1.0), 1.0),
-              1.0);
-    } else {
-      rotation_increment_general(a2, k, c);
+    const double w2q = 0.25 * w2;
+    // inv = 1 / den: MUFU seed (~2^-23) and one cubic Newton step (error ~2^-69)
+    double inv;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(den));
+    {
+      const double e = fma(-den, inv, 1.0);
+      inv = fma(inv, fma(e, e, e), inv);
     }
+    const double x2 = (w2q * inv) * inv;  // (angle / 2)^2
+    const double x4 = x2 * x2;
+    // k = sin(angle/2) / angle, c = cos(angle/2)
+    const double k = fma(x4, fma(x2, -1.0 / 10080, 1.0 / 240), fma(x2, -1.0 / 12, 0.5));
+    const double c = fma(x4, fma(x2, -1.0 / 720, 1.0 / 24), fma(x2, -0.5, 1.0));
     const double ki = k * inv;
-    const double vx = ki * ox, vy = ki * oy, vz = ki * oz;
-    // p = [c, v] * q (Hamilton product)
-    const double pw = fma(c, q.w, -fma(vx, q.x, fma(vy, q.y, vz * q.z)));
-    const double px = fma(c, q.x, fma(vx, q.w, fma(vy, q.z, -vz * q.y)));
-    const double py = fma(c, q.y, fma(vy, q.w, fma(vz, q.x, -vx * q.z)));
-    const double pz = fma(c, q.z, fma(vz, q.w, fma(vx, q.y, -vy * q.x)));
-    const double e = fma(pw, pw, fma(px, px, fma(py, py, pz * pz))) - 1.0;
-    const double r = fabs(e) < 1e-6 ? fma(e, fma(e, 0.375, -0.5), 1.0) : rsqrt(e + 1.0);
-    q = Q4{pw * r, px * r, py * r, pz * r};
+    Q4 p{fma(ki, uw, c * q.w), fma(ki, ux, c * q.x), fma(ki, uy, c * q.y), fma(ki, uz, c * q.z)};
+    const bool stop = (w2 * inv) * inv < tol2;  // |omega| < tolerance (1e-9): keep q
+    if (stop || !(x2 < 1e-4)) {  // one rare branch, at the end of the iteration
+      if (stop) break;
+      const double2 kc = rotation_increment_general(4.0 * x2);
+      const double kg = kc.x * inv;
+      p = Q4{fma(kg, uw, kc.y * q.w), fma(kg, ux, kc.y * q.x), fma(kg, uy, kc.y * q.y), fma(kg, uz, kc.y * q.z)};
+    }
+    q = p;
   }
   if (iters) *iters = it;
-  return q;
+  return qnormalized_fast(q);
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
