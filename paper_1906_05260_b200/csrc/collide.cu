@@ -704,7 +704,8 @@ __global__ void k_seg_filter(Collide c) {
 }
 
 // Narrow phase over the unordered candidates; penetrating pairs are appended (warp-aggregated)
-// to the raw contact list. Four lanes per candidate: each step of the dichotomous search
+// to the raw contact list. Large worlds (kQuad = false, throughput-bound): one thread per
+// candidate. Small worlds (latency-bound): four lanes per candidate: each step of the dichotomous search
 // evaluates x1 and x2 on two lanes at once (a pair_distance is a ~1k-cycle dependent FP64 chain
 // of two square roots and a division), the start value and the final lo / hi / warm candidates
 // run side by side, and the fourth lane does the exact segment test and the warm-start binary
@@ -713,6 +714,7 @@ __global__ void k_seg_filter(Collide c) {
 // raw_idx >= 0 (k_pairs_warp's path): the candidates are the first scalars[raw_idx] (unclamped)
 // sphere-touching pairs in cand_i/cand_j; the count is clamped here (k_clamp_raw's job on the
 // other path) and each pair first passes k_seg_filter's exact segment test.
+template <bool kQuad>
 __global__ void k_narrow_append(Collide c, int split_warm, int raw_idx) {
   pdl_wait();
   pdl_trigger();
@@ -727,6 +729,44 @@ __global__ void k_narrow_append(Collide c, int split_warm, int raw_idx) {
     cj = c.cand_j;
   }
   const int nrr = c.scalars[SC_NRR_PREV], nrk = c.scalars[SC_NRK_PREV];
+  if (!kQuad) {  // large worlds (throughput-bound): one thread per candidate, deepest() as is
+    const int lane = threadIdx.x & 31;
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long q0 = blockIdx.x * static_cast<long long>(blockDim.x); q0 < n; q0 += stride) {
+      const long long q = q0 + threadIdx.x;
+      int i = 0, j = 0;
+      double al = 0, be = 0, d = 1.0;
+      if (q < n) {
+        i = ci[q];
+        j = cj[q];
+      }
+      if (q < n && (raw_idx < 0 || segments_close(c.pill, c.P, i, j))) {
+        const unsigned long long key = pair_key(c.pill_id[i], c.pill_id[j]);
+        const int scene = c.pill_scene ? c.pill_scene[i] : 0;
+        double warm;
+        if (!split_warm || (c.pill_rod[i] >= 0 && c.pill_rod[j] >= 0))
+          warm = warm_lookup(c.warm_rr_key, c.warm_rr_scene, c.warm_rr_alpha, nrr, scene, key);
+        else
+          warm = warm_lookup(c.warm_rk_key, c.warm_rk_scene, c.warm_rk_alpha, nrk, scene, key);
+        deepest(load_pill(c.pill, c.P, i), load_pill(c.pill, c.P, j), c.iters_dich, warm, al, be, d);
+      }
+      const bool hit = q < n && d < 0.0;
+      const unsigned mask = __ballot_sync(0xffffffffu, hit);
+      int base = 0;
+      if (lane == 0 && mask) base = atomicAdd(&c.scalars[SC_NCT_RAW], __popc(mask));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (hit) {
+        const long long k = base + __popc(mask & ((1u << lane) - 1));
+        if (k < c.contact_cap) {
+          c.raw_i[k] = i;
+          c.raw_j[k] = j;
+          c.raw_ab[k] = al;
+          c.raw_ab[c.contact_cap + k] = be;
+        }
+      }
+    }
+    return;
+  }
   const int lane = threadIdx.x & 31, r = lane & 3, gb = lane & ~3;
   const double delta = 1e-6;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
@@ -1277,13 +1317,13 @@ void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
     }
   }
   if (fused_seg) {  // k_narrow_append clamps the count and runs the exact segment test itself
-    launch_kernel(k_narrow_append, narrow_grid(c.cand_cap), kNarrowThreads, 0, st, g_pdl, c, split_warm,
+    launch_kernel(k_narrow_append<true>, narrow_grid(c.cand_cap), kNarrowThreads, 0, st, g_pdl, c, split_warm,
                   int(SC_NCAND_RAW));
   } else {
     launch_kernel(k_clamp_raw, 1, 1, 0, st, g_pdl, c.scalars, SC_NCAND_RAW, SC_NCAND, c.cand_cap, 1);
     if (!do_narrow) return;
     launch_kernel(k_seg_filter, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c);
-    launch_kernel(k_narrow_append, narrow_grid(c.cand_cap), kNarrowThreads, 0, st, g_pdl, c, split_warm, -1);
+    launch_kernel(k_narrow_append<false>, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c, split_warm, -1);
   }
   launch_kernel(k_clamp_raw, 1, 1, 0, st, g_pdl, c.scalars, SC_NCT_RAW, SC_NCT, c.contact_cap, 2);
   launch_order_contacts(c, st);
