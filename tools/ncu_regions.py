@@ -39,7 +39,7 @@ hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
 h = rows[hi]
 body = [r for r in rows[hi + 1:] if len(r) > 5 and r[0].startswith("0x")]
 base = int(body[0][0], 16)
-ci = {k: h.index(k) for k in ("Warp Stall Sampling (All Samples)", "stall_no_inst", "stall_wait", "stall_barrier",
+ci = {k: h.index(k) for k in ("Warp Stall Sampling (All Samples)", "stall_no_inst", "stall_wait", "stall_barrier", "L1 Wavefronts Shared", "L1 Wavefronts Shared Excessive",
                               "stall_long_sb", "stall_short_sb", "Instructions Executed")}
 func_starts = {}
 def func_of(loc):
@@ -69,8 +69,8 @@ for r in body:
         agg[key][k] += float(r[i] or 0)
 tot = sum(v["Warp Stall Sampling (All Samples)"] for v in agg.values())
 print(f"{fn[0][:80]}\n{len(body)} SASS lines, {tot:.0f} samples")
-print(f"{'function':48s} {'samples':>8s} {'share':>6s} {'no_inst':>8s} {'wait':>7s} {'barrier':>8s} {'long_sb':>8s} {'instr':>9s}")
+print(f"{'function':48s} {'samples':>8s} {'share':>6s} {'no_inst':>8s} {'wait':>7s} {'barrier':>8s} {'long_sb':>8s} {'instr':>9s} {'smem_wf':>8s} {'smem_excess':>11s}")
 for k, v in sorted(agg.items(), key=lambda x: -x[1]["Warp Stall Sampling (All Samples)"])[:30]:
     s = v["Warp Stall Sampling (All Samples)"]
     print(f"{k[:48]:48s} {s:8.0f} {s / tot:6.1%} {v['stall_no_inst']:8.0f} {v['stall_wait']:7.0f} {v['stall_barrier']:8.0f} "
-          f"{v['stall_long_sb']:8.0f} {v['Instructions Executed']:9.0f}")
+          f"{v['stall_long_sb']:8.0f} {v['Instructions Executed']:9.0f} {v['L1 Wavefronts Shared']:8.0f} {v['L1 Wavefronts Shared Excessive']:11.0f}")
