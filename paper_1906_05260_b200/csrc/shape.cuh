@@ -315,7 +315,8 @@ __device__ __forceinline__ void shape_end(const World& w, const Groups& g, doubl
       xr[0] = make_double2(x.x, x.y);
       xr[1] = make_double2(x.z, sn);
     }
-    const Q4 fr = qnormalized(qmul(qf, Q4{mr[13], mr[14], mr[15], mr[16]}));
+    // product of unit quaternions: unit to O(1e-16), renormalised by the series (tolerance-pinned)
+    const Q4 fr = qnormalized_fast(qmul(qf, Q4{mr[13], mr[14], mr[15], mr[16]}));
     const int e = M.eslot(i);
     X[QW * vp + e] = fr.w;
     X[QX * vp + e] = fr.x;

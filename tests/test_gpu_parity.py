@@ -139,12 +139,17 @@ def test_cell_broad_phase_path(gpu, oracle, name, monkeypatch):
                 np.testing.assert_array_equal(cg[k], co[k], err_msg=k)
 
 
-@pytest.mark.parametrize("cap", ["-1", "0", "64", "16384"])
+@pytest.mark.parametrize("cap", ["-1", "0", "64", "4096", "16384"])
 def test_contact_ordering_paths(gpu, oracle, cap, monkeypatch):
     """Contacts are put in (i, j) order by one CTA in small worlds (bitonic sort in shared memory
     up to VROD_CT_ORDER_CAP contacts, a single-CTA counting sort beyond it) and by the
     multi-launch counting sort otherwise (-1). Every path must give the oracle's order."""
     monkeypatch.setenv("VROD_CT_ORDER_CAP", cap)
+    # 2,383 pairs: the rank path stops at 1,024, so caps >= 4096 take the bitonic sort here
+    small = random_pills(np.random.default_rng(78), 150, spread=3.0, rmax=0.25)
+    ps = broad_phase(gpu, small)
+    assert 1024 < len(ps) <= 4096
+    np.testing.assert_array_equal(ps, broad_phase(oracle, small))
     rng = np.random.default_rng(77)
     pills = random_pills(rng, 2000, spread=3.0, rmax=0.25)
     pg = broad_phase(gpu, pills)
