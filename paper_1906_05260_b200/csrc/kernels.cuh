@@ -292,6 +292,8 @@ void launch_penetration(const World& w, Collide& c, const double* X, StepAccum* 
 // batch: per-scene residual norms (one CTA per scene) and end-of-substep singular fold-in
 void launch_scene_report(const World& w, const double* X, int classic, int* scene_singular, cudaStream_t st);
 int report_parts(int V);
+// get_state's outputs packed contiguously (centers, scales, frames, velocities: 8V + 7E doubles)
+void launch_pack_state(const World& w, const double* X, int E, double* out, cudaStream_t st);
 // kinetic energy and total volume (out[0], out[1]) in the reference's summation order;
 // terms: 4 x V scratch, rod_vol: R scratch; cw / sw: the layout's center / scale weights
 void launch_energy(const World& w, const double* X, const double* cw, const double* sw, int classic, double* terms,

@@ -365,7 +365,10 @@ Solver::~Solver() {
   if (h_anim_) cudaFreeHost(h_anim_);
   if (h_acc_) cudaFreeHost(h_acc_);
   if (h_scene_acc_) cudaFreeHost(h_scene_acc_);
-  if (h_state_) cudaFreeHost(h_state_);
+  if (h_pack_) cudaFreeHost(h_pack_);
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
+  if (side_) cudaStreamDestroy(side_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -756,12 +759,20 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
     }
     begin(CAT_REPORT);
     vdev::launch_finalize_from(w_, cur, h, keep, st);
+    const bool fork = pack_in_graph_ && use_graph_ && s == substeps - 1 && !probe_log && !prof;
+    if (fork) {  // get_state's pack + copy, as a side branch overlapping the report kernels
+      check_cuda(cudaEventRecord(ev_fork_, st), "fork");
+      check_cuda(cudaStreamWaitEvent(side_, ev_fork_, 0), "fork");
+      enqueue_pack(side_);
+      check_cuda(cudaEventRecord(ev_join_, side_), "join");
+    }
     vdev::launch_residuals(w_, w_.X, w_.classic, d_report_partials_, report_parts_,
                            reinterpret_cast<double*>(reinterpret_cast<char*>(d_acc_) + offsetof(StepAccum, residuals)), st);
     if (ext_possible_ && (c_.contact_cap + c_.hp_cap) > 0) vdev::launch_penetration(w_, c_, w_.X, d_acc_, st);
     if (n_scenes_ > 1) vdev::launch_scene_report(w_, w_.X, w_.classic, d_scene_sing_, st);
     vdev::launch_kernel(k_end_substep, 1, 1, 0, st, vdev::g_pdl, d_acc_, d_singular_ + (iterations - 1),
                         s == substeps - 1 ? 1 : 0, d_err_, c_.scalars);
+    if (fork) check_cuda(cudaStreamWaitEvent(st, ev_join_, 0), "join");
     end();
   }
   vdev::g_pdl = false;
@@ -869,6 +880,7 @@ long long Solver::kernel_nodes_per_step() {
 void Solver::pill_transforms_device(double* d_out) { vdev::launch_pill_transforms(w_, w_.X, d_out, stream_); }
 
 std::vector<double> Solver::shape_match() {
+  pack_fresh_ = false;
   std::vector<double> out(14ull * g_.G);
   if (g_.G == 0) return out;
   if (!d_fits_) d_fits_ = dalloc<double>(out.size());
@@ -881,6 +893,7 @@ std::vector<double> Solver::shape_match() {
 }
 
 std::pair<int, int> Solver::jacobi_sweep(double h, double beta) {
+  pack_fresh_ = false;
   cudaStream_t st = stream_;
   if (ext_possible_) {  // external blocks of this sweep: the soft pins only
     check_cuda(cudaMemsetAsync(c_.scalars + vdev::SC_NCT, 0, 2 * sizeof(int), st), "sweep reset");  // SC_NCT, SC_NHP
@@ -949,6 +962,7 @@ int Solver::trace(long long* out, int cap) {
 int Solver::contact_count_last() { return h_acc_->contact_count; }
 
 double Solver::bench_run(int steps, long long flush_bytes) {
+  pack_fresh_ = false;
   const int S = scene_.settings.substeps;
   const double h = scene_.settings.dt / S;
   ensure_graph();
@@ -979,6 +993,7 @@ double Solver::bench_run(int steps, long long flush_bytes) {
 }
 
 void Solver::kernel_times(int steps, double* ms, long long* launches) {
+  pack_fresh_ = false;
   const int S = scene_.settings.substeps;
   const double h = scene_.settings.dt / S;
   for (int c = 0; c < kCategories; ++c) {
@@ -1037,14 +1052,18 @@ Report Solver::step() {
   } else {
     record_step(h, S, scene_.settings.iterations, nullptr);
   }
+  pack_fresh_ = false;
+  if (prefetch_state_ && !(use_graph_ && pack_in_graph_)) enqueue_pack(stream_);  // rides on the step's sync
   Report rr;
   finish_step(h, S, &rr);
+  pack_fresh_ = prefetch_state_;
   rr.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   last_report_ = rr;
   return rr;
 }
 
 std::vector<double> Solver::probe_convergence(int iterations) {
+  pack_fresh_ = false;
   require(iterations >= 1, "probe needs at least one iteration");
   const double h = scene_.settings.dt / scene_.settings.substeps;
   if (iterations > scene_.settings.iterations) {
@@ -1069,48 +1088,53 @@ std::vector<double> Solver::probe_convergence(int iterations) {
 
 // ---- state access (global slot order with compact element numbering) -----------------------
 
+void Solver::enqueue_pack(cudaStream_t st) {
+  const std::size_t n = 8ull * setup_.V + 7ull * setup_.E;
+  vdev::launch_pack_state(w_, w_.X, setup_.E, d_pack_, st);
+  check_cuda(cudaMemcpyAsync(h_pack_, d_pack_, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "get_state");
+}
+
 void Solver::get_state(double* c, double* s, double* q, double* cv, double* sv, double* av) {
-  const int vpad = setup_.vpad, V = setup_.V;
-  const std::size_t nx = static_cast<std::size_t>(vdev::kStateFields) * vpad;
-  const std::size_t nv = static_cast<std::size_t>(vdev::kVelFields) * vpad;
-  if (!h_state_) check_cuda(cudaMallocHost(&h_state_, sizeof(double) * (nx + nv)), "cudaMallocHost");  // pinned mirror
-  const double* X = h_state_;
-  const double* vel = h_state_ + nx;
-  check_cuda(cudaMemcpyAsync(h_state_, w_.X, sizeof(double) * nx, cudaMemcpyDeviceToHost, stream_), "get_state");
-  if (cv || sv || av)
-    check_cuda(cudaMemcpyAsync(h_state_ + nx, w_.vel, sizeof(double) * nv, cudaMemcpyDeviceToHost, stream_), "get_state");
-  check_cuda(cudaStreamSynchronize(stream_), "get_state");
-  int e = 0;
-  for (int r = 0; r < setup_.R; ++r) {
-    const int n = scene_.rods[r].n, v0 = setup_.vbase[r];
-    for (int k = 0; k < n; ++k) {
-      const int v = v0 + k;
-      if (c) {
-        c[3 * v] = X[vdev::CX * vpad + v];
-        c[3 * v + 1] = X[vdev::CY * vpad + v];
-        c[3 * v + 2] = X[vdev::CZ * vpad + v];
-      }
-      if (s) s[v] = X[vdev::S * vpad + v];
-      if (cv) {
-        cv[3 * v] = vel[vdev::VX * vpad + v];
-        cv[3 * v + 1] = vel[vdev::VY * vpad + v];
-        cv[3 * v + 2] = vel[vdev::VZ * vpad + v];
-      }
-      if (sv) sv[v] = vel[vdev::VS * vpad + v];
-      if (k < n - 1) {
-        if (q)
-          for (int f = 0; f < 4; ++f) q[4 * e + f] = X[(vdev::QW + f) * vpad + v];
-        if (av)
-          for (int f = 0; f < 3; ++f) av[3 * e + f] = vel[(vdev::WX + f) * vpad + v];
-        ++e;
+  if (!d_pack_) {
+    const std::size_t n = 8ull * setup_.V + 7ull * setup_.E;
+    d_pack_ = dalloc<double>(n);
+    check_cuda(cudaMallocHost(&h_pack_, sizeof(double) * std::max<std::size_t>(n, 1)), "cudaMallocHost");
+  }
+  if (!prefetch_state_) {  // from now on every step also packs and copies the state
+    prefetch_state_ = true;
+    if (use_graph_) {
+      check_cuda(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "cudaStreamCreate");
+      check_cuda(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "cudaEventCreate");
+      check_cuda(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "cudaEventCreate");
+      pack_in_graph_ = true;
+      if (graph_exec_) {
+        cudaGraphExecDestroy(graph_exec_);
+        graph_exec_ = nullptr;
       }
     }
   }
-  (void)V;
+  if (!pack_fresh_) {
+    enqueue_pack(stream_);
+    check_cuda(cudaStreamSynchronize(stream_), "get_state");
+    pack_fresh_ = true;
+  }
+  const std::size_t V = static_cast<std::size_t>(setup_.V), E = static_cast<std::size_t>(setup_.E);
+  const double* p = h_pack_;
+  auto put = [&](double* dst, std::size_t n) {
+    if (dst && n) std::memcpy(dst, p, sizeof(double) * n);
+    p += n;
+  };
+  put(c, 3 * V);
+  put(s, V);
+  put(q, 4 * E);
+  put(cv, 3 * V);
+  put(sv, V);
+  put(av, 3 * E);
 }
 
 void Solver::set_state(const double* c, const double* s, const double* q, const double* cv, const double* sv,
                        const double* av) {
+  pack_fresh_ = false;
   const int vpad = setup_.vpad;
   std::vector<double> X(static_cast<std::size_t>(vdev::kStateFields) * vpad), vel(static_cast<std::size_t>(vdev::kVelFields) * vpad);
   check_cuda(cudaMemcpyAsync(X.data(), w_.X, sizeof(double) * X.size(), cudaMemcpyDeviceToHost, stream_), "set_state");

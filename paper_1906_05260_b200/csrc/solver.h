@@ -170,7 +170,18 @@ class Solver {
   int* d_scene_sing_ = nullptr;
   vdev::SceneAcc* h_scene_acc_ = nullptr;  // pinned, n_scenes_ (batch only)
   Report last_report_;
-  double* h_state_ = nullptr;  // pinned mirror of X and the velocities for get_state
+  // get_state: the outputs packed on the device and copied into a pinned buffer. Once get_state
+  // has been called, step() enqueues that pack + copy behind the step (one synchronisation for
+  // both); any other state-changing call invalidates the copy.
+  double* d_pack_ = nullptr;
+  double* h_pack_ = nullptr;
+  bool prefetch_state_ = false, pack_fresh_ = false;
+  // with graphs: the pack + copy is a side branch of the step graph, forked after the last
+  // finalize, so the copy overlaps the report kernels
+  bool pack_in_graph_ = false;
+  cudaStream_t side_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  void enqueue_pack(cudaStream_t st);
 };
 
 void check_cuda(cudaError_t e, const char* what);

@@ -369,6 +369,35 @@ __global__ void k_block_residuals(World w, const double* __restrict__ X, int cla
   }
 }
 
+// get_state's output layout, packed on the device (one D2H copy, contiguous host copies):
+// centers 3V | scales V | frames 4E (wxyz) | center velocities 3V | scale velocities V |
+// angular velocities 3E, in the C-ABI's global slot / compact element order (element e of slot
+// v is e = v - rod(v): every rod has one more vertex than elements).
+__global__ void k_pack_state(World w, const double* __restrict__ X, int E, double* __restrict__ out) {
+  const int V = w.V, vp = w.vpad;
+  double* c = out;
+  double* s = c + 3ll * V;
+  double* q = s + V;
+  double* cv = q + 4ll * E;
+  double* sv = cv + 3ll * V;
+  double* av = sv + V;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+    c[3ll * v] = F(X, CX, vp, v);
+    c[3ll * v + 1] = F(X, CY, vp, v);
+    c[3ll * v + 2] = F(X, CZ, vp, v);
+    s[v] = F(X, S, vp, v);
+    cv[3ll * v] = F(w.vel, VX, vp, v);
+    cv[3ll * v + 1] = F(w.vel, VY, vp, v);
+    cv[3ll * v + 2] = F(w.vel, VZ, vp, v);
+    sv[v] = F(w.vel, VS, vp, v);
+    if (w.slot_loc[v] < w.slot_m[v]) {
+      const long long e = v - w.slot_rod[v];
+      for (int f = 0; f < 4; ++f) q[4 * e + f] = F(X, QW + f, vp, v);
+      for (int f = 0; f < 3; ++f) av[3 * e + f] = F(w.vel, WX + f, vp, v);
+    }
+  }
+}
+
 // ---- Solver::kinetic_energy / total_volume (solver.cpp:400-430, rod.cpp:178-187) on the device.
 // The terms are computed in parallel; the sums run in the reference's sequential order (one
 // thread, or one thread per rod for the per-rod volumes), so the results are the same bits.
@@ -564,6 +593,10 @@ void launch_residuals(const World& w, const double* X, int classic, double* part
                       cudaStream_t st) {
   launch_kernel(k_report_partial, parts, kRepThreads, 0, st, g_pdl, w, X, classic, partials);
   launch_kernel(k_report_final, 1, kRepThreads, 0, st, g_pdl, partials, parts, out8);
+}
+
+void launch_pack_state(const World& w, const double* X, int E, double* out, cudaStream_t st) {
+  launch_kernel(k_pack_state, grid_for(w.V), kThreads, 0, st, false, w, X, E, out);
 }
 
 void launch_energy(const World& w, const double* X, const double* cw, const double* sw, int classic, double* terms,

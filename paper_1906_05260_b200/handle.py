@@ -140,8 +140,8 @@ class SolverHandle:
     def state(self) -> dict:
         """Live state, global slot order: centers (V,3), scales (V,), frames (E,4) wxyz, velocities."""
         V, E = self.total_vertices, self.total_elements
-        out = dict(centers=np.zeros((V, 3)), scales=np.zeros(V), frames=np.zeros((E, 4)),
-                   center_vel=np.zeros((V, 3)), scale_vel=np.zeros(V), angular_vel=np.zeros((E, 3)))
+        out = dict(centers=np.empty((V, 3)), scales=np.empty(V), frames=np.empty((E, 4)),
+                   center_vel=np.empty((V, 3)), scale_vel=np.empty(V), angular_vel=np.empty((E, 3)))
         check(self._lib, self._lib.vrod_solver_get_state(
             self._h, capi.ptr(out["centers"]), capi.ptr(out["scales"]), capi.ptr(out["frames"]),
             capi.ptr(out["center_vel"]), capi.ptr(out["scale_vel"]), capi.ptr(out["angular_vel"])))
