@@ -292,6 +292,12 @@ void launch_penetration(const World& w, Collide& c, const double* X, StepAccum* 
 // batch: per-scene residual norms (one CTA per scene) and end-of-substep singular fold-in
 void launch_scene_report(const World& w, const double* X, int classic, int* scene_singular, cudaStream_t st);
 int report_parts(int V);
+// k_report_partial only, and the fused end of a single-scene substep (penetration, residual
+// norms from the partials, singular count / error word)
+void launch_report_partial(const World& w, const double* X, int classic, double* partials, int parts, cudaStream_t st);
+void launch_report_tail(const World& w, Collide& c, const double* X, StepAccum* acc, bool do_pen, const double* partials,
+                        int parts, const int* singular_last, int last, const unsigned long long* err, unsigned* counter,
+                        cudaStream_t st);
 // get_state's outputs packed contiguously (centers, scales, frames, velocities: 8V + 7E doubles)
 void launch_pack_state(const World& w, const double* X, int E, double* out, cudaStream_t st);
 // kinetic energy and total volume (out[0], out[1]) in the reference's summation order;

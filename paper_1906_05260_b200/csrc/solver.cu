@@ -352,6 +352,7 @@ Solver::Solver(const SceneData& scene, const BatchLayout* batch) : scene_(scene)
   }
   report_parts_ = vdev::report_parts(V);
   d_report_partials_ = dalloc<double>(16ull * std::max(report_parts_, 1));
+  d_tail_counter_ = dalloc<unsigned>(1);
 
   upload_static();
   check_cuda(cudaStreamSynchronize(stream_), "setup");
@@ -766,12 +767,19 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
       enqueue_pack(side_);
       check_cuda(cudaEventRecord(ev_join_, side_), "join");
     }
-    vdev::launch_residuals(w_, w_.X, w_.classic, d_report_partials_, report_parts_,
-                           reinterpret_cast<double*>(reinterpret_cast<char*>(d_acc_) + offsetof(StepAccum, residuals)), st);
-    if (ext_possible_ && (c_.contact_cap + c_.hp_cap) > 0) vdev::launch_penetration(w_, c_, w_.X, d_acc_, st);
-    if (n_scenes_ > 1) vdev::launch_scene_report(w_, w_.X, w_.classic, d_scene_sing_, st);
-    vdev::launch_kernel(k_end_substep, 1, 1, 0, st, vdev::g_pdl, d_acc_, d_singular_ + (iterations - 1),
-                        s == substeps - 1 ? 1 : 0, d_err_, c_.scalars);
+    const bool do_pen = ext_possible_ && (c_.contact_cap + c_.hp_cap) > 0;
+    if (n_scenes_ == 1) {  // partials, then one fused tail launch
+      vdev::launch_report_partial(w_, w_.X, w_.classic, d_report_partials_, report_parts_, st);
+      vdev::launch_report_tail(w_, c_, w_.X, d_acc_, do_pen, d_report_partials_, report_parts_,
+                               d_singular_ + (iterations - 1), s == substeps - 1 ? 1 : 0, d_err_, d_tail_counter_, st);
+    } else {
+      vdev::launch_residuals(w_, w_.X, w_.classic, d_report_partials_, report_parts_,
+                             reinterpret_cast<double*>(reinterpret_cast<char*>(d_acc_) + offsetof(StepAccum, residuals)), st);
+      if (do_pen) vdev::launch_penetration(w_, c_, w_.X, d_acc_, st);
+      vdev::launch_scene_report(w_, w_.X, w_.classic, d_scene_sing_, st);
+      vdev::launch_kernel(k_end_substep, 1, 1, 0, st, vdev::g_pdl, d_acc_, d_singular_ + (iterations - 1),
+                          s == substeps - 1 ? 1 : 0, d_err_, c_.scalars);
+    }
     if (fork) check_cuda(cudaStreamWaitEvent(st, ev_join_, 0), "join");
     end();
   }

@@ -130,7 +130,8 @@ class Solver {
   double* d_ptrans_ = nullptr;       // pill transforms download buffer (lazy)
   double* d_fits_ = nullptr;         // shape_match() fit records (lazy)
   double* d_blockw_ = nullptr;       // elastic_residuals() output (lazy)
-  double* d_energy_ = nullptr;       // energy(): terms 4V, cw V, sw V, rod volumes R, out 2 (lazy)
+  double* d_energy_ = nullptr;
+  unsigned* d_tail_counter_ = nullptr;  // k_report_tail's last-CTA ticket       // energy(): terms 4V, cw V, sw V, rod volumes R, out 2 (lazy)
   unsigned long long* d_trace_ = nullptr;  // VROD_TRACE=1: persistent-kernel phase timestamps
  public:
   int trace(long long* out, int cap);

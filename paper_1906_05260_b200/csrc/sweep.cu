@@ -476,9 +476,7 @@ __global__ void k_report_partial(World w, const double* __restrict__ X, int clas
 
 // Sums the per-CTA partials: 16 quantities x `parts`, one CTA of 256 threads, each thread a
 // strided fixed subset, then a fixed tree — deterministic, no atomics.
-__global__ void k_report_final(const double* partials, int parts, double* out8) {
-  pdl_wait();
-  pdl_trigger();
+__device__ __forceinline__ void report_final_block(const double* partials, int parts, double* out8) {
   __shared__ double red[16][kRepThreads / 16];
   const int q = threadIdx.x & 15, lane = threadIdx.x >> 4;  // 16 threads per quantity
   double acc = 0.0;
@@ -494,10 +492,14 @@ __global__ void k_report_final(const double* partials, int parts, double* out8) 
     out8[threadIdx.x] = den > 0 ? sqrt(num / den) : 0.0;
   }
 }
-
-__global__ void k_penetration(World w, Collide c, const double* __restrict__ X, StepAccum* acc) {
+__global__ void k_report_final(const double* partials, int parts, double* out8) {
   pdl_wait();
   pdl_trigger();
+  report_final_block(partials, parts, out8);
+}
+
+__device__ __forceinline__ void penetration_part(const World& w, const Collide& c, const double* __restrict__ X,
+                                                 StepAccum* acc) {
   const int npins = c.n_pins;
   const int nct = c.scalars[SC_NCT];
   const int n = nct + c.scalars[SC_NHP];
@@ -515,6 +517,42 @@ __global__ void k_penetration(World w, Collide c, const double* __restrict__ X, 
   if ((threadIdx.x & 31) == 0 && deepest > 0.0)
     atomicMax(reinterpret_cast<unsigned long long*>(&acc->max_penetration),
               static_cast<unsigned long long>(__double_as_longlong(deepest)));
+}
+__global__ void k_penetration(World w, Collide c, const double* __restrict__ X, StepAccum* acc) {
+  pdl_wait();
+  pdl_trigger();
+  penetration_part(w, c, X, acc);
+}
+
+// The end of a single-scene substep in one launch: the max penetration over the contact and
+// half-plane blocks, then — in the last CTA to finish (ticket counter, reset by that CTA) — the
+// residual norms from k_report_partial's partials (the same fixed-order tree as k_report_final)
+// and the substep's singular count / error word (solver.cpp:335, 370-375).
+__global__ void k_report_tail(World w, Collide c, const double* __restrict__ X, StepAccum* acc, int do_pen,
+                              const double* partials, int parts, const int* singular_last, int last,
+                              const unsigned long long* err, unsigned* counter) {
+  pdl_wait();
+  pdl_trigger();
+  if (do_pen) penetration_part(w, c, X, acc);
+  __shared__ int is_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  report_final_block(partials, parts, acc->residuals);
+  if (threadIdx.x == 0) {
+    *counter = 0;
+    acc->skipped_singular += *singular_last;
+    if (last) {
+      unsigned long long e = *err;
+      if (c.scalars[SC_OVF]) e = err_code(0, ERR_CAPACITY, c.scalars[SC_OVF], 0);  // results invalid
+      acc->error = e;
+    }
+  }
 }
 
 // Batch: per-scene residual norms of the scene's slot range (one CTA per scene, fixed tree),
@@ -589,6 +627,10 @@ void launch_iteration(const World& w, Collide& c, const double* X, double* Y, co
   launch_rod_sweep(w, c, X, Y, sp, singular_counter, err, st);
 }
 
+void launch_report_partial(const World& w, const double* X, int classic, double* partials, int parts, cudaStream_t st) {
+  launch_kernel(k_report_partial, parts, kRepThreads, 0, st, g_pdl, w, X, classic, partials);
+}
+
 void launch_residuals(const World& w, const double* X, int classic, double* partials, int parts, double* out8,
                       cudaStream_t st) {
   launch_kernel(k_report_partial, parts, kRepThreads, 0, st, g_pdl, w, X, classic, partials);
@@ -613,6 +655,14 @@ void launch_block_residuals(const World& w, const double* X, int classic, double
 void launch_scene_report(const World& w, const double* X, int classic, int* scene_singular, cudaStream_t st) {
   launch_kernel(k_report_scene, w.n_scenes, kRepThreads, 0, st, g_pdl, w, X, classic);
   launch_kernel(k_scene_singular, (w.n_scenes + kThreads - 1) / kThreads, kThreads, 0, st, g_pdl, w, scene_singular);
+}
+
+void launch_report_tail(const World& w, Collide& c, const double* X, StepAccum* acc, bool do_pen, const double* partials,
+                        int parts, const int* singular_last, int last, const unsigned long long* err, unsigned* counter,
+                        cudaStream_t st) {
+  const int g = do_pen ? grid_for(c.contact_cap + c.hp_cap) : 1;
+  launch_kernel(k_report_tail, g, kRepThreads, 0, st, g_pdl, w, c, X, acc, do_pen ? 1 : 0, partials, parts, singular_last,
+                last, err, counter);
 }
 
 void launch_penetration(const World& w, Collide& c, const double* X, StepAccum* acc, cudaStream_t st) {
