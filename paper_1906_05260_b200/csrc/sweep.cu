@@ -224,6 +224,113 @@ __global__ void k_ext_sort(Collide c, int V) {
   }
 }
 
+// Small worlds: the whole external-block incidence setup (k_ext_count, the scan, k_ext_fill,
+// k_ext_sort) in ONE CTA of 1024 threads, phase by phase with block barriers — same entries,
+// same order, one launch instead of five.
+constexpr int kExtSetupThreads = 1024;
+__global__ void __launch_bounds__(kExtSetupThreads) k_ext_setup_small(Collide c, int V, int npins) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ int ws[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int v = tid; v <= V; v += kExtSetupThreads) {
+    c.ext_cnt[v] = 0;
+    if (v < V) c.ext_cur[v] = 0;
+  }
+  __syncthreads();
+  const int nct = c.scalars[SC_NCT];
+  const int n = npins + nct + c.scalars[SC_NHP];
+  for (int b = tid; b < n; b += kExtSetupThreads) {  // k_ext_count
+    int slots[4];
+    const int ne = ext_endpoints(c, b, npins, nct, slots);
+    for (int e = 0; e < ne; ++e)
+      if (slots[e] >= 0) atomicAdd(&c.ext_cnt[slots[e]], 1);
+    if (b >= npins && b < npins + nct) {
+      c.ct_va[b - npins] = slots[0];
+      c.ct_vb[b - npins] = slots[2];
+    }
+    c.ext_lam[b] = 0.0;
+    c.ext_lam[c.ext_cap + b] = 0.0;
+    c.ext_lam[2 * c.ext_cap + b] = 0.0;
+  }
+  __syncthreads();
+  int carry = 0;  // exclusive scan ext_cnt[0, V) -> ext_off[0, V]
+  for (int b0 = 0; b0 < V; b0 += kExtSetupThreads) {
+    const int x = b0 + tid < V ? c.ext_cnt[b0 + tid] : 0;
+    int incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) ws[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int y = ws[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += t;
+      }
+      ws[lane] = y;
+    }
+    __syncthreads();
+    if (b0 + tid < V) c.ext_off[b0 + tid] = carry + (wid ? ws[wid - 1] : 0) + incl - x;
+    carry += ws[31];
+    __syncthreads();
+  }
+  if (tid == 0) c.ext_off[V] = carry;
+  __syncthreads();
+  for (int b = tid; b < n; b += kExtSetupThreads) {  // k_ext_fill
+    int slots[4];
+    const int ne = ext_endpoints(c, b, npins, nct, slots);
+    for (int e = 0; e < ne; ++e) {
+      if (slots[e] < 0) continue;
+      const int pos = c.ext_off[slots[e]] + atomicAdd(&c.ext_cur[slots[e]], 1);
+      c.ext_items[pos] = (b << 2) | e;
+    }
+  }
+  __syncthreads();
+  // k_ext_sort: each warp takes 32 consecutive slots at a time, finds the ones with entries with
+  // one ballot (most slots have none), and sorts just those
+  for (int v0 = 32 * wid; v0 < V; v0 += kExtSetupThreads) {
+    const int vl = v0 + lane;
+    const int ml = vl < V ? c.ext_off[vl + 1] - c.ext_off[vl] : 0;
+    unsigned busy = __ballot_sync(0xffffffffu, ml > 0);
+    while (busy) {
+      const int src = __ffs(busy) - 1;
+      busy &= busy - 1;
+      const int v = v0 + src;
+      const int s0 = c.ext_off[v], m = __shfl_sync(0xffffffffu, ml, src), s1 = s0 + m;
+      if (m <= 32) {
+        const int key = lane < m ? c.ext_items[s0 + lane] : 0x7fffffff;
+        int rank = 0;
+        for (int j = 0; j < m; ++j) rank += __shfl_sync(0xffffffffu, key, j) < key ? 1 : 0;
+        __syncwarp();
+        if (lane < m) {
+          c.ext_items[s0 + rank] = key;
+          c.ext_pos[key] = s0 + rank;
+        }
+        __syncwarp();
+      } else {
+        if (lane == 0) {
+          for (int a = s0 + 1; a < s1; ++a) {
+            const int key = c.ext_items[a];
+            int b = a - 1;
+            while (b >= s0 && c.ext_items[b] > key) {
+              c.ext_items[b + 1] = c.ext_items[b];
+              --b;
+            }
+            c.ext_items[b + 1] = key;
+          }
+          for (int a = s0; a < s1; ++a) c.ext_pos[c.ext_items[a]] = a;
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
 // ---- end-of-substep report (elastic_residual_norms, constraints.cpp:558-596, and
 //      end_of_step_penetration, solver.cpp:291-299) ----------------------------------------
 
@@ -604,6 +711,10 @@ int grid_for(long long n) {
 int report_parts(int V) { return (V + kRepThreads - 1) / kRepThreads; }
 
 void launch_ext_setup(const World& w, Collide& c, cudaStream_t st) {
+  if (c.order_smem_cap >= 0 && w.V < (1 << 16)) {  // small worlds (same switch as the contact ordering)
+    launch_kernel(k_ext_setup_small, 1, kExtSetupThreads, 0, st, g_pdl, c, w.V, c.n_pins);
+    return;
+  }
   FillList f;
   f.add(c.ext_cnt, w.V + 1, 0);
   f.add(c.ext_cur, w.V, 0);
