@@ -140,8 +140,11 @@ class SolverHandle:
     def state(self) -> dict:
         """Live state, global slot order: centers (V,3), scales (V,), frames (E,4) wxyz, velocities."""
         V, E = self.total_vertices, self.total_elements
-        out = dict(centers=np.empty((V, 3)), scales=np.empty(V), frames=np.empty((E, 4)),
-                   center_vel=np.empty((V, 3)), scale_vel=np.empty(V), angular_vel=np.empty((E, 3)))
+        buf = np.empty(8 * V + 7 * E)  # one allocation, six views (the C-ABI's packed layout)
+        o = (0, 3 * V, 4 * V, 4 * V + 4 * E, 7 * V + 4 * E, 8 * V + 4 * E, 8 * V + 7 * E)
+        out = dict(centers=buf[o[0]:o[1]].reshape(V, 3), scales=buf[o[1]:o[2]], frames=buf[o[2]:o[3]].reshape(E, 4),
+                   center_vel=buf[o[3]:o[4]].reshape(V, 3), scale_vel=buf[o[4]:o[5]],
+                   angular_vel=buf[o[5]:o[6]].reshape(E, 3))
         check(self._lib, self._lib.vrod_solver_get_state(
             self._h, capi.ptr(out["centers"]), capi.ptr(out["scales"]), capi.ptr(out["frames"]),
             capi.ptr(out["center_vel"]), capi.ptr(out["scale_vel"]), capi.ptr(out["angular_vel"])))
