@@ -1009,14 +1009,11 @@ struct SweepOutcome {
 // contiguous chunks, index-addressed results — so the outcome is independent of scheduling. (The
 // reference's own multi-threaded run crashes on its thread_local update buffer, DESIGN.md §2;
 // this restatement keeps one shared buffer.)
-int thread_count() {
-  static const int cached = [] {
-    const char* env = std::getenv("VROD_THREADS");
-    if (!env) return 1;
-    const int hw = std::max(1u, std::thread::hardware_concurrency());
-    return std::clamp(std::atoi(env), 1, hw);
-  }();
-  return cached;
+int thread_count() {  // read per sweep (like parallel.h), so one process can compare thread counts
+  const char* env = std::getenv("VROD_THREADS");
+  if (!env) return 1;
+  static const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  return std::clamp(std::atoi(env), 1, hw);
 }
 template <typename Fn>
 void parallel_for(int n, int threads, Fn&& fn) {
