@@ -148,6 +148,56 @@ def kitchen_sink(lib) -> Scene:
     return s
 
 
+def _axis_quat(axis, angle):
+    a = np.asarray(axis, dtype=np.float64)
+    a = a / np.linalg.norm(a)
+    return (math.cos(0.5 * angle), *(math.sin(0.5 * angle) * a))
+
+
+def lbs_rig(lib) -> Scene:
+    """Bone-rigged rods: the linear-blend warm start `warm_start_lbs`
+    (solver.cpp:75-100) moves every unpinned vertex by its bones' slerped relative transform
+    between t_prev and t_new (Bone::position_at / rotation_at, scene.cpp:22-48) before the sweeps.
+    Two keyframed bones with several spans each (the slerp and the linear position blend are both
+    exercised); a two-bone rod with weights blending linearly from root to tip, a one-bone rod, a
+    three-weight rod crossing the others (contacts), an unrigged rod, a bone-posed kinematic pill,
+    gravity, two substeps."""
+    s = Scene(materials=[MaterialParams(stretch_x=1e5, stretch_y=1e5, stretch_z=1e5, bend_x=1e4, bend_y=1e4,
+                                        volume=1e7)])
+    s.bones.append(Bone([RigidKeyframe(0.0, (0.0, 0.0, 0.0), (1.0, 0.0, 0.0, 0.0)),
+                         RigidKeyframe(0.08, (0.02, 0.0, 0.01), _axis_quat((0, 0, 1), 0.15)),
+                         RigidKeyframe(0.2, (0.01, 0.03, -0.01), _axis_quat((1, 1, 0), 0.2)),
+                         RigidKeyframe(0.5, (-0.02, 0.01, 0.0), _axis_quat((0, 1, 1), -0.15))]))
+    s.bones.append(Bone([RigidKeyframe(0.02, (0.0, 0.0, 0.6), (1.0, 0.0, 0.0, 0.0)),
+                         RigidKeyframe(0.15, (0.0, -0.03, 0.63), _axis_quat((1, 0, 0), 0.2)),
+                         RigidKeyframe(0.4, (0.03, 0.0, 0.62), _axis_quat((0.3, -1, 0.2), 0.3))]))
+    n = 13
+    # two bones, weights root -> tip
+    rod = straight_rod(lib, (0.0, 0.0, 0.0), (0, 0, 1), 0.6, n - 1, 0.03)
+    w1 = np.arange(n) / (n - 1)
+    rod.bones = [0, 1]
+    rod.bone_weights = np.stack([1.0 - w1, w1], axis=1)
+    rod.pinned[0] = 1
+    s.rods.append(rod)
+    # one bone
+    rod = straight_rod(lib, (0.07, 0.0, 0.0), (0, 0, 1), 0.6, n - 1, 0.03)
+    rod.bones = [1]
+    rod.bone_weights = np.ones((n, 1))
+    s.rods.append(rod)
+    # three weights (bone 0 twice: duplicate bone entries are allowed), crossing the others
+    rod = straight_rod(lib, (-0.3, 0.035, 0.3), (1, 0, 0), 0.6, n - 1, 0.025)
+    u = np.arange(n) / (n - 1)
+    rod.bones = [0, 1, 0]
+    w0, w1 = 0.5 * (1.0 - u), 0.25 + 0.5 * u * (1.0 - u)
+    rod.bone_weights = np.stack([w0, w1, 1.0 - w0 - w1], axis=1)
+    s.rods.append(rod)
+    # unrigged
+    s.rods.append(straight_rod(lib, (0.035, -0.3, 0.45), (0, 1, 0), 0.6, n - 1, 0.025))
+    s.kinematic_pills.append(KinematicPill(Pill((-0.05, 0.0, 0.2), (0.05, 0.0, 0.2), 0.03, 0.03), bone=0))
+    s.settings = SolverSettings(substeps=2, iterations=10, velocity_damping=0.02)
+    return s
+
+
 def mini_muscle(lib) -> Scene:
     """C3 pattern at 1/8 scale: 4 muscles x 8 rods x 10 vertices."""
     return workloads.c3_muscle_bundle(lib, rods_per_muscle=8, vertices=10)
@@ -168,6 +218,7 @@ SCENES = {
     "pile": pile,
     "crossing": crossing,
     "kitchen_sink": kitchen_sink,
+    "lbs_rig": lbs_rig,
     "mini_muscle": mini_muscle,
     "mini_forest": mini_forest,
     "C1": workloads.c1_single_rod,
