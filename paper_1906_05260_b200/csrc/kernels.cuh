@@ -149,6 +149,7 @@ struct Groups {  // shape matching (bundling.cpp)
   double* grest = nullptr;       // 4 per group: rcent(3) denom
   double* warm = nullptr;        // 4 per group: warm rotation (w,x,y,z), persistent
   uint8_t* serial = nullptr;
+  int exact = 0;                 // exact-order path (shape.cuh shape_group_exact, VROD_SHAPE_EXACT)
   int* level_off = nullptr;      // host-side only (levels+1)
   int* level_groups = nullptr;   // device: group ids ordered by level
   // chain schedule (host_model.cpp), 0 chains when the frame dependencies are not chains

@@ -103,6 +103,7 @@ struct Tile {
 // corrections.
 template <int TP>
 struct PTile : Tile<TP> {
+  static_assert(sizeof(PosRes) * TP >= 2 * kShapeScratch * sizeof(double), "shape scratch in res");
   int eoff[TP];
   int ent_next;                   // dynamic entry distribution of the current sweep
   int e_item[kTileEntries];
@@ -936,7 +937,7 @@ __device__ __forceinline__ void aux_ext_phase(const World& w, const Collide& c, 
 // k_ext_solve, so the same bits) and only the block's owner entry commits its multiplier
 // (ping-pong lam_ext[2]) and counts; all CTAs share the shape work. The slot records are
 // ping-ponged (xrec[2]), so blocks solved elsewhere during a sweep always see the snapshot.
-template <int TP>
+template <int TP, bool kExactShape>
 __global__ void __launch_bounds__(32 * (warps_for<TP>() + 1), 1) k_iterate(World w, Collide c, Groups g, PersistParams pp,
                                                                       SweepParams sp, int* singular,
                                                                       unsigned long long* err) {
@@ -1098,8 +1099,14 @@ __global__ void __launch_bounds__(32 * (warps_for<TP>() + 1), 1) k_iterate(World
           const int k0 = chains ? g.chain_off[u] : u, k1 = chains ? g.chain_off[u + 1] : u + 1;
           for (int k = k0; k < k1; ++k) {
             const bool tr = pp.trace && it == 1 && (chains ? u == 28 : u == u0);
-            shape_group(w, g, cur, xr_cur, chains ? g.chain_groups[k] : g.level_groups[k], lane,
-                        tr ? pp.trace + 600 + 8 * (chains ? k - k0 : l) : nullptr, cache_shape ? &t.shape : nullptr);
+            // exact path: warps 0 and 1 order their member sums through the tile's block-result
+            // rows (idle between sweeps), other warps use shuffles
+            double* scratch = kExactShape && warp < 2 && !is_aux
+                                  ? reinterpret_cast<double*>(&t.res[0]) + warp * kShapeScratch
+                                  : nullptr;
+            shape_group<kExactShape ? 1 : 0>(w, g, cur, xr_cur, chains ? g.chain_groups[k] : g.level_groups[k], lane,
+                        tr ? pp.trace + 600 + 8 * (chains ? k - k0 : l) : nullptr, cache_shape ? &t.shape : nullptr,
+                        nullptr, scratch);
             __syncwarp();
           }
         }
@@ -1152,10 +1159,13 @@ int persistent_tiles(const World& w) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = sizeof(PTile<kPersistTP>);
-  if (cudaFuncSetAttribute(k_iterate<kPersistTP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iterate<kPersistTP>, 32 * (warps_for<kPersistTP>() + 1), smem) !=
-      cudaSuccess)
-    return 0;
+  for (auto* k : {k_iterate<kPersistTP, false>, k_iterate<kPersistTP, true>})
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
+  for (auto* k : {k_iterate<kPersistTP, false>, k_iterate<kPersistTP, true>}) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, 32 * (warps_for<kPersistTP>() + 1), smem) != cudaSuccess) return 0;
+    per_sm = per_sm == 0 ? n : (n < per_sm ? n : per_sm);
+  }
   return tiles <= per_sm * sms ? tiles : 0;
 }
 
@@ -1172,7 +1182,10 @@ void launch_iterate_persistent(const World& w, Collide& c, const Groups& g, cons
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_iterate<kPersistTP>, w, c, g, pp, sp, singular_counters, err);
+  if (g.exact)
+    cudaLaunchKernelEx(&cfg, k_iterate<kPersistTP, true>, w, c, g, pp, sp, singular_counters, err);
+  else
+    cudaLaunchKernelEx(&cfg, k_iterate<kPersistTP, false>, w, c, g, pp, sp, singular_counters, err);
 }
 
 }  // namespace vdev

@@ -18,10 +18,12 @@ __global__ void k_shape_level(World w, Groups g, double* __restrict__ X, int gbe
     pdl_wait();
     pdl_trigger();
   }
+  __shared__ double scratch[kWarpsPerBlock][kShapeScratch];  // exact path's ordered sums
   const int gi = gbeg + (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   if (gi >= gend) return;
   const int grp = g.level_groups[gi];
-  shape_group(w, g, X, w.xrec, grp, threadIdx.x & 31, nullptr, nullptr, fits ? fits + 14ll * grp : nullptr);
+  shape_group(w, g, X, w.xrec, grp, threadIdx.x & 31, nullptr, nullptr, fits ? fits + 14ll * grp : nullptr,
+              g.exact ? scratch[threadIdx.x >> 5] : nullptr);
 }
 
 // Standalone extract_rotation (bundling.h:42-43): one thread per problem.

@@ -9,6 +9,8 @@
 // chain uses explicit FMAs (both translation units compile with --fmad=false).
 #pragma once
 
+#include "crtrig.cuh"
+#include "rnops.cuh"
 #include "kernels.cuh"
 #include "vmath.cuh"
 
@@ -355,14 +357,299 @@ __device__ __forceinline__ void shape_degenerate_fit(const Groups& g, const Shap
   for (int k = 0; k < 14; ++k) fit[k] = rec[k];
 }
 
+// ---- exact-order variant (Groups::exact, VROD_SHAPE_EXACT) -----------------------------------
+// The reference's arithmetic in the reference's order: every member sum is sequential in member
+// order (all lanes run the same serial accumulation, reading member i's terms from lane i by
+// shuffle), the rotation extraction is bundling.cpp:50-67 verbatim (division by |dot| + 1e-9,
+// norm, Quaternion(AngleAxis) with correctly rounded sin / cos, crtrig.cuh, normalized()), and the
+// projection uses the exact normalisation. Compiled --fmad=false like every kernel, so the result
+// equals the reference bit for bit wherever glibc's sin / cos are correctly rounded.
+
+// std::max(v, kMinScale) (NaN propagates, unlike fmax)
+__device__ __forceinline__ double max_min_scale(double v) { return v < vm::kMinScale ? vm::kMinScale : v; }
+
+// extract_rotation, bundling.cpp:50-67, in the reference's operation order (IEEE division and
+// square root are correctly rounded, like the CPU's). kDevSin: CUDA's sincos instead of the
+// correctly rounded one (diagnostics only: not the reference's bits).
+template <bool kDevSin = false>
+static __device__ __noinline__ vm::Q4 extract_rotation_exact(const vm::M3& B, const vm::Q4& guess, int* iters = nullptr,
+                                                             int max_iterations = 100, double tolerance = 1e-9) {
+  using namespace vm;
+  // Eigen normalized(): coefficient / sqrt(squaredNorm) when it is > 0 (correctly rounded, rnops.cuh)
+  auto normalized_rn = [](const Q4& p) {
+    const double n = qsqnorm(p);
+    if (n <= 0.0) return p;
+    const double a[4] = {p.w, p.x, p.y, p.z};
+    double o[4];
+    rn::div_by(a, sqrt(n), o);
+    return Q4{o[0], o[1], o[2], o[3]};
+  };
+  Q4 q = normalized_rn(guess);
+  int it = 0;
+#pragma unroll 1
+  for (; it < max_iterations; ++it) {
+    const M3 R = qmat(q);
+    V3 omega{0, 0, 0};
+    double d = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      omega = omega + cross(col(R, a), col(B, a));
+      d += dot(col(R, a), col(B, a));
+    }
+    double w[3];
+    rn::div_by({omega.x, omega.y, omega.z}, fabs(d) + 1e-9, w);
+    const double angle = sqrt((w[0] * w[0] + w[1] * w[1]) + w[2] * w[2]);  // norm()
+    if (angle < tolerance) break;
+    double ax[3];
+    rn::div_by(w, angle, ax);
+    crt::DD sc;
+    if (kDevSin)
+      sincos(0.5 * angle, &sc.hi, &sc.lo);
+    else
+      sc = crt::sincos_rn(0.5 * angle);  // Quaternion(AngleAxisd(angle, axis)): (cos, sin * axis)
+    q = normalized_rn(qmul(Q4{sc.lo, sc.hi * ax[0], sc.hi * ax[1], sc.hi * ax[2]}, q));
+  }
+  if (iters) *iters = it;
+  return q;
+}
+
+__device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+// Doubles of per-warp scratch the exact path uses for its ordered sums (32 members x 18 terms).
+constexpr int kShapeScratch = 32 * 18;
+
+// Ordered (member-sequential) accumulation of a 32-member chunk: lane j holds member j's N terms
+// v[0..N); accumulator e (< E, held by lane e) adds, for j = 0 .. cnt-1 in order, the terms
+// v_j[e], v_j[e + E], .. (K = N / E terms per member, in that order). With a scratch buffer the
+// chunk is transposed through shared memory and the E serial chains run on E lanes side by side;
+// without one, every lane runs every chain on shuffled values (same order, same bits, slower).
+template <int N, int E>
+__device__ __forceinline__ void ordered_accumulate(const double (&v)[N], int cnt, int lane, double* scratch,
+                                                   double (&acc)[E]) {
+  constexpr int K = N / E;
+  if (scratch) {
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < N; ++i) scratch[lane * N + i] = v[i];
+    __syncwarp();
+    if (lane < E) {
+      double a = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (e == lane) a = acc[e];
+#pragma unroll 8
+      for (int j = 0; j < cnt; ++j)
+#pragma unroll
+        for (int k = 0; k < K; ++k) a = a + scratch[j * N + lane + k * E];
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (e == lane) acc[e] = a;
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = shfl_d(acc[e], e);
+  } else {
+    for (int j = 0; j < cnt; ++j)
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = acc[e] + shfl_d(v[e + k * E], j);
+  }
+}
+
+// One member's state and static data, loaded by the lane that owns it in a 32-member chunk.
+struct ExactMember {
+  vm::V3 c;   // current center (minus the centroid once known)
+  double s;
+  vm::M3 R;   // current frame as a matrix
+  const double* mr;
+};
+
+__device__ __forceinline__ ExactMember exact_load(const ShapeMembers& M, const double* X, long long vp, int i) {
+  using namespace vm;
+  ExactMember e;
+  const int v = M.slot(i), el = M.eslot(i);
+  e.c = V3{X[CX * vp + v], X[CY * vp + v], X[CZ * vp + v]};
+  e.s = X[S * vp + v];
+  e.R = qmat(Q4{X[QW * vp + el], X[QX * vp + el], X[QY * vp + el], X[QZ * vp + el]});
+  e.mr = M.rest(i);
+  return e;
+}
+
+static __device__ __forceinline__ void shape_group_exact(const World& w, const Groups& g, double* X, double* xrec, int grp, int lane,
+                                  const ShapeCache* sc, double* fit, unsigned long long* tr = nullptr,
+                                  double* scratch = nullptr) {
+  using namespace vm;
+  if (tr && lane == 0) tr[0] = gtimer();
+  int ci = -1;
+  if (sc)
+    for (int k = 0; k < sc->ng; ++k)
+      if (sc->gid[k] == grp) ci = k;
+  const int m0 = ci >= 0 ? sc->m0[ci] : g.off[grp], m1 = ci >= 0 ? sc->m1[ci] : g.off[grp + 1];
+  const int lb = ci >= 0 ? sc->base[ci] - m0 : 0;
+  const ShapeMembers M{g, sc, ci, lb};
+  const long long vp = w.vpad;
+  const int n = m1 - m0;
+  const double* gr = ci >= 0 ? sc->grest[ci] : g.grest + 4ll * grp;
+  const V3 rcent{gr[0], gr[1], gr[2]};
+  const double denom = gr[3];
+  // centroid (bundling.cpp:73-75): sequential sum, then division by n
+  double cacc[3] = {0.0, 0.0, 0.0};
+  for (int b = m0; b < m1; b += 32) {
+    const int i = b + lane, cnt = min(32, m1 - b);
+    double c[3] = {0.0, 0.0, 0.0};
+    if (i < m1) {
+      const int v = M.slot(i);
+      c[0] = X[CX * vp + v];
+      c[1] = X[CY * vp + v];
+      c[2] = X[CZ * vp + v];
+    }
+    ordered_accumulate<3, 3>(c, cnt, lane, scratch, cacc);
+  }
+  const V3 cent = V3{cacc[0], cacc[1], cacc[2]} / static_cast<double>(n);
+  if (tr && lane == 0) tr[1] = gtimer();
+  // covariance (:77-85): B += (s * s_rest) R R_rest^T; B += c c_rest^T, member after member
+  double bacc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int b = m0; b < m1; b += 32) {
+    const int i = b + lane, cnt = min(32, m1 - b);
+    double PO[18];  // the member's (s s_rest) R R_rest^T, then c c_rest^T, row-major
+#pragma unroll
+    for (int k = 0; k < 18; ++k) PO[k] = 0.0;
+    if (i < m1) {
+      const ExactMember e = exact_load(M, X, vp, i);
+      const V3 c = e.c - cent;
+      const double ss = e.s * e.mr[3];
+      M3 A, rR;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          A.m[a][q] = ss * e.R.m[a][q];
+          rR.m[a][q] = e.mr[4 + 3 * a + q];
+        }
+      const M3 Pm = mmul_bt(A, rR);
+      const double cv[3] = {c.x, c.y, c.z};
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          PO[3 * a + q] = Pm.m[a][q];
+          PO[9 + 3 * a + q] = cv[a] * e.mr[q];
+        }
+    }
+    if (tr && lane == 0 && b == m0) tr[7] = gtimer();
+    ordered_accumulate<18, 9>(PO, cnt, lane, scratch, bacc);
+  }
+  M3 B;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) B.m[k / 3][k % 3] = bacc[k];
+  double sq[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) sq[a + 3 * q] = B.m[a][q] * B.m[a][q];
+  if (sqrt(sum9(sq)) < 1e-12 || denom < 1e-300) {  // degenerate (:86-90): no write
+    if (fit && lane == 0) {
+      const V3 t = cent - rcent;
+      const double rec[14] = {1.0, t.x, t.y, t.z, 1, 0, 0, 0, 1, 0, 0, 0, 1, 1.0};
+      for (int k = 0; k < 14; ++k) fit[k] = rec[k];
+    }
+    return;
+  }
+  if (tr && lane == 0) tr[2] = gtimer();
+  double* wq = g.warm + 4ll * grp;
+  int nit = 0;
+  const Q4 q = extract_rotation_exact(B, Q4{wq[0], wq[1], wq[2], wq[3]}, &nit);
+  if (tr && lane == 0) {
+    tr[3] = gtimer();
+    tr[6] = nit;
+  }
+  const M3 Rf = qmat(q);
+  // scale numerator (:97-108), sequential
+  double nacc[1] = {0.0};
+  for (int b = m0; b < m1; b += 32) {
+    const int i = b + lane, cnt = min(32, m1 - b);
+    double tt[2] = {0.0, 0.0};
+    if (i < m1) {
+      const ExactMember e = exact_load(M, X, vp, i);
+      const V3 c = e.c - cent;
+      M3 rR;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) rR.m[a][r] = e.mr[4 + 3 * a + r];
+      const M3 RR = mmul(Rf, rR);
+      double el[9];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) el[a + 3 * r] = RR.m[a][r] * e.R.m[a][r];
+      tt[0] = (e.s * e.mr[3]) * sum9(el);
+      tt[1] = dot(c, mvmul(Rf, V3{e.mr[0], e.mr[1], e.mr[2]}));
+    }
+    ordered_accumulate<2, 1>(tt, cnt, lane, scratch, nacc);
+  }
+  const double numer = nacc[0];
+  if (tr && lane == 0) tr[4] = gtimer();
+  const double scale = max_min_scale(numer / denom);
+  const V3 t = cent - scale * mvmul(Rf, rcent);
+  const Q4 qf = qfrom_mat(Rf);
+  // projection (apply_shape_match, :116-133)
+  auto apply = [&](int i) {
+    const double* mr = M.rest(i);
+    const int v = M.slot(i);
+    if (!(ci >= 0 ? sc->pinned[i + lb] : w.pinned[v])) {
+      const V3 x = scale * mvmul(Rf, V3{mr[0], mr[1], mr[2]} + rcent) + t;
+      X[CX * vp + v] = x.x;
+      X[CY * vp + v] = x.y;
+      X[CZ * vp + v] = x.z;
+      const double sn = max_min_scale(scale * mr[3]);
+      X[S * vp + v] = sn;
+      double2* xr = reinterpret_cast<double2*>(xrec + 8ll * v);
+      xr[0] = make_double2(x.x, x.y);
+      xr[1] = make_double2(x.z, sn);
+    }
+    const Q4 fr = qnormalized(qmul(qf, Q4{mr[13], mr[14], mr[15], mr[16]}));
+    const int e = M.eslot(i);
+    X[QW * vp + e] = fr.w;
+    X[QX * vp + e] = fr.x;
+    X[QY * vp + e] = fr.y;
+    X[QZ * vp + e] = fr.z;
+  };
+  __syncwarp();
+  if (ci >= 0 ? sc->serial[ci] : g.serial[grp]) {
+    if (lane == 0)
+      for (int i = m0; i < m1; ++i) apply(i);
+  } else {
+    for (int i = m0 + lane; i < m1; i += 32) apply(i);
+  }
+  if (tr && lane == 0) tr[5] = gtimer();
+  if (fit && lane == 0) {
+    const double rec[14] = {scale, t.x, t.y, t.z, Rf.m[0][0], Rf.m[0][1], Rf.m[0][2], Rf.m[1][0], Rf.m[1][1],
+                            Rf.m[1][2], Rf.m[2][0], Rf.m[2][1], Rf.m[2][2], 0.0};
+    for (int k = 0; k < 14; ++k) fit[k] = rec[k];
+  }
+  if (lane == 0) {
+    wq[0] = q.w;
+    wq[1] = q.x;
+    wq[2] = q.y;
+    wq[3] = q.z;
+  }
+}
+
 // Fit and apply group `grp` (apply_shape_match, bundling.cpp:116-133) on the state rows X and
 // the slot records xrec, all phases in one warp (the rotation extraction redundantly in every
 // lane). tr: optional phase timestamps; sc: optional shared-memory copy of the group's statics;
 // fit: optional SimilarityFit record (bundling.h:18-23), 14 doubles: scale, translation xyz,
 // rotation (row-major 3x3), degenerate flag.
+// kMode: 0 the latency-tuned path, 1 the exact-order path, -1 chosen by Groups::exact at run time.
+template <int kMode = -1>
 __device__ __forceinline__ void shape_group(const World& w, const Groups& g, double* X, double* xrec, int grp,
                                             int lane, unsigned long long* tr = nullptr, const ShapeCache* sc = nullptr,
-                                            double* fit = nullptr) {
+                                            double* fit = nullptr, double* scratch = nullptr) {
+  if (kMode == 1 || (kMode < 0 && g.exact)) {
+    shape_group_exact(w, g, X, xrec, grp, lane, sc, fit, tr, scratch);
+    return;
+  }
   if (tr && lane == 0) tr[0] = gtimer();
   const ShapeState st = shape_begin(w, g, X, grp, lane, sc, tr);
   if (st.degenerate) {

@@ -238,6 +238,8 @@ Solver::Solver(const SceneData& scene, const BatchLayout* batch) : scene_(scene)
   // ---- shape matching ----------------------------------------------------------------------
   g_.G = static_cast<int>(setup_.groups.size());
   g_.levels = setup_.levels;
+  // exact-order shape matching (shape.cuh shape_group_exact): VROD_SHAPE_EXACT=1
+  g_.exact = std::getenv("VROD_SHAPE_EXACT") && std::getenv("VROD_SHAPE_EXACT")[0] == '1';
   {
     std::vector<int> off(1, 0), ms, mes, lvl_groups;
     std::vector<double> mrest, grest, warm;

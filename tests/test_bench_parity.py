@@ -3,9 +3,10 @@ bench.py builds them, against the CPU oracle (the restatement, bitwise equal to 
 test_oracle_pinning) or, at C4, against digests of the reference's own output.
 
 - C2 (64 rods x 256 vertices, stretched by pin motions; no contacts, no bundles): bitwise, K = 60.
-- C3 (the 26k-DOF muscle bundle, shape matching + contacts): identical input -> one substep
-  within 1e-10; free-running K = 10 within 1e-6 with the contact set (pill_a, pill_b) exact at
-  every substep and alpha/beta within 1e-9. C3g (SURVEY's literal C3, gravity on, O(10^3) contacts) the same.
+- C3 (the 26k-DOF muscle bundle, shape matching + contacts), default (latency-tuned) shape
+  matching: identical input -> one substep within 1e-10; free-running K = 10 within 1e-6 with the
+  contact set (pill_a, pill_b) exact at every substep and alpha/beta within 1e-9. With the
+  exact-order shape path (VROD_SHAPE_EXACT=1): bit for bit, K = 10. C3g (SURVEY's literal C3, gravity on, O(10^3) contacts) the same.
 - C4 (1,000,000 vertices, ~2.8 M contacts): two substeps, every output array bit for bit
   (SHA-256 against tests/golden/c4_hashes.json, made by tests/golden/make_c4_hashes.py from
   oracle/_ref and the restatement).
@@ -98,6 +99,29 @@ def _contacts_match(g, o, where):
     if not len(cg["alpha"]):
         return 0.0
     return float(max(np.abs(cg["alpha"] - co["alpha"]).max(), np.abs(cg["beta"] - co["beta"]).max()))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", sorted(C3_VARIANTS))
+def test_c3_exact_mode_bitwise(oracle, variant, monkeypatch):
+    """VROD_SHAPE_EXACT=1 (shape.cuh shape_group_exact): the C3 scenes bench.py times are
+    bit-identical to the oracle (= the reference) for K = 10 substeps: states, velocities,
+    contacts with alpha/beta, counters, penetration."""
+    monkeypatch.setenv("VROD_SHAPE_EXACT", "1")
+    lib = pb.library()
+    scene = C3_VARIANTS[variant](lib)
+    g, o = SolverHandle(lib, scene), SolverHandle(oracle, scene)
+    for k in range(10):
+        rg, ro = g.step(), o.step()
+        assert (rg.contact_count, rg.broad_pairs, rg.skipped_singular, rg.max_penetration) == \
+               (ro.contact_count, ro.broad_pairs, ro.skipped_singular, ro.max_penetration), (variant, k)
+        cg, co = g.contacts(), o.contacts()
+        for key in cg:
+            np.testing.assert_array_equal(cg[key], co[key], err_msg=f"{variant} substep {k}: {key}")
+        sg, so = g.state(), o.state()
+        for key in sg:
+            np.testing.assert_array_equal(sg[key], so[key], err_msg=f"{variant} substep {k}: {key}")
+    MAXIMA[f"{variant}_exact"] = {"steps": 10, "bitwise": True}
 
 
 @pytest.mark.gpu

@@ -67,6 +67,16 @@ def test_gpu_reproduces_reference_golden(golden, name):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(SHAPE_MATCHING))
+def test_gpu_exact_shape_mode_reproduces_reference_golden(golden, name, monkeypatch):
+    """The exact-order shape-matching path (VROD_SHAPE_EXACT=1) reproduces the reference's own
+    output (oracle/_ref) bit for bit on the shape-matching golden scenes too."""
+    import paper_1906_05260_b200 as pb
+    monkeypatch.setenv("VROD_SHAPE_EXACT", "1")
+    check_scene(pb.library(), golden, name, exact=True)
+
+
+@pytest.mark.gpu
 def test_gpu_collision_golden(golden):
     import paper_1906_05260_b200 as pb
     check_collision(pb.library(), golden)

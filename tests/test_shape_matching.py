@@ -109,6 +109,19 @@ def test_gpu_shape_pass(oracle, name):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name", SHAPE_SCENES)
+def test_gpu_shape_pass_exact_mode_bitwise(oracle, name, monkeypatch):
+    """The exact-order path (VROD_SHAPE_EXACT=1): fits, states and frames bit-identical."""
+    import paper_1906_05260_b200 as pb
+    monkeypatch.setenv("VROD_SHAPE_EXACT", "1")
+    fa, sa = shape_pass(pb.library(), name)
+    fb, sb = shape_pass(oracle, name)
+    np.testing.assert_array_equal(fa, fb)
+    for k in sa:
+        np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
+
+
+@pytest.mark.gpu
 def test_gpu_similarity_recovery(oracle):
     import paper_1906_05260_b200 as pb
     fa, sigma, R, t = similarity_recovery(pb.library())

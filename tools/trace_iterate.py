@@ -54,7 +54,8 @@ for l in range(2):
     ph = raw[600 + 8 * l: 606 + 8 * l]
     if ph[0] > 0:
         print(f"shape level/chain pos {l} group phases us: centroid {(ph[1]-ph[0])/1e3:.2f} covariance {(ph[2]-ph[1])/1e3:.2f} "
-              f"rotation {(ph[3]-ph[2])/1e3:.2f} ({int(raw[606 + 8 * l])} it) scale {(ph[4]-ph[3])/1e3:.2f} apply {(ph[5]-ph[4])/1e3:.2f}")
+              f"rotation {(ph[3]-ph[2])/1e3:.2f} ({int(raw[606 + 8 * l])} it) scale {(ph[4]-ph[3])/1e3:.2f} apply {(ph[5]-ph[4])/1e3:.2f}"
+              + (f" [covariance terms {(raw[607 + 8 * l]-ph[1])/1e3:.2f}, ordered sum {(ph[2]-raw[607 + 8 * l])/1e3:.2f}]" if raw[607 + 8 * l] > 0 else ""))
 cta = int(os.environ.get("VROD_TRACE_CTA", "0"))
 t0 = raw[899]
 if t0 > 0:
