@@ -201,6 +201,19 @@ int vrod_solver_get_state(vrod_solver* solver, double* centers, double* scales, 
 int vrod_solver_set_state(vrod_solver* solver, const double* centers, const double* scales,
                           const double* frames, const double* center_vel, const double* scale_vel,
                           const double* angular_vel);
+/* Product options, no reference counterpart (the reference has no GPU); name -> value:
+ *   "state_prefetch"        1: each step also copies the state to pinned host memory inside the
+ *                           step's own synchronisation (get_state after a step is a memcpy);
+ *                           0 (default): get_state copies on demand.
+ *   "exact_shape_matching"  1: shape matching in the reference's exact operation order (states
+ *                           bit-identical to the reference); 0: the latency-tuned path (within
+ *                           BASELINE.md §5's tolerance). Default: environment VROD_SHAPE_EXACT.
+ *   "phase_timing"          1: fill vrod_step_report's predict/broad/narrow/solve/finalize_ms
+ *                           (device time per phase, solver.h:14-21) at the cost of direct kernel
+ *                           launches instead of one CUDA graph per step; 0 (default): zeros.
+ * Unknown name: VROD_INVALID_ARGUMENT. */
+int vrod_solver_set_option(vrod_solver* solver, const char* name, int64_t value);
+
 /* Live rest quantities (activation rewrites lengths & derived data, rod.cpp:164-176). */
 int vrod_solver_get_rest(vrod_solver* solver, double* lengths, double* darboux_per_element,
                          double* scale_grads, double* scale_laplacians_per_element);

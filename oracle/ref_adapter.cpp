@@ -453,6 +453,14 @@ int vrod_solver_get_state(vrod_solver* s, double* c, double* sc, double* f, doub
   });
 }
 
+// Product options (include/vrod_capi.h): the CPU path is always the reference's exact order and
+// copies state on demand, so the options are accepted and change nothing here.
+int vrod_solver_set_option(vrod_solver*, const char* name, int64_t) {
+  return guarded([&] {
+    const std::string n = name ? name : "";
+    vrod::require(n == "state_prefetch" || n == "exact_shape_matching" || n == "phase_timing", "unknown solver option");
+  });
+}
 int vrod_solver_set_state(vrod_solver* s, const double* c, const double* sc, const double* f,
                           const double* cv, const double* sv, const double* av) {
   return guarded([&] {

@@ -110,6 +110,7 @@ _SIGNATURES = {
     "vrod_solver_get_rod_sizes": (C.c_int, [C.c_void_p, _ip]),
     "vrod_solver_get_state": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp]),
     "vrod_solver_set_state": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp]),
+    "vrod_solver_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
     "vrod_solver_get_rest": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp]),
     "vrod_solver_set_loads": (C.c_int, [C.c_void_p, _dp, _u8p, _dp, _u8p, _dp, _u8p]),
     "vrod_solver_energy": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),

@@ -306,6 +306,11 @@ static void put_report(const Report& r, vrod_step_report* out) {
   out->broad_pairs = r.broad;
   out->skipped_singular = r.singular;
   out->dof_count = r.dof;
+  out->predict_ms = r.predict_ms;
+  out->broad_ms = r.broad_ms;
+  out->narrow_ms = r.narrow_ms;
+  out->solve_ms = r.solve_ms;
+  out->finalize_ms = r.finalize_ms;
   out->total_ms = r.total_ms;
 }
 
@@ -382,6 +387,11 @@ int vrod_solver_get_rod_sizes(const vrod_solver* h, int32_t* counts) {
 }
 int vrod_solver_get_state(vrod_solver* h, double* c, double* sc, double* f, double* cv, double* sv, double* av) {
   return guarded([&] { h->s->get_state(c, sc, f, cv, sv, av); });
+}
+int vrod_solver_set_option(vrod_solver* h, const char* name, int64_t value) {
+  return guarded([&] {
+    require(name != nullptr && h->s->set_option(name, value), "unknown solver option");
+  });
 }
 int vrod_solver_set_state(vrod_solver* h, const double* c, const double* sc, const double* f, const double* cv,
                           const double* sv, const double* av) {

@@ -1280,6 +1280,8 @@ void launch_order_contacts(Collide& c, cudaStream_t st) {
 // Broad + narrow phase on the pill arrays already in `c` (pill, pill_rod/el/group/self/id).
 // prefilter=0 keeps every allowed pair (the standalone broad_phase contract); with do_narrow=0
 // the (unordered) candidates are left in cand_i/cand_j, scalars[SC_NCAND].
+cudaEvent_t g_broad_mark = nullptr;
+
 void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int prefilter, int do_narrow,
                          int split_warm, int store_d, cudaStream_t st) {
   (void)store_d;
@@ -1318,6 +1320,7 @@ void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
                     g_pdl, c, prefilter, c.scalars + SC_BROAD, c.scalars + SC_NCAND_RAW);
     }
   }
+  if (g_broad_mark) cudaEventRecord(g_broad_mark, st);  // end of the broad phase (phase timing)
   if (fused_seg) {  // k_narrow_append clamps the count and runs the exact segment test itself
     launch_kernel(k_narrow_append<true>, narrow_grid(c.cand_cap), kNarrowThreads, 0, st, g_pdl, c, split_warm,
                   int(SC_NCAND_RAW));

@@ -265,6 +265,9 @@ void launch_finalize_from(const World& w, const double* src, double h, double ke
 void launch_copy_state(const World& w, const double* src, double* dst, cudaStream_t st);
 
 // collide.cu
+// When set (phase timing, Solver::set_option "phase_timing"), recorded on the stream between the
+// broad phase (pair scan) and the narrow phase of launch_collide.
+extern cudaEvent_t g_broad_mark;
 void launch_collide(const World& w, Collide& c, const double* anim, const AnimLayout& al, int substep,
                     unsigned long long* err, StepAccum* acc, int possible, cudaStream_t st);
 void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int prefilter, int do_narrow,

@@ -675,6 +675,15 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
   auto end = [&]() {
     if (prof) cudaEventRecord(prof->ev.back(), st);
   };
+  // the collide bracket also marks the end of its broad phase (phase timing: broad vs narrow)
+  auto begin_collide = [&]() {
+    begin(CAT_COLLIDE);
+    if (!prof) return;
+    cudaEvent_t m;
+    cudaEventCreate(&m);
+    prof->broad_end.push_back(m);
+    vdev::g_broad_mark = m;
+  };
   // Programmatic dependent launch between the step's kernels (not when profiling: the event
   // brackets between categories would serialize them anyway).
   vdev::g_pdl = pdl_ && !prof;
@@ -690,8 +699,13 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
                          n_act_rods_, st);
     vdev::launch_predict(w_, anim, al_, g, h, s, d_err_, st);
     end();
-    begin(CAT_COLLIDE);
+    begin_collide();
     if (c_.P >= 1) vdev::launch_collide(w_, c_, anim, al_, s, d_err_, d_acc_, collide_possible_ ? 1 : 0, st);
+    if (prof && vdev::g_broad_mark) {
+      // no pair scan ran (nothing can collide): the broad phase ends here
+      if (c_.P < 1 || !collide_possible_) cudaEventRecord(vdev::g_broad_mark, st);
+      vdev::g_broad_mark = nullptr;
+    }
     vdev::launch_halfplanes(w_, c_, st);
     end();
     begin(CAT_EXT_SETUP);
@@ -1024,7 +1038,74 @@ void Solver::kernel_times(int steps, double* ms, long long* launches) {
       cudaEventDestroy(prof.ev[2 * i]);
       cudaEventDestroy(prof.ev[2 * i + 1]);
     }
+    for (cudaEvent_t m : prof.broad_end) cudaEventDestroy(m);
   }
+}
+
+// Device time per reference phase (solver.cpp:310-359: predict = animate + predict; broad =
+// broad_phase; narrow = find_contacts + contact / half-plane blocks; solve = the sweeps and shape
+// matching; finalize = velocities + report) from one profiled step's event brackets.
+void Solver::phase_times(Prof& prof, Report* r) {
+  std::size_t collide_k = 0;
+  for (std::size_t i = 0; i < prof.cat.size(); ++i) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, prof.ev[2 * i], prof.ev[2 * i + 1]);
+    switch (prof.cat[i]) {
+      case CAT_PREDICT: r->predict_ms += t; break;
+      case CAT_COLLIDE: {
+        float b = t;
+        if (collide_k < prof.broad_end.size()) cudaEventElapsedTime(&b, prof.ev[2 * i], prof.broad_end[collide_k]);
+        ++collide_k;
+        r->broad_ms += b;
+        r->narrow_ms += t - b;
+        break;
+      }
+      case CAT_EXT_SETUP: r->narrow_ms += t; break;  // contact / half-plane block generation
+      case CAT_REPORT: r->finalize_ms += t; break;
+      default: r->solve_ms += t; break;
+    }
+    cudaEventDestroy(prof.ev[2 * i]);
+    cudaEventDestroy(prof.ev[2 * i + 1]);
+  }
+  for (cudaEvent_t m : prof.broad_end) cudaEventDestroy(m);
+}
+
+bool Solver::set_option(const std::string& name, long long value) {
+  auto drop_graph = [&]() {
+    if (graph_exec_) {
+      cudaGraphExecDestroy(graph_exec_);
+      graph_exec_ = nullptr;
+    }
+  };
+  if (name == "state_prefetch") {
+    const bool on = value != 0;
+    if (on == prefetch_state_) return true;
+    prefetch_state_ = on;
+    pack_fresh_ = false;
+    if (on && !d_pack_) {
+      const std::size_t n = 8ull * setup_.V + 7ull * setup_.E;
+      d_pack_ = dalloc<double>(n);
+      check_cuda(cudaMallocHost(&h_pack_, sizeof(double) * std::max<std::size_t>(n, 1)), "cudaMallocHost");
+    }
+    if (on && use_graph_ && !side_) {
+      check_cuda(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "cudaStreamCreate");
+      check_cuda(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "cudaEventCreate");
+      check_cuda(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    pack_in_graph_ = on && use_graph_;
+    drop_graph();
+    return true;
+  }
+  if (name == "exact_shape_matching") {
+    g_.exact = value != 0 ? 1 : 0;
+    drop_graph();
+    return true;
+  }
+  if (name == "phase_timing") {
+    phase_timing_ = value != 0;
+    return true;
+  }
+  return false;
 }
 
 void Solver::finish_step(double h, int substeps, Report* out) {
@@ -1056,16 +1137,19 @@ Report Solver::step() {
   const int S = scene_.settings.substeps;
   const double h = scene_.settings.dt / S;
   fill_animation(S, h);
-  if (use_graph_) {
+  Prof prof;
+  const bool graph = use_graph_ && !phase_timing_;
+  if (graph) {
     ensure_graph();
     check_cuda(cudaGraphLaunch(graph_exec_, stream_), "graph launch");
   } else {
-    record_step(h, S, scene_.settings.iterations, nullptr);
+    record_step(h, S, scene_.settings.iterations, nullptr, phase_timing_ ? &prof : nullptr);
   }
   pack_fresh_ = false;
-  if (prefetch_state_ && !(use_graph_ && pack_in_graph_)) enqueue_pack(stream_);  // rides on the step's sync
+  if (prefetch_state_ && !(graph && pack_in_graph_)) enqueue_pack(stream_);  // rides on the step's sync
   Report rr;
   finish_step(h, S, &rr);
+  if (phase_timing_) phase_times(prof, &rr);
   pack_fresh_ = prefetch_state_;
   rr.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   last_report_ = rr;
@@ -1109,19 +1193,6 @@ void Solver::get_state(double* c, double* s, double* q, double* cv, double* sv, 
     const std::size_t n = 8ull * setup_.V + 7ull * setup_.E;
     d_pack_ = dalloc<double>(n);
     check_cuda(cudaMallocHost(&h_pack_, sizeof(double) * std::max<std::size_t>(n, 1)), "cudaMallocHost");
-  }
-  if (!prefetch_state_) {  // from now on every step also packs and copies the state
-    prefetch_state_ = true;
-    if (use_graph_) {
-      check_cuda(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "cudaStreamCreate");
-      check_cuda(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "cudaEventCreate");
-      check_cuda(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "cudaEventCreate");
-      pack_in_graph_ = true;
-      if (graph_exec_) {
-        cudaGraphExecDestroy(graph_exec_);
-        graph_exec_ = nullptr;
-      }
-    }
   }
   if (!pack_fresh_) {
     enqueue_pack(stream_);

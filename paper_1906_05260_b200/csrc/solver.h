@@ -20,6 +20,9 @@ struct Report {
   double time = 0.0;
   double residuals[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   double max_pen = 0.0;
+  // PhaseTimings (solver.h:14-21 of the reference): device time per phase, summed over the
+  // substeps, filled when the "phase_timing" option is on (else 0)
+  double predict_ms = 0.0, broad_ms = 0.0, narrow_ms = 0.0, solve_ms = 0.0, finalize_ms = 0.0;
   double total_ms = 0.0;
 };
 
@@ -37,6 +40,17 @@ class Solver {
 
   Report step();
   std::vector<double> probe_convergence(int iterations);  // iterations x 8
+  // Product options (no reference counterpart), include/vrod_capi.h vrod_solver_set_option:
+  //  "state_prefetch"        1: every step also packs the state and copies it to pinned host
+  //                          memory (a side branch of the step graph), so get_state after a step
+  //                          costs no extra synchronisation; 0 (default): get_state copies on demand
+  //  "exact_shape_matching"  1: the exact-order shape-matching path (bitwise equal to the
+  //                          reference); 0: the latency-tuned one. Default: VROD_SHAPE_EXACT
+  //  "phase_timing"          1: step() launches its kernels directly with CUDA events between the
+  //                          reference's phases and fills Report::{predict,broad,narrow,solve,
+  //                          finalize}_ms; 0 (default): one CUDA graph per step, phases unmeasured
+  // Returns false for an unknown name.
+  bool set_option(const std::string& name, long long value);
 
   int rod_count() const { return setup_.R; }
   int total_vertices() const { return setup_.V; }
@@ -98,12 +112,15 @@ class Solver {
     std::vector<int> cat;
     std::vector<cudaEvent_t> ev;  // pairs
     std::vector<int> launches;
+    std::vector<cudaEvent_t> broad_end;  // per CAT_COLLIDE bracket: end of the broad phase
   };
+  bool phase_timing_ = false;
   void upload_static();
   void fill_animation(int substeps, double h);
   void record_step(double h, int substeps, int iterations, double* probe_log, Prof* prof = nullptr);
   void ensure_graph();
   void finish_step(double h, int substeps, Report* out);
+  void phase_times(Prof& prof, Report* r);
   void* flush_buf_ = nullptr;
   long long flush_bytes_ = 0;
   void check_error();
@@ -171,9 +188,9 @@ class Solver {
   int* d_scene_sing_ = nullptr;
   vdev::SceneAcc* h_scene_acc_ = nullptr;  // pinned, n_scenes_ (batch only)
   Report last_report_;
-  // get_state: the outputs packed on the device and copied into a pinned buffer. Once get_state
-  // has been called, step() enqueues that pack + copy behind the step (one synchronisation for
-  // both); any other state-changing call invalidates the copy.
+  // get_state: the outputs packed on the device and copied into a pinned buffer. With the
+  // "state_prefetch" option on, step() enqueues that pack + copy behind the step (one
+  // synchronisation for both); any other state-changing call invalidates the copy.
   double* d_pack_ = nullptr;
   double* h_pack_ = nullptr;
   bool prefetch_state_ = false, pack_fresh_ = false;

@@ -109,6 +109,11 @@ class SolverHandle:
     def backend(self) -> str:
         return self._lib.vrod_backend_name().decode()
 
+    # -- product options (vrod_solver_set_option) ----------------------------------------------
+    def set_option(self, name: str, value: int | bool) -> None:
+        """"state_prefetch", "exact_shape_matching" or "phase_timing" (include/vrod_capi.h)."""
+        check(self._lib, self._lib.vrod_solver_set_option(self._h, name.encode(), int(value)))
+
     # -- stepping -------------------------------------------------------------------------------
     def step(self) -> StepReport:
         """Solver::step(), solver.cpp:363-388."""

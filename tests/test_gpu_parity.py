@@ -374,3 +374,37 @@ def test_large_world_tiles_bitwise(gpu, oracle):
     cg, co = g.contacts(), o.contacts()
     for k in cg:
         np.testing.assert_array_equal(cg[k], co[k], err_msg=k)
+
+
+def test_solver_options(gpu, oracle):
+    """vrod_solver_set_option: phase timing (direct launches + events, StepReport PhaseTimings of
+    solver.h:14-21) and state prefetch change no result bit; exact shape matching can be switched
+    on at run time; unknown names are rejected."""
+    from paper_1906_05260_b200.scene import InvalidArgument
+    scene = SCENES["kitchen_sink"](oracle)
+    a, b = SolverHandle(gpu, scene), SolverHandle(gpu, scene)
+    b.set_option("phase_timing", 1)
+    b.set_option("state_prefetch", 1)
+    for _ in range(3):
+        ra, rb = a.step(), b.step()
+        assert (ra.contact_count, ra.broad_pairs, ra.max_penetration) == (rb.contact_count, rb.broad_pairs,
+                                                                          rb.max_penetration)
+        np.testing.assert_array_equal(ra.residuals, rb.residuals)
+        sa, sb = a.state(), b.state()
+        for k in sa:
+            np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
+        for k in ("predict_ms", "broad_ms", "narrow_ms", "solve_ms", "finalize_ms"):
+            assert rb.timings[k] > 0.0, (k, rb.timings)
+            assert ra.timings[k] == 0.0
+        assert sum(rb.timings[k] for k in ("predict_ms", "broad_ms", "narrow_ms", "solve_ms", "finalize_ms")) \
+            <= rb.timings["total_ms"]
+    with pytest.raises(InvalidArgument, match="unknown solver option"):
+        a.set_option("no_such_option", 1)
+    c, o = SolverHandle(gpu, SCENES["band"](oracle)), SolverHandle(oracle, SCENES["band"](oracle))
+    c.set_option("exact_shape_matching", 1)
+    for _ in range(3):
+        c.step()
+        o.step()
+    sc, so = c.state(), o.state()
+    for k in sc:
+        np.testing.assert_array_equal(sc[k], so[k], err_msg=k)
