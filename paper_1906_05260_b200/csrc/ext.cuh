@@ -56,6 +56,7 @@ __device__ __forceinline__ ExtGeom resolve_rec(const double* xrec, const Collide
 // kExtCenter | kExtScale.
 struct ExtResult {
   double lam[3];
+  double rec[4];  // the block's record for Collide::ext_rec (see there)
   int nlam;
   int owner;  // endpoint whose entry commits the block (lowest existing endpoint)
   bool singular, bad;
@@ -85,6 +86,7 @@ __device__ __forceinline__ ExtResult ext_block(const World& w, const Collide& c,
   ExtResult r;
   r.singular = r.bad = false;
   r.owner = 0;
+  r.rec[0] = r.rec[1] = r.rec[2] = r.rec[3] = ext_none();
   const int npins = sp.n_pins;
   const int vp = w.vpad;
   const double h2 = sp.h2;
@@ -124,6 +126,7 @@ __device__ __forceinline__ ExtResult ext_block(const World& w, const Collide& c,
         r.lam[d] = r.lam[d] + dl[d];
         o[d] = f * dl[d];
         finite = finite && isfinite(dl[d]) && isfinite(o[d]);
+        r.rec[d] = o[d];
       }
       emit(0, kExtCenter, o[0], o[1], o[2], 0.0);
     }
@@ -184,6 +187,12 @@ __device__ __forceinline__ ExtResult ext_block(const World& w, const Collide& c,
         active = true;
         r.lam[0] = r.lam[0] + dl;
         finite = isfinite(dl);
+        if (live) {
+          r.rec[0] = nrm.x;
+          r.rec[1] = nrm.y;
+          r.rec[2] = nrm.z;
+          r.rec[3] = dl;
+        }
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           if (!has[e]) continue;
@@ -233,6 +242,10 @@ __device__ __forceinline__ ExtResult ext_block(const World& w, const Collide& c,
         const double ox = fc * (n3.x * dl), oy = fc * (n3.y * dl), oz = fc * (n3.z * dl);
         const double os = -h2 * is * (-rbar * dl);
         finite = isfinite(dl) && isfinite(ox) && isfinite(oy) && isfinite(oz) && isfinite(os);
+        r.rec[0] = ox;
+        r.rec[1] = oy;
+        r.rec[2] = oz;
+        r.rec[3] = os;
         emit(0, kExtCenter | kExtScale, ox, oy, oz, os);
       }
     }
@@ -240,6 +253,21 @@ __device__ __forceinline__ ExtResult ext_block(const World& w, const Collide& c,
   }
   r.bad = active && !finite;
   return r;
+}
+
+// Endpoint e's correction of a contact from its block record {n xyz, dl} (Collide::ext_rec): the
+// expressions of ext_block's emission loop above, operand for operand, with the endpoint slot's
+// own inverse weights and rest radius and the contact's alpha (e < 2) or beta (e >= 2).
+__device__ __forceinline__ void contact_endpoint(int e, double ab, double nx, double ny, double nz, double dl, double h2,
+                                                 double ic, double is, double rb, double (&o)[3], double& os) {
+  const double coef = e == 0 ? 1.0 - ab : e == 1 ? ab : e == 2 ? -(1.0 - ab) : -ab;  // coef[e]
+  const double sj = (e < 2 ? -coef : coef) * rb;                                      // sj[e]
+  const double jx = coef * nx, jy = coef * ny, jz = coef * nz;
+  const double fc = -h2 * ic;
+  o[0] = fc * (jx * dl);
+  o[1] = fc * (jy * dl);
+  o[2] = fc * (jz * dl);
+  os = -h2 * is * (sj * dl);
 }
 
 // Scene of external block b (batch only).

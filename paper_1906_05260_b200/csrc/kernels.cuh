@@ -108,6 +108,12 @@ struct Collide {
   // Results are written per incidence entry q (slot-sorted), so the sweep's gather reads
   // contiguous entries instead of chasing block ids.
   double* ext_contrib = nullptr; // 4 x (4 x ext_cap): entry q -> dc xyz, ds (kExtNone markers)
+  // Per external block b, 4 doubles (k_ext_solve -> the per-launch sweeps' gathers): pin
+  // {dc xyz, none}, half-plane {dc xyz, ds}, contact {unit normal xyz, dlambda}; kExtNone in
+  // [0] (pin, half-plane) or [3] (contact) = no update. A contact's four endpoint corrections are
+  // re-formed by each endpoint's gather from these (ext.cuh contact_endpoint), 32 B per contact
+  // instead of 4 x 32 B of per-endpoint entries.
+  double* ext_rec = nullptr;
   int* ext_pos = nullptr;        // 4 x ext_cap: (block << 2 | endpoint) -> entry q
   int* ext_cnt = nullptr;        // V+1 incidence counts
   int* ext_off = nullptr;        // V+1

@@ -15,6 +15,7 @@
 // snapshot semantics, test_sweep.cpp:132-142).
 #include <cstdlib>
 
+#include "blocks.cuh"
 #include "ext.cuh"
 #include "kernels.cuh"
 #include "shape.cuh"
@@ -278,176 +279,67 @@ __device__ __forceinline__ void solve_items(Tile<TP>& t, const World& w, const S
     auto fail = [&](int local) { bad = umin64(bad, err_code(sp.substep, ERR_SWEEP, sp.iter, t.bbase[pi] + local)); };
     const int ne = __popc(ek), nv = __popc(vk);
 
-    if (k < m && kind < A_BT) {  // element pass of element k (constraints.cpp:302-314)
+    if (k < m && kind < A_BT) {  // element pass of element k (constraints.cpp:302-314), blocks.cuh
       const V3 c0{t.st[T_CX][si], t.st[T_CY][si], t.st[T_CZ][si]}, c1{t.st[T_CX][si + 1], t.st[T_CY][si + 1], t.st[T_CZ][si + 1]};
       const double s0 = t.st[T_S][si], s1 = t.st[T_S][si + 1];
       const double ic0 = t.st[T_IC][si], ic1 = t.st[T_IC][si + 1], is0 = t.st[T_IS][si], is1 = t.st[T_IS][si + 1];
       const V3 it{t.st[T_ITX][si], t.st[T_ITY][si], t.st[T_ITZ][si]};
+      const Q4 q{t.st[T_QW][si], t.st[T_QX][si], t.st[T_QY][si], t.st[T_QZ][si]};
       const int lbase = k * ne;
       if (kind == A_SZ && (ek & EK_SZ)) {  // StretchZ (:106-119), dim 3
-        const M3 Rm = qmat(Q4{t.st[T_QW][si], t.st[T_QX][si], t.st[T_QY][si], t.st[T_QZ][si]});
-        const double tbar = t.st[T_TDOT][si];
-        const double l = t.st[T_LEN][si];
-        const double inv_l = 1.0 / l;
-        const V3 dzc = (c1 - c0) / l;
-        const V3 wv = col(Rm, 2);
-        const double W[3] = {dzc.x - tbar * wv.x, dzc.y - tbar * wv.y, dzc.z - tbar * wv.z};
-        const double J0[3] = {tbar * Rm.m[0][1], tbar * Rm.m[1][1], tbar * Rm.m[2][1]};
-        const double J1[3] = {-tbar * Rm.m[0][0], -tbar * Rm.m[1][0], -tbar * Rm.m[2][0]};
-        double M[3][3];
-        double cd = 0.0;
-        if (ic0 != 0.0) cd = cd + (h2 * ic0 * inv_l) * inv_l;
-        if (ic1 != 0.0) cd = cd + (h2 * ic1 * inv_l) * inv_l;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          const double b0 = (h2 * J0[a]) * it.x, b1 = (h2 * J1[a]) * it.y;
-#pragma unroll
-          for (int b = 0; b < 3; ++b) M[a][b] = (a == b ? cd : 0.0) + (b0 * J0[b] + b1 * J1[b]);
-        }
-        const double kinv = t.st[T_KSZ][si];
-        double rhs[3], dl[3];
         const double lam[3] = {t.st[T_LAM + L_SZ0][si], t.st[T_LAM + L_SZ1][si], t.st[T_LAM + L_SZ2][si]};
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          M[d][d] = M[d][d] + kinv;
-          rhs[d] = W[d] - kinv * lam[d];
-        }
-        if (solve3(M, rhs, beta, dl)) {
-          const double f0 = -h2 * ic0, f1 = -h2 * ic1;
-          bool ok = true;
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            R.sz_dc0[d] = f0 * (-inv_l * dl[d]);
-            R.sz_dc1[d] = f1 * (inv_l * dl[d]);
-            ok = ok && isfinite(dl[d]) && isfinite(R.sz_dc0[d]) && isfinite(R.sz_dc1[d]);
-          }
-          const double jt0 = (J0[0] * dl[0] + J0[1] * dl[1]) + J0[2] * dl[2];
-          const double jt1 = (J1[0] * dl[0] + J1[1] * dl[1]) + J1[2] * dl[2];
-          R.sz_dt[0] = -h2 * (it.x * jt0);
-          R.sz_dt[1] = -h2 * (it.y * jt1);
-          R.sz_dt[2] = 0.0;
+        double ln[3];
+        bool ok = true;
+        if (blk::stretch_z(c0, c1, ic0, ic1, it, q, t.st[T_TDOT][si], t.st[T_LEN][si], t.st[T_KSZ][si], lam, h2, beta,
+                           R.sz_dc0, R.sz_dc1, R.sz_dt, ln, ok)) {
           t.act[A_SZ][pi] = 1;
-          put_lam(L_SZ0, lam[0] + dl[0]);
-          put_lam(L_SZ1, lam[1] + dl[1]);
-          put_lam(L_SZ2, lam[2] + dl[2]);
-          if (owned) {
-            if (!(ok && isfinite(R.sz_dt[0]) && isfinite(R.sz_dt[1]))) fail(lbase + __popc(ek & (EK_SZ - 1)));
-          }
+          put_lam(L_SZ0, ln[0]);
+          put_lam(L_SZ1, ln[1]);
+          put_lam(L_SZ2, ln[2]);
+          if (owned && !ok) fail(lbase + __popc(ek & (EK_SZ - 1)));
         } else {
           sing();
           keep_lam(L_SZ0, 3);
         }
       }
       if (kind == A_CS && (ek & EK_CS)) {  // CrossSection (:120-129), dim 1
-        const double W = 0.5 * (s0 + s1) - 0.5 * (t.st[T_SBAR][si] + t.st[T_SBAR][si + 1]);
-        double M = 0.0;
-        if (is0 != 0.0) M = M + (h2 * is0 * 0.5) * 0.5;
-        if (is1 != 0.0) M = M + (h2 * is1 * 0.5) * 0.5;
-        const double kinv = t.st[T_KCS][si];
-        const double lam = t.st[T_LAM + L_CS][si];
-        M = M + kinv;
-        if (M > 1e-250) {
-          const double dl = beta * (W - kinv * lam) / M;
-          R.cs[0] = -h2 * is0 * (0.5 * dl);
-          R.cs[1] = -h2 * is1 * (0.5 * dl);
+        double ln;
+        bool ok = true;
+        if (blk::cross_section(s0, s1, t.st[T_SBAR][si], t.st[T_SBAR][si + 1], is0, is1, t.st[T_KCS][si],
+                               t.st[T_LAM + L_CS][si], h2, beta, R.cs, ln, ok)) {
           t.act[A_CS][pi] = 1;
-          put_lam(L_CS, lam + dl);
-          if (owned) {
-            if (!(isfinite(dl) && isfinite(R.cs[0]) && isfinite(R.cs[1]))) fail(lbase + __popc(ek & (EK_CS - 1)));
-          }
+          put_lam(L_CS, ln);
+          if (owned && !ok) fail(lbase + __popc(ek & (EK_CS - 1)));
         } else {
           sing();
           keep_lam(L_CS, 1);
         }
       }
       if (kind == A_SS && (ek & EK_SS)) {  // SurfaceStretch (:130-138), dim 1
-        const double l = t.st[T_LEN][si];
-        const double W = (s1 - s0) / l - t.st[T_SGRAD][si];
-        const double j0 = -1.0 / l, j1 = 1.0 / l;
-        double M = 0.0;
-        if (is0 != 0.0) M = M + (h2 * is0 * j0) * j0;
-        if (is1 != 0.0) M = M + (h2 * is1 * j1) * j1;
-        const double kinv = t.st[T_KSS][si];
-        const double lam = t.st[T_LAM + L_SS][si];
-        M = M + kinv;
-        if (M > 1e-250) {
-          const double dl = beta * (W - kinv * lam) / M;
-          R.ss[0] = -h2 * is0 * (j0 * dl);
-          R.ss[1] = -h2 * is1 * (j1 * dl);
+        double ln;
+        bool ok = true;
+        if (blk::surface_stretch(s0, s1, t.st[T_LEN][si], t.st[T_SGRAD][si], is0, is1, t.st[T_KSS][si],
+                                 t.st[T_LAM + L_SS][si], h2, beta, R.ss, ln, ok)) {
           t.act[A_SS][pi] = 1;
-          put_lam(L_SS, lam + dl);
-          if (owned) {
-            if (!(isfinite(dl) && isfinite(R.ss[0]) && isfinite(R.ss[1]))) fail(lbase + __popc(ek & (EK_SS - 1)));
-          }
+          put_lam(L_SS, ln);
+          if (owned && !ok) fail(lbase + __popc(ek & (EK_SS - 1)));
         } else {
           sing();
           keep_lam(L_SS, 1);
         }
       }
       if (kind == A_VS && (ek & EK_VS)) {  // VolumeStretch (:169-188), dim 3
-        const M3 Rm = qmat(Q4{t.st[T_QW][si], t.st[T_QX][si], t.st[T_QY][si], t.st[T_QZ][si]});
-        const double tbar = t.st[T_TDOT][si];
-        const double l0 = t.st[T_LEN0][si];
-        const double smid = 0.5 * (s0 + s1);
-        const double smr = 0.5 * (t.st[T_SBAR][si] + t.st[T_SBAR][si + 1]);
-        const V3 dzc = (c1 - c0) / l0;
-        const V3 wv = col(Rm, 2);
-        const double ka = smid * smid, kb = smr * smr * tbar;
-        const double W[3] = {ka * dzc.x - kb * wv.x, ka * dzc.y - kb * wv.y, ka * dzc.z - kb * wv.z};
-        const double jc = smid * smid / l0;
-        const double js[3] = {smid * dzc.x, smid * dzc.y, smid * dzc.z};
-        const double fac = -smr * smr * tbar;
-        const double J0[3] = {fac * -Rm.m[0][1], fac * -Rm.m[1][1], fac * -Rm.m[2][1]};
-        const double J1[3] = {fac * Rm.m[0][0], fac * Rm.m[1][0], fac * Rm.m[2][0]};
-        double M[3][3];
-        double cd = 0.0;
-        if (ic0 != 0.0) cd = cd + (h2 * ic0 * jc) * jc;
-        if (ic1 != 0.0) cd = cd + (h2 * ic1 * jc) * jc;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          const double sa0 = h2 * is0 * js[a], sa1 = h2 * is1 * js[a];
-          const double b0 = (h2 * J0[a]) * it.x, b1 = (h2 * J1[a]) * it.y;
-#pragma unroll
-          for (int b = 0; b < 3; ++b) {
-            double v = a == b ? cd : 0.0;
-            if (is0 != 0.0) v = v + sa0 * js[b];
-            if (is1 != 0.0) v = v + sa1 * js[b];
-            M[a][b] = v + (b0 * J0[b] + b1 * J1[b]);
-          }
-        }
-        const double kinv = t.st[T_KVS][si];
-        double rhs[3], dl[3];
         const double lam[3] = {t.st[T_LAM + L_VS0][si], t.st[T_LAM + L_VS1][si], t.st[T_LAM + L_VS2][si]};
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          M[d][d] = M[d][d] + kinv;
-          rhs[d] = W[d] - kinv * lam[d];
-        }
-        if (solve3(M, rhs, beta, dl)) {
-          const double f0 = -h2 * ic0, f1 = -h2 * ic1;
-          bool ok = true;
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            R.vs_dc0[d] = f0 * (-jc * dl[d]);
-            R.vs_dc1[d] = f1 * (jc * dl[d]);
-            ok = ok && isfinite(dl[d]) && isfinite(R.vs_dc0[d]) && isfinite(R.vs_dc1[d]);
-          }
-          const double jd = (js[0] * dl[0] + js[1] * dl[1]) + js[2] * dl[2];
-          R.vs_ds[0] = -h2 * is0 * jd;
-          R.vs_ds[1] = -h2 * is1 * jd;
-          const double jt0 = (J0[0] * dl[0] + J0[1] * dl[1]) + J0[2] * dl[2];
-          const double jt1 = (J1[0] * dl[0] + J1[1] * dl[1]) + J1[2] * dl[2];
-          R.vs_dt[0] = -h2 * (it.x * jt0);
-          R.vs_dt[1] = -h2 * (it.y * jt1);
-          R.vs_dt[2] = 0.0;
+        double ln[3];
+        bool ok = true;
+        if (blk::volume_stretch(c0, c1, s0, s1, t.st[T_SBAR][si], t.st[T_SBAR][si + 1], ic0, ic1, is0, is1, it, q,
+                                t.st[T_TDOT][si], t.st[T_LEN0][si], t.st[T_KVS][si], lam, h2, beta, R.vs_dc0, R.vs_dc1,
+                                R.vs_ds, R.vs_dt, ln, ok)) {
           t.act[A_VS][pi] = 1;
-          put_lam(L_VS0, lam[0] + dl[0]);
-          put_lam(L_VS1, lam[1] + dl[1]);
-          put_lam(L_VS2, lam[2] + dl[2]);
-          if (owned) {
-            if (!(ok && isfinite(R.vs_ds[0]) && isfinite(R.vs_ds[1]) && isfinite(R.vs_dt[0]) && isfinite(R.vs_dt[1])))
-              fail(lbase + __popc(ek & (EK_VS - 1)));
-          }
+          put_lam(L_VS0, ln[0]);
+          put_lam(L_VS1, ln[1]);
+          put_lam(L_VS2, ln[2]);
+          if (owned && !ok) fail(lbase + __popc(ek & (EK_VS - 1)));
         } else {
           sing();
           keep_lam(L_VS0, 3);
@@ -455,7 +347,7 @@ __device__ __forceinline__ void solve_items(Tile<TP>& t, const World& w, const S
       }
     }
 
-    if (k >= 1 && k <= m - 1 && kind >= A_BT) {  // vertex pass of vertex k (:315-327)
+    if (k >= 1 && k <= m - 1 && kind >= A_BT) {  // vertex pass of vertex k (:315-327), blocks.cuh
       const Q4 qa{t.st[T_QW][si - 1], t.st[T_QX][si - 1], t.st[T_QY][si - 1], t.st[T_QZ][si - 1]};
       const Q4 qb{t.st[T_QW][si], t.st[T_QX][si], t.st[T_QY][si], t.st[T_QZ][si]};
       const double sm = t.st[T_S][si - 1], s0 = t.st[T_S][si], spp = t.st[T_S][si + 1];
@@ -465,103 +357,32 @@ __device__ __forceinline__ void solve_items(Tile<TP>& t, const World& w, const S
       const double sbar = t.st[T_SBAR][si];
       const double la = t.st[T_LEN][si - 1], lb = t.st[T_LEN][si];
       const int lbase = m * ne + (k - 1) * nv;
-      Q4 pr{1, 0, 0, 0};
-      if (vk & (VK_BT | VK_VBU | VK_VBV)) pr = relative_rotation(qa, qb);
-      // 0.5*(-+p.w I + [p_v]x) (constraints.cpp:50-51)
-      const double Da[3][3] = {{0.5 * -pr.w, 0.5 * -pr.z, 0.5 * pr.y},
-                               {0.5 * pr.z, 0.5 * -pr.w, 0.5 * -pr.x},
-                               {0.5 * -pr.y, 0.5 * pr.x, 0.5 * -pr.w}};
-      const double Db[3][3] = {{0.5 * pr.w, 0.5 * -pr.z, 0.5 * pr.y},
-                               {0.5 * pr.z, 0.5 * pr.w, 0.5 * -pr.x},
-                               {0.5 * -pr.y, 0.5 * pr.x, 0.5 * pr.w}};
+      const blk::VertexFrame vf = blk::vertex_frame(qa, qb, (vk & (VK_BT | VK_VBU | VK_VBV)) != 0);
       if (kind == A_BT && (vk & VK_BT)) {  // BendTwist (:139-155), dim 3
-        const double inv_len = 4.0 / (la + lb);
-        const V3 om = inv_len * qvec(pr);
-        const double s = sp.classic ? sbar : s0;
         const V3 darb{t.st[T_DARBX][si - 1], t.st[T_DARBY][si - 1], t.st[T_DARBZ][si - 1]};
-        const double W[3] = {s * om.x - sbar * darb.x, s * om.y - sbar * darb.y, s * om.z - sbar * darb.z};
-        const double fs = s * inv_len;
-        double Ja[3][3], Jb[3][3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int b = 0; b < 3; ++b) {
-            Ja[a][b] = fs * Da[a][b];
-            Jb[a][b] = fs * Db[a][b];
-          }
-        const double omv[3] = {om.x, om.y, om.z};
-        const bool sc_on = !sp.classic && is0 != 0.0;
-        double M[3][3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          const double sa = h2 * is0 * omv[a];
-          const double ba0 = (h2 * Ja[a][0]) * ita.x, ba1 = (h2 * Ja[a][1]) * ita.y, ba2 = (h2 * Ja[a][2]) * ita.z;
-          const double bb0 = (h2 * Jb[a][0]) * itb.x, bb1 = (h2 * Jb[a][1]) * itb.y, bb2 = (h2 * Jb[a][2]) * itb.z;
-#pragma unroll
-          for (int b = 0; b < 3; ++b) {
-            double v = sc_on ? sa * omv[b] : 0.0;
-            v = v + ((ba0 * Ja[b][0] + ba1 * Ja[b][1]) + ba2 * Ja[b][2]);
-            v = v + ((bb0 * Jb[b][0] + bb1 * Jb[b][1]) + bb2 * Jb[b][2]);
-            M[a][b] = v;
-          }
-        }
-        const double kinv[3] = {t.st[T_KBT0][si], t.st[T_KBT0][si],
-                                t.st[T_KBT2][si]};
         const double lam[3] = {t.st[T_LAM + L_BT0][si], t.st[T_LAM + L_BT1][si], t.st[T_LAM + L_BT2][si]};
-        double rhs[3], dl[3];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          M[d][d] = M[d][d] + kinv[d];
-          rhs[d] = W[d] - kinv[d] * lam[d];
-        }
-        if (solve3(M, rhs, beta, dl)) {
-          bool ok = isfinite(dl[0]) && isfinite(dl[1]) && isfinite(dl[2]);
-          R.bt_ds = 0.0;
-          if (!sp.classic) {
-            R.bt_ds = -h2 * is0 * ((omv[0] * dl[0] + omv[1] * dl[1]) + omv[2] * dl[2]);
-            ok = ok && isfinite(R.bt_ds);
-          }
-#pragma unroll
-          for (int b = 0; b < 3; ++b) {
-            R.bt_dta[b] = -h2 * (comp(ita, b) * ((Ja[0][b] * dl[0] + Ja[1][b] * dl[1]) + Ja[2][b] * dl[2]));
-            R.bt_dtb[b] = -h2 * (comp(itb, b) * ((Jb[0][b] * dl[0] + Jb[1][b] * dl[1]) + Jb[2][b] * dl[2]));
-            ok = ok && isfinite(R.bt_dta[b]) && isfinite(R.bt_dtb[b]);
-          }
+        double ln[3];
+        bool ok = true;
+        if (blk::bend_twist(vf, s0, sbar, is0, ita, itb, la, lb, darb, t.st[T_KBT0][si], t.st[T_KBT2][si], lam,
+                            sp.classic, h2, beta, R.bt_ds, R.bt_dta, R.bt_dtb, ln, ok)) {
           t.act[A_BT][pi] = 1;
-          put_lam(L_BT0, lam[0] + dl[0]);
-          put_lam(L_BT1, lam[1] + dl[1]);
-          put_lam(L_BT2, lam[2] + dl[2]);
-          if (owned) {
-            if (!ok) fail(lbase + __popc(vk & (VK_BT - 1)));
-          }
+          put_lam(L_BT0, ln[0]);
+          put_lam(L_BT1, ln[1]);
+          put_lam(L_BT2, ln[2]);
+          if (owned && !ok) fail(lbase + __popc(vk & (VK_BT - 1)));
         } else {
           sing();
           keep_lam(L_BT0, 3);
         }
       }
       if (kind == A_SB && (vk & VK_SB)) {  // SurfaceBending (:156-168), dim 1
-        const double lap = (spp - s0) / lb - (s0 - sm) / la;
-        const double W = lap - t.st[T_SLAP][si - 1];
-        const double jm = 1.0 / la, j0 = -1.0 / la - 1.0 / lb, jp = 1.0 / lb;
-        const double ism = t.st[T_IS][si - 1], isp = t.st[T_IS][si + 1];
-        double M = 0.0;
-        if (ism != 0.0) M = M + (h2 * ism * jm) * jm;
-        if (is0 != 0.0) M = M + (h2 * is0 * j0) * j0;
-        if (isp != 0.0) M = M + (h2 * isp * jp) * jp;
-        const double kinv = t.st[T_KSB][si];
-        const double lam = t.st[T_LAM + L_SB][si];
-        M = M + kinv;
-        if (M > 1e-250) {
-          const double dl = beta * (W - kinv * lam) / M;
-          R.sb[0] = -h2 * ism * (jm * dl);
-          R.sb[1] = -h2 * is0 * (j0 * dl);
-          R.sb[2] = -h2 * isp * (jp * dl);
+        double ln;
+        bool ok = true;
+        if (blk::surface_bending(sm, s0, spp, la, lb, t.st[T_SLAP][si - 1], t.st[T_IS][si - 1], is0,
+                                 t.st[T_IS][si + 1], t.st[T_KSB][si], t.st[T_LAM + L_SB][si], h2, beta, R.sb, ln, ok)) {
           t.act[A_SB][pi] = 1;
-          put_lam(L_SB, lam + dl);
-          if (owned) {
-            if (!(isfinite(dl) && isfinite(R.sb[0]) && isfinite(R.sb[1]) && isfinite(R.sb[2])))
-              fail(lbase + __popc(vk & (VK_SB - 1)));
-          }
+          put_lam(L_SB, ln);
+          if (owned && !ok) fail(lbase + __popc(vk & (VK_SB - 1)));
         } else {
           sing();
           keep_lam(L_SB, 1);
@@ -572,40 +393,15 @@ __device__ __forceinline__ void solve_items(Tile<TP>& t, const World& w, const S
         for (int cc = 0; cc < 2; ++cc) {
           const int bit = cc == 0 ? VK_VBU : VK_VBV;
           if (kind != A_VBU + cc || !(vk & bit)) continue;
-          const double la0 = t.st[T_LEN0][si - 1], lb0 = t.st[T_LEN0][si];
-          const double inv_len0 = 4.0 / (la0 + lb0);
-          const double om = inv_len0 * (cc == 0 ? pr.x : pr.y);
-          const double darb = t.st[cc == 0 ? T_DARBX : T_DARBY][si - 1];
-          const double rest_om = darb * (la + lb) / (la0 + lb0);
-          const double s = s0;
-          const double W = s * s * s * om - sbar * sbar * sbar * rest_om;
-          const double js = 3.0 * s * s * om;
-          const double fs = s * s * s * inv_len0;
-          const double ja[3] = {fs * Da[cc][0], fs * Da[cc][1], fs * Da[cc][2]};
-          const double jb[3] = {fs * Db[cc][0], fs * Db[cc][1], fs * Db[cc][2]};
-          double M = 0.0;
-          if (is0 != 0.0) M = M + (h2 * is0 * js) * js;
-          M = M + (((h2 * ja[0]) * ita.x * ja[0] + (h2 * ja[1]) * ita.y * ja[1]) + (h2 * ja[2]) * ita.z * ja[2]);
-          M = M + (((h2 * jb[0]) * itb.x * jb[0] + (h2 * jb[1]) * itb.y * jb[1]) + (h2 * jb[2]) * itb.z * jb[2]);
-          const double kinv = t.st[T_KVB][si];
           const int lf = cc == 0 ? L_VBU : L_VBV;
-          const double lam = t.st[T_LAM + lf][si];
-          M = M + kinv;
-          if (M > 1e-250) {
-            const double dl = beta * (W - kinv * lam) / M;
-            R.vb_ds[cc] = -h2 * is0 * (js * dl);
-            bool ok = isfinite(dl) && isfinite(R.vb_ds[cc]);
-#pragma unroll
-            for (int b = 0; b < 3; ++b) {
-              R.vb_dta[cc][b] = -h2 * (comp(ita, b) * (ja[b] * dl));
-              R.vb_dtb[cc][b] = -h2 * (comp(itb, b) * (jb[b] * dl));
-              ok = ok && isfinite(R.vb_dta[cc][b]) && isfinite(R.vb_dtb[cc][b]);
-            }
+          double ln;
+          bool ok = true;
+          if (blk::volume_bend(cc, vf, s0, sbar, is0, ita, itb, la, lb, t.st[T_LEN0][si - 1], t.st[T_LEN0][si],
+                               t.st[cc == 0 ? T_DARBX : T_DARBY][si - 1], t.st[T_KVB][si], t.st[T_LAM + lf][si], h2,
+                               beta, R.vb_ds[cc], R.vb_dta[cc], R.vb_dtb[cc], ln, ok)) {
             t.act[cc == 0 ? A_VBU : A_VBV][pi] = 1;
-            put_lam(lf, lam + dl);
-            if (owned) {
-              if (!ok) fail(lbase + __popc(vk & (bit - 1)));
-            }
+            put_lam(lf, ln);
+            if (owned && !ok) fail(lbase + __popc(vk & (bit - 1)));
           } else {
             sing();
             keep_lam(lf, 1);
@@ -732,7 +528,7 @@ __device__ __forceinline__ void gather_apply(const Tile<TP>& t, const World& w, 
       V3 cn{t.st[T_CX][si], t.st[T_CY][si], t.st[T_CZ][si]};
       if (ccnt > 0) cn = cn + csum / static_cast<double>(ccnt);
       double sn = t.st[T_S][si];
-      if (scnt > 0) sn = fmax(sn + ssum / static_cast<double>(scnt), kMinScale);
+      if (scnt > 0) sn = fmax(sn + qdiv(ssum, static_cast<double>(scnt)), kMinScale);
       Y[CX * (long long)vp + p] = cn.x;
       Y[CY * (long long)vp + p] = cn.y;
       Y[CZ * (long long)vp + p] = cn.z;
@@ -784,6 +580,54 @@ __device__ __forceinline__ void gather_entries(const Collide& c, int e0, int e1,
   }
 }
 
+// The external blocks touching slot p (incidence entries [e0, e1), block order) from the blocks'
+// records (Collide::ext_rec, written by k_ext_solve): pins and half-planes carry their single
+// endpoint's correction, contacts their normal and dlambda, from which the endpoint's correction
+// is re-formed exactly as ext_block forms it (contact_endpoint). Chunks of 4 entries: all loads
+// of a chunk are issued before the first add. ic, is, rb: the slot's inverse weights and rest
+// radius.
+template <class AddC, class AddS>
+__device__ __forceinline__ void gather_recs(const Collide& c, int e0, int e1, int npins, int nct, double h2, double ic,
+                                            double is, double rb, AddC& addc, AddS& adds) {
+  for (int q0 = e0; q0 < e1; q0 += 4) {
+    int it[4];
+    double2 r01[4], r23[4];
+    double ab[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) it[u] = c.ext_items[q0 + u < e1 ? q0 + u : e0];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int b = it[u] >> 2, e = it[u] & 3;
+      const double2* rr = reinterpret_cast<const double2*>(c.ext_rec + 4ll * b);
+      r01[u] = rr[0];
+      r23[u] = rr[1];
+      const int k = b - npins;
+      ab[u] = (k >= 0 && k < nct) ? (e < 2 ? c.ct_alpha[k] : c.ct_beta[k]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (q0 + u >= e1) continue;
+      const int b = it[u] >> 2, e = it[u] & 3;
+      if (b < npins) {  // soft pin: center only
+        if (is_ext_none(r01[u].x)) continue;
+        const double d[3] = {r01[u].x, r01[u].y, r23[u].x};
+        addc(d);
+      } else if (b < npins + nct) {  // contact
+        if (is_ext_none(r23[u].y)) continue;
+        double o[3], os;
+        contact_endpoint(e, ab[u], r01[u].x, r01[u].y, r23[u].x, r23[u].y, h2, ic, is, rb, o, os);
+        addc(o);
+        adds(os);
+      } else {  // half-plane
+        if (is_ext_none(r01[u].x)) continue;
+        const double d[3] = {r01[u].x, r01[u].y, r23[u].x};
+        addc(d);
+        adds(r23[u].y);
+      }
+    }
+  }
+}
+
 // Writes an endpoint's correction into its incidence entry o (4 doubles; flag 0 = no update from
 // the block; kExtNone in ds = no scale update).
 __device__ __forceinline__ void put_entry(double* out, int flag, double x, double y, double z, double ds) {
@@ -831,10 +675,10 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 32 ? 2 : 4) k_rod_
     pdl_wait();
     pdl_trigger();
   }
-  if (kEarlyWait && has_ext) {
+  if (kEarlyWait && has_ext) {  // the tile's incidence items, for the gather after the block solves
     const int e0 = c.ext_off[max(start, 0)], e1 = c.ext_off[min(start + kTileOwned, V)];
-    const char* lo = reinterpret_cast<const char*>(c.ext_contrib + 4ll * e0);
-    const char* hi = reinterpret_cast<const char*>(c.ext_contrib + 4ll * e1);
+    const char* lo = reinterpret_cast<const char*>(c.ext_items + e0);
+    const char* hi = reinterpret_cast<const char*>(c.ext_items + e1);
     for (const char* a = lo + 128ll * tid; a < hi; a += 128ll * 32 * kWarps)
       asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a));
   }
@@ -850,8 +694,14 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 32 ? 2 : 4) k_rod_
     pdl_wait();
     pdl_trigger();
   }
+  const int nct = has_ext ? c.scalars[SC_NCT] : 0;
   gather_apply(t, w, sp, start, Y, has_ext ? w.xrec : nullptr, [&](int p, auto& addc, auto& adds) {
-    if (has_ext) gather_entries(c, c.ext_off[p], c.ext_off[p + 1], addc, adds);
+    if (!has_ext) return;
+    const int e0 = c.ext_off[p], e1 = c.ext_off[p + 1];
+    if (e0 == e1) return;
+    const int si = p - start + 2;
+    gather_recs(c, e0, e1, sp.n_pins, nct, sp.h2, t.st[T_IC][si], t.st[T_IS][si], w.vstat[RBAR * (long long)w.vpad + p],
+                addc, adds);
   });
 }
 
@@ -1117,6 +967,367 @@ __global__ void __launch_bounds__(32 * (warps_for<TP>() + 1), 1) k_iterate(World
   }
 }
 
+// ---- warp-per-rod sweep (every rod <= 32 vertices: C4, C5) -----------------------------------
+// One warp per rod, lane k = the rod's slot k (vertex k, element k). Each lane loads its slot's
+// snapshot, static rows and multipliers straight into registers (coalesced rows), takes what its
+// blocks need from the neighbouring lanes by shuffle, solves the element-pass blocks of element k
+// and the vertex-pass blocks of vertex k (blocks.cuh: the tile sweep's arithmetic, so the same
+// bits), and gathers in the reference's block order (constraints.cpp:509-534): element k-1's and
+// element k's results, then vertex k-1's, k's and k+1's — the neighbours' by shuffle — then the
+// external blocks through the incidence list. No shared memory, no halo recomputation, no
+// block barrier; a lane owns its slot's multipliers, so they are updated in place.
+constexpr int kWarpRodsPerCta = 4;
+
+__device__ __forceinline__ double shup(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ double shdn(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ int shup_i(int v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ int shdn_i(int v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+
+template <int kMinBlocks>
+__global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_warp(World w, Collide c, const double* __restrict__ X,
+                                                                      double* __restrict__ Y, SweepParams sp,
+                                                                      int* singular, unsigned long long* err,
+                                                                      int has_ext) {
+  if (sp.pdl == 1) {  // predecessor wrote X: wait before loading
+    pdl_wait();
+    pdl_trigger();
+  }
+  const int r = blockIdx.x * kWarpRodsPerCta + (threadIdx.x >> 5);
+  if (r >= w.R) return;  // whole warps only
+  const int k = threadIdx.x & 31;
+  const int n = w.rod_n[r], m = n - 1, vb = w.rod_vbase[r];
+  const int ek = w.rod_ekinds[r], vk = w.rod_vkinds[r], bb = w.rod_block_base[r];
+  const int ne = __popc(ek), nv = __popc(vk);
+  const bool valid = k < n;
+  const long long vp = w.vpad;
+  const int p = vb + (valid ? k : 0);
+  const double h2 = sp.h2, beta = sp.beta;
+  auto ld = [&](const double* a, int f) { return valid ? a[f * vp + p] : 0.0; };
+  const double* L = sp.lam_in;
+  int nsing = 0;
+  unsigned long long bad = kNoError;
+  auto fail = [&](int local) { bad = umin64(bad, err_code(sp.substep, ERR_SWEEP, sp.iter, bb + local)); };
+  auto sing = [&]() {
+    ++nsing;
+    if (sp.scene_singular) atomicAdd(&sp.scene_singular[w.rod_scene[r]], 1);
+  };
+  auto put_lam = [&](int f, double v) { sp.lam_out[f * vp + p] = v; };
+  // The gather sums (constraints.cpp:509-534) are built as the blocks are solved, kind by kind,
+  // keeping the reference's order: the three accumulators are independent, and within each the
+  // terms go element k-1, element k, vertex k-1, vertex k, vertex k+1 — a term that must wait for
+  // a later one is held in a register meanwhile. So only a few results are alive at a time.
+  V3 csum{0, 0, 0}, tsum{0, 0, 0};
+  double ssum = 0.0;
+  int ccnt = 0, scnt = 0, tcnt = 0;
+  auto addc = [&](const double* d) {
+    csum = csum + V3{d[0], d[1], d[2]};
+    ++ccnt;
+  };
+  auto adds = [&](double d) {
+    ssum += d;
+    ++scnt;
+  };
+  auto addt = [&](const double* d) {
+    tsum = tsum + V3{d[0], d[1], d[2]};
+    ++tcnt;
+  };
+  const bool el = valid && k < m;         // element k exists
+  const bool pel = valid && k >= 1;       // element k-1 exists
+  // ---- this slot's snapshot ----
+  const V3 c0{ld(X, CX), ld(X, CY), ld(X, CZ)};
+  const double s0 = ld(X, S);
+  const Q4 q{ld(X, QW), ld(X, QX), ld(X, QY), ld(X, QZ)};
+  const double sbar = ld(w.vstat, SBAR), is0 = ld(w.vstat, IS);
+  const V3 it{ld(w.estat, ITX), ld(w.estat, ITY), ld(w.estat, ITZ)};
+  const double len = ld(w.estat, LEN);
+
+  // ---- element pass of element k (constraints.cpp:302-314) ----
+  double b_sz[3] = {0, 0, 0}, b_vs[3] = {0, 0, 0}, b_cs = 0.0, b_ss = 0.0, b_vsds = 0.0;  // element k's c0 / s0 terms
+  int bact = 0;
+  {
+    const double ic0 = ld(w.vstat, IC);
+    const V3 c1{shdn(c0.x), shdn(c0.y), shdn(c0.z)};
+    const double s1 = shdn(s0), ic1 = shdn(ic0), is1 = shdn(is0), sbar1 = shdn(sbar);
+    const int lbase = k * ne;
+    if (ek & EK_SZ) {  // StretchZ (:106-119)
+      double dc1[3] = {0, 0, 0}, dt[3];
+      int act = 0;
+      if (el) {
+        const double lam[3] = {ld(L, L_SZ0), ld(L, L_SZ1), ld(L, L_SZ2)};
+        double ln[3];
+        bool ok = true;
+        if (blk::stretch_z(c0, c1, ic0, ic1, it, q, ld(w.estat, TDOT), len, ld(w.estat, KSZ), lam, h2, beta, b_sz, dc1,
+                           dt, ln, ok)) {
+          act = 1;
+          put_lam(L_SZ0, ln[0]);
+          put_lam(L_SZ1, ln[1]);
+          put_lam(L_SZ2, ln[2]);
+          addt(dt);
+          if (!ok) fail(lbase + __popc(ek & (EK_SZ - 1)));
+        } else {
+          sing();
+          put_lam(L_SZ0, lam[0]);
+          put_lam(L_SZ1, lam[1]);
+          put_lam(L_SZ2, lam[2]);
+        }
+      }
+      bact |= act << A_SZ;
+      const double a[3] = {shup(dc1[0]), shup(dc1[1]), shup(dc1[2])};
+      const int pa = shup_i(act);
+      if (pel && pa) addc(a);
+    }
+    if (ek & EK_CS) {  // CrossSection (:120-129)
+      double ds[2] = {0, 0};
+      int act = 0;
+      if (el) {
+        const double lam = ld(L, L_CS);
+        double ln;
+        bool ok = true;
+        if (blk::cross_section(s0, s1, sbar, sbar1, is0, is1, ld(w.estat, KCS), lam, h2, beta, ds, ln, ok)) {
+          act = 1;
+          put_lam(L_CS, ln);
+          if (!ok) fail(lbase + __popc(ek & (EK_CS - 1)));
+        } else {
+          sing();
+          put_lam(L_CS, lam);
+        }
+      }
+      b_cs = ds[0];
+      bact |= act << A_CS;
+      const double a = shup(ds[1]);
+      const int pa = shup_i(act);
+      if (pel && pa) adds(a);
+    }
+    if (ek & EK_SS) {  // SurfaceStretch (:130-138)
+      double ds[2] = {0, 0};
+      int act = 0;
+      if (el) {
+        const double lam = ld(L, L_SS);
+        double ln;
+        bool ok = true;
+        if (blk::surface_stretch(s0, s1, len, ld(w.estat, SGRAD), is0, is1, ld(w.estat, KSS), lam, h2, beta, ds, ln,
+                                 ok)) {
+          act = 1;
+          put_lam(L_SS, ln);
+          if (!ok) fail(lbase + __popc(ek & (EK_SS - 1)));
+        } else {
+          sing();
+          put_lam(L_SS, lam);
+        }
+      }
+      b_ss = ds[0];
+      bact |= act << A_SS;
+      const double a = shup(ds[1]);
+      const int pa = shup_i(act);
+      if (pel && pa) adds(a);
+    }
+    if (ek & EK_VS) {  // VolumeStretch (:169-188)
+      double dc1[3] = {0, 0, 0}, ds[2] = {0, 0}, dt[3];
+      int act = 0;
+      if (el) {
+        const double lam[3] = {ld(L, L_VS0), ld(L, L_VS1), ld(L, L_VS2)};
+        double ln[3];
+        bool ok = true;
+        if (blk::volume_stretch(c0, c1, s0, s1, sbar, sbar1, ic0, ic1, is0, is1, it, q, ld(w.estat, TDOT),
+                                ld(w.estat, LEN0), ld(w.estat, KVS), lam, h2, beta, b_vs, dc1, ds, dt, ln, ok)) {
+          act = 1;
+          put_lam(L_VS0, ln[0]);
+          put_lam(L_VS1, ln[1]);
+          put_lam(L_VS2, ln[2]);
+          addt(dt);
+          if (!ok) fail(lbase + __popc(ek & (EK_VS - 1)));
+        } else {
+          sing();
+          put_lam(L_VS0, lam[0]);
+          put_lam(L_VS1, lam[1]);
+          put_lam(L_VS2, lam[2]);
+        }
+      }
+      b_vsds = ds[0];
+      bact |= act << A_VS;
+      const double a[3] = {shup(dc1[0]), shup(dc1[1]), shup(dc1[2])};
+      const double ads = shup(ds[1]);
+      const int pa = shup_i(act);
+      if (pel && pa) {
+        addc(a);
+        adds(ads);
+      }
+    }
+  }
+  // element k's own terms (c0 / s0 side) after all of element k-1's
+  if (el) {
+    if (bact & (1 << A_SZ)) addc(b_sz);
+    if (bact & (1 << A_CS)) adds(b_cs);
+    if (bact & (1 << A_SS)) adds(b_ss);
+    if (bact & (1 << A_VS)) {
+      addc(b_vs);
+      adds(b_vsds);
+    }
+  }
+
+  // ---- vertex pass of interior vertex k (constraints.cpp:315-327) ----
+  {
+    const bool vx = valid && k >= 1 && k <= m - 1;  // vertex k is interior
+    const bool nvx = valid && k + 1 <= m - 1;        // vertex k+1 is interior
+    const Q4 qa{shup(q.w), shup(q.x), shup(q.y), shup(q.z)};
+    const V3 ita{shup(it.x), shup(it.y), shup(it.z)};
+    const double la = shup(len);
+    const double lb = len;
+    const int lbase = m * ne + (k - 1) * nv;
+    const blk::VertexFrame vf = blk::vertex_frame(qa, q, (vk & (VK_BT | VK_VBU | VK_VBV)) != 0);
+    double bt_ds = 0.0;
+    int bt_act = 0;
+    double n_bta[3] = {0, 0, 0};
+    int n_bt = 0;
+    if (vk & VK_BT) {  // BendTwist (:139-155)
+      const V3 darb_a{shup(ld(w.estat, DARBX)), shup(ld(w.estat, DARBY)), shup(ld(w.estat, DARBZ))};
+      double dta[3] = {0, 0, 0}, dtb[3];
+      if (vx) {
+        const double lam[3] = {ld(L, L_BT0), ld(L, L_BT1), ld(L, L_BT2)};
+        double ln[3];
+        bool ok = true;
+        if (blk::bend_twist(vf, s0, sbar, is0, ita, it, la, lb, darb_a, ld(w.estat, KBT0), ld(w.estat, KBT2), lam,
+                            sp.classic, h2, beta, bt_ds, dta, dtb, ln, ok)) {
+          bt_act = 1;
+          put_lam(L_BT0, ln[0]);
+          put_lam(L_BT1, ln[1]);
+          put_lam(L_BT2, ln[2]);
+          addt(dtb);
+          if (!ok) fail(lbase + __popc(vk & (VK_BT - 1)));
+        } else {
+          sing();
+          put_lam(L_BT0, lam[0]);
+          put_lam(L_BT1, lam[1]);
+          put_lam(L_BT2, lam[2]);
+        }
+      }
+      n_bta[0] = shdn(dta[0]);
+      n_bta[1] = shdn(dta[1]);
+      n_bta[2] = shdn(dta[2]);
+      n_bt = shdn_i(bt_act);
+    }
+    double sb_mid = 0.0, n_sb0 = 0.0;
+    int sb_act = 0, n_sb = 0;
+    {
+      double a_sb2 = 0.0;
+      int p_sb = 0;
+      if (vk & VK_SB) {  // SurfaceBending (:156-168)
+        const double sm = shup(s0), ism = shup(is0), slap_a = shup(ld(w.estat, SLAP));
+        const double spp = shdn(s0), isp = shdn(is0);
+        double ds[3] = {0, 0, 0};
+        if (vx) {
+          const double lam = ld(L, L_SB);
+          double ln;
+          bool ok = true;
+          if (blk::surface_bending(sm, s0, spp, la, lb, slap_a, ism, is0, isp, ld(w.estat, KSB), lam, h2, beta, ds, ln,
+                                   ok)) {
+            sb_act = 1;
+            put_lam(L_SB, ln);
+            if (!ok) fail(lbase + __popc(vk & (VK_SB - 1)));
+          } else {
+            sing();
+            put_lam(L_SB, lam);
+          }
+        }
+        sb_mid = ds[1];
+        a_sb2 = shup(ds[2]);
+        p_sb = shup_i(sb_act);
+        n_sb0 = shdn(ds[0]);
+        n_sb = shdn_i(sb_act);
+      }
+      // scale terms: vertex k-1's s_{j+1}, then vertex k's (BendTwist, SurfaceBending; the volume
+      // bends follow below)
+      if (valid && k - 1 >= 1 && p_sb) adds(a_sb2);
+      if (vx && bt_act && !sp.classic) adds(bt_ds);
+      if (vx && sb_act) adds(sb_mid);
+    }
+    double n_vb[2][3] = {{0, 0, 0}, {0, 0, 0}};
+    int n_vba[2] = {0, 0};
+    if (vk & (VK_VBU | VK_VBV)) {  // VolumeBendU / V (:189-214)
+      const double la0 = shup(ld(w.estat, LEN0)), lb0 = ld(w.estat, LEN0);
+      const double dax = shup(ld(w.estat, DARBX)), day = shup(ld(w.estat, DARBY));
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const int bit = cc == 0 ? VK_VBU : VK_VBV;
+        if (!(vk & bit)) continue;
+        const int lf = cc == 0 ? L_VBU : L_VBV;
+        double ds = 0.0, dta[3] = {0, 0, 0}, dtb[3];
+        int act = 0;
+        if (vx) {
+          const double lam = ld(L, lf);
+          double ln;
+          bool ok = true;
+          if (blk::volume_bend(cc, vf, s0, sbar, is0, ita, it, la, lb, la0, lb0, cc == 0 ? dax : day,
+                               ld(w.estat, KVB), lam, h2, beta, ds, dta, dtb, ln, ok)) {
+            act = 1;
+            put_lam(lf, ln);
+            adds(ds);
+            addt(dtb);
+            if (!ok) fail(lbase + __popc(vk & (bit - 1)));
+          } else {
+            sing();
+            put_lam(lf, lam);
+          }
+        }
+        n_vb[cc][0] = shdn(dta[0]);
+        n_vb[cc][1] = shdn(dta[1]);
+        n_vb[cc][2] = shdn(dta[2]);
+        n_vba[cc] = shdn_i(act);
+      }
+    }
+    // vertex k+1's terms last
+    if (nvx) {
+      if (n_bt) addt(n_bta);
+      if (n_sb) adds(n_sb0);
+      if (n_vba[0]) addt(n_vb[0]);
+      if (n_vba[1]) addt(n_vb[1]);
+    }
+  }
+  // singular / error counts of this warp's blocks
+  if (__any_sync(0xffffffffu, nsing != 0 || bad != kNoError)) {
+    for (int o = 16; o > 0; o >>= 1) {
+      nsing += __shfl_down_sync(0xffffffffu, nsing, o);
+      bad = umin64(bad, __shfl_down_sync(0xffffffffu, bad, o));
+    }
+    if (k == 0) {
+      if (nsing) atomicAdd(singular, nsing);
+      if (bad != kNoError) atomicMin(err, bad);
+    }
+  }
+  // the ext solve of this iteration (the predecessor) writes the incidence entries and reads the
+  // slot records this sweep rewrites: wait for it only now
+  if (sp.pdl == 2) {
+    pdl_wait();
+    pdl_trigger();
+  }
+  if (!valid) return;
+  if (has_ext) {
+    const int e0 = c.ext_off[p], e1 = c.ext_off[p + 1];
+    if (e0 < e1)
+      gather_recs(c, e0, e1, sp.n_pins, c.scalars[SC_NCT], h2, ld(w.vstat, IC), is0, ld(w.vstat, RBAR), addc, adds);
+  }
+  // ---- apply (constraints.cpp:537-554) ----
+  V3 cn = c0;
+  if (ccnt > 0) cn = cn + csum / static_cast<double>(ccnt);
+  double sn = s0;
+  if (scnt > 0) sn = fmax(sn + qdiv(ssum, static_cast<double>(scnt)), kMinScale);
+  Y[CX * vp + p] = cn.x;
+  Y[CY * vp + p] = cn.y;
+  Y[CZ * vp + p] = cn.z;
+  Y[S * vp + p] = sn;
+  if (has_ext) {
+    double2* xr = reinterpret_cast<double2*>(w.xrec + 8ll * p);
+    xr[0] = make_double2(cn.x, cn.y);
+    xr[1] = make_double2(cn.z, sn);
+  }
+  Q4 qn = q;
+  if (k < m && tcnt > 0) qn = apply_increment(qn, tsum / static_cast<double>(tcnt));
+  Y[QW * vp + p] = qn.w;
+  Y[QX * vp + p] = qn.x;
+  Y[QY * vp + p] = qn.y;
+  Y[QZ * vp + p] = qn.z;
+}
+
 template <int TP>
 void launch_tiles(const World& w, Collide& c, const double* X, double* Y, const SweepParams& sp, int* singular_counter,
                   unsigned long long* err, cudaStream_t st) {
@@ -1135,6 +1346,17 @@ constexpr int kPersistTP = 32;
 
 void launch_rod_sweep(const World& w, Collide& c, const double* X, double* Y, const SweepParams& sp,
                       int* singular_counter, unsigned long long* err, cudaStream_t st) {
+  // every rod fits a warp: one warp per rod (VROD_ROD_WARP=0 forces the tiles, for A/B runs)
+  const bool warp_ok = !(std::getenv("VROD_ROD_WARP") && std::getenv("VROD_ROD_WARP")[0] == '0');
+  if (warp_ok && w.max_rod_n <= 32 && w.R > 0) {
+    const int has_ext = c.ext_cap > 0 ? 1 : 0;
+    const int minb = std::getenv("VROD_WARP_MINB") ? std::atoi(std::getenv("VROD_WARP_MINB")) : 4;
+    auto* kern = minb <= 2 ? k_rod_sweep_warp<2> : minb == 3 ? k_rod_sweep_warp<3> : minb == 4 ? k_rod_sweep_warp<4>
+                                                                                     : k_rod_sweep_warp<5>;
+    launch_kernel(kern, (w.R + kWarpRodsPerCta - 1) / kWarpRodsPerCta, 32 * kWarpRodsPerCta, 0, st, sp.pdl != 0, w,
+                  c, X, Y, sp, singular_counter, err, has_ext);
+    return;
+  }
   // 64-wide tiles once they fill every SM twice over (148 SMs x 2 x 62 slots).
   if (w.V >= 2 * 148 * 62)
     launch_tiles<64>(w, c, X, Y, sp, singular_counter, err, st);

@@ -190,6 +190,7 @@ Solver::Solver(const SceneData& scene, const BatchLayout* batch) : scene_(scene)
   c_.pin_data = dalloc<double>(4 * std::max(c_.n_pins, 1));
   c_.ext_lam = dalloc<double>(3 * c_.ext_cap);
   c_.ext_contrib = dalloc<double>(16 * c_.ext_cap);
+  c_.ext_rec = dalloc<double>(4 * c_.ext_cap);
   c_.ext_pos = dalloc<int>(4 * c_.ext_cap);
   c_.ext_cnt = dalloc<int>(V + 1);
   c_.ext_off = dalloc<int>(V + 1);
@@ -389,6 +390,7 @@ void Solver::upload_static() {
     bones.insert(bones.end(), rod.bones.begin(), rod.bones.end());
     bone_off.push_back(static_cast<int>(bones.size()));
   }
+  w_.max_rod_n = R ? *std::max_element(rn.begin(), rn.end()) : 0;
   upload(w_.rod_vbase, vbase, stream_);
   upload(w_.rod_n, rn, stream_);
   upload(w_.rod_block_base, setup_.block_base, stream_);

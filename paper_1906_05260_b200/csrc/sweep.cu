@@ -102,21 +102,13 @@ __global__ void __launch_bounds__(256, 4) k_ext_solve(World w, Collide c, const 
       ++nsing;
       if (sp.scene_singular) atomicAdd(&sp.scene_singular[ext_scene(w, c, b, npins, nct)], 1);
     };
-    // Writes an endpoint's update into its incidence entry q (flag 0 = no update from this block).
-    // The flag is folded into the entry: kExtNone in dc.x = no update, in ds = no scale update.
-    auto put_at = [&](int q, int flag, double x, double y, double z, double ds) {
-      double2* o = reinterpret_cast<double2*>(c.ext_contrib + 4ll * q);
-      if (flag) {
-        o[0] = make_double2(x, y);
-        o[1] = make_double2(z, (flag & kExtScale) ? ds : ext_none());
-      } else {
-        o[0].x = ext_none();
-      }
-    };  // (rodsweep.cu put_entry is the same record format)
-    const ExtResult r = ext_block(
-        w, c, X, w.xrec, c.ext_lam, ls, b, sp,
-        [&](int e, int flag, double x, double y, double z, double ds) { put_at(c.ext_pos[4 * b + e], flag, x, y, z, ds); },
-        nullptr, nct);
+    // the block's record (32 B, coalesced by block): the per-launch sweeps' gathers form every
+    // endpoint's correction from it (Collide::ext_rec)
+    const ExtResult r = ext_block(w, c, X, w.xrec, c.ext_lam, ls, b, sp, [](int, int, double, double, double, double) {},
+                                  nullptr, nct);
+    double2* rec = reinterpret_cast<double2*>(c.ext_rec + 4ll * b);
+    rec[0] = make_double2(r.rec[0], r.rec[1]);
+    rec[1] = make_double2(r.rec[2], r.rec[3]);
     for (int d = 0; d < r.nlam; ++d) c.ext_lam[d * ls + b] = r.lam[d];
     if (r.singular) sing();
     if (r.bad)

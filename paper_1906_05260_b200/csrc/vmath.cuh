@@ -33,12 +33,22 @@ struct Q4 {
   double w, x, y, z;
 };
 
+// a / b, IEEE. On the device a zero numerator is answered directly (+-0 with the quotient's
+// sign): the compiler's div.rn.f64 expansion sends zero (and tiny) numerators down its slow-path
+// subroutine call, and resting / straight rods divide exact zeros all the time.
+VHD double qdiv(double a, double b) {
+#ifdef __CUDA_ARCH__
+  if (a == 0.0 && b != 0.0 && isfinite(b)) return a * copysign(1.0, b);
+#endif
+  return a / b;
+}
+
 VHD V3 v3(double x, double y, double z) { return V3{x, y, z}; }
 VHD V3 operator+(const V3& a, const V3& b) { return V3{a.x + b.x, a.y + b.y, a.z + b.z}; }
 VHD V3 operator-(const V3& a, const V3& b) { return V3{a.x - b.x, a.y - b.y, a.z - b.z}; }
 VHD V3 operator-(const V3& a) { return V3{-a.x, -a.y, -a.z}; }
 VHD V3 operator*(double s, const V3& a) { return V3{s * a.x, s * a.y, s * a.z}; }
-VHD V3 operator/(const V3& a, double s) { return V3{a.x / s, a.y / s, a.z / s}; }
+VHD V3 operator/(const V3& a, double s) { return V3{qdiv(a.x, s), qdiv(a.y, s), qdiv(a.z, s)}; }
 VHD V3 cwmul(const V3& a, const V3& b) { return V3{a.x * b.x, a.y * b.y, a.z * b.z}; }
 VHD double dot(const V3& a, const V3& b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
 VHD double sqnorm(const V3& a) { return (a.x * a.x + a.y * a.y) + a.z * a.z; }
@@ -65,7 +75,7 @@ VHD Q4 qnormalized(const Q4& q) {
   const double n = qsqnorm(q);
   if (n <= 0.0) return q;
   const double s = sqrt(n);
-  return Q4{q.w / s, q.x / s, q.y / s, q.z / s};
+  return Q4{qdiv(q.w, s), qdiv(q.x, s), qdiv(q.y, s), qdiv(q.z, s)};
 }
 VHD Q4 qmul(const Q4& a, const Q4& b) {
   return Q4{a.w * b.w - a.x * b.x - a.y * b.y - a.z * b.z, a.w * b.x + a.x * b.w + a.y * b.z - a.z * b.y,

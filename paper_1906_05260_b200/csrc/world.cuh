@@ -91,6 +91,7 @@ struct World {
   int K = 0;          // kinematic pills
   int P = 0;          // pills = E + K
   int classic = 0;    // ScaleMode::kPostStepLengthRatio
+  int max_rod_n = 0;  // longest rod (vertices): <= 32 selects the warp-per-rod sweep
   int has_bones = 0;
   int has_loads = 0;
 
