@@ -983,7 +983,39 @@ __device__ __forceinline__ double shdn(double v) { return __shfl_down_sync(0xfff
 __device__ __forceinline__ int shup_i(int v) { return __shfl_up_sync(0xffffffffu, v, 1); }
 __device__ __forceinline__ int shdn_i(int v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 
-template <int kMinBlocks>
+// Staged rows of one rod (warp): snapshot, vertex statics, element statics, multipliers.
+enum WRow : int {
+  W_CX = 0, W_CY, W_CZ, W_S, W_QW, W_QX, W_QY, W_QZ, W_SBAR, W_IC, W_IS, W_RBAR, W_ITX, W_ITY, W_ITZ, W_LEN, W_LEN0,
+  W_TDOT, W_SGRAD, W_SLAP, W_DARBX, W_DARBY, W_DARBZ, W_KSZ, W_KCS, W_KSS, W_KVS, W_KBT0, W_KBT2, W_KSB, W_KVB, W_LAM,
+  kWRows = W_LAM + kLamFields
+};
+__constant__ uint8_t kWRowArr[kWRows] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2,
+                                         2, 2, 2, 2, 2, 2, 2, 2, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3};
+__constant__ uint8_t kWRowField[kWRows] = {
+    CX, CY, CZ, S, QW, QX, QY, QZ, SBAR, IC, IS, RBAR, ITX, ITY, ITZ, LEN, LEN0, TDOT, SGRAD, SLAP, DARBX, DARBY, DARBZ,
+    KSZ, KCS, KSS, KVS, KBT0, KBT2, KSB, KVB,
+    L_SZ0, L_SZ1, L_SZ2, L_CS, L_SS, L_VS0, L_VS1, L_VS2, L_BT0, L_BT1, L_BT2, L_SB, L_VBU, L_VBV};
+constexpr int kWCols = 34;  // a rod of <= 32 slots, its segment aligned down to 16 bytes, rounded up to 16
+struct alignas(16) WarpStage {
+  double rows[kWRows][kWCols];
+  alignas(8) unsigned long long bar;
+};
+__host__ __device__ constexpr int wrow(int a, int f) {
+  return a == 0 ? f
+         : a == 1 ? (f == SBAR ? W_SBAR : f == IC ? W_IC : f == IS ? W_IS : W_RBAR)
+         : a == 3 ? W_LAM + f
+                  : (f == ITX ? W_ITX : f == ITY ? W_ITY : f == ITZ ? W_ITZ : f == LEN ? W_LEN : f == LEN0 ? W_LEN0
+                     : f == TDOT ? W_TDOT : f == SGRAD ? W_SGRAD : f == SLAP ? W_SLAP : f == DARBX ? W_DARBX
+                     : f == DARBY ? W_DARBY : f == DARBZ ? W_DARBZ : f == KSZ ? W_KSZ : f == KCS ? W_KCS
+                     : f == KSS ? W_KSS : f == KVS ? W_KVS : f == KBT0 ? W_KBT0 : f == KBT2 ? W_KBT2
+                     : f == KSB ? W_KSB : W_KVB);
+}
+
+// kStaged: the rod's rows are first copied into shared memory by the TMA engine (one bulk copy
+// per row, all completing on one mbarrier), and every operand — the lane's own and its
+// neighbours' — is read from there; otherwise each lane loads its own rows and takes the
+// neighbours' by shuffle.
+template <int kMinBlocks, bool kStaged>
 __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_warp(World w, Collide c, const double* __restrict__ X,
                                                                       double* __restrict__ Y, SweepParams sp,
                                                                       int* singular, unsigned long long* err,
@@ -1002,8 +1034,42 @@ __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_
   const long long vp = w.vpad;
   const int p = vb + (valid ? k : 0);
   const double h2 = sp.h2, beta = sp.beta;
-  auto ld = [&](const double* a, int f) { return valid ? a[f * vp + p] : 0.0; };
   const double* L = sp.lam_in;
+  auto src_row = [&](int row) -> const double* {
+    const int a = kWRowArr[row];
+    return (a == 0 ? X : a == 1 ? w.vstat : a == 2 ? w.estat : L) + static_cast<long long>(kWRowField[row]) * vp;
+  };
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WarpStage& ws = reinterpret_cast<WarpStage*>(smem_raw)[threadIdx.x >> 5];
+  const int base = vb & ~1, col = (vb - base) + k;
+  if constexpr (kStaged) {
+    const int cnt = (n + (vb - base) + 1) & ~1;
+    if (base + cnt <= vp) {  // TMA bulk copies, 16-byte aligned segments
+      if (k == 0) mbar_init(&ws.bar);
+      __syncwarp();
+      if (k == 0) mbar_arrive_expect(&ws.bar, static_cast<unsigned>(kWRows * cnt * sizeof(double)));
+      __syncwarp();
+      for (int row = k; row < kWRows; row += 32) bulk_g2s(&ws.rows[row][0], src_row(row) + base, cnt * sizeof(double), &ws.bar);
+      mbar_wait(&ws.bar, 0);
+    } else {  // the world's last rod when the segment would run past the rows' padding
+      for (int row = 0; row < kWRows; ++row)
+        for (int j = k; j < cnt; j += 32) ws.rows[row][j] = base + j < vp ? src_row(row)[base + j] : 0.0;
+      __syncwarp();
+    }
+  }
+  // the lane's own value of (array, field) and a neighbour's (d = +-1)
+  auto G = [&](int a, int f) -> double {
+    if constexpr (kStaged)
+      return ws.rows[wrow(a, f)][col];
+    else
+      return valid ? (a == 0 ? X : a == 1 ? w.vstat : a == 2 ? w.estat : L)[f * vp + p] : 0.0;
+  };
+  auto GN = [&](int a, int f, int d) -> double {
+    if constexpr (kStaged)
+      return ws.rows[wrow(a, f)][col + d];
+    else
+      return d > 0 ? shdn(G(a, f)) : shup(G(a, f));
+  };
   int nsing = 0;
   unsigned long long bad = kNoError;
   auto fail = [&](int local) { bad = umin64(bad, err_code(sp.substep, ERR_SWEEP, sp.iter, bb + local)); };
@@ -1034,29 +1100,29 @@ __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_
   const bool el = valid && k < m;         // element k exists
   const bool pel = valid && k >= 1;       // element k-1 exists
   // ---- this slot's snapshot ----
-  const V3 c0{ld(X, CX), ld(X, CY), ld(X, CZ)};
-  const double s0 = ld(X, S);
-  const Q4 q{ld(X, QW), ld(X, QX), ld(X, QY), ld(X, QZ)};
-  const double sbar = ld(w.vstat, SBAR), is0 = ld(w.vstat, IS);
-  const V3 it{ld(w.estat, ITX), ld(w.estat, ITY), ld(w.estat, ITZ)};
-  const double len = ld(w.estat, LEN);
+  const V3 c0{G(0, CX), G(0, CY), G(0, CZ)};
+  const double s0 = G(0, S);
+  const Q4 q{G(0, QW), G(0, QX), G(0, QY), G(0, QZ)};
+  const double sbar = G(1, SBAR), is0 = G(1, IS);
+  const V3 it{G(2, ITX), G(2, ITY), G(2, ITZ)};
+  const double len = G(2, LEN);
 
   // ---- element pass of element k (constraints.cpp:302-314) ----
   double b_sz[3] = {0, 0, 0}, b_vs[3] = {0, 0, 0}, b_cs = 0.0, b_ss = 0.0, b_vsds = 0.0;  // element k's c0 / s0 terms
   int bact = 0;
   {
-    const double ic0 = ld(w.vstat, IC);
-    const V3 c1{shdn(c0.x), shdn(c0.y), shdn(c0.z)};
-    const double s1 = shdn(s0), ic1 = shdn(ic0), is1 = shdn(is0), sbar1 = shdn(sbar);
+    const double ic0 = G(1, IC);
+    const V3 c1{GN(0, CX, 1), GN(0, CY, 1), GN(0, CZ, 1)};
+    const double s1 = GN(0, S, 1), ic1 = GN(1, IC, 1), is1 = GN(1, IS, 1), sbar1 = GN(1, SBAR, 1);
     const int lbase = k * ne;
     if (ek & EK_SZ) {  // StretchZ (:106-119)
       double dc1[3] = {0, 0, 0}, dt[3];
       int act = 0;
       if (el) {
-        const double lam[3] = {ld(L, L_SZ0), ld(L, L_SZ1), ld(L, L_SZ2)};
+        const double lam[3] = {G(3, L_SZ0), G(3, L_SZ1), G(3, L_SZ2)};
         double ln[3];
         bool ok = true;
-        if (blk::stretch_z(c0, c1, ic0, ic1, it, q, ld(w.estat, TDOT), len, ld(w.estat, KSZ), lam, h2, beta, b_sz, dc1,
+        if (blk::stretch_z(c0, c1, ic0, ic1, it, q, G(2, TDOT), len, G(2, KSZ), lam, h2, beta, b_sz, dc1,
                            dt, ln, ok)) {
           act = 1;
           put_lam(L_SZ0, ln[0]);
@@ -1080,10 +1146,10 @@ __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_
       double ds[2] = {0, 0};
       int act = 0;
       if (el) {
-        const double lam = ld(L, L_CS);
+        const double lam = G(3, L_CS);
         double ln;
         bool ok = true;
-        if (blk::cross_section(s0, s1, sbar, sbar1, is0, is1, ld(w.estat, KCS), lam, h2, beta, ds, ln, ok)) {
+        if (blk::cross_section(s0, s1, sbar, sbar1, is0, is1, G(2, KCS), lam, h2, beta, ds, ln, ok)) {
           act = 1;
           put_lam(L_CS, ln);
           if (!ok) fail(lbase + __popc(ek & (EK_CS - 1)));
@@ -1102,10 +1168,10 @@ __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_
       double ds[2] = {0, 0};
       int act = 0;
       if (el) {
-        const double lam = ld(L, L_SS);
+        const double lam = G(3, L_SS);
         double ln;
         bool ok = true;
-        if (blk::surface_stretch(s0, s1, len, ld(w.estat, SGRAD), is0, is1, ld(w.estat, KSS), lam, h2, beta, ds, ln,
+        if (blk::surface_stretch(s0, s1, len, G(2, SGRAD), is0, is1, G(2, KSS), lam, h2, beta, ds, ln,
                                  ok)) {
           act = 1;
           put_lam(L_SS, ln);
@@ -1125,11 +1191,11 @@ __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_
       double dc1[3] = {0, 0, 0}, ds[2] = {0, 0}, dt[3];
       int act = 0;
       if (el) {
-        const double lam[3] = {ld(L, L_VS0), ld(L, L_VS1), ld(L, L_VS2)};
+        const double lam[3] = {G(3, L_VS0), G(3, L_VS1), G(3, L_VS2)};
         double ln[3];
         bool ok = true;
-        if (blk::volume_stretch(c0, c1, s0, s1, sbar, sbar1, ic0, ic1, is0, is1, it, q, ld(w.estat, TDOT),
-                                ld(w.estat, LEN0), ld(w.estat, KVS), lam, h2, beta, b_vs, dc1, ds, dt, ln, ok)) {
+        if (blk::volume_stretch(c0, c1, s0, s1, sbar, sbar1, ic0, ic1, is0, is1, it, q, G(2, TDOT),
+                                G(2, LEN0), G(2, KVS), lam, h2, beta, b_vs, dc1, ds, dt, ln, ok)) {
           act = 1;
           put_lam(L_VS0, ln[0]);
           put_lam(L_VS1, ln[1]);
@@ -1169,9 +1235,9 @@ __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_
   {
     const bool vx = valid && k >= 1 && k <= m - 1;  // vertex k is interior
     const bool nvx = valid && k + 1 <= m - 1;        // vertex k+1 is interior
-    const Q4 qa{shup(q.w), shup(q.x), shup(q.y), shup(q.z)};
-    const V3 ita{shup(it.x), shup(it.y), shup(it.z)};
-    const double la = shup(len);
+    const Q4 qa{GN(0, QW, -1), GN(0, QX, -1), GN(0, QY, -1), GN(0, QZ, -1)};
+    const V3 ita{GN(2, ITX, -1), GN(2, ITY, -1), GN(2, ITZ, -1)};
+    const double la = GN(2, LEN, -1);
     const double lb = len;
     const int lbase = m * ne + (k - 1) * nv;
     const blk::VertexFrame vf = blk::vertex_frame(qa, q, (vk & (VK_BT | VK_VBU | VK_VBV)) != 0);
@@ -1180,13 +1246,13 @@ __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_
     double n_bta[3] = {0, 0, 0};
     int n_bt = 0;
     if (vk & VK_BT) {  // BendTwist (:139-155)
-      const V3 darb_a{shup(ld(w.estat, DARBX)), shup(ld(w.estat, DARBY)), shup(ld(w.estat, DARBZ))};
+      const V3 darb_a{GN(2, DARBX, -1), GN(2, DARBY, -1), GN(2, DARBZ, -1)};
       double dta[3] = {0, 0, 0}, dtb[3];
       if (vx) {
-        const double lam[3] = {ld(L, L_BT0), ld(L, L_BT1), ld(L, L_BT2)};
+        const double lam[3] = {G(3, L_BT0), G(3, L_BT1), G(3, L_BT2)};
         double ln[3];
         bool ok = true;
-        if (blk::bend_twist(vf, s0, sbar, is0, ita, it, la, lb, darb_a, ld(w.estat, KBT0), ld(w.estat, KBT2), lam,
+        if (blk::bend_twist(vf, s0, sbar, is0, ita, it, la, lb, darb_a, G(2, KBT0), G(2, KBT2), lam,
                             sp.classic, h2, beta, bt_ds, dta, dtb, ln, ok)) {
           bt_act = 1;
           put_lam(L_BT0, ln[0]);
@@ -1212,14 +1278,14 @@ __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_
       double a_sb2 = 0.0;
       int p_sb = 0;
       if (vk & VK_SB) {  // SurfaceBending (:156-168)
-        const double sm = shup(s0), ism = shup(is0), slap_a = shup(ld(w.estat, SLAP));
-        const double spp = shdn(s0), isp = shdn(is0);
+        const double sm = GN(0, S, -1), ism = GN(1, IS, -1), slap_a = GN(2, SLAP, -1);
+        const double spp = GN(0, S, 1), isp = GN(1, IS, 1);
         double ds[3] = {0, 0, 0};
         if (vx) {
-          const double lam = ld(L, L_SB);
+          const double lam = G(3, L_SB);
           double ln;
           bool ok = true;
-          if (blk::surface_bending(sm, s0, spp, la, lb, slap_a, ism, is0, isp, ld(w.estat, KSB), lam, h2, beta, ds, ln,
+          if (blk::surface_bending(sm, s0, spp, la, lb, slap_a, ism, is0, isp, G(2, KSB), lam, h2, beta, ds, ln,
                                    ok)) {
             sb_act = 1;
             put_lam(L_SB, ln);
@@ -1244,8 +1310,8 @@ __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_
     double n_vb[2][3] = {{0, 0, 0}, {0, 0, 0}};
     int n_vba[2] = {0, 0};
     if (vk & (VK_VBU | VK_VBV)) {  // VolumeBendU / V (:189-214)
-      const double la0 = shup(ld(w.estat, LEN0)), lb0 = ld(w.estat, LEN0);
-      const double dax = shup(ld(w.estat, DARBX)), day = shup(ld(w.estat, DARBY));
+      const double la0 = GN(2, LEN0, -1), lb0 = G(2, LEN0);
+      const double dax = GN(2, DARBX, -1), day = GN(2, DARBY, -1);
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
         const int bit = cc == 0 ? VK_VBU : VK_VBV;
@@ -1254,11 +1320,11 @@ __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_
         double ds = 0.0, dta[3] = {0, 0, 0}, dtb[3];
         int act = 0;
         if (vx) {
-          const double lam = ld(L, lf);
+          const double lam = G(3, lf);
           double ln;
           bool ok = true;
           if (blk::volume_bend(cc, vf, s0, sbar, is0, ita, it, la, lb, la0, lb0, cc == 0 ? dax : day,
-                               ld(w.estat, KVB), lam, h2, beta, ds, dta, dtb, ln, ok)) {
+                               G(2, KVB), lam, h2, beta, ds, dta, dtb, ln, ok)) {
             act = 1;
             put_lam(lf, ln);
             adds(ds);
@@ -1304,7 +1370,7 @@ __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_
   if (has_ext) {
     const int e0 = c.ext_off[p], e1 = c.ext_off[p + 1];
     if (e0 < e1)
-      gather_recs(c, e0, e1, sp.n_pins, c.scalars[SC_NCT], h2, ld(w.vstat, IC), is0, ld(w.vstat, RBAR), addc, adds);
+      gather_recs(c, e0, e1, sp.n_pins, c.scalars[SC_NCT], h2, G(1, IC), is0, G(1, RBAR), addc, adds);
   }
   // ---- apply (constraints.cpp:537-554) ----
   V3 cn = c0;
@@ -1350,10 +1416,19 @@ void launch_rod_sweep(const World& w, Collide& c, const double* X, double* Y, co
   const bool warp_ok = !(std::getenv("VROD_ROD_WARP") && std::getenv("VROD_ROD_WARP")[0] == '0');
   if (warp_ok && w.max_rod_n <= 32 && w.R > 0) {
     const int has_ext = c.ext_cap > 0 ? 1 : 0;
+    // VROD_WARP_TMA=0: operands by per-lane loads and shuffles instead of the staged rows (A/B)
+    const bool staged = !(std::getenv("VROD_WARP_TMA") && std::getenv("VROD_WARP_TMA")[0] == '0');
     const int minb = std::getenv("VROD_WARP_MINB") ? std::atoi(std::getenv("VROD_WARP_MINB")) : 4;
-    auto* kern = minb <= 2 ? k_rod_sweep_warp<2> : minb == 3 ? k_rod_sweep_warp<3> : minb == 4 ? k_rod_sweep_warp<4>
-                                                                                     : k_rod_sweep_warp<5>;
-    launch_kernel(kern, (w.R + kWarpRodsPerCta - 1) / kWarpRodsPerCta, 32 * kWarpRodsPerCta, 0, st, sp.pdl != 0, w,
+    const size_t smem = staged ? kWarpRodsPerCta * sizeof(WarpStage) : 0;
+    static const bool attrs = [] {
+      for (auto* k : {k_rod_sweep_warp<3, true>, k_rod_sweep_warp<4, true>, k_rod_sweep_warp<5, true>})
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpRodsPerCta * sizeof(WarpStage));
+      return true;
+    }();
+    (void)attrs;
+    auto* kern = staged ? (minb <= 3 ? k_rod_sweep_warp<3, true> : minb == 4 ? k_rod_sweep_warp<4, true> : k_rod_sweep_warp<5, true>)
+                        : (minb <= 3 ? k_rod_sweep_warp<3, false> : minb == 4 ? k_rod_sweep_warp<4, false> : k_rod_sweep_warp<5, false>);
+    launch_kernel(kern, (w.R + kWarpRodsPerCta - 1) / kWarpRodsPerCta, 32 * kWarpRodsPerCta, smem, st, sp.pdl != 0, w,
                   c, X, Y, sp, singular_counter, err, has_ext);
     return;
   }
