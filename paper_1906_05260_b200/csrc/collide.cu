@@ -717,7 +717,7 @@ __global__ void k_seg_filter(Collide c) {
 // sphere-touching pairs in cand_i/cand_j; the count is clamped here (k_clamp_raw's job on the
 // other path) and each pair first passes k_seg_filter's exact segment test.
 template <bool kQuad>
-__global__ void k_narrow_append(Collide c, int split_warm, int raw_idx) {
+__global__ void __launch_bounds__(kQuad ? 64 : 256, kQuad ? 1 : 3) k_narrow_append(Collide c, int split_warm, int raw_idx) {
   pdl_wait();
   pdl_trigger();
   int n = c.scalars[SC_NCAND2];
