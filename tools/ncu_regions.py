@@ -1,6 +1,6 @@
 """Attribute ncu warp-stall samples of one kernel to source functions (inlined code included).
 
-usage: python tools/ncu_regions.py report.ncu-rep kernel_regex lib.so [cubin_name_substr]
+usage: python tools/ncu_regions.py report.ncu-rep kernel_regex lib.so [cubin_name_substr] [mangled_fn_regex]
 Maps each SASS address of the ncu source page to the innermost file:line that `nvdisasm -g`
 reports (build with -lineinfo), then to the enclosing function (the last `__device__` /
 `__global__` definition above that line). Prints samples and stall_no_inst per function."""
@@ -8,6 +8,7 @@ import collections, csv, glob, os, re, subprocess, sys, tempfile
 
 rep, kern, lib = sys.argv[1], sys.argv[2], sys.argv[3]
 cub_sub = sys.argv[4] if len(sys.argv) > 4 else ""
+fn_re = sys.argv[5] if len(sys.argv) > 5 else kern  # mangled-name regex of the SASS function, if it differs
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
 lines_of = {}
@@ -29,7 +30,7 @@ for cub in glob.glob(os.path.join(tmp, "*.cubin")):
         m = re.match(r"\s+/\*([0-9a-f]{4,})\*/", ln)
         if m and cur:
             lines_of[cur][int(m.group(1), 16)] = loc
-fn = [k for k in lines_of if re.search(kern, k)]
+fn = [k for k in lines_of if re.search(fn_re, k)]
 assert fn, f"no function matching {kern}"
 amap = lines_of[fn[0]]
 out = subprocess.run(["ncu", "-i", rep, "-k", f"regex:{kern}", "--page", "source", "--csv", "--print-source", "sass"],
