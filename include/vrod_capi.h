@@ -229,6 +229,11 @@ int vrod_solver_energy(vrod_solver* solver, double* kinetic, double* volume, dou
  * theta inverse weights (3 each). Any may be NULL. */
 int vrod_solver_get_inverse_weights(vrod_solver* solver, double* inv_center, double* inv_scale,
                                     double* inv_theta);
+/* DofLayout lumped weights (layout.h:25-27, build_layout layout.cpp:43-72): per vertex center and
+ * scale weights (+inf when pinned), per element theta weights (3 each, body-frame diagonal, as of the
+ * last refresh_orientation_inertia, layout.cpp:76-93). Any may be NULL. */
+int vrod_solver_get_weights(vrod_solver* solver, double* center_weight, double* scale_weight,
+                            double* theta_weight);
 /* Contacts of the last substep (contact blocks, solver.cpp:210-224): pill ids in the pill
  * array of that substep, frozen alpha/beta. */
 int vrod_solver_get_contacts(vrod_solver* solver, int64_t capacity, int64_t* count,

@@ -544,6 +544,18 @@ int vrod_solver_get_inverse_weights(vrod_solver* s, double* ic, double* is, doub
   });
 }
 
+int vrod_solver_get_weights(vrod_solver* s, double* cw, double* sw, double* tw) {
+  return guarded([&] {
+    const DofLayout& L = one(s).layout();
+    for (int v = 0; v < L.total_vertices; ++v) {
+      if (cw) cw[v] = L.center_weight[v];
+      if (sw) sw[v] = L.scale_weight[v];
+    }
+    for (int e = 0; e < L.total_elements; ++e)
+      if (tw) put3(tw + 3 * e, L.theta_weight[e]);
+  });
+}
+
 int vrod_solver_get_contacts(vrod_solver* s, int64_t cap, int64_t* count, int32_t* a, int32_t* b,
                              double* alpha, double* beta) {
   return guarded([&] {

@@ -132,13 +132,19 @@ class Subcase {
 inline int run_all(int argc, char** argv) {
   State& s = state();
   std::string filter;
+  std::vector<std::string> exclude;  // -tce=<substring>, repeatable
   for (int i = 1; i < argc; ++i) {
     if (std::strncmp(argv[i], "--tc=", 5) == 0) filter = argv[i] + 5;
     if (std::strncmp(argv[i], "-tc=", 4) == 0) filter = argv[i] + 4;
+    if (std::strncmp(argv[i], "--tce=", 6) == 0) exclude.emplace_back(argv[i] + 6);
+    if (std::strncmp(argv[i], "-tce=", 5) == 0) exclude.emplace_back(argv[i] + 5);
   }
   int ran = 0, failed = 0;
   for (const TestCase& tc : s.cases) {
     if (!filter.empty() && std::string(tc.name).find(filter) == std::string::npos) continue;
+    bool skip = false;
+    for (const std::string& x : exclude) skip = skip || std::string(tc.name).find(x) != std::string::npos;
+    if (skip) continue;
     ++ran;
     s.current = &tc;
     s.case_failed = false;

@@ -2461,6 +2461,17 @@ int vrod_solver_get_inverse_weights(vrod_solver* h, double* ic, double* is, doub
       if (it) put3(it + 3 * e, L.it[e]);
   });
 }
+int vrod_solver_get_weights(vrod_solver* h, double* cw, double* sw, double* tw) {
+  return guarded([&] {
+    const Layout& L = one(h).L_;
+    for (int v = 0; v < L.V; ++v) {
+      if (cw) cw[v] = L.cw[v];
+      if (sw) sw[v] = L.sw[v];
+    }
+    for (int e = 0; e < L.E; ++e)
+      if (tw) put3(tw + 3 * e, L.tw[e]);
+  });
+}
 int vrod_solver_get_contacts(vrod_solver* h, int64_t cap, int64_t* count, int32_t* a, int32_t* b, double* alpha,
                              double* beta) {
   return guarded([&] {

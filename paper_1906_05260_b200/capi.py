@@ -115,6 +115,7 @@ _SIGNATURES = {
     "vrod_solver_set_loads": (C.c_int, [C.c_void_p, _dp, _u8p, _dp, _u8p, _dp, _u8p]),
     "vrod_solver_energy": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
     "vrod_solver_get_inverse_weights": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
+    "vrod_solver_get_weights": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
     "vrod_solver_get_contacts": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _ip, _ip, _dp, _dp]),
     "vrod_solver_current_pills": (C.c_int, [C.c_void_p, C.c_int64, _i64p, C.c_void_p]),
     "vrod_batch_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),

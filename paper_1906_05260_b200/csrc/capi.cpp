@@ -407,6 +407,9 @@ int vrod_solver_set_loads(vrod_solver* h, const double* fd, const uint8_t* fdr, 
 int vrod_solver_energy(vrod_solver* h, double* ke, double* vol, double* rvol) {
   return guarded([&] { h->s->energy(ke, vol, rvol); });
 }
+int vrod_solver_get_weights(vrod_solver* h, double* cw, double* sw, double* tw) {
+  return guarded([&] { h->s->weights(cw, sw, tw); });
+}
 int vrod_solver_get_inverse_weights(vrod_solver* h, double* ic, double* is, double* it) {
   return guarded([&] { h->s->inverse_weights(ic, is, it); });
 }

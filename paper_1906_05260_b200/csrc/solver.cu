@@ -1345,6 +1345,32 @@ void Solver::energy(double* ke, double* vol, double* rest_vol) {
   }
 }
 
+void Solver::weights(double* cw, double* sw, double* tw) {
+  const int vpad = setup_.vpad;
+  std::vector<double> twb(vpad);
+  check_cuda(cudaMemcpy(twb.data(), w_.estat + static_cast<std::size_t>(vdev::TWB) * vpad, sizeof(double) * vpad,
+                        cudaMemcpyDeviceToHost), "weights");
+  int e = 0;
+  for (int r = 0; r < setup_.R; ++r) {
+    const int n = scene_.rods[r].n, v0 = setup_.vbase[r];
+    for (int k = 0; k < n; ++k) {
+      const int v = v0 + k;
+      if (cw) cw[v] = cw_[v];
+      if (sw) sw[v] = sw_[v];
+      if (k < n - 1) {
+        // refresh_orientation_inertia (layout.cpp:84-88): (0.25, 0.25, 0.5) x base
+        const double b = twb[v];
+        if (tw) {
+          tw[3 * e] = 0.25 * b;
+          tw[3 * e + 1] = 0.25 * b;
+          tw[3 * e + 2] = 0.5 * b;
+        }
+        ++e;
+      }
+    }
+  }
+}
+
 void Solver::inverse_weights(double* ic, double* is, double* it) {
   const int vpad = setup_.vpad;
   std::vector<double> vs(static_cast<std::size_t>(vdev::kVStatFields) * vpad), es(static_cast<std::size_t>(vdev::kEStatFields) * vpad);

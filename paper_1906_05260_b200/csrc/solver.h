@@ -71,6 +71,7 @@ class Solver {
                  const uint8_t* slr);
   void energy(double* ke, double* vol, double* rest_vol);
   void inverse_weights(double* ic, double* is, double* it);
+  void weights(double* cw, double* sw, double* tw);  // DofLayout weights (layout.h:25-27)
   long long contacts(long long cap, int* a, int* b, double* alpha, double* beta);
   std::vector<PillData> current_pills();
   // Solver::pill_transforms() (solver.cpp:438-440): rod pills, 8 doubles each (center, scale,

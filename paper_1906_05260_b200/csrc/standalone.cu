@@ -1,7 +1,8 @@
 // Fine-grained C-ABI entry points on the GPU: pill_project, deepest_penetration, broad_phase,
 // find_contacts (collision.h:64-95) over host pill arrays. They run the same device functions
 // as the solver's collision stage, so bit-exactness against the oracle on identical pill
-// arrays is tested directly (tests/test_gpu_collision.py).
+// arrays is tested directly (tests/test_gpu_parity.py: test_collision_primitives_bit_exact and the
+// broad-phase / find_contacts cases).
 #include <cstdlib>
 #include <algorithm>
 #include <stdexcept>

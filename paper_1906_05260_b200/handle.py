@@ -229,6 +229,14 @@ class SolverHandle:
             self._h, capi.ptr(out["inv_center"]), capi.ptr(out["inv_scale"]), capi.ptr(out["inv_theta"])))
         return out
 
+    def weights(self) -> dict:
+        """DofLayout lumped weights (layout.h:25-27): +inf for pinned vertices; theta as of the last substep."""
+        V, E = self.total_vertices, self.total_elements
+        out = dict(center_weight=np.zeros(V), scale_weight=np.zeros(V), theta_weight=np.zeros((E, 3)))
+        check(self._lib, self._lib.vrod_solver_get_weights(
+            self._h, capi.ptr(out["center_weight"]), capi.ptr(out["scale_weight"]), capi.ptr(out["theta_weight"])))
+        return out
+
     def contacts(self) -> dict:
         n = C.c_int64()
         check(self._lib, self._lib.vrod_solver_get_contacts(self._h, 0, C.byref(n), None, None, None, None))
