@@ -22,8 +22,10 @@ __device__ __forceinline__ bool stretch_z(const V3& c0, const V3& c1, double ic0
                                           double beta, double (&dc0)[3], double (&dc1)[3], double (&dt)[3],
                                           double (&lam_out)[3], bool& ok) {
   const M3 Rm = qmat(q);
-  const double inv_l = 1.0 / l;
-  const V3 dzc = (c1 - c0) / l;
+  const Recip rl = recip(l);
+  const double inv_l = rinv(rl);
+  const V3 d = c1 - c0;
+  const V3 dzc{divr(d.x, rl), divr(d.y, rl), divr(d.z, rl)};
   const V3 wv = col(Rm, 2);
   const double W[3] = {dzc.x - tbar * wv.x, dzc.y - tbar * wv.y, dzc.z - tbar * wv.z};
   const double J0[3] = {tbar * Rm.m[0][1], tbar * Rm.m[1][1], tbar * Rm.m[2][1]};
@@ -86,8 +88,9 @@ __device__ __forceinline__ bool cross_section(double s0, double s1, double sbar0
 __device__ __forceinline__ bool surface_stretch(double s0, double s1, double l, double sgrad, double is0, double is1,
                                                 double kinv, double lam, double h2, double beta, double (&ds)[2],
                                                 double& lam_out, bool& ok) {
-  const double W = qdiv(s1 - s0, l) - sgrad;
-  const double j0 = -1.0 / l, j1 = 1.0 / l;
+  const Recip rl = recip(l);
+  const double W = divr(s1 - s0, rl) - sgrad;
+  const double j1 = rinv(rl), j0 = -j1;  // -1.0 / l == -(1.0 / l) under round-to-nearest
   double M = 0.0;
   if (is0 != 0.0) M = M + (h2 * is0 * j0) * j0;
   if (is1 != 0.0) M = M + (h2 * is1 * j1) * j1;
@@ -111,11 +114,13 @@ __device__ __forceinline__ bool volume_stretch(const V3& c0, const V3& c1, doubl
   const M3 Rm = qmat(q);
   const double smid = 0.5 * (s0 + s1);
   const double smr = 0.5 * (sbar0 + sbar1);
-  const V3 dzc = (c1 - c0) / l0;
+  const Recip rl0 = recip(l0);
+  const V3 d = c1 - c0;
+  const V3 dzc{divr(d.x, rl0), divr(d.y, rl0), divr(d.z, rl0)};
   const V3 wv = col(Rm, 2);
   const double ka = smid * smid, kb = smr * smr * tbar;
   const double W[3] = {ka * dzc.x - kb * wv.x, ka * dzc.y - kb * wv.y, ka * dzc.z - kb * wv.z};
-  const double jc = qdiv(smid * smid, l0);
+  const double jc = divr(smid * smid, rl0);
   const double js[3] = {smid * dzc.x, smid * dzc.y, smid * dzc.z};
   const double fac = -smr * smr * tbar;
   const double J0[3] = {fac * -Rm.m[0][1], fac * -Rm.m[1][1], fac * -Rm.m[2][1]};
@@ -251,9 +256,10 @@ __device__ __forceinline__ bool bend_twist(const VertexFrame& vf, double s0, dou
 __device__ __forceinline__ bool surface_bending(double sm, double s0, double spp, double la, double lb, double slap,
                                                 double ism, double is0, double isp, double kinv, double lam,
                                                 double h2, double beta, double (&ds)[3], double& lam_out, bool& ok) {
-  const double lap = qdiv(spp - s0, lb) - qdiv(s0 - sm, la);
+  const Recip ra = recip(la), rb = recip(lb);
+  const double lap = divr(spp - s0, rb) - divr(s0 - sm, ra);
   const double W = lap - slap;
-  const double jm = 1.0 / la, j0 = -1.0 / la - 1.0 / lb, jp = 1.0 / lb;
+  const double jm = rinv(ra), jp = rinv(rb), j0 = -jm - jp;  // (-1.0 / la) - 1.0 / lb
   double M = 0.0;
   if (ism != 0.0) M = M + (h2 * ism * jm) * jm;
   if (is0 != 0.0) M = M + (h2 * is0 * j0) * j0;

@@ -415,8 +415,9 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) k_pairs_warp(Collide c, in
                                                                 int* cand_total, int* out_i, int* out_j) {
   pdl_wait();
   pdl_trigger();
-  __shared__ int s_start[kPairWarps][27];
-  __shared__ int s_off[kPairWarps][28];
+  constexpr int kHalf = 14;  // half stencil (see k_pairs_cell): the own cell + 13 positive offsets
+  __shared__ int s_start[kPairWarps][kHalf];
+  __shared__ int s_off[kPairWarps][kHalf + 1];
   __shared__ int s_buf[kPairWarps][kPairBuf];
   __shared__ int s_cnt[kPairWarps], s_broad[kPairWarps];
   __shared__ int s_base;
@@ -426,9 +427,10 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) k_pairs_warp(Collide c, in
   const bool live = i < P;
   int size = 0;
   const int scene = live && c.pill_scene ? c.pill_scene[i] : 0;
-  if (live && lane < 27) {
-    const int h = find_cell(c, c.cellkey[i] + (lane / 9 - 1), c.cellkey[P + i] + ((lane / 3) % 3 - 1),
-                            c.cellkey[2 * P + i] + (lane % 3 - 1), scene);
+  if (live && lane < kHalf) {
+    const int o = 13 + lane;
+    const int h = find_cell(c, c.cellkey[i] + (o / 9 - 1), c.cellkey[P + i] + ((o / 3) % 3 - 1),
+                            c.cellkey[2 * P + i] + (o % 3 - 1), scene);
     if (h >= 0) {
       s_start[warp][lane] = c.cell_start[h];
       size = c.cell_start[h + 1] - c.cell_start[h];
@@ -436,13 +438,13 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) k_pairs_warp(Collide c, in
   }
   int incl = size;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
+  for (int o = 1; o < 16; o <<= 1) {
     const int v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += v;
   }
-  if (lane < 27) s_off[warp][lane + 1] = incl;
+  if (lane < kHalf) s_off[warp][lane + 1] = incl;
   if (lane == 0) s_off[warp][0] = 0;
-  const int total = __shfl_sync(0xffffffffu, incl, 26);
+  const int total = __shfl_sync(0xffffffffu, incl, kHalf - 1);
   __syncwarp();
   int ri = 0, gi = 0, ei = 0;
   bool si = false;
@@ -467,8 +469,8 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) k_pairs_warp(Collide c, in
     base = __shfl_sync(0xffffffffu, base, 0);
     for (int q = lane; q < nbuf; q += 32)
       if (base + q < cap) {
-        out_i[base + q] = i;
-        out_j[base + q] = s_buf[warp][q];
+        out_i[base + q] = min(i, s_buf[warp][q]);
+        out_j[base + q] = max(i, s_buf[warp][q]);
       }
     __syncwarp();
     nbuf = 0;
@@ -485,12 +487,15 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) k_pairs_warp(Collide c, in
     for (int k0 = 0; k0 < total; k0 += 32 * kPairUnroll) {
       int4 at[kPairUnroll];
       double2 s01[kPairUnroll], s23[kPairUnroll];
+      bool own[kPairUnroll];  // item from pill i's own cell (there only j > i counts)
 #pragma unroll
       for (int u = 0; u < kPairUnroll; ++u) {
         const int k = k0 + u * 32 + lane;
         at[u].x = -1;
+        own[u] = false;
         if (k < total) {
           while (s_off[warp][cur_d + 1] <= k) ++cur_d;
+          own[u] = cur_d == 0;
           const int pos = s_start[warp][cur_d] + (k - s_off[warp][cur_d]);
           at[u] = attr[pos];
           s01[u] = sph[2 * pos];
@@ -501,7 +506,9 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) k_pairs_warp(Collide c, in
       for (int u = 0; u < kPairUnroll; ++u) {
         const int j = at[u].x;
         bool cand = false;
-        if (j > i && pair_allowed(ri, gi, si, ei, at[u].y, at[u].z, at[u].w >> 1)) {
+        // pair_allowed(pills[min], pills[max]): its only asymmetry is the first pill's self_collide
+        const bool s_first = j > i ? si : (at[u].w & 1) != 0;
+        if (j >= 0 && (!own[u] || j > i) && pair_allowed(ri, gi, s_first, ei, at[u].y, at[u].z, at[u].w >> 1)) {
           ++broad;
           cand = true;
           if (prefilter) {  // spheres_touch on the cell-sorted copies
@@ -535,19 +542,24 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) k_pairs_warp(Collide c, in
   const long long base = static_cast<long long>(s_base) + s_cnt[warp];
   for (int q = lane; q < nbuf; q += 32)
     if (base + q < cap) {
-      out_i[base + q] = i;
-      out_j[base + q] = s_buf[warp][q];
+      out_i[base + q] = min(i, s_buf[warp][q]);
+      out_j[base + q] = max(i, s_buf[warp][q]);
     }
 }
 
-// One WARP per non-empty grid cell (table slot). Lanes 0..26 probe the 27 cells of its 3x3x3
-// block; the cell's member pills are staged in shared memory, and the warp strides over the
-// flattened neighbourhood items j, loading each j once and testing it against every member i
-// (the neighbourhood is shared by all members of a cell). It counts every allowed pair j > i
-// (broad_phase, collision.cpp:213-226 — StepReport.broad_pairs, the reference has no overlap
-// test) and keeps the pairs whose bounding spheres touch (prefilter; all allowed pairs without
-// it). Kept pairs collect in a per-warp shared buffer flushed with one atomic per fill. The
-// list is unordered; contacts are put in (i, j) order after the narrow phase.
+// One WARP per non-empty grid cell (table slot), over a HALF stencil: the cell itself and the 13
+// neighbours whose offset is lexicographically positive, so every pair of distinct cells is
+// visited from exactly one side (the reference's 27-cell scan with j > i visits each pair from
+// both sides and drops one). Lanes 0..13 probe those 14 cells; the cell's member pills are staged
+// in shared memory, and the warp strides over the flattened neighbourhood items j, loading each j
+// once and testing it against every member i. It counts every allowed pair once — j > i within
+// the cell, any order across cells, evaluated as pair_allowed(pills[min], pills[max]) (its one
+// asymmetric operand, the first pill's self_collide, is taken from the lower index; the sphere
+// test is symmetric: commutative sums and squared differences) — for broad_phase (collision.cpp:213-226, StepReport.broad_pairs; the reference
+// has no overlap test), and keeps the pairs whose bounding spheres touch (prefilter; all allowed
+// pairs without it) as (min, max). Kept pairs collect in a per-warp shared buffer flushed with
+// one atomic per fill. The list is unordered; contacts are put in (i, j) order after the narrow
+// phase.
 constexpr int kCellWarps = 8;
 constexpr int kCellPathMinPills = 1 << 16;
 constexpr int kCellBuf = 128;
@@ -555,8 +567,9 @@ __global__ void __launch_bounds__(32 * kCellWarps) k_pairs_cell(Collide c, int p
                                                                 int* cand_total) {
   pdl_wait();
   pdl_trigger();
-  __shared__ int s_start[kCellWarps][27];
-  __shared__ int s_off[kCellWarps][28];
+  constexpr int kHalf = 14;  // the cell + 13 lexicographically positive neighbours
+  __shared__ int s_start[kCellWarps][kHalf];
+  __shared__ int s_off[kCellWarps][kHalf + 1];
   __shared__ int s_mi[kCellWarps][32], s_mrod[kCellWarps][32], s_mgrp[kCellWarps][32], s_mel[kCellWarps][32];
   __shared__ uint8_t s_mself[kCellWarps][32];
   __shared__ double s_mb[kCellWarps][4][32];
@@ -571,9 +584,11 @@ __global__ void __launch_bounds__(32 * kCellWarps) k_pairs_cell(Collide c, int p
   const int rep = c.table[h];
   const int scene = c.pill_scene ? c.pill_scene[rep] : 0;
   int size = 0;
-  if (lane < 27) {
-    const int hn = find_cell(c, c.cellkey[rep] + (lane / 9 - 1), c.cellkey[P + rep] + ((lane / 3) % 3 - 1),
-                             c.cellkey[2 * P + rep] + (lane % 3 - 1), scene);
+  if (lane < kHalf) {
+    const int o = 13 + lane;  // offsets (o/9-1, (o/3)%3-1, o%3-1): 13 = (0,0,0), 14..26 positive
+    const int hn = lane == 0 ? h
+                             : find_cell(c, c.cellkey[rep] + (o / 9 - 1), c.cellkey[P + rep] + ((o / 3) % 3 - 1),
+                                         c.cellkey[2 * P + rep] + (o % 3 - 1), scene);
     if (hn >= 0) {
       s_start[warp][lane] = c.cell_start[hn];
       size = c.cell_start[hn + 1] - c.cell_start[hn];
@@ -581,13 +596,13 @@ __global__ void __launch_bounds__(32 * kCellWarps) k_pairs_cell(Collide c, int p
   }
   int incl = size;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
+  for (int o = 1; o < 16; o <<= 1) {
     const int v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += v;
   }
-  if (lane < 27) s_off[warp][lane + 1] = incl;
+  if (lane < kHalf) s_off[warp][lane + 1] = incl;
   if (lane == 0) s_off[warp][0] = 0;
-  const int total = __shfl_sync(0xffffffffu, incl, 26);
+  const int total = __shfl_sync(0xffffffffu, incl, kHalf - 1);
   const int mbase = c.cell_start[h];
   auto flush = [&]() {
     int base = 0;
@@ -621,6 +636,7 @@ __global__ void __launch_bounds__(32 * kCellWarps) k_pairs_cell(Collide c, int p
     for (int k0 = 0; k0 < total; k0 += 32) {
       const int k = k0 + lane;
       int j = -1, rj = 0, gj = 0, ej = 0;
+      bool sj = false;
       double jx = 0, jy = 0, jz = 0, jr = 0;
       if (k < total) {
         while (s_off[warp][cur_d + 1] <= k) ++cur_d;
@@ -628,6 +644,7 @@ __global__ void __launch_bounds__(32 * kCellWarps) k_pairs_cell(Collide c, int p
         rj = c.pill_rod[j];
         gj = c.pill_group[j];
         ej = c.pill_el[j];
+        sj = c.pill_self[j] != 0;
         jx = c.bsph[j];
         jy = c.bsph[P + j];
         jz = c.bsph[2 * P + j];
@@ -636,7 +653,10 @@ __global__ void __launch_bounds__(32 * kCellWarps) k_pairs_cell(Collide c, int p
       for (int m = 0; m < nm; ++m) {
         const int i = s_mi[warp][m];
         bool cand = false;
-        if (j > i && pair_allowed(s_mrod[warp][m], s_mgrp[warp][m], s_mself[warp][m] != 0, s_mel[warp][m], rj, gj, ej)) {
+        // pair_allowed(pills[min], pills[max]): its only asymmetry is the first pill's self_collide
+        if (j >= 0 && (cur_d > 0 || j > i) &&
+            pair_allowed(s_mrod[warp][m], s_mgrp[warp][m], j > i ? s_mself[warp][m] != 0 : sj, s_mel[warp][m], rj, gj,
+                         ej)) {
           ++broad;
           if (prefilter) {  // spheres_touch, same arithmetic
             const double dx = s_mb[warp][0][m] - jx, dy = s_mb[warp][1][m] - jy, dz = s_mb[warp][2][m] - jz;
@@ -651,8 +671,8 @@ __global__ void __launch_bounds__(32 * kCellWarps) k_pairs_cell(Collide c, int p
           if (nbuf + __popc(msk) > kCellBuf) flush();
           if (cand) {
             const int q = nbuf + __popc(msk & ((1u << lane) - 1));
-            s_buf[warp][0][q] = i;
-            s_buf[warp][1][q] = j;
+            s_buf[warp][0][q] = min(i, j);
+            s_buf[warp][1][q] = max(i, j);
           }
           nbuf += __popc(msk);
         }

@@ -13,7 +13,14 @@
 // --fmad=false the result is the reference's arithmetic bit for bit; there are no atomics on
 // the data path (bitwise run-to-run determinism) and no colouring (Jacobi
 // snapshot semantics, test_sweep.cpp:132-142).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <tuple>
 
 #include "blocks.cuh"
 #include "ext.cuh"
@@ -646,7 +653,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 32 ? 2 : 4) k_rod_
                                                           double* __restrict__ Y, SweepParams sp, int* singular,
                                                           unsigned long long* err, int has_ext) {
   constexpr int kWarps = warps_for<TP>();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int kTileOwned = TP - 2;
   Tile<TP>& t = *reinterpret_cast<Tile<TP>*>(smem_raw);
   if (sp.pdl == 1) {  // predecessor wrote X: wait before staging
@@ -792,7 +799,7 @@ __global__ void __launch_bounds__(32 * (warps_for<TP>() + 1), 1) k_iterate(World
                                                                       SweepParams sp, int* singular,
                                                                       unsigned long long* err) {
   constexpr int kWarps = warps_for<TP>();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int kTileOwned = TP - 2, kTileStage = TP + 2;
   PTile<TP>& t = *reinterpret_cast<PTile<TP>*>(smem_raw);
   const bool is_aux = blockIdx.x >= pp.tiles;
@@ -983,43 +990,47 @@ __device__ __forceinline__ double shdn(double v) { return __shfl_down_sync(0xfff
 __device__ __forceinline__ int shup_i(int v) { return __shfl_up_sync(0xffffffffu, v, 1); }
 __device__ __forceinline__ int shdn_i(int v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 
-// Staged rows of one rod (warp): snapshot, vertex statics, element statics, multipliers.
-enum WRow : int {
-  W_CX = 0, W_CY, W_CZ, W_S, W_QW, W_QX, W_QY, W_QZ, W_SBAR, W_IC, W_IS, W_RBAR, W_ITX, W_ITY, W_ITZ, W_LEN, W_LEN0,
-  W_TDOT, W_SGRAD, W_SLAP, W_DARBX, W_DARBY, W_DARBZ, W_KSZ, W_KCS, W_KSS, W_KVS, W_KBT0, W_KBT2, W_KSB, W_KVB, W_LAM,
-  kWRows = W_LAM + kLamFields
-};
-__constant__ uint8_t kWRowArr[kWRows] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2,
-                                         2, 2, 2, 2, 2, 2, 2, 2, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3};
-__constant__ uint8_t kWRowField[kWRows] = {
-    CX, CY, CZ, S, QW, QX, QY, QZ, SBAR, IC, IS, RBAR, ITX, ITY, ITZ, LEN, LEN0, TDOT, SGRAD, SLAP, DARBX, DARBY, DARBZ,
-    KSZ, KCS, KSS, KVS, KBT0, KBT2, KSB, KVB,
-    L_SZ0, L_SZ1, L_SZ2, L_CS, L_SS, L_VS0, L_VS1, L_VS2, L_BT0, L_BT1, L_BT2, L_SB, L_VBU, L_VBV};
-constexpr int kWCols = 34;  // a rod of <= 32 slots, its segment aligned down to 16 bytes, rounded up to 16
-struct alignas(16) WarpStage {
-  double rows[kWRows][kWCols];
+// Staged rows of one rod (warp), one 128-byte aligned block per source array (the TMA tensor
+// copy's shared-memory destination must be 128-byte aligned): snapshot X, vertex statics, the
+// sweep's element statics (EStatField LEN .. ITZ), multipliers. The box starts at an even slot
+// (the copy's inner start coordinate must be 16-byte aligned, measured: an odd FP64 start is an
+// illegal instruction), base = (vb - 1) rounded down to even (0 for the first rod), and spans 36
+// columns: the rod's <= 32 slots and one neighbour each side; columns past the arrays arrive
+// zero-filled. `lead` keeps the first rod's column -1 (never used) inside shared memory.
+constexpr int kWCols = 36;
+struct alignas(128) WarpStage {
+  double lead[16];
+  alignas(128) double x[kStateFields][kWCols];
+  alignas(128) double vs[kVStatFields][kWCols];
+  alignas(128) double es[kSweepEStatFields][kWCols];
+  alignas(128) double lm[kLamFields][kWCols];
   alignas(8) unsigned long long bar;
 };
-__host__ __device__ constexpr int wrow(int a, int f) {
-  return a == 0 ? f
-         : a == 1 ? (f == SBAR ? W_SBAR : f == IC ? W_IC : f == IS ? W_IS : W_RBAR)
-         : a == 3 ? W_LAM + f
-                  : (f == ITX ? W_ITX : f == ITY ? W_ITY : f == ITZ ? W_ITZ : f == LEN ? W_LEN : f == LEN0 ? W_LEN0
-                     : f == TDOT ? W_TDOT : f == SGRAD ? W_SGRAD : f == SLAP ? W_SLAP : f == DARBX ? W_DARBX
-                     : f == DARBY ? W_DARBY : f == DARBZ ? W_DARBZ : f == KSZ ? W_KSZ : f == KCS ? W_KCS
-                     : f == KSS ? W_KSS : f == KVS ? W_KVS : f == KBT0 ? W_KBT0 : f == KBT2 ? W_KBT2
-                     : f == KSB ? W_KSB : W_KVB);
+constexpr unsigned kWarpStageBytes =
+    (kStateFields + kVStatFields + kSweepEStatFields + kLamFields) * kWCols * sizeof(double);
+
+// One 2D tensor copy (rows x 34 columns of a field-major array) into shared memory, completing
+// on the warp's mbarrier.
+__device__ __forceinline__ void tma_rows(void* dst, const CUtensorMap* map, int col, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(0), "r"(smem_u32(bar))
+      : "memory");
 }
 
-// kStaged: the rod's rows are first copied into shared memory by the TMA engine (one bulk copy
-// per row, all completing on one mbarrier), and every operand — the lane's own and its
-// neighbours' — is read from there; otherwise each lane loads its own rows and takes the
-// neighbours' by shuffle.
+// kStaged: the rod's rows are first copied into shared memory by the TMA engine — four 2D tensor
+// copies (X, vertex statics, element statics, multipliers) issued by one lane, completing on one
+// mbarrier — and every operand, the lane's own and its neighbours', is read from there;
+// otherwise each lane loads its own rows and takes the neighbours' by shuffle.
 template <int kMinBlocks, bool kStaged>
 __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_warp(World w, Collide c, const double* __restrict__ X,
                                                                       double* __restrict__ Y, SweepParams sp,
                                                                       int* singular, unsigned long long* err,
-                                                                      int has_ext) {
+                                                                      int has_ext, const __grid_constant__ CUtensorMap tm_x,
+                                                                      const __grid_constant__ CUtensorMap tm_vs,
+                                                                      const __grid_constant__ CUtensorMap tm_es,
+                                                                      const __grid_constant__ CUtensorMap tm_lm) {
   if (sp.pdl == 1) {  // predecessor wrote X: wait before loading
     pdl_wait();
     pdl_trigger();
@@ -1035,38 +1046,35 @@ __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_
   const int p = vb + (valid ? k : 0);
   const double h2 = sp.h2, beta = sp.beta;
   const double* L = sp.lam_in;
-  auto src_row = [&](int row) -> const double* {
-    const int a = kWRowArr[row];
-    return (a == 0 ? X : a == 1 ? w.vstat : a == 2 ? w.estat : L) + static_cast<long long>(kWRowField[row]) * vp;
-  };
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   WarpStage& ws = reinterpret_cast<WarpStage*>(smem_raw)[threadIdx.x >> 5];
-  const int base = vb & ~1, col = (vb - base) + k;
+  const int base = vb >= 1 ? (vb - 1) & ~1 : 0;
+  const int col = vb - base + k;
   if constexpr (kStaged) {
-    const int cnt = (n + (vb - base) + 1) & ~1;
-    if (base + cnt <= vp) {  // TMA bulk copies, 16-byte aligned segments
-      if (k == 0) mbar_init(&ws.bar);
-      __syncwarp();
-      if (k == 0) mbar_arrive_expect(&ws.bar, static_cast<unsigned>(kWRows * cnt * sizeof(double)));
-      __syncwarp();
-      for (int row = k; row < kWRows; row += 32) bulk_g2s(&ws.rows[row][0], src_row(row) + base, cnt * sizeof(double), &ws.bar);
-      mbar_wait(&ws.bar, 0);
-    } else {  // the world's last rod when the segment would run past the rows' padding
-      for (int row = 0; row < kWRows; ++row)
-        for (int j = k; j < cnt; j += 32) ws.rows[row][j] = base + j < vp ? src_row(row)[base + j] : 0.0;
-      __syncwarp();
+    if (k == 0) {
+      mbar_init(&ws.bar);
+      mbar_arrive_expect(&ws.bar, kWarpStageBytes);
+      tma_rows(&ws.x[0][0], &tm_x, base, &ws.bar);
+      tma_rows(&ws.vs[0][0], &tm_vs, base, &ws.bar);
+      tma_rows(&ws.es[0][0], &tm_es, base, &ws.bar);
+      tma_rows(&ws.lm[0][0], &tm_lm, base, &ws.bar);
     }
+    __syncwarp();
+    mbar_wait(&ws.bar, 0);
   }
   // the lane's own value of (array, field) and a neighbour's (d = +-1)
+  auto SM = [&](int a, int f, int cc) -> double {
+    return a == 0 ? ws.x[f][cc] : a == 1 ? ws.vs[f][cc] : a == 2 ? ws.es[f][cc] : ws.lm[f][cc];
+  };
   auto G = [&](int a, int f) -> double {
     if constexpr (kStaged)
-      return ws.rows[wrow(a, f)][col];
+      return SM(a, f, col);
     else
       return valid ? (a == 0 ? X : a == 1 ? w.vstat : a == 2 ? w.estat : L)[f * vp + p] : 0.0;
   };
   auto GN = [&](int a, int f, int d) -> double {
     if constexpr (kStaged)
-      return ws.rows[wrow(a, f)][col + d];
+      return SM(a, f, col + d);
     else
       return d > 0 ? shdn(G(a, f)) : shup(G(a, f));
   };
@@ -1408,6 +1416,37 @@ void launch_tiles(const World& w, Collide& c, const double* X, double* Y, const 
 
 constexpr int kPersistTP = 32;
 
+// Tensor map of the first `rows` fields of a field-major FP64 array (row stride vpad doubles):
+// boxes of rows x kWCols, zero fill out of range. Encoded once per (array, rows, vpad) through the
+// driver entry point (no libcuda link), then passed by value as a __grid_constant__ parameter.
+CUtensorMap rows_map(const double* base, int rows, int vpad) {
+  static const auto encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || fn == nullptr)
+      throw std::runtime_error("CUDA error: cuTensorMapEncodeTiled is unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int>, CUtensorMap> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(static_cast<const void*>(base), rows, vpad);
+  const auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(vpad), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(vpad) * sizeof(double)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kWCols), static_cast<cuuint32_t>(rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("CUDA error: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  cache.emplace(key, map);
+  return map;
+}
+
 }  // namespace
 
 void launch_rod_sweep(const World& w, Collide& c, const double* X, double* Y, const SweepParams& sp,
@@ -1418,18 +1457,21 @@ void launch_rod_sweep(const World& w, Collide& c, const double* X, double* Y, co
     const int has_ext = c.ext_cap > 0 ? 1 : 0;
     // VROD_WARP_TMA=0: operands by per-lane loads and shuffles instead of the staged rows (A/B)
     const bool staged = !(std::getenv("VROD_WARP_TMA") && std::getenv("VROD_WARP_TMA")[0] == '0');
-    const int minb = std::getenv("VROD_WARP_MINB") ? std::atoi(std::getenv("VROD_WARP_MINB")) : 4;
+    // 3 CTAs per SM (168 registers, no spills) measured fastest at C4 with the tensor staging
+    const int minb = std::getenv("VROD_WARP_MINB") ? std::atoi(std::getenv("VROD_WARP_MINB")) : 3;
     const size_t smem = staged ? kWarpRodsPerCta * sizeof(WarpStage) : 0;
+    const CUtensorMap tx = rows_map(X, kStateFields, w.vpad), tv = rows_map(w.vstat, kVStatFields, w.vpad),
+                      te = rows_map(w.estat, kSweepEStatFields, w.vpad), tl = rows_map(sp.lam_in, kLamFields, w.vpad);
     static const bool attrs = [] {
-      for (auto* k : {k_rod_sweep_warp<3, true>, k_rod_sweep_warp<4, true>, k_rod_sweep_warp<5, true>})
+      for (auto* k : {k_rod_sweep_warp<2, true>, k_rod_sweep_warp<3, true>, k_rod_sweep_warp<4, true>})
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpRodsPerCta * sizeof(WarpStage));
       return true;
     }();
     (void)attrs;
-    auto* kern = staged ? (minb <= 3 ? k_rod_sweep_warp<3, true> : minb == 4 ? k_rod_sweep_warp<4, true> : k_rod_sweep_warp<5, true>)
-                        : (minb <= 3 ? k_rod_sweep_warp<3, false> : minb == 4 ? k_rod_sweep_warp<4, false> : k_rod_sweep_warp<5, false>);
+    auto* kern = staged ? (minb <= 2 ? k_rod_sweep_warp<2, true> : minb == 3 ? k_rod_sweep_warp<3, true> : k_rod_sweep_warp<4, true>)
+                        : (minb <= 2 ? k_rod_sweep_warp<2, false> : minb == 3 ? k_rod_sweep_warp<3, false> : k_rod_sweep_warp<4, false>);
     launch_kernel(kern, (w.R + kWarpRodsPerCta - 1) / kWarpRodsPerCta, 32 * kWarpRodsPerCta, smem, st, sp.pdl != 0, w,
-                  c, X, Y, sp, singular_counter, err, has_ext);
+                  c, X, Y, sp, singular_counter, err, has_ext, tx, tv, te, tl);
     return;
   }
   // 64-wide tiles once they fill every SM twice over (148 SMs x 2 x 62 slots).

@@ -3,8 +3,8 @@
 // (proj/core/include/vrod/types.h:31-61 and their call sites): dot3 = (a0b0 + a1b1) + a2b2,
 // quaternion squared norm over Eigen's (x,y,z,w) coefficient order = (x^2 + z^2) + (y^2 + w^2),
 // Hamilton product and toRotationMatrix in Eigen's closed forms. Kernels compiled with
-// --fmad=false (collision, integration) therefore reproduce the reference bit for bit;
-// the sweep kernels are compiled with FMA contraction and agree to the BASELINE.md tolerance.
+// --fmad=false therefore reproduce the reference bit for bit (the latency-tuned shape-matching
+// chain in shape.cuh is the one place that uses explicit FMAs, within BASELINE.md's tolerance).
 #pragma once
 
 #include <cmath>
@@ -43,12 +43,57 @@ VHD double qdiv(double a, double b) {
   return a / b;
 }
 
+// Division by a shared reciprocal, bit-identical to a / b (Markstein's theorem): y = RN(1/b),
+// q = RN(a*y), e = a - b*q exactly (FMA), RN(q + e*y) == RN(a/b) whenever nothing under- or
+// overflows on the way — guarded here to |a|, |b| in [2^-500, 2^500]; any other operand (zero,
+// subnormal, huge, inf, nan) takes the IEEE division. Several quotients by one denominator then
+// cost one correctly rounded reciprocal plus a multiply and two FMAs each, instead of one
+// div.rn.f64 expansion each. tools/ubench/divcheck.cu: 8.6e9 random and adversarial operand
+// pairs (all-ones / power-of-two / near-halfway mantissas, exponents -60..60), 0 mismatches on
+// B200. Host code (no __drcp_rn) always divides.
+struct Recip {
+  double b, y;
+  bool ok;
+};
+VHD Recip recip(double b) {
+#ifdef __CUDA_ARCH__
+  const double ab = fabs(b);
+  const bool ok = ab >= 0x1p-500 && ab <= 0x1p500;
+  return Recip{b, ok ? __drcp_rn(b) : 0.0, ok};
+#else
+  return Recip{b, 0.0, false};
+#endif
+}
+// 1.0 / b (RN(1/b) is exactly the reciprocal recip() holds)
+VHD double rinv(const Recip& r) { return r.ok ? r.y : 1.0 / r.b; }
+#ifdef __CUDA_ARCH__
+// the rare operands out of divr's range: one out-of-line IEEE division (keeps the inlined code small)
+__device__ __noinline__ double div_slow(double a, double b) { return qdiv(a, b); }
+#endif
+VHD double divr(double a, const Recip& r) {
+#ifdef __CUDA_ARCH__
+  const double aa = fabs(a);
+  if (r.ok && aa >= 0x1p-500 && aa <= 0x1p500) {
+    const double q = a * r.y;
+    const double e = fma(-r.b, q, a);
+    return fma(e, r.y, q);
+  }
+  if (r.ok && a == 0.0) return a * copysign(1.0, r.b);  // exact zeros are common (qdiv's shortcut)
+  return div_slow(a, r.b);
+#else
+  return qdiv(a, r.b);
+#endif
+}
+
 VHD V3 v3(double x, double y, double z) { return V3{x, y, z}; }
 VHD V3 operator+(const V3& a, const V3& b) { return V3{a.x + b.x, a.y + b.y, a.z + b.z}; }
 VHD V3 operator-(const V3& a, const V3& b) { return V3{a.x - b.x, a.y - b.y, a.z - b.z}; }
 VHD V3 operator-(const V3& a) { return V3{-a.x, -a.y, -a.z}; }
 VHD V3 operator*(double s, const V3& a) { return V3{s * a.x, s * a.y, s * a.z}; }
-VHD V3 operator/(const V3& a, double s) { return V3{qdiv(a.x, s), qdiv(a.y, s), qdiv(a.z, s)}; }
+VHD V3 operator/(const V3& a, double s) {
+  const Recip r = recip(s);
+  return V3{divr(a.x, r), divr(a.y, r), divr(a.z, r)};
+}
 VHD V3 cwmul(const V3& a, const V3& b) { return V3{a.x * b.x, a.y * b.y, a.z * b.z}; }
 VHD double dot(const V3& a, const V3& b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
 VHD double sqnorm(const V3& a) { return (a.x * a.x + a.y * a.y) + a.z * a.z; }
@@ -74,8 +119,8 @@ VHD V3 qvec(const Q4& q) { return V3{q.x, q.y, q.z}; }
 VHD Q4 qnormalized(const Q4& q) {
   const double n = qsqnorm(q);
   if (n <= 0.0) return q;
-  const double s = sqrt(n);
-  return Q4{qdiv(q.w, s), qdiv(q.x, s), qdiv(q.y, s), qdiv(q.z, s)};
+  const Recip r = recip(sqrt(n));
+  return Q4{divr(q.w, r), divr(q.x, r), divr(q.y, r), divr(q.z, r)};
 }
 VHD Q4 qmul(const Q4& a, const Q4& b) {
   return Q4{a.w * b.w - a.x * b.x - a.y * b.y - a.z * b.z, a.w * b.x + a.x * b.w + a.y * b.z - a.z * b.y,

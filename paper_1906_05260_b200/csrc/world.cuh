@@ -24,16 +24,20 @@ enum VelField : int { VX = 0, VY, VZ, VS, WX, WY, WZ, kVelFields };
 enum VStatField : int { RBAR = 0, SBAR, IC, IS, kVStatFields };
 // Per-element rest fields (element k of a rod at its slot). DARB*/SLAP are the rest Darboux
 // vector / scale laplacian of interior vertex k+1 (reference index j-1 = k).
+// The rows a sweep reads come first (LEN .. ITZ, kSweepEStatFields), so the warp-per-rod sweep
+// stages them with ONE 2D tensor copy per rod (rodsweep.cu).
 enum EStatField : int {
-  LEN = 0, LEN0, TDOT, SGRAD, SLAP, DARBX, DARBY, DARBZ, RQW, RQX, RQY, RQZ,
-  A2E,      // pi * rmid^2
-  A4EP,     // 0.25 * pi * pow(rmid, 4)   (refresh_stiffness form, constraints.cpp:352)
-  A4VP,     // 0.25 * pi * pow(r_k, 4) of vertex k (constraints.cpp:357,363)
+  LEN = 0, LEN0, TDOT, SGRAD, SLAP, DARBX, DARBY, DARBZ,
   // Stiffness rows hold the INVERSE stiffness inverse_stiffness(k) (constraints.cpp:274-278),
   // computed once at setup / on activation refresh instead of once per block per sweep.
   KSZ, KCS, KSS, KVS,     // element-pass (StretchZ/VolumeStretch are Constant)
   KBT0, KBT1, KBT2, KSB, KVB,  // vertex-pass of vertex k (VolumeBendU == V; KBT1 == KBT0 always)
   ITX, ITY, ITZ,          // inverse theta weights (refreshed every substep)
+  kSweepEStatFields,
+  RQW = kSweepEStatFields, RQX, RQY, RQZ,
+  A2E,      // pi * rmid^2
+  A4EP,     // 0.25 * pi * pow(rmid, 4)   (refresh_stiffness form, constraints.cpp:352)
+  A4VP,     // 0.25 * pi * pow(r_k, 4) of vertex k (constraints.cpp:357,363)
   TWB,                    // theta weight base rho*s_mid^2*pi*r^4*l0 (weights = 0.25,0.25,0.5 x base)
   kEStatFields
 };
