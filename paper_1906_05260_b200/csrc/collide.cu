@@ -737,7 +737,7 @@ __global__ void k_seg_filter(Collide c) {
 // sphere-touching pairs in cand_i/cand_j; the count is clamped here (k_clamp_raw's job on the
 // other path) and each pair first passes k_seg_filter's exact segment test.
 template <bool kQuad>
-__global__ void __launch_bounds__(kQuad ? 64 : 256, kQuad ? 1 : 3) k_narrow_append(Collide c, int split_warm, int raw_idx) {
+__global__ void __launch_bounds__(kQuad ? 64 : 256, kQuad ? 1 : 3) k_narrow_append(Collide c, int split_warm, int raw_idx, int seg_test) {
   pdl_wait();
   pdl_trigger();
   int n = c.scalars[SC_NCAND2];
@@ -762,7 +762,7 @@ __global__ void __launch_bounds__(kQuad ? 64 : 256, kQuad ? 1 : 3) k_narrow_appe
         i = ci[q];
         j = cj[q];
       }
-      if (q < n && (raw_idx < 0 || segments_close(c.pill, c.P, i, j))) {
+      if (q < n && (!seg_test || segments_close(c.pill, c.P, i, j))) {
         const unsigned long long key = pair_key(c.pill_id[i], c.pill_id[j]);
         const int scene = c.pill_scene ? c.pill_scene[i] : 0;
         double warm;
@@ -808,7 +808,7 @@ __global__ void __launch_bounds__(kQuad ? 64 : 256, kQuad ? 1 : 3) k_narrow_appe
     PillPrep pb{};
     if (live) {
       if (r == 3) {
-        keep = raw_idx < 0 || segments_close(c.pill, c.P, i, j);
+        keep = !seg_test || segments_close(c.pill, c.P, i, j);
         if (keep) {
           const unsigned long long key = pair_key(c.pill_id[i], c.pill_id[j]);
           const int scene = c.pill_scene ? c.pill_scene[i] : 0;
@@ -1343,12 +1343,12 @@ void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
   if (g_broad_mark) cudaEventRecord(g_broad_mark, st);  // end of the broad phase (phase timing)
   if (fused_seg) {  // k_narrow_append clamps the count and runs the exact segment test itself
     launch_kernel(k_narrow_append<true>, narrow_grid(c.cand_cap), kNarrowThreads, 0, st, g_pdl, c, split_warm,
-                  int(SC_NCAND_RAW));
+                  int(SC_NCAND_RAW), 1);
   } else {
     launch_kernel(k_clamp_raw, 1, 1, 0, st, g_pdl, c.scalars, SC_NCAND_RAW, SC_NCAND, c.cand_cap, 1);
     if (!do_narrow) return;
     launch_kernel(k_seg_filter, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c);
-    launch_kernel(k_narrow_append<false>, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c, split_warm, -1);
+    launch_kernel(k_narrow_append<false>, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c, split_warm, -1, 0);
   }
   launch_kernel(k_clamp_raw, 1, 1, 0, st, g_pdl, c.scalars, SC_NCT_RAW, SC_NCT, c.contact_cap, 2);
   launch_order_contacts(c, st);

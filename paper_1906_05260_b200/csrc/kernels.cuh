@@ -119,6 +119,8 @@ struct Collide {
   int* ext_off = nullptr;        // V+1
   int* ext_cur = nullptr;        // V
   int* ext_items = nullptr;      // 4 x ext_cap entries (block << 2 | endpoint)
+  double* ext_ab = nullptr;      // 4 x ext_cap, per entry q: its contact's alpha (endpoints 0, 1) /
+                                 // beta (2, 3), 0 for pins and half-planes — frozen for the substep
   // batch of scenes (World::n_scenes > 1): pairs only within a scene, per-scene grid cell
   int* pill_scene = nullptr;     // P
   unsigned long long* scene_maxr = nullptr;  // per scene: max bounding radius bits

@@ -27,6 +27,7 @@ struct PillPrep {
   double r0, r1;
   bool degenerate;
   double l;
+  Recip rl;  // 1 / l, shared by every projection's divisions (divr: the same bits as / l)
   V3 j;
   double tan_t;
 };
@@ -39,9 +40,10 @@ __device__ __forceinline__ PillPrep prep_pill(const PillV& p) {
   const V3 axis = p.c1 - p.c0;
   q.l = norm(axis);
   q.degenerate = q.l <= fabs(p.r0 - p.r1) || q.l < 1e-14;
+  q.rl = recip(q.l);
   if (!q.degenerate) {
-    q.j = axis / q.l;
-    const double sin_t = (p.r1 - p.r0) / q.l;
+    q.j = V3{divr(axis.x, q.rl), divr(axis.y, q.rl), divr(axis.z, q.rl)};
+    const double sin_t = divr(p.r1 - p.r0, q.rl);
     q.tan_t = sin_t / sqrt(fmax(1e-16, 1.0 - sin_t * sin_t));
   } else {
     q.j = V3{0, 0, 0};
@@ -65,7 +67,7 @@ __device__ __forceinline__ double project(const V3& x, const PillPrep& p, double
   const V3 y = x - p.c0;
   const double a = dot(y, p.j);
   const double b = norm(y - a * p.j);
-  double t = (a + b * p.tan_t) / p.l;
+  double t = divr(a + b * p.tan_t, p.rl);
   t = fmin(fmax(t, 0.0), 1.0);
   t_out = t;
   const V3 c = (1.0 - t) * p.c0 + t * p.c1;  // pill_distance_at, collision.cpp:9-13

@@ -590,31 +590,43 @@ __device__ __forceinline__ void gather_entries(const Collide& c, int e0, int e1,
 // The external blocks touching slot p (incidence entries [e0, e1), block order) from the blocks'
 // records (Collide::ext_rec, written by k_ext_solve): pins and half-planes carry their single
 // endpoint's correction, contacts their normal and dlambda, from which the endpoint's correction
-// is re-formed exactly as ext_block forms it (contact_endpoint). Chunks of 4 entries: all loads
-// of a chunk are issued before the first add. ic, is, rb: the slot's inverse weights and rest
-// radius.
+// is re-formed exactly as ext_block forms it (contact_endpoint) with the entry's frozen alpha /
+// beta (Collide::ext_ab, beside the entry). Chunks of 4 entries, software-pipelined: a chunk's
+// entries (static for the substep) are loaded while the previous chunk's records are in flight,
+// and all loads of a chunk are issued before its first add. `pre`: the first chunk's entries,
+// loaded by the caller ahead of time (before waiting for the ext solve). ic, is, rb: the slot's
+// inverse weights and rest radius.
+struct EntryChunk {
+  int it[4];
+  double ab[4];
+};
+__device__ __forceinline__ EntryChunk load_entries(const Collide& c, int q0, int e0, int e1) {
+  EntryChunk ch;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int q = q0 + u < e1 ? q0 + u : e0;
+    ch.it[u] = c.ext_items[q];
+    ch.ab[u] = c.ext_ab[q];
+  }
+  return ch;
+}
 template <class AddC, class AddS>
 __device__ __forceinline__ void gather_recs(const Collide& c, int e0, int e1, int npins, int nct, double h2, double ic,
-                                            double is, double rb, AddC& addc, AddS& adds) {
+                                            double is, double rb, AddC& addc, AddS& adds, EntryChunk nxt) {
   for (int q0 = e0; q0 < e1; q0 += 4) {
-    int it[4];
+    const EntryChunk ch = nxt;
     double2 r01[4], r23[4];
-    double ab[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) it[u] = c.ext_items[q0 + u < e1 ? q0 + u : e0];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int b = it[u] >> 2, e = it[u] & 3;
-      const double2* rr = reinterpret_cast<const double2*>(c.ext_rec + 4ll * b);
+      const double2* rr = reinterpret_cast<const double2*>(c.ext_rec + 4ll * (ch.it[u] >> 2));
       r01[u] = rr[0];
       r23[u] = rr[1];
-      const int k = b - npins;
-      ab[u] = (k >= 0 && k < nct) ? (e < 2 ? c.ct_alpha[k] : c.ct_beta[k]) : 0.0;
     }
+    if (q0 + 4 < e1) nxt = load_entries(c, q0 + 4, e0, e1);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       if (q0 + u >= e1) continue;
-      const int b = it[u] >> 2, e = it[u] & 3;
+      const int b = ch.it[u] >> 2, e = ch.it[u] & 3;
       if (b < npins) {  // soft pin: center only
         if (is_ext_none(r01[u].x)) continue;
         const double d[3] = {r01[u].x, r01[u].y, r23[u].x};
@@ -622,7 +634,7 @@ __device__ __forceinline__ void gather_recs(const Collide& c, int e0, int e1, in
       } else if (b < npins + nct) {  // contact
         if (is_ext_none(r23[u].y)) continue;
         double o[3], os;
-        contact_endpoint(e, ab[u], r01[u].x, r01[u].y, r23[u].x, r23[u].y, h2, ic, is, rb, o, os);
+        contact_endpoint(e, ch.ab[u], r01[u].x, r01[u].y, r23[u].x, r23[u].y, h2, ic, is, rb, o, os);
         addc(o);
         adds(os);
       } else {  // half-plane
@@ -708,7 +720,7 @@ __global__ void __launch_bounds__(32 * warps_for<TP>(), TP == 32 ? 2 : 4) k_rod_
     if (e0 == e1) return;
     const int si = p - start + 2;
     gather_recs(c, e0, e1, sp.n_pins, nct, sp.h2, t.st[T_IC][si], t.st[T_IS][si], w.vstat[RBAR * (long long)w.vpad + p],
-                addc, adds);
+                addc, adds, load_entries(c, e0, e0, e1));
   });
 }
 
@@ -1368,18 +1380,22 @@ __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_
       if (bad != kNoError) atomicMin(err, bad);
     }
   }
-  // the ext solve of this iteration (the predecessor) writes the incidence entries and reads the
-  // slot records this sweep rewrites: wait for it only now
+  // the slot's incidence entries are static for the substep: the first chunk is loaded before
+  // waiting for this iteration's ext solve (the predecessor), which writes the block records and
+  // reads the slot records this sweep rewrites
+  int e0 = 0, e1 = 0;
+  EntryChunk first{};
+  if (has_ext && valid) {
+    e0 = c.ext_off[p];
+    e1 = c.ext_off[p + 1];
+    if (e0 < e1) first = load_entries(c, e0, e0, e1);
+  }
   if (sp.pdl == 2) {
     pdl_wait();
     pdl_trigger();
   }
   if (!valid) return;
-  if (has_ext) {
-    const int e0 = c.ext_off[p], e1 = c.ext_off[p + 1];
-    if (e0 < e1)
-      gather_recs(c, e0, e1, sp.n_pins, c.scalars[SC_NCT], h2, G(1, IC), is0, G(1, RBAR), addc, adds);
-  }
+  if (e0 < e1) gather_recs(c, e0, e1, sp.n_pins, c.scalars[SC_NCT], h2, G(1, IC), is0, G(1, RBAR), addc, adds, first);
   // ---- apply (constraints.cpp:537-554) ----
   V3 cn = c0;
   if (ccnt > 0) cn = cn + csum / static_cast<double>(ccnt);

@@ -196,6 +196,7 @@ Solver::Solver(const SceneData& scene, const BatchLayout* batch) : scene_(scene)
   c_.ext_off = dalloc<int>(V + 1);
   c_.ext_cur = dalloc<int>(V);
   c_.ext_items = dalloc<int>(4 * c_.ext_cap);
+  c_.ext_ab = dalloc<double>(4 * c_.ext_cap);
   c_.scalars = dalloc<int>(vdev::kScalars);
   c_.maxr_bits = dalloc<unsigned long long>(1);
   const long long scan_max = std::max<long long>({c_.cand_cap, static_cast<long long>(c_.T), static_cast<long long>(c_.P),

@@ -182,11 +182,19 @@ __global__ void k_ext_fill(Collide c, int npins) {
     }
   }
 }
+// The frozen alpha / beta an incidence entry's gather scales its contact's correction by.
+__device__ __forceinline__ double entry_ab(const Collide& c, int key, int npins, int nct) {
+  const int k = (key >> 2) - npins;
+  return k >= 0 && k < nct ? ((key & 3) < 2 ? c.ct_alpha[k] : c.ct_beta[k]) : 0.0;
+}
+
 // Orders each slot's incidence entries by (block, endpoint): one warp per slot; up to 32 entries
-// are ranked in registers (keys are distinct), longer lists fall back to an insertion sort.
-__global__ void k_ext_sort(Collide c, int V) {
+// are ranked in registers (keys are distinct), longer lists fall back to an insertion sort. Each
+// entry's alpha / beta is stored beside it (ext_ab), so the sweeps' gathers read it contiguously.
+__global__ void k_ext_sort(Collide c, int V, int npins) {
   pdl_wait();
   pdl_trigger();
+  const int nct = c.scalars[SC_NCT];
   const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (blockDim.x >> 5);
   for (int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < V; v += warps) {
@@ -200,6 +208,7 @@ __global__ void k_ext_sort(Collide c, int V) {
       if (lane < n) {
         c.ext_items[s0 + rank] = key;
         c.ext_pos[key] = s0 + rank;
+        c.ext_ab[s0 + rank] = entry_ab(c, key, npins, nct);
       }
     } else if (lane == 0) {
       for (int a = s0 + 1; a < s1; ++a) {  // insertion sort: block order, then endpoint
@@ -211,7 +220,10 @@ __global__ void k_ext_sort(Collide c, int V) {
         }
         c.ext_items[b + 1] = key;
       }
-      for (int a = s0; a < s1; ++a) c.ext_pos[c.ext_items[a]] = a;
+      for (int a = s0; a < s1; ++a) {
+        c.ext_pos[c.ext_items[a]] = a;
+        c.ext_ab[a] = entry_ab(c, c.ext_items[a], npins, nct);
+      }
     }
   }
 }
@@ -302,6 +314,7 @@ __global__ void __launch_bounds__(kExtSetupThreads) k_ext_setup_small(Collide c,
         if (lane < m) {
           c.ext_items[s0 + rank] = key;
           c.ext_pos[key] = s0 + rank;
+          c.ext_ab[s0 + rank] = entry_ab(c, key, npins, nct);
         }
         __syncwarp();
       } else {
@@ -315,7 +328,10 @@ __global__ void __launch_bounds__(kExtSetupThreads) k_ext_setup_small(Collide c,
             }
             c.ext_items[b + 1] = key;
           }
-          for (int a = s0; a < s1; ++a) c.ext_pos[c.ext_items[a]] = a;
+          for (int a = s0; a < s1; ++a) {
+            c.ext_pos[c.ext_items[a]] = a;
+            c.ext_ab[a] = entry_ab(c, c.ext_items[a], npins, nct);
+          }
         }
         __syncwarp();
       }
@@ -715,7 +731,7 @@ void launch_ext_setup(const World& w, Collide& c, cudaStream_t st) {
   launch_kernel(k_ext_count, g, kThreads, 0, st, g_pdl, c, c.n_pins);
   scan_exclusive(c.ext_cnt, c.ext_off, w.V, nullptr, c.scan_tmp, c.scan_parts, st);
   launch_kernel(k_ext_fill, g, kThreads, 0, st, g_pdl, c, c.n_pins);
-  launch_kernel(k_ext_sort, grid_for(32ll * w.V), kThreads, 0, st, g_pdl, c, w.V);
+  launch_kernel(k_ext_sort, grid_for(32ll * w.V), kThreads, 0, st, g_pdl, c, w.V, c.n_pins);
 }
 
 void launch_ext_solve(const World& w, Collide& c, const double* X, const SweepParams& sp, int* singular_counter,
