@@ -189,20 +189,17 @@ __global__ void k_build_pills(World w, Collide c, const double* __restrict__ ani
       const int i = v - r;
       const int vp = w.vpad;
       const double* X = w.X;
-      c.pill[i] = X[CX * vp + v];
-      c.pill[P + i] = X[CY * vp + v];
-      c.pill[2 * P + i] = X[CZ * vp + v];
-      c.pill[3 * P + i] = X[CX * vp + v + 1];
-      c.pill[4 * P + i] = X[CY * vp + v + 1];
-      c.pill[5 * P + i] = X[CZ * vp + v + 1];
-      c.pill[6 * P + i] = X[S * vp + v] * w.vstat[RBAR * vp + v];
-      c.pill[7 * P + i] = X[S * vp + v + 1] * w.vstat[RBAR * vp + v + 1];
+      double2* o = reinterpret_cast<double2*>(c.pill + 8ll * i);
+      o[0] = make_double2(X[CX * vp + v], X[CY * vp + v]);
+      o[1] = make_double2(X[CZ * vp + v], X[CX * vp + v + 1]);
+      o[2] = make_double2(X[CY * vp + v + 1], X[CZ * vp + v + 1]);
+      o[3] = make_double2(X[S * vp + v] * w.vstat[RBAR * vp + v], X[S * vp + v + 1] * w.vstat[RBAR * vp + v + 1]);
     }
   }
   if (v < al.n_kin) {
     const double* kp = anim + al.off_kin + 8 * v;
     const int i = w.E + v;
-    for (int f = 0; f < 8; ++f) c.pill[f * P + i] = kp[f];
+    for (int f = 0; f < 8; ++f) c.pill[8ll * i + f] = kp[f];
   }
 }
 

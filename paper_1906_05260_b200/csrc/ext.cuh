@@ -37,11 +37,10 @@ __device__ __forceinline__ ExtGeom resolve_rec(const double* xrec, const Collide
     is[0] = b.z;
     is[1] = e.z;
   } else {
-    const int P = c.P;
-    g.c0 = vm::V3{c.pill[pill], c.pill[P + pill], c.pill[2 * P + pill]};
-    g.c1 = vm::V3{c.pill[3 * P + pill], c.pill[4 * P + pill], c.pill[5 * P + pill]};
-    g.r0 = c.pill[6 * P + pill];
-    g.r1 = c.pill[7 * P + pill];
+    g.c0 = vm::V3{c.pill[8ll * pill], c.pill[8ll * pill + 1], c.pill[8ll * pill + 2]};
+    g.c1 = vm::V3{c.pill[8ll * pill + 3], c.pill[8ll * pill + 4], c.pill[8ll * pill + 5]};
+    g.r0 = c.pill[8ll * pill + 6];
+    g.r1 = c.pill[8ll * pill + 7];
     g.rb0 = g.rb1 = 0.0;
     g.v0 = -1;
     ic[0] = ic[1] = is[0] = is[1] = 0.0;

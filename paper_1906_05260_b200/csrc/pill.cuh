@@ -14,9 +14,13 @@ struct PillV {
   double r0, r1;
 };
 
+// Collide::pill is AoS, 8 doubles (64 B, two sectors) per pill: c0 xyz, c1 xyz, r0, r1 — a
+// random pill costs two sectors instead of eight scattered SoA rows. (P kept for the callers.)
 __device__ __forceinline__ PillV load_pill(const double* __restrict__ pill, int P, int i) {
-  return PillV{V3{pill[i], pill[P + i], pill[2 * P + i]}, V3{pill[3 * P + i], pill[4 * P + i], pill[5 * P + i]},
-               pill[6 * P + i], pill[7 * P + i]};
+  (void)P;
+  const double2* q = reinterpret_cast<const double2*>(pill + 8ll * i);
+  const double2 a = q[0], b = q[1], d = q[2], e = q[3];
+  return PillV{V3{a.x, a.y, b.x}, V3{b.y, d.x, d.y}, e.x, e.y};
 }
 
 // pill_project (collision.cpp:15-49) with the per-pill constants (axis, length, unit axis,

@@ -60,12 +60,12 @@ void make_collide(Buf& b, vdev::Collide& c, const vrod_pill* pills, int P, long 
   std::vector<uint32_t> id(P);
   for (int i = 0; i < P; ++i) {
     const vrod_pill& p = pills[i];
-    for (int f = 0; f < 3; ++f) {
-      geo[f * P + i] = p.c0[f];
-      geo[(3 + f) * P + i] = p.c1[f];
+    for (int f = 0; f < 3; ++f) {  // AoS, 8 doubles per pill (pill.cuh load_pill)
+      geo[8ll * i + f] = p.c0[f];
+      geo[8ll * i + 3 + f] = p.c1[f];
     }
-    geo[6 * P + i] = p.r0;
-    geo[7 * P + i] = p.r1;
+    geo[8ll * i + 6] = p.r0;
+    geo[8ll * i + 7] = p.r1;
     rod[i] = p.rod;
     el[i] = p.element;
     grp[i] = p.group;

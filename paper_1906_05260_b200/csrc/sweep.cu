@@ -48,11 +48,10 @@ __device__ __forceinline__ ExtGeom resolve_at(const World& w, const Collide& c, 
     g.r1 = F(X, S, vp, v + 1) * g.rb1;
     g.v0 = v;
   } else {
-    const int P = c.P;
-    g.c0 = V3{c.pill[pill], c.pill[P + pill], c.pill[2 * P + pill]};
-    g.c1 = V3{c.pill[3 * P + pill], c.pill[4 * P + pill], c.pill[5 * P + pill]};
-    g.r0 = c.pill[6 * P + pill];
-    g.r1 = c.pill[7 * P + pill];
+    g.c0 = V3{c.pill[8ll * pill], c.pill[8ll * pill + 1], c.pill[8ll * pill + 2]};
+    g.c1 = V3{c.pill[8ll * pill + 3], c.pill[8ll * pill + 4], c.pill[8ll * pill + 5]};
+    g.r0 = c.pill[8ll * pill + 6];
+    g.r1 = c.pill[8ll * pill + 7];
     g.rb0 = g.rb1 = 0.0;
     g.v0 = -1;
   }
