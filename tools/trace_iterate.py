@@ -50,6 +50,8 @@ print(f"iteration 1 barrier arrivals over {len(arr)} CTAs: first..last spread {(
       f"latest CTA {int(np.argmax(raw[700:700 + 148]))}")
 order = np.argsort(arr)
 print("  latest 8 CTAs (us after first):", [(int(i), round((arr[i] - arr.min()) / 1e3, 2)) for i in order[-8:]])
+rel = (arr - arr.min()) / 1e3
+print("  arrival percentiles (us after first): p10 %.2f p50 %.2f p90 %.2f max %.2f" % tuple(np.percentile(rel, [10, 50, 90, 100])))
 for l in range(2):
     ph = raw[600 + 8 * l: 606 + 8 * l]
     if ph[0] > 0:
