@@ -212,6 +212,22 @@ class Activation:
 
 
 @dataclass
+class Probe:  # scene.h:95-100 — per-step logging of one vertex (metrics.py ProbeWriter)
+    name: str = ""
+    rod: int = 0
+    vertex: int = 0
+
+
+@dataclass
+class SkinSetup:  # scene.h:102-107 — surface mesh skinned to the rods' pills
+    vertices: list = field(default_factory=list)   # (x, y, z) per vertex
+    triangles: list = field(default_factory=list)  # (a, b, c) vertex ids
+    max_influences: int = 8
+    epsilon: float = 1e-4
+    smooth_iterations: int = 0
+
+
+@dataclass
 class Scene:
     rods: list = field(default_factory=list)
     materials: list = field(default_factory=list)
@@ -223,6 +239,8 @@ class Scene:
     soft_pins: list = field(default_factory=list)
     activations: list = field(default_factory=list)
     settings: SolverSettings = field(default_factory=SolverSettings)
+    probes: list = field(default_factory=list)  # caller-side (metrics), not sent to the solver
+    skin: SkinSetup | None = None               # caller-side (the CLI binds it), not sent to the solver
 
     def vertex_count(self) -> int:
         return sum(r.rest.vertex_count() for r in self.rods)
@@ -312,8 +330,12 @@ def _check_sizes(rod: Rod, r: int) -> None:
         raise InvalidArgument(f"rod {r} state size")
     if sizes(st.frames) != m or sizes(st.angular_vel) != m:
         raise InvalidArgument(f"rod {r} frame count")
-    if len(rod.bones) and (rod.bone_weights is None or np.asarray(rod.bone_weights).size != n * len(rod.bones)):
-        raise InvalidArgument(f"rod {r} bone weights per vertex")
+    if len(rod.bones):
+        rows = rod.bone_weights
+        if rows is None or len(rows) != n:
+            raise InvalidArgument(f"rod {r} bone weights per vertex")
+        if any(len(row) != len(rod.bones) for row in rows):
+            raise InvalidArgument(f"rod {r} bone weight row size")
 
 
 def _rod_desc(rod: Rod, keep: list) -> capi.RodDesc:
