@@ -2,6 +2,7 @@
 
     python -m paper_1906_05260_b200 run  <scene.json | builtin:C1..C5> [--steps N] [--out DIR] [--deterministic]
     python -m paper_1906_05260_b200 bench <scene.json | builtin:C1..C5> [--steps N]
+    (either: --exact-shape-matching, the bit-identical shape-matching path)
 
 Scene files are the reference's schema-1 JSON (scene_json.py). `builtin:` names the benchmark
 workloads of this repository (workloads.CONFIGS); the reference's own builtin scenarios are its
@@ -30,13 +31,15 @@ def resolve_scene(lib, arg: str):
     return load_scene(lib, arg)
 
 
-def run_scene(scene, out_dir: str, steps: int, deterministic: bool) -> int:
+def run_scene(scene, out_dir: str, steps: int, deterministic: bool, exact: bool = False) -> int:
     """run_scene, vrod_main.cpp:45-101 (OBJ frames are out of scope)."""
     from . import Solver, SimulationError
     from .metrics import MetricsWriter, ProbeWriter
     scene.settings.deterministic = scene.settings.deterministic or deterministic
     os.makedirs(out_dir, exist_ok=True)
     solver = Solver(scene)
+    if exact:
+        solver.set_option("exact_shape_matching", 1)
     metrics = MetricsWriter(os.path.join(out_dir, "metrics.csv"), scene)
     probes = ProbeWriter(os.path.join(out_dir, "probes.csv"), scene)
     probes.write(0, solver.time(), solver.rod_state)
@@ -61,11 +64,13 @@ def run_scene(scene, out_dir: str, steps: int, deterministic: bool) -> int:
     return 0
 
 
-def cmd_bench(scene, steps: int) -> int:
+def cmd_bench(scene, steps: int, exact: bool = False) -> int:
     """cmd_bench, vrod_main.cpp:127-158, with device phase timings (StepReport.timings)."""
     from . import Solver, SimulationError
     solver = Solver(scene)
     solver.set_option("phase_timing", 1)
+    if exact:
+        solver.set_option("exact_shape_matching", 1)
     keys = ("predict_ms", "broad_ms", "narrow_ms", "solve_ms", "finalize_ms", "total_ms")
     total = dict.fromkeys(keys, 0.0)
     t0 = time.perf_counter()
@@ -99,6 +104,8 @@ def main(argv=None) -> int:
     bench = sub.add_parser("bench", help="measure stepping throughput")
     bench.add_argument("scene")
     bench.add_argument("--steps", type=int, default=100)
+    for p in (run, bench):  # shape matching in the reference's exact operation order (bit-identical results)
+        p.add_argument("--exact-shape-matching", action="store_true")
     args = ap.parse_args(argv)
     if args.steps < 0:
         ap.error("--steps must be non-negative")
@@ -111,8 +118,8 @@ def main(argv=None) -> int:
         print(f"error: {e}", file=sys.stderr)
         return 1
     if args.cmd == "run":
-        return run_scene(scene, args.out, args.steps, args.deterministic)
-    return cmd_bench(scene, args.steps)
+        return run_scene(scene, args.out, args.steps, args.deterministic, args.exact_shape_matching)
+    return cmd_bench(scene, args.steps, args.exact_shape_matching)
 
 
 if __name__ == "__main__":
