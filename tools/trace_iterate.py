@@ -1,6 +1,6 @@
 """Phase timeline of the persistent iteration kernel (CTA 0), VROD_TRACE=1: per iteration
 stage X / solve blocks / gather / barrier, then shape-matching levels; per-warp phases of CTA
-$VROD_TRACE_CTA in iteration 1. Usage: trace_iterate.py [C3]"""
+$VROD_TRACE_CTA in iteration 1. Usage: trace_iterate.py [C3 [warm-up steps, default 5]]"""
 import ctypes as C, os, sys
 os.environ["VROD_TRACE"] = "1"
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -11,7 +11,7 @@ from paper_1906_05260_b200 import workloads
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 lib = pb.library()
 s = pb.Solver(workloads.CONFIGS[name](lib))
-for _ in range(5):
+for _ in range(int(sys.argv[2]) if len(sys.argv) > 2 else 5):
     s.step()
 lib.vrod_bench_trace.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
 buf = (C.c_int64 * 1024)()
