@@ -216,6 +216,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
       : "memory");
 }
 
+// One 2D tensor copy (a box of rows x columns of a field-major FP64 array, as encoded in `map`)
+// into shared memory at dst (128-byte aligned), completing on the mbarrier `bar`; col: the box's
+// first column (slot), even.
+__device__ __forceinline__ void tma_rows(void* dst, const CUtensorMap* map, int col, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(0), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // Interior tiles of the per-sweep kernel: every needed row segment (TP + 2 doubles, 16-byte
 // aligned, a multiple of 16 bytes) is ONE bulk copy issued by the lanes of warp 0, all
 // completing on the tile's mbarrier (initialised by tile_meta's caller). A handful of
@@ -809,7 +820,9 @@ __device__ __forceinline__ void aux_ext_phase(const World& w, const Collide& c, 
 template <int TP, bool kExactShape>
 __global__ void __launch_bounds__(32 * (warps_for<TP>() + 1), 1) k_iterate(World w, Collide c, Groups g, PersistParams pp,
                                                                       SweepParams sp, int* singular,
-                                                                      unsigned long long* err) {
+                                                                      unsigned long long* err,
+                                                                      const __grid_constant__ CUtensorMap tm_x0,
+                                                                      const __grid_constant__ CUtensorMap tm_x1) {
   constexpr int kWarps = warps_for<TP>();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int kTileOwned = TP - 2, kTileStage = TP + 2;
@@ -823,6 +836,7 @@ __global__ void __launch_bounds__(32 * (warps_for<TP>() + 1), 1) k_iterate(World
   unsigned mask = 0;
   int ent_q0 = 0, ent_n = 0;  // staged entries: [ent_q0, ent_q0 + ent_n)
   if (!is_aux) {
+    if (tid == 0) mbar_init(&t.bar);  // the per-sweep tensor copy of the snapshot rows (published by tile_meta)
     mask = tile_meta(t, w, start);
     stage_rows(t, w, nullptr, nullptr, start, mask, T_SBAR, T_LAM);  // statics: once per substep
     if (has_ext) {
@@ -872,9 +886,16 @@ __global__ void __launch_bounds__(32 * (warps_for<TP>() + 1), 1) k_iterate(World
       if (it > 0) {
         for (int i = tid; i < kKinds * TP; i += 32 * kWarps) t.act[i / TP][i % TP] = 0;
       }
-      if (tid == 0) t.ent_next = 0;  // published by the __syncthreads below
-      stage_rows(t, w, cur, nullptr, start, mask, 0, T_SBAR);
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      if (tid == 0) {
+        t.ent_next = 0;  // published by the __syncthreads below
+        // the snapshot rows (CX .. QZ, slots start-2 .. start+31) in ONE tensor copy; the other CTAs'
+        // gathers wrote them before the grid barrier (generic proxy): order them before the async read
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        mbar_arrive_expect(&t.bar, static_cast<unsigned>(kStateFields * kTileStage * sizeof(double)));
+        tma_rows(&t.st[T_CX][0], (it & 1) ? &tm_x1 : &tm_x0, start - 2, &t.bar);
+      }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");  // the substep's static rows (first sweep)
+      mbar_wait(&t.bar, static_cast<unsigned>(it & 1));
       __syncthreads();
       mark();
       // Inline external blocks: every incidence entry of the tile's owned slots (a contiguous
@@ -1020,16 +1041,6 @@ struct alignas(128) WarpStage {
 };
 constexpr unsigned kWarpStageBytes =
     (kStateFields + kVStatFields + kSweepEStatFields + kLamFields) * kWCols * sizeof(double);
-
-// One 2D tensor copy (rows x 34 columns of a field-major array) into shared memory, completing
-// on the warp's mbarrier.
-__device__ __forceinline__ void tma_rows(void* dst, const CUtensorMap* map, int col, unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(0), "r"(smem_u32(bar))
-      : "memory");
-}
 
 // kStaged: the rod's rows are first copied into shared memory by the TMA engine — four 2D tensor
 // copies (X, vertex statics, element statics, multipliers) issued by one lane, completing on one
@@ -1433,9 +1444,9 @@ void launch_tiles(const World& w, Collide& c, const double* X, double* Y, const 
 constexpr int kPersistTP = 32;
 
 // Tensor map of the first `rows` fields of a field-major FP64 array (row stride vpad doubles):
-// boxes of rows x kWCols, zero fill out of range. Encoded once per (array, rows, vpad) through the
+// boxes of rows x cols, zero fill out of range. Encoded once per (array, rows, vpad) through the
 // driver entry point (no libcuda link), then passed by value as a __grid_constant__ parameter.
-CUtensorMap rows_map(const double* base, int rows, int vpad) {
+CUtensorMap rows_map(const double* base, int rows, int vpad, int cols = kWCols) {
   static const auto encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q{};
@@ -1445,15 +1456,15 @@ CUtensorMap rows_map(const double* base, int rows, int vpad) {
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }();
   static std::mutex mu;
-  static std::map<std::tuple<const void*, int, int>, CUtensorMap> cache;
+  static std::map<std::tuple<const void*, int, int, int>, CUtensorMap> cache;
   std::lock_guard<std::mutex> lock(mu);
-  const auto key = std::make_tuple(static_cast<const void*>(base), rows, vpad);
+  const auto key = std::make_tuple(static_cast<const void*>(base), rows, vpad, cols);
   const auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   CUtensorMap map;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(vpad), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(vpad) * sizeof(double)};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kWCols), static_cast<cuuint32_t>(rows)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(cols), static_cast<cuuint32_t>(rows)};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1537,10 +1548,12 @@ void launch_iterate_persistent(const World& w, Collide& c, const Groups& g, cons
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  const CUtensorMap t0 = rows_map(pp.X, kStateFields, w.vpad, kPersistTP + 2),
+                    t1 = rows_map(pp.Y, kStateFields, w.vpad, kPersistTP + 2);
   if (g.exact)
-    cudaLaunchKernelEx(&cfg, k_iterate<kPersistTP, true>, w, c, g, pp, sp, singular_counters, err);
+    cudaLaunchKernelEx(&cfg, k_iterate<kPersistTP, true>, w, c, g, pp, sp, singular_counters, err, t0, t1);
   else
-    cudaLaunchKernelEx(&cfg, k_iterate<kPersistTP, false>, w, c, g, pp, sp, singular_counters, err);
+    cudaLaunchKernelEx(&cfg, k_iterate<kPersistTP, false>, w, c, g, pp, sp, singular_counters, err, t0, t1);
 }
 
 }  // namespace vdev
