@@ -176,12 +176,31 @@ __device__ __forceinline__ bool pair_allowed(int ra, int ga, bool sa, int ea, in
 
 // ---- pipeline kernels ----------------------------------------------------------------------
 
-// rod_pills from the predicted state + the posed kinematic pills of this substep.
-__global__ void k_build_pills(World w, Collide c, const double* __restrict__ anim, AnimLayout al) {
+// Pill i's bounding sphere into bsph, the finiteness check; returns its radius bits (0 if not finite).
+__device__ __forceinline__ unsigned long long pill_bounds(const Collide& c, const PillV& p, int i, int substep,
+                                                         unsigned long long* err) {
+  V3 ctr;
+  double r;
+  bounding_sphere(p, ctr, r);
+  c.bsph[i] = ctr.x;
+  c.bsph[c.P + i] = ctr.y;
+  c.bsph[2 * c.P + i] = ctr.z;
+  c.bsph[3 * c.P + i] = r;
+  if (!(finite3(ctr) && isfinite(r))) {
+    if (c.P >= 2) atomicMin(err, err_code(substep, ERR_BROAD, 0, i));
+    return 0;
+  }
+  return static_cast<unsigned long long>(__double_as_longlong(r));  // r >= 0: bit order == value order
+}
+// rod_pills from the predicted state + the posed kinematic pills of this substep. bounds != 0
+// (single-scene worlds; the broad phase's resets already ran): each pill's bounding sphere and the
+// max radius too (k_bounds' work, one launch less).
+__global__ void k_build_pills(World w, Collide c, const double* __restrict__ anim, AnimLayout al, int bounds,
+                              int substep, unsigned long long* err) {
   pdl_wait();
   pdl_trigger();
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  const int P = c.P;
+  unsigned long long bits = 0;
   if (v < w.V) {
     const int k = w.slot_loc[v], m = w.slot_m[v];
     if (k < m) {
@@ -189,17 +208,33 @@ __global__ void k_build_pills(World w, Collide c, const double* __restrict__ ani
       const int i = v - r;
       const int vp = w.vpad;
       const double* X = w.X;
+      const PillV p{V3{X[CX * vp + v], X[CY * vp + v], X[CZ * vp + v]},
+                    V3{X[CX * vp + v + 1], X[CY * vp + v + 1], X[CZ * vp + v + 1]},
+                    X[S * vp + v] * w.vstat[RBAR * vp + v], X[S * vp + v + 1] * w.vstat[RBAR * vp + v + 1]};
       double2* o = reinterpret_cast<double2*>(c.pill + 8ll * i);
-      o[0] = make_double2(X[CX * vp + v], X[CY * vp + v]);
-      o[1] = make_double2(X[CZ * vp + v], X[CX * vp + v + 1]);
-      o[2] = make_double2(X[CY * vp + v + 1], X[CZ * vp + v + 1]);
-      o[3] = make_double2(X[S * vp + v] * w.vstat[RBAR * vp + v], X[S * vp + v + 1] * w.vstat[RBAR * vp + v + 1]);
+      o[0] = make_double2(p.c0.x, p.c0.y);
+      o[1] = make_double2(p.c0.z, p.c1.x);
+      o[2] = make_double2(p.c1.y, p.c1.z);
+      o[3] = make_double2(p.r0, p.r1);
+      if (bounds) bits = pill_bounds(c, p, i, substep, err);
     }
   }
   if (v < al.n_kin) {
     const double* kp = anim + al.off_kin + 8 * v;
     const int i = w.E + v;
     for (int f = 0; f < 8; ++f) c.pill[8ll * i + f] = kp[f];
+    if (bounds) {
+      const unsigned long long b2 = pill_bounds(c, PillV{V3{kp[0], kp[1], kp[2]}, V3{kp[3], kp[4], kp[5]}, kp[6], kp[7]},
+                                                i, substep, err);
+      bits = b2 > bits ? b2 : bits;
+    }
+  }
+  if (bounds) {  // warp max, one atomic per warp (max is order independent)
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long x = __shfl_down_sync(0xffffffffu, bits, o);
+      bits = x > bits ? x : bits;
+    }
+    if ((threadIdx.x & 31) == 0 && bits) atomicMax(c.maxr_bits, bits);
   }
 }
 
@@ -209,21 +244,7 @@ __global__ void k_bounds(Collide c, int substep, unsigned long long* err) {
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long bits = 0;
-  if (i < c.P) {
-    const PillV p = load_pill(c.pill, c.P, i);
-    V3 ctr;
-    double r;
-    bounding_sphere(p, ctr, r);
-    c.bsph[i] = ctr.x;
-    c.bsph[c.P + i] = ctr.y;
-    c.bsph[2 * c.P + i] = ctr.z;
-    c.bsph[3 * c.P + i] = r;
-    if (!(finite3(ctr) && isfinite(r))) {
-      if (c.P >= 2) atomicMin(err, err_code(substep, ERR_BROAD, 0, i));
-    } else {
-      bits = static_cast<unsigned long long>(__double_as_longlong(r));  // r >= 0: bit order == value order
-    }
-  }
+  if (i < c.P) bits = pill_bounds(c, load_pill(c.pill, c.P, i), i, substep, err);
   // warp max, one atomic per warp (max is order independent); a batch keeps one max per scene
   const int sc = c.pill_scene && i < c.P ? c.pill_scene[i] : 0;
   const int sc0 = __shfl_sync(0xffffffffu, sc, 0);
@@ -978,13 +999,49 @@ __device__ __forceinline__ int block_excl_1024(int v, int* total, int* ws) {
   __syncthreads();
   return r;
 }
-__global__ void __launch_bounds__(kOrderThreads) k_ct_order(Collide c, int smem_cap) {
+// The warm-start list entry of ordered contact k (pair key, frozen alpha; k_warm_build without the
+// kinematic split) and the substep's contact counters (k_warm_counts), for the fused small-world
+// ordering kernel.
+__device__ __forceinline__ void warm_rr_put(const Collide& c, int k, int a, int b, double alpha) {
+  const unsigned long long key = pair_key(c.pill_id[a], c.pill_id[b]);
+  const int scene = c.pill_scene ? c.pill_scene[a] : 0;
+  if (c.pill_scene) {
+    atomicAdd(&c.scene_acc[scene].contact_count, 1);
+    c.warm_rr_scene[k] = scene;
+  }
+  c.warm_rr_key[k] = key;
+  c.warm_rr_alpha[k] = alpha;
+}
+__device__ __forceinline__ void warm_counts_unsplit(const Collide& c, StepAccum* acc, int n) {
+  atomicAdd(&acc->contact_count, n);
+  atomicAdd(&acc->broad_pairs, c.scalars[SC_BROAD]);
+  if (c.scalars[SC_NCT_RAW] > acc->max_contacts) acc->max_contacts = c.scalars[SC_NCT_RAW];
+  if (c.scalars[SC_NCAND_RAW] > acc->max_candidates) acc->max_candidates = c.scalars[SC_NCAND_RAW];
+  c.scalars[SC_NRK_PREV] = 0;
+  c.scalars[SC_NRR_PREV] = n;
+}
+
+// `acc` non-null (small worlds without kinematic pills): the ordering kernel also clamps the raw
+// contact count (k_clamp_raw), builds the warm-start list (k_warm_build) and the counters
+// (k_warm_counts) — three launches less per substep, the same writes.
+__global__ void __launch_bounds__(kOrderThreads) k_ct_order(Collide c, int smem_cap, StepAccum* acc) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ unsigned long long okey[];  // smem_cap packed keys
   __shared__ int ws[32];
-  const int n = c.scalars[SC_NCT];
   const int tid = threadIdx.x;
+  int n;
+  if (acc) {  // k_clamp_raw (contacts) + k_warm_counts
+    const int raw = c.scalars[SC_NCT_RAW];
+    n = raw > c.contact_cap ? static_cast<int>(c.contact_cap) : raw;
+    if (tid == 0) {
+      if (raw > c.contact_cap) atomicExch(&c.scalars[SC_OVF], 2);
+      c.scalars[SC_NCT] = n;
+      warm_counts_unsplit(c, acc, n);
+    }
+  } else {
+    n = c.scalars[SC_NCT];
+  }
   if (n == 0) return;
   if (n <= smem_cap && c.P <= 65536) {
     // packed key (i << 48 | j << 32 | raw index): pill ids < 2^16 here, so sorting the packed
@@ -1004,10 +1061,13 @@ __global__ void __launch_bounds__(kOrderThreads) k_ct_order(Collide c, int smem_
     bar();
     auto emit = [&](int r, unsigned long long key) {
       const int q = static_cast<int>(key & 0xffffffffu);
-      c.ct_a[r] = static_cast<int>(key >> 48);
-      c.ct_b[r] = static_cast<int>((key >> 32) & 0xffffu);
-      c.ct_alpha[r] = c.raw_ab[q];
+      const int a = static_cast<int>(key >> 48), b = static_cast<int>((key >> 32) & 0xffffu);
+      const double alpha = c.raw_ab[q];
+      c.ct_a[r] = a;
+      c.ct_b[r] = b;
+      c.ct_alpha[r] = alpha;
       c.ct_beta[r] = c.raw_ab[c.contact_cap + q];
+      if (acc) warm_rr_put(c, r, a, b, alpha);
     };
     if (rank) {  // one key per thread: its rank among the (unique) keys, broadcast pair reads
       if (tid >= n) return;
@@ -1065,6 +1125,10 @@ __global__ void __launch_bounds__(kOrderThreads) k_ct_order(Collide c, int smem_
   }
   __syncthreads();
   for (int i = tid; i < P; i += kOrderThreads) sort_pill_contacts(c, i);
+  if (acc) {
+    __syncthreads();
+    for (int k = tid; k < n; k += kOrderThreads) warm_rr_put(c, k, c.ct_a[k], c.ct_b[k], c.ct_alpha[k]);
+  }
 }
 
 // Narrow phase over the candidate list (find_contacts, collision.cpp:261-271).
@@ -1276,11 +1340,11 @@ int order_cap_for(int P) {
   return P < kCellPathMinPills ? 4096 : -1;
 }
 
-void launch_order_contacts(Collide& c, cudaStream_t st) {
+void launch_order_contacts(Collide& c, cudaStream_t st, StepAccum* fuse_acc) {
   if (c.order_smem_cap >= 0) {  // one CTA (small worlds)
     const std::size_t smem = 8ull * (c.order_smem_cap + 2);
     cudaFuncSetAttribute(k_ct_order, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    launch_kernel(k_ct_order, 1, kOrderThreads, smem, st, g_pdl, c, c.order_smem_cap);
+    launch_kernel(k_ct_order, 1, kOrderThreads, smem, st, g_pdl, c, c.order_smem_cap, fuse_acc);
     return;
   }
   const int g = grid_for(c.contact_cap);
@@ -1299,12 +1363,9 @@ void launch_order_contacts(Collide& c, cudaStream_t st) {
 // the (unordered) candidates are left in cand_i/cand_j, scalars[SC_NCAND].
 cudaEvent_t g_broad_mark = nullptr;
 
-void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int prefilter, int do_narrow,
-                         int split_warm, int store_d, cudaStream_t st) {
-  (void)store_d;
-  const int P = c.P;
-  const int b = (P + kThreads - 1) / kThreads;
-  FillList f;  // per-call resets, one launch
+// The broad phase's per-call resets, one fill launch.
+void launch_broad_resets(Collide& c, int do_narrow, cudaStream_t st) {
+  FillList f;
   f.add(c.maxr_bits, 2, 0);
   if (c.pill_scene) f.add(c.scene_maxr, 2ll * c.n_scenes, 0);
   f.add(c.table, c.T, -1);
@@ -1315,9 +1376,17 @@ void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
   f.add(c.scalars + SC_NCT_RAW, 1, 0);
   if (do_narrow) f.add(c.scalars + SC_NCAND2, 1, 0);  // k_seg_filter's counter
   launch_fill(f, st);
+}
+
+bool launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int prefilter, int do_narrow,
+                         int split_warm, int store_d, cudaStream_t st, StepAccum* fuse_acc, bool prepared) {
+  (void)store_d;
+  const int P = c.P;
+  const int b = (P + kThreads - 1) / kThreads;
+  if (!prepared) launch_broad_resets(c, do_narrow, st);  // else: resets, bounds and max radius done by the caller
   bool fused_seg = false;
   if (P > 0) {
-    launch_kernel(k_bounds, b, kThreads, 0, st, g_pdl, c, substep, err);
+    if (!prepared) launch_kernel(k_bounds, b, kThreads, 0, st, g_pdl, c, substep, err);
     launch_kernel(k_insert, b, kThreads, 0, st, g_pdl, c);
   }
   scan_exclusive(c.cell_count, c.cell_start, c.T, nullptr, c.scan_tmp, c.scan_parts, st);
@@ -1343,31 +1412,37 @@ void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
                   int(SC_NCAND_RAW), 1);
   } else {
     launch_kernel(k_clamp_raw, 1, 1, 0, st, g_pdl, c.scalars, SC_NCAND_RAW, SC_NCAND, c.cand_cap, 1);
-    if (!do_narrow) return;
+    if (!do_narrow) return false;
     launch_kernel(k_seg_filter, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c);
     launch_kernel(k_narrow_append<false>, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c, split_warm, -1, 0);
   }
-  launch_kernel(k_clamp_raw, 1, 1, 0, st, g_pdl, c.scalars, SC_NCT_RAW, SC_NCT, c.contact_cap, 2);
-  launch_order_contacts(c, st);
+  // small worlds without kinematic pills: the ordering kernel clamps the count and builds the warm list
+  const bool fused = fuse_acc && c.order_smem_cap >= 0 && !split_warm;
+  if (!fused) launch_kernel(k_clamp_raw, 1, 1, 0, st, g_pdl, c.scalars, SC_NCT_RAW, SC_NCT, c.contact_cap, 2);
+  launch_order_contacts(c, st, fused ? fuse_acc : nullptr);
+  return fused;
 }
 
 // Standalone broad_phase: every allowed pair, in the reference's (i, j) order.
 void launch_broad_ordered(Collide& c, unsigned long long* err, cudaStream_t st) {
-  launch_broad_narrow(c, 0, err, 0, 0, 0, 0, st);
+  launch_broad_narrow(c, 0, err, 0, 0, 0, 0, st, nullptr, false);
   launch_kernel(k_cand_to_raw, grid_for(c.cand_cap), kThreads, 0, st, g_pdl, c);
-  launch_order_contacts(c, st);
+  launch_order_contacts(c, st, nullptr);
 }
 
 void launch_collide(const World& w, Collide& c, const double* anim, const AnimLayout& al, int substep,
                     unsigned long long* err, StepAccum* acc, int possible, cudaStream_t st) {
   const int nb = (std::max(w.V, al.n_kin) + kThreads - 1) / kThreads;
-  launch_kernel(k_build_pills, nb, kThreads, 0, st, g_pdl, w, c, anim, al);
+  // single-scene worlds: the broad phase's resets first, then the pills with their bounding spheres
+  const bool fused_bounds = possible && !c.pill_scene;
+  if (fused_bounds) launch_broad_resets(c, 1, st);
+  launch_kernel(k_build_pills, nb, kThreads, 0, st, g_pdl, w, c, anim, al, fused_bounds ? 1 : 0, substep, err);
   if (!possible) {  // no pair can pass pair_allowed: only broad_phase's finiteness check remains
     if (c.P >= 2) launch_kernel(k_bounds, (c.P + kThreads - 1) / kThreads, kThreads, 0, st, g_pdl, c, substep, err);
     return;
   }
   const int split = w.K > 0 ? 1 : 0;
-  launch_broad_narrow(c, substep, err, 1, 1, split, 0, st);
+  if (launch_broad_narrow(c, substep, err, 1, 1, split, 0, st, acc, fused_bounds)) return;  // warm list built by the ordering
   const int g = grid_for(c.contact_cap);
   if (split) {
     launch_kernel(k_warm_flags, g, kThreads, 0, st, g_pdl, c);

@@ -278,8 +278,10 @@ void launch_copy_state(const World& w, const double* src, double* dst, cudaStrea
 extern cudaEvent_t g_broad_mark;
 void launch_collide(const World& w, Collide& c, const double* anim, const AnimLayout& al, int substep,
                     unsigned long long* err, StepAccum* acc, int possible, cudaStream_t st);
-void launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int prefilter, int do_narrow,
-                         int split_warm, int store_d, cudaStream_t st);
+// Returns true when the ordering kernel also built the warm-start list and counters (fuse_acc).
+bool launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int prefilter, int do_narrow,
+                         int split_warm, int store_d, cudaStream_t st, StepAccum* fuse_acc = nullptr,
+                         bool prepared = false);
 void launch_narrow_only(Collide& c, int split_warm, int store_d, cudaStream_t st);
 int order_cap_for(int P);  // Collide::order_smem_cap for a world of P pills
 void launch_broad_ordered(Collide& c, unsigned long long* err, cudaStream_t st);
