@@ -302,12 +302,56 @@ __global__ void k_insert(Collide c) {
   atomicAdd(&c.cell_count[h], 1);
 }
 
-// Non-empty cells listed in representative-pill order (spatially coherent, deterministic).
-__global__ void k_cell_list(Collide c) {
+// Non-empty cells listed in representative-pill order (spatially coherent, deterministic), each
+// with the spans (first position in the cell-sorted arrays, size) of its half-stencil
+// neighbourhood (see k_pairs_cell): the cell itself and its 13 lexicographically positive
+// neighbours. The representative's thread probes the 13 neighbours' hash chains side by side
+// (first probes, key checks and span loads each issued together), so the pair scan starts from
+// ready spans instead of walking those chains cell by cell.
+constexpr int kHalfStencil = 14;
+__device__ __forceinline__ int find_cell(const Collide& c, long long kx, long long ky, long long kz, int scene);
+__global__ void __launch_bounds__(128) k_cell_list(Collide c) {
   pdl_wait();
   pdl_trigger();
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c.P; i += gridDim.x * blockDim.x)
-    if (c.rep_flag[i]) c.cell_list[c.rep_pos[i]] = c.pill_cell[i];
+  const int P = c.P;
+  const unsigned mask = static_cast<unsigned>(c.T - 1);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+    if (!c.rep_flag[i]) continue;
+    const int ci = c.rep_pos[i];
+    const int h = c.pill_cell[i];
+    c.cell_list[ci] = h;
+    const int scene = c.pill_scene ? c.pill_scene[i] : 0;
+    const long long kx = c.cellkey[i], ky = c.cellkey[P + i], kz = c.cellkey[2 * P + i];
+    // first probes of the 13 chains side by side: (span, key) of each hashed slot
+    int a0[kHalfStencil - 1], a1[kHalfStencil - 1];
+    bool hit[kHalfStencil - 1];
+#pragma unroll
+    for (int l = 1; l < kHalfStencil; ++l) {  // offsets (o/9-1, (o/3)%3-1, o%3-1), o = 13 + l
+      const int o = 13 + l;
+      const long long x = kx + (o / 9 - 1), y = ky + ((o / 3) % 3 - 1), z = kz + (o % 3 - 1);
+      const int hh = static_cast<int>(static_cast<unsigned>(cell_hash(x, y, z, scene)) & mask);
+      a0[l - 1] = c.cell_start[hh];
+      a1[l - 1] = c.cell_start[hh + 1];
+      const longlong4 k = c.slot_key[hh];
+      hit[l - 1] = k.x == x && k.y == y && k.z == z && k.w == scene;
+    }
+    int2* span = c.cell_span + static_cast<long long>(kHalfStencil) * ci;
+    span[0] = make_int2(c.cell_start[h], c.cell_start[h + 1] - c.cell_start[h]);
+#pragma unroll
+    for (int l = 1; l < kHalfStencil; ++l) {
+      const int o = 13 + l;
+      int2 v = make_int2(0, 0);
+      if (a0[l - 1] != a1[l - 1]) {  // occupied slot
+        if (hit[l - 1]) {
+          v = make_int2(a0[l - 1], a1[l - 1] - a0[l - 1]);
+        } else {  // rare: another cell in the slot, follow the chain
+          const int hn = find_cell(c, kx + (o / 9 - 1), ky + ((o / 3) % 3 - 1), kz + (o % 3 - 1), scene);
+          if (hn >= 0) v = make_int2(c.cell_start[hn], c.cell_start[hn + 1] - c.cell_start[hn]);
+        }
+      }
+      span[l] = v;
+    }
+  }
 }
 
 __global__ void k_scatter(Collide c) {
@@ -318,6 +362,8 @@ __global__ void k_scatter(Collide c) {
   const int h = c.pill_cell[i];
   const int pos = c.cell_start[h] + atomicAdd(&c.cell_cursor[h], 1);
   c.cell_items[pos] = i;
+  if (c.rep_flag[i])  // the slot's key, read beside cell_start by find_cell (one load round per probe)
+    c.slot_key[h] = make_longlong4(c.cellkey[i], c.cellkey[c.P + i], c.cellkey[2 * c.P + i], c.pill_scene ? c.pill_scene[i] : 0);
   // cell-sorted copies of what the pair scan reads per neighbour: contiguous per cell, so the
   // scan's loads are coalesced and need no second indirection
   c.cell_attr[pos] = make_int4(i, c.pill_rod[i], c.pill_group[i], 2 * c.pill_el[i] + (c.pill_self[i] ? 1 : 0));
@@ -326,15 +372,18 @@ __global__ void k_scatter(Collide c) {
   sp[1] = make_double2(c.bsph[2 * c.P + i], c.bsph[3 * c.P + i]);
 }
 
+// The table slot of cell (kx, ky, kz, scene), or -1 (after k_scatter). An occupied slot has a
+// non-empty span in cell_start, and its key in slot_key: the three loads of a probe are
+// independent, so each probe of the linear chain costs one load round; the chain ends at the
+// first empty slot.
 __device__ __forceinline__ int find_cell(const Collide& c, long long kx, long long ky, long long kz, int scene) {
   const unsigned mask = static_cast<unsigned>(c.T - 1);
   unsigned h = static_cast<unsigned>(cell_hash(kx, ky, kz, scene)) & mask;
   while (true) {
-    const int e = c.table[h];
-    if (e < 0) return -1;
-    if (c.cellkey[e] == kx && c.cellkey[c.P + e] == ky && c.cellkey[2 * c.P + e] == kz &&
-        (!c.pill_scene || c.pill_scene[e] == scene))
-      return static_cast<int>(h);
+    const int a = c.cell_start[h], b = c.cell_start[h + 1];
+    const longlong4 k = c.slot_key[h];
+    if (a == b) return -1;
+    if (k.x == kx && k.y == ky && k.z == kz && k.w == scene) return static_cast<int>(h);
     h = (h + 1) & mask;
   }
 }
@@ -568,16 +617,18 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) k_pairs_warp(Collide c, in
 // One WARP per non-empty grid cell (table slot), over a HALF stencil: the cell itself and the 13
 // neighbours whose offset is lexicographically positive, so every pair of distinct cells is
 // visited from exactly one side (the reference's 27-cell scan with j > i visits each pair from
-// both sides and drops one). Lanes 0..13 probe those 14 cells; the cell's member pills are staged
-// in shared memory, and the warp strides over the flattened neighbourhood items j, loading each j
-// once and testing it against every member i. It counts every allowed pair once — j > i within
-// the cell, any order across cells, evaluated as pair_allowed(pills[min], pills[max]) (its one
-// asymmetric operand, the first pill's self_collide, is taken from the lower index; the sphere
-// test is symmetric: commutative sums and squared differences) — for broad_phase (collision.cpp:213-226, StepReport.broad_pairs; the reference
-// has no overlap test), and keeps the pairs whose bounding spheres touch (prefilter; all allowed
-// pairs without it) as (min, max). Kept pairs collect in a per-warp shared buffer flushed with
-// one atomic per fill. The list is unordered; contacts are put in (i, j) order after the narrow
-// phase.
+// both sides and drops one). The 14 spans come ready from k_cell_list (lane l loads span l; the
+// next cell's spans are loaded while this one is scanned). The cell's member pills are staged
+// in shared memory from the cell-sorted copies (cell_attr, cell_sph), and the warp strides over
+// the flattened neighbourhood items j, loading each j once and testing it against every member
+// i. It counts every allowed pair once — j > i within the cell, any order across cells,
+// evaluated as pair_allowed(pills[min], pills[max]) (its one asymmetric operand, the first
+// pill's self_collide, is taken from the lower index; the sphere test is symmetric: commutative
+// sums and squared differences) — for broad_phase (collision.cpp:213-226,
+// StepReport.broad_pairs; the reference has no overlap test), and keeps the pairs whose bounding
+// spheres touch (prefilter; all allowed pairs without it) as (min, max). Kept pairs collect in a
+// per-warp shared buffer flushed with one atomic per fill. The list is unordered; contacts are
+// put in (i, j) order after the narrow phase.
 constexpr int kCellWarps = 8;
 constexpr int kCellPathMinPills = 1 << 16;
 constexpr int kCellBuf = 128;
@@ -585,33 +636,27 @@ __global__ void __launch_bounds__(32 * kCellWarps) k_pairs_cell(Collide c, int p
                                                                 int* cand_total) {
   pdl_wait();
   pdl_trigger();
-  constexpr int kHalf = 14;  // the cell + 13 lexicographically positive neighbours
+  constexpr int kHalf = kHalfStencil;
   __shared__ int s_start[kCellWarps][kHalf];
   __shared__ int s_off[kCellWarps][kHalf + 1];
-  __shared__ int s_mi[kCellWarps][32], s_mrod[kCellWarps][32], s_mgrp[kCellWarps][32], s_mel[kCellWarps][32];
-  __shared__ uint8_t s_mself[kCellWarps][32];
-  __shared__ double s_mb[kCellWarps][4][32];
+  __shared__ int4 s_ma[kCellWarps][32];
+  __shared__ double2 s_m01[kCellWarps][32], s_m23[kCellWarps][32];
   __shared__ int s_buf[kCellWarps][2][kCellBuf];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int P = c.P;
   const int ncells = c.rep_pos[P];
+  const int4* __restrict__ attr = c.cell_attr;
+  const double2* __restrict__ sph = reinterpret_cast<const double2*>(c.cell_sph);
+  const int cstride = gridDim.x * kCellWarps;
   int broad = 0, nbuf = 0, scene_broad_done = 0;
-  for (int ci = blockIdx.x * kCellWarps + warp; ci < ncells; ci += gridDim.x * kCellWarps) {
-  const int h = c.cell_list[ci];
-  const int n_c = c.cell_count[h];
-  const int rep = c.table[h];
-  const int scene = c.pill_scene ? c.pill_scene[rep] : 0;
-  int size = 0;
-  if (lane < kHalf) {
-    const int o = 13 + lane;  // offsets (o/9-1, (o/3)%3-1, o%3-1): 13 = (0,0,0), 14..26 positive
-    const int hn = lane == 0 ? h
-                             : find_cell(c, c.cellkey[rep] + (o / 9 - 1), c.cellkey[P + rep] + ((o / 3) % 3 - 1),
-                                         c.cellkey[2 * P + rep] + (o % 3 - 1), scene);
-    if (hn >= 0) {
-      s_start[warp][lane] = c.cell_start[hn];
-      size = c.cell_start[hn + 1] - c.cell_start[hn];
-    }
-  }
+  int ci = blockIdx.x * kCellWarps + warp;
+  int2 nspan = make_int2(0, 0);
+  if (ci < ncells && lane < kHalf) nspan = c.cell_span[static_cast<long long>(kHalf) * ci + lane];
+  for (; ci < ncells; ci += cstride) {
+  const int2 span = nspan;
+  if (ci + cstride < ncells && lane < kHalf) nspan = c.cell_span[static_cast<long long>(kHalf) * (ci + cstride) + lane];
+  const int size = lane < kHalf ? span.y : 0;
+  if (lane < kHalf) s_start[warp][lane] = span.x;
   int incl = size;
 #pragma unroll
   for (int o = 1; o < 16; o <<= 1) {
@@ -621,7 +666,8 @@ __global__ void __launch_bounds__(32 * kCellWarps) k_pairs_cell(Collide c, int p
   if (lane < kHalf) s_off[warp][lane + 1] = incl;
   if (lane == 0) s_off[warp][0] = 0;
   const int total = __shfl_sync(0xffffffffu, incl, kHalf - 1);
-  const int mbase = c.cell_start[h];
+  const int mbase = __shfl_sync(0xffffffffu, span.x, 0);
+  const int n_c = __shfl_sync(0xffffffffu, span.y, 0);
   auto flush = [&]() {
     int base = 0;
     if (lane == 0) base = atomicAdd(cand_total, nbuf);
@@ -636,49 +682,44 @@ __global__ void __launch_bounds__(32 * kCellWarps) k_pairs_cell(Collide c, int p
     __syncwarp();
     nbuf = 0;
   };
+  int scene = 0;
   for (int ib = 0; ib < n_c; ib += 32) {
     const int nm = min(32, n_c - ib);
     __syncwarp();
     if (lane < nm) {
-      const int i = c.cell_items[mbase + ib + lane];
-      s_mi[warp][lane] = i;
-      s_mrod[warp][lane] = c.pill_rod[i];
-      s_mgrp[warp][lane] = c.pill_group[i];
-      s_mel[warp][lane] = c.pill_el[i];
-      s_mself[warp][lane] = c.pill_self[i];
-#pragma unroll
-      for (int f = 0; f < 4; ++f) s_mb[warp][f][lane] = c.bsph[f * P + i];
+      const int pos = mbase + ib + lane;
+      s_ma[warp][lane] = attr[pos];
+      s_m01[warp][lane] = sph[2 * pos];
+      s_m23[warp][lane] = sph[2 * pos + 1];
     }
     __syncwarp();
+    if (ib == 0 && c.pill_scene) scene = c.pill_scene[s_ma[warp][0].x];
     int cur_d = 0;  // a lane's k only grows, so its cell index only moves forward
     for (int k0 = 0; k0 < total; k0 += 32) {
       const int k = k0 + lane;
-      int j = -1, rj = 0, gj = 0, ej = 0;
-      bool sj = false;
-      double jx = 0, jy = 0, jz = 0, jr = 0;
+      int4 at = make_int4(-1, 0, 0, 0);
+      double2 j01 = make_double2(0, 0), j23 = make_double2(0, 0);
       if (k < total) {
         while (s_off[warp][cur_d + 1] <= k) ++cur_d;
-        j = c.cell_items[s_start[warp][cur_d] + (k - s_off[warp][cur_d])];
-        rj = c.pill_rod[j];
-        gj = c.pill_group[j];
-        ej = c.pill_el[j];
-        sj = c.pill_self[j] != 0;
-        jx = c.bsph[j];
-        jy = c.bsph[P + j];
-        jz = c.bsph[2 * P + j];
-        jr = c.bsph[3 * P + j];
+        const int pos = s_start[warp][cur_d] + (k - s_off[warp][cur_d]);
+        at = attr[pos];
+        j01 = sph[2 * pos];
+        j23 = sph[2 * pos + 1];
       }
+      const int j = at.x;
+      const bool sj = (at.w & 1) != 0;
       for (int m = 0; m < nm; ++m) {
-        const int i = s_mi[warp][m];
+        const int4 mi = s_ma[warp][m];
+        const int i = mi.x;
         bool cand = false;
         // pair_allowed(pills[min], pills[max]): its only asymmetry is the first pill's self_collide
         if (j >= 0 && (cur_d > 0 || j > i) &&
-            pair_allowed(s_mrod[warp][m], s_mgrp[warp][m], j > i ? s_mself[warp][m] != 0 : sj, s_mel[warp][m], rj, gj,
-                         ej)) {
+            pair_allowed(mi.y, mi.z, j > i ? (mi.w & 1) != 0 : sj, mi.w >> 1, at.y, at.z, at.w >> 1)) {
           ++broad;
           if (prefilter) {  // spheres_touch, same arithmetic
-            const double dx = s_mb[warp][0][m] - jx, dy = s_mb[warp][1][m] - jy, dz = s_mb[warp][2][m] - jz;
-            const double rr = (s_mb[warp][3][m] + jr) * (1.0 + 1e-9) + 1e-12;
+            const double2 m01 = s_m01[warp][m], m23 = s_m23[warp][m];
+            const double dx = m01.x - j01.x, dy = m01.y - j01.y, dz = m23.x - j23.x;
+            const double rr = (m23.y + j23.y) * (1.0 + 1e-9) + 1e-12;
             cand = dx * dx + dy * dy + dz * dz <= rr * rr;
           } else {
             cand = true;
@@ -1401,7 +1442,7 @@ bool launch_broad_narrow(Collide& c, int substep, unsigned long long* err, int p
                     c.scalars + SC_BROAD, c.scalars + SC_NCAND_RAW, c.cand_i, c.cand_j);
     } else {  // large worlds: one warp per non-empty cell, neighbourhood loads shared by its pills
       scan_exclusive(c.rep_flag, c.rep_pos, P, nullptr, c.scan_tmp, c.scan_parts, st);
-      launch_kernel(k_cell_list, b, kThreads, 0, st, g_pdl, c);
+      launch_kernel(k_cell_list, (P + 127) / 128, 128, 0, st, g_pdl, c);
       launch_kernel(k_pairs_cell, std::min((P + kCellWarps - 1) / kCellWarps, 148 * 16), 32 * kCellWarps, 0, st,
                     g_pdl, c, prefilter, c.scalars + SC_BROAD, c.scalars + SC_NCAND_RAW);
     }

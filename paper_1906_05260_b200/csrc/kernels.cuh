@@ -54,6 +54,7 @@ struct Collide {
   int* cell_count = nullptr;     // T
   int* cell_start = nullptr;     // T+1
   int* cell_cursor = nullptr;    // T
+  longlong4* slot_key = nullptr; // T: key (kx, ky, kz, scene) of an occupied table slot (written by k_scatter)
   int* cell_items = nullptr;     // P
   int4* cell_attr = nullptr;     // P, cell-sorted: (pill, rod, group, 2 * element + self)
   double* cell_sph = nullptr;    // 4 x P, cell-sorted AoS bounding spheres (cx cy cz R)
@@ -61,6 +62,7 @@ struct Collide {
   int* rep_flag = nullptr;       // P+1: pill is its cell's representative
   int* rep_pos = nullptr;        // P+1: exclusive scan of rep_flag ([P] = cell count)
   int* cell_list = nullptr;      // P: non-empty table slots, representative order
+  int2* cell_span = nullptr;     // 14 x P: per non-empty cell, its half-stencil neighbourhood spans (start, size)
   // candidates
   int* cand_count = nullptr;     // P+1
   int* cand_off = nullptr;       // P+1

@@ -151,6 +151,7 @@ Solver::Solver(const SceneData& scene, const BatchLayout* batch) : scene_(scene)
   c_.cell_count = dalloc<int>(c_.T);
   c_.cell_start = dalloc<int>(c_.T + 1);
   c_.cell_cursor = dalloc<int>(c_.T);
+  c_.slot_key = dalloc<longlong4>(c_.T);
   c_.cell_items = dalloc<int>(c_.P);
   c_.order_smem_cap = vdev::order_cap_for(c_.P);
   c_.cell_attr = dalloc<int4>(std::max(c_.P, 1));
@@ -159,6 +160,7 @@ Solver::Solver(const SceneData& scene, const BatchLayout* batch) : scene_(scene)
   c_.rep_flag = dalloc<int>(c_.P + 1);
   c_.rep_pos = dalloc<int>(c_.P + 1);
   c_.cell_list = dalloc<int>(c_.P);
+  c_.cell_span = dalloc<int2>(14ull * std::max(c_.P, 1));
   c_.cand_i = dalloc<int>(c_.cand_cap);
   c_.cand_j = dalloc<int>(c_.cand_cap);
   c_.cand2_i = dalloc<int>(c_.cand_cap);

@@ -84,6 +84,7 @@ void make_collide(Buf& b, vdev::Collide& c, const vrod_pill* pills, int P, long 
   c.cell_count = b.get<int>(c.T);
   c.cell_start = b.get<int>(c.T + 1);
   c.cell_cursor = b.get<int>(c.T);
+  c.slot_key = b.get<longlong4>(c.T);
   c.cell_items = b.get<int>(P);
   // broad_phase lists every allowed pair (often far more than one CTA sorts well): multi-launch
   // ordering unless a test forces a path
@@ -94,6 +95,7 @@ void make_collide(Buf& b, vdev::Collide& c, const vrod_pill* pills, int P, long 
   c.rep_flag = b.get<int>(P + 1);
   c.rep_pos = b.get<int>(P + 1);
   c.cell_list = b.get<int>(P);
+  c.cell_span = b.get<int2>(14ull * std::max(P, 1));
   c.raw_i = b.get<int>(cap);
   c.raw_j = b.get<int>(cap);
   c.raw_ab = b.get<double>(2 * cap);
