@@ -1405,8 +1405,9 @@ void launch_order_contacts(Collide& c, cudaStream_t st, StepAccum* fuse_acc) {
 cudaEvent_t g_broad_mark = nullptr;
 
 // The broad phase's per-call resets, one fill launch.
-void launch_broad_resets(Collide& c, int do_narrow, cudaStream_t st) {
-  FillList f;
+bool g_broad_resets_done = false;
+
+void broad_reset_list(const Collide& c, int do_narrow, FillList& f) {
   f.add(c.maxr_bits, 2, 0);
   if (c.pill_scene) f.add(c.scene_maxr, 2ll * c.n_scenes, 0);
   f.add(c.table, c.T, -1);
@@ -1416,6 +1417,11 @@ void launch_broad_resets(Collide& c, int do_narrow, cudaStream_t st) {
   f.add(c.scalars + SC_NCAND_RAW, 1, 0);
   f.add(c.scalars + SC_NCT_RAW, 1, 0);
   if (do_narrow) f.add(c.scalars + SC_NCAND2, 1, 0);  // k_seg_filter's counter
+}
+
+void launch_broad_resets(Collide& c, int do_narrow, cudaStream_t st) {
+  FillList f;
+  broad_reset_list(c, do_narrow, f);
   launch_fill(f, st);
 }
 
@@ -1476,7 +1482,9 @@ void launch_collide(const World& w, Collide& c, const double* anim, const AnimLa
   const int nb = (std::max(w.V, al.n_kin) + kThreads - 1) / kThreads;
   // single-scene worlds: the broad phase's resets first, then the pills with their bounding spheres
   const bool fused_bounds = possible && !c.pill_scene;
-  if (fused_bounds) launch_broad_resets(c, 1, st);
+  // (g_broad_resets_done: the step prologue already did them, see Solver::record_step)
+  if (fused_bounds && !g_broad_resets_done) launch_broad_resets(c, 1, st);
+  g_broad_resets_done = false;
   launch_kernel(k_build_pills, nb, kThreads, 0, st, g_pdl, w, c, anim, al, fused_bounds ? 1 : 0, substep, err);
   if (!possible) {  // no pair can pass pair_allowed: only broad_phase's finiteness check remains
     if (c.P >= 2) launch_kernel(k_bounds, (c.P + kThreads - 1) / kThreads, kThreads, 0, st, g_pdl, c, substep, err);

@@ -97,26 +97,56 @@ __global__ void k_activation(World w, const double* __restrict__ anim, AnimLayou
   }
 }
 
-// predict_rod vertex loop (solver.cpp:29-58) + warm_start_lbs (:75-100) + the non-finite
-// prediction check (:179-181). Also takes the pre-predict snapshot (solver.cpp:311-316).
-__global__ void k_predict_vertices(World w, const double* __restrict__ anim, AnimLayout al, V3 g, double h,
-                                   int substep, unsigned long long* err) {
-  pdl_wait();
-  pdl_trigger();
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= w.V) return;
+// The predicted scale of vertex v (predict_rod, solver.cpp:41-50): s + h * sdot plus the radial
+// load term, floored; unchanged for pinned vertices. gamma_bad: the load term is not finite.
+__device__ __forceinline__ double predicted_scale(const World& w, double h, int v, bool& gamma_bad) {
   const int vp = w.vpad;
+  double s = F(w.X, S, vp, v);
+  gamma_bad = false;
+  if (w.pinned[v]) return s;
   const int r = w.slot_rod[v];
   const int k = w.slot_loc[v];
   const int m = w.slot_m[v];
+  const uint8_t lf = w.has_loads ? w.load_flags[r] : 0;
+  double ds = h * F(w.vel, VS, vp, v);
+  if ((lf & 4) && !w.classic) {
+    const double rho = w.mat[8 * w.rod_material[r] + 7];
+    double gamma = 0.0;
+    int count = 0;
+    if (k > 0) {
+      gamma += F(w.loads, 6, vp, v - 1);
+      ++count;
+    }
+    if (k < m) {
+      gamma += F(w.loads, 6, vp, v);
+      ++count;
+    }
+    gamma /= count;
+    gamma_bad = !isfinite(gamma);
+    const double rr = F(w.vstat, RBAR, vp, v);
+    const double h2 = h * h;
+    ds += 2.0 * h2 * gamma / (kPi * rr * rr * rr * rr * rho);
+  }
+  return fmax(s + ds, kMinScale);
+}
+
+// predict_rod vertex loop (solver.cpp:29-58) + warm_start_lbs (:75-100) + the non-finite
+// prediction check (:179-181). Also takes the pre-predict snapshot (solver.cpp:311-316).
+// Returns the predicted scale.
+__device__ __forceinline__ double predict_vertex(const World& w, const double* __restrict__ anim, const AnimLayout& al,
+                                                 const V3& g, double h, int substep, unsigned long long* err, int v) {
+  const int vp = w.vpad;
+  const int r = w.slot_rod[v];
+  const int k = w.slot_loc[v];
   V3 c{F(w.X, CX, vp, v), F(w.X, CY, vp, v), F(w.X, CZ, vp, v)};
-  double s = F(w.X, S, vp, v);
   Fr(w.prev, CX, vp, v) = c.x;
   Fr(w.prev, CY, vp, v) = c.y;
   Fr(w.prev, CZ, vp, v) = c.z;
-  Fr(w.prev, S, vp, v) = s;
+  Fr(w.prev, S, vp, v) = F(w.X, S, vp, v);
   const double h2 = h * h;
   const uint8_t lf = w.has_loads ? w.load_flags[r] : 0;
+  bool gamma_bad;
+  const double s = predicted_scale(w, h, v, gamma_bad);
   if (!w.pinned[v]) {
     const double rho = w.mat[8 * w.rod_material[r] + 7];
     V3 accel = g;
@@ -127,24 +157,7 @@ __global__ void k_predict_vertices(World w, const double* __restrict__ anim, Ani
     }
     const V3 vel{F(w.vel, VX, vp, v), F(w.vel, VY, vp, v), F(w.vel, VZ, vp, v)};
     c = c + (h * vel + h2 * accel);
-    double ds = h * F(w.vel, VS, vp, v);
-    if ((lf & 4) && !w.classic) {
-      double gamma = 0.0;
-      int count = 0;
-      if (k > 0) {
-        gamma += F(w.loads, 6, vp, v - 1);
-        ++count;
-      }
-      if (k < m) {
-        gamma += F(w.loads, 6, vp, v);
-        ++count;
-      }
-      gamma /= count;
-      if (!isfinite(gamma)) atomicMin(err, err_code(substep, ERR_PREDICT, r, 2ull * k + 1));
-      const double rr = F(w.vstat, RBAR, vp, v);
-      ds += 2.0 * h2 * gamma / (kPi * rr * rr * rr * rr * rho);
-    }
-    s = fmax(s + ds, kMinScale);
+    if (gamma_bad) atomicMin(err, err_code(substep, ERR_PREDICT, r, 2ull * k + 1));
     if (w.has_bones) {
       const int b0 = w.rod_bone_off[r], b1 = w.rod_bone_off[r + 1];
       if (b1 > b0) {  // warm_start_lbs
@@ -170,20 +183,17 @@ __global__ void k_predict_vertices(World w, const double* __restrict__ anim, Ani
   double2* xr = reinterpret_cast<double2*>(w.xrec + 8ll * v);
   xr[0] = make_double2(c.x, c.y);
   xr[1] = make_double2(c.z, s);
+  return s;
 }
 
 // predict_rod element loop (solver.cpp:60-72) + refresh_orientation_inertia (layout.cpp:76-93)
-// from the predicted scales.
-__global__ void k_predict_elements(World w, double h, int substep, unsigned long long* err) {
-  pdl_wait();
-  pdl_trigger();
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= w.V) return;
-  const int k = w.slot_loc[v];
+// from the predicted scales s0, s1 of the element's vertices.
+__device__ __forceinline__ void predict_element(const World& w, double h, int substep, unsigned long long* err, int v,
+                                                double s0, double s1) {
   const int m = w.slot_m[v];
-  if (k >= m) return;
   const int vp = w.vpad;
   const int r = w.slot_rod[v];
+  const int k = w.slot_loc[v];
   Q4 q{F(w.X, QW, vp, v), F(w.X, QX, vp, v), F(w.X, QY, vp, v), F(w.X, QZ, vp, v)};
   Fr(w.prev, QW, vp, v) = q.w;
   Fr(w.prev, QX, vp, v) = q.x;
@@ -191,7 +201,6 @@ __global__ void k_predict_elements(World w, double h, int substep, unsigned long
   Fr(w.prev, QZ, vp, v) = q.z;
   const double h2 = h * h;
   const double rho = w.mat[8 * w.rod_material[r] + 7];
-  const double s0 = F(w.X, S, vp, v), s1 = F(w.X, S, vp, v + 1);
   V3 dth = h * V3{F(w.vel, WX, vp, v), F(w.vel, WY, vp, v), F(w.vel, WZ, vp, v)};
   if (w.has_loads && (w.load_flags[r] & 2)) {
     const V3 tq{F(w.loads, 3, vp, v), F(w.loads, 4, vp, v), F(w.loads, 5, vp, v)};
@@ -217,6 +226,39 @@ __global__ void k_predict_elements(World w, double h, int substep, unsigned long
   Fr(w.estat, ITX, vp, v) = 1.0 / (0.25 * base);
   Fr(w.estat, ITY, vp, v) = 1.0 / (0.25 * base);
   Fr(w.estat, ITZ, vp, v) = 1.0 / (0.5 * base);
+}
+
+__global__ void k_predict_vertices(World w, const double* __restrict__ anim, AnimLayout al, V3 g, double h,
+                                   int substep, unsigned long long* err) {
+  pdl_wait();
+  pdl_trigger();
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < w.V) predict_vertex(w, anim, al, g, h, substep, err, v);
+}
+__global__ void k_predict_elements(World w, double h, int substep, unsigned long long* err) {
+  pdl_wait();
+  pdl_trigger();
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= w.V || w.slot_loc[v] >= w.slot_m[v]) return;
+  predict_element(w, h, substep, err, v, F(w.X, S, w.vpad, v), F(w.X, S, w.vpad, v + 1));
+}
+
+// Worlds whose rods all have <= 32 vertices: the whole prediction in one launch, one warp per
+// rod (lane k = slot k): vertex k, then element k with the predicted scale of vertex k + 1 from
+// the next lane. A rod never spans two warps, so no lane reads a scale another warp rewrites.
+constexpr int kPredictRodsPerCta = 4;
+__global__ void __launch_bounds__(32 * kPredictRodsPerCta) k_predict_rods(World w, const double* __restrict__ anim,
+                                                                         AnimLayout al, V3 g, double h, int substep,
+                                                                         unsigned long long* err) {
+  pdl_wait();
+  pdl_trigger();
+  const int r = blockIdx.x * kPredictRodsPerCta + (threadIdx.x >> 5);
+  if (r >= w.R) return;  // whole warps
+  const int k = threadIdx.x & 31, n = w.rod_n[r], v = w.rod_vbase[r] + k;
+  double s0 = 0.0;
+  if (k < n) s0 = predict_vertex(w, anim, al, g, h, substep, err, v);
+  const double s1 = __shfl_down_sync(0xffffffffu, s0, 1);
+  if (k < n - 1) predict_element(w, h, substep, err, v, s0, s1);
 }
 
 // post_step_scales (classic mode, solver.cpp:253-271) + finalize_velocities (:273-289).
@@ -296,6 +338,11 @@ void launch_predict(const World& w, const double* anim, const AnimLayout& al, co
                     int substep, unsigned long long* err, cudaStream_t st) {
   const V3 g{gravity_h[0], gravity_h[1], gravity_h[2]};
   const int b = (w.V + 127) / 128;
+  if (w.max_rod_n <= 32) {
+    launch_kernel(k_predict_rods, (w.R + kPredictRodsPerCta - 1) / kPredictRodsPerCta, 32 * kPredictRodsPerCta, 0, st,
+                  g_pdl, w, anim, al, g, h, substep, err);
+    return;
+  }
   launch_kernel(k_predict_vertices, b, 128, 0, st, g_pdl, w, anim, al, g, h, substep, err);
   launch_kernel(k_predict_elements, b, 128, 0, st, g_pdl, w, h, substep, err);
 }

@@ -261,6 +261,10 @@ struct FillList {
   }
 };
 void launch_fill(const FillList& f, cudaStream_t st);
+// The broad phase's per-substep resets (launch_broad_resets' list); g_broad_resets_done: the
+// next launch_collide skips them (already done by the caller).
+void broad_reset_list(const Collide& c, int do_narrow, FillList& f);
+extern bool g_broad_resets_done;
 void scan_exclusive(const int* in, int* out, long long n_cap, const int* n_dev, int* partials, int parts,
                     cudaStream_t st);
 long long scan_partials_needed(long long n);

@@ -633,9 +633,16 @@ void Solver::fill_animation(int substeps, double h) {
   }
 }
 
-__global__ void k_init_acc(StepAccum* acc, unsigned long long* err, int* scalars) {
+// Step prologue: the step accumulator and error word, plus the first substep's resets (the broad
+// phase's and the iteration loop's, `f`), one launch instead of three.
+__global__ void k_init_acc(StepAccum* acc, unsigned long long* err, int* scalars, vdev::FillList f) {
   vdev::pdl_wait();
   vdev::pdl_trigger();
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (int a = 0; a < f.n; ++a)
+    for (long long i = t; i < f.count[a]; i += stride) f.ptr[a][i] = f.value[a];
+  if (t != 0) return;
   scalars[vdev::SC_OVF] = 0;
   for (int q = 0; q < 8; ++q) acc->residuals[q] = 0.0;
   acc->max_penetration = 0.0;
@@ -694,7 +701,24 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
   vdev::g_pdl = pdl_ && !prof;
   if (n_scenes_ > 1)
     check_cuda(cudaMemsetAsync(w_.scene_acc, 0, sizeof(vdev::SceneAcc) * n_scenes_, st), "scene report reset");
-  vdev::launch_kernel(k_init_acc, 1, 1, 0, st, vdev::g_pdl, d_acc_, d_err_, c_.scalars);
+  // the first substep's resets ride on the prologue
+  const bool persistent0 = persist_tiles_ > 0 && !probe_log;
+  auto substep_resets = [&](vdev::FillList& f) {  // multipliers (per-launch path; the persistent kernel keeps
+                                                 // them on chip), singular counters, grid-barrier counter
+    if (!persistent0) f.add(w_.lam, 2ll * vdev::kLamFields * w_.vpad, 0);
+    f.add(d_singular_, iterations, 0);
+    if (persistent0) f.add(d_bar_, 2, 0);
+  };
+  const bool pro_broad = c_.P >= 1 && collide_possible_ && !c_.pill_scene;  // launch_collide's fused-bounds path
+  {
+    vdev::FillList f;
+    if (pro_broad) vdev::broad_reset_list(c_, 1, f);
+    substep_resets(f);
+    long long mx = 1;
+    for (int a = 0; a < f.n; ++a) mx = std::max(mx, f.count[a]);
+    const long long b = std::min<long long>((mx + 255) / 256, 148 * 8);
+    vdev::launch_kernel(k_init_acc, static_cast<unsigned>(b), 256, 0, st, vdev::g_pdl, d_acc_, d_err_, c_.scalars, f);
+  }
   check_cuda(cudaMemcpyAsync(d_anim_, h_anim_, sizeof(double) * al_.stride * substeps, cudaMemcpyHostToDevice, st),
              "anim upload");
   for (int s = 0; s < substeps; ++s) {
@@ -705,6 +729,7 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
     vdev::launch_predict(w_, anim, al_, g, h, s, d_err_, st);
     end();
     begin_collide();
+    vdev::g_broad_resets_done = s == 0 && pro_broad;
     if (c_.P >= 1) vdev::launch_collide(w_, c_, anim, al_, s, d_err_, d_acc_, collide_possible_ ? 1 : 0, st);
     if (prof && vdev::g_broad_mark) {
       // no pair scan ran (nothing can collide): the broad phase ends here
@@ -716,12 +741,9 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
     begin(CAT_EXT_SETUP);
     if (ext_possible_) vdev::launch_ext_setup(w_, c_, st);
     const bool persistent = persist_tiles_ > 0 && !probe_log;
-    {  // per-substep resets, one launch: multipliers (per-launch path; the persistent kernel keeps
-       // them on chip), singular counters, grid-barrier counter
+    if (s > 0) {  // per-substep resets (the first substep's ran in the prologue)
       vdev::FillList f;
-      if (!persistent) f.add(w_.lam, 2ll * vdev::kLamFields * w_.vpad, 0);
-      f.add(d_singular_, iterations, 0);
-      if (persistent) f.add(d_bar_, 2, 0);
+      substep_resets(f);
       vdev::launch_fill(f, st);
     }
     end();

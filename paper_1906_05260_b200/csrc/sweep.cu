@@ -227,6 +227,125 @@ __global__ void k_ext_sort(Collide c, int V, int npins) {
   }
 }
 
+// Small worlds whose slot counters fit in shared memory (V <= kExtSmemSlots): the same setup as
+// k_ext_setup_small, with the per-slot counts, offsets and cursors — and the entries, when they
+// fit — in shared memory, so each phase costs shared-memory atomics and one block barrier instead
+// of a global-memory round trip; ext_off / ext_items / ext_pos / ext_ab are written once at the end.
+constexpr int kExtSmemThreads = 1024;
+constexpr int kExtSmemSlots = 12288;
+constexpr int kExtSmemItems = 8192;
+unsigned ext_smem_bytes(int V) { return static_cast<unsigned>((2 * (V + 1) + kExtSmemItems) * sizeof(int)); }
+__global__ void __launch_bounds__(kExtSmemThreads) k_ext_setup_smem(Collide c, int V, int npins) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ int s_ext[];
+  int* s_off = s_ext;              // V + 1: counts, then exclusive offsets
+  int* s_cur = s_ext + V + 1;      // V + 1: fill cursors
+  int* s_items = s_cur + V + 1;    // kExtSmemItems
+  __shared__ int ws[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int v = tid; v <= V; v += kExtSmemThreads) {
+    s_off[v] = 0;
+    s_cur[v] = 0;
+  }
+  __syncthreads();
+  const int nct = c.scalars[SC_NCT];
+  const int n = npins + nct + c.scalars[SC_NHP];
+  for (int b = tid; b < n; b += kExtSmemThreads) {  // k_ext_count
+    int slots[4];
+    const int ne = ext_endpoints(c, b, npins, nct, slots);
+    for (int e = 0; e < ne; ++e)
+      if (slots[e] >= 0) atomicAdd(&s_off[slots[e]], 1);
+    if (b >= npins && b < npins + nct) {
+      c.ct_va[b - npins] = slots[0];
+      c.ct_vb[b - npins] = slots[2];
+    }
+    c.ext_lam[b] = 0.0;
+    c.ext_lam[c.ext_cap + b] = 0.0;
+    c.ext_lam[2 * c.ext_cap + b] = 0.0;
+  }
+  __syncthreads();
+  int carry = 0;  // exclusive scan in place, s_off[0, V) -> s_off[0, V]
+  for (int b0 = 0; b0 < V; b0 += kExtSmemThreads) {
+    const int x = b0 + tid < V ? s_off[b0 + tid] : 0;
+    int incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) ws[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int y = ws[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += t;
+      }
+      ws[lane] = y;
+    }
+    __syncthreads();
+    if (b0 + tid < V) s_off[b0 + tid] = carry + (wid ? ws[wid - 1] : 0) + incl - x;
+    carry += ws[31];
+    __syncthreads();
+  }
+  if (tid == 0) s_off[V] = carry;
+  __syncthreads();
+  const int total = s_off[V];
+  for (int v = tid; v <= V; v += kExtSmemThreads) c.ext_off[v] = s_off[v];
+  int* items = total <= kExtSmemItems ? s_items : c.ext_items;  // entries in shared memory when they fit
+  for (int b = tid; b < n; b += kExtSmemThreads) {  // k_ext_fill
+    int slots[4];
+    const int ne = ext_endpoints(c, b, npins, nct, slots);
+    for (int e = 0; e < ne; ++e) {
+      if (slots[e] < 0) continue;
+      items[s_off[slots[e]] + atomicAdd(&s_cur[slots[e]], 1)] = (b << 2) | e;
+    }
+  }
+  __syncthreads();
+  // k_ext_sort: warps over 32 consecutive slots at a time, ranking the busy slots' entries
+  for (int v0 = 32 * wid; v0 < V; v0 += kExtSmemThreads) {
+    const int vl = v0 + lane;
+    const int ml = vl < V ? s_off[vl + 1] - s_off[vl] : 0;
+    unsigned busy = __ballot_sync(0xffffffffu, ml > 0);
+    while (busy) {
+      const int src = __ffs(busy) - 1;
+      busy &= busy - 1;
+      const int s0 = s_off[v0 + src], m = __shfl_sync(0xffffffffu, ml, src);
+      if (m <= 32) {
+        const int key = lane < m ? items[s0 + lane] : 0x7fffffff;
+        int rank = 0;
+        for (int j = 0; j < m; ++j) rank += __shfl_sync(0xffffffffu, key, j) < key ? 1 : 0;
+        if (lane < m) {
+          c.ext_items[s0 + rank] = key;
+          c.ext_pos[key] = s0 + rank;
+          c.ext_ab[s0 + rank] = entry_ab(c, key, npins, nct);
+        }
+      } else {
+        __syncwarp();
+        if (lane == 0) {  // insertion sort in place, then out
+          for (int a = s0 + 1; a < s0 + m; ++a) {
+            const int key = items[a];
+            int b = a - 1;
+            while (b >= s0 && items[b] > key) {
+              items[b + 1] = items[b];
+              --b;
+            }
+            items[b + 1] = key;
+          }
+          for (int a = s0; a < s0 + m; ++a) {
+            c.ext_items[a] = items[a];
+            c.ext_pos[items[a]] = a;
+            c.ext_ab[a] = entry_ab(c, items[a], npins, nct);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
 // Small worlds: the whole external-block incidence setup (k_ext_count, the scan, k_ext_fill,
 // k_ext_sort) in ONE CTA of 1024 threads, phase by phase with block barriers — same entries,
 // same order, one launch instead of five.
@@ -718,6 +837,13 @@ int grid_for(long long n) {
 int report_parts(int V) { return (V + kRepThreads - 1) / kRepThreads; }
 
 void launch_ext_setup(const World& w, Collide& c, cudaStream_t st) {
+  if (c.order_smem_cap >= 0 && w.V <= kExtSmemSlots && !std::getenv("VROD_EXT_SETUP_GLOBAL")) {
+    static const cudaError_t attr = cudaFuncSetAttribute(k_ext_setup_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         ext_smem_bytes(kExtSmemSlots));
+    (void)attr;  // a failure surfaces as a launch error
+    launch_kernel(k_ext_setup_smem, 1, kExtSmemThreads, ext_smem_bytes(w.V), st, g_pdl, c, w.V, c.n_pins);
+    return;
+  }
   if (c.order_smem_cap >= 0 && w.V < (1 << 16)) {  // small worlds (same switch as the contact ordering)
     launch_kernel(k_ext_setup_small, 1, kExtSetupThreads, 0, st, g_pdl, c, w.V, c.n_pins);
     return;
