@@ -30,19 +30,28 @@ __global__ void k_pin_motions(World w, const double* __restrict__ anim, AnimLayo
 // One CTA per rod carrying activations: apply_activation (rod.cpp:164-176) for every activation
 // whose amount changed, then refresh_length_derived (rod.cpp:42-56) and refresh_stiffness
 // (constraints.cpp:331-372) for the rod.
-__global__ void k_activation(World w, const double* __restrict__ anim, AnimLayout al, const int* __restrict__ rod_off,
-                             const int* __restrict__ act_list, double* applied, const int* __restrict__ act_rods,
-                             const double* __restrict__ act_static) {
-  pdl_wait();
-  pdl_trigger();
-  const int r = act_rods[blockIdx.x];
+struct ActArgs {
+  const int* rod_off;
+  const int* list;
+  double* applied;
+  const int* rods;
+  const double* stat;
+  int n_rods;
+};
+__device__ __forceinline__ void activation_block(const World& w, const double* __restrict__ anim, const AnimLayout& al,
+                                                 const ActArgs& aa, int blk) {
+  const int* __restrict__ rod_off = aa.rod_off;
+  const int* __restrict__ act_list = aa.list;
+  double* applied = aa.applied;
+  const double* __restrict__ act_static = aa.stat;
+  const int r = aa.rods[blk];
   const int v0 = w.rod_vbase[r];
   const int n = w.rod_n[r];
   const int m = n - 1;
   __shared__ int changed;
   if (threadIdx.x == 0) changed = 0;
   __syncthreads();
-  for (int k = rod_off[blockIdx.x]; k < rod_off[blockIdx.x + 1]; ++k) {  // activation order
+  for (int k = rod_off[blk]; k < rod_off[blk + 1]; ++k) {  // activation order
     const int a_id = act_list[k];
     const double a = anim[al.off_act + a_id];
     const double prev = applied[a_id];
@@ -95,6 +104,11 @@ __global__ void k_activation(World w, const double* __restrict__ anim, AnimLayou
       Fr(w.estat, KSB, vp, j) = inverse_stiffness(a4 * (mat[3] + mat[4]) * lw);
     }
   }
+}
+__global__ void k_activation(World w, const double* __restrict__ anim, AnimLayout al, ActArgs aa) {
+  pdl_wait();
+  pdl_trigger();
+  activation_block(w, anim, al, aa, blockIdx.x);
 }
 
 // The predicted scale of vertex v (predict_rod, solver.cpp:41-50): s + h * sdot plus the radial
@@ -246,13 +260,19 @@ __global__ void k_predict_elements(World w, double h, int substep, unsigned long
 // Worlds whose rods all have <= 32 vertices: the whole prediction in one launch, one warp per
 // rod (lane k = slot k): vertex k, then element k with the predicted scale of vertex k + 1 from
 // the next lane. A rod never spans two warps, so no lane reads a scale another warp rewrites.
+// With activations, their rods' CTAs come first in the same launch (activation_block: disjoint
+// fields — LEN and the length-derived statics — from the ones the prediction reads and writes).
 constexpr int kPredictRodsPerCta = 4;
 __global__ void __launch_bounds__(32 * kPredictRodsPerCta) k_predict_rods(World w, const double* __restrict__ anim,
                                                                          AnimLayout al, V3 g, double h, int substep,
-                                                                         unsigned long long* err) {
+                                                                         unsigned long long* err, ActArgs aa) {
   pdl_wait();
   pdl_trigger();
-  const int r = blockIdx.x * kPredictRodsPerCta + (threadIdx.x >> 5);
+  if (static_cast<int>(blockIdx.x) < aa.n_rods) {
+    activation_block(w, anim, al, aa, blockIdx.x);
+    return;
+  }
+  const int r = (blockIdx.x - aa.n_rods) * kPredictRodsPerCta + (threadIdx.x >> 5);
   if (r >= w.R) return;  // whole warps
   const int k = threadIdx.x & 31, n = w.rod_n[r], v = w.rod_vbase[r] + k;
   double s0 = 0.0;
@@ -323,26 +343,21 @@ __global__ void k_copy_state(int V, int vpad, const double* __restrict__ src, do
 
 }  // namespace
 
-void launch_animate(const World& w, const double* anim, const AnimLayout& al, const int* pm_slot,
-                    const int* act_rod_off, const int* act_list, double* act_applied, const int* act_rods,
-                    int n_act_rods, cudaStream_t st) {
+void launch_animate_predict(const World& w, const double* anim, const AnimLayout& al, const int* pm_slot,
+                            const int* act_rod_off, const int* act_list, double* act_applied, const int* act_rods,
+                            int n_act_rods, const double* gravity_h, double h, int substep, unsigned long long* err,
+                            cudaStream_t st) {
   if (al.n_pm > 0) launch_kernel(k_pin_motions, (al.n_pm + 127) / 128, 128, 0, st, g_pdl, w, anim, al, pm_slot);
-  if (n_act_rods > 0) {
-    // act_static follows act_applied in the same allocation (see solver.cu)
-    const double* act_static = act_applied + al.n_act;
-    launch_kernel(k_activation, n_act_rods, 128, 0, st, g_pdl, w, anim, al, act_rod_off, act_list, act_applied, act_rods, act_static);
-  }
-}
-
-void launch_predict(const World& w, const double* anim, const AnimLayout& al, const double* gravity_h, double h,
-                    int substep, unsigned long long* err, cudaStream_t st) {
+  // act_static follows act_applied in the same allocation (see solver.cu)
+  ActArgs aa{act_rod_off, act_list, act_applied, act_rods, act_applied + al.n_act, n_act_rods};
   const V3 g{gravity_h[0], gravity_h[1], gravity_h[2]};
-  const int b = (w.V + 127) / 128;
-  if (w.max_rod_n <= 32) {
-    launch_kernel(k_predict_rods, (w.R + kPredictRodsPerCta - 1) / kPredictRodsPerCta, 32 * kPredictRodsPerCta, 0, st,
-                  g_pdl, w, anim, al, g, h, substep, err);
+  if (w.max_rod_n <= 32) {  // activation + prediction in one launch
+    launch_kernel(k_predict_rods, n_act_rods + (w.R + kPredictRodsPerCta - 1) / kPredictRodsPerCta,
+                  32 * kPredictRodsPerCta, 0, st, g_pdl, w, anim, al, g, h, substep, err, aa);
     return;
   }
+  if (n_act_rods > 0) launch_kernel(k_activation, n_act_rods, 128, 0, st, g_pdl, w, anim, al, aa);
+  const int b = (w.V + 127) / 128;
   launch_kernel(k_predict_vertices, b, 128, 0, st, g_pdl, w, anim, al, g, h, substep, err);
   launch_kernel(k_predict_elements, b, 128, 0, st, g_pdl, w, h, substep, err);
 }

@@ -270,11 +270,11 @@ void scan_exclusive(const int* in, int* out, long long n_cap, const int* n_dev, 
 long long scan_partials_needed(long long n);
 
 // integrate.cu
-void launch_animate(const World& w, const double* anim, const AnimLayout& al, const int* pm_slot,
-                    const int* act_rod_off, const int* act_list, double* act_applied, const int* act_rods,
-                    int n_act_rods, cudaStream_t st);
-void launch_predict(const World& w, const double* anim, const AnimLayout& al, const double* gravity_h,
-                    double h, int substep, unsigned long long* err, cudaStream_t st);
+// animate (pin motions, activations) + predict_rod / warm_start_lbs / orientation inertia
+void launch_animate_predict(const World& w, const double* anim, const AnimLayout& al, const int* pm_slot,
+                            const int* act_rod_off, const int* act_list, double* act_applied, const int* act_rods,
+                            int n_act_rods, const double* gravity_h, double h, int substep, unsigned long long* err,
+                            cudaStream_t st);
 void launch_finalize_from(const World& w, const double* src, double h, double keep, cudaStream_t st);
 void launch_copy_state(const World& w, const double* src, double* dst, cudaStream_t st);
 
@@ -314,10 +314,13 @@ void launch_scene_report(const World& w, const double* X, int classic, int* scen
 int report_parts(int V);
 // k_report_partial only, and the fused end of a single-scene substep (penetration, residual
 // norms from the partials, singular count / error word)
-void launch_report_partial(const World& w, const double* X, int classic, double* partials, int parts, cudaStream_t st);
-void launch_report_tail(const World& w, Collide& c, const double* X, StepAccum* acc, bool do_pen, const double* partials,
-                        int parts, const int* singular_last, int last, const unsigned long long* err, unsigned* counter,
-                        cudaStream_t st);
+// The substep's report in one launch: residual partials (k_report_partial's partition), max
+// penetration (from the slot records xrec when non-null: they must hold X's centers and scales),
+// then the last CTA's fixed-order reduction, singular count and error word.
+void launch_report_tail(const World& w, Collide& c, const double* X, const double* xrec, int classic, StepAccum* acc,
+                        bool do_pen,
+                        double* partials, int parts, const int* singular_last, int last, const unsigned long long* err,
+                        unsigned* counter, cudaStream_t st);
 // get_state's outputs packed contiguously (centers, scales, frames, velocities: 8V + 7E doubles)
 void launch_pack_state(const World& w, const double* X, int E, double* out, cudaStream_t st);
 // kinetic energy and total volume (out[0], out[1]) in the reference's summation order;

@@ -724,9 +724,8 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
   for (int s = 0; s < substeps; ++s) {
     const double* anim = d_anim_ + static_cast<std::size_t>(al_.stride) * s;
     begin(CAT_PREDICT);
-    vdev::launch_animate(w_, anim, al_, d_pm_slot_, d_act_rod_off_, d_act_list_, d_act_applied_, d_act_rods_,
-                         n_act_rods_, st);
-    vdev::launch_predict(w_, anim, al_, g, h, s, d_err_, st);
+    vdev::launch_animate_predict(w_, anim, al_, d_pm_slot_, d_act_rod_off_, d_act_list_, d_act_applied_, d_act_rods_,
+                                 n_act_rods_, g, h, s, d_err_, st);
     end();
     begin_collide();
     vdev::g_broad_resets_done = s == 0 && pro_broad;
@@ -812,8 +811,10 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
     }
     const bool do_pen = ext_possible_ && (c_.contact_cap + c_.hp_cap) > 0;
     if (n_scenes_ == 1) {  // partials, then one fused tail launch
-      vdev::launch_report_partial(w_, w_.X, w_.classic, d_report_partials_, report_parts_, st);
-      vdev::launch_report_tail(w_, c_, w_.X, d_acc_, do_pen, d_report_partials_, report_parts_,
+      // the per-launch sweeps leave the final centers / scales in the slot records too (not the
+      // persistent kernel's ping-pong, nor classic mode's post-step scales)
+      const double* pen_xrec = !w_.classic && !persistent ? w_.xrec : nullptr;
+      vdev::launch_report_tail(w_, c_, w_.X, pen_xrec, w_.classic, d_acc_, do_pen, d_report_partials_, report_parts_,
                                d_singular_ + (iterations - 1), s == substeps - 1 ? 1 : 0, d_err_, d_tail_counter_, st);
     } else {
       vdev::launch_residuals(w_, w_.X, w_.classic, d_report_partials_, report_parts_,

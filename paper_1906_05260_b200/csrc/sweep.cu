@@ -63,12 +63,23 @@ __device__ __forceinline__ ExtGeom resolve(const World& w, const Collide& c, con
 }
 
 // Residual of an external block (contact / half-plane only), for the end-of-step penetration.
-__device__ double ext_residual(const World& w, const Collide& c, const double* X, int b, int npins, int nct) {
+// The endpoints' first slots come from ct_va / ct_vb (stored by the incidence setup); xrec
+// (nullable): the slot records, when they hold X's centers and scales (not in classic mode,
+// whose post-step scales change X after the last sweep).
+__device__ double ext_residual(const World& w, const Collide& c, const double* X, const double* xrec, int b, int npins,
+                               int nct) {
   const int vp = w.vpad;
   if (b < npins + nct) {
     const int k = b - npins;
-    const ExtGeom A = resolve(w, c, X, c.ct_a[k]);
-    const ExtGeom B = resolve(w, c, X, c.ct_b[k]);
+    ExtGeom A, B;
+    if (xrec) {
+      double ic[2], is[2];
+      A = resolve_rec(xrec, c, c.ct_a[k], c.ct_va[k], ic, is);
+      B = resolve_rec(xrec, c, c.ct_b[k], c.ct_vb[k], ic, is);
+    } else {
+      A = resolve_at(w, c, X, c.ct_a[k], c.ct_va[k]);
+      B = resolve_at(w, c, X, c.ct_b[k], c.ct_vb[k]);
+    }
     const double al = c.ct_alpha[k], be = c.ct_beta[k];
     const V3 ca = (1.0 - al) * A.c0 + al * A.c1;
     const V3 cb = (1.0 - be) * B.c0 + be * B.c1;
@@ -681,10 +692,9 @@ __global__ void k_energy_sum(World w, const double* __restrict__ terms, const do
   out[1] = vol;
 }
 
-__global__ void k_report_partial(World w, const double* __restrict__ X, int classic, double* partials) {
-  pdl_wait();
-  pdl_trigger();
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void report_partial_block(const World& w, const double* __restrict__ X, int classic,
+                                                     double* partials, int blk) {
+  const int v = blk * kRepThreads + threadIdx.x;
   double acc[16];
 #pragma unroll
   for (int q = 0; q < 16; ++q) acc[q] = 0.0;
@@ -703,8 +713,13 @@ __global__ void k_report_partial(World w, const double* __restrict__ X, int clas
   if (threadIdx.x < 16) {
     double x = red[threadIdx.x][0];
     for (int k = 1; k < kRepThreads / 32; ++k) x += red[threadIdx.x][k];
-    partials[16ll * blockIdx.x + threadIdx.x] = x;
+    partials[16ll * blk + threadIdx.x] = x;
   }
+}
+__global__ void k_report_partial(World w, const double* __restrict__ X, int classic, double* partials) {
+  pdl_wait();
+  pdl_trigger();
+  report_partial_block(w, X, classic, partials, blockIdx.x);
 }
 
 // Sums the per-CTA partials: 16 quantities x `parts`, one CTA of 256 threads, each thread a
@@ -732,13 +747,13 @@ __global__ void k_report_final(const double* partials, int parts, double* out8) 
 }
 
 __device__ __forceinline__ void penetration_part(const World& w, const Collide& c, const double* __restrict__ X,
-                                                 StepAccum* acc) {
+                                                 const double* __restrict__ xrec, StepAccum* acc) {
   const int npins = c.n_pins;
   const int nct = c.scalars[SC_NCT];
   const int n = nct + c.scalars[SC_NHP];
   double deepest = 0.0;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
-    const double pen = -ext_residual(w, c, X, npins + q, npins, nct);
+    const double pen = -ext_residual(w, c, X, xrec, npins + q, npins, nct);
     if (pen > deepest) deepest = pen;
     if (c.pill_scene && pen > 0.0) {  // batch: per-scene max as well
       const int scene = q < nct ? c.pill_scene[c.ct_a[q]] : c.plane_scene[c.hp_plane[q - nct]];
@@ -754,19 +769,27 @@ __device__ __forceinline__ void penetration_part(const World& w, const Collide& 
 __global__ void k_penetration(World w, Collide c, const double* __restrict__ X, StepAccum* acc) {
   pdl_wait();
   pdl_trigger();
-  penetration_part(w, c, X, acc);
+  penetration_part(w, c, X, nullptr, acc);
 }
 
 // The end of a single-scene substep in one launch: the max penetration over the contact and
 // half-plane blocks, then — in the last CTA to finish (ticket counter, reset by that CTA) — the
 // residual norms from k_report_partial's partials (the same fixed-order tree as k_report_final)
 // and the substep's singular count / error word (solver.cpp:335, 370-375).
-__global__ void k_report_tail(World w, Collide c, const double* __restrict__ X, StepAccum* acc, int do_pen,
-                              const double* partials, int parts, const int* singular_last, int last,
-                              const unsigned long long* err, unsigned* counter) {
+// kPartials: the residual partials too (block b < parts computes partial b, k_report_partial's
+// work and partition), so the whole report is one launch.
+template <bool kPartials>
+__global__ void k_report_tail(World w, Collide c, const double* __restrict__ X, const double* __restrict__ xrec,
+                              StepAccum* acc, int do_pen,
+                              double* partials, int parts, const int* singular_last, int last,
+                              const unsigned long long* err, unsigned* counter, int classic) {
   pdl_wait();
   pdl_trigger();
-  if (do_pen) penetration_part(w, c, X, acc);
+  if (kPartials && static_cast<int>(blockIdx.x) < parts) {
+    report_partial_block(w, X, classic, partials, blockIdx.x);
+    if (threadIdx.x < 16) __threadfence();  // the partial, before this block's ticket
+  }
+  if (do_pen) penetration_part(w, c, X, xrec, acc);
   __shared__ int is_last;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -871,10 +894,6 @@ void launch_iteration(const World& w, Collide& c, const double* X, double* Y, co
   launch_rod_sweep(w, c, X, Y, sp, singular_counter, err, st);
 }
 
-void launch_report_partial(const World& w, const double* X, int classic, double* partials, int parts, cudaStream_t st) {
-  launch_kernel(k_report_partial, parts, kRepThreads, 0, st, g_pdl, w, X, classic, partials);
-}
-
 void launch_residuals(const World& w, const double* X, int classic, double* partials, int parts, double* out8,
                       cudaStream_t st) {
   launch_kernel(k_report_partial, parts, kRepThreads, 0, st, g_pdl, w, X, classic, partials);
@@ -901,12 +920,16 @@ void launch_scene_report(const World& w, const double* X, int classic, int* scen
   launch_kernel(k_scene_singular, (w.n_scenes + kThreads - 1) / kThreads, kThreads, 0, st, g_pdl, w, scene_singular);
 }
 
-void launch_report_tail(const World& w, Collide& c, const double* X, StepAccum* acc, bool do_pen, const double* partials,
-                        int parts, const int* singular_last, int last, const unsigned long long* err, unsigned* counter,
-                        cudaStream_t st) {
-  const int g = do_pen ? grid_for(c.contact_cap + c.hp_cap) : 1;
-  launch_kernel(k_report_tail, g, kRepThreads, 0, st, g_pdl, w, c, X, acc, do_pen ? 1 : 0, partials, parts, singular_last,
-                last, err, counter);
+void launch_report_tail(const World& w, Collide& c, const double* X, const double* xrec, int classic, StepAccum* acc,
+                        bool do_pen,
+                        double* partials, int parts, const int* singular_last, int last, const unsigned long long* err,
+                        unsigned* counter, cudaStream_t st) {
+  // small worlds: the partials in the same launch (latency); large ones (C4: 0.31 vs 0.21 ms): separate
+  const bool fused = parts <= 148;
+  if (!fused) launch_kernel(k_report_partial, parts, kRepThreads, 0, st, g_pdl, w, X, classic, partials);
+  const int g = std::max(do_pen ? grid_for(c.contact_cap + c.hp_cap) : 1, fused ? parts : 1);
+  launch_kernel(fused ? k_report_tail<true> : k_report_tail<false>, g, kRepThreads, 0, st, g_pdl, w, c, X, xrec, acc,
+                do_pen ? 1 : 0, partials, parts, singular_last, last, err, counter, classic);
 }
 
 void launch_penetration(const World& w, Collide& c, const double* X, StepAccum* acc, cudaStream_t st) {
