@@ -191,6 +191,7 @@ struct SweepParams {
   const double* lam_in;  // elastic multipliers before this sweep (kLamFields x vpad)
   double* lam_out;       // after this sweep (ping-pong partner)
   unsigned long long* dbg = nullptr;  // debug trace (persistent kernel, VROD_TRACE=1)
+  int prefetch_rods = 0;  // warp-per-rod sweep: L2 prefetch distance in rods (0: none)
 };
 
 // The persistent small-world iteration kernel (rodsweep.cu k_iterate): the whole iteration

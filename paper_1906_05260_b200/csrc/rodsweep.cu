@@ -227,6 +227,13 @@ __device__ __forceinline__ void tma_rows(void* dst, const CUtensorMap* map, int 
       : "memory");
 }
 
+// L2 prefetch of the same box (no shared memory, no completion): cp.async.bulk.prefetch.tensor.
+__device__ __forceinline__ void tma_prefetch_rows(const CUtensorMap* map, int col) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(col), "r"(0)
+               : "memory");
+}
+
 // Interior tiles of the per-sweep kernel: every needed row segment (TP + 2 doubles, 16-byte
 // aligned, a multiple of 16 bytes) is ONE bulk copy issued by the lanes of warp 0, all
 // completing on the tile's mbarrier (initialised by tile_meta's caller). A handful of
@@ -1081,6 +1088,17 @@ __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_
       tma_rows(&ws.vs[0][0], &tm_vs, base, &ws.bar);
       tma_rows(&ws.es[0][0], &tm_es, base, &ws.bar);
       tma_rows(&ws.lm[0][0], &tm_lm, base, &ws.bar);
+      // the rows of rod r + sp.prefetch_rods, which a warp of a later wave takes, into L2: its
+      // own tensor copies then hit L2
+      const int rf = r + sp.prefetch_rods;
+      if (sp.prefetch_rods > 0 && rf < w.R) {
+        const int vf = w.rod_vbase[rf];
+        const int bf = vf >= 1 ? (vf - 1) & ~1 : 0;
+        tma_prefetch_rows(&tm_x, bf);
+        tma_prefetch_rows(&tm_vs, bf);
+        tma_prefetch_rows(&tm_es, bf);
+        tma_prefetch_rows(&tm_lm, bf);
+      }
     }
     __syncwarp();
     mbar_wait(&ws.bar, 0);
@@ -1487,6 +1505,11 @@ void launch_rod_sweep(const World& w, Collide& c, const double* X, double* Y, co
     // 3 CTAs per SM (168 registers, no spills) measured fastest at C4 with the tensor staging
     const int minb = std::getenv("VROD_WARP_MINB") ? std::atoi(std::getenv("VROD_WARP_MINB")) : 3;
     const size_t smem = staged ? kWarpRodsPerCta * sizeof(WarpStage) : 0;
+    // L2 prefetch distance in rods (VROD_WARP_PREFETCH, 0 = off). Measured at C4: 444 (148 x 3)
+    // sweep 3.33 -> 3.29 ms per substep; 222 / 888 / 1776 / 3552 less; also prefetching the
+    // incidence entries is slower (lane 0's extra offset loads)
+    SweepParams spp = sp;
+    spp.prefetch_rods = std::getenv("VROD_WARP_PREFETCH") ? std::atoi(std::getenv("VROD_WARP_PREFETCH")) : 444;
     const CUtensorMap tx = rows_map(X, kStateFields, w.vpad), tv = rows_map(w.vstat, kVStatFields, w.vpad),
                       te = rows_map(w.estat, kSweepEStatFields, w.vpad), tl = rows_map(sp.lam_in, kLamFields, w.vpad);
     static const bool attrs = [] {
@@ -1498,7 +1521,7 @@ void launch_rod_sweep(const World& w, Collide& c, const double* X, double* Y, co
     auto* kern = staged ? (minb <= 2 ? k_rod_sweep_warp<2, true> : minb == 3 ? k_rod_sweep_warp<3, true> : k_rod_sweep_warp<4, true>)
                         : (minb <= 2 ? k_rod_sweep_warp<2, false> : minb == 3 ? k_rod_sweep_warp<3, false> : k_rod_sweep_warp<4, false>);
     launch_kernel(kern, (w.R + kWarpRodsPerCta - 1) / kWarpRodsPerCta, 32 * kWarpRodsPerCta, smem, st, sp.pdl != 0, w,
-                  c, X, Y, sp, singular_counter, err, has_ext, tx, tv, te, tl);
+                  c, X, Y, spp, singular_counter, err, has_ext, tx, tv, te, tl);
     return;
   }
   // 64-wide tiles once they fill every SM twice over (148 SMs x 2 x 62 slots).
