@@ -411,3 +411,24 @@ def test_solver_options(gpu, oracle):
     sc, so = c.state(), o.state()
     for k in sc:
         np.testing.assert_array_equal(sc[k], so[k], err_msg=k)
+
+
+@pytest.mark.parametrize("name", ["pile", "crossing", "kitchen_sink"])
+def test_incidence_setup_paths_agree(gpu, oracle, name, monkeypatch):
+    """Small worlds build the external-block incidence lists in one CTA with shared-memory
+    counters (sweep.cu k_ext_setup_smem); VROD_EXT_SETUP_GLOBAL=1 takes the global-memory
+    single-CTA kernel (k_ext_setup_small). Same lists, so the same bits, step after step."""
+    scene = SCENES[name](oracle)
+    monkeypatch.setenv("VROD_EXT_SETUP_GLOBAL", "1")
+    b = SolverHandle(gpu, scene)
+    rb = b.step()
+    monkeypatch.delenv("VROD_EXT_SETUP_GLOBAL")
+    a2 = SolverHandle(gpu, scene)
+    ra = a2.step()
+    for _ in range(3):
+        assert (ra.contact_count, ra.broad_pairs, ra.max_penetration) == (rb.contact_count, rb.broad_pairs, rb.max_penetration)
+        np.testing.assert_array_equal(ra.residuals, rb.residuals)
+        sa, sb = a2.state(), b.state()
+        for k in sa:
+            np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
+        ra, rb = a2.step(), b.step()
