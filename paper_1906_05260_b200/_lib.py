@@ -8,9 +8,10 @@ import subprocess
 from . import capi
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-# VROD_B200_VARIANT=fast selects the FMA-contracted build of the same kernels (experiments).
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libvrod_b200_fast.so" if os.environ.get("VROD_B200_VARIANT") == "fast"
-                        else "libvrod_b200.so")
+# VROD_B200_VARIANT=<name> selects an experiment build lib/libvrod_b200_<name>.so of the same
+# kernels (`make -C csrc VARIANT=<name> XFLAGS=...`; `fast` = the FMA-contracted build).
+_VARIANT = os.environ.get("VROD_B200_VARIANT")
+LIB_PATH = os.path.join(PKG_DIR, "lib", f"libvrod_b200_{_VARIANT}.so" if _VARIANT else "libvrod_b200.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 
 _lib = None
