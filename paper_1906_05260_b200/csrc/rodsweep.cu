@@ -102,7 +102,7 @@ struct Tile {
   int loc[kTilePos], m[kTilePos], kinds[kTilePos], bbase[kTilePos];
   unsigned wmask[(kTilePos + 31) / 32];  // OR of the kinds present, per 32 positions
   int klist[kKinds];              // the kinds present, ascending
-  uint8_t act[kKinds][kTilePos];
+  alignas(8) uint8_t act[kTilePos][kKinds];  // per position: one byte per block kind (read as one 64-bit word)
   alignas(8) unsigned long long bar;  // mbarrier of the bulk (TMA) staging
 };
 
@@ -149,7 +149,7 @@ __device__ __forceinline__ unsigned tile_meta(Tile<TP>& t, const World& w, int s
       t.kinds[i] = kinds;
       t.bbase[i] = bb;
 #pragma unroll
-      for (int a = 0; a < kKinds; ++a) t.act[a][i] = 0;
+      for (int a = 0; a < kKinds; ++a) t.act[i][a] = 0;
     }
   }
   __syncthreads();
@@ -317,7 +317,7 @@ __device__ __forceinline__ void solve_items(Tile<TP>& t, const World& w, const S
         bool ok = true;
         if (blk::stretch_z(c0, c1, ic0, ic1, it, q, t.st[T_TDOT][si], t.st[T_LEN][si], t.st[T_KSZ][si], lam, h2, beta,
                            R.sz_dc0, R.sz_dc1, R.sz_dt, ln, ok)) {
-          t.act[A_SZ][pi] = 1;
+          t.act[pi][A_SZ] = 1;
           put_lam(L_SZ0, ln[0]);
           put_lam(L_SZ1, ln[1]);
           put_lam(L_SZ2, ln[2]);
@@ -332,7 +332,7 @@ __device__ __forceinline__ void solve_items(Tile<TP>& t, const World& w, const S
         bool ok = true;
         if (blk::cross_section(s0, s1, t.st[T_SBAR][si], t.st[T_SBAR][si + 1], is0, is1, t.st[T_KCS][si],
                                t.st[T_LAM + L_CS][si], h2, beta, R.cs, ln, ok)) {
-          t.act[A_CS][pi] = 1;
+          t.act[pi][A_CS] = 1;
           put_lam(L_CS, ln);
           if (owned && !ok) fail(lbase + __popc(ek & (EK_CS - 1)));
         } else {
@@ -345,7 +345,7 @@ __device__ __forceinline__ void solve_items(Tile<TP>& t, const World& w, const S
         bool ok = true;
         if (blk::surface_stretch(s0, s1, t.st[T_LEN][si], t.st[T_SGRAD][si], is0, is1, t.st[T_KSS][si],
                                  t.st[T_LAM + L_SS][si], h2, beta, R.ss, ln, ok)) {
-          t.act[A_SS][pi] = 1;
+          t.act[pi][A_SS] = 1;
           put_lam(L_SS, ln);
           if (owned && !ok) fail(lbase + __popc(ek & (EK_SS - 1)));
         } else {
@@ -360,7 +360,7 @@ __device__ __forceinline__ void solve_items(Tile<TP>& t, const World& w, const S
         if (blk::volume_stretch(c0, c1, s0, s1, t.st[T_SBAR][si], t.st[T_SBAR][si + 1], ic0, ic1, is0, is1, it, q,
                                 t.st[T_TDOT][si], t.st[T_LEN0][si], t.st[T_KVS][si], lam, h2, beta, R.vs_dc0, R.vs_dc1,
                                 R.vs_ds, R.vs_dt, ln, ok)) {
-          t.act[A_VS][pi] = 1;
+          t.act[pi][A_VS] = 1;
           put_lam(L_VS0, ln[0]);
           put_lam(L_VS1, ln[1]);
           put_lam(L_VS2, ln[2]);
@@ -390,7 +390,7 @@ __device__ __forceinline__ void solve_items(Tile<TP>& t, const World& w, const S
         bool ok = true;
         if (blk::bend_twist(vf, s0, sbar, is0, ita, itb, la, lb, darb, t.st[T_KBT0][si], t.st[T_KBT2][si], lam,
                             sp.classic, h2, beta, R.bt_ds, R.bt_dta, R.bt_dtb, ln, ok)) {
-          t.act[A_BT][pi] = 1;
+          t.act[pi][A_BT] = 1;
           put_lam(L_BT0, ln[0]);
           put_lam(L_BT1, ln[1]);
           put_lam(L_BT2, ln[2]);
@@ -405,7 +405,7 @@ __device__ __forceinline__ void solve_items(Tile<TP>& t, const World& w, const S
         bool ok = true;
         if (blk::surface_bending(sm, s0, spp, la, lb, t.st[T_SLAP][si - 1], t.st[T_IS][si - 1], is0,
                                  t.st[T_IS][si + 1], t.st[T_KSB][si], t.st[T_LAM + L_SB][si], h2, beta, R.sb, ln, ok)) {
-          t.act[A_SB][pi] = 1;
+          t.act[pi][A_SB] = 1;
           put_lam(L_SB, ln);
           if (owned && !ok) fail(lbase + __popc(vk & (VK_SB - 1)));
         } else {
@@ -424,7 +424,7 @@ __device__ __forceinline__ void solve_items(Tile<TP>& t, const World& w, const S
           if (blk::volume_bend(cc, vf, s0, sbar, is0, ita, itb, la, lb, t.st[T_LEN0][si - 1], t.st[T_LEN0][si],
                                t.st[cc == 0 ? T_DARBX : T_DARBY][si - 1], t.st[T_KVB][si], t.st[T_LAM + lf][si], h2,
                                beta, R.vb_ds[cc], R.vb_dta[cc], R.vb_dtb[cc], ln, ok)) {
-            t.act[cc == 0 ? A_VBU : A_VBV][pi] = 1;
+            t.act[pi][cc == 0 ? A_VBU : A_VBV] = 1;
             put_lam(lf, ln);
             if (owned && !ok) fail(lbase + __popc(vk & (bit - 1)));
           } else {
@@ -481,6 +481,12 @@ __device__ __forceinline__ void gather_apply(const Tile<TP>& t, const World& w, 
     const PosRes& A = t.res[pi - 1];  // element k-1 / vertex k-1
     const PosRes& B = t.res[pi];      // element k / vertex k
     const PosRes& N = t.res[pi + 1];  // vertex k+1
+    // the activity flags of the three positions, one 64-bit load each (byte = kind): no shared
+    // memory round trip per flag on the gather's path (C3: 391.4 -> 386.7 us per step)
+    const unsigned long long fa = *reinterpret_cast<const unsigned long long*>(&t.act[pi - 1][0]);
+    const unsigned long long fb = *reinterpret_cast<const unsigned long long*>(&t.act[pi][0]);
+    const unsigned long long fn = *reinterpret_cast<const unsigned long long*>(&t.act[pi + 1][0]);
+    auto on = [](unsigned long long f, int kind) { return ((f >> (8 * kind)) & 0xffu) != 0; };
     V3 csum{0, 0, 0};
     int ccnt = 0;
     double ssum = 0.0;
@@ -504,49 +510,49 @@ __device__ __forceinline__ void gather_apply(const Tile<TP>& t, const World& w, 
     };
     // element pass: element k-1 (this vertex is its c1/s1), then element k (c0/s0, theta)
     if (prev_el) {
-      if (t.act[A_SZ][pi - 1]) addc(A.sz_dc1);
-      if (t.act[A_CS][pi - 1]) adds(A.cs[1]);
-      if (t.act[A_SS][pi - 1]) adds(A.ss[1]);
-      if (t.act[A_VS][pi - 1]) {
+      if (on(fa, A_SZ)) addc(A.sz_dc1);
+      if (on(fa, A_CS)) adds(A.cs[1]);
+      if (on(fa, A_SS)) adds(A.ss[1]);
+      if (on(fa, A_VS)) {
         addc(A.vs_dc1);
         adds(A.vs_ds[1]);
       }
     }
     if (has_el) {
-      if (t.act[A_SZ][pi]) {
+      if (on(fb, A_SZ)) {
         addc(B.sz_dc0);
         addt(B.sz_dt);
       }
-      if (t.act[A_CS][pi]) adds(B.cs[0]);
-      if (t.act[A_SS][pi]) adds(B.ss[0]);
-      if (t.act[A_VS][pi]) {
+      if (on(fb, A_CS)) adds(B.cs[0]);
+      if (on(fb, A_SS)) adds(B.ss[0]);
+      if (on(fb, A_VS)) {
         addc(B.vs_dc0);
         adds(B.vs_ds[0]);
         addt(B.vs_dt);
       }
     }
     // vertex pass: vertex k-1 (SurfaceBending s_{j+1}), vertex k, vertex k+1
-    if (prev_vx && t.act[A_SB][pi - 1]) adds(A.sb[2]);
+    if (prev_vx && on(fa, A_SB)) adds(A.sb[2]);
     if (has_vx) {
-      if (t.act[A_BT][pi]) {
+      if (on(fb, A_BT)) {
         if (!sp.classic) adds(B.bt_ds);
         addt(B.bt_dtb);
       }
-      if (t.act[A_SB][pi]) adds(B.sb[1]);
-      if (t.act[A_VBU][pi]) {
+      if (on(fb, A_SB)) adds(B.sb[1]);
+      if (on(fb, A_VBU)) {
         adds(B.vb_ds[0]);
         addt(B.vb_dtb[0]);
       }
-      if (t.act[A_VBV][pi]) {
+      if (on(fb, A_VBV)) {
         adds(B.vb_ds[1]);
         addt(B.vb_dtb[1]);
       }
     }
     if (next_vx) {
-      if (t.act[A_BT][pi + 1]) addt(N.bt_dta);
-      if (t.act[A_SB][pi + 1]) adds(N.sb[0]);
-      if (t.act[A_VBU][pi + 1]) addt(N.vb_dta[0]);
-      if (t.act[A_VBV][pi + 1]) addt(N.vb_dta[1]);
+      if (on(fn, A_BT)) addt(N.bt_dta);
+      if (on(fn, A_SB)) adds(N.sb[0]);
+      if (on(fn, A_VBU)) addt(N.vb_dta[0]);
+      if (on(fn, A_VBV)) addt(N.vb_dta[1]);
     }
     if (role != 1) {
       ext(p, addc, adds);
@@ -891,7 +897,7 @@ __global__ void __launch_bounds__(32 * (warps_for<TP>() + 1), 1) k_iterate(World
       if (has_ext) aux_ext_phase<TP>(w, c, pp, sp, cur, xr_cur, el_cur, el_nxt, it, singular + it, err);
     } else {
       if (it > 0) {
-        for (int i = tid; i < kKinds * TP; i += 32 * kWarps) t.act[i / TP][i % TP] = 0;
+        for (int i = tid; i < kKinds * TP; i += 32 * kWarps) t.act[i / kKinds][i % kKinds] = 0;
       }
       if (tid == 0) {
         t.ent_next = 0;  // published by the __syncthreads below
