@@ -89,7 +89,6 @@ __device__ __forceinline__ ExtResult ext_block(const World& w, const Collide& c,
   const int npins = sp.n_pins;
   const int vp = w.vpad;
   const double h2 = sp.h2;
-  const double contact_k = sp.contact_k;
   bool active = false, finite = true;
   if (b < npins) {  // kPin (constraints.cpp:261-267), dim 3
     r.nlam = 3;
@@ -175,7 +174,7 @@ __device__ __forceinline__ ExtResult ext_block(const World& w, const Collide& c,
         if (is == 0.0) continue;
         M = M + (h2 * is * sj[e]) * sj[e];
       }
-      const double kinv = inverse_stiffness(contact_k);
+      const double kinv = sp.contact_kinv;
       M = M + kinv;
       const double rhs = W - kinv * r.lam[0];
       if (M <= 1e-250) {
@@ -227,7 +226,7 @@ __device__ __forceinline__ ExtResult ext_block(const World& w, const Collide& c,
         M = M + (((s * n3.x) * n3.x + (s * n3.y) * n3.y) + (s * n3.z) * n3.z);
       }
       if (is != 0.0) M = M + (h2 * is * -rbar) * -rbar;
-      const double kinv = inverse_stiffness(contact_k);
+      const double kinv = sp.contact_kinv;
       M = M + kinv;
       const double rhs = W - kinv * r.lam[0];
       if (M <= 1e-250) {

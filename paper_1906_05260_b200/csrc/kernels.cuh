@@ -182,7 +182,7 @@ struct SweepParams {
   int substep;         // substep index within the step (error word)
   int n_pins;
   int elastic_blocks;  // first external block index in the reference's block list
-  double contact_k;    // settings.contact_stiffness
+  double contact_kinv;  // inverse_stiffness(settings.contact_stiffness), computed once on the host
   // Programmatic dependent launch inside the iteration loop: 0 off; 1 the kernel waits for its
   // predecessor before touching any state; 2 (rod sweep right after an ext solve) it stages
   // and solves its tile first and waits only before gathering the external contributions.

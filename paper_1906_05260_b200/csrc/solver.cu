@@ -749,7 +749,7 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
     double* cur = w_.X;
     double* nxt = w_.Y;
     vdev::SweepParams sp{h, h2, scene_.settings.beta, classic_ ? 1 : 0, 0, s, c_.n_pins, setup_.elastic_blocks,
-                         scene_.settings.contact_k, 0, nullptr, nullptr, nullptr};
+                         vm::inverse_stiffness(scene_.settings.contact_k), 0, nullptr, nullptr, nullptr};
     const bool pdl = vdev::g_pdl;
     double* lam_a = w_.lam;
     double* lam_b = w_.lam + static_cast<std::size_t>(vdev::kLamFields) * w_.vpad;
@@ -961,7 +961,7 @@ std::pair<int, int> Solver::jacobi_sweep(double h, double beta) {
   double* lam_a = w_.lam;
   double* lam_b = w_.lam + static_cast<std::size_t>(vdev::kLamFields) * w_.vpad;
   vdev::SweepParams sp{h, h * h, beta, classic_ ? 1 : 0, 0, 0, c_.n_pins, setup_.elastic_blocks,
-                       scene_.settings.contact_k, 0, nullptr, lam_a, lam_b};
+                       vm::inverse_stiffness(scene_.settings.contact_k), 0, nullptr, lam_a, lam_b};
   vdev::launch_iteration(w_, c_, w_.X, w_.Y, sp, d_singular_, d_err_, st);
   vdev::launch_copy_state(w_, w_.Y, w_.X, st);
   check_cuda(cudaGetLastError(), "sweep launch");
