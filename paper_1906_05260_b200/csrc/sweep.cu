@@ -315,7 +315,8 @@ __global__ void __launch_bounds__(kExtSmemThreads) k_ext_setup_smem(Collide c, i
     }
   }
   __syncthreads();
-  // k_ext_sort: warps over 32 consecutive slots at a time, ranking the busy slots' entries
+  // k_ext_sort: warps over 32 consecutive slots at a time, ranking the busy slots' entries in
+  // place (no global memory on this loop's path) ...
   for (int v0 = 32 * wid; v0 < V; v0 += kExtSmemThreads) {
     const int vl = v0 + lane;
     const int ml = vl < V ? s_off[vl + 1] - s_off[vl] : 0;
@@ -328,14 +329,10 @@ __global__ void __launch_bounds__(kExtSmemThreads) k_ext_setup_smem(Collide c, i
         const int key = lane < m ? items[s0 + lane] : 0x7fffffff;
         int rank = 0;
         for (int j = 0; j < m; ++j) rank += __shfl_sync(0xffffffffu, key, j) < key ? 1 : 0;
-        if (lane < m) {
-          c.ext_items[s0 + rank] = key;
-          c.ext_pos[key] = s0 + rank;
-          c.ext_ab[s0 + rank] = entry_ab(c, key, npins, nct);
-        }
+        if (lane < m) items[s0 + rank] = key;
       } else {
         __syncwarp();
-        if (lane == 0) {  // insertion sort in place, then out
+        if (lane == 0) {  // insertion sort in place
           for (int a = s0 + 1; a < s0 + m; ++a) {
             const int key = items[a];
             int b = a - 1;
@@ -345,15 +342,18 @@ __global__ void __launch_bounds__(kExtSmemThreads) k_ext_setup_smem(Collide c, i
             }
             items[b + 1] = key;
           }
-          for (int a = s0; a < s0 + m; ++a) {
-            c.ext_items[a] = items[a];
-            c.ext_pos[items[a]] = a;
-            c.ext_ab[a] = entry_ab(c, items[a], npins, nct);
-          }
         }
       }
       __syncwarp();
     }
+  }
+  __syncthreads();
+  // ... then every entry's outputs in one parallel pass (the alpha / beta loads all in flight)
+  for (int q = tid; q < total; q += kExtSmemThreads) {
+    const int key = items[q];
+    c.ext_items[q] = key;
+    c.ext_pos[key] = q;
+    c.ext_ab[q] = entry_ab(c, key, npins, nct);
   }
 }
 
