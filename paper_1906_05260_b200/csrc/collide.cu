@@ -18,6 +18,7 @@
 
 #include "kernels.cuh"
 #include "pill.cuh"
+#include "pillbounds.cuh"
 #include "vmath.cuh"
 
 namespace vdev {
@@ -121,25 +122,6 @@ __device__ void deepest(const PillV& A, const PillV& B, int iterations, double w
   deepest_search(A, B, iterations, s);
   deepest_finish(s, warm, alpha_out, beta_out, dist_out);
 }
-// bounding_sphere, collision.cpp:137-153.
-__device__ __forceinline__ void bounding_sphere(const PillV& p, V3& c, double& r) {
-  const V3 axis = p.c1 - p.c0;
-  const double l = norm(axis);
-  if (l + p.r1 <= p.r0) {
-    c = p.c0;
-    r = p.r0;
-    return;
-  }
-  if (l + p.r0 <= p.r1) {
-    c = p.c1;
-    r = p.r1;
-    return;
-  }
-  const double u = 0.5 * (l + p.r1 - p.r0);
-  c = p.c0 + (u / l) * axis;
-  r = 0.5 * (l + p.r0 + p.r1);
-}
-
 __device__ __forceinline__ unsigned long long pair_key(uint32_t ia, uint32_t ib) {  // collision.cpp:240-249
   if (ia > ib) {
     const uint32_t t = ia;
@@ -176,22 +158,6 @@ __device__ __forceinline__ bool pair_allowed(int ra, int ga, bool sa, int ea, in
 
 // ---- pipeline kernels ----------------------------------------------------------------------
 
-// Pill i's bounding sphere into bsph, the finiteness check; returns its radius bits (0 if not finite).
-__device__ __forceinline__ unsigned long long pill_bounds(const Collide& c, const PillV& p, int i, int substep,
-                                                         unsigned long long* err) {
-  V3 ctr;
-  double r;
-  bounding_sphere(p, ctr, r);
-  c.bsph[i] = ctr.x;
-  c.bsph[c.P + i] = ctr.y;
-  c.bsph[2 * c.P + i] = ctr.z;
-  c.bsph[3 * c.P + i] = r;
-  if (!(finite3(ctr) && isfinite(r))) {
-    if (c.P >= 2) atomicMin(err, err_code(substep, ERR_BROAD, 0, i));
-    return 0;
-  }
-  return static_cast<unsigned long long>(__double_as_longlong(r));  // r >= 0: bit order == value order
-}
 // rod_pills from the predicted state + the posed kinematic pills of this substep. bounds != 0
 // (single-scene worlds; the broad phase's resets already ran): each pill's bounding sphere and the
 // max radius too (k_bounds' work, one launch less).
@@ -1406,6 +1372,7 @@ cudaEvent_t g_broad_mark = nullptr;
 
 // The broad phase's per-call resets, one fill launch.
 bool g_broad_resets_done = false;
+bool g_pills_built = false;
 
 void broad_reset_list(const Collide& c, int do_narrow, FillList& f) {
   f.add(c.maxr_bits, 2, 0);
@@ -1485,7 +1452,10 @@ void launch_collide(const World& w, Collide& c, const double* anim, const AnimLa
   // (g_broad_resets_done: the step prologue already did them, see Solver::record_step)
   if (fused_bounds && !g_broad_resets_done) launch_broad_resets(c, 1, st);
   g_broad_resets_done = false;
-  launch_kernel(k_build_pills, nb, kThreads, 0, st, g_pdl, w, c, anim, al, fused_bounds ? 1 : 0, substep, err);
+  // (g_pills_built: the prediction launch built the pills and bounds, launch_animate_predict)
+  if (!(g_pills_built && fused_bounds))
+    launch_kernel(k_build_pills, nb, kThreads, 0, st, g_pdl, w, c, anim, al, fused_bounds ? 1 : 0, substep, err);
+  g_pills_built = false;
   if (!possible) {  // no pair can pass pair_allowed: only broad_phase's finiteness check remains
     if (c.P >= 2) launch_kernel(k_bounds, (c.P + kThreads - 1) / kThreads, kThreads, 0, st, g_pdl, c, substep, err);
     return;

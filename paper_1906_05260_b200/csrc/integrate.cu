@@ -4,6 +4,7 @@
 // solver.cpp:253-289). Compiled with --fmad=false: every expression keeps the reference's
 // operation order, so these kernels reproduce the oracle bit for bit.
 #include "kernels.cuh"
+#include "pillbounds.cuh"
 #include "vmath.cuh"
 
 namespace vdev {
@@ -148,7 +149,8 @@ __device__ __forceinline__ double predicted_scale(const World& w, double h, int 
 // prediction check (:179-181). Also takes the pre-predict snapshot (solver.cpp:311-316).
 // Returns the predicted scale.
 __device__ __forceinline__ double predict_vertex(const World& w, const double* __restrict__ anim, const AnimLayout& al,
-                                                 const V3& g, double h, int substep, unsigned long long* err, int v) {
+                                                 const V3& g, double h, int substep, unsigned long long* err, int v,
+                                                 V3* c_out = nullptr) {
   const int vp = w.vpad;
   const int r = w.slot_rod[v];
   const int k = w.slot_loc[v];
@@ -197,6 +199,7 @@ __device__ __forceinline__ double predict_vertex(const World& w, const double* _
   double2* xr = reinterpret_cast<double2*>(w.xrec + 8ll * v);
   xr[0] = make_double2(c.x, c.y);
   xr[1] = make_double2(c.z, s);
+  if (c_out) *c_out = c;
   return s;
 }
 
@@ -263,9 +266,13 @@ __global__ void k_predict_elements(World w, double h, int substep, unsigned long
 // With activations, their rods' CTAs come first in the same launch (activation_block: disjoint
 // fields — LEN and the length-derived statics — from the ones the prediction reads and writes).
 constexpr int kPredictRodsPerCta = 4;
+// pills != 0 (single-scene worlds without kinematic pills; the broad phase's resets already ran):
+// also the rod pills of the predicted state with their bounding spheres and the max radius
+// (k_build_pills' work: the same values from the same operands, one launch less).
 __global__ void __launch_bounds__(32 * kPredictRodsPerCta) k_predict_rods(World w, const double* __restrict__ anim,
                                                                          AnimLayout al, V3 g, double h, int substep,
-                                                                         unsigned long long* err, ActArgs aa) {
+                                                                         unsigned long long* err, ActArgs aa,
+                                                                         Collide cl, int pills) {
   pdl_wait();
   pdl_trigger();
   if (static_cast<int>(blockIdx.x) < aa.n_rods) {
@@ -276,8 +283,30 @@ __global__ void __launch_bounds__(32 * kPredictRodsPerCta) k_predict_rods(World 
   if (r >= w.R) return;  // whole warps
   const int k = threadIdx.x & 31, n = w.rod_n[r], v = w.rod_vbase[r] + k;
   double s0 = 0.0;
-  if (k < n) s0 = predict_vertex(w, anim, al, g, h, substep, err, v);
+  V3 c0{0, 0, 0};
+  if (k < n) s0 = predict_vertex(w, anim, al, g, h, substep, err, v, &c0);
   const double s1 = __shfl_down_sync(0xffffffffu, s0, 1);
+  if (pills) {  // rod_pills (collision.cpp:275-296) + bounding spheres
+    const V3 c1{__shfl_down_sync(0xffffffffu, c0.x, 1), __shfl_down_sync(0xffffffffu, c0.y, 1),
+                __shfl_down_sync(0xffffffffu, c0.z, 1)};
+    unsigned long long bits = 0;
+    if (k < n - 1) {
+      const int vp = w.vpad;
+      const PillV p{c0, c1, s0 * w.vstat[RBAR * vp + v], s1 * w.vstat[RBAR * vp + v + 1]};
+      const int i = v - r;
+      double2* o = reinterpret_cast<double2*>(cl.pill + 8ll * i);
+      o[0] = make_double2(p.c0.x, p.c0.y);
+      o[1] = make_double2(p.c0.z, p.c1.x);
+      o[2] = make_double2(p.c1.y, p.c1.z);
+      o[3] = make_double2(p.r0, p.r1);
+      bits = pill_bounds(cl, p, i, substep, err);
+    }
+    for (int o = 16; o > 0; o >>= 1) {  // warp max, one atomic per warp
+      const unsigned long long x = __shfl_down_sync(0xffffffffu, bits, o);
+      bits = x > bits ? x : bits;
+    }
+    if (k == 0 && bits) atomicMax(cl.maxr_bits, bits);
+  }
   if (k < n - 1) predict_element(w, h, substep, err, v, s0, s1);
 }
 
@@ -346,14 +375,15 @@ __global__ void k_copy_state(int V, int vpad, const double* __restrict__ src, do
 void launch_animate_predict(const World& w, const double* anim, const AnimLayout& al, const int* pm_slot,
                             const int* act_rod_off, const int* act_list, double* act_applied, const int* act_rods,
                             int n_act_rods, const double* gravity_h, double h, int substep, unsigned long long* err,
-                            cudaStream_t st) {
+                            const Collide* pills, cudaStream_t st) {
   if (al.n_pm > 0) launch_kernel(k_pin_motions, (al.n_pm + 127) / 128, 128, 0, st, g_pdl, w, anim, al, pm_slot);
   // act_static follows act_applied in the same allocation (see solver.cu)
   ActArgs aa{act_rod_off, act_list, act_applied, act_rods, act_applied + al.n_act, n_act_rods};
   const V3 g{gravity_h[0], gravity_h[1], gravity_h[2]};
   if (w.max_rod_n <= 32) {  // activation + prediction in one launch
     launch_kernel(k_predict_rods, n_act_rods + (w.R + kPredictRodsPerCta - 1) / kPredictRodsPerCta,
-                  32 * kPredictRodsPerCta, 0, st, g_pdl, w, anim, al, g, h, substep, err, aa);
+                  32 * kPredictRodsPerCta, 0, st, g_pdl, w, anim, al, g, h, substep, err, aa, pills ? *pills : Collide{},
+                  pills ? 1 : 0);
     return;
   }
   if (n_act_rods > 0) launch_kernel(k_activation, n_act_rods, 128, 0, st, g_pdl, w, anim, al, aa);

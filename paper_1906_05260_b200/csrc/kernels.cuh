@@ -265,17 +265,21 @@ void launch_fill(const FillList& f, cudaStream_t st);
 // The broad phase's per-substep resets (launch_broad_resets' list); g_broad_resets_done: the
 // next launch_collide skips them (already done by the caller).
 void broad_reset_list(const Collide& c, int do_narrow, FillList& f);
+void launch_broad_resets(Collide& c, int do_narrow, cudaStream_t st);
 extern bool g_broad_resets_done;
+extern bool g_pills_built;  // the next launch_collide skips k_build_pills (built by the prediction launch)
 void scan_exclusive(const int* in, int* out, long long n_cap, const int* n_dev, int* partials, int parts,
                     cudaStream_t st);
 long long scan_partials_needed(long long n);
 
 // integrate.cu
 // animate (pin motions, activations) + predict_rod / warm_start_lbs / orientation inertia
+// pills (non-null, rods <= 32 vertices only): the prediction launch also builds the rod pills and
+// their bounding spheres (the broad-phase resets must have run), see launch_collide's pills_built.
 void launch_animate_predict(const World& w, const double* anim, const AnimLayout& al, const int* pm_slot,
                             const int* act_rod_off, const int* act_list, double* act_applied, const int* act_rods,
                             int n_act_rods, const double* gravity_h, double h, int substep, unsigned long long* err,
-                            cudaStream_t st);
+                            const Collide* pills, cudaStream_t st);
 void launch_finalize_from(const World& w, const double* src, double h, double keep, cudaStream_t st);
 void launch_copy_state(const World& w, const double* src, double* dst, cudaStream_t st);
 

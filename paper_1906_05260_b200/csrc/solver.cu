@@ -724,11 +724,16 @@ void Solver::record_step(double h, int substeps, int iterations, double* probe_l
   for (int s = 0; s < substeps; ++s) {
     const double* anim = d_anim_ + static_cast<std::size_t>(al_.stride) * s;
     begin(CAT_PREDICT);
+    // single-scene worlds of short rods without kinematic pills: the prediction launch also builds
+    // the pills and their bounds, after the broad phase's resets (the prologue's for substep 0)
+    const bool pills_in_predict = pro_broad && w_.max_rod_n <= 32 && w_.K == 0 && !std::getenv("VROD_PILLS_APART");
+    if (pills_in_predict && s > 0) vdev::launch_broad_resets(c_, 1, st);
     vdev::launch_animate_predict(w_, anim, al_, d_pm_slot_, d_act_rod_off_, d_act_list_, d_act_applied_, d_act_rods_,
-                                 n_act_rods_, g, h, s, d_err_, st);
+                                 n_act_rods_, g, h, s, d_err_, pills_in_predict ? &c_ : nullptr, st);
+    vdev::g_pills_built = pills_in_predict;
     end();
     begin_collide();
-    vdev::g_broad_resets_done = s == 0 && pro_broad;
+    vdev::g_broad_resets_done = (s == 0 && pro_broad) || pills_in_predict;
     if (c_.P >= 1) vdev::launch_collide(w_, c_, anim, al_, s, d_err_, d_acc_, collide_possible_ ? 1 : 0, st);
     if (prof && vdev::g_broad_mark) {
       // no pair scan ran (nothing can collide): the broad phase ends here
