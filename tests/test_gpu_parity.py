@@ -432,3 +432,27 @@ def test_incidence_setup_paths_agree(gpu, oracle, name, monkeypatch):
         for k in sa:
             np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
         ra, rb = a2.step(), b.step()
+
+
+@pytest.mark.parametrize("name", ["pile", "crossing", "kitchen_sink", "mini_muscle"])
+def test_pills_in_prediction_launch_agree(gpu, oracle, name, monkeypatch):
+    """Single-scene worlds of short rods build their pills and bounding spheres inside the
+    prediction launch (integrate.cu k_predict_rods); VROD_PILLS_APART=1 keeps k_build_pills.
+    Same operands, same bits: states, reports and contacts, step after step."""
+    scene = SCENES[name](oracle)
+    monkeypatch.setenv("VROD_PILLS_APART", "1")
+    b = SolverHandle(gpu, scene)
+    rb = b.step()
+    monkeypatch.delenv("VROD_PILLS_APART")
+    a = SolverHandle(gpu, scene)
+    ra = a.step()
+    for _ in range(3):
+        assert (ra.contact_count, ra.broad_pairs, ra.max_penetration) == (rb.contact_count, rb.broad_pairs, rb.max_penetration)
+        np.testing.assert_array_equal(ra.residuals, rb.residuals)
+        sa, sb = a.state(), b.state()
+        for k in sa:
+            np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
+        ca, cb = a.contacts(), b.contacts()
+        for k in ca:
+            np.testing.assert_array_equal(ca[k], cb[k], err_msg=k)
+        ra, rb = a.step(), b.step()
