@@ -353,15 +353,23 @@ def test_persistent_kernel_matches_per_launch_path(gpu, oracle, name, exact, mon
     assert _iterate_launches(gpu, a) > 0 and _iterate_launches(gpu, c) > 0  # the persistent paths really ran
 
 
-@pytest.mark.parametrize("warp", ["1", "0"])
+WARP_VARIANTS = {"1": {"VROD_ROD_WARP": "1"}, "0": {"VROD_ROD_WARP": "0"},
+                 "lanes": {"VROD_WARP_TMA": "0"}, "minb4": {"VROD_WARP_MINB": "4"},
+                 "noprefetch": {"VROD_WARP_PREFETCH": "0"}, "nopdl": {"VROD_PDL": "0"}}
+
+
+@pytest.mark.parametrize("warp", list(WARP_VARIANTS))
 def test_large_world_tiles_bitwise(gpu, oracle, warp, monkeypatch):
     """Large worlds whose rods all fit a warp (<= 32 vertices: C4, C5) run the warp-per-rod sweep
     (k_rod_sweep_warp); VROD_ROD_WARP=0 forces the 64-wide tile kernel that longer rods take in
     worlds of >= 2 x 148 x 62 slots (bulk TMA staging of interior tiles, cp.async at the world's
-    edges, early ext wait + L2 prefetch). A 40 x 20 forest of 24-vertex rods (19,200 slots, live
-    contacts) must stay bit-identical to the oracle on both."""
+    edges, early ext wait + L2 prefetch). The warp sweep's A/B switches (per-lane loads instead
+    of the tensor staging, 4 CTAs per SM, no L2 prefetch) and no programmatic dependent launch
+    must not change a bit either. A 40 x 20 forest of 24-vertex rods (19,200 slots, live
+    contacts) must stay bit-identical to the oracle on every variant."""
     from paper_1906_05260_b200 import workloads
-    monkeypatch.setenv("VROD_ROD_WARP", warp)
+    for k, v in WARP_VARIANTS[warp].items():
+        monkeypatch.setenv(k, v)
     scene = workloads.c4_rod_forest(oracle, nx=40, ny=20, vertices=24)
     g, o = SolverHandle(gpu, scene), SolverHandle(oracle, scene)
     assert g.total_vertices >= 2 * 148 * 62
