@@ -201,39 +201,79 @@ __device__ __forceinline__ double entry_ab(const Collide& c, int key, int npins,
 // Orders each slot's incidence entries by (block, endpoint): one warp per slot; up to 32 entries
 // are ranked in registers (keys are distinct), longer lists fall back to an insertion sort. Each
 // entry's alpha / beta is stored beside it (ext_ab), so the sweeps' gathers read it contiguously.
+// A slot's list, whole warp: ranked in registers up to 32 entries (keys are distinct), longer
+// lists by an insertion sort on lane 0.
+__device__ __forceinline__ void ext_sort_slot_warp(const Collide& c, int s0, int n, int npins, int nct, int lane) {
+  if (n <= 32) {
+    const int key = lane < n ? c.ext_items[s0 + lane] : 0x7fffffff;
+    int rank = 0;
+    for (int j = 0; j < n; ++j) rank += __shfl_sync(0xffffffffu, key, j) < key ? 1 : 0;
+    __syncwarp();
+    if (lane < n) {
+      c.ext_items[s0 + rank] = key;
+      c.ext_pos[key] = s0 + rank;
+      c.ext_ab[s0 + rank] = entry_ab(c, key, npins, nct);
+    }
+  } else if (lane == 0) {
+    const int s1 = s0 + n;
+    for (int a = s0 + 1; a < s1; ++a) {  // insertion sort: block order, then endpoint
+      const int key = c.ext_items[a];
+      int b = a - 1;
+      while (b >= s0 && c.ext_items[b] > key) {
+        c.ext_items[b + 1] = c.ext_items[b];
+        --b;
+      }
+      c.ext_items[b + 1] = key;
+    }
+    for (int a = s0; a < s1; ++a) {
+      c.ext_pos[c.ext_items[a]] = a;
+      c.ext_ab[a] = entry_ab(c, c.ext_items[a], npins, nct);
+    }
+  }
+  __syncwarp();
+}
+
+#ifndef VROD_EXT_SORT_G
+#define VROD_EXT_SORT_G 16  // C4: incidence setup 0.352 -> 0.334 ms per substep (8: 0.334, A/B)
+#endif
+// Each warp takes 32 / kG consecutive slots at a time, one kG-lane group per slot: lists of up to
+// kG entries are ranked inside their group, longer ones afterwards by the whole warp.
 __global__ void k_ext_sort(Collide c, int V, int npins) {
   pdl_wait();
   pdl_trigger();
+  constexpr int kG = VROD_EXT_SORT_G, kPer = 32 / kG;
   const int nct = c.scalars[SC_NCT];
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, sub = lane / kG, gl = lane % kG;
   const int warps = gridDim.x * (blockDim.x >> 5);
-  for (int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < V; v += warps) {
-    const int s0 = c.ext_off[v], s1 = c.ext_off[v + 1], n = s1 - s0;
-    if (n <= 0) continue;
-    if (n <= 32) {
-      const int key = lane < n ? c.ext_items[s0 + lane] : 0x7fffffff;
-      int rank = 0;
-      for (int j = 0; j < n; ++j) rank += __shfl_sync(0xffffffffu, key, j) < key ? 1 : 0;
-      __syncwarp();
-      if (lane < n) {
-        c.ext_items[s0 + rank] = key;
-        c.ext_pos[key] = s0 + rank;
-        c.ext_ab[s0 + rank] = entry_ab(c, key, npins, nct);
-      }
-    } else if (lane == 0) {
-      for (int a = s0 + 1; a < s1; ++a) {  // insertion sort: block order, then endpoint
-        const int key = c.ext_items[a];
-        int b = a - 1;
-        while (b >= s0 && c.ext_items[b] > key) {
-          c.ext_items[b + 1] = c.ext_items[b];
-          --b;
-        }
-        c.ext_items[b + 1] = key;
-      }
-      for (int a = s0; a < s1; ++a) {
-        c.ext_pos[c.ext_items[a]] = a;
-        c.ext_ab[a] = entry_ab(c, c.ext_items[a], npins, nct);
-      }
+  for (int v0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kPer; v0 < V; v0 += warps * kPer) {
+    if (kG == 32) {
+      const int s0 = c.ext_off[v0], n = c.ext_off[v0 + 1] - s0;
+      if (n > 0) ext_sort_slot_warp(c, s0, n, npins, nct, lane);
+      continue;
+    }
+    const int v = v0 + sub;
+    int s0 = 0, n = 0;
+    if (v < V) {
+      s0 = c.ext_off[v];
+      n = c.ext_off[v + 1] - s0;
+    }
+    const bool small = n <= kG;
+    const int key = small && gl < n ? c.ext_items[s0 + gl] : 0x7fffffff;
+    int rank = 0;
+#pragma unroll
+    for (int j = 0; j < kG; ++j) rank += __shfl_sync(0xffffffffu, key, sub * kG + j) < key ? 1 : 0;
+    __syncwarp();
+    if (small && gl < n) {
+      c.ext_items[s0 + rank] = key;
+      c.ext_pos[key] = s0 + rank;
+      c.ext_ab[s0 + rank] = entry_ab(c, key, npins, nct);
+    }
+    unsigned big = __ballot_sync(0xffffffffu, !small && gl == 0);
+    while (big) {
+      const int src = __ffs(big) - 1;
+      big &= big - 1;
+      const int bs0 = __shfl_sync(0xffffffffu, s0, src), bn = __shfl_sync(0xffffffffu, n, src);
+      ext_sort_slot_warp(c, bs0, bn, npins, nct, lane);
     }
   }
 }
