@@ -1059,7 +1059,7 @@ constexpr unsigned kWarpStageBytes =
 // copies (X, vertex statics, element statics, multipliers) issued by one lane, completing on one
 // mbarrier — and every operand, the lane's own and its neighbours', is read from there;
 // otherwise each lane loads its own rows and takes the neighbours' by shuffle.
-template <int kMinBlocks, bool kStaged>
+template <int kMinBlocks, bool kStaged, bool kAll = false>
 __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_warp(World w, Collide c, const double* __restrict__ X,
                                                                       double* __restrict__ Y, SweepParams sp,
                                                                       int* singular, unsigned long long* err,
@@ -1075,7 +1075,8 @@ __global__ void __launch_bounds__(32 * kWarpRodsPerCta, kMinBlocks) k_rod_sweep_
   if (r >= w.R) return;  // whole warps only
   const int k = threadIdx.x & 31;
   const int n = w.rod_n[r], m = n - 1, vb = w.rod_vbase[r];
-  const int ek = w.rod_ekinds[r], vk = w.rod_vkinds[r], bb = w.rod_block_base[r];
+  // kAll (every rod has every kind): the kind tests below are compile-time true (C4: -1.3 %)
+  const int ek = kAll ? 15 : w.rod_ekinds[r], vk = kAll ? 15 : w.rod_vkinds[r], bb = w.rod_block_base[r];
   const int ne = __popc(ek), nv = __popc(vk);
   const bool valid = k < n;
   const long long vp = w.vpad;
@@ -1519,13 +1520,15 @@ void launch_rod_sweep(const World& w, Collide& c, const double* X, double* Y, co
     const CUtensorMap tx = rows_map(X, kStateFields, w.vpad), tv = rows_map(w.vstat, kVStatFields, w.vpad),
                       te = rows_map(w.estat, kSweepEStatFields, w.vpad), tl = rows_map(sp.lam_in, kLamFields, w.vpad);
     static const bool attrs = [] {
-      for (auto* k : {k_rod_sweep_warp<2, true>, k_rod_sweep_warp<3, true>, k_rod_sweep_warp<4, true>})
+      for (auto* k : {k_rod_sweep_warp<2, true>, k_rod_sweep_warp<3, true>, k_rod_sweep_warp<4, true>,
+                      k_rod_sweep_warp<3, true, true>})
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpRodsPerCta * sizeof(WarpStage));
       return true;
     }();
     (void)attrs;
     auto* kern = staged ? (minb <= 2 ? k_rod_sweep_warp<2, true> : minb == 3 ? k_rod_sweep_warp<3, true> : k_rod_sweep_warp<4, true>)
                         : (minb <= 2 ? k_rod_sweep_warp<2, false> : minb == 3 ? k_rod_sweep_warp<3, false> : k_rod_sweep_warp<4, false>);
+    if (staged && minb == 3 && w.all_kinds) kern = k_rod_sweep_warp<3, true, true>;
     launch_kernel(kern, (w.R + kWarpRodsPerCta - 1) / kWarpRodsPerCta, 32 * kWarpRodsPerCta, smem, st, sp.pdl != 0, w,
                   c, X, Y, spp, singular_counter, err, has_ext, tx, tv, te, tl);
     return;

@@ -402,6 +402,8 @@ void Solver::upload_static() {
   upload(w_.rod_self, self, stream_);
   upload(w_.rod_ekinds, setup_.ekinds, stream_);
   upload(w_.rod_vkinds, setup_.vkinds, stream_);
+  w_.all_kinds = R > 0 && std::all_of(setup_.ekinds.begin(), setup_.ekinds.end(), [](int k) { return k == 15; }) &&
+                 std::all_of(setup_.vkinds.begin(), setup_.vkinds.end(), [](int k) { return k == 15; });
   upload(w_.rod_bone_off, bone_off, stream_);
   upload(w_.rod_bones, bones, stream_);
   std::vector<double> mats;

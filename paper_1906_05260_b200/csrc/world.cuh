@@ -96,6 +96,7 @@ struct World {
   int P = 0;          // pills = E + K
   int classic = 0;    // ScaleMode::kPostStepLengthRatio
   int max_rod_n = 0;  // longest rod (vertices): <= 32 selects the warp-per-rod sweep
+  int all_kinds = 0;  // every rod has all 8 block kinds: the warp sweep's kind tests fold away
   int has_bones = 0;
   int has_loads = 0;
 
