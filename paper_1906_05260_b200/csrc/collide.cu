@@ -947,9 +947,48 @@ __global__ void k_ct_sort(Collide c) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < c.P) sort_pill_contacts(c, i);
 }
-// insertion sort of pill i's contacts by j (they are few)
+// pill i's contacts sorted by j (the pairs are unique): up to 8 in registers — all loads in flight
+// together, a fixed compare-exchange network, one store round — else an insertion sort in place
 __device__ void sort_pill_contacts(const Collide& c, int i) {
   const int s0 = c.ct_off[i], s1 = c.ct_off[i + 1];
+#ifndef VROD_CT_SORT_GLOBAL
+  constexpr int kR = 8;
+  if (s1 - s0 <= 1) return;
+  if (s1 - s0 <= kR) {
+    int kj[kR];
+    double ka[kR], kb[kR];
+#pragma unroll
+    for (int u = 0; u < kR; ++u) {
+      const bool in = s0 + u < s1;
+      kj[u] = in ? c.ct_b[s0 + u] : 0x7fffffff;
+      ka[u] = in ? c.ct_alpha[s0 + u] : 0.0;
+      kb[u] = in ? c.ct_beta[s0 + u] : 0.0;
+    }
+#pragma unroll
+    for (int a = 1; a < kR; ++a)
+#pragma unroll
+      for (int b = a; b > 0; --b)
+        if (kj[b - 1] > kj[b]) {
+          const int tj = kj[b - 1];
+          kj[b - 1] = kj[b];
+          kj[b] = tj;
+          const double ta = ka[b - 1];
+          ka[b - 1] = ka[b];
+          ka[b] = ta;
+          const double tb = kb[b - 1];
+          kb[b - 1] = kb[b];
+          kb[b] = tb;
+        }
+#pragma unroll
+    for (int u = 0; u < kR; ++u)
+      if (s0 + u < s1) {
+        c.ct_b[s0 + u] = kj[u];
+        c.ct_alpha[s0 + u] = ka[u];
+        c.ct_beta[s0 + u] = kb[u];
+      }
+    return;
+  }
+#endif
   for (int a = s0 + 1; a < s1; ++a) {
     const int kj = c.ct_b[a];
     const double ka = c.ct_alpha[a], kb = c.ct_beta[a];
