@@ -338,6 +338,18 @@ __global__ void k_scatter(Collide c) {
   sp[1] = make_double2(c.bsph[2 * c.P + i], c.bsph[3 * c.P + i]);
 }
 
+// The half-stencil span holding flattened item k: the largest d with off[d] <= k (off[0] = 0,
+// off[14] = the total > k); empty spans share their start with the next, which this picks.
+__device__ __forceinline__ int span_of(const int* off, int k) {
+  int lo = 0, hi = 13;
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= k) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 // The table slot of cell (kx, ky, kz, scene), or -1 (after k_scatter). An occupied slot has a
 // non-empty span in cell_start, and its key in slot_key: the three loads of a probe are
 // independent, so each probe of the linear chain costs one load round; the chain ends at the
@@ -495,7 +507,7 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) k_pairs_warp(Collide c, in
   const int4* __restrict__ attr = c.cell_attr;
   const double2* __restrict__ sph = reinterpret_cast<const double2*>(c.cell_sph);
   const long long cap = c.cand_cap;
-  int broad = 0, nbuf = 0, cur_d = 0;  // a lane's k only grows: its cell index only moves forward
+  int broad = 0, nbuf = 0, cur_d = 0;  // the span of the lane's current item (span_of)
   auto flush = [&]() {  // rare: the survivor buffer is full — reserve its slots with its own atomic
     int base = 0;
     if (lane == 0) base = atomicAdd(cand_total, nbuf);
@@ -527,7 +539,7 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) k_pairs_warp(Collide c, in
         at[u].x = -1;
         own[u] = false;
         if (k < total) {
-          while (s_off[warp][cur_d + 1] <= k) ++cur_d;
+          cur_d = span_of(s_off[warp], k);
           own[u] = cur_d == 0;
           const int pos = s_start[warp][cur_d] + (k - s_off[warp][cur_d]);
           at[u] = attr[pos];
@@ -660,13 +672,13 @@ __global__ void __launch_bounds__(32 * kCellWarps) k_pairs_cell(Collide c, int p
     }
     __syncwarp();
     if (ib == 0 && c.pill_scene) scene = c.pill_scene[s_ma[warp][0].x];
-    int cur_d = 0;  // a lane's k only grows, so its cell index only moves forward
+    int cur_d = 0;  // the span of the lane's current item (span_of)
     for (int k0 = 0; k0 < total; k0 += 32) {
       const int k = k0 + lane;
       int4 at = make_int4(-1, 0, 0, 0);
       double2 j01 = make_double2(0, 0), j23 = make_double2(0, 0);
       if (k < total) {
-        while (s_off[warp][cur_d + 1] <= k) ++cur_d;
+        cur_d = span_of(s_off[warp], k);
         const int pos = s_start[warp][cur_d] + (k - s_off[warp][cur_d]);
         at = attr[pos];
         j01 = sph[2 * pos];
