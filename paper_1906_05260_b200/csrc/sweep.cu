@@ -184,7 +184,17 @@ __global__ void k_ext_fill(Collide c, int npins) {
   const int n = npins + nct + c.scalars[SC_NHP];
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) {
     int slots[4];
-    const int ne = ext_endpoints(c, b, npins, nct, slots);
+    int ne;
+    if (b >= npins && b < npins + nct) {  // a contact's endpoint slots, as k_ext_count stored them
+      const int va = c.ct_va[b - npins], vb = c.ct_vb[b - npins];
+      slots[0] = va;
+      slots[1] = va >= 0 ? va + 1 : -1;
+      slots[2] = vb;
+      slots[3] = vb >= 0 ? vb + 1 : -1;
+      ne = vb >= 0 ? 4 : 2;
+    } else {
+      ne = ext_endpoints(c, b, npins, nct, slots);
+    }
     for (int e = 0; e < ne; ++e) {
       if (slots[e] < 0) continue;
       const int pos = c.ext_off[slots[e]] + atomicAdd(&c.ext_cur[slots[e]], 1);
